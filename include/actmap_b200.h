@@ -1,0 +1,154 @@
+/*
+ * actmap_b200.h -- C ABI of the B200-native oMAP hot path.
+ *
+ * This is the drop-in boundary under the reference's actmap:: planner API
+ * (/root/reference/proj/core/include/actmap/).  Plain pointers and sizes,
+ * status codes instead of exceptions, caller-owned host buffers,
+ * context-owned device buffers; a context is externally synchronised (one
+ * host thread at a time).  Every entry point names the reference interface
+ * it serves.  The C++ API (the include/actmap/ headers, same signatures as the
+ * reference headers) is implemented on top of these calls, and INTEGRATION.md
+ * shows the ctypes / C++ bindings.
+ *
+ * Status -> reference exception (errors.hpp:10-44):
+ *   AM_EINVAL      -> actmap::InvalidInputError  (CLI exit 1)
+ *   AM_EUNCOVERED  -> actmap::UncoveredTargetError (CLI exit 2; per target in batch calls)
+ *   AM_ECUDA/AM_EOOM/AM_ENCCL/AM_EINTERNAL -> actmap::Error
+ */
+#ifndef ACTMAP_B200_H
+#define ACTMAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AM_ABI_VERSION 1
+
+typedef enum am_status {
+  AM_OK = 0,
+  AM_EINVAL = 1,
+  AM_EUNCOVERED = 2,
+  AM_ECUDA = 3,
+  AM_EOOM = 4,
+  AM_ENCCL = 5,
+  AM_EINTERNAL = 6
+} am_status;
+
+/* propagate.hpp:45-49 (AutoStop) plus the fixed-L case of report.hpp:75. */
+enum { AM_STOP_FILLED = 0, AM_STOP_STALLED = 1, AM_STOP_CAP = 2, AM_STOP_FIXED = 3 };
+/* propagate.hpp:22 */
+enum { AM_MODE_BATCHED = 0, AM_MODE_ITERATIVE = 1 };
+/* report.hpp:15 */
+enum { AM_METHOD_SIMPLE = 0, AM_METHOD_EUCLIDEAN = 1 };
+
+typedef struct am_ctx am_ctx;
+typedef struct am_grid am_grid;
+
+#define AM_CTX_TIMING 1u /* time every stencil block launch with CUDA events */
+
+typedef struct am_ctx_opts {
+  int32_t device; /* CUDA ordinal */
+  uint32_t flags; /* AM_CTX_* */
+} am_ctx_opts;
+
+typedef struct am_prop_result {
+  uint32_t layers_used;     /* AutoResult::layers_used (propagate.hpp:53) */
+  uint32_t cause;           /* AM_STOP_* (AutoResult::cause, propagate.hpp:54) */
+  uint32_t layers_computed; /* layers actually run on the device (>= layers_used; overshoot rolled back exactly) */
+  uint32_t cell_bits;       /* final device cell width (16 or 32) */
+  uint64_t block_launches;  /* temporally blocked stencil launches */
+  uint64_t layer_launches;  /* single-layer stencil launches */
+  double stencil_ms;        /* summed CUDA-event time of the block launches (AM_CTX_TIMING) */
+} am_prop_result;
+
+typedef struct am_grid_info {
+  uint32_t width, height, pitch, rows, bands, segments, seg_len, halo;
+  uint32_t cell_bits, layers_used, layers_computed;
+} am_grid_info;
+
+typedef struct am_stats {
+  uint64_t kernel_launches; /* every kernel this context has launched */
+} am_stats;
+
+/* ---- context ---------------------------------------------------------- */
+am_status am_ctx_create(const am_ctx_opts *opts, am_ctx **out);
+void am_ctx_destroy(am_ctx *ctx);
+const char *am_last_error(const am_ctx *ctx);
+am_status am_ctx_stats(const am_ctx *ctx, am_stats *out);
+am_status am_ctx_synchronize(am_ctx *ctx);
+/* The cudaStream_t every kernel of this context is launched on (so callers
+ * can bracket work with CUDA events on the launching stream). */
+am_status am_ctx_get_stream(const am_ctx *ctx, void **stream);
+
+/* ---- grid + sources (GridMap grid.hpp:18-57, SourceSet grid.hpp:80-90) --
+ * occupancy: width*height bytes, row-major, nonzero = obstacle.
+ * src_rc: n_src (row, col) pairs; each in bounds and free, n_src >= 1
+ * (duplicates collapse).  *_device variants take device pointers (inputs
+ * already resident in HBM). */
+am_status am_grid_create(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *occupancy,
+                         const uint32_t *src_rc, uint64_t n_src, am_grid **out);
+am_status am_grid_create_device(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *d_occupancy,
+                                const uint32_t *d_src_rc, uint64_t n_src, am_grid **out);
+am_status am_grid_destroy(am_ctx *ctx, am_grid *grid);
+am_status am_grid_get_info(const am_grid *grid, am_grid_info *out);
+
+/* ---- propagation (propagate.hpp:40-61) ---------------------------------
+ * layers >= 1: fixed L (propagate); layers == 0: auto mode with auto_cap
+ * (propagate_auto).  mode: AM_MODE_BATCHED (temporally blocked) or
+ * AM_MODE_ITERATIVE (one launch + host-visible boundary per layer); outputs
+ * are bit-identical.  The map stays resident on the device. */
+am_status am_propagate(am_ctx *ctx, am_grid *grid, uint32_t layers, uint32_t auto_cap, uint32_t mode,
+                       am_prop_result *res);
+
+/* ActivityMap::values() (activity.hpp:40): dense row-major uint32 W*H. */
+am_status am_activity_download(am_ctx *ctx, am_grid *grid, uint32_t *dense_host);
+am_status am_activity_download_device(am_ctx *ctx, am_grid *grid, uint32_t *dense_device);
+/* Replace the grid's map by a caller-supplied dense map (reconstruct on an
+ * ActivityMap that did not come from am_propagate; reconstruct.hpp:38,45). */
+am_status am_activity_upload(am_ctx *ctx, am_grid *grid, const uint32_t *dense_host, uint32_t layers_applied);
+
+/* ---- path extraction (reconstruct.hpp:34-47), batched over targets ------
+ * Step 1: am_path_counts -> offsets[0..n] (exclusive scan; offsets[n] =
+ * total points) and per-target status (AM_OK / AM_EINVAL / AM_EUNCOVERED).
+ * Step 2: am_trace_paths writes target->source points (row, col pairs) at
+ * pts_rc[2*offsets[i] ..].  method: AM_METHOD_*; seed: simple-method
+ * tie-break seed (pin P2).  Euclidean paths are returned straightened
+ * (strict corner rule); for maps produced by am_propagate straightening is
+ * provably the identity and is skipped. */
+am_status am_path_counts(am_ctx *ctx, am_grid *grid, const uint32_t *tgt_rc, uint64_t n, uint32_t method,
+                         uint64_t seed, uint64_t *offsets, int32_t *status);
+am_status am_trace_paths(am_ctx *ctx, am_grid *grid, const uint32_t *tgt_rc, uint64_t n, uint32_t method,
+                         uint64_t seed, const uint64_t *offsets, uint32_t *pts_rc, uint64_t pts_capacity,
+                         int32_t *status);
+/* Device-resident variant: targets, offsets (n+1), points and status are
+ * device pointers; counts, scan and trace run back to back on the stream
+ * with no host round trip.  pts capacity must be >= the total. */
+am_status am_trace_paths_device(am_ctx *ctx, am_grid *grid, const uint32_t *d_tgt_rc, uint64_t n,
+                                uint32_t method, uint64_t seed, uint64_t *d_offsets, uint32_t *d_pts_rc,
+                                uint64_t pts_capacity, int32_t *d_status);
+
+/* ---- single-shot entry points over host buffers ------------------------ */
+/* propagate_layer (propagate.hpp:37-38): one layer from an arbitrary map. */
+am_status am_propagate_layer(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *occupancy,
+                             const uint32_t *src_rc, uint64_t n_src, const uint32_t *in, uint32_t *out);
+/* propagate_reference (propagate.hpp:67-68): literal INT32_MIN sentinel kernel. */
+am_status am_propagate_reference(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *occupancy,
+                                 const uint32_t *src_rc, uint64_t n_src, uint32_t layers, uint32_t *out);
+
+/* ---- host helpers of the planner API (no device work) ------------------ */
+/* random_maze / comb_maze (grid.hpp:65-76) into a caller buffer of W*H bytes. */
+am_status am_random_maze(uint32_t width, uint32_t height, double density, uint64_t seed, uint8_t *occupancy);
+am_status am_comb_maze(uint32_t width, uint32_t height, uint8_t *occupancy);
+/* straighten (reconstruct.hpp:49-58); occupancy may be NULL for the
+ * geometric variant; rule 0 = strict, 1 = permissive.  out may alias pts. */
+am_status am_straighten(const uint32_t *pts_rc, uint64_t n, const uint8_t *occupancy, uint32_t width,
+                        uint32_t height, uint32_t rule, uint32_t *out_rc, uint64_t *n_out);
+/* path_metrics (reconstruct.hpp:26-32). */
+am_status am_path_metrics(const uint32_t *pts_rc, uint64_t n, uint64_t *steps, double *euclidean_length);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

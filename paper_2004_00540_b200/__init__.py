@@ -1,0 +1,438 @@
+"""B200-native oMAP hot path (arXiv 2004.00540) -- Python mirror of the actmap:: API.
+
+Thin ctypes layer over the C ABI in ``include/actmap_b200.h`` (library
+``libactmap_b200.so``, built in-tree for sm_100a).  Names, argument meaning and
+error behaviour follow the reference planner API
+(/root/reference/proj/core/include/actmap/propagate.hpp, reconstruct.hpp,
+grid.hpp, errors.hpp).  All compute runs in the CUDA library; there is no
+CPU fallback -- importing works without a GPU, the first device call raises
+``Error`` if the extension or the device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libactmap_b200.so")
+
+OK, EINVAL, EUNCOVERED, ECUDA, EOOM, ENCCL, EINTERNAL = 0, 1, 2, 3, 4, 5, 6
+FILLED, STALLED, CAP, FIXED = 0, 1, 2, 3          # AutoStop (propagate.hpp:45-49) + fixed
+BATCHED, ITERATIVE = 0, 1                          # Mode (propagate.hpp:22)
+SIMPLE, EUCLIDEAN = 0, 1                           # Method (report.hpp:15)
+STRICT, PERMISSIVE = 0, 1                          # CornerRule (reconstruct.hpp:14)
+CTX_TIMING = 1
+K_MAX_LAYERS = 2147483646                          # propagate.hpp:15-16
+K_MAX_GRID_DIM = 65535                             # grid.hpp:14
+
+
+class Error(RuntimeError):
+    """actmap::Error (errors.hpp:10)."""
+
+
+class InvalidInputError(Error):
+    """actmap::InvalidInputError (errors.hpp:17)."""
+
+
+class UncoveredTargetError(Error):
+    """actmap::UncoveredTargetError (errors.hpp:41)."""
+
+
+class _PropResult(C.Structure):
+    _fields_ = [("layers_used", C.c_uint32), ("cause", C.c_uint32), ("layers_computed", C.c_uint32),
+                ("cell_bits", C.c_uint32), ("block_launches", C.c_uint64), ("layer_launches", C.c_uint64),
+                ("stencil_ms", C.c_double)]
+
+
+class _GridInfo(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in ("width", "height", "pitch", "rows", "bands", "segments", "seg_len",
+                                           "halo", "cell_bits", "layers_used", "layers_computed")]
+
+
+class _CtxOpts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("flags", C.c_uint32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64)]
+
+
+_lib = None
+_lock = threading.RLock()
+_vp, _u8p, _u32p, _u64p, _i32p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), \
+    C.POINTER(C.c_int32)
+
+
+def lib():
+    """Loads libactmap_b200.so (raises Error if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise Error(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        st, u32, u64 = C.c_int, C.c_uint32, C.c_uint64
+        sig = {
+            "am_ctx_create": (st, [C.POINTER(_CtxOpts), C.POINTER(_vp)]),
+            "am_ctx_destroy": (None, [_vp]),
+            "am_last_error": (C.c_char_p, [_vp]),
+            "am_ctx_stats": (st, [_vp, C.POINTER(_Stats)]),
+            "am_ctx_synchronize": (st, [_vp]),
+            "am_ctx_get_stream": (st, [_vp, C.POINTER(_vp)]),
+            "am_grid_create": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
+            "am_grid_create_device": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
+            "am_grid_destroy": (st, [_vp, _vp]),
+            "am_grid_get_info": (st, [_vp, C.POINTER(_GridInfo)]),
+            "am_propagate": (st, [_vp, _vp, u32, u32, u32, C.POINTER(_PropResult)]),
+            "am_activity_download": (st, [_vp, _vp, _vp]),
+            "am_activity_download_device": (st, [_vp, _vp, _vp]),
+            "am_activity_upload": (st, [_vp, _vp, _vp, u32]),
+            "am_path_counts": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp]),
+            "am_trace_paths": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
+            "am_trace_paths_device": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
+            "am_propagate_layer": (st, [_vp, u32, u32, _vp, _vp, u64, _vp, _vp]),
+            "am_propagate_reference": (st, [_vp, u32, u32, _vp, _vp, u64, u32, _vp]),
+            "am_random_maze": (st, [u32, u32, C.c_double, u64, _vp]),
+            "am_comb_maze": (st, [u32, u32, _vp]),
+            "am_straighten": (st, [_vp, u64, _vp, u32, u32, u32, _vp, _u64p]),
+            "am_path_metrics": (st, [_vp, u64, _u64p, C.POINTER(C.c_double)]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _raise(st, ctx, what):
+    msg = what
+    if ctx is not None and ctx.handle:
+        err = lib().am_last_error(ctx.handle)
+        if err:
+            msg = f"{what}: {err.decode(errors='replace')}"
+    if st == EINVAL:
+        raise InvalidInputError(msg)
+    if st == EUNCOVERED:
+        raise UncoveredTargetError(msg)
+    raise Error(f"{msg} (status {st})")
+
+
+def _check(st, ctx, what):
+    if st != OK:
+        _raise(st, ctx, what)
+
+
+class Context:
+    """One CUDA device + stream (am_ctx).  Externally synchronised."""
+
+    def __init__(self, device: int = 0, timing: bool = False):
+        h = C.c_void_p()
+        opts = _CtxOpts(device, CTX_TIMING if timing else 0)
+        st = lib().am_ctx_create(C.byref(opts), C.byref(h))
+        if st != OK:
+            raise Error(f"cannot create a B200 context on device {device} (status {st})")
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            lib().am_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def kernel_launches(self) -> int:
+        s = _Stats()
+        _check(lib().am_ctx_stats(self.handle, C.byref(s)), self, "stats")
+        return s.kernel_launches
+
+    def synchronize(self):
+        _check(lib().am_ctx_synchronize(self.handle), self, "synchronize")
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t of this context (wrap with torch.cuda.ExternalStream for events)."""
+        s = C.c_void_p()
+        _check(lib().am_ctx_get_stream(self.handle, C.byref(s)), self, "stream")
+        return s.value or 0
+
+    def trace_device(self, grid: "Grid", d_tgt: int, n: int, method: int, seed: int, d_offsets: int, d_pts: int,
+                     cap: int, d_status: int):
+        """am_trace_paths_device: device pointers in, no host round trip."""
+        _check(lib().am_trace_paths_device(self.handle, grid.handle, C.c_void_p(d_tgt), n, method, seed,
+                                           C.c_void_p(d_offsets), C.c_void_p(d_pts), cap, C.c_void_p(d_status)),
+               self, "trace_device")
+
+
+_default = None
+
+
+def default_context() -> Context:
+    global _default
+    with _lock:
+        if _default is None:
+            _default = Context(int(os.environ.get("ACTMAP_DEVICE", "0")))
+        return _default
+
+
+def _occ(occupancy):
+    occ = np.ascontiguousarray(occupancy, dtype=np.uint8)
+    if occ.ndim != 2:
+        raise InvalidInputError("occupancy must be a 2-D (height, width) array")
+    return occ
+
+
+def _rc(points):
+    a = np.ascontiguousarray(np.asarray(points, dtype=np.uint32).reshape(-1, 2))
+    return a
+
+
+class PropResult:
+    def __init__(self, r: _PropResult):
+        self.layers_used = r.layers_used
+        self.cause = r.cause
+        self.layers_computed = r.layers_computed
+        self.cell_bits = r.cell_bits
+        self.block_launches = r.block_launches
+        self.layer_launches = r.layer_launches
+        self.stencil_ms = r.stencil_ms
+
+
+class Grid:
+    """GridMap + SourceSet resident on the device (am_grid), plus its activity map."""
+
+    def __init__(self, occupancy, sources, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.occ = _occ(occupancy)
+        self.height, self.width = self.occ.shape
+        src = _rc(sources)
+        h = C.c_void_p()
+        _check(lib().am_grid_create(self.ctx.handle, self.width, self.height, _ptr(self.occ), _ptr(src), len(src),
+                                    C.byref(h)), self.ctx, "SourceSet/grid")
+        self.handle = h
+        self.layers = 0
+
+    @classmethod
+    def from_device(cls, width, height, d_occ_ptr: int, d_src_ptr: int, n_src: int, ctx: Context | None = None):
+        """Inputs already resident in HBM (device pointers)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.occ = None
+        self.width, self.height = width, height
+        h = C.c_void_p()
+        _check(lib().am_grid_create_device(self.ctx.handle, width, height, C.c_void_p(d_occ_ptr),
+                                           C.c_void_p(d_src_ptr), n_src, C.byref(h)), self.ctx, "grid")
+        self.handle = h
+        self.layers = 0
+        return self
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().am_grid_destroy(self.ctx.handle, self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = _GridInfo()
+        _check(lib().am_grid_get_info(self.handle, C.byref(i)), self.ctx, "info")
+        return {n: getattr(i, n) for n, _ in _GridInfo._fields_}
+
+    def propagate(self, layers: int, mode: int = BATCHED) -> PropResult:
+        if layers < 1:
+            raise InvalidInputError("propagate: L must be >= 1")
+        r = _PropResult()
+        _check(lib().am_propagate(self.ctx.handle, self.handle, layers, 0, mode, C.byref(r)), self.ctx, "propagate")
+        self.layers = r.layers_used
+        return PropResult(r)
+
+    def propagate_auto(self, auto_cap: int) -> PropResult:
+        r = _PropResult()
+        _check(lib().am_propagate(self.ctx.handle, self.handle, 0, auto_cap, BATCHED, C.byref(r)), self.ctx,
+               "propagate_auto")
+        self.layers = r.layers_used
+        return PropResult(r)
+
+    def activity(self, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.height, self.width), np.uint32)
+        _check(lib().am_activity_download(self.ctx.handle, self.handle, _ptr(out)), self.ctx, "download")
+        return out
+
+    def activity_to_device(self, d_ptr: int):
+        _check(lib().am_activity_download_device(self.ctx.handle, self.handle, C.c_void_p(d_ptr)), self.ctx,
+               "download")
+
+    def upload_activity(self, values, layers_applied: int):
+        v = np.ascontiguousarray(values, dtype=np.uint32)
+        if v.shape != (self.height, self.width):
+            raise InvalidInputError("activity/grid dimension mismatch")
+        _check(lib().am_activity_upload(self.ctx.handle, self.handle, _ptr(v), layers_applied), self.ctx, "upload")
+        self.layers = layers_applied
+
+    def path_counts(self, targets, method=EUCLIDEAN, seed=0):
+        t = _rc(targets)
+        off = np.zeros(len(t) + 1, np.uint64)
+        st = np.zeros(len(t), np.int32)
+        _check(lib().am_path_counts(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
+                                    _ptr(st)), self.ctx, "path counts")
+        return off, st
+
+    def trace(self, targets, method=EUCLIDEAN, seed=0):
+        """Batched path extraction: returns (offsets, points (total, 2), status)."""
+        t = _rc(targets)
+        off, st = self.path_counts(t, method, seed)
+        total = int(off[-1])
+        pts = np.empty((max(total, 1), 2), np.uint32)
+        _check(lib().am_trace_paths(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
+                                    _ptr(pts), total, _ptr(st)), self.ctx, "trace")
+        return off, pts[:total], st
+
+    def paths(self, targets, method=EUCLIDEAN, seed=0):
+        off, pts, st = self.trace(targets, method, seed)
+        out = []
+        for i in range(len(st)):
+            if st[i] != OK:
+                out.append((int(st[i]), None))
+                continue
+            p = pts[off[i]:off[i + 1]]
+            keep = p[:, 0] != 0xFFFFFFFF
+            out.append((OK, p[keep]))
+        return out
+
+
+# ---------------------------------------------------------------- free functions
+def propagate_layer(activity, occupancy, sources, threads: int = 1, ctx: Context | None = None) -> np.ndarray:
+    """propagate.hpp:37-38."""
+    ctx = ctx or default_context()
+    occ = _occ(occupancy)
+    a = np.ascontiguousarray(activity, dtype=np.uint32)
+    if a.shape != occ.shape:
+        raise InvalidInputError("propagate_layer: activity/grid dimension mismatch")
+    src = _rc(sources)
+    out = np.empty_like(a)
+    _check(lib().am_propagate_layer(ctx.handle, occ.shape[1], occ.shape[0], _ptr(occ), _ptr(src), len(src), _ptr(a),
+                                    _ptr(out)), ctx, "propagate_layer")
+    return out
+
+
+def propagate(occupancy, sources, layers: int, mode: int = BATCHED, threads: int = 1,
+              ctx: Context | None = None) -> np.ndarray:
+    """propagate.hpp:40-43."""
+    if layers < 1 or layers > K_MAX_LAYERS:
+        raise InvalidInputError("propagate: L out of range")
+    g = Grid(occupancy, sources, ctx)
+    try:
+        g.propagate(layers, mode)
+        return g.activity()
+    finally:
+        g.close()
+
+
+def propagate_auto(occupancy, sources, auto_cap: int, threads: int = 1, ctx: Context | None = None):
+    """propagate.hpp:57-61 -> (map, layers_used, cause)."""
+    if auto_cap < 1 or auto_cap > K_MAX_LAYERS:
+        raise InvalidInputError("propagate_auto: auto_cap out of range")
+    g = Grid(occupancy, sources, ctx)
+    try:
+        r = g.propagate_auto(auto_cap)
+        return g.activity(), r.layers_used, r.cause
+    finally:
+        g.close()
+
+
+def propagate_reference(occupancy, sources, layers: int, ctx: Context | None = None) -> np.ndarray:
+    """propagate.hpp:63-68 (INT32_MIN sentinel kernel)."""
+    ctx = ctx or default_context()
+    occ = _occ(occupancy)
+    src = _rc(sources)
+    out = np.empty(occ.shape, np.uint32)
+    _check(lib().am_propagate_reference(ctx.handle, occ.shape[1], occ.shape[0], _ptr(occ), _ptr(src), len(src),
+                                        layers, _ptr(out)), ctx, "propagate_reference")
+    return out
+
+
+def layer_bound(width: int, height: int):
+    """propagate.hpp:70-79 -> (worst_case, heuristic_low, heuristic_high)."""
+    mx, mn = max(width, height), min(width, height)
+    return mx * ((mn + 1) // 2) + mn // 2, (3 * mx + 1) // 2, 2 * mx
+
+
+def _reconstruct(activity, occupancy, sources, target, method, seed, ctx, layers_applied=None):
+    occ = _occ(occupancy)
+    g = Grid(occ, sources, ctx)
+    try:
+        a = np.ascontiguousarray(activity, dtype=np.uint32)
+        g.upload_activity(a, int(layers_applied if layers_applied is not None else a.max(initial=0)))
+        (st, pts), = g.paths([target], method, seed)
+    finally:
+        g.close()
+    if st == EUNCOVERED:
+        raise UncoveredTargetError(f"uncovered target {tuple(target)}: increase L or target unreachable")
+    if st == EINVAL:
+        raise InvalidInputError(f"invalid target {tuple(target)}")
+    if st != OK:
+        raise Error("activity map has no ascending neighbour on the path")
+    return pts
+
+
+def reconstruct_simple(activity, occupancy, sources, target, seed: int, ctx: Context | None = None) -> np.ndarray:
+    """reconstruct.hpp:38-40 (device trace on the given map)."""
+    return _reconstruct(activity, occupancy, sources, target, SIMPLE, seed, ctx)
+
+
+def reconstruct_euclidean(activity, occupancy, sources, target, rule: int = STRICT,
+                          ctx: Context | None = None) -> np.ndarray:
+    """reconstruct.hpp:45-47 (device trace, then straighten)."""
+    pts = _reconstruct(activity, occupancy, sources, target, EUCLIDEAN, 0, ctx)
+    return straighten(pts, occupancy, rule)
+
+
+def straighten(points, occupancy=None, rule: int = STRICT) -> np.ndarray:
+    """reconstruct.hpp:49-58."""
+    p = _rc(points)
+    out = np.empty_like(p)
+    n = C.c_uint64(0)
+    if occupancy is None:
+        _check(lib().am_straighten(_ptr(p), len(p), None, 0, 0, rule, _ptr(out), C.byref(n)), None, "straighten")
+    else:
+        occ = _occ(occupancy)
+        _check(lib().am_straighten(_ptr(p), len(p), _ptr(occ), occ.shape[1], occ.shape[0], rule, _ptr(out),
+                                   C.byref(n)), None, "straighten")
+    return out[: n.value].copy()
+
+
+def path_metrics(points):
+    """reconstruct.hpp:26-32 -> (steps, euclidean_length)."""
+    p = _rc(points)
+    s, length = C.c_uint64(0), C.c_double(0.0)
+    _check(lib().am_path_metrics(_ptr(p), len(p), C.byref(s), C.byref(length)), None, "path_metrics")
+    return s.value, length.value
+
+
+def random_maze(width: int, height: int, density: float, seed: int) -> np.ndarray:
+    """grid.hpp:72-76."""
+    occ = np.empty((height, width), np.uint8)
+    _check(lib().am_random_maze(width, height, density, seed, _ptr(occ)), None, "random_maze")
+    return occ
+
+
+def comb_maze(width: int, height: int) -> np.ndarray:
+    """grid.hpp:65-70."""
+    occ = np.empty((height, width), np.uint8)
+    _check(lib().am_comb_maze(width, height, _ptr(occ)), None, "comb_maze")
+    return occ

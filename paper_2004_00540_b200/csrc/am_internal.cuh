@@ -1,0 +1,96 @@
+// am_internal.cuh -- device layout, cell encoding and kernel declarations
+// shared by the sm_100a kernels and the C-ABI host code.
+//
+// Device layout.  The reference map is a dense row-major
+// uint32 field (activity.hpp:51) plus a dense uint8 occupancy grid
+// (grid.hpp:56).  On the device one pitched field carries BOTH: every free
+// cell has its top bit set ("flag") and its activity a in the low bits; every
+// obstacle or padding cell has the flag clear and is semantically 0.  Then the
+// layer step  out = max3x3(in) & (in_center | LOWMASK)  is exactly
+// propagate_layer (propagate.hpp:34-38): a free centre keeps the flagged max
+// of its neighbourhood (unflagged obstacles can never win against the
+// centre's own flagged value), an obstacle centre loses its flag.  Sources
+// add +1 (rare; see the source-row flags).  No occupancy bytes are read
+// inside the stencil at all.
+//
+// Cell width: 16-bit (a <= 0x7FFF) while layers+1 <= 32767, packed two
+// independent tiles per 32-bit word ("u16x2 tile pairs": lo half = tile A,
+// hi half = tile B, so the 3x3 max never needs a byte permute); promoted
+// exactly to 32-bit cells (a <= 2^31-1 = kMaxLayers+1) beyond that.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace am {
+
+constexpr uint32_t kFlag16 = 0x8000u;
+constexpr uint32_t kLow16x2 = 0x7FFF7FFFu;
+constexpr uint32_t kFlag32 = 0x80000000u;
+constexpr uint32_t kLow32 = 0x7FFFFFFFu;
+constexpr uint32_t kMax16Activity = 0x7FFFu;      // largest a representable in 16-bit cells
+constexpr uint32_t kMaxLayers = 2147483646u;      // propagate.hpp:15-16
+
+// Temporal-block kernel shape: each warp streams a vertical band of
+// 32*kWPL cells (kK-cell halo each side) down a row segment, running kK
+// layers per HBM round trip in registers.
+constexpr int kWPL = 8;          // words per lane
+constexpr int kK = 8;            // layers per block (= halo depth)
+constexpr int kBand = 32 * kWPL; // band width in cells (incl. halo)
+constexpr int kBandUseful = kBand - 2 * kK;
+constexpr int kBlockThreads = 128;
+
+struct Geo {
+  uint32_t W, H;          // grid extent (cells)
+  uint32_t pad;           // = kK: rows above / cols left of the grid
+  uint32_t pitch;         // elements per allocated row
+  uint32_t rows;          // allocated rows
+  uint32_t nbands;        // vertical bands of kBandUseful cells
+  uint32_t nseg;          // row segments (even)
+  uint32_t seg_len;       // rows per segment (even)
+  __host__ __device__ size_t idx(uint32_t r, uint32_t c) const {
+    return (size_t)(r + pad) * pitch + (c + pad);
+  }
+};
+
+Geo make_geo(uint32_t W, uint32_t H, int num_sms);
+
+// ---- kernels (stencil.cu) ----
+void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcmask, void* d_val,
+                 int cell_bits, cudaStream_t s);
+void launch_scatter_sources(const Geo& g, const uint32_t* d_src_rc, uint64_t n, uint8_t* d_srcmask,
+                            uint8_t* d_rowsrc, int* d_err, cudaStream_t s);
+void launch_block(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
+                  const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s);
+void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
+                  uint32_t* flag, cudaStream_t s);
+void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);
+void launch_zero_check(const Geo& g, int cell_bits, const void* val, uint32_t* flag, cudaStream_t s);
+void launch_decode(const Geo& g, int cell_bits, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,
+                   uint32_t* dense_rows, cudaStream_t s);
+int block_kernel_blocks_per_sm(int cell_bits);
+void launch_encode_dense(const Geo& g, const uint32_t* dense, const uint8_t* occ_dense, uint32_t* val32,
+                         cudaStream_t s);
+void launch_plain_layer(uint32_t W, uint32_t H, const uint8_t* occ, const uint8_t* srcmask_dense,
+                        const uint32_t* in, uint32_t* out, cudaStream_t s);
+void launch_sentinel_layer(uint32_t W, uint32_t H, const uint8_t* occ, const uint8_t* srcmask_dense,
+                           const int32_t* in, int32_t* out, cudaStream_t s);
+void launch_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* d_src_rc, uint64_t n, uint8_t* d_srcmask,
+                          const uint8_t* d_occ, int* d_err, cudaStream_t s);
+
+// ---- path extraction (trace.cu) ----
+struct MapView {
+  const void* val;        // encoded pitched field (cell_bits 16/32) or plain dense uint32 (cell_bits 0)
+  const uint8_t* srcmask; // pitched (encoded) or dense (plain)
+  Geo g;
+  int cell_bits;          // 16, 32, or 0 = plain dense uint32 + dense occupancy
+  const uint8_t* occ;     // plain mode only: dense occupancy
+  uint32_t layers;        // layers represented by the values (for point counts)
+};
+void launch_path_counts(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int method, uint64_t seed,
+                        uint64_t* counts, int32_t* status, cudaStream_t s);
+void launch_scan(const uint64_t* counts, uint64_t n, uint64_t* offsets, cudaStream_t s);
+void launch_trace(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int method, uint64_t seed,
+                  const uint64_t* offsets, uint32_t* pts_rc, int32_t* status, cudaStream_t s);
+
+}  // namespace am

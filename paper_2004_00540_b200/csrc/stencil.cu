@@ -1,0 +1,487 @@
+// stencil.cu -- sm_100a kernels for the oMAP layer stack (propagate.hpp:34-68).
+//
+// K1+K2: k_block streams one band of 32*kWPL cells down a row segment and
+// runs kK pool+add+ReLU layers per HBM round trip entirely in registers
+// (per-layer 3-row window, warp-shuffle horizontal halo), then writes the
+// useful middle of the band and folds the fixed-point signal (min over
+// covered cells of a-1) into one atomicMin per warp.  See DESIGN.md §4.
+#include <cstdio>
+
+#include "am_internal.cuh"
+
+namespace am {
+
+Geo make_geo(uint32_t W, uint32_t H, int warp_slots) {
+  Geo g{};
+  g.W = W;
+  g.H = H;
+  g.pad = kK;
+  g.nbands = (W + kBandUseful - 1) / kBandUseful;
+  uint32_t need = g.nbands * kBandUseful + 2 * kK;
+  uint32_t minw = W + 2 * kK;
+  if (need < minw) need = minw;
+  g.pitch = (need + 63) / 64 * 64;
+  // one wave of warps: pairs of row segments per band
+  uint32_t pairs = warp_slots > 0 ? (uint32_t)warp_slots / g.nbands : 1;
+  if (pairs < 1) pairs = 1;
+  uint32_t seg = (H + 2 * pairs - 1) / (2 * pairs);
+  if (seg < 64) seg = 64;
+  seg = (seg + 1) & ~1u;
+  uint32_t nseg = (H + seg - 1) / seg;
+  nseg = (nseg + 1) & ~1u;
+  g.seg_len = seg;
+  g.nseg = nseg;
+  g.rows = nseg * seg + 2 * kK;
+  return g;
+}
+
+// ------------------------------------------------------------------ traits
+template <int CB>
+struct Cell;
+
+template <>
+struct Cell<16> {
+  using T = uint16_t;
+  static constexpr uint32_t LOW = kLow16x2;
+  __device__ __forceinline__ static uint32_t max3(uint32_t a, uint32_t b, uint32_t c) {
+    return __vimax3_u16x2(a, b, c);
+  }
+  // running min over halves of (v - 0x8001) mod 2^16: a-1 for flagged cells,
+  // >= 0x7FFF for unflagged ones (obstacles, padding, garbage).
+  __device__ __forceinline__ static uint32_t acc_min(uint32_t v, uint32_t acc) {
+    return __viaddmin_u16x2(v, 0x7FFF7FFFu, acc);
+  }
+  __device__ __forceinline__ static uint32_t fold(uint32_t acc) {
+    uint32_t lo = acc & 0xFFFFu, hi = acc >> 16;
+    return lo < hi ? lo : hi;
+  }
+};
+
+template <>
+struct Cell<32> {
+  using T = uint32_t;
+  static constexpr uint32_t LOW = kLow32;
+  __device__ __forceinline__ static uint32_t max3(uint32_t a, uint32_t b, uint32_t c) {
+    return __vimax3_u32(a, b, c);
+  }
+  __device__ __forceinline__ static uint32_t acc_min(uint32_t v, uint32_t acc) {
+    return __viaddmin_u32(v, 0x7FFFFFFFu, acc);
+  }
+  __device__ __forceinline__ static uint32_t fold(uint32_t acc) { return acc; }
+};
+
+// ------------------------------------------------------------- init / misc
+__global__ void k_scatter_sources(Geo g, const uint32_t* __restrict__ rc, uint64_t n,
+                                  uint8_t* __restrict__ srcmask, uint8_t* __restrict__ rowsrc,
+                                  int* __restrict__ err) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t r = rc[2 * i], c = rc[2 * i + 1];
+  if (r >= g.H || c >= g.W) {
+    atomicOr(err, 1);
+    return;
+  }
+  srcmask[g.idx(r, c)] = 1;
+  rowsrc[r + g.pad] = 1;
+}
+
+// layer-0 field (activity.hpp:20-21): free = flag|[source], obstacle = 0.
+template <int CB>
+__global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ srcmask,
+                       typename Cell<CB>::T* __restrict__ val) {
+  uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t r = blockIdx.y;
+  if (c >= g.W) return;
+  uint8_t o = occ[(size_t)r * g.W + c];
+  size_t i = g.idx(r, c);
+  uint32_t flag = CB == 16 ? kFlag16 : kFlag32;
+  val[i] = (typename Cell<CB>::T)(o ? 0u : (flag | (uint32_t)srcmask[i]));
+}
+
+// ----------------------------------------------------------- K1+K2 block
+template <int CB>
+struct Rows;
+
+// Loads one row of both tiles and interleaves them into u16x2 words.
+template <>
+struct Rows<16> {
+  uint4 a, b;
+  __device__ __forceinline__ void load(const uint16_t* pa, const uint16_t* pb) {
+    a = __ldg(reinterpret_cast<const uint4*>(pa));
+    b = __ldg(reinterpret_cast<const uint4*>(pb));
+  }
+  __device__ __forceinline__ void words(uint32_t (&x)[kWPL]) const {
+    const uint32_t A[4] = {a.x, a.y, a.z, a.w}, B[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[2 * i] = __byte_perm(A[i], B[i], 0x5410);
+      x[2 * i + 1] = __byte_perm(A[i], B[i], 0x7632);
+    }
+  }
+  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint16_t* pa, uint16_t* pb) {
+    uint32_t A[4], B[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      A[i] = __byte_perm(x[2 * i], x[2 * i + 1], 0x5410);
+      B[i] = __byte_perm(x[2 * i], x[2 * i + 1], 0x7632);
+    }
+    *reinterpret_cast<uint4*>(pa) = make_uint4(A[0], A[1], A[2], A[3]);
+    *reinterpret_cast<uint4*>(pb) = make_uint4(B[0], B[1], B[2], B[3]);
+  }
+  __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t* sb, uint32_t (&s)[kWPL]) {
+    const uint2 A = *reinterpret_cast<const uint2*>(sa);
+    const uint2 B = *reinterpret_cast<const uint2*>(sb);
+    const uint32_t a4[2] = {A.x, A.y}, b4[2] = {B.x, B.y};
+#pragma unroll
+    for (int w = 0; w < kWPL; ++w) {
+      uint32_t ab = (a4[w / 4] >> (8 * (w % 4))) & 0xFFu, bb = (b4[w / 4] >> (8 * (w % 4))) & 0xFFu;
+      s[w] = ab | (bb << 16);
+    }
+  }
+};
+
+template <>
+struct Rows<32> {
+  uint4 a, b;
+  __device__ __forceinline__ void load(const uint32_t* pa, const uint32_t*) {
+    a = __ldg(reinterpret_cast<const uint4*>(pa));
+    b = __ldg(reinterpret_cast<const uint4*>(pa) + 1);
+  }
+  __device__ __forceinline__ void words(uint32_t (&x)[kWPL]) const {
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  }
+  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint32_t* pa, uint32_t*) {
+    reinterpret_cast<uint4*>(pa)[0] = make_uint4(x[0], x[1], x[2], x[3]);
+    reinterpret_cast<uint4*>(pa)[1] = make_uint4(x[4], x[5], x[6], x[7]);
+  }
+  __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t*, uint32_t (&s)[kWPL]) {
+    const uint2 A = *reinterpret_cast<const uint2*>(sa);
+    const uint32_t a4[2] = {A.x, A.y};
+#pragma unroll
+    for (int w = 0; w < kWPL; ++w) s[w] = (a4[w / 4] >> (8 * (w % 4))) & 0xFFu;
+  }
+};
+
+// One streaming step: x holds the newly loaded row (layer 0, row t); layer j
+// produces row t-j from layer j-1's rows t-j-1, t-j (window) and t-j+1 (x).
+// PH selects which window slot holds the older row (it is overwritten).
+template <int CB, int PH>
+__device__ __forceinline__ void stream_step(uint32_t (&x)[kWPL], uint32_t (&P0)[kK][kWPL],
+                                            uint32_t (&P1)[kK][kWPL], uint32_t srcbits,
+                                            const uint8_t* sA, const uint8_t* sB, size_t pitch, int lane) {
+  using C = Cell<CB>;
+#pragma unroll
+  for (int j = 0; j < kK; ++j) {
+    uint32_t v[kWPL];
+#pragma unroll
+    for (int w = 0; w < kWPL; ++w) v[w] = C::max3(P0[j][w], P1[j][w], x[w]);
+    const uint32_t left = __shfl_up_sync(0xffffffffu, v[kWPL - 1], 1);
+    const uint32_t right = __shfl_down_sync(0xffffffffu, v[0], 1);
+    uint32_t y[kWPL];
+#pragma unroll
+    for (int w = 0; w < kWPL; ++w) {
+      const uint32_t l = w == 0 ? left : v[w - 1];
+      const uint32_t r = w == kWPL - 1 ? right : v[w + 1];
+      const uint32_t ctr = PH == 0 ? P1[j][w] : P0[j][w];  // layer j-1, row t-j-1+1
+      y[w] = C::max3(l, v[w], r) & (ctr | C::LOW);
+    }
+    if ((srcbits >> (j + 1)) & 1u) {  // row t-(j+1) holds a source (warp-uniform, rare)
+      uint32_t s[kWPL];
+      const size_t off = (size_t)(j + 1) * pitch;
+      Rows<CB>::src_words(sA - off, sB - off, s);
+#pragma unroll
+      for (int w = 0; w < kWPL; ++w) y[w] += s[w];
+    }
+#pragma unroll
+    for (int w = 0; w < kWPL; ++w) {
+      if (PH == 0) P0[j][w] = x[w];
+      else P1[j][w] = x[w];
+      x[w] = y[w];
+    }
+  }
+  (void)lane;
+}
+
+template <int CB>
+__global__ void __launch_bounds__(kBlockThreads) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
+                                                         typename Cell<CB>::T* __restrict__ out,
+                                                         const uint8_t* __restrict__ srcmask,
+                                                         const uint8_t* __restrict__ rowsrc,
+                                                         uint32_t* __restrict__ flag) {
+  using C = Cell<CB>;
+  using T = typename C::T;
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t ntiles = CB == 16 ? g.nseg / 2 : g.nseg;
+  if (warp >= g.nbands * ntiles) return;
+  const uint32_t band = warp % g.nbands, tile = warp / g.nbands;
+  const uint32_t col = band * kBandUseful + lane * kWPL;  // allocated column of this lane's first cell
+  const uint32_t rA = tile * g.seg_len;                   // allocated row of step 0
+  const uint32_t rB = (CB == 16 ? tile + ntiles : tile) * g.seg_len;
+  const uint32_t T_steps = g.seg_len + 2 * kK;
+  const size_t pitch = g.pitch;
+
+  const T* pA = in + (size_t)rA * pitch + col;
+  const T* pB = in + (size_t)rB * pitch + col;
+  T* oA = out + (size_t)rA * pitch + col;  // output row for step t is rA + t - kK
+  T* oB = out + (size_t)rB * pitch + col;
+  const uint8_t* sA = srcmask + (size_t)rA * pitch + col;
+  const uint8_t* sB = srcmask + (size_t)rB * pitch + col;
+  const bool store_lane = lane >= kK / kWPL && lane < 32 - kK / kWPL;
+
+  uint32_t P0[kK][kWPL], P1[kK][kWPL];
+#pragma unroll
+  for (int j = 0; j < kK; ++j)
+#pragma unroll
+    for (int w = 0; w < kWPL; ++w) P0[j][w] = P1[j][w] = 0u;
+  uint32_t acc = 0xFFFFFFFFu;
+  uint32_t srcbits = 0;
+
+  Rows<CB> nxt;
+  nxt.load(pA, pB);
+  for (uint32_t t = 0; t < T_steps; t += 2) {
+#pragma unroll
+    for (int ph = 0; ph < 2; ++ph) {
+      const uint32_t tt = t + ph;
+      uint32_t x[kWPL];
+      nxt.words(x);
+      const size_t roff = (size_t)tt * pitch;
+      if (tt + 1 < T_steps) nxt.load(pA + roff + pitch, pB + roff + pitch);
+      uint32_t f = rowsrc[rA + tt];
+      if (CB == 16) f |= rowsrc[rB + tt];
+      srcbits = (srcbits << 1) | (f ? 1u : 0u);
+      if (ph == 0)
+        stream_step<CB, 0>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+      else
+        stream_step<CB, 1>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+      if (tt >= 2 * kK && tt < 2 * kK + g.seg_len && store_lane) {
+        Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch);
+#pragma unroll
+        for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
+      }
+    }
+  }
+  const uint32_t m = __reduce_min_sync(0xffffffffu, C::fold(acc));
+  if (lane == 0) atomicMin(flag, m);
+}
+
+// -------------------------------------------------------- single layer
+// One layer over the grid region (remainder layers, Mode::kIterative).
+template <int CB>
+__global__ void k_layer(Geo g, const typename Cell<CB>::T* __restrict__ in, typename Cell<CB>::T* __restrict__ out,
+                        const uint8_t* __restrict__ srcmask, uint32_t* __restrict__ flag) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = blockIdx.y;
+  uint32_t m = 0xFFFFFFFFu;
+  if (c < g.W) {
+    const size_t i = g.idx(r, c);
+    const size_t p = g.pitch;
+    uint32_t v = 0;
+#pragma unroll
+    for (int dr = -1; dr <= 1; ++dr)
+#pragma unroll
+      for (int dc = -1; dc <= 1; ++dc) {
+        uint32_t u = in[i + dr * (long)p + dc];
+        v = u > v ? u : v;
+      }
+    const uint32_t low = CB == 16 ? 0x7FFFu : kLow32;
+    const uint32_t y = (v & ((uint32_t)in[i] | low)) + srcmask[i];
+    out[i] = (typename Cell<CB>::T)y;
+    m = Cell<CB>::fold(Cell<CB>::acc_min(CB == 16 ? (y | (y << 16)) : y, 0xFFFFFFFFu));
+  }
+  m = __reduce_min_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMin(flag, m);
+}
+
+// ------------------------------------------------------- promote / decode
+__global__ void k_promote(Geo g, const uint16_t* __restrict__ in, uint32_t* __restrict__ out) {
+  const size_t n = (size_t)g.rows * g.pitch;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t v = in[i];
+    out[i] = (v & kFlag16) ? (kFlag32 | (v & 0x7FFFu)) : 0u;
+  }
+}
+
+template <int CB>
+__global__ void k_zero_check(Geo g, const typename Cell<CB>::T* __restrict__ val, uint32_t* __restrict__ flag) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = blockIdx.y;
+  bool z = false;
+  if (c < g.W) {
+    const uint32_t v = val[g.idx(r, c)];
+    z = v == (CB == 16 ? kFlag16 : kFlag32);  // free and a == 0
+  }
+  if (__any_sync(0xffffffffu, z) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+template <int CB>
+__global__ void k_decode(Geo g, const typename Cell<CB>::T* __restrict__ val, uint32_t rollback, uint32_t r0,
+                         uint32_t* __restrict__ dense) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = blockIdx.y + r0;
+  if (c >= g.W) return;
+  const uint32_t v = val[g.idx(r, c)];
+  const uint32_t flagbit = CB == 16 ? kFlag16 : kFlag32;
+  const uint32_t low = CB == 16 ? 0x7FFFu : kLow32;
+  const uint32_t a = v & low;
+  dense[(size_t)(r - r0) * g.W + c] = ((v & flagbit) && a) ? a - rollback : 0u;
+}
+
+// user-supplied dense map -> encoded 32-bit field (reconstruct on foreign maps)
+__global__ void k_encode_dense(Geo g, const uint32_t* __restrict__ dense, const uint8_t* __restrict__ occ,
+                               uint32_t* __restrict__ val) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = blockIdx.y;
+  if (c >= g.W) return;
+  const size_t d = (size_t)r * g.W + c;
+  val[g.idx(r, c)] = occ[d] ? 0u : (kFlag32 | (dense[d] & kLow32));
+}
+
+// ------------------------------------------ plain / sentinel single layers
+// propagate_layer on an arbitrary uint32 input (propagate.hpp:37-38): dense
+// layout, explicit occupancy, wrap-around uint32 arithmetic like the host API.
+__global__ void k_plain_layer(uint32_t W, uint32_t H, const uint8_t* __restrict__ occ,
+                              const uint8_t* __restrict__ src, const uint32_t* __restrict__ in,
+                              uint32_t* __restrict__ out) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = blockIdx.y;
+  if (c >= W) return;
+  uint32_t m = 0;
+  for (int dr = -1; dr <= 1; ++dr) {
+    const long rr = (long)r + dr;
+    if (rr < 0 || rr >= (long)H) continue;
+    for (int dc = -1; dc <= 1; ++dc) {
+      const long cc = (long)c + dc;
+      if (cc < 0 || cc >= (long)W) continue;
+      const uint32_t u = in[(size_t)rr * W + cc];
+      m = u > m ? u : m;
+    }
+  }
+  const size_t i = (size_t)r * W + c;
+  out[i] = occ[i] ? 0u : m + (uint32_t)(src[i] != 0);
+}
+
+// propagate_reference (propagate.hpp:63-68): literal signed formulation with
+// the INT32_MIN obstacle sentinel re-added every layer, then ReLU.
+__global__ void k_sentinel_layer(uint32_t W, uint32_t H, const uint8_t* __restrict__ occ,
+                                 const uint8_t* __restrict__ src, const int32_t* __restrict__ in,
+                                 int32_t* __restrict__ out) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = blockIdx.y;
+  if (c >= W) return;
+  int32_t m = 0;  // zero padding
+  for (int dr = -1; dr <= 1; ++dr) {
+    const long rr = (long)r + dr;
+    if (rr < 0 || rr >= (long)H) continue;
+    for (int dc = -1; dc <= 1; ++dc) {
+      const long cc = (long)c + dc;
+      if (cc < 0 || cc >= (long)W) continue;
+      const int32_t u = in[(size_t)rr * W + cc];
+      m = u > m ? u : m;
+    }
+  }
+  const size_t i = (size_t)r * W + c;
+  const long long t = (long long)m + (occ[i] ? INT32_MIN : 0) + (src[i] ? 1 : 0);
+  out[i] = t > 0 ? (int32_t)t : 0;
+}
+
+__global__ void k_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* __restrict__ rc, uint64_t n,
+                                uint8_t* __restrict__ m, const uint8_t* __restrict__ occ, int* __restrict__ err) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t r = rc[2 * i], c = rc[2 * i + 1];
+  if (r >= H || c >= W || occ[(size_t)r * W + c]) {
+    atomicOr(err, 1);
+    return;
+  }
+  m[(size_t)r * W + c] = 1;
+}
+
+// ------------------------------------------------------------- launchers
+static dim3 grid2d(uint32_t W, uint32_t H, int bx) { return dim3((W + bx - 1) / bx, H); }
+
+void launch_scatter_sources(const Geo& g, const uint32_t* d_src_rc, uint64_t n, uint8_t* d_srcmask,
+                            uint8_t* d_rowsrc, int* d_err, cudaStream_t s) {
+  if (!n) return;
+  k_scatter_sources<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, d_src_rc, n, d_srcmask, d_rowsrc, d_err);
+}
+
+void launch_init(const Geo& g, const uint8_t* d_occ, const uint8_t* d_srcmask, void* d_val, int cb,
+                 cudaStream_t s) {
+  if (cb == 16)
+    k_init<16><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, d_occ, d_srcmask, (uint16_t*)d_val);
+  else
+    k_init<32><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, d_occ, d_srcmask, (uint32_t*)d_val);
+}
+
+void launch_block(const Geo& g, int cb, const void* in, void* out, const uint8_t* srcmask, const uint8_t* rowsrc,
+                  uint32_t* flag, cudaStream_t s) {
+  const uint32_t ntiles = cb == 16 ? g.nseg / 2 : g.nseg;
+  const uint32_t warps = g.nbands * ntiles;
+  const uint32_t blocks = (warps + kBlockThreads / 32 - 1) / (kBlockThreads / 32);
+  if (cb == 16)
+    k_block<16><<<blocks, kBlockThreads, 0, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, rowsrc, flag);
+  else
+    k_block<32><<<blocks, kBlockThreads, 0, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, rowsrc, flag);
+}
+
+int block_kernel_blocks_per_sm(int cb) {
+  int n = 0;
+  if (cb == 16)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<16>, kBlockThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<32>, kBlockThreads, 0);
+  return n;
+}
+
+void launch_layer(const Geo& g, int cb, const void* in, void* out, const uint8_t* srcmask, uint32_t* flag,
+                  cudaStream_t s) {
+  if (cb == 16)
+    k_layer<16><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, flag);
+  else
+    k_layer<32><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, flag);
+}
+
+void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s) {
+  k_promote<<<148 * 8, 256, 0, s>>>(g, in, out);
+}
+
+void launch_zero_check(const Geo& g, int cb, const void* val, uint32_t* flag, cudaStream_t s) {
+  if (cb == 16)
+    k_zero_check<16><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, (const uint16_t*)val, flag);
+  else
+    k_zero_check<32><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, (const uint32_t*)val, flag);
+}
+
+void launch_decode(const Geo& g, int cb, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,
+                   uint32_t* dense, cudaStream_t s) {
+  if (r1 <= r0) return;
+  if (cb == 16)
+    k_decode<16><<<grid2d(g.W, r1 - r0, 256), 256, 0, s>>>(g, (const uint16_t*)val, rollback, r0, dense);
+  else
+    k_decode<32><<<grid2d(g.W, r1 - r0, 256), 256, 0, s>>>(g, (const uint32_t*)val, rollback, r0, dense);
+}
+
+void launch_encode_dense(const Geo& g, const uint32_t* dense, const uint8_t* occ, uint32_t* val32,
+                         cudaStream_t s) {
+  k_encode_dense<<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, dense, occ, val32);
+}
+
+void launch_plain_layer(uint32_t W, uint32_t H, const uint8_t* occ, const uint8_t* src, const uint32_t* in,
+                        uint32_t* out, cudaStream_t s) {
+  k_plain_layer<<<grid2d(W, H, 256), 256, 0, s>>>(W, H, occ, src, in, out);
+}
+
+void launch_sentinel_layer(uint32_t W, uint32_t H, const uint8_t* occ, const uint8_t* src, const int32_t* in,
+                           int32_t* out, cudaStream_t s) {
+  k_sentinel_layer<<<grid2d(W, H, 256), 256, 0, s>>>(W, H, occ, src, in, out);
+}
+
+void launch_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* rc, uint64_t n, uint8_t* m, const uint8_t* occ,
+                          int* err, cudaStream_t s) {
+  if (!n) return;
+  k_srcmask_dense<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(W, H, rc, n, m, occ, err);
+}
+
+}  // namespace am

@@ -1,0 +1,220 @@
+// trace.cu -- K3: batched gradient-ascent path extraction, one warp per target
+// (reconstruct.hpp:34-47, pins P1/P2/P5).
+//
+// Lanes 0..7 each fetch one of the 8 neighbours (row-major order, the order
+// the tie-break enumerates) and the warp reduces them with a vote, so each
+// path step costs one dependent L2/L1 round trip.  Encoded maps (produced by
+// the device propagate) have a closed-form point count L_used+2-A(t), so the
+// output offsets are an exclusive scan with no atomics.
+#include "am_internal.cuh"
+
+namespace am {
+
+__constant__ int kDR[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+__constant__ int kDC[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+
+enum : int32_t { ST_OK = 0, ST_EINVAL = 1, ST_EUNCOVERED = 2, ST_EINTERNAL = 6 };
+
+struct Reader {
+  MapView m;
+  __device__ __forceinline__ uint32_t value(uint32_t r, uint32_t c) const {
+    if (m.cell_bits == 16) {
+      const uint32_t v = static_cast<const uint16_t*>(m.val)[m.g.idx(r, c)];
+      return (v & kFlag16) ? (v & 0x7FFFu) : 0u;
+    }
+    if (m.cell_bits == 32) {
+      const uint32_t v = static_cast<const uint32_t*>(m.val)[m.g.idx(r, c)];
+      return (v & kFlag32) ? (v & kLow32) : 0u;
+    }
+    return static_cast<const uint32_t*>(m.val)[(size_t)r * m.g.W + c];
+  }
+  __device__ __forceinline__ bool source(uint32_t r, uint32_t c) const {
+    if (m.cell_bits) return m.srcmask[m.g.idx(r, c)] != 0;
+    return m.srcmask[(size_t)r * m.g.W + c] != 0;
+  }
+  __device__ __forceinline__ bool obstacle(uint32_t r, uint32_t c) const {
+    if (m.cell_bits == 16) return !(static_cast<const uint16_t*>(m.val)[m.g.idx(r, c)] & kFlag16);
+    if (m.cell_bits == 32) return !(static_cast<const uint32_t*>(m.val)[m.g.idx(r, c)] & kFlag32);
+    return m.occ[(size_t)r * m.g.W + c] != 0;
+  }
+};
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {
+  uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ int32_t target_status(const Reader& rd, uint32_t r, uint32_t c) {
+  if (r >= rd.m.g.H || c >= rd.m.g.W) return ST_EINVAL;  // pin P8
+  if (rd.obstacle(r, c)) return ST_EINVAL;               // reconstruct.hpp:36
+  if (rd.value(r, c) == 0) return ST_EUNCOVERED;         // reconstruct.hpp:37
+  return ST_OK;
+}
+
+// Walks one path with a full warp.  WRITE=false only counts points.
+// Returns the point count (>= 1) or 0 with *st set on failure.
+template <bool WRITE>
+__device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, uint64_t seed, uint64_t limit,
+                         uint32_t* out, int32_t* st) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t W = rd.m.g.W, H = rd.m.g.H;
+  uint64_t rng = seed;
+  uint32_t cur = rd.value(r, c);
+  uint64_t n = 1;
+  if (WRITE && lane == 0) {
+    out[0] = r;
+    out[1] = c;
+  }
+  while (!rd.source(r, c)) {
+    if (n >= limit) {
+      *st = ST_EINTERNAL;
+      return 0;
+    }
+    uint32_t v = 0;
+    if (lane < 8) {
+      const long rr = (long)r + kDR[lane], cc = (long)c + kDC[lane];
+      if (rr >= 0 && cc >= 0 && rr < (long)H && cc < (long)W) v = rd.value((uint32_t)rr, (uint32_t)cc);
+    }
+    int sel = -1;
+    uint32_t best;
+    if (method == 0) {  // simple: 8-neighbour argmax, seeded tie-break (pin P2)
+      best = __reduce_max_sync(0xffffffffu, v);
+      const uint32_t mask = __ballot_sync(0xffffffffu, lane < 8 && v == best);
+      if (best > cur) {
+        const int cnt = __popc(mask);
+        int pick = 0;
+        if (cnt >= 2) pick = (int)__umul64hi(splitmix64(rng), (uint64_t)cnt);
+        uint32_t mm = mask;
+        for (int k = 0; k < pick; ++k) mm &= mm - 1;
+        sel = __ffs(mm) - 1;
+      }
+    } else {  // Euclidean: axis order L,R,U,D then diagonals (pin P1)
+      uint32_t nb[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) nb[k] = __shfl_sync(0xffffffffu, v, k);
+      const int axis[4] = {3, 4, 1, 6}, dg[4] = {0, 2, 5, 7};
+      int ba = axis[0];
+      uint32_t bv = nb[axis[0]];
+#pragma unroll
+      for (int k = 1; k < 4; ++k)
+        if (nb[axis[k]] > bv) {
+          bv = nb[axis[k]];
+          ba = axis[k];
+        }
+      if (bv > cur) {
+        sel = ba;
+      } else {
+        ba = dg[0];
+        bv = nb[dg[0]];
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+          if (nb[dg[k]] > bv) {
+            bv = nb[dg[k]];
+            ba = dg[k];
+          }
+        if (bv > cur) sel = ba;
+      }
+      best = bv;
+    }
+    if (sel < 0) {
+      *st = ST_EINTERNAL;  // no ascending neighbour
+      return 0;
+    }
+    r = (uint32_t)((long)r + kDR[sel]);
+    c = (uint32_t)((long)c + kDC[sel]);
+    cur = best;
+    if (WRITE && lane == 0) {
+      out[2 * n] = r;
+      out[2 * n + 1] = c;
+    }
+    ++n;
+  }
+  return n;
+}
+
+// Encoded maps: closed-form count L+2-A(t).  Plain maps: a counting walk.
+__global__ void k_path_counts(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method,
+                              uint64_t seed, uint64_t* __restrict__ counts, int32_t* __restrict__ status) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  const int lane = threadIdx.x & 31;
+  Reader rd{m};
+  const uint32_t r = tgt[2 * w], c = tgt[2 * w + 1];
+  int32_t st = target_status(rd, r, c);
+  uint64_t cnt = 0;
+  if (st == ST_OK) {
+    if (m.cell_bits) {
+      cnt = (uint64_t)m.layers + 2 - rd.value(r, c);
+    } else {
+      cnt = walk<false>(rd, r, c, method, seed, 0xFFFFFFFFFFFFull, nullptr, &st);
+    }
+  }
+  if (lane == 0) {
+    counts[w] = st == ST_OK ? cnt : 0;
+    status[w] = st;
+  }
+}
+
+__global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method, uint64_t seed,
+                        const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pts,
+                        int32_t* __restrict__ status) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  if (status[w] != ST_OK) return;
+  Reader rd{m};
+  const uint64_t off = offsets[w], limit = offsets[w + 1] - off;
+  int32_t st = ST_OK;
+  const uint64_t got = walk<true>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st);
+  if ((threadIdx.x & 31) == 0) {
+    if (st != ST_OK) status[w] = st;
+    else if (got != limit) status[w] = ST_EINTERNAL;
+  }
+}
+
+void launch_path_counts(const MapView& m, const uint32_t* tgt, uint64_t n, int method, uint64_t seed,
+                        uint64_t* counts, int32_t* status, cudaStream_t s) {
+  if (!n) return;
+  const unsigned blocks = (unsigned)((n * 32 + 127) / 128);
+  k_path_counts<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, counts, status);
+}
+
+void launch_trace(const MapView& m, const uint32_t* tgt, uint64_t n, int method, uint64_t seed,
+                  const uint64_t* offsets, uint32_t* pts, int32_t* status, cudaStream_t s) {
+  if (!n) return;
+  const unsigned blocks = (unsigned)((n * 32 + 127) / 128);
+  k_trace<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status);
+}
+
+}  // namespace am
+
+namespace am {
+// Exclusive scan of n counts into offsets[0..n] (single CTA; n is the target
+// count, a few thousand), so offsets never leave the device.
+__global__ void k_scan(const uint64_t* __restrict__ counts, uint64_t n, uint64_t* __restrict__ offsets) {
+  __shared__ uint64_t part[1024];
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t b = threadIdx.x * per, e = b + per < n ? b + per : n;
+  uint64_t s = 0;
+  for (uint64_t i = b; i < e; ++i) s += counts[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (unsigned d = 1; d < blockDim.x; d <<= 1) {
+    uint64_t v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint64_t run = part[threadIdx.x] - s;
+  for (uint64_t i = b; i < e; ++i) {
+    offsets[i] = run;
+    run += counts[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) offsets[n] = part[threadIdx.x];
+}
+
+void launch_scan(const uint64_t* counts, uint64_t n, uint64_t* offsets, cudaStream_t s) {
+  k_scan<<<1, 1024, 0, s>>>(counts, n, offsets);
+}
+}  // namespace am

@@ -1,0 +1,168 @@
+"""GPU parity suite: the CUDA path through the C ABI vs the CPU oracle, bit-exact.
+
+Integer work, so the bar is exact equality of every activity value, of
+layers_used / termination cause, and of every path point."""
+import numpy as np
+import pytest
+
+from tests.kat_runner import load_kats, run_kat
+from tests.oracle_adapter import O
+
+am = pytest.importorskip("paper_2004_00540_b200")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def impl():
+    from tests.product_adapter import ProductImpl
+
+    return ProductImpl()
+
+
+@pytest.mark.parametrize("kat", load_kats(), ids=lambda k: k["name"])
+def test_spec_kat_on_device(impl, kat):
+    assert run_kat(impl, kat) in (None, "skip")
+
+
+SHAPES = [(1, 1), (1, 300), (300, 1), (7, 5), (37, 1000), (1000, 37), (241, 239), (255, 257), (513, 130),
+          (129, 700), (2000, 64)]
+
+
+@pytest.mark.parametrize("w,h", SHAPES)
+def test_fixed_layers_match_oracle(w, h):
+    for seed, dens, ns in [(1, 0.0, 1), (2, 0.3, 3), (3, 0.45, 9)]:
+        occ = O.random_maze(w, h, dens, seed)
+        if (occ == 0).sum() < ns:
+            continue
+        src = O.sample_free_cells(occ, ns, seed)
+        sm = O.source_mask(occ, src)
+        for L in (1, 2, 7, 8, 9, 16, 17, 40, 2 * max(w, h) + 3):
+            ref = O.propagate(occ, sm, L, threads=8)
+            got = am.propagate(occ, src, L)
+            assert np.array_equal(got, ref), (w, h, seed, L, np.argwhere(got != ref)[:5])
+
+
+def test_iterative_mode_and_sentinel_kernel():
+    occ = O.random_maze(300, 211, 0.3, 5)
+    src = O.sample_free_cells(occ, 4, 5)
+    sm = O.source_mask(occ, src)
+    for L in (1, 9, 33):
+        ref = O.propagate(occ, sm, L)
+        assert np.array_equal(am.propagate(occ, src, L, mode=am.ITERATIVE), ref)
+        assert np.array_equal(am.propagate_reference(occ, src, L), ref)
+
+
+def test_propagate_layer_arbitrary_input():
+    rng = np.random.default_rng(0)
+    occ = O.random_maze(130, 77, 0.3, 9)
+    src = O.sample_free_cells(occ, 3, 9)
+    sm = O.source_mask(occ, src)
+    a = rng.integers(0, 2**32, size=occ.shape, dtype=np.uint64).astype(np.uint32)
+    a[occ != 0] = 0
+    assert np.array_equal(am.propagate_layer(a, occ, src), O.propagate_layer(occ, sm, a))
+
+
+@pytest.mark.parametrize("w,h", [(64, 64), (300, 200), (513, 257), (1000, 37), (37, 1000), (1024, 1024)])
+def test_auto_matches_oracle(w, h):
+    for seed, dens, ns in [(11, 0.0, 1), (12, 0.3, 1), (13, 0.45, 5), (14, 0.6, 2), (15, 0.3, 9)]:
+        occ = O.random_maze(w, h, dens, seed)
+        src = O.sample_free_cells(occ, ns, seed)
+        sm = O.source_mask(occ, src)
+        for cap in (1, 5, 8, 9, 37, 4 * max(w, h)):
+            ref, rl, rc = O.propagate_auto(occ, sm, cap, threads=8)
+            got, gl, gc = am.propagate_auto(occ, src, cap)
+            assert (gl, gc) == (rl, rc), (w, h, seed, cap, gl, gc, rl, rc)
+            assert np.array_equal(got, ref), (w, h, seed, cap)
+
+
+def test_auto_all_sources_and_isolated_source():
+    occ = np.zeros((20, 30), np.uint8)
+    src = np.argwhere(occ == 0).astype(np.uint32)  # every free cell is a source
+    got, gl, gc = am.propagate_auto(occ, src, 50)
+    ref, rl, rc = O.propagate_auto(occ, O.source_mask(occ, src), 50)
+    assert (gl, gc) == (rl, rc) == (1, O.FILLED) and np.array_equal(got, ref)
+    occ = np.ones((9, 9), np.uint8)
+    occ[4, 4] = 0
+    occ[0, 0] = 0
+    got, gl, gc = am.propagate_auto(occ, [[4, 4]], 50)
+    ref, rl, rc = O.propagate_auto(occ, O.source_mask(occ, np.array([[4, 4]], np.uint32)), 50)
+    assert (gl, gc) == (rl, rc) == (1, O.STALLED) and np.array_equal(got, ref)
+
+
+def test_paths_match_oracle():
+    occ = O.random_maze(700, 500, 0.3, 21)
+    src = O.sample_free_cells(occ, 5, 21)
+    sm = O.source_mask(occ, src)
+    g = am.Grid(occ, src)
+    r = g.propagate_auto(4 * 700)
+    amap = g.activity()
+    ref, rl, _ = O.propagate_auto(occ, sm, 4 * 700, threads=8)
+    assert r.layers_used == rl and np.array_equal(amap, ref)
+    tg = O.sample_free_cells(occ, 200, 22, exclude=sm)
+    tg = np.concatenate([tg, src[:1], np.array([[0, 0], [499, 699]], np.uint32)])
+    for method in (am.EUCLIDEAN, am.SIMPLE):
+        for seed in ((0,) if method == am.EUCLIDEAN else (0, 1, 2, 3, 4)):
+            res = g.paths(tg, method, seed)
+            for (st, pts), t in zip(res, tg):
+                if method == am.SIMPLE:
+                    ost, opts = O.reconstruct_simple(occ, sm, ref, t, seed)
+                else:
+                    ost, opts = O.reconstruct_euclidean(occ, sm, ref, t)
+                assert st == ost, (t, st, ost)
+                if st == 0:
+                    assert np.array_equal(pts, opts), (t, method, seed)
+    g.close()
+
+
+def test_path_errors():
+    occ = np.zeros((9, 9), np.uint8)
+    occ[2, 2] = 1
+    g = am.Grid(occ, [[0, 0]])
+    g.propagate(3)
+    res = g.paths([[2, 2], [8, 8], [9, 0], [0, 0], [1, 1]], am.EUCLIDEAN)
+    assert [s for s, _ in res] == [am.EINVAL, am.EUNCOVERED, am.EINVAL, am.OK, am.OK]
+    assert res[3][1].tolist() == [[0, 0]]
+    with pytest.raises(am.UncoveredTargetError):
+        am.reconstruct_euclidean(am.propagate(occ, [[0, 0]], 1), occ, [[0, 0]], [8, 8])
+    with pytest.raises(am.InvalidInputError):
+        am.Grid(occ, [[2, 2]])
+    with pytest.raises(am.InvalidInputError):
+        am.Grid(occ, [[9, 9]])
+    g.close()
+
+
+def test_promotion_to_32bit_cells():
+    """A serpentine longer than the 16-bit range: auto mode promotes mid-run, exactly."""
+    occ = O.comb_maze(330, 200)  # corridor ~ 330*100 cells > 32767
+    src = np.array([[0, 329]], np.uint32)
+    sm = O.source_mask(occ, src)
+    g = am.Grid(occ, src)
+    r = g.propagate_auto(200_000)
+    hops = O.bfs_multi_source(occ, sm)
+    ecc = int(hops[hops != O.UNREACH].max())
+    assert ecc > 32767 and r.cell_bits == 32
+    assert (r.layers_used, r.cause) == (ecc, O.FILLED)
+    bad, _ = O.check_activity(occ, g.activity(), hops, r.layers_used)
+    assert bad == 0
+    # fixed L beyond 16 bits starts in 32-bit cells
+    occ2 = O.random_maze(64, 48, 0.2, 3)
+    src2 = O.sample_free_cells(occ2, 2, 3)
+    L = 40_000
+    assert np.array_equal(am.propagate(occ2, src2, L), O.propagate(occ2, O.source_mask(occ2, src2), L, threads=8))
+    g.close()
+
+
+def test_repeat_after_download_and_mixed_calls():
+    """Download reuses the idle buffer as staging; the next solve must be unaffected."""
+    occ = O.random_maze(777, 333, 0.3, 8)
+    src = O.sample_free_cells(occ, 3, 8)
+    sm = O.source_mask(occ, src)
+    g = am.Grid(occ, src)
+    ref, rl, rc = O.propagate_auto(occ, sm, 5000, threads=8)
+    for _ in range(3):
+        r = g.propagate_auto(5000)
+        assert (r.layers_used, r.cause) == (rl, rc)
+        assert np.array_equal(g.activity(), ref)
+    g.propagate(20)
+    assert np.array_equal(g.activity(), O.propagate(occ, sm, 20))
+    g.close()
