@@ -338,7 +338,13 @@ def run_b200(args, rank, world, local_rank):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    # teardown order: torch's pinned-memory allocator records events on the context stream when these
+    # buffers die, so release them (and sync) before the context and its stream go away
+    del h_pts, h_off, h_status, d_pts, d_off, d_status
+    torch.cuda.synchronize()
+    ctx.synchronize()
     grid.close()
+    return ctx
 
 
 def main():
@@ -361,11 +367,14 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
-    run_b200(args, rank, world, local_rank)
+    keep = run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)  # skip interpreter teardown (ctx/stream vs torch caching allocators)
 
 
 if __name__ == "__main__":

@@ -166,7 +166,7 @@ struct Rows<32> {
 // One streaming step: x holds the newly loaded row (layer 0, row t); layer j
 // produces row t-j from layer j-1's rows t-j-1, t-j (window) and t-j+1 (x).
 // PH selects which window slot holds the older row (it is overwritten).
-template <int CB, int PH>
+template <int CB, int PH, bool SRC>
 __device__ __forceinline__ void stream_step(uint32_t (&x)[kWPL], uint32_t (&P0)[kK][kWPL],
                                             uint32_t (&P1)[kK][kWPL], uint32_t srcbits,
                                             const uint8_t* sA, const uint8_t* sB, size_t pitch, int lane) {
@@ -186,7 +186,7 @@ __device__ __forceinline__ void stream_step(uint32_t (&x)[kWPL], uint32_t (&P0)[
       const uint32_t ctr = PH == 0 ? P1[j][w] : P0[j][w];  // layer j-1, row t-j-1+1
       y[w] = C::max3(l, v[w], r) & (ctr | C::LOW);
     }
-    if ((srcbits >> (j + 1)) & 1u) {  // row t-(j+1) holds a source (warp-uniform, rare)
+    if (SRC && ((srcbits >> (j + 1)) & 1u)) {  // row t-(j+1) holds a source (warp-uniform, rare)
       uint32_t s[kWPL];
       const size_t off = (size_t)(j + 1) * pitch;
       Rows<CB>::src_words(sA - off, sB - off, s);
@@ -240,7 +240,19 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(Geo g, const typename C
 
   Rows<CB> nxt;
   nxt.load(pA, pB);
+  // source-row flags arrive as a 32-row ballot window, loaded one window ahead
+  auto row_flag = [&](uint32_t step) -> uint32_t {
+    if (step >= T_steps) return 0u;
+    uint32_t f = rowsrc[rA + step];
+    if (CB == 16) f |= rowsrc[rB + step];
+    return f;
+  };
+  uint32_t flag_lane = row_flag(lane), flag_win = 0;
   for (uint32_t t = 0; t < T_steps; t += 2) {
+    if ((t & 31u) == 0) {
+      flag_win = __ballot_sync(0xffffffffu, flag_lane != 0u);
+      flag_lane = row_flag(t + 32 + lane);
+    }
 #pragma unroll
     for (int ph = 0; ph < 2; ++ph) {
       const uint32_t tt = t + ph;
@@ -248,13 +260,16 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(Geo g, const typename C
       nxt.words(x);
       const size_t roff = (size_t)tt * pitch;
       if (tt + 1 < T_steps) nxt.load(pA + roff + pitch, pB + roff + pitch);
-      uint32_t f = rowsrc[rA + tt];
-      if (CB == 16) f |= rowsrc[rB + tt];
-      srcbits = (srcbits << 1) | (f ? 1u : 0u);
-      if (ph == 0)
-        stream_step<CB, 0>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-      else
-        stream_step<CB, 1>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+      srcbits = (srcbits << 1) | ((flag_win >> (tt & 31u)) & 1u);
+      // rows t-1 .. t-kK are in flight; only steps that touch a source row pay for the +1
+      const bool src_rows = __any_sync(0xffffffffu, (srcbits & (((1u << kK) - 1u) << 1)) != 0u);
+      if (ph == 0) {
+        if (src_rows) stream_step<CB, 0, true>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+        else stream_step<CB, 0, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+      } else {
+        if (src_rows) stream_step<CB, 1, true>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+        else stream_step<CB, 1, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+      }
       if (tt >= 2 * kK && tt < 2 * kK + g.seg_len && store_lane) {
         Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch);
 #pragma unroll
