@@ -17,7 +17,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libactmap_b200.so")
+LIB_PATH = os.environ.get("ACTMAP_LIB") or os.path.join(_HERE, "libactmap_b200.so")  # override: A/B kernel builds
 
 OK, EINVAL, EUNCOVERED, ECUDA, EOOM, ENCCL, EINTERNAL = 0, 1, 2, 3, 4, 5, 6
 FILLED, STALLED, CAP, FIXED = 0, 1, 2, 3          # AutoStop (propagate.hpp:45-49) + fixed

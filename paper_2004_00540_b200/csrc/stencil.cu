@@ -178,33 +178,93 @@ __device__ __forceinline__ void stream_step(uint32_t (&x)[kWPL], uint32_t (&P0)[
     for (int w = 0; w < kWPL; ++w) v[w] = C::max3(P0[j][w], P1[j][w], x[w]);
     const uint32_t left = __shfl_up_sync(0xffffffffu, v[kWPL - 1], 1);
     const uint32_t right = __shfl_down_sync(0xffffffffu, v[0], 1);
-    uint32_t y[kWPL];
+    // the older window row is dead once v exists: it takes this layer's input row
 #pragma unroll
     for (int w = 0; w < kWPL; ++w) {
-      const uint32_t l = w == 0 ? left : v[w - 1];
-      const uint32_t r = w == kWPL - 1 ? right : v[w + 1];
-      const uint32_t ctr = PH == 0 ? P1[j][w] : P0[j][w];  // layer j-1, row t-j-1+1
-      y[w] = C::max3(l, v[w], r) & (ctr | C::LOW);
+      if (PH == 0) P0[j][w] = x[w];
+      else P1[j][w] = x[w];
     }
+    // interior words first: they do not wait for the shuffles
+#pragma unroll
+    for (int w = 1; w < kWPL - 1; ++w) {
+      const uint32_t ctr = PH == 0 ? P1[j][w] : P0[j][w];  // layer j-1, row t-j-1+1
+      x[w] = C::max3(v[w - 1], v[w], v[w + 1]) & (ctr | C::LOW);
+    }
+    x[0] = C::max3(left, v[0], v[1]) & ((PH == 0 ? P1[j][0] : P0[j][0]) | C::LOW);
+    x[kWPL - 1] = C::max3(v[kWPL - 2], v[kWPL - 1], right) & ((PH == 0 ? P1[j][kWPL - 1] : P0[j][kWPL - 1]) | C::LOW);
     if (SRC && ((srcbits >> (j + 1)) & 1u)) {  // row t-(j+1) holds a source (warp-uniform, rare)
       uint32_t s[kWPL];
       const size_t off = (size_t)(j + 1) * pitch;
       Rows<CB>::src_words(sA - off, sB - off, s);
 #pragma unroll
-      for (int w = 0; w < kWPL; ++w) y[w] += s[w];
-    }
-#pragma unroll
-    for (int w = 0; w < kWPL; ++w) {
-      if (PH == 0) P0[j][w] = x[w];
-      else P1[j][w] = x[w];
-      x[w] = y[w];
+      for (int w = 0; w < kWPL; ++w) x[w] += s[w];
     }
   }
   (void)lane;
 }
 
+// ---- TMA bulk-copy staging (cp.async.bulk + mbarrier), one ring per warp ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+#ifndef AM_STAGES
+#define AM_STAGES 4
+#endif
+constexpr int kStages = AM_STAGES;                 // rows in flight per warp
+constexpr int kStageBytes = kBand * 4;             // one u32 row, or the A+B pair of u16 rows
+constexpr int kWarpsPerCta = kBlockThreads / 32;
+constexpr int kBlockSmem = kWarpsPerCta * kStages * kStageBytes;
+
 template <int CB>
-__global__ void __launch_bounds__(kBlockThreads) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
+__device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint32_t (&x)[kWPL]) {
+  if constexpr (CB == 16) {
+    const uint4 a = reinterpret_cast<const uint4*>(stage)[lane];
+    const uint4 b = reinterpret_cast<const uint4*>(stage + kBand * 2)[lane];
+    const uint32_t A[4] = {a.x, a.y, a.z, a.w}, B[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[2 * i] = __byte_perm(A[i], B[i], 0x5410);
+      x[2 * i + 1] = __byte_perm(A[i], B[i], 0x7632);
+    }
+  } else {
+    const uint4 a = reinterpret_cast<const uint4*>(stage)[2 * lane];
+    const uint4 b = reinterpret_cast<const uint4*>(stage)[2 * lane + 1];
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  }
+}
+
+#ifndef AM_BLOCK_MINB
+#define AM_BLOCK_MINB 3  // CTAs per SM the register budget is sized for (12 warps, <= 170 regs)
+#endif
+template <int CB>
+__global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
                                                          typename Cell<CB>::T* __restrict__ out,
                                                          const uint8_t* __restrict__ srcmask,
                                                          const uint8_t* __restrict__ rowsrc,
@@ -238,8 +298,28 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(Geo g, const typename C
   uint32_t acc = 0xFFFFFFFFu;
   uint32_t srcbits = 0;
 
-  Rows<CB> nxt;
-  nxt.load(pA, pB);
+  // Each lane streams its own 16-32 B of every row through a private kStages
+  // deep shared-memory ring with cp.async (LDGSTS): the copies run
+  // kStages-1 rows ahead without holding registers, and since no lane reads
+  // another lane's slot no barrier or fence is needed.
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * kStages * kStageBytes;
+  auto issue = [&](uint32_t step) {
+    uint8_t* dst = ring + (step % kStages) * kStageBytes;
+    if (step < T_steps) {
+      const size_t off = (size_t)step * pitch;
+      if (CB == 16) {
+        cp_async16(dst + lane * 16, pA + off);
+        cp_async16(dst + kBand * 2 + lane * 16, pB + off);
+      } else {
+        cp_async16(dst + lane * 32, pA + off);
+        cp_async16(dst + lane * 32 + 16, pA + off + 16 / sizeof(T));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) issue(s);
   // source-row flags arrive as a 32-row ballot window, loaded one window ahead
   auto row_flag = [&](uint32_t step) -> uint32_t {
     if (step >= T_steps) return 0u;
@@ -257,9 +337,10 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(Geo g, const typename C
     for (int ph = 0; ph < 2; ++ph) {
       const uint32_t tt = t + ph;
       uint32_t x[kWPL];
-      nxt.words(x);
+      issue(tt + kStages - 1);  // refills the slot consumed by the previous step
+      asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
+      stage_words<CB>(ring + (tt % kStages) * kStageBytes, lane, x);
       const size_t roff = (size_t)tt * pitch;
-      if (tt + 1 < T_steps) nxt.load(pA + roff + pitch, pB + roff + pitch);
       srcbits = (srcbits << 1) | ((flag_win >> (tt & 31u)) & 1u);
       // rows t-1 .. t-kK are in flight; only steps that touch a source row pay for the +1
       const bool src_rows = __any_sync(0xffffffffu, (srcbits & (((1u << kK) - 1u) << 1)) != 0u);
@@ -436,17 +517,17 @@ void launch_block(const Geo& g, int cb, const void* in, void* out, const uint8_t
   const uint32_t warps = g.nbands * ntiles;
   const uint32_t blocks = (warps + kBlockThreads / 32 - 1) / (kBlockThreads / 32);
   if (cb == 16)
-    k_block<16><<<blocks, kBlockThreads, 0, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, rowsrc, flag);
+    k_block<16><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, rowsrc, flag);
   else
-    k_block<32><<<blocks, kBlockThreads, 0, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, rowsrc, flag);
+    k_block<32><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, rowsrc, flag);
 }
 
 int block_kernel_blocks_per_sm(int cb) {
   int n = 0;
   if (cb == 16)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<16>, kBlockThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<16>, kBlockThreads, kBlockSmem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<32>, kBlockThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<32>, kBlockThreads, kBlockSmem);
   return n;
 }
 
