@@ -244,10 +244,11 @@ def _path_cap(vals):
     return int(np.max(vals)) + 2 if vals.size else 2
 
 
-def reconstruct_simple(occ, srcmask, vals, target, seed):
+def reconstruct_simple(occ, srcmask, vals, target, seed, cap=None):
+    """cap: point capacity (defaults to max(vals)+2; pass layers+2 on big maps)."""
     occ, sm, v = _u8(occ), _u8(srcmask), _u32(vals)
     h, w = occ.shape
-    cap = _path_cap(v)
+    cap = cap or _path_cap(v)
     pts = np.empty((cap, 2), np.uint32)
     n = C.c_uint64(0)
     st = lib().or_reconstruct_simple(w, h, _p(occ, _u8p), _p(sm, _u8p), _p(v, _u32p), int(target[0]),
@@ -255,10 +256,10 @@ def reconstruct_simple(occ, srcmask, vals, target, seed):
     return st, pts[: n.value].copy()
 
 
-def reconstruct_euclidean(occ, srcmask, vals, target, rule=STRICT):
+def reconstruct_euclidean(occ, srcmask, vals, target, rule=STRICT, cap=None):
     occ, sm, v = _u8(occ), _u8(srcmask), _u32(vals)
     h, w = occ.shape
-    cap = _path_cap(v)
+    cap = cap or _path_cap(v)
     pts = np.empty((cap, 2), np.uint32)
     n = C.c_uint64(0)
     st = lib().or_reconstruct_euclidean(w, h, _p(occ, _u8p), _p(sm, _u8p), _p(v, _u32p), int(target[0]),

@@ -1,0 +1,130 @@
+// Drop-in check of the actmap:: C++ API (include/actmap/*.hpp, same
+// signatures as the reference headers) on the device.  Built and run by
+// tests/test_cpp_api.py; prints one line per check, exits nonzero on failure.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "actmap/b200.hpp"
+#include "actmap/errors.hpp"
+#include "actmap/propagate.hpp"
+#include "actmap/reconstruct.hpp"
+
+using namespace actmap;
+
+static int failures = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #cond);           \
+      ++failures;                                                          \
+    }                                                                      \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main() {
+  // 9x9 empty grid, centre source, L=4 -> corner 1, centre 5, no zeros
+  {
+    const GridMap g = build_grid(9, 9, {});
+    const std::vector<Coord> s{{4, 4}};
+    const SourceSet src(g, s);
+    const ActivityMap m = propagate(g, src, 4);
+    CHECK(m.at(0, 0) == 1 && m.at(4, 4) == 5 && m.zero_free_cells(g) == 0 && m.layers_applied() == 4);
+    for (uint32_t r = 0; r < 9; ++r)
+      for (uint32_t c = 0; c < 9; ++c) CHECK(m.at(r, c) == 5 - chebyshev({r, c}, {4, 4}));
+    const ActivityMap it = propagate(g, src, 4, Mode::kIterative);
+    CHECK(it == m);
+    CHECK(propagate_reference(g, src, 4) == m);
+    // auto -> L_used 4, filled
+    const AutoResult a = propagate_auto(g, src, 100);
+    CHECK(a.layers_used == 4 && a.cause == AutoStop::kFilled && a.map == m);
+    // simple path, any seed -> 4 steps
+    for (uint64_t seed : {0ull, 1ull, 7ull}) CHECK(reconstruct_simple(m, g, src, {0, 0}, seed).steps() == 4);
+    // propagate_layer from the initial map == propagate(L=1)
+    CHECK(propagate_layer(ActivityMap::initial(g, src), g, src) == propagate(g, src, 1));
+    CHECK(layer_bound(g).worst_case == 49);
+  }
+  // Euclidean path (2,2) -> (0,0) is two diagonal moves, length 2*sqrt(2)
+  {
+    const GridMap g = build_grid(5, 5, {});
+    const std::vector<Coord> s{{0, 0}};
+    const SourceSet src(g, s);
+    const AutoResult a = propagate_auto(g, src, 20);
+    const Path p = reconstruct_euclidean(a.map, g, src, {2, 2});
+    CHECK(p.points.size() == 3 && p.points[1] == (Coord{1, 1}));
+    CHECK(std::fabs(path_metrics(p).euclidean_length - 2 * std::sqrt(2.0)) < 1e-12);
+    // reconstruct on a host-built map (uploaded, not device-backed)
+    const ActivityMap host(a.map.width(), a.map.height(),
+                           std::vector<uint32_t>(a.map.values().begin(), a.map.values().end()), a.layers_used);
+    CHECK(reconstruct_euclidean(host, g, src, {2, 2}).points == p.points);
+  }
+  // errors (errors.hpp; grid.hpp:59-61,78)
+  {
+    const GridMap g = build_grid(9, 9, std::vector<Coord>{{2, 2}});
+    const std::vector<Coord> s{{0, 0}};
+    const SourceSet src(g, s);
+    const ActivityMap m = propagate(g, src, 1);
+    CHECK(throws<UncoveredTargetError>([&] { reconstruct_euclidean(m, g, src, {8, 8}); }));
+    CHECK(throws<InvalidInputError>([&] { reconstruct_simple(m, g, src, {2, 2}, 0); }));
+    CHECK(throws<InvalidInputError>([&] { reconstruct_simple(m, g, src, {9, 0}, 0); }));
+    CHECK(throws<InvalidInputError>([&] { propagate(g, src, 0); }));
+    CHECK(throws<InvalidInputError>([&] { propagate_auto(g, src, 0); }));
+    CHECK(throws<InvalidInputError>([&] { build_grid(0, 3, {}); }));
+    CHECK(throws<InvalidInputError>([&] { build_grid(3, 3, std::vector<Coord>{{3, 0}}); }));
+    CHECK(throws<InvalidInputError>([&] { SourceSet(g, std::vector<Coord>{{2, 2}}); }));
+    CHECK(throws<InvalidInputError>([&] { SourceSet(g, std::vector<Coord>{}); }));
+  }
+  // comb maze: auto L_used == BFS eccentricity of the corridor end
+  {
+    const GridMap g = comb_maze(9, 9);
+    const std::vector<Coord> s{{0, 8}};
+    const SourceSet src(g, s);
+    const AutoResult a = propagate_auto(g, src, 1000);
+    CHECK(a.cause == AutoStop::kFilled);
+    CHECK(a.map.max_value() == a.layers_used + 1);
+  }
+  // batched planner on a random maze: every path step-optimal and ends at a source
+  {
+    const GridMap g = random_maze(600, 400, 0.3, 11);
+    std::vector<Coord> s;
+    for (uint32_t r = 0; r < 400 && s.size() < 4; r += 97)
+      for (uint32_t c = 0; c < 600 && s.size() < 4; c += 131)
+        if (g.is_free({r, c})) s.push_back({r, c});
+    const SourceSet src(g, s);
+    b200::Planner planner(g, src);
+    const AutoResult a = planner.propagate_auto(2400);
+    std::vector<Coord> targets;
+    for (uint32_t r = 5; r < 400; r += 37)
+      for (uint32_t c = 3; c < 600; c += 53)
+        if (g.is_free({r, c})) targets.push_back({r, c});
+    const auto paths = planner.reconstruct_all(targets, b200::Method::kEuclidean);
+    int ok = 0;
+    for (size_t i = 0; i < paths.size(); ++i) {
+      const uint32_t at = a.map.at(targets[i]);
+      if (at == 0) {
+        CHECK(paths[i].status == b200::TargetStatus::kUncovered);
+        continue;
+      }
+      CHECK(paths[i].status == b200::TargetStatus::kOk);
+      CHECK(paths[i].path.steps() == a.layers_used + 1 - at);
+      CHECK(src.contains(paths[i].path.source()));
+      CHECK(paths[i].path.points == reconstruct_euclidean(a.map, g, src, targets[i]).points);
+      ++ok;
+    }
+    CHECK(ok > 10);
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
