@@ -185,6 +185,95 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+class Solver:
+    """One timed step = propagate_auto to the fixed point + Euclidean paths of this rank's targets to the host.
+
+    N == 1: the whole C4 grid on one GPU (inputs resident in HBM).
+    N > 1: row slabs (one per rank, NCCL halo exchange per block), the fixed-point map all-gathered into a
+    full-size field on every rank, each rank tracing targets[rank::N]."""
+
+    def __init__(self, am, torch, ctx, occ, src, tgt, rank, world, local_rank):
+        self.am, self.torch, self.ctx, self.world, self.rank = am, torch, ctx, world, rank
+        dev = torch.device(f"cuda:{local_rank}")
+        self.stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+        d_occ = torch.from_numpy(occ).to(dev)
+        d_src = torch.from_numpy(src.astype(np.int32)).to(dev)
+        my_tgt = tgt[rank::world]
+        self.tgt = my_tgt
+        self.d_tgt = torch.from_numpy(my_tgt.astype(np.int32)).to(dev)
+        torch.cuda.synchronize()
+        self.full = am.Grid.from_device(W, H, d_occ.data_ptr(), d_src.data_ptr(), len(src), ctx)
+        self.slab = None
+        if world > 1:
+            r0, r1 = ctx.slab_rows(H)
+            self.slab = am.Grid.slab(occ, src, r0, r1, ctx)
+        del d_occ, d_src
+        n = len(my_tgt)
+        self.n = n
+        self.d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        self.d_status = torch.zeros(n, dtype=torch.int32, device=dev)
+        r = self.propagate()
+        off, st = self.full.path_counts(my_tgt, am.EUCLIDEAN)
+        self.total = int(off[-1])
+        self.covered = int((st == 0).sum())
+        self.d_pts = torch.empty(2 * max(self.total, 1), dtype=torch.int32, device=dev)
+        self.h_pts = torch.empty(2 * max(self.total, 1), dtype=torch.int32, pin_memory=True)
+        self.h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        self.h_status = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        log(f"[rank {rank}] L_used={r.layers_used} cause={r.cause} computed={r.layers_computed} bits={r.cell_bits} "
+            f"blocks={r.block_launches} paths: points={self.total}, covered={self.covered}/{n}")
+
+    def propagate(self):
+        if self.slab is None:
+            return self.full.propagate_auto(AUTO_CAP)
+        r = self.slab.propagate_auto(AUTO_CAP)
+        self.ctx.comm_gather(self.slab, self.full)
+        return r
+
+    def trace(self):
+        self.ctx.trace_device(self.full, self.d_tgt.data_ptr(), self.n, self.am.EUCLIDEAN, 0, self.d_off.data_ptr(),
+                              self.d_pts.data_ptr(), self.total, self.d_status.data_ptr())
+
+    def step(self):
+        r = self.propagate()
+        self.trace()
+        with self.torch.cuda.stream(self.stream):
+            self.h_pts.copy_(self.d_pts, non_blocking=True)
+            self.h_off.copy_(self.d_off, non_blocking=True)
+            self.h_status.copy_(self.d_status, non_blocking=True)
+        return r
+
+    def close(self):
+        del self.h_pts, self.h_off, self.h_status, self.d_pts, self.d_off, self.d_status, self.d_tgt
+        self.torch.cuda.synchronize()
+        self.ctx.synchronize()
+        if self.slab is not None:
+            self.slab.close()
+        self.full.close()
+
+
+def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map):
+    """One end-to-end solve through the C ABI with host buffers (pinned)."""
+    my_tgt = tgt[rank::world]
+    if world == 1:
+        g = am.Grid(occ, src, ctx)
+        g.propagate_auto(AUTO_CAP)
+        off, pts, st = g.trace(my_tgt, am.EUCLIDEAN)
+        g.activity(out=h_map)
+        g.close()
+        return off, pts, st
+    r0, r1 = ctx.slab_rows(H)
+    s = am.Grid.slab(occ, src, r0, r1, ctx)
+    s.propagate_auto(AUTO_CAP)
+    s.activity(out=h_map[r0:r1])
+    full = am.Grid(occ, src, ctx)
+    ctx.comm_gather(s, full)
+    off, pts, st = full.trace(my_tgt, am.EUCLIDEAN)
+    s.close()
+    full.close()
+    return off, pts, st
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
 
@@ -197,48 +286,22 @@ def run_b200(args, rank, world, local_rank):
 
     occ, src, tgt = make_workload(am)
     ctx = am.Context(local_rank, timing=True)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=f"cuda:{local_rank}")
-    dev = torch.device(f"cuda:{local_rank}")
-    d_occ = torch.from_numpy(occ).to(dev)
-    d_src = torch.from_numpy(src.astype(np.int32)).to(dev)
-    d_tgt = torch.from_numpy(tgt.astype(np.int32)).to(dev)
-    torch.cuda.synchronize()
-    grid = am.Grid.from_device(W, H, d_occ.data_ptr(), d_src.data_ptr(), len(src), ctx)
-    n = len(tgt)
-    d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    d_status = torch.zeros(n, dtype=torch.int32, device=dev)
-
-    # first solve sizes the point buffer (total points is a pure function of the workload)
-    r = grid.propagate_auto(AUTO_CAP)
-    off, st = grid.path_counts(tgt, am.EUCLIDEAN)
-    total = int(off[-1])
-    d_pts = torch.empty(2 * max(total, 1), dtype=torch.int32, device=dev)
-    h_pts = torch.empty(2 * max(total, 1), dtype=torch.int32, pin_memory=True)
-    h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
-    h_status = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    log(f"L_used={r.layers_used} cause={r.cause} computed={r.layers_computed} bits={r.cell_bits} "
-        f"blocks={r.block_launches} paths: total points={total}, covered={(st == 0).sum()}/{n}")
-
-    def step():
-        rr = grid.propagate_auto(AUTO_CAP)
-        ctx.trace_device(grid, d_tgt.data_ptr(), n, am.EUCLIDEAN, 0, d_off.data_ptr(), d_pts.data_ptr(), total,
-                         d_status.data_ptr())
-        with torch.cuda.stream(stream):
-            h_pts.copy_(d_pts, non_blocking=True)
-            h_off.copy_(d_off, non_blocking=True)
-            h_status.copy_(d_status, non_blocking=True)
-        return rr
+    if world > 1:
+        uid = [am.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(world, rank, uid[0])
+    sol = Solver(am, torch, ctx, occ, src, tgt, rank, world, local_rank)
+    stream = sol.stream
 
     for _ in range(args.warmup):
-        step()
+        sol.step()
     ctx.synchronize()
-    # phase split for the report (untimed): propagate alone
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    # phase split for the report (untimed): propagate (+ gather) vs paths
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record(stream)
-    rprop = grid.propagate_auto(AUTO_CAP)
+    sol.propagate()
     ev[1].record(stream)
-    ctx.trace_device(grid, d_tgt.data_ptr(), n, am.EUCLIDEAN, 0, d_off.data_ptr(), d_pts.data_ptr(), total,
-                     d_status.data_ptr())
+    sol.trace()
     ev[2].record(stream)
     ctx.synchronize()
     prop_ms, path_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
@@ -253,7 +316,7 @@ def run_b200(args, rank, world, local_rank):
     t_start.record(stream)
     stencil_ms, blocks, res = 0.0, 0, None
     for _ in range(args.steps):
-        res = step()
+        res = sol.step()
         stencil_ms += res.stencil_ms
         blocks += res.block_launches
     t_end.record(stream)
@@ -265,47 +328,52 @@ def run_b200(args, rank, world, local_rank):
     launches = ctx.kernel_launches() - launches0
     clk = clocks.stop() if clocks else None
     if dist:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    assert int((h_status == 0).sum()) == int((st == 0).sum())
+    assert int((sol.h_status == 0).sum()) == sol.covered
     L = res.layers_used
     cell_updates = W * H * L
-    value = world * cell_updates / (ms_step / 1000) / 1e9
+    value = cell_updates / (ms_step / 1000) / 1e9  # whole job: the full grid's cell-updates per second
 
     # roofline of the dominant kernel (k_block): algorithmic bytes per launch / mean launch time
     peak, peak_src = peaks()
+    rows_here = (sol.slab.height if sol.slab is not None else H)
     per_launch_ms = stencil_ms / max(blocks, 1)
-    alg_bytes = BYTES_PER_CELL_UPDATE * W * H * LAYERS_PER_BLOCK
+    alg_bytes = BYTES_PER_CELL_UPDATE * W * rows_here * LAYERS_PER_BLOCK
     achieved = alg_bytes / (per_launch_ms / 1000) / 1e9
-    stencil_gcells = W * H * LAYERS_PER_BLOCK / (per_launch_ms / 1000) / 1e9
+    stencil_gcells = W * rows_here * LAYERS_PER_BLOCK / (per_launch_ms / 1000) / 1e9
 
     # end-to-end through the C ABI with host buffers (H2D of the grid, D2H of map + paths inside the timing)
     e2e = None
-    if rank == 0 or world > 1:
+    if not args.no_e2e:
         h_occ = torch.from_numpy(occ).pin_memory().numpy()
         h_map = torch.empty((H, W), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         e2e_times = []
         for i in range(3):
+            if dist:
+                dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            g2 = am.Grid(h_occ, src, ctx)
-            g2.propagate_auto(AUTO_CAP)
-            off2, pts2, st2 = g2.trace(tgt, am.EUCLIDEAN)
-            g2.activity(out=h_map)
+            off2, pts2, st2 = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map)
             ctx.synchronize()
             dt = time.perf_counter() - t0
-            g2.close()
+            if dist:
+                t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local_rank}")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t.item())
             if i:
                 e2e_times.append(dt)
         e2e_s = statistics.median(e2e_times)
-        h2d = occ.nbytes + src.nbytes + tgt.nbytes * 2 + off2.nbytes + st2.nbytes
-        d2h = h_map.nbytes + pts2.nbytes + off2.nbytes + st2.nbytes * 2
-        e2e = {"value": round(world * cell_updates / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        rows_map = rows_here
+        h2d = occ.nbytes + src.nbytes + tgt.nbytes * 2 // world + off2.nbytes + st2.nbytes
+        d2h = W * rows_map * 4 + pts2.nbytes + off2.nbytes + st2.nbytes * 2
+        e2e = {"value": round(cell_updates / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "time_to_solve_s": round(e2e_s, 4),
                "api": "am_grid_create(host) + am_propagate(auto) + am_path_counts + am_trace_paths + "
-                      "am_activity_download (pinned host buffers)"}
+                      "am_activity_download (pinned host buffers)" +
+                      ("; per rank: slab grid, NCCL halos, am_comm_gather" if world > 1 else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -315,15 +383,16 @@ def run_b200(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u16x2" if res.cell_bits == 16 else "u32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u16x2" if res.cell_bits == 16 else "u32",
             "data": "synthetic",
             "config": {"workload": f"C4: {W}x{H} random_maze(density 0.40, seed 4), {N_SOURCES} sources, "
                                    f"{N_TARGETS} targets, propagate_auto(cap {AUTO_CAP}) + Euclidean paths to host",
                        "grid": [W, H], "sources": N_SOURCES, "targets": N_TARGETS, "auto_cap": AUTO_CAP,
-                       "parallelism": "single GPU" if world == 1 else f"replicas x{world}",
+                       "parallelism": "single GPU" if world == 1 else f"row slabs x{world} (NCCL K=8 halos)",
                        "l2": "inputs larger than L2 (1.07 GB 16-bit field vs 126 MB L2), no flush"},
             "time_to_solve_s": round(ms_step / 1000, 4),
-            "layers_used": L, "layers_computed": res.layers_computed, "termination": ["filled", "stalled", "cap"][res.cause],
+            "layers_used": L, "layers_computed": res.layers_computed,
+            "termination": ["filled", "stalled", "cap"][res.cause],
             "phase_ms": {"propagate": round(prop_ms, 3), "paths": round(path_ms, 3),
                          "path_share": round(path_ms / max(prop_ms + path_ms, 1e-9), 4)},
             "stencil_gcell_per_s": round(stencil_gcells, 2),
@@ -331,7 +400,8 @@ def run_b200(args, rank, world, local_rank):
                          "frac": round(achieved / peak, 3), "traffic": ncu_traffic(),
                          "kernel": "am::k_block<16>", "algorithmic_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src,
-                         "note": "9 B per cell-update (reference uint32 layout) x W*H x 8 layers per launch"},
+                         "note": "9 B per cell-update (reference uint32 layout) x W*rows x 8 layers per launch; "
+                                 "traffic = ncu dram read+write per launch (profiles/)"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "e2e": e2e,
@@ -340,10 +410,7 @@ def run_b200(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
     # teardown order: torch's pinned-memory allocator records events on the context stream when these
     # buffers die, so release them (and sync) before the context and its stream go away
-    del h_pts, h_off, h_status, d_pts, d_off, d_status
-    torch.cuda.synchronize()
-    ctx.synchronize()
-    grid.close()
+    sol.close()
     return ctx
 
 
@@ -354,6 +421,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

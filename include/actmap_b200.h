@@ -137,6 +137,28 @@ am_status am_propagate_layer(am_ctx *ctx, uint32_t width, uint32_t height, const
 am_status am_propagate_reference(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *occupancy,
                                  const uint32_t *src_rc, uint64_t n_src, uint32_t layers, uint32_t *out);
 
+/* ---- multi-GPU row slabs ---------------------------------
+ * A slab grid owns rows [row0, row1) of a width x height grid; occupancy is
+ * the FULL grid (host), sources use global coordinates.  Slabs keep K=8
+ * halo rows refreshed before every launch.
+ *
+ * One process per GPU: am_comm_unique_id on one rank, share the 128 bytes,
+ * am_comm_init on every rank, am_comm_slab_rows for this rank's rows, then
+ * am_propagate on the slab grid (NCCL halo send/recv + flag all-reduce) and
+ * am_comm_gather into a full-size grid (am_grid_create) to trace paths.
+ *
+ * In-process (one device): am_slabs_propagate drives n consecutive slabs
+ * created on the same context; am_slabs_gather assembles the full map. */
+am_status am_grid_create_slab(am_ctx *ctx, uint32_t width, uint32_t height, uint32_t row0, uint32_t row1,
+                              const uint8_t *occupancy_full, const uint32_t *src_rc, uint64_t n_src, am_grid **out);
+am_status am_slabs_propagate(am_ctx *ctx, am_grid **slabs, uint32_t n, uint32_t layers, uint32_t auto_cap,
+                             uint32_t mode, am_prop_result *res);
+am_status am_slabs_gather(am_ctx *ctx, am_grid **slabs, uint32_t n, am_grid *full);
+am_status am_comm_unique_id(uint8_t *id_out /* 128 bytes */);
+am_status am_comm_init(am_ctx *ctx, uint32_t nranks, uint32_t rank, const uint8_t *id /* 128 bytes */);
+am_status am_comm_slab_rows(const am_ctx *ctx, uint32_t height, uint32_t *row0, uint32_t *row1);
+am_status am_comm_gather(am_ctx *ctx, am_grid *slab, am_grid *full);
+
 /* ---- host helpers of the planner API (no device work) ------------------ */
 /* random_maze / comb_maze (grid.hpp:65-76) into a caller buffer of W*H bytes. */
 am_status am_random_maze(uint32_t width, uint32_t height, double density, uint64_t seed, uint8_t *occupancy);

@@ -94,6 +94,13 @@ def lib():
             "am_trace_paths_device": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
             "am_propagate_layer": (st, [_vp, u32, u32, _vp, _vp, u64, _vp, _vp]),
             "am_propagate_reference": (st, [_vp, u32, u32, _vp, _vp, u64, u32, _vp]),
+            "am_grid_create_slab": (st, [_vp, u32, u32, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
+            "am_slabs_propagate": (st, [_vp, C.POINTER(_vp), u32, u32, u32, u32, C.POINTER(_PropResult)]),
+            "am_slabs_gather": (st, [_vp, C.POINTER(_vp), u32, _vp]),
+            "am_comm_unique_id": (st, [_vp]),
+            "am_comm_init": (st, [_vp, u32, u32, _vp]),
+            "am_comm_slab_rows": (st, [_vp, u32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+            "am_comm_gather": (st, [_vp, _vp, _vp]),
             "am_random_maze": (st, [u32, u32, C.c_double, u64, _vp]),
             "am_comb_maze": (st, [u32, u32, _vp]),
             "am_straighten": (st, [_vp, u64, _vp, u32, u32, u32, _vp, _u64p]),
@@ -166,6 +173,20 @@ class Context:
         _check(lib().am_ctx_get_stream(self.handle, C.byref(s)), self, "stream")
         return s.value or 0
 
+    # ---- multi-GPU (one process per GPU, NCCL) ----
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib().am_comm_init(self.handle, nranks, rank, C.cast(buf, C.c_void_p)), self, "comm_init")
+
+    def slab_rows(self, height: int):
+        a, b = C.c_uint32(0), C.c_uint32(0)
+        _check(lib().am_comm_slab_rows(self.handle, height, C.byref(a), C.byref(b)), self, "slab_rows")
+        return a.value, b.value
+
+    def comm_gather(self, slab: "Grid", full: "Grid"):
+        _check(lib().am_comm_gather(self.handle, slab.handle, full.handle), self, "comm_gather")
+        full.layers = slab.layers
+
     def trace_device(self, grid: "Grid", d_tgt: int, n: int, method: int, seed: int, d_offsets: int, d_pts: int,
                      cap: int, d_status: int):
         """am_trace_paths_device: device pointers in, no host round trip."""
@@ -234,6 +255,23 @@ class Grid:
                                            C.c_void_p(d_src_ptr), n_src, C.byref(h)), self.ctx, "grid")
         self.handle = h
         self.layers = 0
+        return self
+
+    @classmethod
+    def slab(cls, occupancy_full, sources, row0: int, row1: int, ctx: Context | None = None):
+        """Rows [row0, row1) of the full grid as a row slab (multi-GPU decomposition)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        occ = _occ(occupancy_full)
+        self.occ = None
+        self.height, self.width = row1 - row0, occ.shape[1]
+        src = _rc(sources)
+        h = C.c_void_p()
+        _check(lib().am_grid_create_slab(self.ctx.handle, occ.shape[1], occ.shape[0], row0, row1, _ptr(occ),
+                                         _ptr(src), len(src), C.byref(h)), self.ctx, "slab")
+        self.handle = h
+        self.layers = 0
+        self.row0, self.row1 = row0, row1
         return self
 
     def close(self):
@@ -313,6 +351,34 @@ class Grid:
             keep = p[:, 0] != 0xFFFFFFFF
             out.append((OK, p[keep]))
         return out
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL id for am_comm_init (create on one rank, share with all)."""
+    buf = (C.c_uint8 * 128)()
+    st = lib().am_comm_unique_id(C.cast(buf, C.c_void_p))
+    if st != OK:
+        raise Error(f"am_comm_unique_id failed (status {st})")
+    return bytes(buf)
+
+
+def slabs_propagate(slabs, layers: int = 0, auto_cap: int = 0, mode: int = BATCHED) -> PropResult:
+    """In-process row-slab group on one context: layers>0 fixed L, else auto with auto_cap."""
+    arr = (C.c_void_p * len(slabs))(*[s.handle for s in slabs])
+    r = _PropResult()
+    ctx = slabs[0].ctx
+    _check(lib().am_slabs_propagate(ctx.handle, arr, len(slabs), layers, auto_cap, mode, C.byref(r)), ctx,
+           "slabs_propagate")
+    for s in slabs:
+        s.layers = r.layers_used
+    return PropResult(r)
+
+
+def slabs_gather(slabs, full: Grid):
+    arr = (C.c_void_p * len(slabs))(*[s.handle for s in slabs])
+    ctx = slabs[0].ctx
+    _check(lib().am_slabs_gather(ctx.handle, arr, len(slabs), full.handle), ctx, "slabs_gather")
+    full.layers = slabs[0].layers
 
 
 # ---------------------------------------------------------------- free functions

@@ -1,0 +1,126 @@
+// am_host.hpp -- host-side state shared by capi.cu (single grid, propagation
+// driver, paths) and multigpu.cu (row slabs: in-process groups and NCCL).
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/actmap_b200.h"
+#include "am_internal.cuh"
+
+namespace am {
+constexpr int kFlagSlots = 64;
+constexpr int kLag = 2;  // blocks in flight before the host reads a fixed-point flag
+struct Comm;             // NCCL communicator wrapper (multigpu.cu)
+}  // namespace am
+
+struct am_ctx {
+  int device = 0;
+  uint32_t flags = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  int warp_slots = 0;
+  uint64_t launches = 0;
+  std::string err;
+  struct Timer {
+    cudaEvent_t a, b;
+  };
+  std::vector<Timer> timers;
+  am::Comm* comm = nullptr;  // set by am_comm_init
+};
+
+struct am_grid {
+  am::Geo g{};
+  int cell_bits = 16;
+  void* val[2] = {nullptr, nullptr};
+  int cur = 0;
+  uint8_t* srcmask = nullptr;        // pitched 0/1 (owned rows + halo rows for slabs)
+  uint8_t* rowsrc = nullptr;         // per allocated row: any source
+  uint8_t* occ = nullptr;            // dense owned rows (re-initialisation / plain maps)
+  uint8_t* srcmask_dense = nullptr;  // dense owned rows (plain maps)
+  uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots
+  uint32_t* h_flags = nullptr;       // pinned mirror
+  cudaEvent_t flag_ev[am::kFlagSlots];
+  uint32_t* plain = nullptr;         // caller-uploaded dense map
+  int plain_active = 0;
+  uint32_t plain_layers = 0;
+  int have_map = 0;
+  int dirty[2] = {0, 0};    // buffer reused as download staging: padding no longer unflagged
+  uint32_t computed = 0;    // layers represented by val[cur]
+  uint32_t layers_used = 0; // logical layers (val[cur] minus rollback)
+  // row-slab membership: this grid holds rows [row0, row0 + g.H) of a total_h-row grid
+  int slab = 0;
+  uint32_t total_h = 0, row0 = 0;
+  // scratch for path extraction
+  uint32_t* d_tgt = nullptr;
+  uint64_t* d_counts = nullptr;
+  uint64_t* d_offsets = nullptr;
+  int32_t* d_status = nullptr;
+  uint64_t tgt_cap = 0;
+  uint32_t* d_pts = nullptr;
+  uint64_t pts_cap = 0;
+};
+
+namespace am {
+
+inline am_status fail(am_ctx* ctx, am_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+inline bool dims_ok(uint32_t w, uint32_t h) { return w >= 1 && h >= 1 && w <= 65535 && h <= 65535; }
+
+// rows [first, last) of slab r out of n over h rows
+inline void slab_rows(uint32_t h, uint32_t n, uint32_t r, uint32_t* first, uint32_t* last) {
+  *first = (uint32_t)((uint64_t)h * r / n);
+  *last = (uint32_t)((uint64_t)h * (r + 1) / n);
+}
+
+// Halo transport used by the propagation driver between blocks.
+struct Transport {
+  virtual ~Transport() = default;
+  // enqueue the K-row halo refresh of every local slab (reads current buffers)
+  virtual am_status exchange() = 0;
+  // make the per-slab device word *w (one per local slab) global: min or max over all slabs
+  virtual am_status reduce(std::vector<uint32_t*>& words, bool take_max) = 0;
+  // local values must still be combined on the host (in-process groups)
+  virtual bool host_combine() const = 0;
+};
+
+struct SlabRef {
+  am_ctx* ctx;
+  am_grid* g;
+};
+
+// The propagation driver (capi.cu): runs slabs in lock step, 1 slab = single grid.
+am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t layers, uint32_t auto_cap,
+                            uint32_t mode, am_prop_result* res);
+am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t row0, uint32_t row1,
+                           const uint8_t* occ_full, const uint32_t* src, uint64_t n_src, bool device_ptrs,
+                           bool slab, am_grid** out);
+am_status set_cell_bits(am_ctx* ctx, am_grid* g, int cell_bits);
+
+}  // namespace am
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      (void)cudaGetLastError();                                                                      \
+      return am::fail(ctx, e_ == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s: %s (%s:%d)", #call, \
+                      cudaGetErrorString(e_), __FILE__, __LINE__);                                   \
+    }                                                                                                \
+  } while (0)
+
+#define CKL()                  \
+  do {                         \
+    ++ctx->launches;           \
+    CK(cudaPeekAtLastError()); \
+  } while (0)

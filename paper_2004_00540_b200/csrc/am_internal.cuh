@@ -58,8 +58,9 @@ Geo make_geo(uint32_t W, uint32_t H, int num_sms);
 // ---- kernels (stencil.cu) ----
 void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcmask, void* d_val,
                  int cell_bits, cudaStream_t s);
-void launch_scatter_sources(const Geo& g, const uint32_t* d_src_rc, uint64_t n, uint8_t* d_srcmask,
-                            uint8_t* d_rowsrc, int* d_err, cudaStream_t s);
+void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const uint32_t* d_src_rc, uint64_t n,
+                         uint8_t* d_dense, const uint8_t* d_occ, uint8_t* d_srcmask, uint8_t* d_rowsrc, int* d_err,
+                         cudaStream_t s);
 void launch_block(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
                   const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s);
 void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,

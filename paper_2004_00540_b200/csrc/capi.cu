@@ -9,98 +9,23 @@
 // layer without new cells exactly; blocks launched past it are undone by
 // subtracting the overshoot from every covered cell (exact: a covered cell
 // gains exactly +1 per layer once coverage is fixed).
+//
+// The same driver runs a stack of row slabs in lock step (multigpu.cu):
+// halos are refreshed through a Transport before every launch and the
+// per-block number is reduced across slabs.
 #include <algorithm>
-#include <cstdarg>
-#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <new>
-#include <string>
-#include <vector>
 
-#include "../../include/actmap_b200.h"
-#include "am_internal.cuh"
+#include "am_host.hpp"
 
 using am::Geo;
 
-namespace {
-
-constexpr int kFlagSlots = 64;
-constexpr int kLag = 2;  // blocks in flight before the host reads a flag
-
-struct Timer {
-  cudaEvent_t a, b;
-};
-
-}  // namespace
-
-struct am_ctx {
-  int device = 0;
-  uint32_t flags = 0;
-  cudaStream_t stream = nullptr;
-  int sms = 148;
-  int warp_slots = 0;
-  uint64_t launches = 0;
-  std::string err;
-  std::vector<Timer> timers;
-};
-
-struct am_grid {
-  Geo g{};
-  int cell_bits = 16;
-  void* val[2] = {nullptr, nullptr};
-  int cur = 0;
-  uint8_t* srcmask = nullptr;        // pitched 0/1
-  uint8_t* rowsrc = nullptr;         // per allocated row: any source
-  uint8_t* occ = nullptr;            // dense W*H (kept for re-init / plain maps)
-  uint8_t* srcmask_dense = nullptr;  // dense W*H (plain maps)
-  uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots
-  uint32_t* h_flags = nullptr;       // pinned mirror
-  cudaEvent_t flag_ev[kFlagSlots];
-  uint32_t* plain = nullptr;         // caller-uploaded dense map
-  int plain_active = 0;
-  uint32_t plain_layers = 0;
-  int have_map = 0;
-  int dirty[2] = {0, 0};    // buffer reused as download staging: padding no longer unflagged
-  uint32_t computed = 0;    // layers represented by val[cur]
-  uint32_t layers_used = 0; // logical layers (val[cur] minus rollback)
-  // scratch for path extraction
-  uint32_t* d_tgt = nullptr;
-  uint64_t* d_counts = nullptr;
-  uint64_t* d_offsets = nullptr;
-  int32_t* d_status = nullptr;
-  uint64_t tgt_cap = 0;
-  uint32_t* d_pts = nullptr;
-  uint64_t pts_cap = 0;
-};
-
-static am_status fail(am_ctx* ctx, am_status st, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  if (ctx) ctx->err = buf;
-  return st;
-}
-
-#define CK(call)                                                                        \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess) {                                                            \
-      (void)cudaGetLastError();                                                         \
-      return fail(ctx, e_ == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s: %s (%s:%d)", \
-                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                   \
-    }                                                                                   \
-  } while (0)
-
-#define CKL()                        \
-  do {                               \
-    ++ctx->launches;                 \
-    CK(cudaPeekAtLastError());       \
-  } while (0)
-
-static bool dims_ok(uint32_t w, uint32_t h) { return w >= 1 && h >= 1 && w <= 65535 && h <= 65535; }
+namespace am {
+void comm_destroy(Comm* c);
+Transport* make_nccl_transport(am_ctx* ctx, am_grid* g);
+}  // namespace am
 
 extern "C" {
 
@@ -129,6 +54,8 @@ am_status am_ctx_create(const am_ctx_opts* opts, am_ctx** out) {
 void am_ctx_destroy(am_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  am::comm_destroy(ctx->comm);
   for (auto& t : ctx->timers) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -157,6 +84,10 @@ am_status am_ctx_synchronize(am_ctx* ctx) {
   return AM_OK;
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------------ grids
+
 static void grid_free(am_grid* g) {
   if (!g) return;
   for (int i = 0; i < 2; ++i) cudaFree(g->val[i]);
@@ -166,7 +97,7 @@ static void grid_free(am_grid* g) {
   cudaFree(g->srcmask_dense);
   cudaFree(g->d_flags);
   if (g->h_flags) cudaFreeHost(g->h_flags);
-  for (int i = 0; i < kFlagSlots; ++i)
+  for (int i = 0; i < am::kFlagSlots; ++i)
     if (g->flag_ev[i]) cudaEventDestroy(g->flag_ev[i]);
   cudaFree(g->plain);
   cudaFree(g->d_tgt);
@@ -177,84 +108,97 @@ static void grid_free(am_grid* g) {
   delete g;
 }
 
-static am_status grid_create_impl(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t* occ, const uint32_t* src,
-                                  uint64_t n_src, bool device_ptrs, am_grid** out) {
+namespace am {
+
+// Rows [row0, row1) of an H_total-row grid.  occ_full / src use global
+// coordinates (host or device per device_ptrs).  For slabs, sources inside
+// the K-row halo bands are marked too (their +1 matters for the recomputed
+// halo rows); the halo values themselves arrive through the transport.
+am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t row0, uint32_t row1,
+                           const uint8_t* occ_full, const uint32_t* src, uint64_t n_src, bool device_ptrs,
+                           bool slab, am_grid** out) {
   if (!ctx || !out) return AM_EINVAL;
   *out = nullptr;
-  if (!dims_ok(W, H)) return fail(ctx, AM_EINVAL, "grid dimensions %ux%u outside 1..65535", W, H);
+  if (!dims_ok(W, H_total)) return fail(ctx, AM_EINVAL, "grid dimensions %ux%u outside 1..65535", W, H_total);
   if (n_src == 0) return fail(ctx, AM_EINVAL, "SourceSet must be nonempty");
-  if (!occ || !src) return fail(ctx, AM_EINVAL, "null occupancy or sources");
+  if (!occ_full || !src) return fail(ctx, AM_EINVAL, "null occupancy or sources");
+  if (row1 <= row0 || row1 > H_total) return fail(ctx, AM_EINVAL, "bad slab rows [%u, %u)", row0, row1);
+  if (slab && row1 - row0 < (uint32_t)kK) return fail(ctx, AM_EINVAL, "slab of %u rows < halo depth %d", row1 - row0, kK);
   CK(cudaSetDevice(ctx->device));
   am_grid* g = new (std::nothrow) am_grid();
   if (!g) return AM_EOOM;
   memset(g->flag_ev, 0, sizeof g->flag_ev);
-  g->g = am::make_geo(W, H, ctx->warp_slots);
+  const uint32_t H = row1 - row0;
+  g->g = make_geo(W, H, ctx->warp_slots);
+  g->slab = slab ? 1 : 0;
+  g->total_h = H_total;
+  g->row0 = row0;
   const size_t cells = (size_t)g->g.rows * g->g.pitch;
   const size_t dense = (size_t)W * H;
   cudaStream_t s = ctx->stream;
-  am_status st = AM_OK;
-  auto bail = [&](am_status code) {
-    grid_free(g);
-    return code;
-  };
-#define GCK(call)                                                                             \
-  do {                                                                                        \
-    cudaError_t e_ = (call);                                                                  \
-    if (e_ != cudaSuccess) {                                                                  \
-      (void)cudaGetLastError();                                                               \
-      st = fail(ctx, e_ == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s: %s", #call,   \
-                cudaGetErrorString(e_));                                                      \
-      return bail(st);                                                                        \
-    }                                                                                         \
-  } while (0)
-  GCK(cudaMalloc(&g->val[0], cells * 2));
-  GCK(cudaMalloc(&g->val[1], cells * 2));
-  GCK(cudaMalloc(&g->srcmask, cells));
-  GCK(cudaMalloc(&g->rowsrc, g->g.rows));
-  GCK(cudaMalloc(&g->occ, dense));
-  GCK(cudaMalloc(&g->srcmask_dense, dense));
-  GCK(cudaMalloc(&g->d_flags, kFlagSlots * sizeof(uint32_t)));
-  GCK(cudaHostAlloc(&g->h_flags, kFlagSlots * sizeof(uint32_t), cudaHostAllocDefault));
-  for (int i = 0; i < kFlagSlots; ++i) GCK(cudaEventCreateWithFlags(&g->flag_ev[i], cudaEventDisableTiming));
-  GCK(cudaMemsetAsync(g->val[0], 0, cells * 2, s));
-  GCK(cudaMemsetAsync(g->val[1], 0, cells * 2, s));
-  GCK(cudaMemsetAsync(g->srcmask, 0, cells, s));
-  GCK(cudaMemsetAsync(g->rowsrc, 0, g->g.rows, s));
-  GCK(cudaMemsetAsync(g->srcmask_dense, 0, dense, s));
-  GCK(cudaMemcpyAsync(g->occ, occ, dense, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   uint32_t* d_src = nullptr;
   int* d_err = nullptr;
-  GCK(cudaMalloc(&d_src, n_src * 2 * sizeof(uint32_t)));
-  GCK(cudaMalloc(&d_err, sizeof(int)));
-  GCK(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-  GCK(cudaMemcpyAsync(d_src, src, n_src * 2 * sizeof(uint32_t),
-                      device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-  am::launch_srcmask_dense(W, H, d_src, n_src, g->srcmask_dense, g->occ, d_err, s);
-  ++ctx->launches;
-  am::launch_scatter_sources(g->g, d_src, n_src, g->srcmask, g->rowsrc, d_err, s);
-  ++ctx->launches;
+  am_status st = AM_OK;
   int h_err = 0;
-  GCK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GCK(cudaStreamSynchronize(s));
+  cudaError_t e = cudaMalloc(&g->val[0], cells * 2);
+  if (!e) e = cudaMalloc(&g->val[1], cells * 2);
+  if (!e) e = cudaMalloc(&g->srcmask, cells);
+  if (!e) e = cudaMalloc(&g->rowsrc, g->g.rows);
+  if (!e) e = cudaMalloc(&g->occ, dense);
+  if (!e) e = cudaMalloc(&g->srcmask_dense, dense);
+  if (!e) e = cudaMalloc(&g->d_flags, kFlagSlots * sizeof(uint32_t));
+  if (!e) e = cudaHostAlloc(&g->h_flags, kFlagSlots * sizeof(uint32_t), cudaHostAllocDefault);
+  for (int i = 0; !e && i < kFlagSlots; ++i) e = cudaEventCreateWithFlags(&g->flag_ev[i], cudaEventDisableTiming);
+  if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
+  if (!e) e = cudaMemsetAsync(g->val[1], 0, cells * 2, s);
+  if (!e) e = cudaMemsetAsync(g->srcmask, 0, cells, s);
+  if (!e) e = cudaMemsetAsync(g->rowsrc, 0, g->g.rows, s);
+  if (!e) e = cudaMemsetAsync(g->srcmask_dense, 0, dense, s);
+  if (!e)
+    e = cudaMemcpyAsync(g->occ, occ_full + (size_t)row0 * W, dense,
+                        device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaMalloc(&d_src, n_src * 2 * sizeof(uint32_t));
+  if (!e) e = cudaMalloc(&d_err, sizeof(int));
+  if (!e) e = cudaMemsetAsync(d_err, 0, sizeof(int), s);
+  if (!e)
+    e = cudaMemcpyAsync(d_src, src, n_src * 2 * sizeof(uint32_t),
+                        device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+  if (!e) {
+    launch_srcmask_rows(g->g, H_total, row0, d_src, n_src, g->srcmask_dense, g->occ, g->srcmask, g->rowsrc, d_err,
+                        s);
+    ++ctx->launches;
+    e = cudaPeekAtLastError();
+  }
+  if (!e) e = cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
   cudaFree(d_src);
   cudaFree(d_err);
-  if (h_err) {
-    grid_free(g);
-    return fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle (grid.hpp:78)");
+  if (e) {
+    (void)cudaGetLastError();
+    st = fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "grid create: %s", cudaGetErrorString(e));
+  } else if (h_err) {
+    st = fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle (grid.hpp:78)");
   }
-#undef GCK
+  if (st) {
+    grid_free(g);
+    return st;
+  }
   *out = g;
   return AM_OK;
 }
 
+}  // namespace am
+
+extern "C" {
+
 am_status am_grid_create(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t* occ, const uint32_t* src,
                          uint64_t n_src, am_grid** out) {
-  return grid_create_impl(ctx, W, H, occ, src, n_src, false, out);
+  return am::grid_create_rows(ctx, W, H, 0, H, occ, src, n_src, false, false, out);
 }
 
 am_status am_grid_create_device(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t* occ, const uint32_t* src,
                                 uint64_t n_src, am_grid** out) {
-  return grid_create_impl(ctx, W, H, occ, src, n_src, true, out);
+  return am::grid_create_rows(ctx, W, H, 0, H, occ, src, n_src, true, false, out);
 }
 
 am_status am_grid_destroy(am_ctx* ctx, am_grid* g) {
@@ -280,7 +224,11 @@ am_status am_grid_get_info(const am_grid* g, am_grid_info* o) {
   return AM_OK;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------- propagate
+
+namespace am {
 
 struct PendingBlock {
   int slot;
@@ -289,8 +237,8 @@ struct PendingBlock {
   int cell_bits;
 };
 
-// Layers-before-first-layer-without-new-cells (l'), or 0 if the block still
-// added cells in its last layer.
+// First layer without new cells (l'), or 0 if the block still added cells
+// in its last layer.  m = min over covered cells of (a-1) at the block end.
 static uint32_t block_termination(const PendingBlock& b, uint32_t m) {
   const uint32_t none = b.cell_bits == 16 ? 0x7FFFu : 0x7FFFFFFFu;
   uint64_t vmin = m >= none ? 0xFFFFFFFFull : (uint64_t)m + 1;  // smallest covered activity
@@ -311,7 +259,7 @@ static am_status promote(am_ctx* ctx, am_grid* g) {
     (void)cudaGetLastError();
     return fail(ctx, AM_EOOM, "32-bit promotion: %s", cudaGetErrorString(e));
   }
-  am::launch_promote(g->g, (const uint16_t*)g->val[g->cur], (uint32_t*)n0, ctx->stream);
+  launch_promote(g->g, (const uint16_t*)g->val[g->cur], (uint32_t*)n0, ctx->stream);
   CKL();
   CK(cudaMemsetAsync(n1, 0, cells * 4, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -321,10 +269,12 @@ static am_status promote(am_ctx* ctx, am_grid* g) {
   g->val[1] = n1;
   g->cur = 0;
   g->cell_bits = 32;
+  g->dirty[0] = g->dirty[1] = 0;
   return AM_OK;
 }
 
-static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
+// (Re)allocates both fields at cell_bits and clears stale padding.
+am_status set_cell_bits(am_ctx* ctx, am_grid* g, int cell_bits) {
   const size_t cells = (size_t)g->g.rows * g->g.pitch;
   if (g->cell_bits != cell_bits) {
     cudaFree(g->val[0]);
@@ -343,8 +293,14 @@ static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
       CK(cudaMemsetAsync(g->val[i], 0, cells * (cell_bits / 8), ctx->stream));
       g->dirty[i] = 0;
     }
+  return AM_OK;
+}
+
+static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
+  am_status st = set_cell_bits(ctx, g, cell_bits);
+  if (st) return st;
   g->cur = 0;
-  am::launch_init(g->g, g->occ, g->srcmask, g->val[0], cell_bits, ctx->stream);
+  launch_init(g->g, g->occ, g->srcmask, g->val[0], cell_bits, ctx->stream);
   CKL();
   g->plain_active = 0;
   g->computed = g->layers_used = 0;
@@ -352,113 +308,140 @@ static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
   return AM_OK;
 }
 
-am_status am_propagate(am_ctx* ctx, am_grid* g, uint32_t layers, uint32_t auto_cap, uint32_t mode,
-                       am_prop_result* res) {
-  if (!ctx || !g) return AM_EINVAL;
+am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t layers, uint32_t auto_cap,
+                            uint32_t mode, am_prop_result* res) {
+  am_ctx* ctx = slabs[0].ctx;
   const bool autom = layers == 0;
   const uint32_t target = autom ? auto_cap : layers;
   if (target == 0) return fail(ctx, AM_EINVAL, "auto_cap must be >= 1");
-  if (target > am::kMaxLayers) return fail(ctx, AM_EINVAL, "layer count %u exceeds kMaxLayers", target);
+  if (target > kMaxLayers) return fail(ctx, AM_EINVAL, "layer count %u exceeds kMaxLayers", target);
   if (mode != AM_MODE_BATCHED && mode != AM_MODE_ITERATIVE) return fail(ctx, AM_EINVAL, "bad mode");
   CK(cudaSetDevice(ctx->device));
-  cudaStream_t s = ctx->stream;
   // 16-bit cells unless the run can never fit (fixed L beyond the 16-bit range)
-  const int start_bits = (!autom && (uint64_t)target + 1 > am::kMax16Activity) ? 32 : 16;
-  am_status st = reset_map(ctx, g, start_bits);
-  if (st) return st;
+  const int start_bits = (!autom && (uint64_t)target + 1 > kMax16Activity) ? 32 : 16;
+  am_status st;
+  for (auto& s : slabs)
+    if ((st = reset_map(s.ctx, s.g, start_bits))) return st;
 
   am_prop_result r{};
   const bool timing = (ctx->flags & AM_CTX_TIMING) != 0;
   size_t timer_used = 0;
   std::deque<PendingBlock> pend;
-  uint32_t l = 0;             // layers applied so far
-  uint32_t lprime = 0;        // first layer without new cells (0 = not found)
+  uint32_t l = 0;       // layers applied so far
+  uint32_t lprime = 0;  // first layer without new cells (0 = not found)
   uint64_t nblock = 0;
-  const int K = am::kK;
+  const int K = kK;
+  std::vector<uint32_t*> words(slabs.size());
 
   auto drain_one = [&]() -> am_status {
     PendingBlock b = pend.front();
     pend.pop_front();
-    CK(cudaEventSynchronize(g->flag_ev[b.slot]));
+    uint32_t m = 0xFFFFFFFFu;
+    for (auto& s : slabs) {
+      am_ctx* c = s.ctx;
+      cudaError_t e = cudaEventSynchronize(s.g->flag_ev[b.slot]);
+      if (e) return fail(c, AM_ECUDA, "flag event: %s", cudaGetErrorString(e));
+      m = std::min(m, s.g->h_flags[b.slot]);
+    }
     if (!lprime) {
-      uint32_t t = block_termination(b, g->h_flags[b.slot]);
+      const uint32_t t = block_termination(b, m);
       if (t) lprime = t;
     }
     return AM_OK;
   };
 
   while (l < target && !lprime) {
-    uint32_t kk;
-    bool blocked;
-    if (mode == AM_MODE_BATCHED && target - l >= (uint32_t)K) {
-      kk = K;
-      blocked = true;
-    } else {
-      kk = 1;
-      blocked = false;
-    }
-    if (g->cell_bits == 16 && (uint64_t)l + kk + 1 > am::kMax16Activity) {
-      while (!pend.empty() && !lprime) {
-        st = drain_one();
-        if (st) return st;
-      }
+    const bool blocked = mode == AM_MODE_BATCHED && target - l >= (uint32_t)K;
+    const uint32_t kk = blocked ? (uint32_t)K : 1u;
+    if (slabs[0].g->cell_bits == 16 && (uint64_t)l + kk + 1 > kMax16Activity) {
+      while (!pend.empty() && !lprime)
+        if ((st = drain_one())) return st;
       pend.clear();
       if (lprime) break;
-      st = promote(ctx, g);
-      if (st) return st;
+      for (auto& s : slabs)
+        if ((st = promote(s.ctx, s.g))) return st;
     }
+    if (tr && (st = tr->exchange())) return st;
     const int slot = (int)(nblock % kFlagSlots);
-    uint32_t* flag = g->d_flags + slot;
-    if (autom) CK(cudaMemsetAsync(flag, 0xFF, sizeof(uint32_t), s));
-    void* in = g->val[g->cur];
-    void* outp = g->val[g->cur ^ 1];
-    if (blocked) {
-      if (timing) {
-        if (timer_used == ctx->timers.size()) {
-          Timer t;
-          CK(cudaEventCreate(&t.a));
-          CK(cudaEventCreate(&t.b));
-          ctx->timers.push_back(t);
-        }
-        CK(cudaEventRecord(ctx->timers[timer_used].a, s));
+    for (size_t i = 0; i < slabs.size(); ++i) {
+      am_ctx* c = slabs[i].ctx;
+      am_grid* g = slabs[i].g;
+      uint32_t* flag = g->d_flags + slot;
+      words[i] = flag;
+      cudaStream_t s = c->stream;
+      if (autom) {
+        cudaError_t e = cudaMemsetAsync(flag, 0xFF, sizeof(uint32_t), s);
+        if (e) return fail(c, AM_ECUDA, "memset: %s", cudaGetErrorString(e));
       }
-      am::launch_block(g->g, g->cell_bits, in, outp, g->srcmask, g->rowsrc, flag, s);
-      CKL();
-      if (timing) CK(cudaEventRecord(ctx->timers[timer_used++].b, s));
-      ++r.block_launches;
-    } else {
-      am::launch_layer(g->g, g->cell_bits, in, outp, g->srcmask, flag, s);
-      CKL();
-      ++r.layer_launches;
+      void* in = g->val[g->cur];
+      void* outp = g->val[g->cur ^ 1];
+      if (blocked) {
+        if (timing) {
+          if (timer_used == ctx->timers.size()) {
+            am_ctx::Timer t;
+            CK(cudaEventCreate(&t.a));
+            CK(cudaEventCreate(&t.b));
+            ctx->timers.push_back(t);
+          }
+          CK(cudaEventRecord(ctx->timers[timer_used].a, s));
+        }
+        launch_block(g->g, g->cell_bits, in, outp, g->srcmask, g->rowsrc, flag, s);
+        ++c->launches;
+        if (cudaError_t e = cudaPeekAtLastError()) return fail(c, AM_ECUDA, "k_block: %s", cudaGetErrorString(e));
+        if (timing) CK(cudaEventRecord(ctx->timers[timer_used++].b, s));
+        ++r.block_launches;
+      } else {
+        launch_layer(g->g, g->cell_bits, in, outp, g->srcmask, flag, s);
+        ++c->launches;
+        if (cudaError_t e = cudaPeekAtLastError()) return fail(c, AM_ECUDA, "k_layer: %s", cudaGetErrorString(e));
+        ++r.layer_launches;
+      }
+      g->cur ^= 1;
     }
-    g->cur ^= 1;
     if (autom) {
-      CK(cudaMemcpyAsync(g->h_flags + slot, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-      CK(cudaEventRecord(g->flag_ev[slot], s));
-      pend.push_back(PendingBlock{slot, l, kk, g->cell_bits});
+      if (tr && (st = tr->reduce(words, false))) return st;
+      for (auto& sr : slabs) {
+        am_ctx* c = sr.ctx;
+        cudaError_t e = cudaMemcpyAsync(sr.g->h_flags + slot, sr.g->d_flags + slot, sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, c->stream);
+        if (!e) e = cudaEventRecord(sr.g->flag_ev[slot], c->stream);
+        if (e) return fail(c, AM_ECUDA, "flag copy: %s", cudaGetErrorString(e));
+      }
+      pend.push_back(PendingBlock{slot, l, kk, slabs[0].g->cell_bits});
     }
     l += kk;
     ++nblock;
-    if (mode == AM_MODE_ITERATIVE) CK(cudaStreamSynchronize(s));  // per-layer call boundary
-    while ((int)pend.size() > kLag) {
-      st = drain_one();
-      if (st) return st;
-    }
+    if (mode == AM_MODE_ITERATIVE)  // per-layer call boundary
+      for (auto& sr : slabs) {
+        am_ctx* c = sr.ctx;
+        CK(cudaStreamSynchronize(c->stream));
+      }
+    while ((int)pend.size() > kLag)
+      if ((st = drain_one())) return st;
   }
-  while (!pend.empty()) {
-    st = drain_one();
-    if (st) return st;
-  }
-  g->computed = l;
+  while (!pend.empty())
+    if ((st = drain_one())) return st;
   uint32_t used = l, cause = AM_STOP_FIXED;
   if (autom) {
-    uint32_t* zflag = g->d_flags + (int)(nblock % kFlagSlots);
-    CK(cudaMemsetAsync(zflag, 0, sizeof(uint32_t), s));
-    am::launch_zero_check(g->g, g->cell_bits, g->val[g->cur], zflag, s);
-    CKL();
+    const int zslot = (int)(nblock % kFlagSlots);
+    for (size_t i = 0; i < slabs.size(); ++i) {
+      am_ctx* c = slabs[i].ctx;
+      am_grid* g = slabs[i].g;
+      uint32_t* z = g->d_flags + zslot;
+      words[i] = z;
+      CK(cudaMemsetAsync(z, 0, sizeof(uint32_t), c->stream));
+      launch_zero_check(g->g, g->cell_bits, g->val[g->cur], z, c->stream);
+      CKL();
+    }
+    if (tr && (st = tr->reduce(words, true))) return st;
     uint32_t any_zero = 0;
-    CK(cudaMemcpyAsync(&any_zero, zflag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    for (auto& sr : slabs) {
+      am_ctx* c = sr.ctx;
+      uint32_t v = 0;
+      CK(cudaMemcpyAsync(&v, sr.g->d_flags + zslot, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      any_zero |= v;
+    }
     if (lprime) {
       if (!any_zero) {
         used = lprime > 1 ? lprime - 1 : 1;
@@ -472,11 +455,17 @@ am_status am_propagate(am_ctx* ctx, am_grid* g, uint32_t layers, uint32_t auto_c
       cause = any_zero ? AM_STOP_CAP : AM_STOP_FILLED;
     }
   } else {
-    if (mode == AM_MODE_BATCHED) CK(cudaStreamSynchronize(s));
+    for (auto& sr : slabs) {
+      am_ctx* c = sr.ctx;
+      CK(cudaStreamSynchronize(c->stream));
+    }
   }
-  g->layers_used = used;
+  for (auto& sr : slabs) {
+    sr.g->computed = l;
+    sr.g->layers_used = used;
+  }
   if (timing) {
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(ctx->stream));
     double ms = 0;
     for (size_t i = 0; i < timer_used; ++i) {
       float f = 0;
@@ -488,14 +477,37 @@ am_status am_propagate(am_ctx* ctx, am_grid* g, uint32_t layers, uint32_t auto_c
   r.layers_used = used;
   r.cause = cause;
   r.layers_computed = l;
-  r.cell_bits = g->cell_bits;
+  r.cell_bits = slabs[0].g->cell_bits;
   if (res) *res = r;
   return AM_OK;
 }
 
+}  // namespace am
+
+extern "C" {
+
+am_status am_propagate(am_ctx* ctx, am_grid* g, uint32_t layers, uint32_t auto_cap, uint32_t mode,
+                       am_prop_result* res) {
+  if (!ctx || !g) return AM_EINVAL;
+  std::vector<am::SlabRef> one{{ctx, g}};
+  am::Transport* tr = nullptr;
+  if (g->slab) {
+    if (!ctx->comm) return am::fail(ctx, AM_EINVAL, "slab grid: call am_comm_init or use am_slabs_propagate");
+    tr = am::make_nccl_transport(ctx, g);
+    if (!tr) return am::fail(ctx, AM_ENCCL, "cannot build the NCCL halo transport");
+  }
+  am_status st = am::drive_propagation(one, tr, layers, auto_cap, mode, res);
+  delete tr;
+  return st;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- download
+
 static am_status download_impl(am_ctx* ctx, am_grid* g, uint32_t* dst, bool dst_device) {
   if (!ctx || !g || !dst) return AM_EINVAL;
-  if (!g->have_map) return fail(ctx, AM_EINVAL, "no activity map: call am_propagate first");
+  if (!g->have_map) return am::fail(ctx, AM_EINVAL, "no activity map: call am_propagate first");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   const size_t W = g->g.W, H = g->g.H;
@@ -530,9 +542,9 @@ static am_status download_impl(am_ctx* ctx, am_grid* g, uint32_t* dst, bool dst_
   return AM_OK;
 }
 
-am_status am_activity_download(am_ctx* ctx, am_grid* g, uint32_t* dense) {
-  return download_impl(ctx, g, dense, false);
-}
+extern "C" {
+
+am_status am_activity_download(am_ctx* ctx, am_grid* g, uint32_t* dense) { return download_impl(ctx, g, dense, false); }
 
 am_status am_activity_download_device(am_ctx* ctx, am_grid* g, uint32_t* dense) {
   return download_impl(ctx, g, dense, true);
@@ -540,6 +552,7 @@ am_status am_activity_download_device(am_ctx* ctx, am_grid* g, uint32_t* dense) 
 
 am_status am_activity_upload(am_ctx* ctx, am_grid* g, const uint32_t* dense, uint32_t layers_applied) {
   if (!ctx || !g || !dense) return AM_EINVAL;
+  if (g->slab) return am::fail(ctx, AM_EINVAL, "activity upload on a slab grid");
   CK(cudaSetDevice(ctx->device));
   const size_t n = (size_t)g->g.W * g->g.H;
   if (!g->plain) CK(cudaMalloc(&g->plain, n * 4));
@@ -550,6 +563,8 @@ am_status am_activity_upload(am_ctx* ctx, am_grid* g, const uint32_t* dense, uin
   g->have_map = 1;
   return AM_OK;
 }
+
+}  // extern "C"
 
 // ------------------------------------------------------------------ paths
 
@@ -590,28 +605,6 @@ static am_status ensure_targets(am_ctx* ctx, am_grid* g, uint64_t n) {
   return AM_OK;
 }
 
-am_status am_path_counts(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
-                         uint64_t* offsets, int32_t* status) {
-  if (!ctx || !g || (n && (!tgt || !status)) || !offsets) return AM_EINVAL;
-  if (!g->have_map) return fail(ctx, AM_EINVAL, "no activity map");
-  if (method > 1) return fail(ctx, AM_EINVAL, "bad method");
-  CK(cudaSetDevice(ctx->device));
-  offsets[0] = 0;
-  if (!n) return AM_OK;
-  am_status st = ensure_targets(ctx, g, n);
-  if (st) return st;
-  cudaStream_t s = ctx->stream;
-  CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
-  am::launch_path_counts(view_of(g), g->d_tgt, n, (int)method, seed, g->d_counts, g->d_status, s);
-  CKL();
-  am::launch_scan(g->d_counts, n, g->d_offsets, s);
-  CKL();
-  CK(cudaMemcpyAsync(offsets, g->d_offsets, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(status, g->d_status, n * 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  return AM_OK;
-}
-
 // Host straighten (reconstruct.hpp:54-58, pin P4, strict rule) -- only needed
 // for caller-uploaded maps; see the header.
 static uint64_t straighten_strict(uint32_t* p, uint64_t n, const std::vector<uint8_t>& occ, uint32_t W) {
@@ -634,15 +627,42 @@ static uint64_t straighten_strict(uint32_t* p, uint64_t n, const std::vector<uin
   return m;
 }
 
+extern "C" {
+
+am_status am_path_counts(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
+                         uint64_t* offsets, int32_t* status) {
+  if (!ctx || !g || (n && (!tgt || !status)) || !offsets) return AM_EINVAL;
+  if (!g->have_map) return am::fail(ctx, AM_EINVAL, "no activity map");
+  if (g->slab) return am::fail(ctx, AM_EINVAL, "path extraction on a slab: gather the map first");
+  if (method > 1) return am::fail(ctx, AM_EINVAL, "bad method");
+  CK(cudaSetDevice(ctx->device));
+  offsets[0] = 0;
+  if (!n) return AM_OK;
+  am_status st = ensure_targets(ctx, g, n);
+  if (st) return st;
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
+  am::launch_path_counts(view_of(g), g->d_tgt, n, (int)method, seed, g->d_counts, g->d_status, s);
+  CKL();
+  am::launch_scan(g->d_counts, n, g->d_offsets, s);
+  CKL();
+  CK(cudaMemcpyAsync(offsets, g->d_offsets, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(status, g->d_status, n * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return AM_OK;
+}
+
 am_status am_trace_paths(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
                          const uint64_t* offsets, uint32_t* pts, uint64_t cap, int32_t* status) {
   if (!ctx || !g || !offsets || (n && (!tgt || !status))) return AM_EINVAL;
-  if (!g->have_map) return fail(ctx, AM_EINVAL, "no activity map");
-  if (method > 1) return fail(ctx, AM_EINVAL, "bad method");
+  if (!g->have_map) return am::fail(ctx, AM_EINVAL, "no activity map");
+  if (g->slab) return am::fail(ctx, AM_EINVAL, "path extraction on a slab: gather the map first");
+  if (method > 1) return am::fail(ctx, AM_EINVAL, "bad method");
   if (!n) return AM_OK;
   const uint64_t total = offsets[n];
-  if (total > cap || (total && !pts)) return fail(ctx, AM_EINVAL, "point buffer too small (%llu < %llu)",
-                                                  (unsigned long long)cap, (unsigned long long)total);
+  if (total > cap || (total && !pts))
+    return am::fail(ctx, AM_EINVAL, "point buffer too small (%llu < %llu)", (unsigned long long)cap,
+                    (unsigned long long)total);
   CK(cudaSetDevice(ctx->device));
   am_status st = ensure_targets(ctx, g, n);
   if (st) return st;
@@ -680,9 +700,10 @@ am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, 
                                 uint64_t seed, uint64_t* d_offsets, uint32_t* d_pts, uint64_t cap,
                                 int32_t* d_status) {
   if (!ctx || !g || !d_offsets || (n && (!d_tgt || !d_status))) return AM_EINVAL;
-  if (!g->have_map) return fail(ctx, AM_EINVAL, "no activity map");
-  if (g->plain_active) return fail(ctx, AM_EINVAL, "device path tracing needs a propagated map");
-  if (method > 1) return fail(ctx, AM_EINVAL, "bad method");
+  if (!g->have_map) return am::fail(ctx, AM_EINVAL, "no activity map");
+  if (g->plain_active) return am::fail(ctx, AM_EINVAL, "device path tracing needs a propagated map");
+  if (g->slab) return am::fail(ctx, AM_EINVAL, "path extraction on a slab: gather the map first");
+  if (method > 1) return am::fail(ctx, AM_EINVAL, "bad method");
   (void)cap;
   if (!n) return AM_OK;
   CK(cudaSetDevice(ctx->device));
@@ -704,8 +725,8 @@ am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, 
 am_status am_propagate_layer(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t* occ, const uint32_t* src,
                              uint64_t n_src, const uint32_t* in, uint32_t* out) {
   if (!ctx || !occ || !in || !out || (n_src && !src)) return AM_EINVAL;
-  if (!dims_ok(W, H)) return fail(ctx, AM_EINVAL, "grid dimensions %ux%u outside 1..65535", W, H);
-  if (!n_src) return fail(ctx, AM_EINVAL, "SourceSet must be nonempty");
+  if (!am::dims_ok(W, H)) return am::fail(ctx, AM_EINVAL, "grid dimensions %ux%u outside 1..65535", W, H);
+  if (!n_src) return am::fail(ctx, AM_EINVAL, "SourceSet must be nonempty");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   const size_t n = (size_t)W * H;
@@ -733,8 +754,8 @@ am_status am_propagate_layer(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t*
   }
   if (!e) e = cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);
-  if (e) st = fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s", cudaGetErrorString(e));
-  else if (h_err) st = fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle");
+  if (e) st = am::fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s", cudaGetErrorString(e));
+  else if (h_err) st = am::fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle");
   (void)cudaGetLastError();
   cudaFree(d_occ);
   cudaFree(d_sm);
@@ -748,9 +769,9 @@ am_status am_propagate_layer(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t*
 am_status am_propagate_reference(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t* occ, const uint32_t* src,
                                  uint64_t n_src, uint32_t layers, uint32_t* out) {
   if (!ctx || !occ || !out || (n_src && !src)) return AM_EINVAL;
-  if (!dims_ok(W, H)) return fail(ctx, AM_EINVAL, "grid dimensions %ux%u outside 1..65535", W, H);
-  if (!n_src) return fail(ctx, AM_EINVAL, "SourceSet must be nonempty");
-  if (layers == 0 || layers > am::kMaxLayers) return fail(ctx, AM_EINVAL, "layer count %u out of range", layers);
+  if (!am::dims_ok(W, H)) return am::fail(ctx, AM_EINVAL, "grid dimensions %ux%u outside 1..65535", W, H);
+  if (!n_src) return am::fail(ctx, AM_EINVAL, "SourceSet must be nonempty");
+  if (layers == 0 || layers > am::kMaxLayers) return am::fail(ctx, AM_EINVAL, "layer count %u out of range", layers);
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   const size_t n = (size_t)W * H;
@@ -790,8 +811,8 @@ am_status am_propagate_reference(am_ctx* ctx, uint32_t W, uint32_t H, const uint
   }
   if (!e) e = cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);
-  if (e) st = fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s", cudaGetErrorString(e));
-  else if (h_err) st = fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle");
+  if (e) st = am::fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s", cudaGetErrorString(e));
+  else if (h_err) st = am::fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle");
   (void)cudaGetLastError();
   cudaFree(d_occ);
   cudaFree(d_sm);

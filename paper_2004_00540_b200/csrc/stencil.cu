@@ -71,18 +71,33 @@ struct Cell<32> {
 };
 
 // ------------------------------------------------------------- init / misc
-__global__ void k_scatter_sources(Geo g, const uint32_t* __restrict__ rc, uint64_t n,
-                                  uint8_t* __restrict__ srcmask, uint8_t* __restrict__ rowsrc,
-                                  int* __restrict__ err) {
-  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+// SourceSet rasterisation for the grid rows [row0, row0+H) of a total_h-row
+// grid (grid.hpp:78-90): validates every source, marks owned sources in the
+// dense mask, and marks owned + halo-band sources in the pitched mask and
+// the per-row flags (a slab recomputes its halo rows inside a block).
+__global__ void k_srcmask_rows(Geo g, uint32_t total_h, uint32_t row0, const uint32_t* __restrict__ rc, uint64_t n,
+                               uint8_t* __restrict__ dense, const uint8_t* __restrict__ occ,
+                               uint8_t* __restrict__ srcmask, uint8_t* __restrict__ rowsrc, int* __restrict__ err) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint32_t r = rc[2 * i], c = rc[2 * i + 1];
-  if (r >= g.H || c >= g.W) {
+  const uint32_t r = rc[2 * i], c = rc[2 * i + 1];
+  if (r >= total_h || c >= g.W) {
     atomicOr(err, 1);
     return;
   }
-  srcmask[g.idx(r, c)] = 1;
-  rowsrc[r + g.pad] = 1;
+  const long local = (long)r - (long)row0;
+  if (local >= 0 && local < (long)g.H) {
+    if (occ[(size_t)local * g.W + c]) {
+      atomicOr(err, 1);
+      return;
+    }
+    dense[(size_t)local * g.W + c] = 1;
+  }
+  const long arow = local + g.pad;
+  if (arow >= 0 && arow < (long)g.rows) {
+    srcmask[(size_t)arow * g.pitch + c + g.pad] = 1;
+    rowsrc[arow] = 1;
+  }
 }
 
 // layer-0 field (activity.hpp:20-21): free = flag|[source], obstacle = 0.
@@ -118,15 +133,20 @@ struct Rows<16> {
       x[2 * i + 1] = __byte_perm(A[i], B[i], 0x7632);
     }
   }
-  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint16_t* pa, uint16_t* pb) {
+  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint16_t* pa, uint16_t* pb, bool wa,
+                                               bool wb) {
     uint32_t A[4], B[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       A[i] = __byte_perm(x[2 * i], x[2 * i + 1], 0x5410);
       B[i] = __byte_perm(x[2 * i], x[2 * i + 1], 0x7632);
     }
-    *reinterpret_cast<uint4*>(pa) = make_uint4(A[0], A[1], A[2], A[3]);
-    *reinterpret_cast<uint4*>(pb) = make_uint4(B[0], B[1], B[2], B[3]);
+    if (wa) *reinterpret_cast<uint4*>(pa) = make_uint4(A[0], A[1], A[2], A[3]);
+    if (wb) *reinterpret_cast<uint4*>(pb) = make_uint4(B[0], B[1], B[2], B[3]);
+  }
+  // words restricted to the valid tiles (an invalid half becomes 0 = unflagged)
+  __device__ __forceinline__ static uint32_t valid_bits(bool wa, bool wb) {
+    return (wa ? 0x0000FFFFu : 0u) | (wb ? 0xFFFF0000u : 0u);
   }
   __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t* sb, uint32_t (&s)[kWPL]) {
     const uint2 A = *reinterpret_cast<const uint2*>(sa);
@@ -151,10 +171,12 @@ struct Rows<32> {
     x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
     x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
   }
-  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint32_t* pa, uint32_t*) {
+  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint32_t* pa, uint32_t*, bool wa, bool) {
+    if (!wa) return;
     reinterpret_cast<uint4*>(pa)[0] = make_uint4(x[0], x[1], x[2], x[3]);
     reinterpret_cast<uint4*>(pa)[1] = make_uint4(x[4], x[5], x[6], x[7]);
   }
+  __device__ __forceinline__ static uint32_t valid_bits(bool wa, bool) { return wa ? 0xFFFFFFFFu : 0u; }
   __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t*, uint32_t (&s)[kWPL]) {
     const uint2 A = *reinterpret_cast<const uint2*>(sa);
     const uint32_t a4[2] = {A.x, A.y};
@@ -352,9 +374,18 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
         else stream_step<CB, 1, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
       }
       if (tt >= 2 * kK && tt < 2 * kK + g.seg_len && store_lane) {
-        Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch);
+        // rows past the grid (last segment; slab halo rows) are neither stored nor counted
+        const uint32_t orow = tt - 2 * kK;
+        const bool wa = rA + orow < g.H, wb = rB + orow < g.H;
+        Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
+        if (wa && wb) {
 #pragma unroll
-        for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
+          for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
+        } else {
+          const uint32_t keep = Rows<CB>::valid_bits(wa, wb);
+#pragma unroll
+          for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w] & keep, acc);
+        }
       }
     }
   }
@@ -497,10 +528,12 @@ __global__ void k_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* __restri
 // ------------------------------------------------------------- launchers
 static dim3 grid2d(uint32_t W, uint32_t H, int bx) { return dim3((W + bx - 1) / bx, H); }
 
-void launch_scatter_sources(const Geo& g, const uint32_t* d_src_rc, uint64_t n, uint8_t* d_srcmask,
-                            uint8_t* d_rowsrc, int* d_err, cudaStream_t s) {
+void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const uint32_t* d_src_rc, uint64_t n,
+                         uint8_t* d_dense, const uint8_t* d_occ, uint8_t* d_srcmask, uint8_t* d_rowsrc, int* d_err,
+                         cudaStream_t s) {
   if (!n) return;
-  k_scatter_sources<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, d_src_rc, n, d_srcmask, d_rowsrc, d_err);
+  k_srcmask_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, total_h, row0, d_src_rc, n, d_dense, d_occ,
+                                                             d_srcmask, d_rowsrc, d_err);
 }
 
 void launch_init(const Geo& g, const uint8_t* d_occ, const uint8_t* d_srcmask, void* d_val, int cb,

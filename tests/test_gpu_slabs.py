@@ -1,0 +1,73 @@
+"""Row-slab decomposition on the device vs the oracle.
+
+One GPU, n in-process slabs (the same halo-exchange / flag-reduction driver
+the NCCL path uses; only the transport differs): the assembled map,
+layers_used / cause and the paths traced on the gathered map must be
+identical to the single-grid oracle results."""
+import numpy as np
+import pytest
+
+from tests.oracle_adapter import O
+
+am = pytest.importorskip("paper_2004_00540_b200")
+pytestmark = pytest.mark.gpu
+
+
+def split(h, n):
+    return [(h * r // n, h * (r + 1) // n) for r in range(n)]
+
+
+def make_slabs(occ, src, n, ctx):
+    return [am.Grid.slab(occ, src, a, b, ctx) for a, b in split(occ.shape[0], n)]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7])
+def test_slabs_auto_match_oracle(n):
+    ctx = am.default_context()
+    for seed, (w, h), dens, ns in [(1, (300, 200), 0.3, 3), (2, (517, 611), 0.4, 5), (3, (64, 129), 0.0, 1),
+                                   (4, (1000, 333), 0.55, 4)]:
+        occ = O.random_maze(w, h, dens, seed)
+        src = O.sample_free_cells(occ, ns, seed)
+        sm = O.source_mask(occ, src)
+        slabs = make_slabs(occ, src, n, ctx)
+        for cap in (3, 9, 4 * max(w, h)):
+            r = am.slabs_propagate(slabs, auto_cap=cap)
+            ref, rl, rc = O.propagate_auto(occ, sm, cap, threads=8)
+            assert (r.layers_used, r.cause) == (rl, rc), (n, seed, cap)
+            got = np.concatenate([s.activity() for s in slabs])
+            assert np.array_equal(got, ref), (n, seed, cap)
+        for L in (1, 8, 17):
+            am.slabs_propagate(slabs, layers=L)
+            got = np.concatenate([s.activity() for s in slabs])
+            assert np.array_equal(got, O.propagate(occ, sm, L)), (n, seed, L)
+        for s in slabs:
+            s.close()
+
+
+def test_slabs_gather_then_trace():
+    ctx = am.default_context()
+    occ = O.random_maze(800, 600, 0.35, 11)
+    src = O.sample_free_cells(occ, 6, 11)
+    sm = O.source_mask(occ, src)
+    slabs = make_slabs(occ, src, 4, ctx)
+    r = am.slabs_propagate(slabs, auto_cap=3200)
+    full = am.Grid(occ, src, ctx)
+    am.slabs_gather(slabs, full)
+    ref, rl, _ = O.propagate_auto(occ, sm, 3200, threads=8)
+    assert r.layers_used == rl and np.array_equal(full.activity(), ref)
+    tg = O.sample_free_cells(occ, 100, 12, exclude=sm)
+    for (st, pts), t in zip(full.paths(tg, am.EUCLIDEAN), tg):
+        ost, opts = O.reconstruct_euclidean(occ, sm, ref, t)
+        assert st == ost and (st != 0 or np.array_equal(pts, opts))
+    for s in slabs:
+        s.close()
+    full.close()
+
+
+def test_slab_validation():
+    ctx = am.default_context()
+    occ = np.zeros((40, 50), np.uint8)
+    with pytest.raises(am.InvalidInputError):
+        am.Grid.slab(occ, [[0, 0]], 0, 4, ctx)  # fewer rows than the halo depth
+    with pytest.raises(am.InvalidInputError):
+        am.Grid.slab(occ, [[0, 0]], 10, 50, ctx)
