@@ -61,7 +61,7 @@ void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcm
 void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const uint32_t* d_src_rc, uint64_t n,
                          uint8_t* d_dense, const uint8_t* d_occ, uint8_t* d_srcmask, uint8_t* d_rowsrc, int* d_err,
                          cudaStream_t s);
-void launch_block(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
+void launch_block(const Geo& g, int cell_bits, bool slab, const void* in, void* out, const uint8_t* srcmask,
                   const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s);
 void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
                   uint32_t* flag, cudaStream_t s);

@@ -385,7 +385,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
           }
           CK(cudaEventRecord(ctx->timers[timer_used].a, s));
         }
-        launch_block(g->g, g->cell_bits, in, outp, g->srcmask, g->rowsrc, flag, s);
+        launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, flag, s);
         ++c->launches;
         if (cudaError_t e = cudaPeekAtLastError()) return fail(c, AM_ECUDA, "k_block: %s", cudaGetErrorString(e));
         if (timing) CK(cudaEventRecord(ctx->timers[timer_used++].b, s));

@@ -285,7 +285,11 @@ __device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint
 #ifndef AM_BLOCK_MINB
 #define AM_BLOCK_MINB 3  // CTAs per SM the register budget is sized for (12 warps, <= 170 regs)
 #endif
-template <int CB>
+// SLAB=false: rows past the grid are padding (unflagged centres compute to
+// unflagged values), so they may be stored and folded into the flag
+// unchanged.  SLAB=true: the rows below the slab are a neighbour's halo
+// (flagged data) and must be neither stored nor counted.
+template <int CB, bool SLAB>
 __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
                                                          typename Cell<CB>::T* __restrict__ out,
                                                          const uint8_t* __restrict__ srcmask,
@@ -374,14 +378,14 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
         else stream_step<CB, 1, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
       }
       if (tt >= 2 * kK && tt < 2 * kK + g.seg_len && store_lane) {
-        // rows past the grid (last segment; slab halo rows) are neither stored nor counted
-        const uint32_t orow = tt - 2 * kK;
-        const bool wa = rA + orow < g.H, wb = rB + orow < g.H;
-        Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
-        if (wa && wb) {
+        if constexpr (!SLAB) {
+          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, true);
 #pragma unroll
           for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
         } else {
+          const uint32_t orow = tt - 2 * kK;
+          const bool wa = rA + orow < g.H, wb = rB + orow < g.H;
+          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
           const uint32_t keep = Rows<CB>::valid_bits(wa, wb);
 #pragma unroll
           for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w] & keep, acc);
@@ -544,23 +548,29 @@ void launch_init(const Geo& g, const uint8_t* d_occ, const uint8_t* d_srcmask, v
     k_init<32><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, d_occ, d_srcmask, (uint32_t*)d_val);
 }
 
-void launch_block(const Geo& g, int cb, const void* in, void* out, const uint8_t* srcmask, const uint8_t* rowsrc,
-                  uint32_t* flag, cudaStream_t s) {
+void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, const uint8_t* srcmask,
+                  const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s) {
   const uint32_t ntiles = cb == 16 ? g.nseg / 2 : g.nseg;
   const uint32_t warps = g.nbands * ntiles;
   const uint32_t blocks = (warps + kBlockThreads / 32 - 1) / (kBlockThreads / 32);
-  if (cb == 16)
-    k_block<16><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, rowsrc, flag);
+  const auto* i16 = (const uint16_t*)in;
+  const auto* i32 = (const uint32_t*)in;
+  if (cb == 16 && !slab)
+    k_block<16, false><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i16, (uint16_t*)out, srcmask, rowsrc, flag);
+  else if (cb == 16)
+    k_block<16, true><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i16, (uint16_t*)out, srcmask, rowsrc, flag);
+  else if (!slab)
+    k_block<32, false><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
   else
-    k_block<32><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, rowsrc, flag);
+    k_block<32, true><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
 }
 
 int block_kernel_blocks_per_sm(int cb) {
   int n = 0;
   if (cb == 16)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<16>, kBlockThreads, kBlockSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<16, false>, kBlockThreads, kBlockSmem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<32>, kBlockThreads, kBlockSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_block<32, false>, kBlockThreads, kBlockSmem);
   return n;
 }
 
