@@ -159,6 +159,26 @@ am_status am_comm_init(am_ctx *ctx, uint32_t nranks, uint32_t rank, const uint8_
 am_status am_comm_slab_rows(const am_ctx *ctx, uint32_t height, uint32_t *row0, uint32_t *row1);
 am_status am_comm_gather(am_ctx *ctx, am_grid *slab, am_grid *full);
 
+/* ---- small-grid batch (BASELINE.json config 5) ---------------------------
+ * n independent width x height mazes solved in one device run: the
+ * reference's propagate / propagate_auto / reconstruct_* applied to every
+ * maze, results per maze.  occupancy: n*height*width bytes (maze-major);
+ * sources of maze i: src_rc[2*src_off[i] .. 2*src_off[i+1]) (maze-local
+ * (row, col)); targets: (maze, row, col) triples; path points come back in
+ * maze-local coordinates. */
+typedef struct am_batch am_batch;
+am_status am_batch_create(am_ctx *ctx, uint32_t n_mazes, uint32_t width, uint32_t height, const uint8_t *occupancy,
+                          const uint64_t *src_off, const uint32_t *src_rc, am_batch **out);
+am_status am_batch_destroy(am_ctx *ctx, am_batch *batch);
+am_status am_batch_propagate(am_ctx *ctx, am_batch *batch, uint32_t layers, uint32_t auto_cap,
+                             uint32_t *layers_used /* n */, uint32_t *cause /* n */, am_prop_result *global);
+am_status am_batch_download(am_ctx *ctx, am_batch *batch, uint32_t *maps /* n*height*width */);
+am_status am_batch_path_counts(am_ctx *ctx, am_batch *batch, const uint32_t *tgt_mrc, uint64_t n, uint32_t method,
+                               uint64_t seed, uint64_t *offsets, int32_t *status);
+am_status am_batch_trace_paths(am_ctx *ctx, am_batch *batch, const uint32_t *tgt_mrc, uint64_t n, uint32_t method,
+                               uint64_t seed, const uint64_t *offsets, uint32_t *pts_rc, uint64_t pts_capacity,
+                               int32_t *status);
+
 /* ---- host helpers of the planner API (no device work) ------------------ */
 /* random_maze / comb_maze (grid.hpp:65-76) into a caller buffer of W*H bytes. */
 am_status am_random_maze(uint32_t width, uint32_t height, double density, uint64_t seed, uint8_t *occupancy);

@@ -101,6 +101,12 @@ def lib():
             "am_comm_init": (st, [_vp, u32, u32, _vp]),
             "am_comm_slab_rows": (st, [_vp, u32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
             "am_comm_gather": (st, [_vp, _vp, _vp]),
+            "am_batch_create": (st, [_vp, u32, u32, u32, _vp, _vp, _vp, C.POINTER(_vp)]),
+            "am_batch_destroy": (st, [_vp, _vp]),
+            "am_batch_propagate": (st, [_vp, _vp, u32, u32, _vp, _vp, C.POINTER(_PropResult)]),
+            "am_batch_download": (st, [_vp, _vp, _vp]),
+            "am_batch_path_counts": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp]),
+            "am_batch_trace_paths": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
             "am_random_maze": (st, [u32, u32, C.c_double, u64, _vp]),
             "am_comb_maze": (st, [u32, u32, _vp]),
             "am_straighten": (st, [_vp, u64, _vp, u32, u32, u32, _vp, _u64p]),
@@ -351,6 +357,66 @@ class Grid:
             keep = p[:, 0] != 0xFFFFFFFF
             out.append((OK, p[keep]))
         return out
+
+
+class Batch:
+    """Many independent small mazes solved in one device run (config C5)."""
+
+    def __init__(self, occupancy, sources, ctx: Context | None = None):
+        """occupancy: (n, h, w) uint8; sources: list of (k_i, 2) arrays of maze-local (row, col)."""
+        self.ctx = ctx or default_context()
+        occ = np.ascontiguousarray(occupancy, dtype=np.uint8)
+        if occ.ndim != 3:
+            raise InvalidInputError("occupancy must be (n, height, width)")
+        self.n, self.height, self.width = occ.shape
+        if len(sources) != self.n:
+            raise InvalidInputError("one source list per maze")
+        src_off = np.zeros(self.n + 1, np.uint64)
+        src_off[1:] = np.cumsum([len(np.asarray(s).reshape(-1, 2)) for s in sources])
+        src = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint32).reshape(-1, 2) for s in sources]),
+                                   dtype=np.uint32)
+        h = C.c_void_p()
+        _check(lib().am_batch_create(self.ctx.handle, self.n, self.width, self.height, _ptr(occ), _ptr(src_off),
+                                     _ptr(src), C.byref(h)), self.ctx, "batch")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().am_batch_destroy(self.ctx.handle, self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def propagate(self, layers: int = 0, auto_cap: int = 0):
+        """layers>0: fixed L for every maze; else auto with auto_cap.  -> (layers_used[n], cause[n], PropResult)."""
+        lu = np.zeros(self.n, np.uint32)
+        cause = np.zeros(self.n, np.uint32)
+        r = _PropResult()
+        _check(lib().am_batch_propagate(self.ctx.handle, self.handle, layers, auto_cap, _ptr(lu), _ptr(cause),
+                                        C.byref(r)), self.ctx, "batch propagate")
+        return lu, cause, PropResult(r)
+
+    def activity(self) -> np.ndarray:
+        out = np.empty((self.n, self.height, self.width), np.uint32)
+        _check(lib().am_batch_download(self.ctx.handle, self.handle, _ptr(out)), self.ctx, "batch download")
+        return out
+
+    def trace(self, targets, method=EUCLIDEAN, seed=0):
+        """targets: (k, 3) (maze, row, col) -> (offsets, points (maze-local), status)."""
+        t = np.ascontiguousarray(np.asarray(targets, np.uint32).reshape(-1, 3))
+        off = np.zeros(len(t) + 1, np.uint64)
+        st = np.zeros(len(t), np.int32)
+        _check(lib().am_batch_path_counts(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
+                                          _ptr(st)), self.ctx, "batch counts")
+        total = int(off[-1])
+        pts = np.empty((max(total, 1), 2), np.uint32)
+        _check(lib().am_batch_trace_paths(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
+                                          _ptr(pts), total, _ptr(st)), self.ctx, "batch trace")
+        return off, pts[:total], st
 
 
 def comm_unique_id() -> bytes:

@@ -1,0 +1,74 @@
+"""Small-grid batch path (config C5: many independent 256x256 mazes) vs the
+oracle run maze by maze: per-maze map, layers_used, cause and paths."""
+import numpy as np
+import pytest
+
+from tests.oracle_adapter import O
+
+am = pytest.importorskip("paper_2004_00540_b200")
+pytestmark = pytest.mark.gpu
+
+
+def make_batch(n, w, h, seed0, dens=0.3, ns=1):
+    occ = np.stack([O.random_maze(w, h, dens, seed0 + i) for i in range(n)])
+    src = [O.sample_free_cells(occ[i], ns, seed0 + i) for i in range(n)]
+    return occ, src
+
+
+def check(b, occ, src, cap, sample, method_seed=((am.EUCLIDEAN, 0), (am.SIMPLE, 2))):
+    lu, cause, _ = b.propagate(auto_cap=cap)
+    maps = b.activity()
+    for i in sample:
+        sm = O.source_mask(occ[i], src[i])
+        ref, rl, rc = O.propagate_auto(occ[i], sm, cap)
+        assert (lu[i], cause[i]) == (rl, rc), (i, lu[i], cause[i], rl, rc)
+        assert np.array_equal(maps[i], ref), i
+    tg = []
+    for i in sample:
+        sm = O.source_mask(occ[i], src[i])
+        for t in O.sample_free_cells(occ[i], 8, 77 + i, exclude=sm):
+            tg.append((i, t[0], t[1]))
+    tg = np.array(tg, np.uint32)
+    for method, seed in method_seed:
+        off, pts, st = b.trace(tg, method, seed)
+        for k, (i, r, c) in enumerate(tg):
+            sm = O.source_mask(occ[i], src[i])
+            if method == am.EUCLIDEAN:
+                ost, opts = O.reconstruct_euclidean(occ[i], sm, maps[i], (r, c))
+            else:
+                ost, opts = O.reconstruct_simple(occ[i], sm, maps[i], (r, c), seed)
+            assert st[k] == ost, (i, r, c)
+            if ost == 0:
+                assert np.array_equal(pts[off[k]:off[k + 1]], opts), (i, r, c, method)
+
+
+def test_batch_small_mixed_outcomes():
+    # densities up to 0.6 give stalled mazes next to filled ones; cap 40 leaves some capped
+    occ = np.stack([O.random_maze(64, 48, d, 100 + i) for i, d in enumerate([0.0, 0.3, 0.45, 0.6] * 6)])
+    src = [O.sample_free_cells(occ[i], 1 + i % 3, 100 + i) for i in range(len(occ))]
+    b = am.Batch(occ, src)
+    for cap in (40, 1000, 1):
+        check(b, occ, src, cap, range(len(occ)))
+    lu, cause, _ = b.propagate(layers=13)
+    maps = b.activity()
+    for i in range(len(occ)):
+        assert lu[i] == 13 and np.array_equal(maps[i], O.propagate(occ[i], O.source_mask(occ[i], src[i]), 13))
+    b.close()
+
+
+def test_batch_c5_shape():
+    """4096 x 256^2 (config C5), checked on a sample of mazes."""
+    n = 4096
+    occ, src = make_batch(n, 256, 256, 5000)
+    b = am.Batch(occ, src)
+    check(b, occ, src, 1024, list(range(0, n, 257)) + [n - 1])
+    b.close()
+
+
+def test_batch_rejects_bad_input():
+    occ = np.zeros((2, 8, 8), np.uint8)
+    with pytest.raises(am.InvalidInputError):
+        am.Batch(occ, [np.zeros((0, 2), np.uint32), [[0, 0]]])
+    occ[1, 0, 0] = 1
+    with pytest.raises(am.InvalidInputError):
+        am.Batch(occ, [[[1, 1]], [[0, 0]]])
