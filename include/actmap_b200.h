@@ -47,6 +47,7 @@ typedef struct am_ctx am_ctx;
 typedef struct am_grid am_grid;
 
 #define AM_CTX_TIMING 1u /* time every stencil block launch with CUDA events */
+#define AM_CTX_DENSE 2u  /* disable exact active-tile skipping: every block sweeps the whole grid */
 
 typedef struct am_ctx_opts {
   int32_t device; /* CUDA ordinal */
@@ -61,6 +62,8 @@ typedef struct am_prop_result {
   uint64_t block_launches;  /* temporally blocked stencil launches */
   uint64_t layer_launches;  /* single-layer stencil launches */
   double stencil_ms;        /* summed CUDA-event time of the block launches (AM_CTX_TIMING) */
+  uint64_t tiles_processed; /* tile-blocks computed with active-tile skipping (0 in dense mode) */
+  uint64_t tiles_total;     /* tiles per grid x blocks: the dense-equivalent tile-blocks */
 } am_prop_result;
 
 typedef struct am_grid_info {

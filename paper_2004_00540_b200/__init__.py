@@ -25,6 +25,7 @@ BATCHED, ITERATIVE = 0, 1                          # Mode (propagate.hpp:22)
 SIMPLE, EUCLIDEAN = 0, 1                           # Method (report.hpp:15)
 STRICT, PERMISSIVE = 0, 1                          # CornerRule (reconstruct.hpp:14)
 CTX_TIMING = 1
+CTX_DENSE = 2
 K_MAX_LAYERS = 2147483646                          # propagate.hpp:15-16
 K_MAX_GRID_DIM = 65535                             # grid.hpp:14
 
@@ -44,7 +45,7 @@ class UncoveredTargetError(Error):
 class _PropResult(C.Structure):
     _fields_ = [("layers_used", C.c_uint32), ("cause", C.c_uint32), ("layers_computed", C.c_uint32),
                 ("cell_bits", C.c_uint32), ("block_launches", C.c_uint64), ("layer_launches", C.c_uint64),
-                ("stencil_ms", C.c_double)]
+                ("stencil_ms", C.c_double), ("tiles_processed", C.c_uint64), ("tiles_total", C.c_uint64)]
 
 
 class _GridInfo(C.Structure):
@@ -145,9 +146,9 @@ def _check(st, ctx, what):
 class Context:
     """One CUDA device + stream (am_ctx).  Externally synchronised."""
 
-    def __init__(self, device: int = 0, timing: bool = False):
+    def __init__(self, device: int = 0, timing: bool = False, dense: bool = False):
         h = C.c_void_p()
-        opts = _CtxOpts(device, CTX_TIMING if timing else 0)
+        opts = _CtxOpts(device, (CTX_TIMING if timing else 0) | (CTX_DENSE if dense else 0))
         st = lib().am_ctx_create(C.byref(opts), C.byref(h))
         if st != OK:
             raise Error(f"cannot create a B200 context on device {device} (status {st})")
@@ -233,6 +234,8 @@ class PropResult:
         self.block_launches = r.block_launches
         self.layer_launches = r.layer_launches
         self.stencil_ms = r.stencil_ms
+        self.tiles_processed = r.tiles_processed
+        self.tiles_total = r.tiles_total
 
 
 class Grid:

@@ -53,6 +53,14 @@ struct am_grid {
   // row-slab membership: this grid holds rows [row0, row0 + g.H) of a total_h-row grid
   int slab = 0;
   uint32_t total_h = 0, row0 = 0;
+  // active-tile skipping state (single grids; stencil.cu k_tiles_*)
+  uint8_t* t_front[2] = {nullptr, nullptr};  // frontier flags: [t_fi] = last block, [t_fi^1] = being written
+  int t_fi = 0;
+  uint8_t* t_was = nullptr;                  // tile processed in the previous block
+  uint32_t* t_ell = nullptr;                 // layer of the tile's stored values
+  uint32_t* t_list = nullptr;                // work list (band << 16 | chunk)
+  uint32_t* t_count = nullptr;               // work-list length
+  unsigned long long* t_processed = nullptr; // tiles processed (statistics)
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;
   uint64_t* d_counts = nullptr;

@@ -40,6 +40,9 @@ constexpr int kBand = 32 * kWPL; // band width in cells (incl. halo)
 constexpr int kBandUseful = kBand - 2 * kK;
 constexpr int kBlockThreads = 128;
 
+// Active-tile skipping works on tiles of kTileRows rows x one band.
+constexpr int kTileRows = 64;
+
 struct Geo {
   uint32_t W, H;          // grid extent (cells)
   uint32_t pad;           // = kK: rows above / cols left of the grid
@@ -48,6 +51,8 @@ struct Geo {
   uint32_t nbands;        // vertical bands of kBandUseful cells
   uint32_t nseg;          // row segments (even)
   uint32_t seg_len;       // rows per segment (even)
+  uint32_t nchunks;       // row chunks of kTileRows (tile rows)
+  __host__ __device__ uint32_t ntiles() const { return nbands * nchunks; }
   __host__ __device__ size_t idx(uint32_t r, uint32_t c) const {
     return (size_t)(r + pad) * pitch + (c + pad);
   }
@@ -65,6 +70,15 @@ void launch_block(const Geo& g, int cell_bits, bool slab, const void* in, void* 
                   const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s);
 void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
                   uint32_t* flag, cudaStream_t s);
+// active-tile skipping (stencil.cu)
+void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cudaStream_t s);
+void launch_tiles_plan(const Geo& g, int cell_bits, const uint8_t* front_prev, uint8_t* front_next, uint8_t* was,
+                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* count,
+                       unsigned long long* processed, cudaStream_t s);
+void launch_block_tiles(const Geo& g, int cell_bits, int ctas, const void* in, void* out, const uint8_t* srcmask,
+                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
+                        const uint32_t* ell, uint32_t l0, uint32_t* flag, cudaStream_t s);
+void launch_tiles_finalize(const Geo& g, int cell_bits, uint32_t* ell, void* val, uint32_t l, cudaStream_t s);
 void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);
 void launch_zero_check(const Geo& g, int cell_bits, const void* val, uint32_t* flag, cudaStream_t s);
 void launch_decode(const Geo& g, int cell_bits, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,

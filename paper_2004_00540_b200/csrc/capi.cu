@@ -105,6 +105,13 @@ static void grid_free(am_grid* g) {
   cudaFree(g->d_offsets);
   cudaFree(g->d_status);
   cudaFree(g->d_pts);
+  cudaFree(g->t_front[0]);
+  cudaFree(g->t_front[1]);
+  cudaFree(g->t_was);
+  cudaFree(g->t_ell);
+  cudaFree(g->t_list);
+  cudaFree(g->t_count);
+  cudaFree(g->t_processed);
   delete g;
 }
 
@@ -149,6 +156,16 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = cudaMalloc(&g->d_flags, kFlagSlots * sizeof(uint32_t));
   if (!e) e = cudaHostAlloc(&g->h_flags, kFlagSlots * sizeof(uint32_t), cudaHostAllocDefault);
   for (int i = 0; !e && i < kFlagSlots; ++i) e = cudaEventCreateWithFlags(&g->flag_ev[i], cudaEventDisableTiming);
+  if (!slab) {  // active-tile skipping state
+    const size_t nt = g->g.ntiles();
+    if (!e) e = cudaMalloc(&g->t_front[0], nt);
+    if (!e) e = cudaMalloc(&g->t_front[1], nt);
+    if (!e) e = cudaMalloc(&g->t_was, nt);
+    if (!e) e = cudaMalloc(&g->t_ell, nt * 4);
+    if (!e) e = cudaMalloc(&g->t_list, nt * 4);
+    if (!e) e = cudaMalloc(&g->t_count, 4);
+    if (!e) e = cudaMalloc(&g->t_processed, 8);
+  }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->val[1], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->srcmask, 0, cells, s);
@@ -323,6 +340,38 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   for (auto& s : slabs)
     if ((st = reset_map(s.ctx, s.g, start_bits))) return st;
 
+  // exact active-tile skipping: single grids in batched mode
+  am_grid* tg = slabs[0].g;
+  const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_ell && mode == AM_MODE_BATCHED &&
+                     !(ctx->flags & AM_CTX_DENSE);
+  const size_t nt = tiles ? tg->g.ntiles() : 0;
+  const int tile_ctas = ctx->sms * 2;  // persistent: k_block_tiles is sized for 2 CTAs per SM
+  // every tile active next block, both fields identical for quiet tiles
+  auto tiles_all_active = [&](uint32_t at_layer) -> am_status {
+    CK(cudaMemsetAsync(tg->t_front[tg->t_fi], 1, nt, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_was, 1, nt, ctx->stream));
+    std::vector<uint32_t> e(nt, at_layer);
+    CK(cudaMemcpyAsync(tg->t_ell, e.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return AM_OK;
+  };
+  auto tiles_finalize = [&](uint32_t at_layer) -> am_status {
+    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_ell, tg->val[tg->cur], at_layer, ctx->stream);
+    CKL();
+    return AM_OK;
+  };
+  if (tiles) {
+    const size_t bytes = (size_t)tg->g.rows * tg->g.pitch * (tg->cell_bits / 8);
+    CK(cudaMemcpyAsync(tg->val[tg->cur ^ 1], tg->val[tg->cur], bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    tg->t_fi = 0;
+    CK(cudaMemsetAsync(tg->t_ell, 0, nt * 4, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_was, 0, nt, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_front[1], 0, nt, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
+    launch_tiles_init(tg->g, tg->srcmask, tg->t_front[0], ctx->stream);
+    CKL();
+  }
+
   am_prop_result r{};
   const bool timing = (ctx->flags & AM_CTX_TIMING) != 0;
   size_t timer_used = 0;
@@ -358,8 +407,13 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         if ((st = drain_one())) return st;
       pend.clear();
       if (lprime) break;
+      if (tiles && (st = tiles_finalize(l))) return st;
       for (auto& s : slabs)
         if ((st = promote(s.ctx, s.g))) return st;
+      if (tiles && (st = tiles_all_active(l))) return st;
+    }
+    if (tiles && !blocked) {  // a dense single layer needs every tile current
+      if ((st = tiles_finalize(l))) return st;
     }
     if (tr && (st = tr->exchange())) return st;
     const int slot = (int)(nblock % kFlagSlots);
@@ -385,7 +439,17 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
           }
           CK(cudaEventRecord(ctx->timers[timer_used].a, s));
         }
-        launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, flag, s);
+        if (tiles) {
+          CK(cudaMemsetAsync(g->t_count, 0, 4, s));
+          launch_tiles_plan(g->g, g->cell_bits, g->t_front[g->t_fi], g->t_front[g->t_fi ^ 1], g->t_was, g->t_ell,
+                            in, outp, l, kk, g->t_list, g->t_count, g->t_processed, s);
+          CKL();
+          launch_block_tiles(g->g, g->cell_bits, tile_ctas, in, outp, g->srcmask, g->rowsrc, g->t_list, g->t_count,
+                             g->t_front[g->t_fi ^ 1], g->t_ell, l, flag, s);
+          g->t_fi ^= 1;
+        } else {
+          launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, flag, s);
+        }
         ++c->launches;
         if (cudaError_t e = cudaPeekAtLastError()) return fail(c, AM_ECUDA, "k_block: %s", cudaGetErrorString(e));
         if (timing) CK(cudaEventRecord(ctx->timers[timer_used++].b, s));
@@ -398,6 +462,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       }
       g->cur ^= 1;
     }
+    if (tiles && !blocked && (st = tiles_all_active(l + kk))) return st;
     if (autom) {
       if (tr && (st = tr->reduce(words, false))) return st;
       for (auto& sr : slabs) {
@@ -421,6 +486,14 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   }
   while (!pend.empty())
     if ((st = drain_one())) return st;
+  if (tiles) {
+    if ((st = tiles_finalize(l))) return st;
+    unsigned long long proc = 0;
+    CK(cudaMemcpyAsync(&proc, tg->t_processed, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    r.tiles_processed = proc;
+    r.tiles_total = (uint64_t)nt * r.block_launches;
+  }
   uint32_t used = l, cause = AM_STOP_FIXED;
   if (autom) {
     const int zslot = (int)(nblock % kFlagSlots);

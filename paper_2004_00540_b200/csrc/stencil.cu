@@ -31,7 +31,9 @@ Geo make_geo(uint32_t W, uint32_t H, int warp_slots) {
   nseg = (nseg + 1) & ~1u;
   g.seg_len = seg;
   g.nseg = nseg;
-  g.rows = nseg * seg + 2 * kK;
+  g.nchunks = (H + kTileRows - 1) / kTileRows;
+  const uint32_t body = nseg * seg > g.nchunks * kTileRows ? nseg * seg : g.nchunks * kTileRows;
+  g.rows = body + 2 * kK;
   return g;
 }
 
@@ -289,31 +291,36 @@ __device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint
 // unflagged values), so they may be stored and folded into the flag
 // unchanged.  SLAB=true: the rows below the slab are a neighbour's halo
 // (flagged data) and must be neither stored nor counted.
-template <int CB, bool SLAB>
-__global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
-                                                         typename Cell<CB>::T* __restrict__ out,
-                                                         const uint8_t* __restrict__ srcmask,
-                                                         const uint8_t* __restrict__ rowsrc,
-                                                         uint32_t* __restrict__ flag) {
+// One work item per warp: tile A = band bA, allocated rows [rA, rA+rows+2K)
+// (rows of output), tile B likewise in the hi halves (16-bit cells; 32-bit
+// cells process A only).  Returns the warp's running u16x2/u32 minimum of
+// (a-1) over its stored cells (lo half = A, hi half = B).
+// LAG (active-tile mode): lagw[0..2] are this lane's per-half lags of the
+// tiles it reads above / inside / below the item (lane 0 and 31 read the
+// neighbouring bands); they are added to covered cells as rows arrive.
+template <int CB>
+__device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw);
+template <int CB, bool SLAB, bool LAG = false>
+__device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cell<CB>::T* __restrict__ in,
+                                                typename Cell<CB>::T* __restrict__ out,
+                                                const uint8_t* __restrict__ srcmask,
+                                                const uint8_t* __restrict__ rowsrc, uint32_t bA, uint32_t rA,
+                                                uint32_t bB, uint32_t rB, uint32_t rows, bool hasB,
+                                                uint32_t lag0 = 0, uint32_t lag1 = 0, uint32_t lag2 = 0) {
   using C = Cell<CB>;
   using T = typename C::T;
   const int lane = threadIdx.x & 31;
-  const uint32_t warp = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5);
-  const uint32_t ntiles = CB == 16 ? g.nseg / 2 : g.nseg;
-  if (warp >= g.nbands * ntiles) return;
-  const uint32_t band = warp % g.nbands, tile = warp / g.nbands;
-  const uint32_t col = band * kBandUseful + lane * kWPL;  // allocated column of this lane's first cell
-  const uint32_t rA = tile * g.seg_len;                   // allocated row of step 0
-  const uint32_t rB = (CB == 16 ? tile + ntiles : tile) * g.seg_len;
-  const uint32_t T_steps = g.seg_len + 2 * kK;
+  const uint32_t colA = bA * kBandUseful + lane * kWPL;  // allocated column of this lane's first cell
+  const uint32_t colB = bB * kBandUseful + lane * kWPL;
+  const uint32_t T_steps = rows + 2 * kK;
   const size_t pitch = g.pitch;
 
-  const T* pA = in + (size_t)rA * pitch + col;
-  const T* pB = in + (size_t)rB * pitch + col;
-  T* oA = out + (size_t)rA * pitch + col;  // output row for step t is rA + t - kK
-  T* oB = out + (size_t)rB * pitch + col;
-  const uint8_t* sA = srcmask + (size_t)rA * pitch + col;
-  const uint8_t* sB = srcmask + (size_t)rB * pitch + col;
+  const T* pA = in + (size_t)rA * pitch + colA;
+  const T* pB = in + (size_t)rB * pitch + colB;
+  T* oA = out + (size_t)rA * pitch + colA;  // output row for step t is rA + t - kK
+  T* oB = out + (size_t)rB * pitch + colB;
+  const uint8_t* sA = srcmask + (size_t)rA * pitch + colA;
+  const uint8_t* sB = srcmask + (size_t)rB * pitch + colB;
   const bool store_lane = lane >= kK / kWPL && lane < 32 - kK / kWPL;
 
   uint32_t P0[kK][kWPL], P1[kK][kWPL];
@@ -366,6 +373,13 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
       issue(tt + kStages - 1);  // refills the slot consumed by the previous step
       asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
       stage_words<CB>(ring + (tt % kStages) * kStageBytes, lane, x);
+      if constexpr (LAG) {
+        const uint32_t lw = tt < (uint32_t)kK ? lag0 : (tt < kK + rows ? lag1 : lag2);
+        if (__any_sync(0xffffffffu, lw != 0u)) {
+#pragma unroll
+          for (int w = 0; w < kWPL; ++w) x[w] = add_lag<CB>(x[w], lw);
+        }
+      }
       const size_t roff = (size_t)tt * pitch;
       srcbits = (srcbits << 1) | ((flag_win >> (tt & 31u)) & 1u);
       // rows t-1 .. t-kK are in flight; only steps that touch a source row pay for the +1
@@ -377,9 +391,9 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
         if (src_rows) stream_step<CB, 1, true>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
         else stream_step<CB, 1, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
       }
-      if (tt >= 2 * kK && tt < 2 * kK + g.seg_len && store_lane) {
+      if (tt >= 2 * kK && tt < 2 * kK + rows && store_lane) {
         if constexpr (!SLAB) {
-          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, true);
+          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
 #pragma unroll
           for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
         } else {
@@ -393,8 +407,204 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
       }
     }
   }
-  const uint32_t m = __reduce_min_sync(0xffffffffu, C::fold(acc));
-  if (lane == 0) atomicMin(flag, m);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  return acc;
+}
+
+// Dense mode: every (band, segment pair) of the grid, one warp each.
+template <int CB, bool SLAB>
+__global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
+                                                         typename Cell<CB>::T* __restrict__ out,
+                                                         const uint8_t* __restrict__ srcmask,
+                                                         const uint8_t* __restrict__ rowsrc,
+                                                         uint32_t* __restrict__ flag) {
+  const uint32_t warp = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t ntiles = CB == 16 ? g.nseg / 2 : g.nseg;
+  if (warp >= g.nbands * ntiles) return;
+  const uint32_t band = warp % g.nbands, tile = warp / g.nbands;
+  const uint32_t rA = tile * g.seg_len;  // allocated row of step 0
+  const uint32_t rB = (CB == 16 ? tile + ntiles : tile) * g.seg_len;
+  const uint32_t acc = stream_item<CB, SLAB>(g, in, out, srcmask, rowsrc, band, rA, band, rB, g.seg_len, true);
+  const uint32_t m = __reduce_min_sync(0xffffffffu, Cell<CB>::fold(acc));
+  if ((threadIdx.x & 31) == 0) atomicMin(flag, m);
+}
+
+// Active-tile mode: the warps walk the work list built by k_tiles_plan
+// (items = band << 16 | chunk), two tiles per warp in 16-bit mode.  Each
+// processed tile records whether it still has a frontier (a cell covered
+// during this block, i.e. 1 <= a <= kK) for the next plan.
+template <int CB>
+__global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: registers over occupancy
+    k_block_tiles(Geo g, const typename Cell<CB>::T* __restrict__ in, typename Cell<CB>::T* __restrict__ out,
+                  const uint8_t* __restrict__ srcmask, const uint8_t* __restrict__ rowsrc,
+                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint8_t* __restrict__ front,
+                  const uint32_t* __restrict__ ell, uint32_t l0, uint32_t* __restrict__ flag) {
+  const uint32_t n = *count;
+  const uint32_t per = CB == 16 ? 2u : 1u;
+  const uint32_t nw = gridDim.x * (kBlockThreads / 32);
+  const int lane = threadIdx.x & 31;
+  const int brel = lane == 0 ? -1 : (lane == 31 ? 1 : 0);  // band this lane's cells belong to
+  auto lag_of = [&](uint32_t c0, uint32_t b0, int dr) -> uint32_t {
+    const int c = (int)c0 + dr, b = (int)b0 + brel;
+    if (c < 0 || b < 0 || c >= (int)g.nchunks || b >= (int)g.nbands) return 0u;
+    const uint32_t e = ell[(uint32_t)c * g.nbands + (uint32_t)b];
+    return e < l0 ? l0 - e : 0u;
+  };
+  uint32_t gmin = 0xFFFFFFFFu;
+  for (uint32_t w = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5); w * per < n; w += nw) {
+    const uint32_t ia = list[w * per];
+    const bool hasB = CB == 16 && w * per + 1 < n;
+    const uint32_t ib = hasB ? list[w * per + 1] : ia;
+    const uint32_t bA = ia >> 16, cA = ia & 0xFFFFu, bB = ib >> 16, cB = ib & 0xFFFFu;
+    uint32_t lw[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const uint32_t la = lag_of(cA, bA, d - 1), lb = lag_of(cB, bB, d - 1);
+      lw[d] = CB == 16 ? (la | lb << 16) : la;
+    }
+    const uint32_t acc = stream_item<CB, false, true>(g, in, out, srcmask, rowsrc, bA, cA * kTileRows, bB,
+                                                      cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2]);
+    uint32_t ma, mb;
+    if (CB == 16) {
+      ma = __reduce_min_sync(0xffffffffu, acc & 0xFFFFu);
+      mb = __reduce_min_sync(0xffffffffu, acc >> 16);
+    } else {
+      ma = mb = __reduce_min_sync(0xffffffffu, acc);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      front[cA * g.nbands + bA] = ma < (uint32_t)kK;  // a-1 < K: covered during this block
+      if (hasB) front[cB * g.nbands + bB] = mb < (uint32_t)kK;
+    }
+    gmin = min(gmin, min(ma, hasB ? mb : ma));
+  }
+  if ((threadIdx.x & 31) == 0 && gmin != 0xFFFFFFFFu) atomicMin(flag, gmin);
+}
+
+// ------------------------------------------------- active-tile bookkeeping
+//
+// Exact skipping.  A cell covered during block b+1 is at
+// most kK hops from a cell covered in the last layer of block b, and tiles
+// are at least kK cells in both directions, so only tiles whose 3x3 tile
+// neighbourhood holds a frontier cell (covered during block b) can change
+// coverage in block b+1.  Every other tile is "quiet": its covered cells
+// just gain +1 per layer, which is applied lazily (ell[t] = layer of the
+// stored values).  Invariant: a tile not processed in the previous block
+// holds identical data in both ping-pong fields.
+
+// Adds lag to every covered cell (flag set, a > 0) of tile t in `val`.
+// Covered cells (flag set, a > 0) are exactly the halves above the bare flag:
+// adds `lagw` (per-half lag) to them, leaving uncovered and obstacle cells.
+template <int CB>
+__device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
+  if constexpr (CB == 16) return w + (__vcmpgtu2(w, 0x80008000u) & lagw);
+  else return w + (w > kFlag32 ? lagw : 0u);
+}
+
+// 16 B per lane-row: 8 cells (u16) or 4 cells (u32, two chunks per lane)
+template <int CB, typename F>
+__device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, uint32_t chunk, F f) {
+  const int lane = threadIdx.x & 31;
+  constexpr int kVecCells = 16 / sizeof(typename Cell<CB>::T);
+  constexpr int kVecs = kBandUseful / kVecCells;  // vectors per tile row
+  for (int v = lane; v < kVecs * kTileRows; v += 32) {
+    const uint32_t r = v / kVecs, k = v % kVecs;
+    f((size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kBandUseful + k * kVecCells);
+  }
+}
+
+// Adds lag to every covered cell of one tile (whole tile, 16 B accesses).
+template <int CB>
+__device__ void tile_catch_up(const Geo& g, typename Cell<CB>::T* val, uint32_t band, uint32_t chunk, uint32_t lag) {
+  const uint32_t lagw = CB == 16 ? (lag | lag << 16) : lag;
+  tile_rows_foreach<CB>(g, band, chunk, [&](size_t i) {
+    uint4* p = reinterpret_cast<uint4*>(val + i);
+    uint4 v = *p;
+    v.x = add_lag<CB>(v.x, lagw);
+    v.y = add_lag<CB>(v.y, lagw);
+    v.z = add_lag<CB>(v.z, lagw);
+    v.w = add_lag<CB>(v.w, lagw);
+    *p = v;
+  });
+}
+
+template <int CB>
+__device__ void tile_copy(const Geo& g, const typename Cell<CB>::T* src, typename Cell<CB>::T* dst, uint32_t band,
+                          uint32_t chunk) {
+  tile_rows_foreach<CB>(g, band, chunk, [&](size_t i) {
+    *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(src + i);
+  });
+}
+
+// One warp per tile: decides the tile's role for the next block of kk
+// layers starting at layer l0 (X = current field, Y = the other one),
+// appends active tiles to the work list and performs its catch-up / copy.
+template <int CB>
+__global__ void k_tiles_plan(Geo g, const uint8_t* __restrict__ front_prev, uint8_t* __restrict__ front_next,
+                             uint8_t* __restrict__ was_active, uint32_t* __restrict__ ell,
+                             typename Cell<CB>::T* __restrict__ X, typename Cell<CB>::T* __restrict__ Y, uint32_t l0,
+                             uint32_t kk, uint32_t* __restrict__ list, uint32_t* __restrict__ count,
+                             unsigned long long* __restrict__ processed) {
+  const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= g.ntiles()) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t chunk = t / g.nbands, band = t % g.nbands;
+  bool f = false, inner = false;
+  if (lane < 25) {
+    const int dr = lane / 5 - 2, dc = lane % 5 - 2;
+    const int c = (int)chunk + dr, b = (int)band + dc;
+    inner = dr >= -1 && dr <= 1 && dc >= -1 && dc <= 1;
+    if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands) f = front_prev[(uint32_t)c * g.nbands + b] != 0;
+  }
+  const bool act = __any_sync(0xffffffffu, f && inner);  // frontier within one tile
+  const uint32_t e = ell[t];
+  const bool prev = was_active[t] != 0;
+  // Quiet neighbours stay lagged: the block kernel adds their lag to the
+  // halo rows/columns it reads (stream_item, LAG).  A tile becoming active
+  // is brought to l0 first; a tile leaving the active set copies its current
+  // values to the other field once (the quiet-tile invariant).
+  if (act) {
+    if (e < l0) tile_catch_up<CB>(g, X, band, chunk, l0 - e);
+  } else if (prev) {
+    tile_copy<CB>(g, X, Y, band, chunk);
+  }
+  if (lane == 0) {
+    front_next[t] = 0;
+    was_active[t] = act;
+    if (act) {
+      ell[t] = l0 + kk;
+      list[atomicAdd(count, 1u)] = band << 16 | chunk;
+      atomicAdd(processed, 1ull);
+    }
+  }
+}
+
+// Brings every lagging tile of `val` to layer l (before dense work, the
+// fixed-point check, downloads and path tracing).
+template <int CB>
+__global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ ell, typename Cell<CB>::T* __restrict__ val, uint32_t l) {
+  const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= g.ntiles()) return;
+  const uint32_t e = ell[t];
+  if (e < l) tile_catch_up<CB>(g, val, t % g.nbands, t / g.nbands, l - e);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) ell[t] = l;
+}
+
+// Layer-0 frontier: every tile holding a source (a = 1 at layer 0).
+__global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint8_t* __restrict__ front) {
+  const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= g.ntiles()) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t chunk = t / g.nbands, band = t % g.nbands;
+  bool any = false;
+  if (lane < kBandUseful / kWPL)
+    for (uint32_t r = 0; r < (uint32_t)kTileRows; ++r) {
+      const size_t base = (size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kBandUseful + lane * kWPL;
+      const uint2 m = *reinterpret_cast<const uint2*>(srcmask + base);
+      any |= (m.x | m.y) != 0;
+    }
+  any = __any_sync(0xffffffffu, any);
+  if (lane == 0) front[t] = any;
 }
 
 // -------------------------------------------------------- single layer
@@ -563,6 +773,42 @@ void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, co
     k_block<32, false><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
   else
     k_block<32, true><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
+}
+
+void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cudaStream_t s) {
+  const uint32_t n = g.ntiles();
+  k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, front);
+}
+
+void launch_tiles_plan(const Geo& g, int cb, const uint8_t* front_prev, uint8_t* front_next, uint8_t* was,
+                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* count,
+                       unsigned long long* processed, cudaStream_t s) {
+  const uint32_t n = g.ntiles();
+  if (cb == 16)
+    k_tiles_plan<16><<<(n + 3) / 4, 128, 0, s>>>(g, front_prev, front_next, was, ell, (uint16_t*)X, (uint16_t*)Y, l0,
+                                                 kk, list, count, processed);
+  else
+    k_tiles_plan<32><<<(n + 3) / 4, 128, 0, s>>>(g, front_prev, front_next, was, ell, (uint32_t*)X, (uint32_t*)Y, l0,
+                                                 kk, list, count, processed);
+}
+
+void launch_block_tiles(const Geo& g, int cb, int ctas, const void* in, void* out, const uint8_t* srcmask,
+                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
+                        const uint32_t* ell, uint32_t l0, uint32_t* flag, cudaStream_t s) {
+  if (cb == 16)
+    k_block_tiles<16><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, rowsrc,
+                                                              list, count, front, ell, l0, flag);
+  else
+    k_block_tiles<32><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, rowsrc,
+                                                              list, count, front, ell, l0, flag);
+}
+
+void launch_tiles_finalize(const Geo& g, int cb, uint32_t* ell, void* val, uint32_t l, cudaStream_t s) {
+  const uint32_t n = g.ntiles();
+  if (cb == 16)
+    k_tiles_finalize<16><<<(n + 3) / 4, 128, 0, s>>>(g, ell, (uint16_t*)val, l);
+  else
+    k_tiles_finalize<32><<<(n + 3) / 4, 128, 0, s>>>(g, ell, (uint32_t*)val, l);
 }
 
 int block_kernel_blocks_per_sm(int cb) {
