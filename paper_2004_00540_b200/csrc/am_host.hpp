@@ -12,7 +12,8 @@
 
 namespace am {
 constexpr int kFlagSlots = 64;
-constexpr int kLag = 2;  // blocks in flight before the host reads a fixed-point flag
+constexpr int kLag = 2;        // blocks in flight before the host reads a fixed-point flag (dense)
+constexpr int kLagTiles = 24;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
 }  // namespace am
 
@@ -59,7 +60,8 @@ struct am_grid {
   uint8_t* t_was = nullptr;                  // tile processed in the previous block
   uint32_t* t_ell = nullptr;                 // layer of the tile's stored values
   uint32_t* t_list = nullptr;                // work list (band << 16 | chunk)
-  uint32_t* t_count = nullptr;               // work-list length
+  uint32_t* t_count = nullptr;               // [0..1] work-list, [2..3] fix-list lengths
+  uint2* t_fix = nullptr;                    // catch-up / copy items
   unsigned long long* t_processed = nullptr; // tiles processed (statistics)
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;

@@ -73,8 +73,9 @@ void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const 
 // active-tile skipping (stencil.cu)
 void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cudaStream_t s);
 void launch_tiles_plan(const Geo& g, int cell_bits, const uint8_t* front_prev, uint8_t* front_next, uint8_t* was,
-                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* count,
-                       unsigned long long* processed, cudaStream_t s);
+                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters,
+                       int parity, uint32_t* flag, unsigned long long* processed, uint2* fixes, int fix_ctas,
+                       cudaStream_t s);
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, const void* in, void* out, const uint8_t* srcmask,
                         const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
                         const uint32_t* ell, uint32_t l0, uint32_t* flag, cudaStream_t s);

@@ -111,6 +111,7 @@ static void grid_free(am_grid* g) {
   cudaFree(g->t_ell);
   cudaFree(g->t_list);
   cudaFree(g->t_count);
+  cudaFree(g->t_fix);
   cudaFree(g->t_processed);
   delete g;
 }
@@ -163,7 +164,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
     if (!e) e = cudaMalloc(&g->t_was, nt);
     if (!e) e = cudaMalloc(&g->t_ell, nt * 4);
     if (!e) e = cudaMalloc(&g->t_list, nt * 4);
-    if (!e) e = cudaMalloc(&g->t_count, 4);
+    if (!e) e = cudaMalloc(&g->t_count, 16);  // alternating work-list and fix-list counters
+    if (!e) e = cudaMalloc(&g->t_fix, nt * sizeof(uint2));
     if (!e) e = cudaMalloc(&g->t_processed, 8);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
@@ -368,6 +370,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     CK(cudaMemsetAsync(tg->t_was, 0, nt, ctx->stream));
     CK(cudaMemsetAsync(tg->t_front[1], 0, nt, ctx->stream));
     CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_count, 0, 16, ctx->stream));
     launch_tiles_init(tg->g, tg->srcmask, tg->t_front[0], ctx->stream);
     CKL();
   }
@@ -423,7 +426,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       uint32_t* flag = g->d_flags + slot;
       words[i] = flag;
       cudaStream_t s = c->stream;
-      if (autom) {
+      if (autom && !(tiles && blocked)) {  // the tile planner resets its own slot
         cudaError_t e = cudaMemsetAsync(flag, 0xFF, sizeof(uint32_t), s);
         if (e) return fail(c, AM_ECUDA, "memset: %s", cudaGetErrorString(e));
       }
@@ -440,11 +443,13 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
           CK(cudaEventRecord(ctx->timers[timer_used].a, s));
         }
         if (tiles) {
-          CK(cudaMemsetAsync(g->t_count, 0, 4, s));
+          uint32_t* cnt = g->t_count + (nblock & 1);  // the planner zeroes the other slot for the next block
           launch_tiles_plan(g->g, g->cell_bits, g->t_front[g->t_fi], g->t_front[g->t_fi ^ 1], g->t_was, g->t_ell,
-                            in, outp, l, kk, g->t_list, g->t_count, g->t_processed, s);
+                            in, outp, l, kk, g->t_list, g->t_count, (int)(nblock & 1), autom ? flag : nullptr,
+                            g->t_processed, g->t_fix, c->sms * 2, s);
           CKL();
-          launch_block_tiles(g->g, g->cell_bits, tile_ctas, in, outp, g->srcmask, g->rowsrc, g->t_list, g->t_count,
+          ++c->launches;
+          launch_block_tiles(g->g, g->cell_bits, tile_ctas, in, outp, g->srcmask, g->rowsrc, g->t_list, cnt,
                              g->t_front[g->t_fi ^ 1], g->t_ell, l, flag, s);
           g->t_fi ^= 1;
         } else {
@@ -481,7 +486,10 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         am_ctx* c = sr.ctx;
         CK(cudaStreamSynchronize(c->stream));
       }
-    while ((int)pend.size() > kLag)
+    // Tile mode runs far ahead of the host: blocks past the fixed point have
+    // no frontier, so they cost a near-empty launch each.  Dense blocks past
+    // it cost a full sweep, so the dense path keeps the lag short.
+    while ((int)pend.size() > (tiles ? kLagTiles : kLag))
       if ((st = drain_one())) return st;
   }
   while (!pend.empty())

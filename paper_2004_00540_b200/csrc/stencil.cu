@@ -535,46 +535,75 @@ __device__ void tile_copy(const Geo& g, const typename Cell<CB>::T* src, typenam
   });
 }
 
-// One warp per tile: decides the tile's role for the next block of kk
-// layers starting at layer l0 (X = current field, Y = the other one),
-// appends active tiles to the work list and performs its catch-up / copy.
+// One lane per tile (a warp covers 32 consecutive tiles): decides each
+// tile's role for the next block of kk layers starting at layer l0 (X =
+// current field, Y = the other one), appends active tiles to the work list
+// with one atomic per warp, then the whole warp performs the few catch-ups
+// (tile becoming active) and copies (tile leaving the active set).  Quiet
+// neighbours stay lagged: the block kernel adds their lag to the halo it
+// reads (stream_item LAG).  Block 0 also resets the next block's work
+// counter and this block's fixed-point slot, so no memset is issued.
 template <int CB>
 __global__ void k_tiles_plan(Geo g, const uint8_t* __restrict__ front_prev, uint8_t* __restrict__ front_next,
                              uint8_t* __restrict__ was_active, uint32_t* __restrict__ ell,
                              typename Cell<CB>::T* __restrict__ X, typename Cell<CB>::T* __restrict__ Y, uint32_t l0,
                              uint32_t kk, uint32_t* __restrict__ list, uint32_t* __restrict__ count,
-                             unsigned long long* __restrict__ processed) {
-  const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (t >= g.ntiles()) return;
+                             uint32_t* __restrict__ next_count, uint32_t* __restrict__ flag,
+                             unsigned long long* __restrict__ processed, uint2* __restrict__ fixes,
+                             uint32_t* __restrict__ fix_count, uint32_t* __restrict__ next_fix_count) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *next_count = 0;
+    *next_fix_count = 0;
+    if (flag) *flag = 0xFFFFFFFFu;
+  }
   const int lane = threadIdx.x & 31;
-  const uint32_t chunk = t / g.nbands, band = t % g.nbands;
-  bool f = false, inner = false;
-  if (lane < 25) {
-    const int dr = lane / 5 - 2, dc = lane % 5 - 2;
-    const int c = (int)chunk + dr, b = (int)band + dc;
-    inner = dr >= -1 && dr <= 1 && dc >= -1 && dc <= 1;
-    if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands) f = front_prev[(uint32_t)c * g.nbands + b] != 0;
-  }
-  const bool act = __any_sync(0xffffffffu, f && inner);  // frontier within one tile
-  const uint32_t e = ell[t];
-  const bool prev = was_active[t] != 0;
-  // Quiet neighbours stay lagged: the block kernel adds their lag to the
-  // halo rows/columns it reads (stream_item, LAG).  A tile becoming active
-  // is brought to l0 first; a tile leaving the active set copies its current
-  // values to the other field once (the quiet-tile invariant).
-  if (act) {
-    if (e < l0) tile_catch_up<CB>(g, X, band, chunk, l0 - e);
-  } else if (prev) {
-    tile_copy<CB>(g, X, Y, band, chunk);
-  }
-  if (lane == 0) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nt = g.ntiles();
+  bool act = false, prev = false;
+  uint32_t e = 0;
+  if (t < nt) {
+    const int chunk = (int)(t / g.nbands), band = (int)(t % g.nbands);
+#pragma unroll
+    for (int dr = -1; dr <= 1; ++dr)
+#pragma unroll
+      for (int dc = -1; dc <= 1; ++dc) {
+        const int c = chunk + dr, b = band + dc;
+        if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands)
+          act |= front_prev[(uint32_t)c * g.nbands + (uint32_t)b] != 0;
+      }
+    e = ell[t];
+    prev = was_active[t] != 0;
     front_next[t] = 0;
     was_active[t] = act;
-    if (act) {
-      ell[t] = l0 + kk;
-      list[atomicAdd(count, 1u)] = band << 16 | chunk;
-      atomicAdd(processed, 1ull);
-    }
+    if (act) ell[t] = l0 + kk;
+  }
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  uint32_t base = 0;
+  if (lane == 0 && am) {
+    base = atomicAdd(count, (uint32_t)__popc(am));
+    atomicAdd(processed, (unsigned long long)__popc(am));
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (act) list[base + __popc(am & ((1u << lane) - 1u))] = (t % g.nbands) << 16 | (t / g.nbands);
+  // fix items: (tile, lag) = catch-up of a tile becoming active; (tile, 0) = copy of one leaving
+  const bool needs = (act && e < l0) || (!act && prev);
+  const uint32_t fm = __ballot_sync(0xffffffffu, needs);
+  uint32_t fbase = 0;
+  if (lane == 0 && fm) fbase = atomicAdd(fix_count, (uint32_t)__popc(fm));
+  fbase = __shfl_sync(0xffffffffu, fbase, 0);
+  if (needs) fixes[fbase + __popc(fm & ((1u << lane) - 1u))] = make_uint2(t, act ? l0 - e : 0u);
+}
+
+// One warp per fix item (persistent grid-stride over the planner's list).
+template <int CB>
+__global__ void k_tiles_fix(Geo g, typename Cell<CB>::T* __restrict__ X, typename Cell<CB>::T* __restrict__ Y,
+                            const uint2* __restrict__ fixes, uint32_t* __restrict__ fix_count) {
+  const uint32_t n = *fix_count;
+  const uint32_t nw = gridDim.x * (blockDim.x / 32);
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += nw) {
+    const uint2 f = fixes[i];
+    if (f.y) tile_catch_up<CB>(g, X, f.x % g.nbands, f.x / g.nbands, f.y);
+    else tile_copy<CB>(g, X, Y, f.x % g.nbands, f.x / g.nbands);
   }
 }
 
@@ -780,16 +809,24 @@ void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cud
   k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, front);
 }
 
+// counters[0..1]: work-list lengths, counters[2..3]: fix-list lengths (alternating per block)
 void launch_tiles_plan(const Geo& g, int cb, const uint8_t* front_prev, uint8_t* front_next, uint8_t* was,
-                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* count,
-                       unsigned long long* processed, cudaStream_t s) {
+                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters,
+                       int parity, uint32_t* flag, unsigned long long* processed, uint2* fixes, int fix_ctas,
+                       cudaStream_t s) {
   const uint32_t n = g.ntiles();
-  if (cb == 16)
-    k_tiles_plan<16><<<(n + 3) / 4, 128, 0, s>>>(g, front_prev, front_next, was, ell, (uint16_t*)X, (uint16_t*)Y, l0,
-                                                 kk, list, count, processed);
-  else
-    k_tiles_plan<32><<<(n + 3) / 4, 128, 0, s>>>(g, front_prev, front_next, was, ell, (uint32_t*)X, (uint32_t*)Y, l0,
-                                                 kk, list, count, processed);
+  const uint32_t blocks = (n + 255) / 256;
+  uint32_t *cnt = counters + parity, *ncnt = counters + (parity ^ 1);
+  uint32_t *fcnt = counters + 2 + parity, *nfcnt = counters + 2 + (parity ^ 1);
+  if (cb == 16) {
+    k_tiles_plan<16><<<blocks, 256, 0, s>>>(g, front_prev, front_next, was, ell, (uint16_t*)X, (uint16_t*)Y, l0, kk,
+                                            list, cnt, ncnt, flag, processed, fixes, fcnt, nfcnt);
+    k_tiles_fix<16><<<fix_ctas, 256, 0, s>>>(g, (uint16_t*)X, (uint16_t*)Y, fixes, fcnt);
+  } else {
+    k_tiles_plan<32><<<blocks, 256, 0, s>>>(g, front_prev, front_next, was, ell, (uint32_t*)X, (uint32_t*)Y, l0, kk,
+                                            list, cnt, ncnt, flag, processed, fixes, fcnt, nfcnt);
+    k_tiles_fix<32><<<fix_ctas, 256, 0, s>>>(g, (uint32_t*)X, (uint32_t*)Y, fixes, fcnt);
+  }
 }
 
 void launch_block_tiles(const Geo& g, int cb, int ctas, const void* in, void* out, const uint8_t* srcmask,
