@@ -57,11 +57,10 @@ struct am_grid {
   // active-tile skipping state (single grids; stencil.cu k_tiles_*)
   uint8_t* t_front[2] = {nullptr, nullptr};  // frontier flags: [t_fi] = last block, [t_fi^1] = being written
   int t_fi = 0;
-  uint8_t* t_was = nullptr;                  // tile processed in the previous block
-  uint32_t* t_ell = nullptr;                 // layer of the tile's stored values
+  uint32_t* t_state[2] = {nullptr, nullptr}; // per tile: layer << 1 | home field; [t_si] = current
+  int t_si = 0;
   uint32_t* t_list = nullptr;                // work list (band << 16 | chunk)
-  uint32_t* t_count = nullptr;               // [0..1] work-list, [2..3] fix-list lengths
-  uint2* t_fix = nullptr;                    // catch-up / copy items
+  uint32_t* t_count = nullptr;               // [0..1] alternating work-list lengths
   unsigned long long* t_processed = nullptr; // tiles processed (statistics)
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;

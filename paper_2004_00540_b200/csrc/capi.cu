@@ -107,11 +107,10 @@ static void grid_free(am_grid* g) {
   cudaFree(g->d_pts);
   cudaFree(g->t_front[0]);
   cudaFree(g->t_front[1]);
-  cudaFree(g->t_was);
-  cudaFree(g->t_ell);
+  cudaFree(g->t_state[0]);
+  cudaFree(g->t_state[1]);
   cudaFree(g->t_list);
   cudaFree(g->t_count);
-  cudaFree(g->t_fix);
   cudaFree(g->t_processed);
   delete g;
 }
@@ -161,11 +160,10 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
     const size_t nt = g->g.ntiles();
     if (!e) e = cudaMalloc(&g->t_front[0], nt);
     if (!e) e = cudaMalloc(&g->t_front[1], nt);
-    if (!e) e = cudaMalloc(&g->t_was, nt);
-    if (!e) e = cudaMalloc(&g->t_ell, nt * 4);
+    if (!e) e = cudaMalloc(&g->t_state[0], nt * 4);
+    if (!e) e = cudaMalloc(&g->t_state[1], nt * 4);
     if (!e) e = cudaMalloc(&g->t_list, nt * 4);
-    if (!e) e = cudaMalloc(&g->t_count, 16);  // alternating work-list and fix-list counters
-    if (!e) e = cudaMalloc(&g->t_fix, nt * sizeof(uint2));
+    if (!e) e = cudaMalloc(&g->t_count, 8);  // alternating work-list counters
     if (!e) e = cudaMalloc(&g->t_processed, 8);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
@@ -344,33 +342,33 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
 
   // exact active-tile skipping: single grids in batched mode
   am_grid* tg = slabs[0].g;
-  const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_ell && mode == AM_MODE_BATCHED &&
+  const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_state[0] && mode == AM_MODE_BATCHED &&
                      !(ctx->flags & AM_CTX_DENSE);
   const size_t nt = tiles ? tg->g.ntiles() : 0;
   const int tile_ctas = ctx->sms * 2;  // persistent: k_block_tiles is sized for 2 CTAs per SM
-  // every tile active next block, both fields identical for quiet tiles
+  // after dense work: every tile current at at_layer in val[cur], all active next block
   auto tiles_all_active = [&](uint32_t at_layer) -> am_status {
     CK(cudaMemsetAsync(tg->t_front[tg->t_fi], 1, nt, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_was, 1, nt, ctx->stream));
-    std::vector<uint32_t> e(nt, at_layer);
-    CK(cudaMemcpyAsync(tg->t_ell, e.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<uint32_t> e(nt, at_layer << 1 | (uint32_t)tg->cur);
+    CK(cudaMemcpyAsync(tg->t_state[tg->t_si], e.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return AM_OK;
   };
+  // every tile current at at_layer in val[0] (then cur = 0)
   auto tiles_finalize = [&](uint32_t at_layer) -> am_status {
-    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_ell, tg->val[tg->cur], at_layer, ctx->stream);
+    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_state[tg->t_si], tg->val[0], tg->val[1], 0, at_layer,
+                          ctx->stream);
     CKL();
+    tg->cur = 0;
     return AM_OK;
   };
-  if (tiles) {
-    const size_t bytes = (size_t)tg->g.rows * tg->g.pitch * (tg->cell_bits / 8);
-    CK(cudaMemcpyAsync(tg->val[tg->cur ^ 1], tg->val[tg->cur], bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (tiles) {  // layer 0 lives in val[cur] (= val[0] after reset_map): state 0 << 1 | 0
     tg->t_fi = 0;
-    CK(cudaMemsetAsync(tg->t_ell, 0, nt * 4, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_was, 0, nt, ctx->stream));
+    tg->t_si = 0;
+    CK(cudaMemsetAsync(tg->t_state[0], 0, nt * 4, ctx->stream));
     CK(cudaMemsetAsync(tg->t_front[1], 0, nt, ctx->stream));
     CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_count, 0, 16, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_count, 0, 8, ctx->stream));
     launch_tiles_init(tg->g, tg->srcmask, tg->t_front[0], ctx->stream);
     CKL();
   }
@@ -443,15 +441,15 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
           CK(cudaEventRecord(ctx->timers[timer_used].a, s));
         }
         if (tiles) {
-          uint32_t* cnt = g->t_count + (nblock & 1);  // the planner zeroes the other slot for the next block
-          launch_tiles_plan(g->g, g->cell_bits, g->t_front[g->t_fi], g->t_front[g->t_fi ^ 1], g->t_was, g->t_ell,
-                            in, outp, l, kk, g->t_list, g->t_count, (int)(nblock & 1), autom ? flag : nullptr,
-                            g->t_processed, g->t_fix, c->sms * 2, s);
+          // the planner zeroes the other counter slot for the next block and writes the next states
+          uint32_t* cnt = g->t_count + g->t_si;
+          launch_tiles_plan(g->g, g->t_front[g->t_fi], g->t_front[g->t_fi ^ 1], g->t_state, g->t_si, l, kk,
+                            g->t_list, g->t_count, autom ? flag : nullptr, g->t_processed, s);
           CKL();
-          ++c->launches;
-          launch_block_tiles(g->g, g->cell_bits, tile_ctas, in, outp, g->srcmask, g->rowsrc, g->t_list, cnt,
-                             g->t_front[g->t_fi ^ 1], g->t_ell, l, flag, s);
+          launch_block_tiles(g->g, g->cell_bits, tile_ctas, g->val[0], g->val[1], g->srcmask, g->rowsrc,
+                             g->t_list, cnt, g->t_front[g->t_fi ^ 1], g->t_state[g->t_si], l, flag, s);
           g->t_fi ^= 1;
+          g->t_si ^= 1;
         } else {
           launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, flag, s);
         }

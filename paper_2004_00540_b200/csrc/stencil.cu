@@ -300,13 +300,18 @@ __device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint
 // neighbouring bands); they are added to covered cells as rows arrive.
 template <int CB>
 __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw);
+// Field selection (active-tile mode): the two ping-pong fields are `in` and
+// `in + delta`; bit r of `homes` (r = 0 above, 1 inside, 2 below the item)
+// says tile A's region r is read from the second field, bits 3..5 the same
+// for B, bit 6 / 7 that A's / B's output goes to `out + delta`.
 template <int CB, bool SLAB, bool LAG = false>
 __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cell<CB>::T* __restrict__ in,
                                                 typename Cell<CB>::T* __restrict__ out,
                                                 const uint8_t* __restrict__ srcmask,
                                                 const uint8_t* __restrict__ rowsrc, uint32_t bA, uint32_t rA,
                                                 uint32_t bB, uint32_t rB, uint32_t rows, bool hasB,
-                                                uint32_t lag0 = 0, uint32_t lag1 = 0, uint32_t lag2 = 0) {
+                                                uint32_t lag0 = 0, uint32_t lag1 = 0, uint32_t lag2 = 0,
+                                                ptrdiff_t delta = 0, uint32_t homes = 0) {
   using C = Cell<CB>;
   using T = typename C::T;
   const int lane = threadIdx.x & 31;
@@ -317,8 +322,8 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
 
   const T* pA = in + (size_t)rA * pitch + colA;
   const T* pB = in + (size_t)rB * pitch + colB;
-  T* oA = out + (size_t)rA * pitch + colA;  // output row for step t is rA + t - kK
-  T* oB = out + (size_t)rB * pitch + colB;
+  T* oA = out + (size_t)rA * pitch + colA + ((homes >> 6) & 1u ? delta : 0);  // output row of step t: rA + t - kK
+  T* oB = out + (size_t)rB * pitch + colB + ((homes >> 7) & 1u ? delta : 0);
   const uint8_t* sA = srcmask + (size_t)rA * pitch + colA;
   const uint8_t* sB = srcmask + (size_t)rB * pitch + colB;
   const bool store_lane = lane >= kK / kWPL && lane < 32 - kK / kWPL;
@@ -341,12 +346,19 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     uint8_t* dst = ring + (step % kStages) * kStageBytes;
     if (step < T_steps) {
       const size_t off = (size_t)step * pitch;
+      const T* a = pA + off;
+      const T* b = pB + off;
+      if constexpr (LAG) {
+        const uint32_t reg = step < (uint32_t)kK ? 0u : (step < kK + rows ? 1u : 2u);
+        if ((homes >> reg) & 1u) a += delta;
+        if ((homes >> (3 + reg)) & 1u) b += delta;
+      }
       if (CB == 16) {
-        cp_async16(dst + lane * 16, pA + off);
-        cp_async16(dst + kBand * 2 + lane * 16, pB + off);
+        cp_async16(dst + lane * 16, a);
+        cp_async16(dst + kBand * 2 + lane * 16, b);
       } else {
-        cp_async16(dst + lane * 32, pA + off);
-        cp_async16(dst + lane * 32 + 16, pA + off + 16 / sizeof(T));
+        cp_async16(dst + lane * 32, a);
+        cp_async16(dst + lane * 32 + 16, a + 16 / sizeof(T));
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -430,24 +442,33 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
 }
 
 // Active-tile mode: the warps walk the work list built by k_tiles_plan
-// (items = band << 16 | chunk), two tiles per warp in 16-bit mode.  Each
-// processed tile records whether it still has a frontier (a cell covered
-// during this block, i.e. 1 <= a <= kK) for the next plan.
+// (items = band << 16 | chunk), two tiles per warp in 16-bit mode.  Every
+// tile has a home field (the ping-pong field holding its latest values) and
+// the layer of those values (state word: layer << 1 | home).  The item reads
+// each region it touches from that region's home with the region's lag
+// added to covered cells, and writes its own rows to the other field, so
+// quiet tiles are never copied or rewritten.  Each processed tile records
+// whether it still has a frontier (a cell covered during this block,
+// 1 <= a <= kK) for the next plan.
 template <int CB>
 __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: registers over occupancy
-    k_block_tiles(Geo g, const typename Cell<CB>::T* __restrict__ in, typename Cell<CB>::T* __restrict__ out,
-                  const uint8_t* __restrict__ srcmask, const uint8_t* __restrict__ rowsrc,
-                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint8_t* __restrict__ front,
-                  const uint32_t* __restrict__ ell, uint32_t l0, uint32_t* __restrict__ flag) {
+    k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
+                  const uint8_t* __restrict__ rowsrc, const uint32_t* __restrict__ list,
+                  const uint32_t* __restrict__ count, uint8_t* __restrict__ front, const uint32_t* __restrict__ state,
+                  uint32_t l0, uint32_t* __restrict__ flag) {
   const uint32_t n = *count;
   const uint32_t per = CB == 16 ? 2u : 1u;
   const uint32_t nw = gridDim.x * (kBlockThreads / 32);
   const int lane = threadIdx.x & 31;
   const int brel = lane == 0 ? -1 : (lane == 31 ? 1 : 0);  // band this lane's cells belong to
-  auto lag_of = [&](uint32_t c0, uint32_t b0, int dr) -> uint32_t {
+  // (lag, home) of the tile this lane reads at chunk c0+dr
+  auto region = [&](uint32_t c0, uint32_t b0, int dr, uint32_t& home) -> uint32_t {
     const int c = (int)c0 + dr, b = (int)b0 + brel;
-    if (c < 0 || b < 0 || c >= (int)g.nchunks || b >= (int)g.nbands) return 0u;
-    const uint32_t e = ell[(uint32_t)c * g.nbands + (uint32_t)b];
+    home = 0;
+    if (c < 0 || b < 0 || c >= (int)g.nchunks || b >= (int)g.nbands) return 0u;  // padding: zero in both fields
+    const uint32_t s = state[(uint32_t)c * g.nbands + (uint32_t)b];
+    home = s & 1u;
+    const uint32_t e = s >> 1;
     return e < l0 ? l0 - e : 0u;
   };
   uint32_t gmin = 0xFFFFFFFFu;
@@ -456,14 +477,20 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
     const bool hasB = CB == 16 && w * per + 1 < n;
     const uint32_t ib = hasB ? list[w * per + 1] : ia;
     const uint32_t bA = ia >> 16, cA = ia & 0xFFFFu, bB = ib >> 16, cB = ib & 0xFFFFu;
-    uint32_t lw[3];
+    uint32_t lw[3], homes = 0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const uint32_t la = lag_of(cA, bA, d - 1), lb = lag_of(cB, bB, d - 1);
+      uint32_t ha, hb;
+      const uint32_t la = region(cA, bA, d - 1, ha), lb = region(cB, bB, d - 1, hb);
       lw[d] = CB == 16 ? (la | lb << 16) : la;
+      homes |= ha << d | hb << (3 + d);
     }
-    const uint32_t acc = stream_item<CB, false, true>(g, in, out, srcmask, rowsrc, bA, cA * kTileRows, bB,
-                                                      cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2]);
+    // own rows go to the field that is not the tile's home
+    const uint32_t sa = state[cA * g.nbands + bA], sb = state[cB * g.nbands + bB];
+    homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
+    const uint32_t acc = stream_item<CB, false, true>(g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB,
+                                                      cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2], delta,
+                                                      homes);
     uint32_t ma, mb;
     if (CB == 16) {
       ma = __reduce_min_sync(0xffffffffu, acc & 0xFFFFu);
@@ -471,13 +498,13 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
     } else {
       ma = mb = __reduce_min_sync(0xffffffffu, acc);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
       front[cA * g.nbands + bA] = ma < (uint32_t)kK;  // a-1 < K: covered during this block
       if (hasB) front[cB * g.nbands + bB] = mb < (uint32_t)kK;
     }
     gmin = min(gmin, min(ma, hasB ? mb : ma));
   }
-  if ((threadIdx.x & 31) == 0 && gmin != 0xFFFFFFFFu) atomicMin(flag, gmin);
+  if (lane == 0 && gmin != 0xFFFFFFFFu) atomicMin(flag, gmin);
 }
 
 // ------------------------------------------------- active-tile bookkeeping
@@ -486,12 +513,10 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
 // most kK hops from a cell covered in the last layer of block b, and tiles
 // are at least kK cells in both directions, so only tiles whose 3x3 tile
 // neighbourhood holds a frontier cell (covered during block b) can change
-// coverage in block b+1.  Every other tile is "quiet": its covered cells
-// just gain +1 per layer, which is applied lazily (ell[t] = layer of the
-// stored values).  Invariant: a tile not processed in the previous block
-// holds identical data in both ping-pong fields.
+// coverage in block b+1.  Every other tile is quiet: its covered cells just
+// gain +1 per layer, applied lazily through its state (layer of the stored
+// values + home field).
 
-// Adds lag to every covered cell (flag set, a > 0) of tile t in `val`.
 // Covered cells (flag set, a > 0) are exactly the halves above the bare flag:
 // adds `lagw` (per-half lag) to them, leaving uncovered and obstacle cells.
 template <int CB>
@@ -500,7 +525,46 @@ __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
   else return w + (w > kFlag32 ? lagw : 0u);
 }
 
-// 16 B per lane-row: 8 cells (u16) or 4 cells (u32, two chunks per lane)
+// One lane per tile: the next block's state (active tiles advance by kk and
+// flip home), the work list (one atomic per warp).  Block 0 also resets the
+// next block's work counter and this block's fixed-point slot.
+__global__ void k_tiles_plan(Geo g, const uint8_t* __restrict__ front_prev, uint8_t* __restrict__ front_next,
+                             const uint32_t* __restrict__ state, uint32_t* __restrict__ state_next, uint32_t kk,
+                             uint32_t* __restrict__ list, uint32_t* __restrict__ count,
+                             uint32_t* __restrict__ next_count, uint32_t* __restrict__ flag,
+                             unsigned long long* __restrict__ processed, uint32_t l0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *next_count = 0;
+    if (flag) *flag = 0xFFFFFFFFu;
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool act = false;
+  if (t < g.ntiles()) {
+    const int chunk = (int)(t / g.nbands), band = (int)(t % g.nbands);
+#pragma unroll
+    for (int dr = -1; dr <= 1; ++dr)
+#pragma unroll
+      for (int dc = -1; dc <= 1; ++dc) {
+        const int c = chunk + dr, b = band + dc;
+        if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands)
+          act |= front_prev[(uint32_t)c * g.nbands + (uint32_t)b] != 0;
+      }
+    const uint32_t s = state[t];
+    state_next[t] = act ? (((l0 + kk) << 1) | ((s & 1u) ^ 1u)) : s;
+    front_next[t] = 0;
+  }
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  uint32_t base = 0;
+  if (lane == 0 && am) {
+    base = atomicAdd(count, (uint32_t)__popc(am));
+    atomicAdd(processed, (unsigned long long)__popc(am));
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (act) list[base + __popc(am & ((1u << lane) - 1u))] = (t % g.nbands) << 16 | (t / g.nbands);
+}
+
+// 16 B per lane-row: 8 cells (u16) or 4 cells (u32)
 template <int CB, typename F>
 __device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, uint32_t chunk, F f) {
   const int lane = threadIdx.x & 31;
@@ -512,111 +576,33 @@ __device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, u
   }
 }
 
-// Adds lag to every covered cell of one tile (whole tile, 16 B accesses).
+// Gathers every tile at layer l into field `dst` (f0 or f0+delta): values from
+// the tile's home plus its lag.  One warp per tile.  Afterwards all tiles are
+// current in dst (state = l << 1 | dst).
 template <int CB>
-__device__ void tile_catch_up(const Geo& g, typename Cell<CB>::T* val, uint32_t band, uint32_t chunk, uint32_t lag) {
-  const uint32_t lagw = CB == 16 ? (lag | lag << 16) : lag;
-  tile_rows_foreach<CB>(g, band, chunk, [&](size_t i) {
-    uint4* p = reinterpret_cast<uint4*>(val + i);
-    uint4 v = *p;
-    v.x = add_lag<CB>(v.x, lagw);
-    v.y = add_lag<CB>(v.y, lagw);
-    v.z = add_lag<CB>(v.z, lagw);
-    v.w = add_lag<CB>(v.w, lagw);
-    *p = v;
-  });
-}
-
-template <int CB>
-__device__ void tile_copy(const Geo& g, const typename Cell<CB>::T* src, typename Cell<CB>::T* dst, uint32_t band,
-                          uint32_t chunk) {
-  tile_rows_foreach<CB>(g, band, chunk, [&](size_t i) {
-    *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(src + i);
-  });
-}
-
-// One lane per tile (a warp covers 32 consecutive tiles): decides each
-// tile's role for the next block of kk layers starting at layer l0 (X =
-// current field, Y = the other one), appends active tiles to the work list
-// with one atomic per warp, then the whole warp performs the few catch-ups
-// (tile becoming active) and copies (tile leaving the active set).  Quiet
-// neighbours stay lagged: the block kernel adds their lag to the halo it
-// reads (stream_item LAG).  Block 0 also resets the next block's work
-// counter and this block's fixed-point slot, so no memset is issued.
-template <int CB>
-__global__ void k_tiles_plan(Geo g, const uint8_t* __restrict__ front_prev, uint8_t* __restrict__ front_next,
-                             uint8_t* __restrict__ was_active, uint32_t* __restrict__ ell,
-                             typename Cell<CB>::T* __restrict__ X, typename Cell<CB>::T* __restrict__ Y, uint32_t l0,
-                             uint32_t kk, uint32_t* __restrict__ list, uint32_t* __restrict__ count,
-                             uint32_t* __restrict__ next_count, uint32_t* __restrict__ flag,
-                             unsigned long long* __restrict__ processed, uint2* __restrict__ fixes,
-                             uint32_t* __restrict__ fix_count, uint32_t* __restrict__ next_fix_count) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *next_count = 0;
-    *next_fix_count = 0;
-    if (flag) *flag = 0xFFFFFFFFu;
-  }
-  const int lane = threadIdx.x & 31;
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t nt = g.ntiles();
-  bool act = false, prev = false;
-  uint32_t e = 0;
-  if (t < nt) {
-    const int chunk = (int)(t / g.nbands), band = (int)(t % g.nbands);
-#pragma unroll
-    for (int dr = -1; dr <= 1; ++dr)
-#pragma unroll
-      for (int dc = -1; dc <= 1; ++dc) {
-        const int c = chunk + dr, b = band + dc;
-        if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands)
-          act |= front_prev[(uint32_t)c * g.nbands + (uint32_t)b] != 0;
-      }
-    e = ell[t];
-    prev = was_active[t] != 0;
-    front_next[t] = 0;
-    was_active[t] = act;
-    if (act) ell[t] = l0 + kk;
-  }
-  const uint32_t am = __ballot_sync(0xffffffffu, act);
-  uint32_t base = 0;
-  if (lane == 0 && am) {
-    base = atomicAdd(count, (uint32_t)__popc(am));
-    atomicAdd(processed, (unsigned long long)__popc(am));
-  }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (act) list[base + __popc(am & ((1u << lane) - 1u))] = (t % g.nbands) << 16 | (t / g.nbands);
-  // fix items: (tile, lag) = catch-up of a tile becoming active; (tile, 0) = copy of one leaving
-  const bool needs = (act && e < l0) || (!act && prev);
-  const uint32_t fm = __ballot_sync(0xffffffffu, needs);
-  uint32_t fbase = 0;
-  if (lane == 0 && fm) fbase = atomicAdd(fix_count, (uint32_t)__popc(fm));
-  fbase = __shfl_sync(0xffffffffu, fbase, 0);
-  if (needs) fixes[fbase + __popc(fm & ((1u << lane) - 1u))] = make_uint2(t, act ? l0 - e : 0u);
-}
-
-// One warp per fix item (persistent grid-stride over the planner's list).
-template <int CB>
-__global__ void k_tiles_fix(Geo g, typename Cell<CB>::T* __restrict__ X, typename Cell<CB>::T* __restrict__ Y,
-                            const uint2* __restrict__ fixes, uint32_t* __restrict__ fix_count) {
-  const uint32_t n = *fix_count;
-  const uint32_t nw = gridDim.x * (blockDim.x / 32);
-  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += nw) {
-    const uint2 f = fixes[i];
-    if (f.y) tile_catch_up<CB>(g, X, f.x % g.nbands, f.x / g.nbands, f.y);
-    else tile_copy<CB>(g, X, Y, f.x % g.nbands, f.x / g.nbands);
-  }
-}
-
-// Brings every lagging tile of `val` to layer l (before dense work, the
-// fixed-point check, downloads and path tracing).
-template <int CB>
-__global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ ell, typename Cell<CB>::T* __restrict__ val, uint32_t l) {
+__global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ state, typename Cell<CB>::T* __restrict__ f0,
+                                 ptrdiff_t delta, uint32_t dst, uint32_t l) {
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= g.ntiles()) return;
-  const uint32_t e = ell[t];
-  if (e < l) tile_catch_up<CB>(g, val, t % g.nbands, t / g.nbands, l - e);
+  const uint32_t s = state[t], home = s & 1u, e = s >> 1;
+  if (e != l || home != dst) {
+    const uint32_t lag = l - e;
+    const uint32_t lagw = CB == 16 ? (lag | lag << 16) : lag;
+    const typename Cell<CB>::T* src = f0 + (home ? delta : 0);
+    typename Cell<CB>::T* out = f0 + (dst ? delta : 0);
+    tile_rows_foreach<CB>(g, t % g.nbands, t / g.nbands, [&](size_t i) {
+      uint4 v = *reinterpret_cast<const uint4*>(src + i);
+      if (lag) {
+        v.x = add_lag<CB>(v.x, lagw);
+        v.y = add_lag<CB>(v.y, lagw);
+        v.z = add_lag<CB>(v.z, lagw);
+        v.w = add_lag<CB>(v.w, lagw);
+      }
+      *reinterpret_cast<uint4*>(out + i) = v;
+    });
+  }
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) ell[t] = l;
+  if ((threadIdx.x & 31) == 0) state[t] = l << 1 | dst;
 }
 
 // Layer-0 frontier: every tile holding a source (a = 1 at layer 0).
@@ -809,43 +795,42 @@ void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cud
   k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, front);
 }
 
-// counters[0..1]: work-list lengths, counters[2..3]: fix-list lengths (alternating per block)
-void launch_tiles_plan(const Geo& g, int cb, const uint8_t* front_prev, uint8_t* front_next, uint8_t* was,
-                       uint32_t* ell, void* X, void* Y, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters,
-                       int parity, uint32_t* flag, unsigned long long* processed, uint2* fixes, int fix_ctas,
-                       cudaStream_t s) {
+// counters[0..1]: work-list lengths (alternating per block); states[parity]
+// holds the tile states at l0, states[parity^1] receives the next ones.
+void launch_tiles_plan(const Geo& g, const uint8_t* front_prev, uint8_t* front_next, uint32_t* const states[2],
+                       int parity, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters, uint32_t* flag,
+                       unsigned long long* processed, cudaStream_t s) {
   const uint32_t n = g.ntiles();
-  const uint32_t blocks = (n + 255) / 256;
-  uint32_t *cnt = counters + parity, *ncnt = counters + (parity ^ 1);
-  uint32_t *fcnt = counters + 2 + parity, *nfcnt = counters + 2 + (parity ^ 1);
+  k_tiles_plan<<<(n + 255) / 256, 256, 0, s>>>(g, front_prev, front_next, states[parity], states[parity ^ 1], kk, list,
+                                               counters + parity, counters + (parity ^ 1), flag, processed, l0);
+}
+
+// f0/f1: the two fields; state: tile states at l0
+void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
+                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
+                        const uint32_t* state, uint32_t l0, uint32_t* flag, cudaStream_t s) {
   if (cb == 16) {
-    k_tiles_plan<16><<<blocks, 256, 0, s>>>(g, front_prev, front_next, was, ell, (uint16_t*)X, (uint16_t*)Y, l0, kk,
-                                            list, cnt, ncnt, flag, processed, fixes, fcnt, nfcnt);
-    k_tiles_fix<16><<<fix_ctas, 256, 0, s>>>(g, (uint16_t*)X, (uint16_t*)Y, fixes, fcnt);
+    auto* a = (uint16_t*)f0;
+    k_block_tiles<16><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, list, count,
+                                                              front, state, l0, flag);
   } else {
-    k_tiles_plan<32><<<blocks, 256, 0, s>>>(g, front_prev, front_next, was, ell, (uint32_t*)X, (uint32_t*)Y, l0, kk,
-                                            list, cnt, ncnt, flag, processed, fixes, fcnt, nfcnt);
-    k_tiles_fix<32><<<fix_ctas, 256, 0, s>>>(g, (uint32_t*)X, (uint32_t*)Y, fixes, fcnt);
+    auto* a = (uint32_t*)f0;
+    k_block_tiles<32><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, list, count,
+                                                              front, state, l0, flag);
   }
 }
 
-void launch_block_tiles(const Geo& g, int cb, int ctas, const void* in, void* out, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
-                        const uint32_t* ell, uint32_t l0, uint32_t* flag, cudaStream_t s) {
-  if (cb == 16)
-    k_block_tiles<16><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, (const uint16_t*)in, (uint16_t*)out, srcmask, rowsrc,
-                                                              list, count, front, ell, l0, flag);
-  else
-    k_block_tiles<32><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, (const uint32_t*)in, (uint32_t*)out, srcmask, rowsrc,
-                                                              list, count, front, ell, l0, flag);
-}
-
-void launch_tiles_finalize(const Geo& g, int cb, uint32_t* ell, void* val, uint32_t l, cudaStream_t s) {
+// every tile to layer l in field dst (0 = f0, 1 = f1)
+void launch_tiles_finalize(const Geo& g, int cb, uint32_t* state, void* f0, void* f1, int dst, uint32_t l,
+                           cudaStream_t s) {
   const uint32_t n = g.ntiles();
-  if (cb == 16)
-    k_tiles_finalize<16><<<(n + 3) / 4, 128, 0, s>>>(g, ell, (uint16_t*)val, l);
-  else
-    k_tiles_finalize<32><<<(n + 3) / 4, 128, 0, s>>>(g, ell, (uint32_t*)val, l);
+  if (cb == 16) {
+    auto* a = (uint16_t*)f0;
+    k_tiles_finalize<16><<<(n + 3) / 4, 128, 0, s>>>(g, state, a, (uint16_t*)f1 - a, (uint32_t)dst, l);
+  } else {
+    auto* a = (uint32_t*)f0;
+    k_tiles_finalize<32><<<(n + 3) / 4, 128, 0, s>>>(g, state, a, (uint32_t*)f1 - a, (uint32_t)dst, l);
+  }
 }
 
 int block_kernel_blocks_per_sm(int cb) {
