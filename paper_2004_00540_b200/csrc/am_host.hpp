@@ -55,7 +55,7 @@ struct am_grid {
   int slab = 0;
   uint32_t total_h = 0, row0 = 0;
   // active-tile skipping state (single grids; stencil.cu k_tiles_*)
-  uint8_t* t_front[2] = {nullptr, nullptr};  // frontier flags: [t_fi] = last block, [t_fi^1] = being written
+  uint16_t* t_front[2] = {nullptr, nullptr}; // frontier region bits: [t_fi] = last block, [t_fi^1] = being written
   int t_fi = 0;
   uint32_t* t_state[2] = {nullptr, nullptr}; // per tile: layer << 1 | home field; [t_si] = current
   int t_si = 0;

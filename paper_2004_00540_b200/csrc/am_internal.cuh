@@ -71,12 +71,12 @@ void launch_block(const Geo& g, int cell_bits, bool slab, const void* in, void* 
 void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
                   uint32_t* flag, cudaStream_t s);
 // active-tile skipping (stencil.cu)
-void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cudaStream_t s);
-void launch_tiles_plan(const Geo& g, const uint8_t* front_prev, uint8_t* front_next, uint32_t* const states[2],
+void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint16_t* front, cudaStream_t s);
+void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front_next, uint32_t* const states[2],
                        int parity, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters, uint32_t* flag,
                        unsigned long long* processed, cudaStream_t s);
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
+                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
                         const uint32_t* state, uint32_t l0, uint32_t* flag, cudaStream_t s);
 void launch_tiles_finalize(const Geo& g, int cell_bits, uint32_t* state, void* f0, void* f1, int dst, uint32_t l,
                            cudaStream_t s);

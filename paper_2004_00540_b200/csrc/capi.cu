@@ -158,8 +158,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   for (int i = 0; !e && i < kFlagSlots; ++i) e = cudaEventCreateWithFlags(&g->flag_ev[i], cudaEventDisableTiming);
   if (!slab) {  // active-tile skipping state
     const size_t nt = g->g.ntiles();
-    if (!e) e = cudaMalloc(&g->t_front[0], nt);
-    if (!e) e = cudaMalloc(&g->t_front[1], nt);
+    if (!e) e = cudaMalloc(&g->t_front[0], nt * 2);
+    if (!e) e = cudaMalloc(&g->t_front[1], nt * 2);
     if (!e) e = cudaMalloc(&g->t_state[0], nt * 4);
     if (!e) e = cudaMalloc(&g->t_state[1], nt * 4);
     if (!e) e = cudaMalloc(&g->t_list, nt * 4);
@@ -348,7 +348,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   const int tile_ctas = ctx->sms * 2;  // persistent: k_block_tiles is sized for 2 CTAs per SM
   // after dense work: every tile current at at_layer in val[cur], all active next block
   auto tiles_all_active = [&](uint32_t at_layer) -> am_status {
-    CK(cudaMemsetAsync(tg->t_front[tg->t_fi], 1, nt, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_front[tg->t_fi], 0xFF, nt * 2, ctx->stream));
     std::vector<uint32_t> e(nt, at_layer << 1 | (uint32_t)tg->cur);
     CK(cudaMemcpyAsync(tg->t_state[tg->t_si], e.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -366,7 +366,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     tg->t_fi = 0;
     tg->t_si = 0;
     CK(cudaMemsetAsync(tg->t_state[0], 0, nt * 4, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_front[1], 0, nt, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_front[1], 0, nt * 2, ctx->stream));
     CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
     CK(cudaMemsetAsync(tg->t_count, 0, 8, ctx->stream));
     launch_tiles_init(tg->g, tg->srcmask, tg->t_front[0], ctx->stream);

@@ -57,6 +57,7 @@ struct Cell<16> {
     uint32_t lo = acc & 0xFFFFu, hi = acc >> 16;
     return lo < hi ? lo : hi;
   }
+  __device__ __forceinline__ static uint32_t vmin(uint32_t a, uint32_t b) { return __vminu2(a, b); }
 };
 
 template <>
@@ -70,6 +71,7 @@ struct Cell<32> {
     return __viaddmin_u32(v, 0x7FFFFFFFu, acc);
   }
   __device__ __forceinline__ static uint32_t fold(uint32_t acc) { return acc; }
+  __device__ __forceinline__ static uint32_t vmin(uint32_t a, uint32_t b) { return a < b ? a : b; }
 };
 
 // ------------------------------------------------------------- init / misc
@@ -311,7 +313,8 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
                                                 const uint8_t* __restrict__ rowsrc, uint32_t bA, uint32_t rA,
                                                 uint32_t bB, uint32_t rB, uint32_t rows, bool hasB,
                                                 uint32_t lag0 = 0, uint32_t lag1 = 0, uint32_t lag2 = 0,
-                                                ptrdiff_t delta = 0, uint32_t homes = 0) {
+                                                ptrdiff_t delta = 0, uint32_t homes = 0, uint32_t* edge_min = nullptr) {
+  uint32_t accTop = 0xFFFFFFFFu, accBot = 0xFFFFFFFFu;  // LAG: minima over the first / last kK output rows
   using C = Cell<CB>;
   using T = typename C::T;
   const int lane = threadIdx.x & 31;
@@ -404,7 +407,16 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
         else stream_step<CB, 1, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
       }
       if (tt >= 2 * kK && tt < 2 * kK + rows && store_lane) {
-        if constexpr (!SLAB) {
+        if constexpr (LAG) {  // also track the first / last kK output rows (tile edge regions)
+          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
+          uint32_t rm = 0xFFFFFFFFu;
+#pragma unroll
+          for (int w = 0; w < kWPL; ++w) rm = C::acc_min(x[w], rm);
+          acc = C::vmin(acc, rm);
+          const uint32_t orow = tt - 2 * kK;
+          if (orow < (uint32_t)kK) accTop = C::vmin(accTop, rm);
+          if (orow >= rows - kK) accBot = C::vmin(accBot, rm);
+        } else if constexpr (!SLAB) {
           Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
 #pragma unroll
           for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
@@ -420,6 +432,10 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (LAG) {
+    edge_min[0] = accTop;
+    edge_min[1] = accBot;
+  }
   return acc;
 }
 
@@ -454,7 +470,7 @@ template <int CB>
 __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: registers over occupancy
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
                   const uint8_t* __restrict__ rowsrc, const uint32_t* __restrict__ list,
-                  const uint32_t* __restrict__ count, uint8_t* __restrict__ front, const uint32_t* __restrict__ state,
+                  const uint32_t* __restrict__ count, uint16_t* __restrict__ front, const uint32_t* __restrict__ state,
                   uint32_t l0, uint32_t* __restrict__ flag) {
   const uint32_t n = *count;
   const uint32_t per = CB == 16 ? 2u : 1u;
@@ -488,9 +504,28 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
     // own rows go to the field that is not the tile's home
     const uint32_t sa = state[cA * g.nbands + bA], sb = state[cB * g.nbands + bB];
     homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
+    uint32_t edge[2];
     const uint32_t acc = stream_item<CB, false, true>(g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB,
                                                       cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2], delta,
-                                                      homes);
+                                                      homes, edge);
+    // Frontier regions of each tile: cells with a == 1 (covered in the block's
+    // last layer; min(a-1) == 0) anywhere / in the first or last kK rows / in
+    // the first (lane 1) or last (lane 30) kK useful columns / the corners.
+    auto regions = [&](int half) -> uint32_t {
+      auto h = [&](uint32_t v) { return CB == 16 ? (half ? v >> 16 : v & 0xFFFFu) : v; };
+      const uint32_t vals[9] = {
+          acc, edge[0], edge[1], __shfl_sync(0xffffffffu, acc, 1), __shfl_sync(0xffffffffu, acc, 30),
+          __shfl_sync(0xffffffffu, edge[0], 1), __shfl_sync(0xffffffffu, edge[0], 30),
+          __shfl_sync(0xffffffffu, edge[1], 1), __shfl_sync(0xffffffffu, edge[1], 30)};
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const uint32_t v = k < 3 ? __reduce_min_sync(0xffffffffu, h(vals[k])) : h(vals[k]);
+        m |= (v == 0u ? 1u : 0u) << k;
+      }
+      return m;
+    };
+    const uint32_t fa = regions(0), fb = CB == 16 ? regions(1) : fa;
     uint32_t ma, mb;
     if (CB == 16) {
       ma = __reduce_min_sync(0xffffffffu, acc & 0xFFFFu);
@@ -499,8 +534,8 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
       ma = mb = __reduce_min_sync(0xffffffffu, acc);
     }
     if (lane == 0) {
-      front[cA * g.nbands + bA] = ma < (uint32_t)kK;  // a-1 < K: covered during this block
-      if (hasB) front[cB * g.nbands + bB] = mb < (uint32_t)kK;
+      front[cA * g.nbands + bA] = (uint16_t)fa;
+      if (hasB) front[cB * g.nbands + bB] = (uint16_t)fb;
     }
     gmin = min(gmin, min(ma, hasB ? mb : ma));
   }
@@ -525,10 +560,15 @@ __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
   else return w + (w > kFlag32 ? lagw : 0u);
 }
 
+// Frontier-region bit a neighbour N at (dr, dc) from tile T must have for T
+// to become active: a frontier cell within kK of T lies in N's region facing
+// T (bits: 0 any, 1 top, 2 bottom, 3 left, 4 right, 5 tl, 6 tr, 7 bl, 8 br).
+__constant__ uint8_t kFacing[3][3] = {{8, 2, 7}, {4, 0, 3}, {6, 1, 5}};
+
 // One lane per tile: the next block's state (active tiles advance by kk and
 // flip home), the work list (one atomic per warp).  Block 0 also resets the
 // next block's work counter and this block's fixed-point slot.
-__global__ void k_tiles_plan(Geo g, const uint8_t* __restrict__ front_prev, uint8_t* __restrict__ front_next,
+__global__ void k_tiles_plan(Geo g, const uint16_t* __restrict__ front_prev, uint16_t* __restrict__ front_next,
                              const uint32_t* __restrict__ state, uint32_t* __restrict__ state_next, uint32_t kk,
                              uint32_t* __restrict__ list, uint32_t* __restrict__ count,
                              uint32_t* __restrict__ next_count, uint32_t* __restrict__ flag,
@@ -548,7 +588,7 @@ __global__ void k_tiles_plan(Geo g, const uint8_t* __restrict__ front_prev, uint
       for (int dc = -1; dc <= 1; ++dc) {
         const int c = chunk + dr, b = band + dc;
         if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands)
-          act |= front_prev[(uint32_t)c * g.nbands + (uint32_t)b] != 0;
+          act |= (front_prev[(uint32_t)c * g.nbands + (uint32_t)b] >> kFacing[dr + 1][dc + 1]) & 1u;
       }
     const uint32_t s = state[t];
     state_next[t] = act ? (((l0 + kk) << 1) | ((s & 1u) ^ 1u)) : s;
@@ -606,7 +646,7 @@ __global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ state, typename C
 }
 
 // Layer-0 frontier: every tile holding a source (a = 1 at layer 0).
-__global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint8_t* __restrict__ front) {
+__global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint16_t* __restrict__ front) {
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= g.ntiles()) return;
   const int lane = threadIdx.x & 31;
@@ -619,7 +659,7 @@ __global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint8_t
       any |= (m.x | m.y) != 0;
     }
   any = __any_sync(0xffffffffu, any);
-  if (lane == 0) front[t] = any;
+  if (lane == 0) front[t] = any ? 0x1FFu : 0u;  // every region (conservative)
 }
 
 // -------------------------------------------------------- single layer
@@ -790,14 +830,14 @@ void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, co
     k_block<32, true><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
 }
 
-void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint8_t* front, cudaStream_t s) {
+void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint16_t* front, cudaStream_t s) {
   const uint32_t n = g.ntiles();
   k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, front);
 }
 
 // counters[0..1]: work-list lengths (alternating per block); states[parity]
 // holds the tile states at l0, states[parity^1] receives the next ones.
-void launch_tiles_plan(const Geo& g, const uint8_t* front_prev, uint8_t* front_next, uint32_t* const states[2],
+void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front_next, uint32_t* const states[2],
                        int parity, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters, uint32_t* flag,
                        unsigned long long* processed, cudaStream_t s) {
   const uint32_t n = g.ntiles();
@@ -807,7 +847,7 @@ void launch_tiles_plan(const Geo& g, const uint8_t* front_prev, uint8_t* front_n
 
 // f0/f1: the two fields; state: tile states at l0
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint8_t* front,
+                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
                         const uint32_t* state, uint32_t l0, uint32_t* flag, cudaStream_t s) {
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
