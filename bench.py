@@ -34,6 +34,8 @@ N_SOURCES, N_TARGETS, PT_SEED = 64, 4096, 4
 AUTO_CAP = 4 * max(W, H)
 BYTES_PER_CELL_UPDATE = 9  # 4 B read + 4 B write of uint32 activity + 1 B mask (activity.hpp:51, grid.hpp:56)
 LAYERS_PER_BLOCK = 8       # am::kK
+TILE_ROWS, TILE_COLS = 64, 240  # am::kTileRows x am::kBandUseful (active-tile mode)
+TILE_CELLS = TILE_ROWS * TILE_COLS
 
 
 def log(*a):
@@ -75,13 +77,12 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per block launch from the committed ncu capture, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_block_summary.json")
+def ncu_traffic(kind):
+    """dram bytes (read + write) per launch of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+            return json.load(f).get(kind, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -314,11 +315,13 @@ def run_b200(args, rank, world, local_rank):
     ctx.synchronize()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    stencil_ms, blocks, res = 0.0, 0, None
+    stencil_ms, blocks, res, tiles_done, tiles_all = 0.0, 0, None, 0, 0
     for _ in range(args.steps):
         res = sol.step()
         stencil_ms += res.stencil_ms
         blocks += res.block_launches
+        tiles_done += res.tiles_processed
+        tiles_all += res.tiles_total
     t_end.record(stream)
     ctx.synchronize()
     torch.cuda.synchronize()
@@ -337,13 +340,38 @@ def run_b200(args, rank, world, local_rank):
     cell_updates = W * H * L
     value = cell_updates / (ms_step / 1000) / 1e9  # whole job: the full grid's cell-updates per second
 
-    # roofline of the dominant kernel (k_block): algorithmic bytes per launch / mean launch time
+    # roofline of the dominant kernel: algorithmic bytes per launch / mean launch time (CUDA events around every
+    # stencil launch on the library stream, inside the timed steps).  Active-tile mode: the launch is the tile
+    # planner + k_block_tiles and its work is the executed (useful) cell-updates of the processed tiles.
     peak, peak_src = peaks()
     rows_here = (sol.slab.height if sol.slab is not None else H)
     per_launch_ms = stencil_ms / max(blocks, 1)
-    alg_bytes = BYTES_PER_CELL_UPDATE * W * rows_here * LAYERS_PER_BLOCK
+    tile_mode = tiles_all > 0
+    if tile_mode:
+        cells_per_launch = tiles_done * TILE_CELLS * LAYERS_PER_BLOCK / max(blocks, 1)
+        kernel = "am::k_tiles_plan + am::k_block_tiles<16>"
+    else:
+        cells_per_launch = W * rows_here * LAYERS_PER_BLOCK
+        kernel = "am::k_block<16>"
+    alg_bytes = BYTES_PER_CELL_UPDATE * cells_per_launch
     achieved = alg_bytes / (per_launch_ms / 1000) / 1e9
-    stencil_gcells = W * rows_here * LAYERS_PER_BLOCK / (per_launch_ms / 1000) / 1e9
+    stencil_gcells = cells_per_launch / (per_launch_ms / 1000) / 1e9
+    # the dense sweep (every tile every block) measured on its own: a fixed-L run of the plain k_block
+    dense = None
+    if rank == 0 and world == 1:
+        dctx = am.Context(local_rank, timing=True, dense=True)
+        dg = am.Grid(occ, src, dctx)
+        best = None
+        for _ in range(3):
+            rr = dg.propagate(64)
+            ms = rr.stencil_ms / max(rr.block_launches, 1)
+            best = ms if best is None else min(best, ms)
+        dg.close()
+        dbytes = BYTES_PER_CELL_UPDATE * W * H * LAYERS_PER_BLOCK
+        dense = {"kernel": "am::k_block<16> (dense, fixed L=64 on the C4 grid)", "mean_launch_ms": round(best, 4),
+                 "gcell_per_s": round(W * H * LAYERS_PER_BLOCK / (best / 1000) / 1e9, 1),
+                 "achieved": round(dbytes / (best / 1000) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                 "frac": round(dbytes / (best / 1000) / 1e9 / peak, 3), "traffic": ncu_traffic("dense")}
 
     # end-to-end through the C ABI with host buffers (H2D of the grid, D2H of map + paths inside the timing)
     e2e = None
@@ -397,11 +425,15 @@ def run_b200(args, rank, world, local_rank):
                          "path_share": round(path_ms / max(prop_ms + path_ms, 1e-9), 4)},
             "stencil_gcell_per_s": round(stencil_gcells, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 3), "traffic": ncu_traffic(),
-                         "kernel": "am::k_block<16>", "algorithmic_bytes_per_launch": alg_bytes,
+                         "frac": round(achieved / peak, 3), "traffic": ncu_traffic("tiles" if tile_mode else "dense"),
+                         "kernel": kernel, "algorithmic_bytes_per_launch": int(alg_bytes),
                          "mean_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src,
-                         "note": "9 B per cell-update (reference uint32 layout) x W*rows x 8 layers per launch; "
-                                 "traffic = ncu dram read+write per launch (profiles/)"},
+                         "note": "9 B per cell-update (reference uint32 layout) x executed cell-updates per launch "
+                                 "(8 layers); traffic = ncu dram read+write per launch (profiles/)"},
+            "active_tiles": ({"processed": tiles_done // args.steps, "dense_equivalent": tiles_all // args.steps,
+                              "fraction": round(tiles_done / max(tiles_all, 1), 4),
+                              "tile": f"{TILE_ROWS} rows x {TILE_COLS} cols"} if tile_mode else None),
+            "dense_stencil": dense,
             "gpu_launches": int(launches),
             "clocks": clk,
             "e2e": e2e,

@@ -1,10 +1,9 @@
 #!/bin/bash
 # One gpurun session: parity tests, bench, then ncu evidence for the bench's
-# dominant kernel.  Usage (from the repo root, on the GPU box):
+# kernels.  Usage (from the repo root, on the GPU box):
 #   bash tools/gpu_session.sh [tests] [bench] [ncu] [probe]
 set -u
 mkdir -p gpurun_out
-want() { [[ " $* " == *" $1 "* ]]; }
 ARGS=" $* "
 if [[ "$ARGS" == *" probe "* ]]; then
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/ipc_probe tools/ipc_probe.cu && timeout 120 /tmp/ipc_probe > gpurun_out/ipc_probe.txt 2>&1
@@ -22,8 +21,9 @@ if [[ "$ARGS" == *" ncu "* ]]; then
   CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
   timeout 300 $CMD > gpurun_out/plain.log 2>&1; rc=$?; echo "plain_rc=$rc"
   if [ $rc -eq 0 ]; then
-    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo "ncu_list_rc=$?"
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_block -s 30 -c 1 -o gpurun_out/prof_block -f $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu_full_rc=$?"
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 2200 -c 2000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo "ncu_list_rc=$?"
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_block_tiles -s 300 -c 1 -o gpurun_out/prof_tiles -f $CMD > gpurun_out/ncu_tiles.log 2>&1; echo "ncu_tiles_rc=$?"
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^k_block$' -s 2 -c 1 -o gpurun_out/prof_dense -f $CMD > gpurun_out/ncu_dense.log 2>&1; echo "ncu_dense_rc=$?"
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_trace -c 1 -o gpurun_out/prof_trace -f $CMD > gpurun_out/ncu_trace.log 2>&1; echo "ncu_trace_rc=$?"
   fi
 fi
