@@ -34,8 +34,6 @@ N_SOURCES, N_TARGETS, PT_SEED = 64, 4096, 4
 AUTO_CAP = 4 * max(W, H)
 BYTES_PER_CELL_UPDATE = 9  # 4 B read + 4 B write of uint32 activity + 1 B mask (activity.hpp:51, grid.hpp:56)
 LAYERS_PER_BLOCK = 8       # am::kK
-TILE_ROWS, TILE_COLS = 64, 240  # am::kTileRows x am::kBandUseful (active-tile mode)
-TILE_CELLS = TILE_ROWS * TILE_COLS
 
 
 def log(*a):
@@ -347,8 +345,9 @@ def run_b200(args, rank, world, local_rank):
     rows_here = (sol.slab.height if sol.slab is not None else H)
     per_launch_ms = stencil_ms / max(blocks, 1)
     tile_mode = tiles_all > 0
+    info = sol.full.info()
     if tile_mode:
-        cells_per_launch = tiles_done * TILE_CELLS * LAYERS_PER_BLOCK / max(blocks, 1)
+        cells_per_launch = tiles_done * info["tile_rows"] * info["tile_cols"] * LAYERS_PER_BLOCK / max(blocks, 1)
         kernel = "am::k_tiles_plan + am::k_block_tiles<16>"
     else:
         cells_per_launch = W * rows_here * LAYERS_PER_BLOCK
@@ -432,7 +431,7 @@ def run_b200(args, rank, world, local_rank):
                                  "(8 layers); traffic = ncu dram read+write per launch (profiles/)"},
             "active_tiles": ({"processed": tiles_done // args.steps, "dense_equivalent": tiles_all // args.steps,
                               "fraction": round(tiles_done / max(tiles_all, 1), 4),
-                              "tile": f"{TILE_ROWS} rows x {TILE_COLS} cols"} if tile_mode else None),
+                              "tile": f"{info['tile_rows']} rows x {info['tile_cols']} cols"} if tile_mode else None),
             "dense_stencil": dense,
             "gpu_launches": int(launches),
             "clocks": clk,

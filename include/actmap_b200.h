@@ -69,6 +69,7 @@ typedef struct am_prop_result {
 typedef struct am_grid_info {
   uint32_t width, height, pitch, rows, bands, segments, seg_len, halo;
   uint32_t cell_bits, layers_used, layers_computed;
+  uint32_t tile_rows, tile_cols, tiles; /* active-tile geometry (tiles = 0 for slab grids) */
 } am_grid_info;
 
 typedef struct am_stats {

@@ -50,7 +50,8 @@ class _PropResult(C.Structure):
 
 class _GridInfo(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in ("width", "height", "pitch", "rows", "bands", "segments", "seg_len",
-                                           "halo", "cell_bits", "layers_used", "layers_computed")]
+                                           "halo", "cell_bits", "layers_used", "layers_computed", "tile_rows",
+                                           "tile_cols", "tiles")]
 
 
 class _CtxOpts(C.Structure):

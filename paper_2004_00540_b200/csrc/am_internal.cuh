@@ -41,7 +41,10 @@ constexpr int kBandUseful = kBand - 2 * kK;
 constexpr int kBlockThreads = 128;
 
 // Active-tile skipping works on tiles of kTileRows rows x one band.
-constexpr int kTileRows = 64;
+#ifndef AM_TILE_ROWS
+#define AM_TILE_ROWS 32
+#endif
+constexpr int kTileRows = AM_TILE_ROWS;
 
 struct Geo {
   uint32_t W, H;          // grid extent (cells)

@@ -238,6 +238,9 @@ am_status am_grid_get_info(const am_grid* g, am_grid_info* o) {
   o->cell_bits = g->cell_bits;
   o->layers_used = g->layers_used;
   o->layers_computed = g->computed;
+  o->tile_rows = am::kTileRows;
+  o->tile_cols = am::kBandUseful;
+  o->tiles = g->t_state[0] ? g->g.ntiles() : 0;
   return AM_OK;
 }
 

@@ -262,10 +262,18 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 #ifndef AM_STAGES
 #define AM_STAGES 4
 #endif
-constexpr int kStages = AM_STAGES;                 // rows in flight per warp
+#ifndef AM_TILE_STAGES
+#define AM_TILE_STAGES 4
+#endif
+#ifndef AM_TILE_PAIR
+#define AM_TILE_PAIR 1
+#endif
+constexpr int kStages = AM_STAGES;                 // rows in flight per warp (dense sweep)
+constexpr int kTileStages = AM_TILE_STAGES;        // rows in flight per warp (active tiles: few warps per SM)
 constexpr int kStageBytes = kBand * 4;             // one u32 row, or the A+B pair of u16 rows
 constexpr int kWarpsPerCta = kBlockThreads / 32;
 constexpr int kBlockSmem = kWarpsPerCta * kStages * kStageBytes;
+constexpr int kTileSmem = kWarpsPerCta * kTileStages * kStageBytes;
 
 template <int CB>
 __device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint32_t (&x)[kWPL]) {
@@ -306,7 +314,7 @@ __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw);
 // `in + delta`; bit r of `homes` (r = 0 above, 1 inside, 2 below the item)
 // says tile A's region r is read from the second field, bits 3..5 the same
 // for B, bit 6 / 7 that A's / B's output goes to `out + delta`.
-template <int CB, bool SLAB, bool LAG = false>
+template <int CB, bool SLAB, bool LAG = false, int ST = kStages>
 __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cell<CB>::T* __restrict__ in,
                                                 typename Cell<CB>::T* __restrict__ out,
                                                 const uint8_t* __restrict__ srcmask,
@@ -344,9 +352,9 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
   // kStages-1 rows ahead without holding registers, and since no lane reads
   // another lane's slot no barrier or fence is needed.
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * kStages * kStageBytes;
+  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * ST * kStageBytes;
   auto issue = [&](uint32_t step) {
-    uint8_t* dst = ring + (step % kStages) * kStageBytes;
+    uint8_t* dst = ring + (step % ST) * kStageBytes;
     if (step < T_steps) {
       const size_t off = (size_t)step * pitch;
       const T* a = pA + off;
@@ -367,7 +375,7 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  for (int s = 0; s < ST - 1; ++s) issue(s);
   // source-row flags arrive as a 32-row ballot window, loaded one window ahead
   auto row_flag = [&](uint32_t step) -> uint32_t {
     if (step >= T_steps) return 0u;
@@ -385,9 +393,9 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     for (int ph = 0; ph < 2; ++ph) {
       const uint32_t tt = t + ph;
       uint32_t x[kWPL];
-      issue(tt + kStages - 1);  // refills the slot consumed by the previous step
-      asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
-      stage_words<CB>(ring + (tt % kStages) * kStageBytes, lane, x);
+      issue(tt + ST - 1);  // refills the slot consumed by the previous step
+      asm volatile("cp.async.wait_group %0;" ::"n"(ST - 1) : "memory");
+      stage_words<CB>(ring + (tt % ST) * kStageBytes, lane, x);
       if constexpr (LAG) {
         const uint32_t lw = tt < (uint32_t)kK ? lag0 : (tt < kK + rows ? lag1 : lag2);
         if (__any_sync(0xffffffffu, lw != 0u)) {
@@ -473,7 +481,9 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
                   const uint32_t* __restrict__ count, uint16_t* __restrict__ front, const uint32_t* __restrict__ state,
                   uint32_t l0, uint32_t* __restrict__ flag) {
   const uint32_t n = *count;
-  const uint32_t per = CB == 16 ? 2u : 1u;
+  // Pairing two tiles per warp halves the instructions but also the warps;
+  // with few active tiles the kernel is latency bound and more warps win.
+  const uint32_t per = (CB == 16 && AM_TILE_PAIR) ? 2u : 1u;
   const uint32_t nw = gridDim.x * (kBlockThreads / 32);
   const int lane = threadIdx.x & 31;
   const int brel = lane == 0 ? -1 : (lane == 31 ? 1 : 0);  // band this lane's cells belong to
@@ -490,7 +500,7 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
   uint32_t gmin = 0xFFFFFFFFu;
   for (uint32_t w = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5); w * per < n; w += nw) {
     const uint32_t ia = list[w * per];
-    const bool hasB = CB == 16 && w * per + 1 < n;
+    const bool hasB = per == 2u && w * per + 1 < n;
     const uint32_t ib = hasB ? list[w * per + 1] : ia;
     const uint32_t bA = ia >> 16, cA = ia & 0xFFFFu, bB = ib >> 16, cB = ib & 0xFFFFu;
     uint32_t lw[3], homes = 0;
@@ -505,7 +515,7 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
     const uint32_t sa = state[cA * g.nbands + bA], sb = state[cB * g.nbands + bB];
     homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
     uint32_t edge[2];
-    const uint32_t acc = stream_item<CB, false, true>(g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB,
+    const uint32_t acc = stream_item<CB, false, true, kTileStages>(g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB,
                                                       cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2], delta,
                                                       homes, edge);
     // Frontier regions of each tile: cells with a == 1 (covered in the block's
@@ -851,11 +861,11 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
                         const uint32_t* state, uint32_t l0, uint32_t* flag, cudaStream_t s) {
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
-    k_block_tiles<16><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, list, count,
+    k_block_tiles<16><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, list, count,
                                                               front, state, l0, flag);
   } else {
     auto* a = (uint32_t*)f0;
-    k_block_tiles<32><<<ctas, kBlockThreads, kBlockSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, list, count,
+    k_block_tiles<32><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, list, count,
                                                               front, state, l0, flag);
   }
 }
