@@ -28,6 +28,16 @@ struct Reader {
     }
     return static_cast<const uint32_t*>(m.val)[(size_t)r * m.g.W + c];
   }
+  // encoded fields only: (r, c) may lie up to the padding width outside the grid
+  __device__ __forceinline__ uint32_t value_pad(int r, int c) const {
+    const size_t i = (size_t)(r + (int)m.g.pad) * m.g.pitch + (size_t)(c + (int)m.g.pad);
+    if (m.cell_bits == 16) {
+      const uint32_t v = static_cast<const uint16_t*>(m.val)[i];
+      return (v & kFlag16) ? (v & 0x7FFFu) : 0u;
+    }
+    const uint32_t v = static_cast<const uint32_t*>(m.val)[i];
+    return (v & kFlag32) ? (v & kLow32) : 0u;
+  }
   __device__ __forceinline__ bool source(uint32_t r, uint32_t c) const {
     if (m.cell_bits) return m.srcmask[m.g.idx(r, c)] != 0;
     return m.srcmask[(size_t)r * m.g.W + c] != 0;
@@ -134,6 +144,126 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
   return n;
 }
 
+// Windowed walk for maps produced by the device propagation (encoded
+// fields): the warp loads the 7x7 window around the current cell (lane k
+// holds window cells k and k+32, row-major), takes up to three steps inside
+// it with votes and shuffles only (the 3x3 neighbourhood of any cell within
+// 2 of the centre lies in the window), then re-centres.  A cell is a source
+// exactly when its activity is L+1 (d = 0), so no source-mask load is
+// needed.  Candidate order is the window's row-major order restricted to
+// the 8 neighbours, i.e. the reference enumeration (pins P1/P2).
+__device__ uint64_t walk_window(const Reader& rd, uint32_t r, uint32_t c, int method, uint64_t seed, uint64_t limit,
+                                uint32_t* out, int32_t* st) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t top = rd.m.layers + 1;  // activity of a source
+  uint64_t rng = seed;
+  uint32_t cur = rd.value(r, c);
+  uint64_t n = 1;
+  if (lane == 0) {
+    out[0] = r;
+    out[1] = c;
+  }
+  const int k0 = lane, k1 = lane + 32;
+  const int r0 = k0 / 7 - 3, c0 = k0 % 7 - 3, r1 = k1 / 7 - 3, c1 = k1 % 7 - 3;
+  uint32_t wr = r, wc = c, v0 = 0, v1 = 0;
+  bool loaded = false;
+  while (cur != top) {
+    if (n >= limit) {
+      *st = ST_EINTERNAL;
+      return 0;
+    }
+    int pr = (int)r - (int)wr, pc = (int)c - (int)wc;
+    if (!loaded || pr < -2 || pr > 2 || pc < -2 || pc > 2) {
+      wr = r;
+      wc = c;
+      pr = pc = 0;
+      // pads are >= kK >= 3 cells wide and decode to 0, so the window never leaves the allocation
+      v0 = rd.value_pad((int)r + r0, (int)c + c0);
+      v1 = k1 < 49 ? rd.value_pad((int)r + r1, (int)c + c1) : 0u;
+      loaded = true;
+    }
+    int sel_r = 0, sel_c = 0;
+    uint32_t best = 0;
+    bool ok = false;
+    if (method == 0) {  // simple: 8-neighbour argmax, seeded tie-break (pin P2)
+      const int a0 = r0 - pr, b0 = c0 - pc, a1 = r1 - pr, b1 = c1 - pc;
+      const bool n0 = a0 >= -1 && a0 <= 1 && b0 >= -1 && b0 <= 1 && (a0 | b0) != 0;
+      const bool n1 = k1 < 49 && a1 >= -1 && a1 <= 1 && b1 >= -1 && b1 <= 1 && (a1 | b1) != 0;
+      best = __reduce_max_sync(0xffffffffu, max(n0 ? v0 : 0u, n1 ? v1 : 0u));
+      if (best > cur) {
+        uint32_t m0 = __ballot_sync(0xffffffffu, n0 && v0 == best);
+        uint32_t m1 = __ballot_sync(0xffffffffu, n1 && v1 == best);
+        const int cnt = __popc(m0) + __popc(m1);
+        int pick = 0;
+        if (cnt >= 2) pick = (int)__umul64hi(splitmix64(rng), (uint64_t)cnt);
+        int k;
+        if (pick < __popc(m0)) {
+          for (int i = 0; i < pick; ++i) m0 &= m0 - 1;
+          k = __ffs(m0) - 1;
+        } else {
+          for (int i = 0; i < pick - __popc(m0); ++i) m1 &= m1 - 1;
+          k = 32 + __ffs(m1) - 1;
+        }
+        sel_r = k / 7 - 3;
+        sel_c = k % 7 - 3;
+        ok = true;
+      }
+    } else {  // Euclidean: axis order L,R,U,D then diagonals (pin P1)
+      auto at = [&](int dr, int dc) -> uint32_t {
+        const int k = (pr + dr + 3) * 7 + (pc + dc + 3);
+        const uint32_t t0 = __shfl_sync(0xffffffffu, v0, k & 31), t1 = __shfl_sync(0xffffffffu, v1, k & 31);
+        return k < 32 ? t0 : t1;
+      };
+      const int ar[4] = {0, 0, -1, 1}, ac[4] = {-1, 1, 0, 0}, gr[4] = {-1, -1, 1, 1}, gc[4] = {-1, 1, -1, 1};
+      int bi = 0;
+      best = at(ar[0], ac[0]);
+#pragma unroll
+      for (int i = 1; i < 4; ++i) {
+        const uint32_t v = at(ar[i], ac[i]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+      if (best > cur) {
+        sel_r = pr + ar[bi];
+        sel_c = pc + ac[bi];
+        ok = true;
+      } else {
+        bi = 0;
+        best = at(gr[0], gc[0]);
+#pragma unroll
+        for (int i = 1; i < 4; ++i) {
+          const uint32_t v = at(gr[i], gc[i]);
+          if (v > best) {
+            best = v;
+            bi = i;
+          }
+        }
+        if (best > cur) {
+          sel_r = pr + gr[bi];
+          sel_c = pc + gc[bi];
+          ok = true;
+        }
+      }
+    }
+    if (!ok) {
+      *st = ST_EINTERNAL;  // no ascending neighbour
+      return 0;
+    }
+    r = (uint32_t)((int)wr + sel_r);
+    c = (uint32_t)((int)wc + sel_c);
+    cur = best;
+    if (lane == 0) {
+      out[2 * n] = r;
+      out[2 * n + 1] = c;
+    }
+    ++n;
+  }
+  if (!rd.source(r, c)) *st = ST_EINTERNAL;  // a non-source at the top value would violate the law
+  return n;
+}
+
 // Encoded maps: closed-form count L+2-A(t).  Plain maps: a counting walk.
 __global__ void k_path_counts(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method,
                               uint64_t seed, uint64_t* __restrict__ counts, int32_t* __restrict__ status) {
@@ -166,7 +296,9 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
   Reader rd{m};
   const uint64_t off = offsets[w], limit = offsets[w + 1] - off;
   int32_t st = ST_OK;
-  const uint64_t got = walk<true>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st);
+  const uint64_t got = m.cell_bits
+                           ? walk_window(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st)
+                           : walk<true>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st);
   if ((threadIdx.x & 31) == 0) {
     if (st != ST_OK) status[w] = st;
     else if (got != limit) status[w] = ST_EINTERNAL;
