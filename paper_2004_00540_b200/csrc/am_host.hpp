@@ -41,8 +41,9 @@ struct am_grid {
   uint8_t* rowsrc = nullptr;         // per allocated row: any source
   uint8_t* occ = nullptr;            // dense owned rows (re-initialisation / plain maps)
   uint8_t* srcmask_dense = nullptr;  // dense owned rows (plain maps)
-  uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots
-  uint32_t* h_flags = nullptr;       // pinned mirror
+  uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots + 1 CTA arrival counter (FlagSink::done)
+  uint32_t* h_flags = nullptr;       // pinned, device-mapped mirror
+  uint32_t* h_flags_dev = nullptr;   // its device address
   cudaEvent_t flag_ev[am::kFlagSlots];
   uint32_t* plain = nullptr;         // caller-uploaded dense map
   int plain_active = 0;

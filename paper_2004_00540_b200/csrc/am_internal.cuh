@@ -63,6 +63,17 @@ struct Geo {
 
 Geo make_geo(uint32_t W, uint32_t H, int num_sms);
 
+// Where a blocked launch leaves its fixed-point word (min over covered cells
+// of a-1): `word` is the device slot the warps atomicMin into.  With `host`
+// set, the last CTA to finish copies the word into that host-mapped pinned
+// slot and re-arms word (all ones) and `done` (0), so the driver reads the
+// signal after an event without a copy-engine op between launches.
+struct FlagSink {
+  uint32_t* word;
+  uint32_t* done;  // CTA arrival counter, 0 between launches
+  uint32_t* host;  // mapped mirror slot, or null (word left for the caller)
+};
+
 // ---- kernels (stencil.cu) ----
 void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcmask, void* d_val,
                  int cell_bits, cudaStream_t s);
@@ -70,7 +81,7 @@ void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const ui
                          uint8_t* d_dense, const uint8_t* d_occ, uint8_t* d_srcmask, uint8_t* d_rowsrc, int* d_err,
                          cudaStream_t s);
 void launch_block(const Geo& g, int cell_bits, bool slab, const void* in, void* out, const uint8_t* srcmask,
-                  const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s);
+                  const uint8_t* rowsrc, FlagSink flag, cudaStream_t s);
 void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
                   uint32_t* flag, cudaStream_t s);
 // active-tile skipping (stencil.cu)
@@ -80,7 +91,7 @@ void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front
                        unsigned long long* processed, cudaStream_t s);
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f1, const uint8_t* srcmask,
                         const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
-                        const uint32_t* state, uint32_t l0, uint32_t* flag, cudaStream_t s);
+                        const uint32_t* state, uint32_t l0, FlagSink flag, cudaStream_t s);
 void launch_tiles_finalize(const Geo& g, int cell_bits, uint32_t* state, void* f0, void* f1, int dst, uint32_t l,
                            cudaStream_t s);
 void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);

@@ -153,8 +153,9 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = cudaMalloc(&g->rowsrc, g->g.rows);
   if (!e) e = cudaMalloc(&g->occ, dense);
   if (!e) e = cudaMalloc(&g->srcmask_dense, dense);
-  if (!e) e = cudaMalloc(&g->d_flags, kFlagSlots * sizeof(uint32_t));
-  if (!e) e = cudaHostAlloc(&g->h_flags, kFlagSlots * sizeof(uint32_t), cudaHostAllocDefault);
+  if (!e) e = cudaMalloc(&g->d_flags, (kFlagSlots + 1) * sizeof(uint32_t));
+  if (!e) e = cudaHostAlloc(&g->h_flags, kFlagSlots * sizeof(uint32_t), cudaHostAllocMapped);
+  if (!e) e = cudaHostGetDevicePointer((void**)&g->h_flags_dev, g->h_flags, 0);
   for (int i = 0; !e && i < kFlagSlots; ++i) e = cudaEventCreateWithFlags(&g->flag_ev[i], cudaEventDisableTiming);
   if (!slab) {  // active-tile skipping state
     const size_t nt = g->g.ntiles();
@@ -170,6 +171,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = cudaMemsetAsync(g->val[1], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->srcmask, 0, cells, s);
   if (!e) e = cudaMemsetAsync(g->rowsrc, 0, g->g.rows, s);
+  if (!e) e = cudaMemsetAsync(g->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), s);  // armed slots
+  if (!e) e = cudaMemsetAsync(g->d_flags + kFlagSlots, 0, sizeof(uint32_t), s);     // arrival counter
   if (!e) e = cudaMemsetAsync(g->srcmask_dense, 0, dense, s);
   if (!e)
     e = cudaMemcpyAsync(g->occ, occ_full + (size_t)row0 * W, dense,
@@ -379,6 +382,22 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   am_prop_result r{};
   const bool timing = (ctx->flags & AM_CTX_TIMING) != 0;
   size_t timer_used = 0;
+  // Timing brackets each run of consecutive blocked launches with one event
+  // pair (stencil_ms includes the gaps between them, not per-launch events).
+  bool run_open = false;
+  auto close_run = [&]() -> am_status {
+    if (run_open) {
+      CK(cudaEventRecord(ctx->timers[timer_used++].b, ctx->stream));
+      run_open = false;
+    }
+    return AM_OK;
+  };
+  // One grid, no transport: blocked launches publish their fixed-point word
+  // straight into the mapped pinned slot (FlagSink), and re-arm the slot.
+  const bool mapped = autom && slabs.size() == 1 && !tr;
+  bool armed[kFlagSlots];
+  for (int i = 0; i < kFlagSlots; ++i) armed[i] = mapped;
+  if (mapped) CK(cudaMemsetAsync(tg->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), ctx->stream));
   std::deque<PendingBlock> pend;
   uint32_t l = 0;       // layers applied so far
   uint32_t lprime = 0;  // first layer without new cells (0 = not found)
@@ -394,7 +413,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       am_ctx* c = s.ctx;
       cudaError_t e = cudaEventSynchronize(s.g->flag_ev[b.slot]);
       if (e) return fail(c, AM_ECUDA, "flag event: %s", cudaGetErrorString(e));
-      m = std::min(m, s.g->h_flags[b.slot]);
+      m = std::min(m, (uint32_t) * (volatile uint32_t*)(s.g->h_flags + b.slot));
     }
     if (!lprime) {
       const uint32_t t = block_termination(b, m);
@@ -406,7 +425,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   while (l < target && !lprime) {
     const bool blocked = mode == AM_MODE_BATCHED && target - l >= (uint32_t)K;
     const uint32_t kk = blocked ? (uint32_t)K : 1u;
-    if (slabs[0].g->cell_bits == 16 && (uint64_t)l + kk + 1 > kMax16Activity) {
+    const bool promoting = slabs[0].g->cell_bits == 16 && (uint64_t)l + kk + 1 > kMax16Activity;
+    if ((!blocked || promoting) && (st = close_run())) return st;
+    if (promoting) {
       while (!pend.empty() && !lprime)
         if ((st = drain_one())) return st;
       pend.clear();
@@ -427,14 +448,17 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       uint32_t* flag = g->d_flags + slot;
       words[i] = flag;
       cudaStream_t s = c->stream;
-      if (autom && !(tiles && blocked)) {  // the tile planner resets its own slot
+      // the tile planner resets its own slot; a mapped slot is re-armed by the launch that used it
+      if (autom && !(tiles && blocked) && !(mapped && blocked && armed[slot])) {
         cudaError_t e = cudaMemsetAsync(flag, 0xFF, sizeof(uint32_t), s);
         if (e) return fail(c, AM_ECUDA, "memset: %s", cudaGetErrorString(e));
       }
+      armed[slot] = mapped && blocked;
+      const FlagSink sink{flag, g->d_flags + kFlagSlots, mapped ? g->h_flags_dev + slot : nullptr};
       void* in = g->val[g->cur];
       void* outp = g->val[g->cur ^ 1];
       if (blocked) {
-        if (timing) {
+        if (timing && i == 0 && !run_open) {
           if (timer_used == ctx->timers.size()) {
             am_ctx::Timer t;
             CK(cudaEventCreate(&t.a));
@@ -442,6 +466,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
             ctx->timers.push_back(t);
           }
           CK(cudaEventRecord(ctx->timers[timer_used].a, s));
+          run_open = true;
         }
         if (tiles) {
           // the planner zeroes the other counter slot for the next block and writes the next states
@@ -450,15 +475,14 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
                             g->t_list, g->t_count, autom ? flag : nullptr, g->t_processed, s);
           CKL();
           launch_block_tiles(g->g, g->cell_bits, tile_ctas, g->val[0], g->val[1], g->srcmask, g->rowsrc,
-                             g->t_list, cnt, g->t_front[g->t_fi ^ 1], g->t_state[g->t_si], l, flag, s);
+                             g->t_list, cnt, g->t_front[g->t_fi ^ 1], g->t_state[g->t_si], l, sink, s);
           g->t_fi ^= 1;
           g->t_si ^= 1;
         } else {
-          launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, flag, s);
+          launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, sink, s);
         }
         ++c->launches;
         if (cudaError_t e = cudaPeekAtLastError()) return fail(c, AM_ECUDA, "k_block: %s", cudaGetErrorString(e));
-        if (timing) CK(cudaEventRecord(ctx->timers[timer_used++].b, s));
         ++r.block_launches;
       } else {
         launch_layer(g->g, g->cell_bits, in, outp, g->srcmask, flag, s);
@@ -473,8 +497,10 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       if (tr && (st = tr->reduce(words, false))) return st;
       for (auto& sr : slabs) {
         am_ctx* c = sr.ctx;
-        cudaError_t e = cudaMemcpyAsync(sr.g->h_flags + slot, sr.g->d_flags + slot, sizeof(uint32_t),
-                                        cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaSuccess;
+        if (!(mapped && blocked))
+          e = cudaMemcpyAsync(sr.g->h_flags + slot, sr.g->d_flags + slot, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                              c->stream);
         if (!e) e = cudaEventRecord(sr.g->flag_ev[slot], c->stream);
         if (e) return fail(c, AM_ECUDA, "flag copy: %s", cudaGetErrorString(e));
       }
@@ -493,6 +519,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     while ((int)pend.size() > (tiles ? kLagTiles : kLag))
       if ((st = drain_one())) return st;
   }
+  if ((st = close_run())) return st;
   while (!pend.empty())
     if ((st = drain_one())) return st;
   if (tiles) {

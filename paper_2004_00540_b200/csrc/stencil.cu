@@ -74,6 +74,30 @@ struct Cell<32> {
   __device__ __forceinline__ static uint32_t vmin(uint32_t a, uint32_t b) { return a < b ? a : b; }
 };
 
+// Each working warp calls this exactly once (m = its min, from lane 0); the
+// last of `arrivals` to arrive publishes the word (see FlagSink).  PER_CTA:
+// every thread of every CTA calls it and one arrival is counted per CTA
+// (fewer same-address atomics); otherwise one arrival per working warp.
+template <bool PER_CTA>
+__device__ __forceinline__ void publish_flag(const FlagSink& f, uint32_t m, uint32_t arrivals) {
+  if ((threadIdx.x & 31) == 0 && m != 0xFFFFFFFFu) atomicMin(f.word, m);
+  if (!f.host) return;  // uniform
+  if (PER_CTA) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+  } else {
+    if ((threadIdx.x & 31) != 0) return;
+    __threadfence();
+  }
+  if (atomicAdd(f.done, 1u) == arrivals - 1) {  // every warp's min is in word
+    __threadfence();
+    const uint32_t v = atomicExch(f.word, 0xFFFFFFFFu);
+    *reinterpret_cast<volatile uint32_t*>(f.host) = v;
+    atomicExch(f.done, 0u);
+  }
+}
+
 // ------------------------------------------------------------- init / misc
 // SourceSet rasterisation for the grid rows [row0, row0+H) of a total_h-row
 // grid (grid.hpp:78-90): validates every source, marks owned sources in the
@@ -105,16 +129,31 @@ __global__ void k_srcmask_rows(Geo g, uint32_t total_h, uint32_t row0, const uin
 }
 
 // layer-0 field (activity.hpp:20-21): free = flag|[source], obstacle = 0.
+// 8 cells per thread (one 16 B / 32 B store); cells past the grid edge are
+// written as padding (0).
 template <int CB>
 __global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ srcmask,
                        typename Cell<CB>::T* __restrict__ val) {
-  uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t r = blockIdx.y;
-  if (c >= g.W) return;
-  uint8_t o = occ[(size_t)r * g.W + c];
-  size_t i = g.idx(r, c);
-  uint32_t flag = CB == 16 ? kFlag16 : kFlag32;
-  val[i] = (typename Cell<CB>::T)(o ? 0u : (flag | (uint32_t)srcmask[i]));
+  const uint32_t c0 = 8 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const uint32_t r = blockIdx.y;
+  if (c0 >= g.W) return;
+  const uint8_t* o = occ + (size_t)r * g.W + c0;
+  const size_t i = g.idx(r, c0);
+  const uint2 sm = *reinterpret_cast<const uint2*>(srcmask + i);
+  const uint32_t flag = CB == 16 ? kFlag16 : kFlag32;
+  uint32_t v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t s = ((k < 4 ? sm.x : sm.y) >> (8 * (k & 3))) & 0xFFu;
+    v[k] = (c0 + k < g.W && !o[k]) ? (flag | s) : 0u;
+  }
+  if constexpr (CB == 16) {
+    *reinterpret_cast<uint4*>(val + i) =
+        make_uint4(v[0] | v[1] << 16, v[2] | v[3] << 16, v[4] | v[5] << 16, v[6] | v[7] << 16);
+  } else {
+    reinterpret_cast<uint4*>(val + i)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<uint4*>(val + i)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+  }
 }
 
 // ----------------------------------------------------------- K1+K2 block
@@ -453,7 +492,7 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
                                                          typename Cell<CB>::T* __restrict__ out,
                                                          const uint8_t* __restrict__ srcmask,
                                                          const uint8_t* __restrict__ rowsrc,
-                                                         uint32_t* __restrict__ flag) {
+                                                         FlagSink flag) {
   const uint32_t warp = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5);
   const uint32_t ntiles = CB == 16 ? g.nseg / 2 : g.nseg;
   if (warp >= g.nbands * ntiles) return;
@@ -461,8 +500,7 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
   const uint32_t rA = tile * g.seg_len;  // allocated row of step 0
   const uint32_t rB = (CB == 16 ? tile + ntiles : tile) * g.seg_len;
   const uint32_t acc = stream_item<CB, SLAB>(g, in, out, srcmask, rowsrc, band, rA, band, rB, g.seg_len, true);
-  const uint32_t m = __reduce_min_sync(0xffffffffu, Cell<CB>::fold(acc));
-  if ((threadIdx.x & 31) == 0) atomicMin(flag, m);
+  publish_flag<false>(flag, __reduce_min_sync(0xffffffffu, Cell<CB>::fold(acc)), g.nbands * ntiles);
 }
 
 // Active-tile mode: the warps walk the work list built by k_tiles_plan
@@ -479,7 +517,7 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
                   const uint8_t* __restrict__ rowsrc, const uint32_t* __restrict__ list,
                   const uint32_t* __restrict__ count, uint16_t* __restrict__ front, const uint32_t* __restrict__ state,
-                  uint32_t l0, uint32_t* __restrict__ flag) {
+                  uint32_t l0, FlagSink flag) {
   const uint32_t n = *count;
   // Pairing two tiles per warp halves the instructions but also the warps;
   // with few active tiles the kernel is latency bound and more warps win.
@@ -549,7 +587,7 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
     }
     gmin = min(gmin, min(ma, hasB ? mb : ma));
   }
-  if (lane == 0 && gmin != 0xFFFFFFFFu) atomicMin(flag, gmin);
+  publish_flag<true>(flag, gmin, gridDim.x);
 }
 
 // ------------------------------------------------- active-tile bookkeeping
@@ -711,12 +749,21 @@ __global__ void k_promote(Geo g, const uint16_t* __restrict__ in, uint32_t* __re
 
 template <int CB>
 __global__ void k_zero_check(Geo g, const typename Cell<CB>::T* __restrict__ val, uint32_t* __restrict__ flag) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t c0 = 8 * (blockIdx.x * blockDim.x + threadIdx.x);  // 8 cells per thread, one vector load
   const uint32_t r = blockIdx.y;
   bool z = false;
-  if (c < g.W) {
-    const uint32_t v = val[g.idx(r, c)];
-    z = v == (CB == 16 ? kFlag16 : kFlag32);  // free and a == 0
+  if (c0 < g.W) {  // cells past the edge are padding (never equal to the bare flag)
+    const size_t i = g.idx(r, c0);
+    if constexpr (CB == 16) {
+      const uint4 q = *reinterpret_cast<const uint4*>(val + i);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z |= (w[k] & 0xFFFFu) == kFlag16 || (w[k] >> 16) == kFlag16;  // free, a == 0
+    } else {
+      const uint4 a = reinterpret_cast<const uint4*>(val + i)[0], b = reinterpret_cast<const uint4*>(val + i)[1];
+      z = a.x == kFlag32 || a.y == kFlag32 || a.z == kFlag32 || a.w == kFlag32 || b.x == kFlag32 || b.y == kFlag32 ||
+          b.z == kFlag32 || b.w == kFlag32;
+    }
   }
   if (__any_sync(0xffffffffu, z) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
@@ -817,14 +864,15 @@ void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const ui
 
 void launch_init(const Geo& g, const uint8_t* d_occ, const uint8_t* d_srcmask, void* d_val, int cb,
                  cudaStream_t s) {
+  const dim3 grid((g.W + 8 * 128 - 1) / (8 * 128), g.H);
   if (cb == 16)
-    k_init<16><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, d_occ, d_srcmask, (uint16_t*)d_val);
+    k_init<16><<<grid, 128, 0, s>>>(g, d_occ, d_srcmask, (uint16_t*)d_val);
   else
-    k_init<32><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, d_occ, d_srcmask, (uint32_t*)d_val);
+    k_init<32><<<grid, 128, 0, s>>>(g, d_occ, d_srcmask, (uint32_t*)d_val);
 }
 
 void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, const uint8_t* srcmask,
-                  const uint8_t* rowsrc, uint32_t* flag, cudaStream_t s) {
+                  const uint8_t* rowsrc, FlagSink flag, cudaStream_t s) {
   const uint32_t ntiles = cb == 16 ? g.nseg / 2 : g.nseg;
   const uint32_t warps = g.nbands * ntiles;
   const uint32_t blocks = (warps + kBlockThreads / 32 - 1) / (kBlockThreads / 32);
@@ -858,7 +906,7 @@ void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front
 // f0/f1: the two fields; state: tile states at l0
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
                         const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
-                        const uint32_t* state, uint32_t l0, uint32_t* flag, cudaStream_t s) {
+                        const uint32_t* state, uint32_t l0, FlagSink flag, cudaStream_t s) {
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
     k_block_tiles<16><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, list, count,
@@ -905,10 +953,11 @@ void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_
 }
 
 void launch_zero_check(const Geo& g, int cb, const void* val, uint32_t* flag, cudaStream_t s) {
+  const dim3 grid((g.W + 8 * 128 - 1) / (8 * 128), g.H);
   if (cb == 16)
-    k_zero_check<16><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, (const uint16_t*)val, flag);
+    k_zero_check<16><<<grid, 128, 0, s>>>(g, (const uint16_t*)val, flag);
   else
-    k_zero_check<32><<<grid2d(g.W, g.H, 256), 256, 0, s>>>(g, (const uint32_t*)val, flag);
+    k_zero_check<32><<<grid, 128, 0, s>>>(g, (const uint32_t*)val, flag);
 }
 
 void launch_decode(const Geo& g, int cb, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,

@@ -11,7 +11,7 @@ agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[hi + 1:]:
     if len(r) <= mi:
         continue
-    us = float(r[mi].replace(",", "")) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+    us = float(r[mi].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}.get(r[ui], 1.0)
     a = agg[r[ki].split("(")[0][:60]]
     a[0] += 1
     a[1] += us
