@@ -251,13 +251,13 @@ class Solver:
         self.full.close()
 
 
-def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map):
+def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts):
     """One end-to-end solve through the C ABI with host buffers (pinned)."""
     my_tgt = tgt[rank::world]
     if world == 1:
         g = am.Grid(occ, src, ctx)
         g.propagate_auto(AUTO_CAP)
-        off, pts, st = g.trace(my_tgt, am.EUCLIDEAN)
+        off, pts, st = g.trace(my_tgt, am.EUCLIDEAN, out=h_pts)
         g.activity(out=h_map)
         g.close()
         return off, pts, st
@@ -267,7 +267,7 @@ def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map):
     s.activity(out=h_map[r0:r1])
     full = am.Grid(occ, src, ctx)
     ctx.comm_gather(s, full)
-    off, pts, st = full.trace(my_tgt, am.EUCLIDEAN)
+    off, pts, st = full.trace(my_tgt, am.EUCLIDEAN, out=h_pts)
     s.close()
     full.close()
     return off, pts, st
@@ -377,13 +377,14 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_e2e:
         h_occ = torch.from_numpy(occ).pin_memory().numpy()
         h_map = torch.empty((H, W), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        h_pts = torch.empty((16 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         e2e_times = []
         for i in range(3):
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            off2, pts2, st2 = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map)
+            off2, pts2, st2 = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map, h_pts)
             ctx.synchronize()
             dt = time.perf_counter() - t0
             if dist:

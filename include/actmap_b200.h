@@ -74,6 +74,8 @@ typedef struct am_grid_info {
 
 typedef struct am_stats {
   uint64_t kernel_launches; /* every kernel this context has launched */
+  uint64_t pool_reserved;   /* device bytes held by the context's memory pool */
+  uint64_t pool_used;       /* of which in use by live grids / scratch */
 } am_stats;
 
 /* ---- context ---------------------------------------------------------- */
@@ -82,6 +84,10 @@ void am_ctx_destroy(am_ctx *ctx);
 const char *am_last_error(const am_ctx *ctx);
 am_status am_ctx_stats(const am_ctx *ctx, am_stats *out);
 am_status am_ctx_synchronize(am_ctx *ctx);
+/* Device memory of destroyed grids stays cached in the context's stream-
+ * ordered pool for the next grid (no cudaMalloc/cudaFree per solve); this
+ * returns the unused part to the driver. */
+am_status am_ctx_trim(am_ctx *ctx);
 /* The cudaStream_t every kernel of this context is launched on (so callers
  * can bracket work with CUDA events on the launching stream). */
 am_status am_ctx_get_stream(const am_ctx *ctx, void **stream);

@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -59,7 +60,7 @@ class _CtxOpts(C.Structure):
 
 
 class _Stats(C.Structure):
-    _fields_ = [("kernel_launches", C.c_uint64)]
+    _fields_ = [("kernel_launches", C.c_uint64), ("pool_reserved", C.c_uint64), ("pool_used", C.c_uint64)]
 
 
 _lib = None
@@ -82,6 +83,7 @@ def lib():
             "am_last_error": (C.c_char_p, [_vp]),
             "am_ctx_stats": (st, [_vp, C.POINTER(_Stats)]),
             "am_ctx_synchronize": (st, [_vp]),
+            "am_ctx_trim": (st, [_vp]),
             "am_ctx_get_stream": (st, [_vp, C.POINTER(_vp)]),
             "am_grid_create": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
             "am_grid_create_device": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
@@ -155,11 +157,27 @@ class Context:
             raise Error(f"cannot create a B200 context on device {device} (status {st})")
         self.handle = h
         self.device = device
+        self._owned = weakref.WeakSet()  # grids / batches: closed before the context
+
+    def _own(self, obj):
+        self._owned.add(obj)
 
     def close(self):
         if self.handle:
+            for o in list(self._owned):
+                o.close()
             lib().am_ctx_destroy(self.handle)
             self.handle = None
+
+    def pool_bytes(self) -> tuple[int, int]:
+        """(reserved, in use) device bytes of the context's memory pool."""
+        s = _Stats()
+        _check(lib().am_ctx_stats(self.handle, C.byref(s)), self, "stats")
+        return s.pool_reserved, s.pool_used
+
+    def trim(self):
+        """Return the pool's cached (unused) device memory to the driver (am_ctx_trim)."""
+        _check(lib().am_ctx_trim(self.handle), self, "trim")
 
     def __del__(self):
         try:
@@ -251,6 +269,7 @@ class Grid:
         _check(lib().am_grid_create(self.ctx.handle, self.width, self.height, _ptr(self.occ), _ptr(src), len(src),
                                     C.byref(h)), self.ctx, "SourceSet/grid")
         self.handle = h
+        self.ctx._own(self)
         self.layers = 0
 
     @classmethod
@@ -264,6 +283,7 @@ class Grid:
         _check(lib().am_grid_create_device(self.ctx.handle, width, height, C.c_void_p(d_occ_ptr),
                                            C.c_void_p(d_src_ptr), n_src, C.byref(h)), self.ctx, "grid")
         self.handle = h
+        self.ctx._own(self)
         self.layers = 0
         return self
 
@@ -280,6 +300,7 @@ class Grid:
         _check(lib().am_grid_create_slab(self.ctx.handle, occ.shape[1], occ.shape[0], row0, row1, _ptr(occ),
                                          _ptr(src), len(src), C.byref(h)), self.ctx, "slab")
         self.handle = h
+        self.ctx._own(self)
         self.layers = 0
         self.row0, self.row1 = row0, row1
         return self
@@ -340,12 +361,18 @@ class Grid:
                                     _ptr(st)), self.ctx, "path counts")
         return off, st
 
-    def trace(self, targets, method=EUCLIDEAN, seed=0):
-        """Batched path extraction: returns (offsets, points (total, 2), status)."""
+    def trace(self, targets, method=EUCLIDEAN, seed=0, out=None):
+        """Batched path extraction: returns (offsets, points (total, 2), status).
+
+        out: optional preallocated (e.g. pinned) uint32 array of shape (>= total, 2) for the points."""
         t = _rc(targets)
         off, st = self.path_counts(t, method, seed)
         total = int(off[-1])
-        pts = np.empty((max(total, 1), 2), np.uint32)
+        if out is not None and out.dtype == np.uint32 and out.ndim == 2 and out.shape[1] == 2 and \
+                out.shape[0] >= max(total, 1) and out.flags.c_contiguous:
+            pts = out
+        else:
+            pts = np.empty((max(total, 1), 2), np.uint32)
         _check(lib().am_trace_paths(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
                                     _ptr(pts), total, _ptr(st)), self.ctx, "trace")
         return off, pts[:total], st
@@ -383,6 +410,7 @@ class Batch:
         _check(lib().am_batch_create(self.ctx.handle, self.n, self.width, self.height, _ptr(occ), _ptr(src_off),
                                      _ptr(src), C.byref(h)), self.ctx, "batch")
         self.handle = h
+        self.ctx._own(self)
 
     def close(self):
         if getattr(self, "handle", None):

@@ -15,6 +15,14 @@ constexpr int kFlagSlots = 64;
 constexpr int kLag = 2;        // blocks in flight before the host reads a fixed-point flag (dense)
 constexpr int kLagTiles = 24;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
+// Host side of a grid's fixed-point slots: pinned device-mapped mirror + one
+// event per slot.  Pinning and event creation are slow, so contexts recycle
+// these across grids.
+struct FlagSet {
+  uint32_t* h = nullptr;     // pinned, device-mapped mirror
+  uint32_t* hdev = nullptr;  // its device address
+  cudaEvent_t ev[kFlagSlots] = {};
+};
 }  // namespace am
 
 struct am_ctx {
@@ -30,6 +38,8 @@ struct am_ctx {
   };
   std::vector<Timer> timers;
   am::Comm* comm = nullptr;  // set by am_comm_init
+  cudaMemPool_t pool = nullptr;  // every device buffer of the context's grids (am::dmalloc)
+  std::vector<am::FlagSet*> flag_sets;  // recycled FlagSets of destroyed grids
 };
 
 struct am_grid {
@@ -42,9 +52,7 @@ struct am_grid {
   uint8_t* occ = nullptr;            // dense owned rows (re-initialisation / plain maps)
   uint8_t* srcmask_dense = nullptr;  // dense owned rows (plain maps)
   uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots + 1 CTA arrival counter (FlagSink::done)
-  uint32_t* h_flags = nullptr;       // pinned, device-mapped mirror
-  uint32_t* h_flags_dev = nullptr;   // its device address
-  cudaEvent_t flag_ev[am::kFlagSlots];
+  am::FlagSet* fs = nullptr;         // host mirror + events of the slots (borrowed from the context)
   uint32_t* plain = nullptr;         // caller-uploaded dense map
   int plain_active = 0;
   uint32_t plain_layers = 0;
@@ -74,6 +82,18 @@ struct am_grid {
 };
 
 namespace am {
+
+// Stream-ordered allocation from the context's pool: memory released by a
+// destroyed grid is reused by the next one without a driver round trip.
+template <class T>
+inline cudaError_t dmalloc(am_ctx* c, T** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) return cudaSuccess;
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, c->pool, c->stream);
+}
+inline void dfree(am_ctx* c, void* p) {
+  if (p) cudaFreeAsync(p, c->stream);
+}
 
 inline am_status fail(am_ctx* ctx, am_status st, const char* fmt, ...) {
   char buf[512];

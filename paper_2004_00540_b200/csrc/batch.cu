@@ -126,8 +126,8 @@ am_status am_batch_create(am_ctx* ctx, uint32_t n, uint32_t mw, uint32_t mh, con
   }
   CK(cudaSetDevice(ctx->device));
   uint8_t *d_m = nullptr, *d_big = nullptr;
-  CK(cudaMalloc(&d_big, W * H));
-  cudaError_t e = cudaMalloc(&d_m, (size_t)n * mw * mh);
+  CK(am::dmalloc(ctx, &d_big, W * H));
+  cudaError_t e = am::dmalloc(ctx, &d_m, (size_t)n * mw * mh);
   if (!e) e = cudaMemsetAsync(d_big, 1, W * H, ctx->stream);  // separators / unused tiles are obstacles
   if (!e) e = cudaMemcpyAsync(d_m, occ, (size_t)n * mw * mh, cudaMemcpyHostToDevice, ctx->stream);
   if (!e) {
@@ -137,8 +137,8 @@ am_status am_batch_create(am_ctx* ctx, uint32_t n, uint32_t mw, uint32_t mh, con
   }
   if (!e) e = cudaStreamSynchronize(ctx->stream);
   if (e) {
-    cudaFree(d_m);
-    cudaFree(d_big);
+    am::dfree(ctx, d_m);
+    am::dfree(ctx, d_big);
     (void)cudaGetLastError();
     return fail(ctx, AM_ECUDA, "batch pack: %s", cudaGetErrorString(e));
   }
@@ -151,14 +151,14 @@ am_status am_batch_create(am_ctx* ctx, uint32_t n, uint32_t mw, uint32_t mh, con
   b->tiles_y = ty;
   // sources are host data (big_src); the packed occupancy is device data
   uint32_t* d_src = nullptr;
-  e = cudaMalloc(&d_src, big_src.size() * 4);
-  if (!e) e = cudaMemcpy(d_src, big_src.data(), big_src.size() * 4, cudaMemcpyHostToDevice);
+  e = am::dmalloc(ctx, &d_src, big_src.size() * 4);
+  if (!e) e = cudaMemcpyAsync(d_src, big_src.data(), big_src.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
   am_status st = e ? fail(ctx, AM_ECUDA, "%s", cudaGetErrorString(e))
                    : grid_create_rows(ctx, (uint32_t)W, (uint32_t)H, 0, (uint32_t)H, d_big, d_src, big_src.size() / 2,
                                       true, false, &b->grid);
-  cudaFree(d_src);
-  cudaFree(d_m);
-  cudaFree(d_big);
+  am::dfree(ctx, d_src);
+  am::dfree(ctx, d_m);
+  am::dfree(ctx, d_big);
   if (st) {
     delete b;
     return st;
@@ -186,8 +186,8 @@ am_status am_batch_propagate(am_ctx* ctx, am_batch* b, uint32_t layers, uint32_t
   b->cause.assign(b->n, AM_STOP_FIXED);
   if (layers == 0) {
     uint32_t *d_min = nullptr, *d_zero = nullptr;
-    CK(cudaMalloc(&d_min, b->n * 4));
-    cudaError_t e = cudaMalloc(&d_zero, b->n * 4);
+    CK(am::dmalloc(ctx, &d_min, b->n * 4));
+    cudaError_t e = am::dmalloc(ctx, &d_zero, b->n * 4);
     std::vector<uint32_t> vmin(b->n), zero(b->n);
     if (!e) {
       if (g->cell_bits == 16)
@@ -200,8 +200,8 @@ am_status am_batch_propagate(am_ctx* ctx, am_batch* b, uint32_t layers, uint32_t
     if (!e) e = cudaMemcpyAsync(vmin.data(), d_min, b->n * 4, cudaMemcpyDeviceToHost, ctx->stream);
     if (!e) e = cudaMemcpyAsync(zero.data(), d_zero, b->n * 4, cudaMemcpyDeviceToHost, ctx->stream);
     if (!e) e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(d_min);
-    cudaFree(d_zero);
+    am::dfree(ctx, d_min);
+    am::dfree(ctx, d_zero);
     if (e) return fail(ctx, AM_ECUDA, "batch stats: %s", cudaGetErrorString(e));
     const uint32_t L = g->computed;
     for (uint32_t i = 0; i < b->n; ++i) {
@@ -238,8 +238,8 @@ am_status am_batch_download(am_ctx* ctx, am_batch* b, uint32_t* maps) {
   am_grid* g = b->grid;
   const size_t bytes = (size_t)b->n * b->mw * b->mh * 4;
   uint32_t *d_out = nullptr, *d_used = nullptr;
-  CK(cudaMalloc(&d_out, bytes));
-  cudaError_t e = cudaMalloc(&d_used, b->n * 4);
+  CK(am::dmalloc(ctx, &d_out, bytes));
+  cudaError_t e = am::dmalloc(ctx, &d_used, b->n * 4);
   if (!e) e = cudaMemcpyAsync(d_used, b->layers_used.data(), b->n * 4, cudaMemcpyHostToDevice, ctx->stream);
   if (!e) {
     if (g->cell_bits == 16)
@@ -253,8 +253,8 @@ am_status am_batch_download(am_ctx* ctx, am_batch* b, uint32_t* maps) {
   }
   if (!e) e = cudaMemcpyAsync(maps, d_out, bytes, cudaMemcpyDeviceToHost, ctx->stream);
   if (!e) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(d_out);
-  cudaFree(d_used);
+  am::dfree(ctx, d_out);
+  am::dfree(ctx, d_used);
   if (e) return fail(ctx, AM_ECUDA, "batch download: %s", cudaGetErrorString(e));
   return AM_OK;
 }

@@ -26,6 +26,7 @@ namespace am {
 void comm_destroy(Comm* c);
 Transport* make_nccl_transport(am_ctx* ctx, am_grid* g);
 }  // namespace am
+static void flag_set_free(am::FlagSet* f);
 
 extern "C" {
 
@@ -38,7 +39,18 @@ am_status am_ctx_create(const am_ctx_opts* opts, am_ctx** out) {
   ctx->flags = opts ? opts->flags : 0;
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = ctx->device;
+    e = cudaMemPoolCreate(&ctx->pool, &props);
+    uint64_t keep = UINT64_MAX;  // never shrink at synchronisation points; am_ctx_trim does
+    if (e == cudaSuccess) e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   if (e != cudaSuccess) {
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     (void)cudaGetLastError();
     return AM_ECUDA;
@@ -60,7 +72,9 @@ void am_ctx_destroy(am_ctx* ctx) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
+  for (auto* f : ctx->flag_sets) flag_set_free(f);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);  // deferred by the driver while grids still hold memory
   delete ctx;
 }
 
@@ -69,6 +83,18 @@ const char* am_last_error(const am_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 am_status am_ctx_stats(const am_ctx* ctx, am_stats* out) {
   if (!ctx || !out) return AM_EINVAL;
   out->kernel_launches = ctx->launches;
+  uint64_t v = 0;
+  out->pool_reserved = cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &v) ? 0 : v;
+  v = 0;
+  out->pool_used = cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &v) ? 0 : v;
+  return AM_OK;
+}
+
+am_status am_ctx_trim(am_ctx* ctx) {
+  if (!ctx) return AM_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemPoolTrimTo(ctx->pool, 0));
   return AM_OK;
 }
 
@@ -88,30 +114,54 @@ am_status am_ctx_synchronize(am_ctx* ctx) {
 
 // ------------------------------------------------------------------ grids
 
-static void grid_free(am_grid* g) {
+static void flag_set_free(am::FlagSet* f) {
+  if (f->h) cudaFreeHost(f->h);
+  for (auto& e : f->ev)
+    if (e) cudaEventDestroy(e);
+  delete f;
+}
+
+static cudaError_t take_flag_set(am_ctx* ctx, am::FlagSet** out) {
+  if (!ctx->flag_sets.empty()) {
+    *out = ctx->flag_sets.back();
+    ctx->flag_sets.pop_back();
+    return cudaSuccess;
+  }
+  auto* f = new (std::nothrow) am::FlagSet();
+  if (!f) return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaHostAlloc(&f->h, am::kFlagSlots * sizeof(uint32_t), cudaHostAllocMapped);
+  if (!e) e = cudaHostGetDevicePointer((void**)&f->hdev, f->h, 0);
+  for (int i = 0; !e && i < am::kFlagSlots; ++i) e = cudaEventCreateWithFlags(&f->ev[i], cudaEventDisableTiming);
+  if (e) {
+    flag_set_free(f);
+    return e;
+  }
+  *out = f;
+  return cudaSuccess;
+}
+
+static void grid_free(am_ctx* ctx, am_grid* g) {
   if (!g) return;
-  for (int i = 0; i < 2; ++i) cudaFree(g->val[i]);
-  cudaFree(g->srcmask);
-  cudaFree(g->rowsrc);
-  cudaFree(g->occ);
-  cudaFree(g->srcmask_dense);
-  cudaFree(g->d_flags);
-  if (g->h_flags) cudaFreeHost(g->h_flags);
-  for (int i = 0; i < am::kFlagSlots; ++i)
-    if (g->flag_ev[i]) cudaEventDestroy(g->flag_ev[i]);
-  cudaFree(g->plain);
-  cudaFree(g->d_tgt);
-  cudaFree(g->d_counts);
-  cudaFree(g->d_offsets);
-  cudaFree(g->d_status);
-  cudaFree(g->d_pts);
-  cudaFree(g->t_front[0]);
-  cudaFree(g->t_front[1]);
-  cudaFree(g->t_state[0]);
-  cudaFree(g->t_state[1]);
-  cudaFree(g->t_list);
-  cudaFree(g->t_count);
-  cudaFree(g->t_processed);
+  for (int i = 0; i < 2; ++i) am::dfree(ctx, g->val[i]);
+  am::dfree(ctx, g->srcmask);
+  am::dfree(ctx, g->rowsrc);
+  am::dfree(ctx, g->occ);
+  am::dfree(ctx, g->srcmask_dense);
+  am::dfree(ctx, g->d_flags);
+  if (g->fs) ctx->flag_sets.push_back(g->fs);
+  am::dfree(ctx, g->plain);
+  am::dfree(ctx, g->d_tgt);
+  am::dfree(ctx, g->d_counts);
+  am::dfree(ctx, g->d_offsets);
+  am::dfree(ctx, g->d_status);
+  am::dfree(ctx, g->d_pts);
+  am::dfree(ctx, g->t_front[0]);
+  am::dfree(ctx, g->t_front[1]);
+  am::dfree(ctx, g->t_state[0]);
+  am::dfree(ctx, g->t_state[1]);
+  am::dfree(ctx, g->t_list);
+  am::dfree(ctx, g->t_count);
+  am::dfree(ctx, g->t_processed);
   delete g;
 }
 
@@ -134,7 +184,6 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   CK(cudaSetDevice(ctx->device));
   am_grid* g = new (std::nothrow) am_grid();
   if (!g) return AM_EOOM;
-  memset(g->flag_ev, 0, sizeof g->flag_ev);
   const uint32_t H = row1 - row0;
   g->g = make_geo(W, H, ctx->warp_slots);
   g->slab = slab ? 1 : 0;
@@ -147,25 +196,23 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   int* d_err = nullptr;
   am_status st = AM_OK;
   int h_err = 0;
-  cudaError_t e = cudaMalloc(&g->val[0], cells * 2);
-  if (!e) e = cudaMalloc(&g->val[1], cells * 2);
-  if (!e) e = cudaMalloc(&g->srcmask, cells);
-  if (!e) e = cudaMalloc(&g->rowsrc, g->g.rows);
-  if (!e) e = cudaMalloc(&g->occ, dense);
-  if (!e) e = cudaMalloc(&g->srcmask_dense, dense);
-  if (!e) e = cudaMalloc(&g->d_flags, (kFlagSlots + 1) * sizeof(uint32_t));
-  if (!e) e = cudaHostAlloc(&g->h_flags, kFlagSlots * sizeof(uint32_t), cudaHostAllocMapped);
-  if (!e) e = cudaHostGetDevicePointer((void**)&g->h_flags_dev, g->h_flags, 0);
-  for (int i = 0; !e && i < kFlagSlots; ++i) e = cudaEventCreateWithFlags(&g->flag_ev[i], cudaEventDisableTiming);
+  cudaError_t e = am::dmalloc(ctx, &g->val[0], cells * 2);
+  if (!e) e = am::dmalloc(ctx, &g->val[1], cells * 2);
+  if (!e) e = am::dmalloc(ctx, &g->srcmask, cells);
+  if (!e) e = am::dmalloc(ctx, &g->rowsrc, g->g.rows);
+  if (!e) e = am::dmalloc(ctx, &g->occ, dense);
+  if (!e) e = am::dmalloc(ctx, &g->srcmask_dense, dense);
+  if (!e) e = am::dmalloc(ctx, &g->d_flags, (kFlagSlots + 1) * sizeof(uint32_t));
+  if (!e) e = take_flag_set(ctx, &g->fs);
   if (!slab) {  // active-tile skipping state
     const size_t nt = g->g.ntiles();
-    if (!e) e = cudaMalloc(&g->t_front[0], nt * 2);
-    if (!e) e = cudaMalloc(&g->t_front[1], nt * 2);
-    if (!e) e = cudaMalloc(&g->t_state[0], nt * 4);
-    if (!e) e = cudaMalloc(&g->t_state[1], nt * 4);
-    if (!e) e = cudaMalloc(&g->t_list, nt * 4);
-    if (!e) e = cudaMalloc(&g->t_count, 8);  // alternating work-list counters
-    if (!e) e = cudaMalloc(&g->t_processed, 8);
+    if (!e) e = am::dmalloc(ctx, &g->t_front[0], nt * 2);
+    if (!e) e = am::dmalloc(ctx, &g->t_front[1], nt * 2);
+    if (!e) e = am::dmalloc(ctx, &g->t_state[0], nt * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_state[1], nt * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_list, nt * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_count, 8);  // alternating work-list counters
+    if (!e) e = am::dmalloc(ctx, &g->t_processed, 8);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->val[1], 0, cells * 2, s);
@@ -177,8 +224,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e)
     e = cudaMemcpyAsync(g->occ, occ_full + (size_t)row0 * W, dense,
                         device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
-  if (!e) e = cudaMalloc(&d_src, n_src * 2 * sizeof(uint32_t));
-  if (!e) e = cudaMalloc(&d_err, sizeof(int));
+  if (!e) e = am::dmalloc(ctx, &d_src, n_src * 2 * sizeof(uint32_t));
+  if (!e) e = am::dmalloc(ctx, &d_err, sizeof(int));
   if (!e) e = cudaMemsetAsync(d_err, 0, sizeof(int), s);
   if (!e)
     e = cudaMemcpyAsync(d_src, src, n_src * 2 * sizeof(uint32_t),
@@ -191,8 +238,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   }
   if (!e) e = cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);
-  cudaFree(d_src);
-  cudaFree(d_err);
+  am::dfree(ctx, d_src);
+  am::dfree(ctx, d_err);
   if (e) {
     (void)cudaGetLastError();
     st = fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "grid create: %s", cudaGetErrorString(e));
@@ -200,7 +247,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
     st = fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle (grid.hpp:78)");
   }
   if (st) {
-    grid_free(g);
+    grid_free(ctx, g);
     return st;
   }
   *out = g;
@@ -222,9 +269,11 @@ am_status am_grid_create_device(am_ctx* ctx, uint32_t W, uint32_t H, const uint8
 }
 
 am_status am_grid_destroy(am_ctx* ctx, am_grid* g) {
-  if (ctx) cudaSetDevice(ctx->device);
-  if (ctx && ctx->stream) cudaStreamSynchronize(ctx->stream);
-  grid_free(g);
+  if (!g) return AM_OK;
+  if (!ctx) return AM_EINVAL;  // the grid's buffers belong to the context's pool
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  grid_free(ctx, g);
   return AM_OK;
 }
 
@@ -275,10 +324,10 @@ static am_status promote(am_ctx* ctx, am_grid* g) {
   void* n0 = nullptr;
   void* n1 = nullptr;
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMalloc(&n0, cells * 4));
-  cudaError_t e = cudaMalloc(&n1, cells * 4);
+  CK(am::dmalloc(ctx, &n0, cells * 4));
+  cudaError_t e = am::dmalloc(ctx, &n1, cells * 4);
   if (e != cudaSuccess) {
-    cudaFree(n0);
+    am::dfree(ctx, n0);
     (void)cudaGetLastError();
     return fail(ctx, AM_EOOM, "32-bit promotion: %s", cudaGetErrorString(e));
   }
@@ -286,8 +335,8 @@ static am_status promote(am_ctx* ctx, am_grid* g) {
   CKL();
   CK(cudaMemsetAsync(n1, 0, cells * 4, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(g->val[0]);
-  cudaFree(g->val[1]);
+  am::dfree(ctx, g->val[0]);
+  am::dfree(ctx, g->val[1]);
   g->val[0] = n0;
   g->val[1] = n1;
   g->cur = 0;
@@ -300,12 +349,12 @@ static am_status promote(am_ctx* ctx, am_grid* g) {
 am_status set_cell_bits(am_ctx* ctx, am_grid* g, int cell_bits) {
   const size_t cells = (size_t)g->g.rows * g->g.pitch;
   if (g->cell_bits != cell_bits) {
-    cudaFree(g->val[0]);
-    cudaFree(g->val[1]);
+    am::dfree(ctx, g->val[0]);
+    am::dfree(ctx, g->val[1]);
     g->val[0] = g->val[1] = nullptr;
     const size_t bytes = cells * (cell_bits / 8);
-    CK(cudaMalloc(&g->val[0], bytes));
-    CK(cudaMalloc(&g->val[1], bytes));
+    CK(am::dmalloc(ctx, &g->val[0], bytes));
+    CK(am::dmalloc(ctx, &g->val[1], bytes));
     CK(cudaMemsetAsync(g->val[0], 0, bytes, ctx->stream));
     CK(cudaMemsetAsync(g->val[1], 0, bytes, ctx->stream));
     g->cell_bits = cell_bits;
@@ -411,9 +460,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     uint32_t m = 0xFFFFFFFFu;
     for (auto& s : slabs) {
       am_ctx* c = s.ctx;
-      cudaError_t e = cudaEventSynchronize(s.g->flag_ev[b.slot]);
+      cudaError_t e = cudaEventSynchronize(s.g->fs->ev[b.slot]);
       if (e) return fail(c, AM_ECUDA, "flag event: %s", cudaGetErrorString(e));
-      m = std::min(m, (uint32_t) * (volatile uint32_t*)(s.g->h_flags + b.slot));
+      m = std::min(m, (uint32_t) * (volatile uint32_t*)(s.g->fs->h + b.slot));
     }
     if (!lprime) {
       const uint32_t t = block_termination(b, m);
@@ -454,7 +503,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         if (e) return fail(c, AM_ECUDA, "memset: %s", cudaGetErrorString(e));
       }
       armed[slot] = mapped && blocked;
-      const FlagSink sink{flag, g->d_flags + kFlagSlots, mapped ? g->h_flags_dev + slot : nullptr};
+      const FlagSink sink{flag, g->d_flags + kFlagSlots, mapped ? g->fs->hdev + slot : nullptr};
       void* in = g->val[g->cur];
       void* outp = g->val[g->cur ^ 1];
       if (blocked) {
@@ -499,9 +548,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         am_ctx* c = sr.ctx;
         cudaError_t e = cudaSuccess;
         if (!(mapped && blocked))
-          e = cudaMemcpyAsync(sr.g->h_flags + slot, sr.g->d_flags + slot, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+          e = cudaMemcpyAsync(sr.g->fs->h + slot, sr.g->d_flags + slot, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                               c->stream);
-        if (!e) e = cudaEventRecord(sr.g->flag_ev[slot], c->stream);
+        if (!e) e = cudaEventRecord(sr.g->fs->ev[slot], c->stream);
         if (e) return fail(c, AM_ECUDA, "flag copy: %s", cudaGetErrorString(e));
       }
       pend.push_back(PendingBlock{slot, l, kk, slabs[0].g->cell_bits});
@@ -664,7 +713,7 @@ am_status am_activity_upload(am_ctx* ctx, am_grid* g, const uint32_t* dense, uin
   if (g->slab) return am::fail(ctx, AM_EINVAL, "activity upload on a slab grid");
   CK(cudaSetDevice(ctx->device));
   const size_t n = (size_t)g->g.W * g->g.H;
-  if (!g->plain) CK(cudaMalloc(&g->plain, n * 4));
+  if (!g->plain) CK(am::dmalloc(ctx, &g->plain, n * 4));
   CK(cudaMemcpyAsync(g->plain, dense, n * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   g->plain_active = 1;
@@ -698,18 +747,18 @@ static am::MapView view_of(am_grid* g) {
 
 static am_status ensure_targets(am_ctx* ctx, am_grid* g, uint64_t n) {
   if (n <= g->tgt_cap) return AM_OK;
-  cudaFree(g->d_tgt);
-  cudaFree(g->d_counts);
-  cudaFree(g->d_offsets);
-  cudaFree(g->d_status);
+  am::dfree(ctx, g->d_tgt);
+  am::dfree(ctx, g->d_counts);
+  am::dfree(ctx, g->d_offsets);
+  am::dfree(ctx, g->d_status);
   g->d_tgt = nullptr;
   g->d_counts = g->d_offsets = nullptr;
   g->d_status = nullptr;
   g->tgt_cap = 0;
-  CK(cudaMalloc(&g->d_tgt, n * 2 * sizeof(uint32_t)));
-  CK(cudaMalloc(&g->d_counts, n * sizeof(uint64_t)));
-  CK(cudaMalloc(&g->d_offsets, (n + 1) * sizeof(uint64_t)));
-  CK(cudaMalloc(&g->d_status, n * sizeof(int32_t)));
+  CK(am::dmalloc(ctx, &g->d_tgt, n * 2 * sizeof(uint32_t)));
+  CK(am::dmalloc(ctx, &g->d_counts, n * sizeof(uint64_t)));
+  CK(am::dmalloc(ctx, &g->d_offsets, (n + 1) * sizeof(uint64_t)));
+  CK(am::dmalloc(ctx, &g->d_status, n * sizeof(int32_t)));
   g->tgt_cap = n;
   return AM_OK;
 }
@@ -777,10 +826,10 @@ am_status am_trace_paths(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t 
   if (st) return st;
   cudaStream_t s = ctx->stream;
   if (total > g->pts_cap) {
-    cudaFree(g->d_pts);
+    am::dfree(ctx, g->d_pts);
     g->d_pts = nullptr;
     g->pts_cap = 0;
-    CK(cudaMalloc(&g->d_pts, total * 8));
+    CK(am::dmalloc(ctx, &g->d_pts, total * 8));
     g->pts_cap = total;
   }
   CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
@@ -844,12 +893,12 @@ am_status am_propagate_layer(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t*
   int* d_err = nullptr;
   int h_err = 0;
   am_status st = AM_OK;
-  cudaError_t e = cudaMalloc(&d_occ, n);
-  if (!e) e = cudaMalloc(&d_sm, n);
-  if (!e) e = cudaMalloc(&d_in, n * 4);
-  if (!e) e = cudaMalloc(&d_out, n * 4);
-  if (!e) e = cudaMalloc(&d_src, n_src * 8);
-  if (!e) e = cudaMalloc(&d_err, 4);
+  cudaError_t e = am::dmalloc(ctx, &d_occ, n);
+  if (!e) e = am::dmalloc(ctx, &d_sm, n);
+  if (!e) e = am::dmalloc(ctx, &d_in, n * 4);
+  if (!e) e = am::dmalloc(ctx, &d_out, n * 4);
+  if (!e) e = am::dmalloc(ctx, &d_src, n_src * 8);
+  if (!e) e = am::dmalloc(ctx, &d_err, 4);
   if (!e) e = cudaMemsetAsync(d_sm, 0, n, s);
   if (!e) e = cudaMemsetAsync(d_err, 0, 4, s);
   if (!e) e = cudaMemcpyAsync(d_occ, occ, n, cudaMemcpyHostToDevice, s);
@@ -866,12 +915,12 @@ am_status am_propagate_layer(am_ctx* ctx, uint32_t W, uint32_t H, const uint8_t*
   if (e) st = am::fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s", cudaGetErrorString(e));
   else if (h_err) st = am::fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle");
   (void)cudaGetLastError();
-  cudaFree(d_occ);
-  cudaFree(d_sm);
-  cudaFree(d_in);
-  cudaFree(d_out);
-  cudaFree(d_src);
-  cudaFree(d_err);
+  am::dfree(ctx, d_occ);
+  am::dfree(ctx, d_sm);
+  am::dfree(ctx, d_in);
+  am::dfree(ctx, d_out);
+  am::dfree(ctx, d_src);
+  am::dfree(ctx, d_err);
   return st;
 }
 
@@ -890,12 +939,12 @@ am_status am_propagate_reference(am_ctx* ctx, uint32_t W, uint32_t H, const uint
   int* d_err = nullptr;
   int h_err = 0;
   am_status st = AM_OK;
-  cudaError_t e = cudaMalloc(&d_occ, n);
-  if (!e) e = cudaMalloc(&d_sm, n);
-  if (!e) e = cudaMalloc(&a, n * 4);
-  if (!e) e = cudaMalloc(&b, n * 4);
-  if (!e) e = cudaMalloc(&d_src, n_src * 8);
-  if (!e) e = cudaMalloc(&d_err, 4);
+  cudaError_t e = am::dmalloc(ctx, &d_occ, n);
+  if (!e) e = am::dmalloc(ctx, &d_sm, n);
+  if (!e) e = am::dmalloc(ctx, &a, n * 4);
+  if (!e) e = am::dmalloc(ctx, &b, n * 4);
+  if (!e) e = am::dmalloc(ctx, &d_src, n_src * 8);
+  if (!e) e = am::dmalloc(ctx, &d_err, 4);
   if (!e) e = cudaMemsetAsync(d_sm, 0, n, s);
   if (!e) e = cudaMemsetAsync(d_err, 0, 4, s);
   if (!e) e = cudaMemcpyAsync(d_occ, occ, n, cudaMemcpyHostToDevice, s);
@@ -923,12 +972,12 @@ am_status am_propagate_reference(am_ctx* ctx, uint32_t W, uint32_t H, const uint
   if (e) st = am::fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "%s", cudaGetErrorString(e));
   else if (h_err) st = am::fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle");
   (void)cudaGetLastError();
-  cudaFree(d_occ);
-  cudaFree(d_sm);
-  cudaFree(a);
-  cudaFree(b);
-  cudaFree(d_src);
-  cudaFree(d_err);
+  am::dfree(ctx, d_occ);
+  am::dfree(ctx, d_sm);
+  am::dfree(ctx, a);
+  am::dfree(ctx, b);
+  am::dfree(ctx, d_src);
+  am::dfree(ctx, d_err);
   return st;
 }
 

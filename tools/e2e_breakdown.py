@@ -37,6 +37,7 @@ def main():
               f"= {b.numel() * b.element_size() / dt / 1e9:.1f} GB/s")
     del d_occ, d_map
     hm = h_map.numpy().view(np.uint32)
+    h_pts = torch.empty((16 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     ho = h_occ.numpy()
     for rep in range(reps):
         t = [time.perf_counter()]
@@ -45,7 +46,7 @@ def main():
         t.append(time.perf_counter())
         g.propagate_auto(bench.AUTO_CAP)
         t.append(time.perf_counter())
-        g.trace(tgt, am.EUCLIDEAN)
+        g.trace(tgt, am.EUCLIDEAN, out=h_pts)
         t.append(time.perf_counter())
         g.activity(out=hm)
         t.append(time.perf_counter())
@@ -53,7 +54,7 @@ def main():
         t.append(time.perf_counter())
         names = ("create", "propagate", "trace", "download", "close")
         parts = " ".join(f"{n}={(b - a) * 1e3:.1f}" for n, a, b in zip(names, t, t[1:]))
-        print(f"rep {rep}: total={(t[-1] - t[0]) * 1e3:.1f} ms  {parts}")
+        print(f"rep {rep}: total={(t[-1] - t[0]) * 1e3:.1f} ms  {parts}  pool={ctx.pool_bytes()}")
     ctx.close()
     os._exit(0)
 
