@@ -147,6 +147,14 @@ am_status am_propagate_layer(am_ctx *ctx, uint32_t width, uint32_t height, const
 am_status am_propagate_reference(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *occupancy,
                                  const uint32_t *src_rc, uint64_t n_src, uint32_t layers, uint32_t *out);
 
+/* ---- benchmark hook (tools/tile_probe.py) ------------------------------
+ * Times the active-tile kernel alone: `items` work items (pairs of tiles,
+ * chosen `stride` tiles apart, all at layer 0) launched `reps` times on the
+ * grid's layer-0 map; writes the mean launch time.  Leaves the grid without
+ * a map (propagate again before reading it). */
+am_status am_bench_tile_kernel(am_ctx *ctx, am_grid *grid, uint32_t items, uint32_t stride, uint32_t reps,
+                               float *ms_per_launch);
+
 /* ---- multi-GPU row slabs ---------------------------------
  * A slab grid owns rows [row0, row1) of a width x height grid; occupancy is
  * the FULL grid (host), sources use global coordinates.  Slabs keep K=8

@@ -84,6 +84,7 @@ def lib():
             "am_ctx_stats": (st, [_vp, C.POINTER(_Stats)]),
             "am_ctx_synchronize": (st, [_vp]),
             "am_ctx_trim": (st, [_vp]),
+            "am_bench_tile_kernel": (st, [_vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)]),
             "am_ctx_get_stream": (st, [_vp, C.POINTER(_vp)]),
             "am_grid_create": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
             "am_grid_create_device": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
@@ -352,6 +353,13 @@ class Grid:
             raise InvalidInputError("activity/grid dimension mismatch")
         _check(lib().am_activity_upload(self.ctx.handle, self.handle, _ptr(v), layers_applied), self.ctx, "upload")
         self.layers = layers_applied
+
+    def bench_tile_kernel(self, items: int, stride: int = 1, reps: int = 20) -> float:
+        """Mean launch time (ms) of the active-tile kernel on `items` tile pairs (am_bench_tile_kernel)."""
+        ms = C.c_float()
+        _check(lib().am_bench_tile_kernel(self.ctx.handle, self.handle, items, stride, reps, C.byref(ms)), self.ctx,
+               "bench tile kernel")
+        return ms.value
 
     def path_counts(self, targets, method=EUCLIDEAN, seed=0):
         t = _rc(targets)

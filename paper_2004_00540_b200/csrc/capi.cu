@@ -981,4 +981,43 @@ am_status am_propagate_reference(am_ctx* ctx, uint32_t W, uint32_t H, const uint
   return st;
 }
 
+am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t stride, uint32_t reps,
+                               float* ms_per_launch) {
+  if (!ctx || !g || !ms_per_launch || !g->t_state[0] || reps == 0 || stride == 0) return AM_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  am_status st = am::reset_map(ctx, g, 16);
+  if (st) return st;
+  g->have_map = 0;
+  const uint32_t nt = (uint32_t)g->g.ntiles();
+  const uint32_t n = std::min<uint64_t>((uint64_t)items * 2, nt);
+  std::vector<uint32_t> list(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t t = (uint32_t)(((uint64_t)i * stride) % nt);
+    list[i] = (t % g->g.nbands) << 16 | (t / g->g.nbands);
+  }
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemsetAsync(g->t_state[0], 0, (size_t)nt * 4, s));
+  CK(cudaMemcpyAsync(g->t_list, list.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(g->t_count, &n, 4, cudaMemcpyHostToDevice, s));
+  const am::FlagSink sink{g->d_flags, g->d_flags + am::kFlagSlots, nullptr};
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (uint32_t r = 0; r < reps + 2; ++r) {
+    if (r == 2) CK(cudaEventRecord(a, s));
+    am::launch_block_tiles(g->g, 16, ctx->sms * 2, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->t_list,
+                           g->t_count, g->t_front[1], g->t_state[0], 0, sink, s);
+    ++ctx->launches;
+  }
+  CK(cudaEventRecord(b, s));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  CK(cudaMemsetAsync(g->d_flags, 0xFF, am::kFlagSlots * sizeof(uint32_t), s));
+  *ms_per_launch = ms / reps;
+  return AM_OK;
+}
+
 }  // extern "C"

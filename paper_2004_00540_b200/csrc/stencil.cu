@@ -307,6 +307,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 #ifndef AM_TILE_PAIR
 #define AM_TILE_PAIR 1
 #endif
+
 constexpr int kStages = AM_STAGES;                 // rows in flight per warp (dense sweep)
 constexpr int kTileStages = AM_TILE_STAGES;        // rows in flight per warp (active tiles: few warps per SM)
 constexpr int kStageBytes = kBand * 4;             // one u32 row, or the A+B pair of u16 rows
@@ -604,8 +605,13 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
 // adds `lagw` (per-half lag) to them, leaving uncovered and obstacle cells.
 template <int CB>
 __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
-  if constexpr (CB == 16) return w + (__vcmpgtu2(w, 0x80008000u) & lagw);
-  else return w + (w > kFlag32 ? lagw : 0u);
+  if constexpr (CB == 16) {
+    // a half is covered iff its low 15 bits are nonzero: adding 0x7FFF then
+    // carries into bit 15 (never out of the half); PRMT replicates that bit
+    uint32_t cov;  // prmt's sign-replicate selectors (__byte_perm drops the selector msb)
+    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(cov) : "r"((w & 0x7FFF7FFFu) + 0x7FFF7FFFu));
+    return w + (cov & lagw);
+  } else return w + (w > kFlag32 ? lagw : 0u);
 }
 
 // Frontier-region bit a neighbour N at (dr, dc) from tile T must have for T
