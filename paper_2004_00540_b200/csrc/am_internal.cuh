@@ -40,11 +40,22 @@ constexpr int kBand = 32 * kWPL; // band width in cells (incl. halo)
 constexpr int kBandUseful = kBand - 2 * kK;
 constexpr int kBlockThreads = 128;
 
-// Active-tile skipping works on tiles of kTileRows rows x one band.
+// Active-tile skipping works on tiles of kTileRows rows x kTileCols columns,
+// streamed by warps with kTileWPL words per lane: narrower than the dense
+// bands, so a frontier activates fewer cells and a warp's item is shorter.
 #ifndef AM_TILE_ROWS
 #define AM_TILE_ROWS 32
 #endif
+#ifndef AM_TILE_WPL
+#define AM_TILE_WPL 4
+#endif
 constexpr int kTileRows = AM_TILE_ROWS;
+constexpr int kTileWPL = AM_TILE_WPL;
+constexpr int kTileCols = 32 * kTileWPL - 2 * kK;  // useful columns of a tile band
+#ifndef AM_TILE_CTAS
+#define AM_TILE_CTAS (AM_TILE_WPL == 4 ? 4 : 2)
+#endif
+constexpr int kTileCtasPerSm = AM_TILE_CTAS;  // k_block_tiles is persistent: this many CTAs per SM
 
 struct Geo {
   uint32_t W, H;          // grid extent (cells)
@@ -55,7 +66,8 @@ struct Geo {
   uint32_t nseg;          // row segments (even)
   uint32_t seg_len;       // rows per segment (even)
   uint32_t nchunks;       // row chunks of kTileRows (tile rows)
-  __host__ __device__ uint32_t ntiles() const { return nbands * nchunks; }
+  uint32_t tbands;        // tile bands of kTileCols columns
+  __host__ __device__ uint32_t ntiles() const { return tbands * nchunks; }
   __host__ __device__ size_t idx(uint32_t r, uint32_t c) const {
     return (size_t)(r + pad) * pitch + (c + pad);
   }

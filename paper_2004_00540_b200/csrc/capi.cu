@@ -291,7 +291,7 @@ am_status am_grid_get_info(const am_grid* g, am_grid_info* o) {
   o->layers_used = g->layers_used;
   o->layers_computed = g->computed;
   o->tile_rows = am::kTileRows;
-  o->tile_cols = am::kBandUseful;
+  o->tile_cols = am::kTileCols;
   o->tiles = g->t_state[0] ? g->g.ntiles() : 0;
   return AM_OK;
 }
@@ -400,7 +400,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_state[0] && mode == AM_MODE_BATCHED &&
                      !(ctx->flags & AM_CTX_DENSE);
   const size_t nt = tiles ? tg->g.ntiles() : 0;
-  const int tile_ctas = ctx->sms * 2;  // persistent: k_block_tiles is sized for 2 CTAs per SM
+  const int tile_ctas = ctx->sms * kTileCtasPerSm;  // persistent k_block_tiles
   // after dense work: every tile current at at_layer in val[cur], all active next block
   auto tiles_all_active = [&](uint32_t at_layer) -> am_status {
     CK(cudaMemsetAsync(tg->t_front[tg->t_fi], 0xFF, nt * 2, ctx->stream));
@@ -1005,7 +1005,7 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
   CK(cudaEventCreate(&b));
   for (uint32_t r = 0; r < reps + 2; ++r) {
     if (r == 2) CK(cudaEventRecord(a, s));
-    am::launch_block_tiles(g->g, 16, ctx->sms * 2, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->t_list,
+    am::launch_block_tiles(g->g, 16, ctx->sms * am::kTileCtasPerSm, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->t_list,
                            g->t_count, g->t_front[1], g->t_state[0], 0, sink, s);
     ++ctx->launches;
   }

@@ -17,9 +17,12 @@ Geo make_geo(uint32_t W, uint32_t H, int warp_slots) {
   g.H = H;
   g.pad = kK;
   g.nbands = (W + kBandUseful - 1) / kBandUseful;
+  g.tbands = (W + kTileCols - 1) / kTileCols;
   uint32_t need = g.nbands * kBandUseful + 2 * kK;
+  const uint32_t tneed = g.tbands * kTileCols + 2 * kK;
   uint32_t minw = W + 2 * kK;
   if (need < minw) need = minw;
+  if (need < tneed) need = tneed;
   g.pitch = (need + 63) / 64 * 64;
   // one wave of warps: pairs of row segments per band
   uint32_t pairs = warp_slots > 0 ? (uint32_t)warp_slots / g.nbands : 1;
@@ -157,112 +160,108 @@ __global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __
 }
 
 // ----------------------------------------------------------- K1+K2 block
-template <int CB>
+template <int CB, int WPL>
 struct Rows;
 
-// Loads one row of both tiles and interleaves them into u16x2 words.
-template <>
-struct Rows<16> {
-  uint4 a, b;
-  __device__ __forceinline__ void load(const uint16_t* pa, const uint16_t* pb) {
-    a = __ldg(reinterpret_cast<const uint4*>(pa));
-    b = __ldg(reinterpret_cast<const uint4*>(pb));
-  }
-  __device__ __forceinline__ void words(uint32_t (&x)[kWPL]) const {
-    const uint32_t A[4] = {a.x, a.y, a.z, a.w}, B[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      x[2 * i] = __byte_perm(A[i], B[i], 0x5410);
-      x[2 * i + 1] = __byte_perm(A[i], B[i], 0x7632);
-    }
-  }
-  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint16_t* pa, uint16_t* pb, bool wa,
+// 16-bit cells: word w of a lane holds cell w of tile A (lo) and of tile B
+// (hi); a lane's WPL cells of one tile row are WPL*2 contiguous bytes.
+template <int WPL>
+struct Rows<16, WPL> {
+  static_assert(WPL == 4 || WPL == 8, "lane width");
+  __device__ __forceinline__ static void store(const uint32_t (&x)[WPL], uint16_t* pa, uint16_t* pb, bool wa,
                                                bool wb) {
-    uint32_t A[4], B[4];
+    uint32_t A[WPL / 2], B[WPL / 2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < WPL / 2; ++i) {
       A[i] = __byte_perm(x[2 * i], x[2 * i + 1], 0x5410);
       B[i] = __byte_perm(x[2 * i], x[2 * i + 1], 0x7632);
     }
-    if (wa) *reinterpret_cast<uint4*>(pa) = make_uint4(A[0], A[1], A[2], A[3]);
-    if (wb) *reinterpret_cast<uint4*>(pb) = make_uint4(B[0], B[1], B[2], B[3]);
+    if constexpr (WPL == 8) {
+      if (wa) *reinterpret_cast<uint4*>(pa) = make_uint4(A[0], A[1], A[2], A[3]);
+      if (wb) *reinterpret_cast<uint4*>(pb) = make_uint4(B[0], B[1], B[2], B[3]);
+    } else {
+      if (wa) *reinterpret_cast<uint2*>(pa) = make_uint2(A[0], A[1]);
+      if (wb) *reinterpret_cast<uint2*>(pb) = make_uint2(B[0], B[1]);
+    }
   }
   // words restricted to the valid tiles (an invalid half becomes 0 = unflagged)
   __device__ __forceinline__ static uint32_t valid_bits(bool wa, bool wb) {
     return (wa ? 0x0000FFFFu : 0u) | (wb ? 0xFFFF0000u : 0u);
   }
-  __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t* sb, uint32_t (&s)[kWPL]) {
-    const uint2 A = *reinterpret_cast<const uint2*>(sa);
-    const uint2 B = *reinterpret_cast<const uint2*>(sb);
-    const uint32_t a4[2] = {A.x, A.y}, b4[2] = {B.x, B.y};
+  __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t* sb, uint32_t (&s)[WPL]) {
+    uint32_t a4[2], b4[2];
+    if constexpr (WPL == 8) {
+      const uint2 A = *reinterpret_cast<const uint2*>(sa), B = *reinterpret_cast<const uint2*>(sb);
+      a4[0] = A.x, a4[1] = A.y, b4[0] = B.x, b4[1] = B.y;
+    } else {
+      a4[0] = *reinterpret_cast<const uint32_t*>(sa), b4[0] = *reinterpret_cast<const uint32_t*>(sb);
+      a4[1] = b4[1] = 0;
+    }
 #pragma unroll
-    for (int w = 0; w < kWPL; ++w) {
+    for (int w = 0; w < WPL; ++w) {
       uint32_t ab = (a4[w / 4] >> (8 * (w % 4))) & 0xFFu, bb = (b4[w / 4] >> (8 * (w % 4))) & 0xFFu;
       s[w] = ab | (bb << 16);
     }
   }
 };
 
-template <>
-struct Rows<32> {
-  uint4 a, b;
-  __device__ __forceinline__ void load(const uint32_t* pa, const uint32_t*) {
-    a = __ldg(reinterpret_cast<const uint4*>(pa));
-    b = __ldg(reinterpret_cast<const uint4*>(pa) + 1);
-  }
-  __device__ __forceinline__ void words(uint32_t (&x)[kWPL]) const {
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-  }
-  __device__ __forceinline__ static void store(const uint32_t (&x)[kWPL], uint32_t* pa, uint32_t*, bool wa, bool) {
+template <int WPL>
+struct Rows<32, WPL> {
+  static_assert(WPL == 4 || WPL == 8, "lane width");
+  __device__ __forceinline__ static void store(const uint32_t (&x)[WPL], uint32_t* pa, uint32_t*, bool wa, bool) {
     if (!wa) return;
     reinterpret_cast<uint4*>(pa)[0] = make_uint4(x[0], x[1], x[2], x[3]);
-    reinterpret_cast<uint4*>(pa)[1] = make_uint4(x[4], x[5], x[6], x[7]);
+    if constexpr (WPL == 8) reinterpret_cast<uint4*>(pa)[1] = make_uint4(x[4], x[5], x[6], x[7]);
   }
   __device__ __forceinline__ static uint32_t valid_bits(bool wa, bool) { return wa ? 0xFFFFFFFFu : 0u; }
-  __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t*, uint32_t (&s)[kWPL]) {
-    const uint2 A = *reinterpret_cast<const uint2*>(sa);
-    const uint32_t a4[2] = {A.x, A.y};
+  __device__ __forceinline__ static void src_words(const uint8_t* sa, const uint8_t*, uint32_t (&s)[WPL]) {
+    uint32_t a4[2];
+    if constexpr (WPL == 8) {
+      const uint2 A = *reinterpret_cast<const uint2*>(sa);
+      a4[0] = A.x, a4[1] = A.y;
+    } else {
+      a4[0] = *reinterpret_cast<const uint32_t*>(sa), a4[1] = 0;
+    }
 #pragma unroll
-    for (int w = 0; w < kWPL; ++w) s[w] = (a4[w / 4] >> (8 * (w % 4))) & 0xFFu;
+    for (int w = 0; w < WPL; ++w) s[w] = (a4[w / 4] >> (8 * (w % 4))) & 0xFFu;
   }
 };
 
 // One streaming step: x holds the newly loaded row (layer 0, row t); layer j
 // produces row t-j from layer j-1's rows t-j-1, t-j (window) and t-j+1 (x).
 // PH selects which window slot holds the older row (it is overwritten).
-template <int CB, int PH, bool SRC>
-__device__ __forceinline__ void stream_step(uint32_t (&x)[kWPL], uint32_t (&P0)[kK][kWPL],
-                                            uint32_t (&P1)[kK][kWPL], uint32_t srcbits,
+template <int CB, int PH, bool SRC, int WPL>
+__device__ __forceinline__ void stream_step(uint32_t (&x)[WPL], uint32_t (&P0)[kK][WPL],
+                                            uint32_t (&P1)[kK][WPL], uint32_t srcbits,
                                             const uint8_t* sA, const uint8_t* sB, size_t pitch, int lane) {
   using C = Cell<CB>;
 #pragma unroll
   for (int j = 0; j < kK; ++j) {
-    uint32_t v[kWPL];
+    uint32_t v[WPL];
 #pragma unroll
-    for (int w = 0; w < kWPL; ++w) v[w] = C::max3(P0[j][w], P1[j][w], x[w]);
-    const uint32_t left = __shfl_up_sync(0xffffffffu, v[kWPL - 1], 1);
+    for (int w = 0; w < WPL; ++w) v[w] = C::max3(P0[j][w], P1[j][w], x[w]);
+    const uint32_t left = __shfl_up_sync(0xffffffffu, v[WPL - 1], 1);
     const uint32_t right = __shfl_down_sync(0xffffffffu, v[0], 1);
     // the older window row is dead once v exists: it takes this layer's input row
 #pragma unroll
-    for (int w = 0; w < kWPL; ++w) {
+    for (int w = 0; w < WPL; ++w) {
       if (PH == 0) P0[j][w] = x[w];
       else P1[j][w] = x[w];
     }
     // interior words first: they do not wait for the shuffles
 #pragma unroll
-    for (int w = 1; w < kWPL - 1; ++w) {
+    for (int w = 1; w < WPL - 1; ++w) {
       const uint32_t ctr = PH == 0 ? P1[j][w] : P0[j][w];  // layer j-1, row t-j-1+1
       x[w] = C::max3(v[w - 1], v[w], v[w + 1]) & (ctr | C::LOW);
     }
     x[0] = C::max3(left, v[0], v[1]) & ((PH == 0 ? P1[j][0] : P0[j][0]) | C::LOW);
-    x[kWPL - 1] = C::max3(v[kWPL - 2], v[kWPL - 1], right) & ((PH == 0 ? P1[j][kWPL - 1] : P0[j][kWPL - 1]) | C::LOW);
+    x[WPL - 1] = C::max3(v[WPL - 2], v[WPL - 1], right) & ((PH == 0 ? P1[j][WPL - 1] : P0[j][WPL - 1]) | C::LOW);
     if (SRC && ((srcbits >> (j + 1)) & 1u)) {  // row t-(j+1) holds a source (warp-uniform, rare)
-      uint32_t s[kWPL];
+      uint32_t s[WPL];
       const size_t off = (size_t)(j + 1) * pitch;
-      Rows<CB>::src_words(sA - off, sB - off, s);
+      Rows<CB, WPL>::src_words(sA - off, sB - off, s);
 #pragma unroll
-      for (int w = 0; w < kWPL; ++w) x[w] += s[w];
+      for (int w = 0; w < WPL; ++w) x[w] += s[w];
     }
   }
   (void)lane;
@@ -297,6 +296,9 @@ __device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t byt
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 
 #ifndef AM_STAGES
 #define AM_STAGES 4
@@ -310,27 +312,39 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 
 constexpr int kStages = AM_STAGES;                 // rows in flight per warp (dense sweep)
 constexpr int kTileStages = AM_TILE_STAGES;        // rows in flight per warp (active tiles: few warps per SM)
-constexpr int kStageBytes = kBand * 4;             // one u32 row, or the A+B pair of u16 rows
+// one stage = one u32 row of the warp's band, or the A+B pair of u16 rows
+template <int WPL>
+constexpr int stage_bytes() { return 32 * WPL * 4; }
 constexpr int kWarpsPerCta = kBlockThreads / 32;
-constexpr int kBlockSmem = kWarpsPerCta * kStages * kStageBytes;
-constexpr int kTileSmem = kWarpsPerCta * kTileStages * kStageBytes;
+constexpr int kBlockSmem = kWarpsPerCta * kStages * stage_bytes<kWPL>();
+constexpr int kTileSmem = kWarpsPerCta * kTileStages * stage_bytes<kTileWPL>();
 
-template <int CB>
-__device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint32_t (&x)[kWPL]) {
+template <int CB, int WPL>
+__device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint32_t (&x)[WPL]) {
+  constexpr int kLaneBytes = WPL * CB / 8;  // one tile row of this lane
+  uint32_t A[4], B[4];
   if constexpr (CB == 16) {
-    const uint4 a = reinterpret_cast<const uint4*>(stage)[lane];
-    const uint4 b = reinterpret_cast<const uint4*>(stage + kBand * 2)[lane];
-    const uint32_t A[4] = {a.x, a.y, a.z, a.w}, B[4] = {b.x, b.y, b.z, b.w};
+    if constexpr (WPL == 8) {
+      const uint4 a = reinterpret_cast<const uint4*>(stage)[lane];
+      const uint4 b = reinterpret_cast<const uint4*>(stage + 32 * kLaneBytes)[lane];
+      A[0] = a.x, A[1] = a.y, A[2] = a.z, A[3] = a.w, B[0] = b.x, B[1] = b.y, B[2] = b.z, B[3] = b.w;
+    } else {
+      const uint2 a = reinterpret_cast<const uint2*>(stage)[lane];
+      const uint2 b = reinterpret_cast<const uint2*>(stage + 32 * kLaneBytes)[lane];
+      A[0] = a.x, A[1] = a.y, B[0] = b.x, B[1] = b.y;
+    }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < WPL / 2; ++i) {
       x[2 * i] = __byte_perm(A[i], B[i], 0x5410);
       x[2 * i + 1] = __byte_perm(A[i], B[i], 0x7632);
     }
   } else {
-    const uint4 a = reinterpret_cast<const uint4*>(stage)[2 * lane];
-    const uint4 b = reinterpret_cast<const uint4*>(stage)[2 * lane + 1];
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    const uint4 a = reinterpret_cast<const uint4*>(stage + lane * kLaneBytes)[0];
+    x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w;
+    if constexpr (WPL == 8) {
+      const uint4 b = reinterpret_cast<const uint4*>(stage + lane * kLaneBytes)[1];
+      x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+    }
   }
 }
 
@@ -354,7 +368,7 @@ __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw);
 // `in + delta`; bit r of `homes` (r = 0 above, 1 inside, 2 below the item)
 // says tile A's region r is read from the second field, bits 3..5 the same
 // for B, bit 6 / 7 that A's / B's output goes to `out + delta`.
-template <int CB, bool SLAB, bool LAG = false, int ST = kStages>
+template <int CB, bool SLAB, bool LAG = false, int ST = kStages, int WPL = kWPL>
 __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cell<CB>::T* __restrict__ in,
                                                 typename Cell<CB>::T* __restrict__ out,
                                                 const uint8_t* __restrict__ srcmask,
@@ -366,8 +380,9 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
   using C = Cell<CB>;
   using T = typename C::T;
   const int lane = threadIdx.x & 31;
-  const uint32_t colA = bA * kBandUseful + lane * kWPL;  // allocated column of this lane's first cell
-  const uint32_t colB = bB * kBandUseful + lane * kWPL;
+  constexpr uint32_t kUseful = 32 * WPL - 2 * kK;  // useful columns of the band
+  const uint32_t colA = bA * kUseful + lane * WPL;   // allocated column of this lane's first cell
+  const uint32_t colB = bB * kUseful + lane * WPL;
   const uint32_t T_steps = rows + 2 * kK;
   const size_t pitch = g.pitch;
 
@@ -377,13 +392,13 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
   T* oB = out + (size_t)rB * pitch + colB + ((homes >> 7) & 1u ? delta : 0);
   const uint8_t* sA = srcmask + (size_t)rA * pitch + colA;
   const uint8_t* sB = srcmask + (size_t)rB * pitch + colB;
-  const bool store_lane = lane >= kK / kWPL && lane < 32 - kK / kWPL;
+  const bool store_lane = lane >= kK / WPL && lane < 32 - kK / WPL;
 
-  uint32_t P0[kK][kWPL], P1[kK][kWPL];
+  uint32_t P0[kK][WPL], P1[kK][WPL];
 #pragma unroll
   for (int j = 0; j < kK; ++j)
 #pragma unroll
-    for (int w = 0; w < kWPL; ++w) P0[j][w] = P1[j][w] = 0u;
+    for (int w = 0; w < WPL; ++w) P0[j][w] = P1[j][w] = 0u;
   uint32_t acc = 0xFFFFFFFFu;
   uint32_t srcbits = 0;
 
@@ -392,9 +407,11 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
   // kStages-1 rows ahead without holding registers, and since no lane reads
   // another lane's slot no barrier or fence is needed.
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * ST * kStageBytes;
+  constexpr int kSB = stage_bytes<WPL>();
+  constexpr int kLaneBytes = WPL * CB / 8;  // one tile row of this lane
+  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * ST * kSB;
   auto issue = [&](uint32_t step) {
-    uint8_t* dst = ring + (step % ST) * kStageBytes;
+    uint8_t* dst = ring + (step % ST) * kSB;
     if (step < T_steps) {
       const size_t off = (size_t)step * pitch;
       const T* a = pA + off;
@@ -404,12 +421,15 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
         if ((homes >> reg) & 1u) a += delta;
         if ((homes >> (3 + reg)) & 1u) b += delta;
       }
-      if (CB == 16) {
+      if constexpr (kLaneBytes == 8) {
+        cp_async8(dst + lane * 8, a);
+        cp_async8(dst + 32 * 8 + lane * 8, b);
+      } else if constexpr (CB == 16) {
         cp_async16(dst + lane * 16, a);
-        cp_async16(dst + kBand * 2 + lane * 16, b);
+        cp_async16(dst + 32 * 16 + lane * 16, b);
       } else {
-        cp_async16(dst + lane * 32, a);
-        cp_async16(dst + lane * 32 + 16, a + 16 / sizeof(T));
+        cp_async16(dst + lane * kLaneBytes, a);
+        if constexpr (kLaneBytes == 32) cp_async16(dst + lane * 32 + 16, a + 16 / sizeof(T));
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -432,15 +452,15 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
 #pragma unroll
     for (int ph = 0; ph < 2; ++ph) {
       const uint32_t tt = t + ph;
-      uint32_t x[kWPL];
+      uint32_t x[WPL];
       issue(tt + ST - 1);  // refills the slot consumed by the previous step
       asm volatile("cp.async.wait_group %0;" ::"n"(ST - 1) : "memory");
-      stage_words<CB>(ring + (tt % ST) * kStageBytes, lane, x);
+      stage_words<CB, WPL>(ring + (tt % ST) * kSB, lane, x);
       if constexpr (LAG) {
         const uint32_t lw = tt < (uint32_t)kK ? lag0 : (tt < kK + rows ? lag1 : lag2);
         if (__any_sync(0xffffffffu, lw != 0u)) {
 #pragma unroll
-          for (int w = 0; w < kWPL; ++w) x[w] = add_lag<CB>(x[w], lw);
+          for (int w = 0; w < WPL; ++w) x[w] = add_lag<CB>(x[w], lw);
         }
       }
       const size_t roff = (size_t)tt * pitch;
@@ -448,33 +468,33 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
       // rows t-1 .. t-kK are in flight; only steps that touch a source row pay for the +1
       const bool src_rows = __any_sync(0xffffffffu, (srcbits & (((1u << kK) - 1u) << 1)) != 0u);
       if (ph == 0) {
-        if (src_rows) stream_step<CB, 0, true>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-        else stream_step<CB, 0, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+        if (src_rows) stream_step<CB, 0, true, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+        else stream_step<CB, 0, false, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
       } else {
-        if (src_rows) stream_step<CB, 1, true>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-        else stream_step<CB, 1, false>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+        if (src_rows) stream_step<CB, 1, true, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
+        else stream_step<CB, 1, false, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
       }
       if (tt >= 2 * kK && tt < 2 * kK + rows && store_lane) {
         if constexpr (LAG) {  // also track the first / last kK output rows (tile edge regions)
-          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
+          Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
           uint32_t rm = 0xFFFFFFFFu;
 #pragma unroll
-          for (int w = 0; w < kWPL; ++w) rm = C::acc_min(x[w], rm);
+          for (int w = 0; w < WPL; ++w) rm = C::acc_min(x[w], rm);
           acc = C::vmin(acc, rm);
           const uint32_t orow = tt - 2 * kK;
           if (orow < (uint32_t)kK) accTop = C::vmin(accTop, rm);
           if (orow >= rows - kK) accBot = C::vmin(accBot, rm);
         } else if constexpr (!SLAB) {
-          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
+          Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
 #pragma unroll
-          for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w], acc);
+          for (int w = 0; w < WPL; ++w) acc = C::acc_min(x[w], acc);
         } else {
           const uint32_t orow = tt - 2 * kK;
           const bool wa = rA + orow < g.H, wb = rB + orow < g.H;
-          Rows<CB>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
-          const uint32_t keep = Rows<CB>::valid_bits(wa, wb);
+          Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
+          const uint32_t keep = Rows<CB, WPL>::valid_bits(wa, wb);
 #pragma unroll
-          for (int w = 0; w < kWPL; ++w) acc = C::acc_min(x[w] & keep, acc);
+          for (int w = 0; w < WPL; ++w) acc = C::acc_min(x[w] & keep, acc);
         }
       }
     }
@@ -514,7 +534,7 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
 // whether it still has a frontier (a cell covered during this block,
 // 1 <= a <= kK) for the next plan.
 template <int CB>
-__global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: registers over occupancy
+__global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
                   const uint8_t* __restrict__ rowsrc, const uint32_t* __restrict__ list,
                   const uint32_t* __restrict__ count, uint16_t* __restrict__ front, const uint32_t* __restrict__ state,
@@ -525,13 +545,14 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
   const uint32_t per = (CB == 16 && AM_TILE_PAIR) ? 2u : 1u;
   const uint32_t nw = gridDim.x * (kBlockThreads / 32);
   const int lane = threadIdx.x & 31;
-  const int brel = lane == 0 ? -1 : (lane == 31 ? 1 : 0);  // band this lane's cells belong to
+  constexpr int kHaloLanes = kK / kTileWPL;  // lanes holding the left / right halo columns
+  const int brel = lane < kHaloLanes ? -1 : (lane >= 32 - kHaloLanes ? 1 : 0);  // band of this lane's cells
   // (lag, home) of the tile this lane reads at chunk c0+dr
   auto region = [&](uint32_t c0, uint32_t b0, int dr, uint32_t& home) -> uint32_t {
     const int c = (int)c0 + dr, b = (int)b0 + brel;
     home = 0;
-    if (c < 0 || b < 0 || c >= (int)g.nchunks || b >= (int)g.nbands) return 0u;  // padding: zero in both fields
-    const uint32_t s = state[(uint32_t)c * g.nbands + (uint32_t)b];
+    if (c < 0 || b < 0 || c >= (int)g.nchunks || b >= (int)g.tbands) return 0u;  // padding: zero in both fields
+    const uint32_t s = state[(uint32_t)c * g.tbands + (uint32_t)b];
     home = s & 1u;
     const uint32_t e = s >> 1;
     return e < l0 ? l0 - e : 0u;
@@ -551,21 +572,34 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
       homes |= ha << d | hb << (3 + d);
     }
     // own rows go to the field that is not the tile's home
-    const uint32_t sa = state[cA * g.nbands + bA], sb = state[cB * g.nbands + bB];
+    const uint32_t sa = state[cA * g.tbands + bA], sb = state[cB * g.tbands + bB];
     homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
     uint32_t edge[2];
-    const uint32_t acc = stream_item<CB, false, true, kTileStages>(g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB,
-                                                      cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2], delta,
-                                                      homes, edge);
+    const uint32_t acc = stream_item<CB, false, true, kTileStages, kTileWPL>(
+        g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB, cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2], delta,
+        homes, edge);
     // Frontier regions of each tile: cells with a == 1 (covered in the block's
     // last layer; min(a-1) == 0) anywhere / in the first or last kK rows / in
-    // the first (lane 1) or last (lane 30) kK useful columns / the corners.
+    // the first or last kK useful columns (the lanes next to the halo lanes) /
+    // the corners.
+    auto lanes_min = [&](uint32_t v, int first) {
+      uint32_t m = __shfl_sync(0xffffffffu, v, first);
+#pragma unroll
+      for (int k = 1; k < kHaloLanes; ++k) m = Cell<CB>::vmin(m, __shfl_sync(0xffffffffu, v, first + k));
+      return m;
+    };
+    constexpr int kL = kHaloLanes, kR = 32 - 2 * kHaloLanes;  // first lane of the left / right edge columns
+    const uint32_t vals[9] = {acc,
+                              edge[0],
+                              edge[1],
+                              lanes_min(acc, kL),
+                              lanes_min(acc, kR),
+                              lanes_min(edge[0], kL),
+                              lanes_min(edge[0], kR),
+                              lanes_min(edge[1], kL),
+                              lanes_min(edge[1], kR)};
     auto regions = [&](int half) -> uint32_t {
       auto h = [&](uint32_t v) { return CB == 16 ? (half ? v >> 16 : v & 0xFFFFu) : v; };
-      const uint32_t vals[9] = {
-          acc, edge[0], edge[1], __shfl_sync(0xffffffffu, acc, 1), __shfl_sync(0xffffffffu, acc, 30),
-          __shfl_sync(0xffffffffu, edge[0], 1), __shfl_sync(0xffffffffu, edge[0], 30),
-          __shfl_sync(0xffffffffu, edge[1], 1), __shfl_sync(0xffffffffu, edge[1], 30)};
       uint32_t m = 0;
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
@@ -583,8 +617,8 @@ __global__ void __launch_bounds__(kBlockThreads, 2)  // few items per block: reg
       ma = mb = __reduce_min_sync(0xffffffffu, acc);
     }
     if (lane == 0) {
-      front[cA * g.nbands + bA] = (uint16_t)fa;
-      if (hasB) front[cB * g.nbands + bB] = (uint16_t)fb;
+      front[cA * g.tbands + bA] = (uint16_t)fa;
+      if (hasB) front[cB * g.tbands + bB] = (uint16_t)fb;
     }
     gmin = min(gmin, min(ma, hasB ? mb : ma));
   }
@@ -635,14 +669,14 @@ __global__ void k_tiles_plan(Geo g, const uint16_t* __restrict__ front_prev, uin
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   bool act = false;
   if (t < g.ntiles()) {
-    const int chunk = (int)(t / g.nbands), band = (int)(t % g.nbands);
+    const int chunk = (int)(t / g.tbands), band = (int)(t % g.tbands);
 #pragma unroll
     for (int dr = -1; dr <= 1; ++dr)
 #pragma unroll
       for (int dc = -1; dc <= 1; ++dc) {
         const int c = chunk + dr, b = band + dc;
-        if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.nbands)
-          act |= (front_prev[(uint32_t)c * g.nbands + (uint32_t)b] >> kFacing[dr + 1][dc + 1]) & 1u;
+        if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.tbands)
+          act |= (front_prev[(uint32_t)c * g.tbands + (uint32_t)b] >> kFacing[dr + 1][dc + 1]) & 1u;
       }
     const uint32_t s = state[t];
     state_next[t] = act ? (((l0 + kk) << 1) | ((s & 1u) ^ 1u)) : s;
@@ -655,7 +689,7 @@ __global__ void k_tiles_plan(Geo g, const uint16_t* __restrict__ front_prev, uin
     atomicAdd(processed, (unsigned long long)__popc(am));
   }
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (act) list[base + __popc(am & ((1u << lane) - 1u))] = (t % g.nbands) << 16 | (t / g.nbands);
+  if (act) list[base + __popc(am & ((1u << lane) - 1u))] = (t % g.tbands) << 16 | (t / g.tbands);
 }
 
 // 16 B per lane-row: 8 cells (u16) or 4 cells (u32)
@@ -663,10 +697,10 @@ template <int CB, typename F>
 __device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, uint32_t chunk, F f) {
   const int lane = threadIdx.x & 31;
   constexpr int kVecCells = 16 / sizeof(typename Cell<CB>::T);
-  constexpr int kVecs = kBandUseful / kVecCells;  // vectors per tile row
+  constexpr int kVecs = kTileCols / kVecCells;  // vectors per tile row
   for (int v = lane; v < kVecs * kTileRows; v += 32) {
     const uint32_t r = v / kVecs, k = v % kVecs;
-    f((size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kBandUseful + k * kVecCells);
+    f((size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kTileCols + k * kVecCells);
   }
 }
 
@@ -684,7 +718,7 @@ __global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ state, typename C
     const uint32_t lagw = CB == 16 ? (lag | lag << 16) : lag;
     const typename Cell<CB>::T* src = f0 + (home ? delta : 0);
     typename Cell<CB>::T* out = f0 + (dst ? delta : 0);
-    tile_rows_foreach<CB>(g, t % g.nbands, t / g.nbands, [&](size_t i) {
+    tile_rows_foreach<CB>(g, t % g.tbands, t / g.tbands, [&](size_t i) {
       uint4 v = *reinterpret_cast<const uint4*>(src + i);
       if (lag) {
         v.x = add_lag<CB>(v.x, lagw);
@@ -704,11 +738,11 @@ __global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint16_
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= g.ntiles()) return;
   const int lane = threadIdx.x & 31;
-  const uint32_t chunk = t / g.nbands, band = t % g.nbands;
+  const uint32_t chunk = t / g.tbands, band = t % g.tbands;
   bool any = false;
-  if (lane < kBandUseful / kWPL)
+  if (lane < kTileCols / 8)
     for (uint32_t r = 0; r < (uint32_t)kTileRows; ++r) {
-      const size_t base = (size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kBandUseful + lane * kWPL;
+      const size_t base = (size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kTileCols + lane * 8;
       const uint2 m = *reinterpret_cast<const uint2*>(srcmask + base);
       any |= (m.x | m.y) != 0;
     }
