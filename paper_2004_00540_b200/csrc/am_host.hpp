@@ -48,7 +48,7 @@ struct am_grid {
   void* val[2] = {nullptr, nullptr};
   int cur = 0;
   uint8_t* srcmask = nullptr;        // pitched 0/1 (owned rows + halo rows for slabs)
-  uint8_t* rowsrc = nullptr;         // per allocated row: any source
+  uint8_t* rowsrc = nullptr;         // per band and allocated row: a source in the band's columns (Geo::rowsrc_bytes)
   uint8_t* occ = nullptr;            // dense owned rows (re-initialisation / plain maps)
   uint8_t* srcmask_dense = nullptr;  // dense owned rows (plain maps)
   uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots + 1 CTA arrival counter (FlagSink::done)

@@ -53,7 +53,7 @@ constexpr int kTileRows = AM_TILE_ROWS;
 constexpr int kTileWPL = AM_TILE_WPL;
 constexpr int kTileCols = 32 * kTileWPL - 2 * kK;  // useful columns of a tile band
 #ifndef AM_TILE_CTAS
-#define AM_TILE_CTAS (AM_TILE_WPL == 4 ? 4 : 2)
+#define AM_TILE_CTAS 2  // 4 warps x 24 KB staged items each
 #endif
 constexpr int kTileCtasPerSm = AM_TILE_CTAS;  // k_block_tiles is persistent: this many CTAs per SM
 
@@ -68,6 +68,12 @@ struct Geo {
   uint32_t nchunks;       // row chunks of kTileRows (tile rows)
   uint32_t tbands;        // tile bands of kTileCols columns
   __host__ __device__ uint32_t ntiles() const { return tbands * nchunks; }
+  // per-band source-row flags (rowsrc): one byte per allocated row for each
+  // dense band, then for each tile band; set where the band's streamed
+  // columns (useful + halo) hold a source in that row
+  __host__ __device__ size_t rowsrc_bytes() const { return (size_t)(nbands + tbands) * rows; }
+  __host__ __device__ size_t dense_rowsrc(uint32_t band) const { return (size_t)band * rows; }
+  __host__ __device__ size_t tile_rowsrc(uint32_t tband) const { return (size_t)(nbands + tband) * rows; }
   __host__ __device__ size_t idx(uint32_t r, uint32_t c) const {
     return (size_t)(r + pad) * pitch + (c + pad);
   }

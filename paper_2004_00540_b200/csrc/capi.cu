@@ -199,7 +199,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   cudaError_t e = am::dmalloc(ctx, &g->val[0], cells * 2);
   if (!e) e = am::dmalloc(ctx, &g->val[1], cells * 2);
   if (!e) e = am::dmalloc(ctx, &g->srcmask, cells);
-  if (!e) e = am::dmalloc(ctx, &g->rowsrc, g->g.rows);
+  if (!e) e = am::dmalloc(ctx, &g->rowsrc, g->g.rowsrc_bytes());
   if (!e) e = am::dmalloc(ctx, &g->occ, dense);
   if (!e) e = am::dmalloc(ctx, &g->srcmask_dense, dense);
   if (!e) e = am::dmalloc(ctx, &g->d_flags, (kFlagSlots + 1) * sizeof(uint32_t));
@@ -217,7 +217,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->val[1], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->srcmask, 0, cells, s);
-  if (!e) e = cudaMemsetAsync(g->rowsrc, 0, g->g.rows, s);
+  if (!e) e = cudaMemsetAsync(g->rowsrc, 0, g->g.rowsrc_bytes(), s);
   if (!e) e = cudaMemsetAsync(g->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), s);  // armed slots
   if (!e) e = cudaMemsetAsync(g->d_flags + kFlagSlots, 0, sizeof(uint32_t), s);     // arrival counter
   if (!e) e = cudaMemsetAsync(g->srcmask_dense, 0, dense, s);

@@ -105,7 +105,7 @@ __device__ __forceinline__ void publish_flag(const FlagSink& f, uint32_t m, uint
 // SourceSet rasterisation for the grid rows [row0, row0+H) of a total_h-row
 // grid (grid.hpp:78-90): validates every source, marks owned sources in the
 // dense mask, and marks owned + halo-band sources in the pitched mask and
-// the per-row flags (a slab recomputes its halo rows inside a block).
+// the per-band row flags (a slab recomputes its halo rows inside a block).
 __global__ void k_srcmask_rows(Geo g, uint32_t total_h, uint32_t row0, const uint32_t* __restrict__ rc, uint64_t n,
                                uint8_t* __restrict__ dense, const uint8_t* __restrict__ occ,
                                uint8_t* __restrict__ srcmask, uint8_t* __restrict__ rowsrc, int* __restrict__ err) {
@@ -126,8 +126,14 @@ __global__ void k_srcmask_rows(Geo g, uint32_t total_h, uint32_t row0, const uin
   }
   const long arow = local + g.pad;
   if (arow >= 0 && arow < (long)g.rows) {
-    srcmask[(size_t)arow * g.pitch + c + g.pad] = 1;
-    rowsrc[arow] = 1;
+    const uint32_t ac = c + g.pad;  // allocated column
+    srcmask[(size_t)arow * g.pitch + ac] = 1;
+    // bands whose streamed columns [b*useful, b*useful + width) hold ac
+    const int db0 = ac >= (uint32_t)kBand ? (int)((ac - kBand) / kBandUseful) + 1 : 0;
+    for (int b = db0; b <= (int)(ac / kBandUseful) && b < (int)g.nbands; ++b) rowsrc[g.dense_rowsrc(b) + arow] = 1;
+    constexpr uint32_t kTW = 32 * kTileWPL;
+    const int tb0 = ac >= kTW ? (int)((ac - kTW) / kTileCols) + 1 : 0;
+    for (int b = tb0; b <= (int)(ac / kTileCols) && b < (int)g.tbands; ++b) rowsrc[g.tile_rowsrc(b) + arow] = 1;
   }
 }
 
@@ -158,6 +164,10 @@ __global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __
     reinterpret_cast<uint4*>(val + i)[1] = make_uint4(v[4], v[5], v[6], v[7]);
   }
 }
+
+#ifdef AM_DEBUG_CLOCK
+__device__ long long am_dbg_clock[64];
+#endif
 
 // ----------------------------------------------------------- K1+K2 block
 template <int CB, int WPL>
@@ -226,6 +236,41 @@ struct Rows<32, WPL> {
     for (int w = 0; w < WPL; ++w) s[w] = (a4[w / 4] >> (8 * (w % 4))) & 0xFFu;
   }
 };
+
+// Layer j of one streaming step (see stream_step), no sources.
+template <int CB, int PH, int WPL>
+__device__ __forceinline__ void stream_layer(int j, uint32_t (&x)[WPL], uint32_t (&P0)[kK][WPL],
+                                             uint32_t (&P1)[kK][WPL]) {
+  using C = Cell<CB>;
+  uint32_t v[WPL];
+#pragma unroll
+  for (int w = 0; w < WPL; ++w) v[w] = C::max3(P0[j][w], P1[j][w], x[w]);
+  const uint32_t left = __shfl_up_sync(0xffffffffu, v[WPL - 1], 1);
+  const uint32_t right = __shfl_down_sync(0xffffffffu, v[0], 1);
+#pragma unroll
+  for (int w = 0; w < WPL; ++w) {
+    if (PH == 0) P0[j][w] = x[w];
+    else P1[j][w] = x[w];
+  }
+#pragma unroll
+  for (int w = 1; w < WPL - 1; ++w) x[w] = C::max3(v[w - 1], v[w], v[w + 1]) & ((PH == 0 ? P1[j][w] : P0[j][w]) | C::LOW);
+  x[0] = C::max3(left, v[0], v[1]) & ((PH == 0 ? P1[j][0] : P0[j][0]) | C::LOW);
+  x[WPL - 1] = C::max3(v[WPL - 2], v[WPL - 1], right) & ((PH == 0 ? P1[j][WPL - 1] : P0[j][WPL - 1]) | C::LOW);
+}
+
+// Steps t (x0, window slot PH 0) and t+1 (x1, slot PH 1) without sources,
+// skewed: step t+1's layer j only needs step t's layer j-1, so layer j of
+// step t and layer j-1 of step t+1 are independent and issue side by side
+// (a warp issues in order; this halves the dependent chain per row pair).
+template <int CB, int WPL>
+__device__ __forceinline__ void stream_step2(uint32_t (&x0)[WPL], uint32_t (&x1)[WPL], uint32_t (&P0)[kK][WPL],
+                                             uint32_t (&P1)[kK][WPL]) {
+#pragma unroll
+  for (int j = 0; j <= kK; ++j) {
+    if (j < kK) stream_layer<CB, 0, WPL>(j, x0, P0, P1);
+    if (j >= 1) stream_layer<CB, 1, WPL>(j - 1, x1, P0, P1);
+  }
+}
 
 // One streaming step: x holds the newly loaded row (layer 0, row t); layer j
 // produces row t-j from layer j-1's rows t-j-1, t-j (window) and t-j+1 (x).
@@ -309,6 +354,9 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 #ifndef AM_TILE_PAIR
 #define AM_TILE_PAIR 1
 #endif
+#ifndef AM_SKEW
+#define AM_SKEW 1
+#endif
 
 constexpr int kStages = AM_STAGES;                 // rows in flight per warp (dense sweep)
 constexpr int kTileStages = AM_TILE_STAGES;        // rows in flight per warp (active tiles: few warps per SM)
@@ -317,7 +365,7 @@ template <int WPL>
 constexpr int stage_bytes() { return 32 * WPL * 4; }
 constexpr int kWarpsPerCta = kBlockThreads / 32;
 constexpr int kBlockSmem = kWarpsPerCta * kStages * stage_bytes<kWPL>();
-constexpr int kTileSmem = kWarpsPerCta * kTileStages * stage_bytes<kTileWPL>();
+constexpr int kTileWarpSmemRing = kTileStages * stage_bytes<kTileWPL>();
 
 template <int CB, int WPL>
 __device__ __forceinline__ void stage_words(const uint8_t* stage, int lane, uint32_t (&x)[WPL]) {
@@ -368,11 +416,12 @@ __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw);
 // `in + delta`; bit r of `homes` (r = 0 above, 1 inside, 2 below the item)
 // says tile A's region r is read from the second field, bits 3..5 the same
 // for B, bit 6 / 7 that A's / B's output goes to `out + delta`.
-template <int CB, bool SLAB, bool LAG = false, int ST = kStages, int WPL = kWPL>
+template <int CB, bool SLAB, bool LAG = false, int ST = kStages, int WPL = kWPL, int RS = ST * stage_bytes<WPL>()>
 __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cell<CB>::T* __restrict__ in,
                                                 typename Cell<CB>::T* __restrict__ out,
                                                 const uint8_t* __restrict__ srcmask,
-                                                const uint8_t* __restrict__ rowsrc, uint32_t bA, uint32_t rA,
+                                                const uint8_t* __restrict__ rfA, const uint8_t* __restrict__ rfB,
+                                                uint32_t bA, uint32_t rA,
                                                 uint32_t bB, uint32_t rB, uint32_t rows, bool hasB,
                                                 uint32_t lag0 = 0, uint32_t lag1 = 0, uint32_t lag2 = 0,
                                                 ptrdiff_t delta = 0, uint32_t homes = 0, uint32_t* edge_min = nullptr) {
@@ -409,7 +458,7 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int kSB = stage_bytes<WPL>();
   constexpr int kLaneBytes = WPL * CB / 8;  // one tile row of this lane
-  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * ST * kSB;
+  uint8_t* ring = smem_raw + (threadIdx.x >> 5) * RS;  // RS: bytes of shared memory per warp
   auto issue = [&](uint32_t step) {
     uint8_t* dst = ring + (step % ST) * kSB;
     if (step < T_steps) {
@@ -434,76 +483,234 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+#ifdef AM_DEBUG_CLOCK  // tools/item_clock.cu: per-iteration timestamps of CTA 0 / warp 0
+  const bool dbg = blockIdx.x == 0 && threadIdx.x == 0;
+  if (dbg) am_dbg_clock[0] = clock64();
+#endif
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) issue(s);
   // source-row flags arrive as a 32-row ballot window, loaded one window ahead
   auto row_flag = [&](uint32_t step) -> uint32_t {
     if (step >= T_steps) return 0u;
-    uint32_t f = rowsrc[rA + step];
-    if (CB == 16) f |= rowsrc[rB + step];
+    uint32_t f = rfA[rA + step];
+    if (CB == 16) f |= rfB[rB + step];
     return f;
   };
   uint32_t flag_lane = row_flag(lane), flag_win = 0;
+  // Output row handling of step tt (x = the row after the last layer).
+  auto emit = [&](uint32_t tt, const uint32_t (&x)[WPL]) {
+    if (!(tt >= 2 * kK && tt < 2 * kK + rows && store_lane)) return;
+    const size_t roff = (size_t)tt * pitch;
+    if constexpr (LAG) {  // also track the first / last kK output rows (tile edge regions)
+      Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
+      uint32_t rm = 0xFFFFFFFFu;
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) rm = C::acc_min(x[w], rm);
+      acc = C::vmin(acc, rm);
+      const uint32_t orow = tt - 2 * kK;
+      if (orow < (uint32_t)kK) accTop = C::vmin(accTop, rm);
+      if (orow >= rows - kK) accBot = C::vmin(accBot, rm);
+    } else if constexpr (!SLAB) {
+      Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) acc = C::acc_min(x[w], acc);
+    } else {
+      const uint32_t orow = tt - 2 * kK;
+      const bool wa = rA + orow < g.H, wb = rB + orow < g.H;
+      Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
+      const uint32_t keep = Rows<CB, WPL>::valid_bits(wa, wb);
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) acc = C::acc_min(x[w] & keep, acc);
+    }
+  };
+  constexpr uint32_t kInFlight = ((1u << kK) - 1u) << 1;  // rows t-1 .. t-kK of a step's srcbits
+  // Two steps per iteration.  On the common path (no source row in flight)
+  // both steps sit in one branch-free block, so the scheduler overlaps step
+  // t+1's early layers with step t's late ones (they are independent).
   for (uint32_t t = 0; t < T_steps; t += 2) {
     if ((t & 31u) == 0) {
       flag_win = __ballot_sync(0xffffffffu, flag_lane != 0u);
       flag_lane = row_flag(t + 32 + lane);
     }
+    uint32_t x0[WPL], x1[WPL];
+    issue(t + ST - 1);  // refills the slot consumed by the previous step
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 1) : "memory");
+    stage_words<CB, WPL>(ring + (t % ST) * kSB, lane, x0);
+    issue(t + ST);  // the slot of row t, now in registers
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 1) : "memory");
+    stage_words<CB, WPL>(ring + ((t + 1) % ST) * kSB, lane, x1);
+    if constexpr (LAG) {
+      auto lag_of = [&](uint32_t tt) { return tt < (uint32_t)kK ? lag0 : (tt < kK + rows ? lag1 : lag2); };
+      const uint32_t l0w = lag_of(t), l1w = lag_of(t + 1);
+      if (__any_sync(0xffffffffu, (l0w | l1w) != 0u)) {
 #pragma unroll
-    for (int ph = 0; ph < 2; ++ph) {
-      const uint32_t tt = t + ph;
-      uint32_t x[WPL];
-      issue(tt + ST - 1);  // refills the slot consumed by the previous step
-      asm volatile("cp.async.wait_group %0;" ::"n"(ST - 1) : "memory");
-      stage_words<CB, WPL>(ring + (tt % ST) * kSB, lane, x);
-      if constexpr (LAG) {
-        const uint32_t lw = tt < (uint32_t)kK ? lag0 : (tt < kK + rows ? lag1 : lag2);
-        if (__any_sync(0xffffffffu, lw != 0u)) {
-#pragma unroll
-          for (int w = 0; w < WPL; ++w) x[w] = add_lag<CB>(x[w], lw);
-        }
-      }
-      const size_t roff = (size_t)tt * pitch;
-      srcbits = (srcbits << 1) | ((flag_win >> (tt & 31u)) & 1u);
-      // rows t-1 .. t-kK are in flight; only steps that touch a source row pay for the +1
-      const bool src_rows = __any_sync(0xffffffffu, (srcbits & (((1u << kK) - 1u) << 1)) != 0u);
-      if (ph == 0) {
-        if (src_rows) stream_step<CB, 0, true, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-        else stream_step<CB, 0, false, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-      } else {
-        if (src_rows) stream_step<CB, 1, true, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-        else stream_step<CB, 1, false, WPL>(x, P0, P1, srcbits, sA + roff, sB + roff, pitch, lane);
-      }
-      if (tt >= 2 * kK && tt < 2 * kK + rows && store_lane) {
-        if constexpr (LAG) {  // also track the first / last kK output rows (tile edge regions)
-          Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
-          uint32_t rm = 0xFFFFFFFFu;
-#pragma unroll
-          for (int w = 0; w < WPL; ++w) rm = C::acc_min(x[w], rm);
-          acc = C::vmin(acc, rm);
-          const uint32_t orow = tt - 2 * kK;
-          if (orow < (uint32_t)kK) accTop = C::vmin(accTop, rm);
-          if (orow >= rows - kK) accBot = C::vmin(accBot, rm);
-        } else if constexpr (!SLAB) {
-          Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, true, hasB);
-#pragma unroll
-          for (int w = 0; w < WPL; ++w) acc = C::acc_min(x[w], acc);
-        } else {
-          const uint32_t orow = tt - 2 * kK;
-          const bool wa = rA + orow < g.H, wb = rB + orow < g.H;
-          Rows<CB, WPL>::store(x, oA + roff - (size_t)kK * pitch, oB + roff - (size_t)kK * pitch, wa, wb);
-          const uint32_t keep = Rows<CB, WPL>::valid_bits(wa, wb);
-#pragma unroll
-          for (int w = 0; w < WPL; ++w) acc = C::acc_min(x[w] & keep, acc);
+        for (int w = 0; w < WPL; ++w) {
+          x0[w] = add_lag<CB>(x0[w], l0w);
+          x1[w] = add_lag<CB>(x1[w], l1w);
         }
       }
     }
+    const uint32_t sb0 = (srcbits << 1) | ((flag_win >> (t & 31u)) & 1u);
+    const uint32_t sb1 = (sb0 << 1) | ((flag_win >> ((t + 1) & 31u)) & 1u);
+    srcbits = sb1;
+    const size_t r0 = (size_t)t * pitch, r1 = r0 + pitch;
+    // only steps that touch a source row pay for the +1 (warp-uniform)
+    if (__any_sync(0xffffffffu, ((sb0 | sb1) & kInFlight) != 0u)) {
+      stream_step<CB, 0, true, WPL>(x0, P0, P1, sb0, sA + r0, sB + r0, pitch, lane);
+      stream_step<CB, 1, true, WPL>(x1, P0, P1, sb1, sA + r1, sB + r1, pitch, lane);
+    } else {
+#if AM_SKEW
+      stream_step2<CB, WPL>(x0, x1, P0, P1);
+#else
+      stream_step<CB, 0, false, WPL>(x0, P0, P1, sb0, sA + r0, sB + r0, pitch, lane);
+      stream_step<CB, 1, false, WPL>(x1, P0, P1, sb1, sA + r1, sB + r1, pitch, lane);
+#endif
+    }
+    emit(t, x0);
+    emit(t + 1, x1);
+#ifdef AM_DEBUG_CLOCK
+    if (dbg && t / 2 + 1 < 63) am_dbg_clock[t / 2 + 1] = clock64();
+#endif
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   if constexpr (LAG) {
     edge_min[0] = accTop;
     edge_min[1] = accBot;
   }
+  return acc;
+}
+
+// ---- active tiles, 16-bit cells: the whole item staged up front ----------
+//
+// An item (tiles A and B, kTileSteps rows each) is small enough to stage
+// completely: every lane issues all of its 8 B row pieces with cp.async at
+// the start (three commit groups, one per input region), so no per-row
+// address arithmetic or ring bookkeeping remains in the loop.  The steps
+// then run in five phases with compile-time roles (input region -> lag,
+// output rows -> top / middle / bottom minima); items whose rows hold a
+// source take the general stream_item path.
+constexpr int kTileSteps = kTileRows + 2 * kK;                 // rows streamed per item
+constexpr int kTileRowBytes = 32 * kTileWPL * 2;               // one u16 tile row of a warp
+constexpr int kTileBufBytes = kTileSteps * 2 * kTileRowBytes;  // A and B rows of an item
+static_assert(kTileWPL == 4, "the staged item path loads 8 B per lane and tile row");
+constexpr int kTileWarpSmem = kTileBufBytes > kTileWarpSmemRing ? kTileBufBytes : kTileWarpSmemRing;
+constexpr int kTileSmem = kWarpsPerCta * kTileWarpSmem;  // dynamic shared memory of k_block_tiles
+static_assert(kTileRows >= 2 * kK && kTileRows % 2 == 0, "top and bottom edge rows must not overlap");
+
+enum { kOutNone = 0, kOutTop = 1, kOutMid = 2, kOutBot = 3 };
+
+template <int OUT>
+__device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, uint32_t lagw, bool lag,
+                                           uint32_t (&P0)[kK][4], uint32_t (&P1)[kK][4], uint16_t*& oA,
+                                           uint16_t*& oB, size_t pitch, bool st_a, bool st_b, uint32_t& acc,
+                                           uint32_t& acc_edge) {
+  using C = Cell<16>;
+  auto words = [](uint2 a, uint2 b, uint32_t (&x)[4]) {
+    x[0] = __byte_perm(a.x, b.x, 0x5410);
+    x[1] = __byte_perm(a.x, b.x, 0x7632);
+    x[2] = __byte_perm(a.y, b.y, 0x5410);
+    x[3] = __byte_perm(a.y, b.y, 0x7632);
+  };
+  auto emit = [&](const uint32_t (&x)[4]) {
+    if (st_a) *reinterpret_cast<uint2*>(oA) = make_uint2(__byte_perm(x[0], x[1], 0x5410), __byte_perm(x[2], x[3], 0x5410));
+    if (st_b) *reinterpret_cast<uint2*>(oB) = make_uint2(__byte_perm(x[0], x[1], 0x7632), __byte_perm(x[2], x[3], 0x7632));
+    oA += pitch;
+    oB += pitch;
+    if constexpr (OUT == kOutMid) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) acc = C::acc_min(x[w], acc);
+    } else {
+      uint32_t rm = 0xFFFFFFFFu;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) rm = C::acc_min(x[w], rm);
+      acc = C::vmin(acc, rm);
+      acc_edge = C::vmin(acc_edge, rm);
+    }
+  };
+#pragma unroll 1
+  for (int s = s0; s < s1; s += 2) {
+    const uint8_t* r = buf + s * 2 * kTileRowBytes;
+    uint32_t x0[4], x1[4];
+    words(*reinterpret_cast<const uint2*>(r), *reinterpret_cast<const uint2*>(r + kTileRowBytes), x0);
+    words(*reinterpret_cast<const uint2*>(r + 2 * kTileRowBytes), *reinterpret_cast<const uint2*>(r + 3 * kTileRowBytes),
+          x1);
+    if (lag) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        x0[w] = add_lag<16>(x0[w], lagw);
+        x1[w] = add_lag<16>(x1[w], lagw);
+      }
+    }
+    stream_step2<16, 4>(x0, x1, P0, P1);
+    if constexpr (OUT != kOutNone) {
+      emit(x0);
+      emit(x1);
+    }
+  }
+}
+
+// Same contract as stream_item<16, false, true, .., kTileWPL> for tile items
+// without source rows; buf = this warp's kTileBufBytes of shared memory.
+__device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta,
+                                                uint32_t bA, uint32_t cA, uint32_t bB, uint32_t cB, bool hasB,
+                                                const uint32_t (&lw)[3], uint32_t homes, uint32_t* edge_min,
+                                                uint8_t* buf) {
+  const int lane = threadIdx.x & 31;
+  const size_t pitch = g.pitch;
+  const uint32_t colA = bA * kTileCols + lane * kTileWPL, colB = bB * kTileCols + lane * kTileWPL;
+  const uint32_t rA = cA * kTileRows, rB = cB * kTileRows;  // allocated row of step 0
+  // Lanes 0-15 copy tile A's row (256 B), lanes 16-31 tile B's, 16 B each
+  // (L2-only cp.async.cg); the staged rows are read back by all lanes after
+  // the group wait and a warp barrier.
+  __syncwarp();  // every lane is done reading the previous item's rows
+  {
+    const int half = lane >> 4;
+    // the 8 cells this lane copies belong to compute lanes 2*lane, 2*lane+1 (mod 32): their band's homes
+    const uint32_t ch = __shfl_sync(0xffffffffu, homes, (2 * lane) & 31);
+    uint8_t* dst = buf + lane * 16;
+    const uint32_t col = (half ? bB : bA) * kTileCols + (lane & 15) * 8, r0 = half ? rB : rA;
+    int s = 0;
+#pragma unroll
+    for (int reg = 0; reg < 3; ++reg) {
+      const uint16_t* q = f0 + (((ch >> (3 * half + reg)) & 1u) ? delta : 0) + (size_t)(r0 + s) * pitch + col;
+      const int e = reg == 0 ? kK : (reg == 1 ? kK + kTileRows : kTileSteps);
+#pragma unroll 4
+      for (; s < e; ++s) {
+        cp_async16(dst + s * 2 * kTileRowBytes, q);
+        q += pitch;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  }
+  uint32_t P0[kK][4], P1[kK][4];
+#pragma unroll
+  for (int j = 0; j < kK; ++j)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) P0[j][w] = P1[j][w] = 0u;
+  uint32_t acc = 0xFFFFFFFFu, accTop = 0xFFFFFFFFu, accBot = 0xFFFFFFFFu;
+  const ptrdiff_t od_a = ((homes >> 6) & 1u) ? delta : 0, od_b = ((homes >> 7) & 1u) ? delta : 0;
+  uint16_t* oA = f0 + od_a + (size_t)(rA + kK) * pitch + colA;  // tile row 0
+  uint16_t* oB = f0 + od_b + (size_t)(rB + kK) * pitch + colB;
+  const bool st_lane = lane >= kK / kTileWPL && lane < 32 - kK / kTileWPL;
+  const bool sa = st_lane, sb = st_lane && hasB;
+  const uint8_t* rb = buf + lane * 8;
+  auto any_lag = [](uint32_t l) { return __any_sync(0xffffffffu, l != 0u); };
+  asm volatile("cp.async.wait_group 2;" ::: "memory");
+  __syncwarp();
+  tile_phase<kOutNone>(rb, 0, kK, lw[0], any_lag(lw[0]), P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncwarp();
+  const bool l1 = any_lag(lw[1]);
+  tile_phase<kOutNone>(rb, kK, 2 * kK, lw[1], l1, P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
+  tile_phase<kOutTop>(rb, 2 * kK, 3 * kK, lw[1], l1, P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
+  tile_phase<kOutMid>(rb, 3 * kK, kK + kTileRows, lw[1], l1, P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  tile_phase<kOutBot>(rb, kK + kTileRows, kTileSteps, lw[2], any_lag(lw[2]), P0, P1, oA, oB, pitch, sa, sb, acc,
+                      accBot);
+  if (!st_lane) acc = accTop = accBot = 0xFFFFFFFFu;  // halo lanes hold no output
+  edge_min[0] = accTop;
+  edge_min[1] = accBot;
   return acc;
 }
 
@@ -520,7 +727,8 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
   const uint32_t band = warp % g.nbands, tile = warp / g.nbands;
   const uint32_t rA = tile * g.seg_len;  // allocated row of step 0
   const uint32_t rB = (CB == 16 ? tile + ntiles : tile) * g.seg_len;
-  const uint32_t acc = stream_item<CB, SLAB>(g, in, out, srcmask, rowsrc, band, rA, band, rB, g.seg_len, true);
+  const uint8_t* rf = rowsrc + g.dense_rowsrc(band);
+  const uint32_t acc = stream_item<CB, SLAB>(g, in, out, srcmask, rf, rf, band, rA, band, rB, g.seg_len, true);
   publish_flag<false>(flag, __reduce_min_sync(0xffffffffu, Cell<CB>::fold(acc)), g.nbands * ntiles);
 }
 
@@ -539,6 +747,7 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
                   const uint8_t* __restrict__ rowsrc, const uint32_t* __restrict__ list,
                   const uint32_t* __restrict__ count, uint16_t* __restrict__ front, const uint32_t* __restrict__ state,
                   uint32_t l0, FlagSink flag) {
+  extern __shared__ __align__(128) uint8_t smem_tiles[];
   const uint32_t n = *count;
   // Pairing two tiles per warp halves the instructions but also the warps;
   // with few active tiles the kernel is latency bound and more warps win.
@@ -575,9 +784,24 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     const uint32_t sa = state[cA * g.tbands + bA], sb = state[cB * g.tbands + bB];
     homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
     uint32_t edge[2];
-    const uint32_t acc = stream_item<CB, false, true, kTileStages, kTileWPL>(
-        g, f0, f0, srcmask, rowsrc, bA, cA * kTileRows, bB, cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2], delta,
-        homes, edge);
+    uint32_t acc;
+    bool staged = false;
+    if constexpr (CB == 16) {  // rows holding a source need the +1 path
+      const uint32_t ra = cA * kTileRows, rb = cB * kTileRows;
+      const uint8_t* rfa = rowsrc + g.tile_rowsrc(bA) + ra;
+      const uint8_t* rfb = rowsrc + g.tile_rowsrc(bB) + rb;
+      uint32_t f = rfa[lane] | rfb[lane];
+      if (lane < kTileSteps - 32) f |= rfa[32 + lane] | rfb[32 + lane];
+      staged = !__any_sync(0xffffffffu, f != 0u);
+      if (staged)
+        acc = tile_item16(g, f0, delta, bA, cA, bB, cB, hasB, lw, homes, edge,
+                          smem_tiles + (threadIdx.x >> 5) * kTileBufBytes);
+    }
+    if (!staged)
+      acc = stream_item<CB, false, true, kTileStages, kTileWPL, kTileWarpSmem>(
+          g, f0, f0, srcmask, rowsrc + g.tile_rowsrc(bA), rowsrc + g.tile_rowsrc(bB), bA, cA * kTileRows, bB,
+          cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2],
+          delta, homes, edge);
     // Frontier regions of each tile: cells with a == 1 (covered in the block's
     // last layer; min(a-1) == 0) anywhere / in the first or last kK rows / in
     // the first or last kK useful columns (the lanes next to the halo lanes) /
@@ -947,6 +1171,12 @@ void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
                         const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
                         const uint32_t* state, uint32_t l0, FlagSink flag, cudaStream_t s) {
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_block_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+    cudaFuncSetAttribute(k_block_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+    return true;
+  }();
+  (void)attr;
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
     k_block_tiles<16><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, list, count,

@@ -17,7 +17,7 @@ def main():
     ctx = am.Context(0)
     g = am.Grid(occ, src, ctx)
     nt = g.info()["tiles"]
-    stride = 7919  # spread the items over the grid (prime, co-prime to the tile count)
+    stride = int(os.environ.get("PROBE_STRIDE", 7919))  # 7919: spread over the grid (prime); 1: adjacent tiles
     sizes = [int(a) for a in sys.argv[1:]] or [1, 2, 8, 32, 148, 296, 592, 1000, 1184, 1500, 2368, 4736, 9472]
     for items in sizes:
         ms = g.bench_tile_kernel(items, stride, 30)
