@@ -64,13 +64,13 @@ struct am_grid {
   int slab = 0;
   uint32_t total_h = 0, row0 = 0;
   // active-tile skipping state (single grids; stencil.cu k_tiles_*)
-  uint16_t* t_front[2] = {nullptr, nullptr}; // frontier region bits: [t_fi] = last block, [t_fi^1] = being written
-  int t_fi = 0;
-  uint32_t* t_state[2] = {nullptr, nullptr}; // per tile: layer << 1 | home field; [t_si] = current
-  int t_si = 0;
-  uint32_t* t_list = nullptr;                // work list (band << 16 | chunk)
-  uint32_t* t_count = nullptr;               // [0..1] alternating work-list lengths
+  unsigned long long* t_state = nullptr;     // per tile: old << 32 | cur (am::TileBook)
+  uint32_t* t_sched = nullptr;               // per tile: index + 1 of the block it is listed for
+  uint32_t* t_list[2] = {nullptr, nullptr};  // work lists (band << 16 | chunk) by block parity
+  uint32_t* t_count = nullptr;               // [3] list lengths by block index mod 3
   unsigned long long* t_processed = nullptr; // tiles processed (statistics)
+  uint32_t t_blk = 0;                        // index of the next tile block (list / counter selection)
+  am::TileBook book() const { return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed}; }
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;
   uint64_t* d_counts = nullptr;

@@ -92,6 +92,24 @@ struct FlagSink {
   uint32_t* host;  // mapped mirror slot, or null (word left for the caller)
 };
 
+// Active-tile bookkeeping (stencil.cu k_block_tiles / k_tiles_*).  A tile's
+// state word is  old << 32 | cur  with cur = layer << 1 | home field of the
+// tile's latest values; a tile processed in the running block writes
+// cur = (l0 + kK) << 1 | home^1 and keeps its pre-block word in `old`, so a
+// neighbour reading it during the same block can still tell the values it
+// must read (cur's layer == l0 + kK marks "processed in this block").  Work
+// lists are pushed by the processed tiles themselves: block `blk` reads
+// list[blk & 1] / count[blk % 3], appends to list[(blk+1) & 1] /
+// count[(blk+1) % 3] (deduplicated by sched[t] = the index + 1 of the block
+// a tile is listed for) and clears count[(blk+2) % 3].
+struct TileBook {
+  unsigned long long* state;
+  uint32_t* sched;
+  uint32_t* list[2];
+  uint32_t* count;                // [3]
+  unsigned long long* processed;  // tiles processed (statistics)
+};
+
 // ---- kernels (stencil.cu) ----
 void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcmask, void* d_val,
                  int cell_bits, cudaStream_t s);
@@ -103,15 +121,15 @@ void launch_block(const Geo& g, int cell_bits, bool slab, const void* in, void* 
 void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const uint8_t* srcmask,
                   uint32_t* flag, cudaStream_t s);
 // active-tile skipping (stencil.cu)
-void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint16_t* front, cudaStream_t s);
-void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front_next, uint32_t* const states[2],
-                       int parity, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters, uint32_t* flag,
-                       unsigned long long* processed, cudaStream_t s);
+// lists the tiles of block 0: the 3x3 tile neighbourhood of every tile holding a source
+void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cudaStream_t s);
+// every tile current at `layer` in field `home`, all listed for block blk
+void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer, int home, cudaStream_t s);
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
-                        const uint32_t* state, uint32_t l0, FlagSink flag, cudaStream_t s);
-void launch_tiles_finalize(const Geo& g, int cell_bits, uint32_t* state, void* f0, void* f1, int dst, uint32_t l,
-                           cudaStream_t s);
+                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                        cudaStream_t s);
+void launch_tiles_finalize(const Geo& g, int cell_bits, unsigned long long* state, void* f0, void* f1, int dst,
+                           uint32_t l, cudaStream_t s);
 void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);
 void launch_zero_check(const Geo& g, int cell_bits, const void* val, uint32_t* flag, cudaStream_t s);
 void launch_decode(const Geo& g, int cell_bits, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,

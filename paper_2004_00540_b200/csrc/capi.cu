@@ -155,11 +155,10 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->d_offsets);
   am::dfree(ctx, g->d_status);
   am::dfree(ctx, g->d_pts);
-  am::dfree(ctx, g->t_front[0]);
-  am::dfree(ctx, g->t_front[1]);
-  am::dfree(ctx, g->t_state[0]);
-  am::dfree(ctx, g->t_state[1]);
-  am::dfree(ctx, g->t_list);
+  am::dfree(ctx, g->t_state);
+  am::dfree(ctx, g->t_sched);
+  am::dfree(ctx, g->t_list[0]);
+  am::dfree(ctx, g->t_list[1]);
   am::dfree(ctx, g->t_count);
   am::dfree(ctx, g->t_processed);
   delete g;
@@ -206,12 +205,11 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = take_flag_set(ctx, &g->fs);
   if (!slab) {  // active-tile skipping state
     const size_t nt = g->g.ntiles();
-    if (!e) e = am::dmalloc(ctx, &g->t_front[0], nt * 2);
-    if (!e) e = am::dmalloc(ctx, &g->t_front[1], nt * 2);
-    if (!e) e = am::dmalloc(ctx, &g->t_state[0], nt * 4);
-    if (!e) e = am::dmalloc(ctx, &g->t_state[1], nt * 4);
-    if (!e) e = am::dmalloc(ctx, &g->t_list, nt * 4);
-    if (!e) e = am::dmalloc(ctx, &g->t_count, 8);  // alternating work-list counters
+    if (!e) e = am::dmalloc(ctx, &g->t_state, nt * 8);
+    if (!e) e = am::dmalloc(ctx, &g->t_sched, nt * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_list[0], nt * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_list[1], nt * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_count, 3 * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_processed, 8);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
@@ -292,7 +290,7 @@ am_status am_grid_get_info(const am_grid* g, am_grid_info* o) {
   o->layers_computed = g->computed;
   o->tile_rows = am::kTileRows;
   o->tile_cols = am::kTileCols;
-  o->tiles = g->t_state[0] ? g->g.ntiles() : 0;
+  o->tiles = g->t_state ? g->g.ntiles() : 0;
   return AM_OK;
 }
 
@@ -397,34 +395,30 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
 
   // exact active-tile skipping: single grids in batched mode
   am_grid* tg = slabs[0].g;
-  const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_state[0] && mode == AM_MODE_BATCHED &&
+  const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_state && mode == AM_MODE_BATCHED &&
                      !(ctx->flags & AM_CTX_DENSE);
   const size_t nt = tiles ? tg->g.ntiles() : 0;
   const int tile_ctas = ctx->sms * kTileCtasPerSm;  // persistent k_block_tiles
   // after dense work: every tile current at at_layer in val[cur], all active next block
   auto tiles_all_active = [&](uint32_t at_layer) -> am_status {
-    CK(cudaMemsetAsync(tg->t_front[tg->t_fi], 0xFF, nt * 2, ctx->stream));
-    std::vector<uint32_t> e(nt, at_layer << 1 | (uint32_t)tg->cur);
-    CK(cudaMemcpyAsync(tg->t_state[tg->t_si], e.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    launch_tiles_all(tg->g, tg->book(), tg->t_blk, at_layer, tg->cur, ctx->stream);
+    CKL();
     return AM_OK;
   };
   // every tile current at at_layer in val[0] (then cur = 0)
   auto tiles_finalize = [&](uint32_t at_layer) -> am_status {
-    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_state[tg->t_si], tg->val[0], tg->val[1], 0, at_layer,
-                          ctx->stream);
+    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_state, tg->val[0], tg->val[1], 0, at_layer, ctx->stream);
     CKL();
     tg->cur = 0;
     return AM_OK;
   };
   if (tiles) {  // layer 0 lives in val[cur] (= val[0] after reset_map): state 0 << 1 | 0
-    tg->t_fi = 0;
-    tg->t_si = 0;
-    CK(cudaMemsetAsync(tg->t_state[0], 0, nt * 4, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_front[1], 0, nt * 2, ctx->stream));
+    tg->t_blk = 0;
+    CK(cudaMemsetAsync(tg->t_state, 0, nt * 8, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_sched, 0, nt * 4, ctx->stream));
     CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_count, 0, 8, ctx->stream));
-    launch_tiles_init(tg->g, tg->srcmask, tg->t_front[0], ctx->stream);
+    CK(cudaMemsetAsync(tg->t_count, 0, 3 * 4, ctx->stream));
+    launch_tiles_init(tg->g, tg->srcmask, tg->book(), ctx->stream);
     CKL();
   }
 
@@ -497,8 +491,8 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       uint32_t* flag = g->d_flags + slot;
       words[i] = flag;
       cudaStream_t s = c->stream;
-      // the tile planner resets its own slot; a mapped slot is re-armed by the launch that used it
-      if (autom && !(tiles && blocked) && !(mapped && blocked && armed[slot])) {
+      // a mapped slot is re-armed by the launch that used it
+      if (autom && !(mapped && blocked && armed[slot])) {
         cudaError_t e = cudaMemsetAsync(flag, 0xFF, sizeof(uint32_t), s);
         if (e) return fail(c, AM_ECUDA, "memset: %s", cudaGetErrorString(e));
       }
@@ -518,15 +512,10 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
           run_open = true;
         }
         if (tiles) {
-          // the planner zeroes the other counter slot for the next block and writes the next states
-          uint32_t* cnt = g->t_count + g->t_si;
-          launch_tiles_plan(g->g, g->t_front[g->t_fi], g->t_front[g->t_fi ^ 1], g->t_state, g->t_si, l, kk,
-                            g->t_list, g->t_count, autom ? flag : nullptr, g->t_processed, s);
-          CKL();
-          launch_block_tiles(g->g, g->cell_bits, tile_ctas, g->val[0], g->val[1], g->srcmask, g->rowsrc,
-                             g->t_list, cnt, g->t_front[g->t_fi ^ 1], g->t_state[g->t_si], l, sink, s);
-          g->t_fi ^= 1;
-          g->t_si ^= 1;
+          // the tiles of this block list the next block's tiles themselves (TileBook)
+          launch_block_tiles(g->g, g->cell_bits, tile_ctas, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->book(),
+                             g->t_blk, l, sink, s);
+          ++g->t_blk;
         } else {
           launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, sink, s);
         }
@@ -983,7 +972,7 @@ am_status am_propagate_reference(am_ctx* ctx, uint32_t W, uint32_t H, const uint
 
 am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t stride, uint32_t reps,
                                float* ms_per_launch) {
-  if (!ctx || !g || !ms_per_launch || !g->t_state[0] || reps == 0 || stride == 0) return AM_EINVAL;
+  if (!ctx || !g || !ms_per_launch || !g->t_state || reps == 0 || stride == 0) return AM_EINVAL;
   CK(cudaSetDevice(ctx->device));
   am_status st = am::reset_map(ctx, g, 16);
   if (st) return st;
@@ -996,17 +985,21 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
     list[i] = (t % g->g.nbands) << 16 | (t / g->g.nbands);
   }
   cudaStream_t s = ctx->stream;
-  CK(cudaMemsetAsync(g->t_state[0], 0, (size_t)nt * 4, s));
-  CK(cudaMemcpyAsync(g->t_list, list.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  // block 0 every launch: list[0] / count[0] stay, the pushes for block 1 are deduplicated away
+  CK(cudaMemsetAsync(g->t_state, 0, (size_t)nt * 8, s));
+  CK(cudaMemsetAsync(g->t_sched, 0, (size_t)nt * 4, s));
+  CK(cudaMemsetAsync(g->t_count, 0, 3 * 4, s));
+  CK(cudaMemcpyAsync(g->t_list[0], list.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->t_count, &n, 4, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
   const am::FlagSink sink{g->d_flags, g->d_flags + am::kFlagSlots, nullptr};
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   for (uint32_t r = 0; r < reps + 2; ++r) {
     if (r == 2) CK(cudaEventRecord(a, s));
-    am::launch_block_tiles(g->g, 16, ctx->sms * am::kTileCtasPerSm, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->t_list,
-                           g->t_count, g->t_front[1], g->t_state[0], 0, sink, s);
+    am::launch_block_tiles(g->g, 16, ctx->sms * am::kTileCtasPerSm, g->val[0], g->val[1], g->srcmask, g->rowsrc,
+                           g->book(), 0, 0, sink, s);
     ++ctx->launches;
   }
   CK(cudaEventRecord(b, s));

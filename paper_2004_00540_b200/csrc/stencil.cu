@@ -165,10 +165,6 @@ __global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __
   }
 }
 
-#ifdef AM_DEBUG_CLOCK
-__device__ long long am_dbg_clock[64];
-#endif
-
 // ----------------------------------------------------------- K1+K2 block
 template <int CB, int WPL>
 struct Rows;
@@ -483,10 +479,6 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-#ifdef AM_DEBUG_CLOCK  // tools/item_clock.cu: per-iteration timestamps of CTA 0 / warp 0
-  const bool dbg = blockIdx.x == 0 && threadIdx.x == 0;
-  if (dbg) am_dbg_clock[0] = clock64();
-#endif
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) issue(s);
   // source-row flags arrive as a 32-row ballot window, loaded one window ahead
@@ -568,9 +560,6 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
     }
     emit(t, x0);
     emit(t + 1, x1);
-#ifdef AM_DEBUG_CLOCK
-    if (dbg && t / 2 + 1 < 63) am_dbg_clock[t / 2 + 1] = clock64();
-#endif
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   if constexpr (LAG) {
@@ -732,23 +721,47 @@ __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, c
   publish_flag<false>(flag, __reduce_min_sync(0xffffffffu, Cell<CB>::fold(acc)), g.nbands * ntiles);
 }
 
-// Active-tile mode: the warps walk the work list built by k_tiles_plan
-// (items = band << 16 | chunk), two tiles per warp in 16-bit mode.  Every
-// tile has a home field (the ping-pong field holding its latest values) and
-// the layer of those values (state word: layer << 1 | home).  The item reads
-// each region it touches from that region's home with the region's lag
-// added to covered cells, and writes its own rows to the other field, so
-// quiet tiles are never copied or rewritten.  Each processed tile records
-// whether it still has a frontier (a cell covered during this block,
-// 1 <= a <= kK) for the next plan.
+// Frontier-region bit a neighbour N at (dr, dc) from tile T must have for T
+// to become active: a frontier cell within kK of T lies in N's region facing
+// T (bits: 0 any, 1 top, 2 bottom, 3 left, 4 right, 5 tl, 6 tr, 7 bl, 8 br).
+__constant__ uint8_t kFacing[3][3] = {{8, 2, 7}, {4, 0, 3}, {6, 1, 5}};
+
+// Lists tile (c, b) for block blk + 1 unless it is already listed (one
+// lane per candidate; the appends are warp-aggregated).
+__device__ __forceinline__ void push_tiles(const Geo& g, TileBook& book, uint32_t blk, bool want, int c, int b) {
+  const bool in = want && c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.tbands;
+  bool add = false;
+  if (in) add = atomicMax(&book.sched[(uint32_t)c * g.tbands + (uint32_t)b], blk + 2) < blk + 2;
+  const uint32_t m = __ballot_sync(0xffffffffu, add);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(&book.count[(blk + 1) % 3], (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (add) book.list[(blk + 1) & 1][base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)b << 16 | (uint32_t)c;
+}
+
+// Active-tile mode: the warps walk the block's work list (items = band << 16
+// | chunk), two tiles per warp in 16-bit mode.  Every tile has a home field
+// (the ping-pong field holding its latest values) and the layer of those
+// values (TileBook state).  The item reads each region it touches from that
+// region's home with the region's lag added to covered cells, and writes its
+// own rows to the other field, so quiet tiles are never copied or
+// rewritten.  Each processed tile then lists, for the next block, itself
+// and the neighbours its frontier (cells covered in the block's last layer)
+// can reach within kK cells.
 template <int CB>
 __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
-                  const uint8_t* __restrict__ rowsrc, const uint32_t* __restrict__ list,
-                  const uint32_t* __restrict__ count, uint16_t* __restrict__ front, const uint32_t* __restrict__ state,
-                  uint32_t l0, FlagSink flag) {
+                  const uint8_t* __restrict__ rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag) {
   extern __shared__ __align__(128) uint8_t smem_tiles[];
-  const uint32_t n = *count;
+  const uint32_t n = book.count[blk % 3];
+  const uint32_t* __restrict__ list = book.list[blk & 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    book.count[(blk + 2) % 3] = 0;
+    atomicAdd(book.processed, (unsigned long long)n);
+  }
+  const uint32_t l1 = l0 + kK;  // layer after this block
   // Pairing two tiles per warp halves the instructions but also the warps;
   // with few active tiles the kernel is latency bound and more warps win.
   const uint32_t per = (CB == 16 && AM_TILE_PAIR) ? 2u : 1u;
@@ -756,12 +769,18 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
   const int lane = threadIdx.x & 31;
   constexpr int kHaloLanes = kK / kTileWPL;  // lanes holding the left / right halo columns
   const int brel = lane < kHaloLanes ? -1 : (lane >= 32 - kHaloLanes ? 1 : 0);  // band of this lane's cells
+  // state at l0 of tile t (cur, or old if t was already processed in this block)
+  auto state_at_l0 = [&](uint32_t t) -> uint32_t {
+    const unsigned long long w = *reinterpret_cast<const volatile unsigned long long*>(book.state + t);
+    const uint32_t cur = (uint32_t)w;
+    return (cur >> 1) == l1 ? (uint32_t)(w >> 32) : cur;
+  };
   // (lag, home) of the tile this lane reads at chunk c0+dr
   auto region = [&](uint32_t c0, uint32_t b0, int dr, uint32_t& home) -> uint32_t {
     const int c = (int)c0 + dr, b = (int)b0 + brel;
     home = 0;
     if (c < 0 || b < 0 || c >= (int)g.nchunks || b >= (int)g.tbands) return 0u;  // padding: zero in both fields
-    const uint32_t s = state[(uint32_t)c * g.tbands + (uint32_t)b];
+    const uint32_t s = state_at_l0((uint32_t)c * g.tbands + (uint32_t)b);
     home = s & 1u;
     const uint32_t e = s >> 1;
     return e < l0 ? l0 - e : 0u;
@@ -772,6 +791,9 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     const bool hasB = per == 2u && w * per + 1 < n;
     const uint32_t ib = hasB ? list[w * per + 1] : ia;
     const uint32_t bA = ia >> 16, cA = ia & 0xFFFFu, bB = ib >> 16, cB = ib & 0xFFFFu;
+    const uint32_t tA = cA * g.tbands + bA, tB = cB * g.tbands + bB;
+    // own states before the reads of the neighbours (they are rewritten below)
+    const uint32_t sa = state_at_l0(tA), sb = state_at_l0(tB);
     uint32_t lw[3], homes = 0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -781,7 +803,6 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
       homes |= ha << d | hb << (3 + d);
     }
     // own rows go to the field that is not the tile's home
-    const uint32_t sa = state[cA * g.tbands + bA], sb = state[cB * g.tbands + bB];
     homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
     uint32_t edge[2];
     uint32_t acc;
@@ -840,9 +861,20 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     } else {
       ma = mb = __reduce_min_sync(0xffffffffu, acc);
     }
+    // new states (old kept in the high word for this block's readers)
     if (lane == 0) {
-      front[cA * g.tbands + bA] = (uint16_t)fa;
-      if (hasB) front[cB * g.tbands + bB] = (uint16_t)fb;
+      book.state[tA] = (unsigned long long)sa << 32 | (l1 << 1 | ((sa & 1u) ^ 1u));
+      if (hasB) book.state[tB] = (unsigned long long)sb << 32 | (l1 << 1 | ((sb & 1u) ^ 1u));
+    }
+    // push the next block's candidates: lanes 0-8 for tile A, 9-17 for tile B
+    {
+      const int k = lane < 9 ? lane : lane - 9;
+      const int dr = k / 3 - 1, dc = k % 3 - 1;  // T = N - (dr, dc) is activated by N's facing region
+      const bool forB = lane >= 9 && lane < 18;
+      const uint32_t m = forB ? (hasB ? fb : 0u) : (lane < 9 ? fa : 0u);
+      const bool want = lane < 18 && ((m >> kFacing[dr + 1][dc + 1]) & 1u);
+      const int c = (int)(forB ? cB : cA) - dr, b = (int)(forB ? bB : bA) - dc;
+      push_tiles(g, book, blk, want, c, b);
     }
     gmin = min(gmin, min(ma, hasB ? mb : ma));
   }
@@ -872,50 +904,6 @@ __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
   } else return w + (w > kFlag32 ? lagw : 0u);
 }
 
-// Frontier-region bit a neighbour N at (dr, dc) from tile T must have for T
-// to become active: a frontier cell within kK of T lies in N's region facing
-// T (bits: 0 any, 1 top, 2 bottom, 3 left, 4 right, 5 tl, 6 tr, 7 bl, 8 br).
-__constant__ uint8_t kFacing[3][3] = {{8, 2, 7}, {4, 0, 3}, {6, 1, 5}};
-
-// One lane per tile: the next block's state (active tiles advance by kk and
-// flip home), the work list (one atomic per warp).  Block 0 also resets the
-// next block's work counter and this block's fixed-point slot.
-__global__ void k_tiles_plan(Geo g, const uint16_t* __restrict__ front_prev, uint16_t* __restrict__ front_next,
-                             const uint32_t* __restrict__ state, uint32_t* __restrict__ state_next, uint32_t kk,
-                             uint32_t* __restrict__ list, uint32_t* __restrict__ count,
-                             uint32_t* __restrict__ next_count, uint32_t* __restrict__ flag,
-                             unsigned long long* __restrict__ processed, uint32_t l0) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *next_count = 0;
-    if (flag) *flag = 0xFFFFFFFFu;
-  }
-  const int lane = threadIdx.x & 31;
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  bool act = false;
-  if (t < g.ntiles()) {
-    const int chunk = (int)(t / g.tbands), band = (int)(t % g.tbands);
-#pragma unroll
-    for (int dr = -1; dr <= 1; ++dr)
-#pragma unroll
-      for (int dc = -1; dc <= 1; ++dc) {
-        const int c = chunk + dr, b = band + dc;
-        if (c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.tbands)
-          act |= (front_prev[(uint32_t)c * g.tbands + (uint32_t)b] >> kFacing[dr + 1][dc + 1]) & 1u;
-      }
-    const uint32_t s = state[t];
-    state_next[t] = act ? (((l0 + kk) << 1) | ((s & 1u) ^ 1u)) : s;
-    front_next[t] = 0;
-  }
-  const uint32_t am = __ballot_sync(0xffffffffu, act);
-  uint32_t base = 0;
-  if (lane == 0 && am) {
-    base = atomicAdd(count, (uint32_t)__popc(am));
-    atomicAdd(processed, (unsigned long long)__popc(am));
-  }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (act) list[base + __popc(am & ((1u << lane) - 1u))] = (t % g.tbands) << 16 | (t / g.tbands);
-}
-
 // 16 B per lane-row: 8 cells (u16) or 4 cells (u32)
 template <int CB, typename F>
 __device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, uint32_t chunk, F f) {
@@ -932,11 +920,11 @@ __device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, u
 // the tile's home plus its lag.  One warp per tile.  Afterwards all tiles are
 // current in dst (state = l << 1 | dst).
 template <int CB>
-__global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ state, typename Cell<CB>::T* __restrict__ f0,
+__global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, typename Cell<CB>::T* __restrict__ f0,
                                  ptrdiff_t delta, uint32_t dst, uint32_t l) {
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= g.ntiles()) return;
-  const uint32_t s = state[t], home = s & 1u, e = s >> 1;
+  const uint32_t s = (uint32_t)state[t], home = s & 1u, e = s >> 1;
   if (e != l || home != dst) {
     const uint32_t lag = l - e;
     const uint32_t lagw = CB == 16 ? (lag | lag << 16) : lag;
@@ -954,13 +942,14 @@ __global__ void k_tiles_finalize(Geo g, uint32_t* __restrict__ state, typename C
     });
   }
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) state[t] = l << 1 | dst;
+  if ((threadIdx.x & 31) == 0) state[t] = (unsigned long long)(l << 1 | dst) << 32 | (l << 1 | dst);
 }
 
-// Layer-0 frontier: every tile holding a source (a = 1 at layer 0).
-__global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint16_t* __restrict__ front) {
+// Block 0's work list: the 3x3 neighbourhood of every tile holding a source
+// (the layer-0 frontier, a = 1); pushed as block "-1" (lists 0, sched 1).
+__global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, TileBook book) {
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (t >= g.ntiles()) return;
+  if (t >= g.ntiles()) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const uint32_t chunk = t / g.tbands, band = t % g.tbands;
   bool any = false;
@@ -971,7 +960,24 @@ __global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, uint16_
       any |= (m.x | m.y) != 0;
     }
   any = __any_sync(0xffffffffu, any);
-  if (lane == 0) front[t] = any ? 0x1FFu : 0u;  // every region (conservative)
+  if (!any) return;
+  const int dr = lane / 3 - 1, dc = lane % 3 - 1;
+  push_tiles(g, book, 0xFFFFFFFFu, lane < 9, (int)chunk + dr, (int)band + dc);
+}
+
+// Every tile current at `layer` in field `home` and listed for block blk
+// (after dense single layers or the 32-bit promotion).
+__global__ void k_tiles_all(Geo g, TileBook book, uint32_t blk, uint32_t layer, uint32_t home) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0) {
+    book.count[blk % 3] = g.ntiles();
+    book.count[(blk + 1) % 3] = 0;
+  }
+  if (t >= g.ntiles()) return;
+  const uint32_t cur = layer << 1 | home;
+  book.state[t] = (unsigned long long)cur << 32 | cur;
+  book.sched[t] = blk + 1;
+  book.list[blk & 1][t] = (t % g.tbands) << 16 | (t / g.tbands);
 }
 
 // -------------------------------------------------------- single layer
@@ -1152,25 +1158,20 @@ void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, co
     k_block<32, true><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
 }
 
-void launch_tiles_init(const Geo& g, const uint8_t* srcmask, uint16_t* front, cudaStream_t s) {
+void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cudaStream_t s) {
   const uint32_t n = g.ntiles();
-  k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, front);
+  k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, book);
 }
 
-// counters[0..1]: work-list lengths (alternating per block); states[parity]
-// holds the tile states at l0, states[parity^1] receives the next ones.
-void launch_tiles_plan(const Geo& g, const uint16_t* front_prev, uint16_t* front_next, uint32_t* const states[2],
-                       int parity, uint32_t l0, uint32_t kk, uint32_t* list, uint32_t* counters, uint32_t* flag,
-                       unsigned long long* processed, cudaStream_t s) {
+void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer, int home, cudaStream_t s) {
   const uint32_t n = g.ntiles();
-  k_tiles_plan<<<(n + 255) / 256, 256, 0, s>>>(g, front_prev, front_next, states[parity], states[parity ^ 1], kk, list,
-                                               counters + parity, counters + (parity ^ 1), flag, processed, l0);
+  k_tiles_all<<<(n + 255) / 256, 256, 0, s>>>(g, book, blk, layer, (uint32_t)home);
 }
 
-// f0/f1: the two fields; state: tile states at l0
+// f0/f1: the two fields; book: tile states / lists (block blk reads list[blk & 1])
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, const uint32_t* list, const uint32_t* count, uint16_t* front,
-                        const uint32_t* state, uint32_t l0, FlagSink flag, cudaStream_t s) {
+                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                        cudaStream_t s) {
   static bool attr = [] {
     cudaFuncSetAttribute(k_block_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
     cudaFuncSetAttribute(k_block_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
@@ -1179,17 +1180,17 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
   (void)attr;
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
-    k_block_tiles<16><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, list, count,
-                                                              front, state, l0, flag);
+    k_block_tiles<16><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
+                                                              flag);
   } else {
     auto* a = (uint32_t*)f0;
-    k_block_tiles<32><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, list, count,
-                                                              front, state, l0, flag);
+    k_block_tiles<32><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
+                                                              flag);
   }
 }
 
 // every tile to layer l in field dst (0 = f0, 1 = f1)
-void launch_tiles_finalize(const Geo& g, int cb, uint32_t* state, void* f0, void* f1, int dst, uint32_t l,
+void launch_tiles_finalize(const Geo& g, int cb, unsigned long long* state, void* f0, void* f1, int dst, uint32_t l,
                            cudaStream_t s) {
   const uint32_t n = g.ntiles();
   if (cb == 16) {
