@@ -338,9 +338,9 @@ def run_b200(args, rank, world, local_rank):
     cell_updates = W * H * L
     value = cell_updates / (ms_step / 1000) / 1e9  # whole job: the full grid's cell-updates per second
 
-    # roofline of the dominant kernel: algorithmic bytes per launch / mean launch time (CUDA events around every
-    # stencil launch on the library stream, inside the timed steps).  Active-tile mode: the launch is the tile
-    # planner + k_block_tiles and its work is the executed (useful) cell-updates of the processed tiles.
+    # roofline of the dominant kernel: algorithmic bytes per launch / mean launch time (CUDA events bracketing the
+    # runs of stencil launches on the library stream, inside the timed steps, so the gaps between launches count).
+    # Active-tile mode: the launch is k_block_tiles and its work is the executed cell-updates of the processed tiles.
     peak, peak_src = peaks()
     rows_here = (sol.slab.height if sol.slab is not None else H)
     per_launch_ms = stencil_ms / max(blocks, 1)
@@ -348,7 +348,7 @@ def run_b200(args, rank, world, local_rank):
     info = sol.full.info()
     if tile_mode:
         cells_per_launch = tiles_done * info["tile_rows"] * info["tile_cols"] * LAYERS_PER_BLOCK / max(blocks, 1)
-        kernel = "am::k_tiles_plan + am::k_block_tiles<16>"
+        kernel = "am::k_block_tiles<16>"
     else:
         cells_per_launch = W * rows_here * LAYERS_PER_BLOCK
         kernel = "am::k_block<16>"

@@ -145,121 +145,125 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
 }
 
 // Windowed walk for maps produced by the device propagation (encoded
-// fields): the warp loads the 7x7 window around the current cell (lane k
-// holds window cells k and k+32, row-major), takes up to three steps inside
-// it with votes and shuffles only (the 3x3 neighbourhood of any cell within
-// 2 of the centre lies in the window), then re-centres.  A cell is a source
-// exactly when its activity is L+1 (d = 0), so no source-mask load is
-// needed.  Candidate order is the window's row-major order restricted to
-// the 8 neighbours, i.e. the reference enumeration (pins P1/P2).
-__device__ uint64_t walk_window(const Reader& rd, uint32_t r, uint32_t c, int method, uint64_t seed, uint64_t limit,
-                                uint32_t* out, int32_t* st) {
+// fields).  The warp stages a 32x32 window of decoded activities around the
+// current cell in shared memory (lane i loads window row i with 16 B
+// vectors), then takes steps inside it with one shared-memory read per
+// candidate lane and two votes per step; it re-stages when the current
+// cell's 3x3 neighbourhood reaches the window border (~15 steps per load).
+// A cell is a source exactly when its activity is L+1 (d = 0), so no
+// source-mask load is needed.  Candidate lanes follow the reference
+// enumerations: row-major for the simple rule (pin P2), axis order L,R,U,D
+// then the diagonals for the Euclidean rule (pin P1).  Points are gathered
+// 32 at a time and written by the whole warp.
+constexpr int kWin = 32;
+
+__device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int method, uint64_t seed, uint64_t limit,
+                              uint32_t* out, int32_t* st, uint32_t* win) {
   const int lane = threadIdx.x & 31;
-  const uint32_t top = rd.m.layers + 1;  // activity of a source
+  const MapView& m = rd.m;
+  const int pad = (int)m.g.pad, pitch = (int)m.g.pitch;
+  const int rmax = (int)m.g.rows - pad - kWin;  // window origin limits (grid coordinates)
+  const uint32_t top = m.layers + 1;            // activity of a source
   uint64_t rng = seed;
-  uint32_t cur = rd.value(r, c);
-  uint64_t n = 1;
-  if (lane == 0) {
-    out[0] = r;
-    out[1] = c;
+  // candidate offsets of this lane (lanes 0..7)
+  int dr = 0, dc = 0;
+  if (method == 0) {
+    dr = kDR[lane & 7];
+    dc = kDC[lane & 7];
+  } else {
+    const int er[8] = {0, 0, -1, 1, -1, -1, 1, 1}, ec[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
+    dr = er[lane & 7];
+    dc = ec[lane & 7];
   }
-  const int k0 = lane, k1 = lane + 32;
-  const int r0 = k0 / 7 - 3, c0 = k0 % 7 - 3, r1 = k1 / 7 - 3, c1 = k1 % 7 - 3;
-  uint32_t wr = r, wc = c, v0 = 0, v1 = 0;
+  int wr = 0, wc = 0;
   bool loaded = false;
+  auto stage = [&]() {
+    wr = min(max((int)r - kWin / 2, -pad), rmax);
+    const int ac = min(max(((int)c + pad - kWin / 2) & ~7, 0), pitch - kWin);  // allocated column, 16 B aligned
+    wc = ac - pad;
+    const size_t row = (size_t)(wr + lane + pad) * pitch + ac;
+    __syncwarp();  // previous window fully read
+    if (m.cell_bits == 16) {
+      const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(m.val) + row);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = p[q];
+        const uint32_t h[4] = {v.x, v.y, v.z, v.w};
+        uint32_t d[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t lo = h[k] & 0xFFFFu, hi = h[k] >> 16;
+          d[2 * k] = (lo & kFlag16) ? (lo & 0x7FFFu) : 0u;
+          d[2 * k + 1] = (hi & kFlag16) ? (hi & 0x7FFFu) : 0u;
+        }
+        uint4* o = reinterpret_cast<uint4*>(win + lane * kWin + q * 8);
+        o[0] = make_uint4(d[0], d[1], d[2], d[3]);
+        o[1] = make_uint4(d[4], d[5], d[6], d[7]);
+      }
+    } else {
+      const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(m.val) + row);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 v = p[q];
+        auto dec = [](uint32_t x) { return (x & kFlag32) ? (x & kLow32) : 0u; };
+        reinterpret_cast<uint4*>(win + lane * kWin)[q] = make_uint4(dec(v.x), dec(v.y), dec(v.z), dec(v.w));
+      }
+    }
+    __syncwarp();
+    loaded = true;
+  };
+  uint32_t cur = rd.value(r, c);
+  uint64_t n = 0;
+  uint32_t keep_r = 0, keep_c = 0;  // point n of this lane's slot (n % 32 == lane)
+  auto record = [&]() {
+    if ((int)(n & 31) == lane) keep_r = r, keep_c = c;
+    if ((n & 31) == 31) {
+      reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r, keep_c);
+    }
+    ++n;
+  };
+  record();
   while (cur != top) {
     if (n >= limit) {
       *st = ST_EINTERNAL;
       return 0;
     }
-    int pr = (int)r - (int)wr, pc = (int)c - (int)wc;
-    if (!loaded || pr < -2 || pr > 2 || pc < -2 || pc > 2) {
-      wr = r;
-      wc = c;
-      pr = pc = 0;
-      // pads are >= kK >= 3 cells wide and decode to 0, so the window never leaves the allocation
-      v0 = rd.value_pad((int)r + r0, (int)c + c0);
-      v1 = k1 < 49 ? rd.value_pad((int)r + r1, (int)c + c1) : 0u;
-      loaded = true;
-    }
-    int sel_r = 0, sel_c = 0;
-    uint32_t best = 0;
-    bool ok = false;
+    const int pr = (int)r - wr, pc = (int)c - wc;
+    if (!loaded || pr < 1 || pr > kWin - 2 || pc < 1 || pc > kWin - 2) stage();
+    const uint32_t v = lane < 8 ? win[((int)r - wr + dr) * kWin + ((int)c - wc + dc)] : 0u;
+    int sel = -1;
+    uint32_t best;
     if (method == 0) {  // simple: 8-neighbour argmax, seeded tie-break (pin P2)
-      const int a0 = r0 - pr, b0 = c0 - pc, a1 = r1 - pr, b1 = c1 - pc;
-      const bool n0 = a0 >= -1 && a0 <= 1 && b0 >= -1 && b0 <= 1 && (a0 | b0) != 0;
-      const bool n1 = k1 < 49 && a1 >= -1 && a1 <= 1 && b1 >= -1 && b1 <= 1 && (a1 | b1) != 0;
-      best = __reduce_max_sync(0xffffffffu, max(n0 ? v0 : 0u, n1 ? v1 : 0u));
+      best = __reduce_max_sync(0xffffffffu, v);
+      uint32_t mask = __ballot_sync(0xffffffffu, lane < 8 && v == best);
       if (best > cur) {
-        uint32_t m0 = __ballot_sync(0xffffffffu, n0 && v0 == best);
-        uint32_t m1 = __ballot_sync(0xffffffffu, n1 && v1 == best);
-        const int cnt = __popc(m0) + __popc(m1);
+        const int cnt = __popc(mask);
         int pick = 0;
         if (cnt >= 2) pick = (int)__umul64hi(splitmix64(rng), (uint64_t)cnt);
-        int k;
-        if (pick < __popc(m0)) {
-          for (int i = 0; i < pick; ++i) m0 &= m0 - 1;
-          k = __ffs(m0) - 1;
-        } else {
-          for (int i = 0; i < pick - __popc(m0); ++i) m1 &= m1 - 1;
-          k = 32 + __ffs(m1) - 1;
-        }
-        sel_r = k / 7 - 3;
-        sel_c = k % 7 - 3;
-        ok = true;
+        for (int k = 0; k < pick; ++k) mask &= mask - 1;
+        sel = __ffs(mask) - 1;
       }
-    } else {  // Euclidean: axis order L,R,U,D then diagonals (pin P1)
-      auto at = [&](int dr, int dc) -> uint32_t {
-        const int k = (pr + dr + 3) * 7 + (pc + dc + 3);
-        const uint32_t t0 = __shfl_sync(0xffffffffu, v0, k & 31), t1 = __shfl_sync(0xffffffffu, v1, k & 31);
-        return k < 32 ? t0 : t1;
-      };
-      const int ar[4] = {0, 0, -1, 1}, ac[4] = {-1, 1, 0, 0}, gr[4] = {-1, -1, 1, 1}, gc[4] = {-1, 1, -1, 1};
-      int bi = 0;
-      best = at(ar[0], ac[0]);
-#pragma unroll
-      for (int i = 1; i < 4; ++i) {
-        const uint32_t v = at(ar[i], ac[i]);
-        if (v > best) {
-          best = v;
-          bi = i;
-        }
-      }
+    } else {  // Euclidean: first maximum of L,R,U,D, else of the diagonals (pin P1)
+      best = __reduce_max_sync(0xffffffffu, lane < 4 ? v : 0u);
       if (best > cur) {
-        sel_r = pr + ar[bi];
-        sel_c = pc + ac[bi];
-        ok = true;
+        sel = __ffs(__ballot_sync(0xffffffffu, lane < 4 && v == best)) - 1;
       } else {
-        bi = 0;
-        best = at(gr[0], gc[0]);
-#pragma unroll
-        for (int i = 1; i < 4; ++i) {
-          const uint32_t v = at(gr[i], gc[i]);
-          if (v > best) {
-            best = v;
-            bi = i;
-          }
-        }
-        if (best > cur) {
-          sel_r = pr + gr[bi];
-          sel_c = pc + gc[bi];
-          ok = true;
-        }
+        best = __reduce_max_sync(0xffffffffu, lane >= 4 && lane < 8 ? v : 0u);
+        if (best > cur) sel = __ffs(__ballot_sync(0xffffffffu, lane >= 4 && lane < 8 && v == best)) - 1;
       }
     }
-    if (!ok) {
+    if (sel < 0) {
       *st = ST_EINTERNAL;  // no ascending neighbour
       return 0;
     }
-    r = (uint32_t)((int)wr + sel_r);
-    c = (uint32_t)((int)wc + sel_c);
+    r = (uint32_t)((int)r + __shfl_sync(0xffffffffu, dr, sel));
+    c = (uint32_t)((int)c + __shfl_sync(0xffffffffu, dc, sel));
     cur = best;
-    if (lane == 0) {
-      out[2 * n] = r;
-      out[2 * n + 1] = c;
-    }
-    ++n;
+    record();
   }
+  // flush the partial group of points
+  const uint64_t base = n & ~(uint64_t)31;
+  if (base + lane < n) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(keep_r, keep_c);
   if (!rd.source(r, c)) *st = ST_EINTERNAL;  // a non-source at the top value would violate the law
   return n;
 }
@@ -296,8 +300,10 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
   Reader rd{m};
   const uint64_t off = offsets[w], limit = offsets[w + 1] - off;
   int32_t st = ST_OK;
+  __shared__ __align__(16) uint32_t wins[4][kWin * kWin];  // one window per warp (128-thread CTAs)
   const uint64_t got = m.cell_bits
-                           ? walk_window(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st)
+                           ? walk_smem(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st,
+                                       wins[(threadIdx.x >> 5) & 3])
                            : walk<true>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st);
   if ((threadIdx.x & 31) == 0) {
     if (st != ST_OK) status[w] = st;
