@@ -79,7 +79,7 @@ def main():
         for r in rows[hi + 1:]:
             if len(r) <= mi:
                 continue
-            scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+            scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
             a = agg[r[ki].split("(")[0]]
             a[0] += 1
             a[1] += float(r[mi].replace(",", "")) * scale
