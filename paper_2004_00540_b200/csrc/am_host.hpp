@@ -67,7 +67,7 @@ struct am_grid {
   unsigned long long* t_state = nullptr;     // per tile: old << 32 | cur (am::TileBook)
   uint32_t* t_sched = nullptr;               // per tile: index + 1 of the block it is listed for
   uint32_t* t_list[2] = {nullptr, nullptr};  // work lists (band << 16 | chunk) by block parity
-  uint32_t* t_count = nullptr;               // [3] list lengths by block index mod 3
+  uint32_t* t_count = nullptr;               // [6] list lengths, item fetch counters (TileBook::count)
   unsigned long long* t_processed = nullptr; // tiles processed (statistics)
   uint32_t t_blk = 0;                        // index of the next tile block (list / counter selection)
   am::TileBook book() const { return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed}; }

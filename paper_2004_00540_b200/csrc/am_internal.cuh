@@ -53,7 +53,7 @@ constexpr int kTileRows = AM_TILE_ROWS;
 constexpr int kTileWPL = AM_TILE_WPL;
 constexpr int kTileCols = 32 * kTileWPL - 2 * kK;  // useful columns of a tile band
 #ifndef AM_TILE_CTAS
-#define AM_TILE_CTAS 2  // 4 warps x 24 KB staged items each
+#define AM_TILE_CTAS 3  // 4 warps x 12 KB staged tiles each, <= 168 registers
 #endif
 constexpr int kTileCtasPerSm = AM_TILE_CTAS;  // k_block_tiles is persistent: this many CTAs per SM
 
@@ -106,7 +106,7 @@ struct TileBook {
   unsigned long long* state;
   uint32_t* sched;
   uint32_t* list[2];
-  uint32_t* count;                // [3]
+  uint32_t* count;                // [6]: list lengths [0..2], item fetch counters [3..5] (both by block mod 3)
   unsigned long long* processed;  // tiles processed (statistics)
 };
 

@@ -209,7 +209,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
     if (!e) e = am::dmalloc(ctx, &g->t_sched, nt * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_list[0], nt * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_list[1], nt * 4);
-    if (!e) e = am::dmalloc(ctx, &g->t_count, 3 * 4);
+    if (!e) e = am::dmalloc(ctx, &g->t_count, 6 * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_processed, 8);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
@@ -305,7 +305,12 @@ struct PendingBlock {
   uint32_t start;  // layers before the block
   uint32_t count;  // layers in the block
   int cell_bits;
+  bool polled;     // mapped slot written by the kernel itself: poll, no event
 };
+
+// Marks a mapped slot "not yet written" (the kernel's word is never this value:
+// minima are < 0x7FFFFFFF or the all-ones "no covered cell").
+constexpr uint32_t kSlotPending = 0xFFFFFFFEu;
 
 // First layer without new cells (l'), or 0 if the block still added cells
 // in its last layer.  m = min over covered cells of (a-1) at the block end.
@@ -417,7 +422,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     CK(cudaMemsetAsync(tg->t_state, 0, nt * 8, ctx->stream));
     CK(cudaMemsetAsync(tg->t_sched, 0, nt * 4, ctx->stream));
     CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_count, 0, 3 * 4, ctx->stream));
+    CK(cudaMemsetAsync(tg->t_count, 0, 6 * 4, ctx->stream));
     launch_tiles_init(tg->g, tg->srcmask, tg->book(), ctx->stream);
     CKL();
   }
@@ -454,9 +459,20 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     uint32_t m = 0xFFFFFFFFu;
     for (auto& s : slabs) {
       am_ctx* c = s.ctx;
-      cudaError_t e = cudaEventSynchronize(s.g->fs->ev[b.slot]);
-      if (e) return fail(c, AM_ECUDA, "flag event: %s", cudaGetErrorString(e));
-      m = std::min(m, (uint32_t) * (volatile uint32_t*)(s.g->fs->h + b.slot));
+      volatile uint32_t* h = s.g->fs->h + b.slot;
+      if (b.polled) {  // the kernel's last CTA writes the slot through the mapping
+        for (uint64_t spin = 1; *h == kSlotPending; ++spin) {
+          if ((spin & 4095) == 0) {
+            const cudaError_t q = cudaStreamQuery(c->stream);
+            if (q == cudaSuccess && *h == kSlotPending) return fail(c, AM_ECUDA, "flag slot never written");
+            if (q != cudaSuccess && q != cudaErrorNotReady) return fail(c, AM_ECUDA, "stencil: %s", cudaGetErrorString(q));
+          }
+        }
+      } else {
+        cudaError_t e = cudaEventSynchronize(s.g->fs->ev[b.slot]);
+        if (e) return fail(c, AM_ECUDA, "flag event: %s", cudaGetErrorString(e));
+      }
+      m = std::min(m, (uint32_t)*h);
     }
     if (!lprime) {
       const uint32_t t = block_termination(b, m);
@@ -497,6 +513,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         if (e) return fail(c, AM_ECUDA, "memset: %s", cudaGetErrorString(e));
       }
       armed[slot] = mapped && blocked;
+      if (mapped && blocked) g->fs->h[slot] = kSlotPending;  // consumed 64 blocks ago (lag < kFlagSlots)
       const FlagSink sink{flag, g->d_flags + kFlagSlots, mapped ? g->fs->hdev + slot : nullptr};
       void* in = g->val[g->cur];
       void* outp = g->val[g->cur ^ 1];
@@ -535,14 +552,13 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       if (tr && (st = tr->reduce(words, false))) return st;
       for (auto& sr : slabs) {
         am_ctx* c = sr.ctx;
-        cudaError_t e = cudaSuccess;
-        if (!(mapped && blocked))
-          e = cudaMemcpyAsync(sr.g->fs->h + slot, sr.g->d_flags + slot, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                              c->stream);
+        if (mapped && blocked) continue;  // polled
+        cudaError_t e = cudaMemcpyAsync(sr.g->fs->h + slot, sr.g->d_flags + slot, sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, c->stream);
         if (!e) e = cudaEventRecord(sr.g->fs->ev[slot], c->stream);
         if (e) return fail(c, AM_ECUDA, "flag copy: %s", cudaGetErrorString(e));
       }
-      pend.push_back(PendingBlock{slot, l, kk, slabs[0].g->cell_bits});
+      pend.push_back(PendingBlock{slot, l, kk, slabs[0].g->cell_bits, mapped && blocked});
     }
     l += kk;
     ++nblock;
@@ -988,7 +1004,7 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
   // block 0 every launch: list[0] / count[0] stay, the pushes for block 1 are deduplicated away
   CK(cudaMemsetAsync(g->t_state, 0, (size_t)nt * 8, s));
   CK(cudaMemsetAsync(g->t_sched, 0, (size_t)nt * 4, s));
-  CK(cudaMemsetAsync(g->t_count, 0, 3 * 4, s));
+  CK(cudaMemsetAsync(g->t_count, 0, 6 * 4, s));
   CK(cudaMemcpyAsync(g->t_list[0], list.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->t_count, &n, 4, cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
@@ -997,6 +1013,7 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   for (uint32_t r = 0; r < reps + 2; ++r) {
+    CK(cudaMemsetAsync(g->t_count + 3, 0, 4, s));  // block 0's item fetch counter
     if (r == 2) CK(cudaEventRecord(a, s));
     am::launch_block_tiles(g->g, 16, ctx->sms * am::kTileCtasPerSm, g->val[0], g->val[1], g->srcmask, g->rowsrc,
                            g->book(), 0, 0, sink, s);

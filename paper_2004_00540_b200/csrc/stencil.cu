@@ -347,9 +347,6 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 #ifndef AM_TILE_STAGES
 #define AM_TILE_STAGES 4
 #endif
-#ifndef AM_TILE_PAIR
-#define AM_TILE_PAIR 1
-#endif
 #ifndef AM_SKEW
 #define AM_SKEW 1
 #endif
@@ -569,31 +566,36 @@ __device__ __forceinline__ uint32_t stream_item(const Geo& g, const typename Cel
   return acc;
 }
 
-// ---- active tiles, 16-bit cells: the whole item staged up front ----------
+// ---- active tiles, 16-bit cells: one tile per warp, staged whole ---------
 //
-// An item (tiles A and B, kTileSteps rows each) is small enough to stage
-// completely: every lane issues all of its 8 B row pieces with cp.async at
-// the start (three commit groups, one per input region), so no per-row
-// address arithmetic or ring bookkeeping remains in the loop.  The steps
-// then run in five phases with compile-time roles (input region -> lag,
-// output rows -> top / middle / bottom minima); items whose rows hold a
-// source take the general stream_item path.
-constexpr int kTileSteps = kTileRows + 2 * kK;                 // rows streamed per item
-constexpr int kTileRowBytes = 32 * kTileWPL * 2;               // one u16 tile row of a warp
-constexpr int kTileBufBytes = kTileSteps * 2 * kTileRowBytes;  // A and B rows of an item
+// The two u16 halves of every word carry the tile's upper half (rows 0-15,
+// lo) and lower half (rows 16-31, hi): both stream 16 + 2K = 32 steps, so an
+// item is short (latency) and the block has one item per active tile (warps
+// to hide it).  The tile's rows -8..39 (its own 32 + K above + K below) are
+// staged in shared memory up front with 16 B cp.async.cg (lanes 0-15 copy
+// one 256 B row, 16-31 the next; two commit groups), then the steps run in
+// four compile-time phases: which region each half reads (lag) and which
+// output minima a step feeds.  Items whose rows hold a source take the
+// general stream_item path (same halves).
+constexpr int kHalfRows = kTileRows / 2;                   // rows per half
+constexpr int kTileSteps = kHalfRows + 2 * kK;             // steps per item
+constexpr int kStageRows = kTileRows + 2 * kK;             // rows staged (-K .. kTileRows+K-1)
+constexpr int kTileRowBytes = 32 * kTileWPL * 2;           // one u16 row of the warp's band
+constexpr int kTileBufBytes = kStageRows * kTileRowBytes;  // 12 KB
 static_assert(kTileWPL == 4, "the staged item path loads 8 B per lane and tile row");
+static_assert(kHalfRows == 2 * kK, "phase layout: 16-row halves with K = 8");
 constexpr int kTileWarpSmem = kTileBufBytes > kTileWarpSmemRing ? kTileBufBytes : kTileWarpSmemRing;
 constexpr int kTileSmem = kWarpsPerCta * kTileWarpSmem;  // dynamic shared memory of k_block_tiles
-static_assert(kTileRows >= 2 * kK && kTileRows % 2 == 0, "top and bottom edge rows must not overlap");
 
-enum { kOutNone = 0, kOutTop = 1, kOutMid = 2, kOutBot = 3 };
+enum { kOutNone = 0, kOutTop = 1, kOutBot = 2 };
 
+// Steps [s0, s1): the upper half reads staged row s, the lower half row s+16.
 template <int OUT>
 __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, uint32_t lagw, bool lag,
                                            uint32_t (&P0)[kK][4], uint32_t (&P1)[kK][4], uint16_t*& oA,
-                                           uint16_t*& oB, size_t pitch, bool st_a, bool st_b, uint32_t& acc,
-                                           uint32_t& acc_edge) {
+                                           uint16_t*& oB, size_t pitch, bool st, uint32_t& acc, uint32_t& acc_edge) {
   using C = Cell<16>;
+  constexpr int kB = kHalfRows * kTileRowBytes;  // the lower half streams 16 rows further down
   auto words = [](uint2 a, uint2 b, uint32_t (&x)[4]) {
     x[0] = __byte_perm(a.x, b.x, 0x5410);
     x[1] = __byte_perm(a.x, b.x, 0x7632);
@@ -601,27 +603,24 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
     x[3] = __byte_perm(a.y, b.y, 0x7632);
   };
   auto emit = [&](const uint32_t (&x)[4]) {
-    if (st_a) *reinterpret_cast<uint2*>(oA) = make_uint2(__byte_perm(x[0], x[1], 0x5410), __byte_perm(x[2], x[3], 0x5410));
-    if (st_b) *reinterpret_cast<uint2*>(oB) = make_uint2(__byte_perm(x[0], x[1], 0x7632), __byte_perm(x[2], x[3], 0x7632));
+    if (st) {
+      *reinterpret_cast<uint2*>(oA) = make_uint2(__byte_perm(x[0], x[1], 0x5410), __byte_perm(x[2], x[3], 0x5410));
+      *reinterpret_cast<uint2*>(oB) = make_uint2(__byte_perm(x[0], x[1], 0x7632), __byte_perm(x[2], x[3], 0x7632));
+    }
     oA += pitch;
     oB += pitch;
-    if constexpr (OUT == kOutMid) {
+    uint32_t rm = 0xFFFFFFFFu;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) acc = C::acc_min(x[w], acc);
-    } else {
-      uint32_t rm = 0xFFFFFFFFu;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) rm = C::acc_min(x[w], rm);
-      acc = C::vmin(acc, rm);
-      acc_edge = C::vmin(acc_edge, rm);
-    }
+    for (int w = 0; w < 4; ++w) rm = C::acc_min(x[w], rm);
+    acc = C::vmin(acc, rm);
+    acc_edge = C::vmin(acc_edge, rm);
   };
 #pragma unroll 1
   for (int s = s0; s < s1; s += 2) {
-    const uint8_t* r = buf + s * 2 * kTileRowBytes;
+    const uint8_t* r = buf + s * kTileRowBytes;
     uint32_t x0[4], x1[4];
-    words(*reinterpret_cast<const uint2*>(r), *reinterpret_cast<const uint2*>(r + kTileRowBytes), x0);
-    words(*reinterpret_cast<const uint2*>(r + 2 * kTileRowBytes), *reinterpret_cast<const uint2*>(r + 3 * kTileRowBytes),
+    words(*reinterpret_cast<const uint2*>(r), *reinterpret_cast<const uint2*>(r + kB), x0);
+    words(*reinterpret_cast<const uint2*>(r + kTileRowBytes), *reinterpret_cast<const uint2*>(r + kB + kTileRowBytes),
           x1);
     if (lag) {
 #pragma unroll
@@ -630,7 +629,12 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
         x1[w] = add_lag<16>(x1[w], lagw);
       }
     }
+#if AM_SKEW
     stream_step2<16, 4>(x0, x1, P0, P1);
+#else
+    stream_step<16, 0, false, 4>(x0, P0, P1, 0u, nullptr, nullptr, 0, 0);
+    stream_step<16, 1, false, 4>(x1, P0, P1, 0u, nullptr, nullptr, 0, 0);
+#endif
     if constexpr (OUT != kOutNone) {
       emit(x0);
       emit(x1);
@@ -638,38 +642,34 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
   }
 }
 
-// Same contract as stream_item<16, false, true, .., kTileWPL> for tile items
-// without source rows; buf = this warp's kTileBufBytes of shared memory.
-__device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta,
-                                                uint32_t bA, uint32_t cA, uint32_t bB, uint32_t cB, bool hasB,
-                                                const uint32_t (&lw)[3], uint32_t homes, uint32_t* edge_min,
-                                                uint8_t* buf) {
+// Tile (band b, chunk c) without source rows; lw / homes: this lane's lag and
+// home field of the regions above / inside / below the tile (bits 0-2), bit
+// 6 = output field.  Returns the min over covered output cells of a-1 (lo =
+// upper half, hi = lower half); edge[0] / edge[1]: the same over the first /
+// last kK rows of each half (use lo of [0] and hi of [1]).
+__device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta, uint32_t b,
+                                                uint32_t c, const uint32_t (&lw)[3], uint32_t homes,
+                                                uint32_t* edge, uint8_t* buf) {
   const int lane = threadIdx.x & 31;
   const size_t pitch = g.pitch;
-  const uint32_t colA = bA * kTileCols + lane * kTileWPL, colB = bB * kTileCols + lane * kTileWPL;
-  const uint32_t rA = cA * kTileRows, rB = cB * kTileRows;  // allocated row of step 0
-  // Lanes 0-15 copy tile A's row (256 B), lanes 16-31 tile B's, 16 B each
-  // (L2-only cp.async.cg); the staged rows are read back by all lanes after
-  // the group wait and a warp barrier.
   __syncwarp();  // every lane is done reading the previous item's rows
   {
-    const int half = lane >> 4;
-    // the 8 cells this lane copies belong to compute lanes 2*lane, 2*lane+1 (mod 32): their band's homes
+    // the 8 cells this lane copies belong to compute lanes 2*(lane&15) and +1: their band's homes
     const uint32_t ch = __shfl_sync(0xffffffffu, homes, (2 * lane) & 31);
-    uint8_t* dst = buf + lane * 16;
-    const uint32_t col = (half ? bB : bA) * kTileCols + (lane & 15) * 8, r0 = half ? rB : rA;
-    int s = 0;
+    const int half = lane >> 4;
+    const uint32_t col = b * kTileCols + (lane & 15) * 8;
+    const uint16_t* base[3];
 #pragma unroll
-    for (int reg = 0; reg < 3; ++reg) {
-      const uint16_t* q = f0 + (((ch >> (3 * half + reg)) & 1u) ? delta : 0) + (size_t)(r0 + s) * pitch + col;
-      const int e = reg == 0 ? kK : (reg == 1 ? kK + kTileRows : kTileSteps);
-#pragma unroll 4
-      for (; s < e; ++s) {
-        cp_async16(dst + s * 2 * kTileRowBytes, q);
-        q += pitch;
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int r = 0; r < 3; ++r) base[r] = f0 + (((ch >> r) & 1u) ? delta : 0) + (size_t)c * kTileRows * pitch + col;
+    uint8_t* dst = buf + (lane & 15) * 16;
+#pragma unroll
+    for (int k = 0; k < kStageRows / 2; ++k) {
+      const int row = 2 * k + half;  // staged row = tile row + kK
+      const int reg = row < kK ? 0 : (row < kK + kTileRows ? 1 : 2);
+      cp_async16(dst + row * kTileRowBytes, base[reg] + (size_t)row * pitch);
+      if (k == kHalfRows - 1) asm volatile("cp.async.commit_group;" ::: "memory");  // rows 0..31: phases 0-1
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   uint32_t P0[kK][4], P1[kK][4];
 #pragma unroll
@@ -677,29 +677,25 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
 #pragma unroll
     for (int w = 0; w < 4; ++w) P0[j][w] = P1[j][w] = 0u;
   uint32_t acc = 0xFFFFFFFFu, accTop = 0xFFFFFFFFu, accBot = 0xFFFFFFFFu;
-  const ptrdiff_t od_a = ((homes >> 6) & 1u) ? delta : 0, od_b = ((homes >> 7) & 1u) ? delta : 0;
-  uint16_t* oA = f0 + od_a + (size_t)(rA + kK) * pitch + colA;  // tile row 0
-  uint16_t* oB = f0 + od_b + (size_t)(rB + kK) * pitch + colB;
-  const bool st_lane = lane >= kK / kTileWPL && lane < 32 - kK / kTileWPL;
-  const bool sa = st_lane, sb = st_lane && hasB;
+  const ptrdiff_t od = ((homes >> 6) & 1u) ? delta : 0;
+  uint16_t* oA = f0 + od + (size_t)(c * kTileRows + kK) * pitch + b * kTileCols + lane * kTileWPL;  // tile row 0
+  uint16_t* oB = oA + (size_t)kHalfRows * pitch;                                                 // tile row 16
+  const bool st = lane >= kK / kTileWPL && lane < 32 - kK / kTileWPL;
   const uint8_t* rb = buf + lane * 8;
-  auto any_lag = [](uint32_t l) { return __any_sync(0xffffffffu, l != 0u); };
-  asm volatile("cp.async.wait_group 2;" ::: "memory");
-  __syncwarp();
-  tile_phase<kOutNone>(rb, 0, kK, lw[0], any_lag(lw[0]), P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
+  const uint32_t lag_up = lw[0] | lw[1] << 16, lag_in = lw[1] | lw[1] << 16, lag_dn = lw[1] | lw[2] << 16;
+  const bool l_up = __any_sync(0xffffffffu, lag_up != 0u), l_in = __any_sync(0xffffffffu, lag_in != 0u),
+             l_dn = __any_sync(0xffffffffu, lag_dn != 0u);
   asm volatile("cp.async.wait_group 1;" ::: "memory");
   __syncwarp();
-  const bool l1 = any_lag(lw[1]);
-  tile_phase<kOutNone>(rb, kK, 2 * kK, lw[1], l1, P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
-  tile_phase<kOutTop>(rb, 2 * kK, 3 * kK, lw[1], l1, P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
-  tile_phase<kOutMid>(rb, 3 * kK, kK + kTileRows, lw[1], l1, P0, P1, oA, oB, pitch, sa, sb, acc, accTop);
+  tile_phase<kOutNone>(rb, 0, kK, lag_up, l_up, P0, P1, oA, oB, pitch, st, acc, accTop);
+  tile_phase<kOutNone>(rb, kK, 2 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
-  tile_phase<kOutBot>(rb, kK + kTileRows, kTileSteps, lw[2], any_lag(lw[2]), P0, P1, oA, oB, pitch, sa, sb, acc,
-                      accBot);
-  if (!st_lane) acc = accTop = accBot = 0xFFFFFFFFu;  // halo lanes hold no output
-  edge_min[0] = accTop;
-  edge_min[1] = accBot;
+  tile_phase<kOutTop>(rb, 2 * kK, 3 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
+  tile_phase<kOutBot>(rb, 3 * kK, kTileSteps, lag_dn, l_dn, P0, P1, oA, oB, pitch, st, acc, accBot);
+  if (!st) acc = accTop = accBot = 0xFFFFFFFFu;  // halo lanes hold no output
+  edge[0] = accTop;
+  edge[1] = accBot;
   return acc;
 }
 
@@ -755,17 +751,19 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
                   const uint8_t* __restrict__ rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag) {
   extern __shared__ __align__(128) uint8_t smem_tiles[];
+  // programmatic dependent launch: this grid may start while the previous
+  // block's grid drains; wait for it (memory visible) before touching state,
+  // and let the next block's grid get scheduled right away
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   const uint32_t n = book.count[blk % 3];
   const uint32_t* __restrict__ list = book.list[blk & 1];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     book.count[(blk + 2) % 3] = 0;
+    book.count[3 + (blk + 2) % 3] = 0;
     atomicAdd(book.processed, (unsigned long long)n);
   }
   const uint32_t l1 = l0 + kK;  // layer after this block
-  // Pairing two tiles per warp halves the instructions but also the warps;
-  // with few active tiles the kernel is latency bound and more warps win.
-  const uint32_t per = (CB == 16 && AM_TILE_PAIR) ? 2u : 1u;
-  const uint32_t nw = gridDim.x * (kBlockThreads / 32);
   const int lane = threadIdx.x & 31;
   constexpr int kHaloLanes = kK / kTileWPL;  // lanes holding the left / right halo columns
   const int brel = lane < kHaloLanes ? -1 : (lane >= 32 - kHaloLanes ? 1 : 0);  // band of this lane's cells
@@ -786,97 +784,84 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     return e < l0 ? l0 - e : 0u;
   };
   uint32_t gmin = 0xFFFFFFFFu;
-  for (uint32_t w = blockIdx.x * (kBlockThreads / 32) + (threadIdx.x >> 5); w * per < n; w += nw) {
-    const uint32_t ia = list[w * per];
-    const bool hasB = per == 2u && w * per + 1 < n;
-    const uint32_t ib = hasB ? list[w * per + 1] : ia;
-    const uint32_t bA = ia >> 16, cA = ia & 0xFFFFu, bB = ib >> 16, cB = ib & 0xFFFFu;
-    const uint32_t tA = cA * g.tbands + bA, tB = cB * g.tbands + bB;
-    // own states before the reads of the neighbours (they are rewritten below)
-    const uint32_t sa = state_at_l0(tA), sb = state_at_l0(tB);
-    uint32_t lw[3], homes = 0;
+  constexpr int kL = kHaloLanes, kR = 32 - 2 * kHaloLanes;  // first lane of the left / right edge columns
+  auto lanes_min = [&](uint32_t v, int first) {
+    uint32_t m = __shfl_sync(0xffffffffu, v, first);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      uint32_t ha, hb;
-      const uint32_t la = region(cA, bA, d - 1, ha), lb = region(cB, bB, d - 1, hb);
-      lw[d] = CB == 16 ? (la | lb << 16) : la;
-      homes |= ha << d | hb << (3 + d);
-    }
-    // own rows go to the field that is not the tile's home
-    homes |= ((sa & 1u) ^ 1u) << 6 | ((sb & 1u) ^ 1u) << 7;
-    uint32_t edge[2];
-    uint32_t acc;
-    bool staged = false;
-    if constexpr (CB == 16) {  // rows holding a source need the +1 path
-      const uint32_t ra = cA * kTileRows, rb = cB * kTileRows;
-      const uint8_t* rfa = rowsrc + g.tile_rowsrc(bA) + ra;
-      const uint8_t* rfb = rowsrc + g.tile_rowsrc(bB) + rb;
-      uint32_t f = rfa[lane] | rfb[lane];
-      if (lane < kTileSteps - 32) f |= rfa[32 + lane] | rfb[32 + lane];
-      staged = !__any_sync(0xffffffffu, f != 0u);
-      if (staged)
-        acc = tile_item16(g, f0, delta, bA, cA, bB, cB, hasB, lw, homes, edge,
-                          smem_tiles + (threadIdx.x >> 5) * kTileBufBytes);
-    }
-    if (!staged)
-      acc = stream_item<CB, false, true, kTileStages, kTileWPL, kTileWarpSmem>(
-          g, f0, f0, srcmask, rowsrc + g.tile_rowsrc(bA), rowsrc + g.tile_rowsrc(bB), bA, cA * kTileRows, bB,
-          cB * kTileRows, kTileRows, hasB, lw[0], lw[1], lw[2],
-          delta, homes, edge);
-    // Frontier regions of each tile: cells with a == 1 (covered in the block's
-    // last layer; min(a-1) == 0) anywhere / in the first or last kK rows / in
-    // the first or last kK useful columns (the lanes next to the halo lanes) /
-    // the corners.
-    auto lanes_min = [&](uint32_t v, int first) {
-      uint32_t m = __shfl_sync(0xffffffffu, v, first);
+    for (int k = 1; k < kHaloLanes; ++k) m = Cell<CB>::vmin(m, __shfl_sync(0xffffffffu, v, first + k));
+    return m;
+  };
+  // items are fetched dynamically: a warp that finishes early takes the next one
+  auto fetch = [&]() {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(&book.count[3 + blk % 3], 1u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  for (uint32_t w = fetch(); w < n; w = fetch()) {
+    const uint32_t it = list[w];
+    const uint32_t bA = it >> 16, cA = it & 0xFFFFu;
+    const uint32_t tA = cA * g.tbands + bA;
+    const uint32_t sa = state_at_l0(tA);  // own state before the neighbours' (rewritten below)
+    uint32_t lw[3], hm[3];
 #pragma unroll
-      for (int k = 1; k < kHaloLanes; ++k) m = Cell<CB>::vmin(m, __shfl_sync(0xffffffffu, v, first + k));
-      return m;
-    };
-    constexpr int kL = kHaloLanes, kR = 32 - 2 * kHaloLanes;  // first lane of the left / right edge columns
-    const uint32_t vals[9] = {acc,
-                              edge[0],
-                              edge[1],
-                              lanes_min(acc, kL),
-                              lanes_min(acc, kR),
-                              lanes_min(edge[0], kL),
-                              lanes_min(edge[0], kR),
-                              lanes_min(edge[1], kL),
-                              lanes_min(edge[1], kR)};
-    auto regions = [&](int half) -> uint32_t {
-      auto h = [&](uint32_t v) { return CB == 16 ? (half ? v >> 16 : v & 0xFFFFu) : v; };
-      uint32_t m = 0;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const uint32_t v = k < 3 ? __reduce_min_sync(0xffffffffu, h(vals[k])) : h(vals[k]);
-        m |= (v == 0u ? 1u : 0u) << k;
+    for (int d = 0; d < 3; ++d) lw[d] = region(cA, bA, d - 1, hm[d]);
+    const uint32_t out_home = (sa & 1u) ^ 1u;  // own rows go to the field that is not the tile's home
+    const uint8_t* rf = rowsrc + g.tile_rowsrc(bA);
+    uint32_t edge[2], acc;
+    uint32_t m9;  // frontier regions (bits: any, top, bottom, left, right, tl, tr, bl, br)
+    if constexpr (CB == 16) {
+      // upper half (lo): tile rows 0-15, lower half (hi): rows 16-31
+      const uint32_t ra = cA * kTileRows;
+      uint32_t f = rf[ra + lane];
+      if (lane < kStageRows - 32) f |= rf[ra + 32 + lane];
+      if (!__any_sync(0xffffffffu, f != 0u)) {
+        acc = tile_item16(g, f0, delta, bA, cA, lw, hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6, edge,
+                          smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem);
+      } else {  // a source in reach: the general path, same halves
+        const uint32_t homes = hm[0] | hm[1] << 1 | hm[1] << 2 | hm[1] << 3 | hm[1] << 4 | hm[2] << 5 |
+                               out_home << 6 | out_home << 7;
+        acc = stream_item<16, false, true, kTileStages, kTileWPL, kTileWarpSmem>(
+            g, f0, f0, srcmask, rf, rf, bA, ra, bA, ra + kHalfRows, kHalfRows, true, lw[0] | lw[1] << 16,
+            lw[1] | lw[1] << 16, lw[1] | lw[2] << 16, delta, homes, edge);
       }
-      return m;
-    };
-    const uint32_t fa = regions(0), fb = CB == 16 ? regions(1) : fa;
-    uint32_t ma, mb;
-    if (CB == 16) {
-      ma = __reduce_min_sync(0xffffffffu, acc & 0xFFFFu);
-      mb = __reduce_min_sync(0xffffffffu, acc >> 16);
+      auto lo = [](uint32_t v) { return v & 0xFFFFu; };
+      auto hi = [](uint32_t v) { return v >> 16; };
+      auto both = [&](uint32_t v) { return min(lo(v), hi(v)); };
+      const uint32_t vals[9] = {both(__reduce_min_sync(0xffffffffu, lo(acc)) | __reduce_min_sync(0xffffffffu, hi(acc)) << 16),
+                                __reduce_min_sync(0xffffffffu, lo(edge[0])),
+                                __reduce_min_sync(0xffffffffu, hi(edge[1])),
+                                both(lanes_min(acc, kL)),
+                                both(lanes_min(acc, kR)),
+                                lo(lanes_min(edge[0], kL)),
+                                lo(lanes_min(edge[0], kR)),
+                                hi(lanes_min(edge[1], kL)),
+                                hi(lanes_min(edge[1], kR))};
+      m9 = 0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) m9 |= (vals[k] == 0u ? 1u : 0u) << k;
+      gmin = min(gmin, vals[0]);
     } else {
-      ma = mb = __reduce_min_sync(0xffffffffu, acc);
+      const uint32_t homes = hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6;
+      acc = stream_item<CB, false, true, kTileStages, kTileWPL, kTileWarpSmem>(
+          g, f0, f0, srcmask, rf, rf, bA, cA * kTileRows, bA, cA * kTileRows, kTileRows, false, lw[0], lw[1], lw[2],
+          delta, homes, edge);
+      const uint32_t vals[9] = {__reduce_min_sync(0xffffffffu, acc), __reduce_min_sync(0xffffffffu, edge[0]),
+                                __reduce_min_sync(0xffffffffu, edge[1]), lanes_min(acc, kL), lanes_min(acc, kR),
+                                lanes_min(edge[0], kL), lanes_min(edge[0], kR), lanes_min(edge[1], kL),
+                                lanes_min(edge[1], kR)};
+      m9 = 0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) m9 |= (vals[k] == 0u ? 1u : 0u) << k;
+      gmin = min(gmin, vals[0]);
     }
-    // new states (old kept in the high word for this block's readers)
-    if (lane == 0) {
-      book.state[tA] = (unsigned long long)sa << 32 | (l1 << 1 | ((sa & 1u) ^ 1u));
-      if (hasB) book.state[tB] = (unsigned long long)sb << 32 | (l1 << 1 | ((sb & 1u) ^ 1u));
-    }
-    // push the next block's candidates: lanes 0-8 for tile A, 9-17 for tile B
+    // new state (old kept in the high word for this block's readers)
+    if (lane == 0) book.state[tA] = (unsigned long long)sa << 32 | (l1 << 1 | out_home);
+    // list the next block's candidates: lane k < 9 for the neighbour at (dr, dc) = (k/3-1, k%3-1)
     {
-      const int k = lane < 9 ? lane : lane - 9;
-      const int dr = k / 3 - 1, dc = k % 3 - 1;  // T = N - (dr, dc) is activated by N's facing region
-      const bool forB = lane >= 9 && lane < 18;
-      const uint32_t m = forB ? (hasB ? fb : 0u) : (lane < 9 ? fa : 0u);
-      const bool want = lane < 18 && ((m >> kFacing[dr + 1][dc + 1]) & 1u);
-      const int c = (int)(forB ? cB : cA) - dr, b = (int)(forB ? bB : bA) - dc;
-      push_tiles(g, book, blk, want, c, b);
+      const int dr = lane / 3 - 1, dc = lane % 3 - 1;  // T = N - (dr, dc) is activated by N's facing region
+      const bool want = lane < 9 && ((m9 >> kFacing[(lane / 3) % 3][lane % 3]) & 1u);
+      push_tiles(g, book, blk, want, (int)cA - dr, (int)bA - dc);
     }
-    gmin = min(gmin, min(ma, hasB ? mb : ma));
   }
   publish_flag<true>(flag, gmin, gridDim.x);
 }
@@ -972,6 +957,8 @@ __global__ void k_tiles_all(Geo g, TileBook book, uint32_t blk, uint32_t layer, 
   if (t == 0) {
     book.count[blk % 3] = g.ntiles();
     book.count[(blk + 1) % 3] = 0;
+    book.count[3 + blk % 3] = 0;
+    book.count[3 + (blk + 1) % 3] = 0;
   }
   if (t >= g.ntiles()) return;
   const uint32_t cur = layer << 1 | home;
@@ -1180,8 +1167,19 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
   (void)attr;
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
-    k_block_tiles<16><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint16_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
-                                                              flag);
+    // programmatic stream serialization: the launch overlaps the previous block's tail (griddepcontrol.wait)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kBlockThreads);
+    cfg.dynamicSmemBytes = kTileSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_block_tiles<16>, g, a, (ptrdiff_t)((uint16_t*)f1 - a), srcmask, rowsrc, book, blk, l0,
+                       flag);
   } else {
     auto* a = (uint32_t*)f0;
     k_block_tiles<32><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
