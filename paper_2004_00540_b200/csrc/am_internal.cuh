@@ -128,8 +128,9 @@ void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer,
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f1, const uint8_t* srcmask,
                         const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
                         cudaStream_t s);
+// zero (nullable): also ORs 1 into *zero if a free cell is still uncovered (fused k_zero_check)
 void launch_tiles_finalize(const Geo& g, int cell_bits, unsigned long long* state, void* f0, void* f1, int dst,
-                           uint32_t l, cudaStream_t s);
+                           uint32_t l, uint32_t* zero, cudaStream_t s);
 void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);
 void launch_zero_check(const Geo& g, int cell_bits, const void* val, uint32_t* flag, cudaStream_t s);
 void launch_decode(const Geo& g, int cell_bits, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,

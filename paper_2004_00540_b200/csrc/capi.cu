@@ -411,8 +411,8 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     return AM_OK;
   };
   // every tile current at at_layer in val[0] (then cur = 0)
-  auto tiles_finalize = [&](uint32_t at_layer) -> am_status {
-    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_state, tg->val[0], tg->val[1], 0, at_layer, ctx->stream);
+  auto tiles_finalize = [&](uint32_t at_layer, uint32_t* zero = nullptr) -> am_status {
+    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_state, tg->val[0], tg->val[1], 0, at_layer, zero, ctx->stream);
     CKL();
     tg->cur = 0;
     return AM_OK;
@@ -576,8 +576,11 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   if ((st = close_run())) return st;
   while (!pend.empty())
     if ((st = drain_one())) return st;
+  const int zslot = (int)(nblock % kFlagSlots);
   if (tiles) {
-    if ((st = tiles_finalize(l))) return st;
+    uint32_t* z = autom ? tg->d_flags + zslot : nullptr;  // the gather also runs the zero check
+    if (z) CK(cudaMemsetAsync(z, 0, sizeof(uint32_t), ctx->stream));
+    if ((st = tiles_finalize(l, z))) return st;
     unsigned long long proc = 0;
     CK(cudaMemcpyAsync(&proc, tg->t_processed, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -586,12 +589,12 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   }
   uint32_t used = l, cause = AM_STOP_FIXED;
   if (autom) {
-    const int zslot = (int)(nblock % kFlagSlots);
     for (size_t i = 0; i < slabs.size(); ++i) {
       am_ctx* c = slabs[i].ctx;
       am_grid* g = slabs[i].g;
       uint32_t* z = g->d_flags + zslot;
       words[i] = z;
+      if (tiles) continue;  // done by the gather
       CK(cudaMemsetAsync(z, 0, sizeof(uint32_t), c->stream));
       launch_zero_check(g->g, g->cell_bits, g->val[g->cur], z, c->stream);
       CKL();

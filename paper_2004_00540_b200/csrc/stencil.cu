@@ -906,15 +906,19 @@ __device__ __forceinline__ void tile_rows_foreach(const Geo& g, uint32_t band, u
 // current in dst (state = l << 1 | dst).
 template <int CB>
 __global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, typename Cell<CB>::T* __restrict__ f0,
-                                 ptrdiff_t delta, uint32_t dst, uint32_t l) {
+                                 ptrdiff_t delta, uint32_t dst, uint32_t l, uint32_t* __restrict__ zero) {
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= g.ntiles()) return;
   const uint32_t s = (uint32_t)state[t], home = s & 1u, e = s >> 1;
-  if (e != l || home != dst) {
+  const bool move = e != l || home != dst;
+  if (move || zero) {
     const uint32_t lag = l - e;
     const uint32_t lagw = CB == 16 ? (lag | lag << 16) : lag;
     const typename Cell<CB>::T* src = f0 + (home ? delta : 0);
     typename Cell<CB>::T* out = f0 + (dst ? delta : 0);
+    // fused fixed-point zero check (k_zero_check): a free cell still at a = 0 is the bare flag
+    const uint32_t bare = CB == 16 ? 0x80008000u : kFlag32;
+    bool z = false;
     tile_rows_foreach<CB>(g, t % g.tbands, t / g.tbands, [&](size_t i) {
       uint4 v = *reinterpret_cast<const uint4*>(src + i);
       if (lag) {
@@ -923,8 +927,14 @@ __global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, 
         v.z = add_lag<CB>(v.z, lagw);
         v.w = add_lag<CB>(v.w, lagw);
       }
-      *reinterpret_cast<uint4*>(out + i) = v;
+      if (zero) {
+        const uint32_t w[4] = {v.x ^ bare, v.y ^ bare, v.z ^ bare, v.w ^ bare};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) z |= CB == 16 ? ((w[k] & 0xFFFFu) == 0u || (w[k] >> 16) == 0u) : w[k] == 0u;
+      }
+      if (move) *reinterpret_cast<uint4*>(out + i) = v;
     });
+    if (zero && __any_sync(0xffffffffu, z) && (threadIdx.x & 31) == 0) atomicOr(zero, 1u);
   }
   __syncwarp();
   if ((threadIdx.x & 31) == 0) state[t] = (unsigned long long)(l << 1 | dst) << 32 | (l << 1 | dst);
@@ -1189,14 +1199,14 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
 
 // every tile to layer l in field dst (0 = f0, 1 = f1)
 void launch_tiles_finalize(const Geo& g, int cb, unsigned long long* state, void* f0, void* f1, int dst, uint32_t l,
-                           cudaStream_t s) {
+                           uint32_t* zero, cudaStream_t s) {
   const uint32_t n = g.ntiles();
   if (cb == 16) {
     auto* a = (uint16_t*)f0;
-    k_tiles_finalize<16><<<(n + 3) / 4, 128, 0, s>>>(g, state, a, (uint16_t*)f1 - a, (uint32_t)dst, l);
+    k_tiles_finalize<16><<<(n + 3) / 4, 128, 0, s>>>(g, state, a, (uint16_t*)f1 - a, (uint32_t)dst, l, zero);
   } else {
     auto* a = (uint32_t*)f0;
-    k_tiles_finalize<32><<<(n + 3) / 4, 128, 0, s>>>(g, state, a, (uint32_t*)f1 - a, (uint32_t)dst, l);
+    k_tiles_finalize<32><<<(n + 3) / 4, 128, 0, s>>>(g, state, a, (uint32_t*)f1 - a, (uint32_t)dst, l, zero);
   }
 }
 
