@@ -145,81 +145,68 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
 }
 
 // Windowed walk for maps produced by the device propagation (encoded
-// fields).  The warp stages a 32x32 window of decoded activities around the
-// current cell in shared memory (lane i loads window row i with 16 B
-// vectors), then takes steps inside it with one shared-memory read per
+// fields).  The warp stages a window of RAW cells around the current cell in
+// shared memory (32x32 cells; 16 B vector
+// loads), then takes steps inside it with one shared-memory read per
 // candidate lane and two votes per step; it re-stages when the current
-// cell's 3x3 neighbourhood reaches the window border (~15 steps per load).
-// A cell is a source exactly when its activity is L+1 (d = 0), so no
-// source-mask load is needed.  Candidate lanes follow the reference
-// enumerations: row-major for the simple rule (pin P2), axis order L,R,U,D
-// then the diagonals for the Euclidean rule (pin P1).  Points are gathered
-// 32 at a time and written by the whole warp.
-constexpr int kWin = 32;
+// cell's 3x3 neighbourhood reaches the window border (~15-31 steps per load).
+// Raw cells compare like decoded activities: every free cell has the flag
+// bit, so it beats any obstacle or padding cell (flag clear), and free cells
+// order by activity; a cell is a source exactly when its activity is L+1
+// (d = 0), so no source-mask load is needed.  Candidate lanes follow the
+// reference enumerations: row-major for the simple rule (pin P2), axis order
+// L,R,U,D then the diagonals for the Euclidean rule (pin P1).  Points are
+// gathered 32 at a time and written by the whole warp.
+#ifndef AM_TWR
+#define AM_TWR 32  // 16-bit window rows
+#endif
+#ifndef AM_TWC
+#define AM_TWC 32  // 16-bit window columns (smaller windows stage faster; tools/ab_trace.sh)
+#endif
+constexpr int kWinBytes = AM_TWR * AM_TWC * 2 > 4096 ? AM_TWR * AM_TWC * 2 : 4096;  // shared memory per warp
 
+template <typename T, int WR, int WC>
 __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int method, uint64_t seed, uint64_t limit,
-                              uint32_t* out, int32_t* st, uint32_t* win) {
+                              uint32_t* out, int32_t* st, T* win) {
+  static_assert(WR * WC * sizeof(T) <= kWinBytes && WR % 32 == 0, "window");
+  constexpr int kVec = 16 / sizeof(T);  // cells per 16 B vector
   const int lane = threadIdx.x & 31;
   const MapView& m = rd.m;
   const int pad = (int)m.g.pad, pitch = (int)m.g.pitch;
-  const int rmax = (int)m.g.rows - pad - kWin;  // window origin limits (grid coordinates)
-  const uint32_t top = m.layers + 1;            // activity of a source
+  const int rmax = (int)m.g.rows - pad - WR;  // window origin limits (grid coordinates)
+  const T* field = static_cast<const T*>(m.val);
+  const uint32_t flag = sizeof(T) == 2 ? kFlag16 : kFlag32;
+  const uint32_t top = flag | (m.layers + 1);  // raw value of a source
   uint64_t rng = seed;
-  // candidate offsets of this lane (lanes 0..7)
-  int dr = 0, dc = 0;
-  if (method == 0) {
-    dr = kDR[lane & 7];
-    dc = kDC[lane & 7];
-  } else {
-    const int er[8] = {0, 0, -1, 1, -1, -1, 1, 1}, ec[8] = {-1, 1, 0, 0, -1, 1, -1, 1};
-    dr = er[lane & 7];
-    dc = ec[lane & 7];
-  }
+  // candidate k (lane k < 8): 2-bit packed (d + 1) offsets, k-th pair
+  const uint32_t pr_ = method == 0 ? 0xA940u : 0xA085u;  // dr: simple -1,-1,-1,0,0,1,1,1 / eucl 0,0,-1,1,-1,-1,1,1
+  const uint32_t pc_ = method == 0 ? 0x9224u : 0x8858u;  // dc: simple -1,0,1,-1,1,-1,0,1 / eucl -1,1,0,0,-1,1,-1,1
+  auto off = [](uint32_t pack, int k) { return (int)((pack >> (2 * k)) & 3u) - 1; };
+  const int dr = off(pr_, lane & 7), dc = off(pc_, lane & 7);
   int wr = 0, wc = 0;
   bool loaded = false;
   auto stage = [&]() {
-    wr = min(max((int)r - kWin / 2, -pad), rmax);
-    const int ac = min(max(((int)c + pad - kWin / 2) & ~7, 0), pitch - kWin);  // allocated column, 16 B aligned
+    wr = min(max((int)r - WR / 2, -pad), rmax);
+    const int ac = min(max(((int)c + pad - WC / 2) & ~(kVec - 1), 0), pitch - WC);  // allocated column, 16 B aligned
     wc = ac - pad;
-    const size_t row = (size_t)(wr + lane + pad) * pitch + ac;
     __syncwarp();  // previous window fully read
-    if (m.cell_bits == 16) {
-      const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(m.val) + row);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 v = p[q];
-        const uint32_t h[4] = {v.x, v.y, v.z, v.w};
-        uint32_t d[8];
+    for (int h = 0; h < WR / 32; ++h) {
+      const int row = lane + 32 * h;
+      const uint4* p = reinterpret_cast<const uint4*>(field + (size_t)(wr + row + pad) * pitch + ac);
+      uint4* o = reinterpret_cast<uint4*>(win + row * WC);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t lo = h[k] & 0xFFFFu, hi = h[k] >> 16;
-          d[2 * k] = (lo & kFlag16) ? (lo & 0x7FFFu) : 0u;
-          d[2 * k + 1] = (hi & kFlag16) ? (hi & 0x7FFFu) : 0u;
-        }
-        uint4* o = reinterpret_cast<uint4*>(win + lane * kWin + q * 8);
-        o[0] = make_uint4(d[0], d[1], d[2], d[3]);
-        o[1] = make_uint4(d[4], d[5], d[6], d[7]);
-      }
-    } else {
-      const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(m.val) + row);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint4 v = p[q];
-        auto dec = [](uint32_t x) { return (x & kFlag32) ? (x & kLow32) : 0u; };
-        reinterpret_cast<uint4*>(win + lane * kWin)[q] = make_uint4(dec(v.x), dec(v.y), dec(v.z), dec(v.w));
-      }
+      for (int q = 0; q < WC / kVec; ++q) o[q] = p[q];
     }
     __syncwarp();
     loaded = true;
   };
-  uint32_t cur = rd.value(r, c);
+  uint32_t cur = field[rd.m.g.idx(r, c)];
   uint64_t n = 0;
   uint32_t keep_r = 0, keep_c = 0;  // point n of this lane's slot (n % 32 == lane)
   auto record = [&]() {
     if ((int)(n & 31) == lane) keep_r = r, keep_c = c;
-    if ((n & 31) == 31) {
-      reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r, keep_c);
-    }
+    if ((n & 31) == 31) reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r, keep_c);
     ++n;
   };
   record();
@@ -229,8 +216,8 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
       return 0;
     }
     const int pr = (int)r - wr, pc = (int)c - wc;
-    if (!loaded || pr < 1 || pr > kWin - 2 || pc < 1 || pc > kWin - 2) stage();
-    const uint32_t v = lane < 8 ? win[((int)r - wr + dr) * kWin + ((int)c - wc + dc)] : 0u;
+    if (!loaded || pr < 1 || pr > WR - 2 || pc < 1 || pc > WC - 2) stage();
+    const uint32_t v = lane < 8 ? (uint32_t)win[((int)r - wr + dr) * WC + ((int)c - wc + dc)] : 0u;
     int sel = -1;
     uint32_t best;
     if (method == 0) {  // simple: 8-neighbour argmax, seeded tie-break (pin P2)
@@ -256,8 +243,8 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
       *st = ST_EINTERNAL;  // no ascending neighbour
       return 0;
     }
-    r = (uint32_t)((int)r + __shfl_sync(0xffffffffu, dr, sel));
-    c = (uint32_t)((int)c + __shfl_sync(0xffffffffu, dc, sel));
+    r = (uint32_t)((int)r + off(pr_, sel));
+    c = (uint32_t)((int)c + off(pc_, sel));
     cur = best;
     record();
   }
@@ -300,10 +287,13 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
   Reader rd{m};
   const uint64_t off = offsets[w], limit = offsets[w + 1] - off;
   int32_t st = ST_OK;
-  __shared__ __align__(16) uint32_t wins[4][kWin * kWin];  // one window per warp (128-thread CTAs)
-  const uint64_t got = m.cell_bits
-                           ? walk_smem(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st,
-                                       wins[(threadIdx.x >> 5) & 3])
+  __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
+  uint8_t* win = wins[(threadIdx.x >> 5) & 3];
+  const uint64_t got = m.cell_bits == 16 ? walk_smem<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed,
+                                                                       limit, pts + 2 * off, &st, (uint16_t*)win)
+                       : m.cell_bits == 32
+                           ? walk_smem<uint32_t, 32, 32>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit,
+                                                         pts + 2 * off, &st, (uint32_t*)win)
                            : walk<true>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit, pts + 2 * off, &st);
   if ((threadIdx.x & 31) == 0) {
     if (st != ST_OK) status[w] = st;
