@@ -70,6 +70,7 @@ struct am_grid {
   uint32_t* t_count = nullptr;               // [6] list lengths, item fetch counters (TileBook::count)
   unsigned long long* t_processed = nullptr; // tiles processed (statistics)
   uint32_t t_blk = 0;                        // index of the next tile block (list / counter selection)
+  void* t_bnd = nullptr;                     // slabs: first / last kK rows gathered for the neighbours (2 x kK x pitch)
   am::TileBook book() const { return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed}; }
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;
@@ -108,9 +109,16 @@ inline am_status fail(am_ctx* ctx, am_status st, const char* fmt, ...) {
 inline bool dims_ok(uint32_t w, uint32_t h) { return w >= 1 && h >= 1 && w <= 65535 && h <= 65535; }
 
 // rows [first, last) of slab r out of n over h rows
+// Slab boundaries fall on tile-chunk multiples (kTileRows) whenever every
+// slab keeps at least two chunks, so active-tile skipping works across slabs.
 inline void slab_rows(uint32_t h, uint32_t n, uint32_t r, uint32_t* first, uint32_t* last) {
-  *first = (uint32_t)((uint64_t)h * r / n);
-  *last = (uint32_t)((uint64_t)h * (r + 1) / n);
+  auto cut = [&](uint32_t k) -> uint32_t {
+    uint64_t b = (uint64_t)h * k / n;
+    if (k > 0 && k < n && h >= 2u * kTileRows * n) b = (b + kTileRows / 2) / kTileRows * kTileRows;
+    return (uint32_t)b;
+  };
+  *first = cut(r);
+  *last = cut(r + 1);
 }
 
 // Halo transport used by the propagation driver between blocks.
@@ -118,6 +126,9 @@ struct Transport {
   virtual ~Transport() = default;
   // enqueue the K-row halo refresh of every local slab (reads current buffers)
   virtual am_status exchange() = 0;
+  // active tiles: send each slab's gathered boundary rows (t_bnd) into its
+  // neighbours' halo rows of field 0
+  virtual am_status exchange_tiles() = 0;
   // make the per-slab device word *w (one per local slab) global: min or max over all slabs
   virtual am_status reduce(std::vector<uint32_t*>& words, bool take_max) = 0;
   // local values must still be combined on the host (in-process groups)

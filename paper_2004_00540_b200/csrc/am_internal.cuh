@@ -125,12 +125,19 @@ void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const 
 void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cudaStream_t s);
 // every tile current at `layer` in field `home`, all listed for block blk
 void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer, int home, cudaStream_t s);
+// pdl: launch with programmatic stream serialization (back-to-back tile blocks on one stream)
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag, bool pdl,
                         cudaStream_t s);
 // zero (nullable): also ORs 1 into *zero if a free cell is still uncovered (fused k_zero_check)
 void launch_tiles_finalize(const Geo& g, int cell_bits, unsigned long long* state, void* f0, void* f1, int dst,
                            uint32_t l, uint32_t* zero, cudaStream_t s);
+// row slabs with active tiles: the slab's first / last kK rows at layer l into
+// bnd (2 x kK x pitch, the halo rows its neighbours read), and the list entry
+// of every boundary tile a frontier cell in the received halo rows can reach
+void launch_tiles_boundary(const Geo& g, int cell_bits, const unsigned long long* state, void* f0, void* f1,
+                           uint32_t l, void* bnd, cudaStream_t s);
+void launch_tiles_halo_scan(const Geo& g, int cell_bits, const void* f0, TileBook book, uint32_t blk, cudaStream_t s);
 void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);
 void launch_zero_check(const Geo& g, int cell_bits, const void* val, uint32_t* flag, cudaStream_t s);
 void launch_decode(const Geo& g, int cell_bits, const void* val, uint32_t rollback, uint32_t r0, uint32_t r1,

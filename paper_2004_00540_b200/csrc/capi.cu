@@ -160,6 +160,7 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->t_list[0]);
   am::dfree(ctx, g->t_list[1]);
   am::dfree(ctx, g->t_count);
+  am::dfree(ctx, g->t_bnd);
   am::dfree(ctx, g->t_processed);
   delete g;
 }
@@ -203,13 +204,15 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = am::dmalloc(ctx, &g->srcmask_dense, dense);
   if (!e) e = am::dmalloc(ctx, &g->d_flags, (kFlagSlots + 1) * sizeof(uint32_t));
   if (!e) e = take_flag_set(ctx, &g->fs);
-  if (!slab) {  // active-tile skipping state
+  {  // active-tile skipping state
     const size_t nt = g->g.ntiles();
     if (!e) e = am::dmalloc(ctx, &g->t_state, nt * 8);
     if (!e) e = am::dmalloc(ctx, &g->t_sched, nt * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_list[0], nt * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_list[1], nt * 4);
     if (!e) e = am::dmalloc(ctx, &g->t_count, 6 * 4);
+    if (slab && !e) e = am::dmalloc(ctx, &g->t_bnd, (size_t)2 * kK * g->g.pitch * 4);  // room for 32-bit cells
+    if (slab && !e) e = cudaMemsetAsync(g->t_bnd, 0, (size_t)2 * kK * g->g.pitch * 4, s);
     if (!e) e = am::dmalloc(ctx, &g->t_processed, 8);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
@@ -398,33 +401,54 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   for (auto& s : slabs)
     if ((st = reset_map(s.ctx, s.g, start_bits))) return st;
 
-  // exact active-tile skipping: single grids in batched mode
-  am_grid* tg = slabs[0].g;
-  const bool tiles = slabs.size() == 1 && !tr && !tg->slab && tg->t_state && mode == AM_MODE_BATCHED &&
-                     !(ctx->flags & AM_CTX_DENSE);
-  const size_t nt = tiles ? tg->g.ntiles() : 0;
+  // exact active-tile skipping in batched mode.  Row slabs
+  // must meet at tile-chunk boundaries, so their halo rows lie outside every
+  // tile (am_comm_slab_rows aligns them); the halos then carry the
+  // neighbours' boundary rows at the block's layer (k_tiles_boundary).
+  bool tiles = mode == AM_MODE_BATCHED && !(ctx->flags & AM_CTX_DENSE);
+  for (size_t i = 0; i < slabs.size(); ++i) {
+    tiles = tiles && slabs[i].g->t_state;
+    if (i + 1 < slabs.size()) tiles = tiles && slabs[i].g->g.H % kTileRows == 0;
+  }
+  const bool halos = tiles && (slabs.size() > 1 || tr);  // boundary exchange + halo scan every block
+  uint64_t nt = 0;
+  for (auto& sr : slabs) nt += tiles ? sr.g->g.ntiles() : 0;
   const int tile_ctas = ctx->sms * kTileCtasPerSm;  // persistent k_block_tiles
   // after dense work: every tile current at at_layer in val[cur], all active next block
   auto tiles_all_active = [&](uint32_t at_layer) -> am_status {
-    launch_tiles_all(tg->g, tg->book(), tg->t_blk, at_layer, tg->cur, ctx->stream);
-    CKL();
+    for (auto& sr : slabs) {
+      am_ctx* c = sr.ctx;
+      launch_tiles_all(sr.g->g, sr.g->book(), sr.g->t_blk, at_layer, sr.g->cur, c->stream);
+      CKL();
+    }
     return AM_OK;
   };
-  // every tile current at at_layer in val[0] (then cur = 0)
-  auto tiles_finalize = [&](uint32_t at_layer, uint32_t* zero = nullptr) -> am_status {
-    launch_tiles_finalize(tg->g, tg->cell_bits, tg->t_state, tg->val[0], tg->val[1], 0, at_layer, zero, ctx->stream);
-    CKL();
-    tg->cur = 0;
+  // every tile current at at_layer in val[0] (then cur = 0); zslot >= 0: fused zero check into that flag slot
+  auto tiles_finalize = [&](uint32_t at_layer, int zslot = -1) -> am_status {
+    for (auto& sr : slabs) {
+      am_ctx* c = sr.ctx;
+      am_grid* g = sr.g;
+      uint32_t* z = zslot >= 0 ? g->d_flags + zslot : nullptr;
+      if (z) CK(cudaMemsetAsync(z, 0, sizeof(uint32_t), c->stream));
+      launch_tiles_finalize(g->g, g->cell_bits, g->t_state, g->val[0], g->val[1], 0, at_layer, z, c->stream);
+      CKL();
+      g->cur = 0;
+    }
     return AM_OK;
   };
   if (tiles) {  // layer 0 lives in val[cur] (= val[0] after reset_map): state 0 << 1 | 0
-    tg->t_blk = 0;
-    CK(cudaMemsetAsync(tg->t_state, 0, nt * 8, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_sched, 0, nt * 4, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_processed, 0, 8, ctx->stream));
-    CK(cudaMemsetAsync(tg->t_count, 0, 6 * 4, ctx->stream));
-    launch_tiles_init(tg->g, tg->srcmask, tg->book(), ctx->stream);
-    CKL();
+    for (auto& sr : slabs) {
+      am_ctx* c = sr.ctx;
+      am_grid* g = sr.g;
+      const size_t n = g->g.ntiles();
+      g->t_blk = 0;
+      CK(cudaMemsetAsync(g->t_state, 0, n * 8, c->stream));
+      CK(cudaMemsetAsync(g->t_sched, 0, n * 4, c->stream));
+      CK(cudaMemsetAsync(g->t_processed, 0, 8, c->stream));
+      CK(cudaMemsetAsync(g->t_count, 0, 6 * 4, c->stream));
+      launch_tiles_init(g->g, g->srcmask, g->book(), c->stream);
+      CKL();
+    }
   }
 
   am_prop_result r{};
@@ -445,7 +469,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   const bool mapped = autom && slabs.size() == 1 && !tr;
   bool armed[kFlagSlots];
   for (int i = 0; i < kFlagSlots; ++i) armed[i] = mapped;
-  if (mapped) CK(cudaMemsetAsync(tg->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), ctx->stream));
+  if (mapped) CK(cudaMemsetAsync(slabs[0].g->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), ctx->stream));
   std::deque<PendingBlock> pend;
   uint32_t l = 0;       // layers applied so far
   uint32_t lprime = 0;  // first layer without new cells (0 = not found)
@@ -499,7 +523,21 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     if (tiles && !blocked) {  // a dense single layer needs every tile current
       if ((st = tiles_finalize(l))) return st;
     }
-    if (tr && (st = tr->exchange())) return st;
+    if (halos && blocked) {
+      for (auto& sr : slabs) {  // boundary rows at layer l from the tiles' homes
+        am_grid* g = sr.g;
+        launch_tiles_boundary(g->g, g->cell_bits, g->t_state, g->val[0], g->val[1], l, g->t_bnd, sr.ctx->stream);
+        CKL();
+      }
+      if (tr && (st = tr->exchange_tiles())) return st;  // (a lone slab has no neighbours: halos stay padding)
+      for (auto& sr : slabs) {  // boundary tiles the received frontier reaches
+        am_grid* g = sr.g;
+        launch_tiles_halo_scan(g->g, g->cell_bits, g->val[0], g->book(), g->t_blk, sr.ctx->stream);
+        CKL();
+      }
+    } else if (tr && (st = tr->exchange())) {  // dense blocks / single layers (tiles gathered into val[0])
+      return st;
+    }
     const int slot = (int)(nblock % kFlagSlots);
     for (size_t i = 0; i < slabs.size(); ++i) {
       am_ctx* c = slabs[i].ctx;
@@ -531,7 +569,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         if (tiles) {
           // the tiles of this block list the next block's tiles themselves (TileBook)
           launch_block_tiles(g->g, g->cell_bits, tile_ctas, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->book(),
-                             g->t_blk, l, sink, s);
+                             g->t_blk, l, sink, !halos, s);
           ++g->t_blk;
         } else {
           launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, sink, s);
@@ -578,14 +616,14 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     if ((st = drain_one())) return st;
   const int zslot = (int)(nblock % kFlagSlots);
   if (tiles) {
-    uint32_t* z = autom ? tg->d_flags + zslot : nullptr;  // the gather also runs the zero check
-    if (z) CK(cudaMemsetAsync(z, 0, sizeof(uint32_t), ctx->stream));
-    if ((st = tiles_finalize(l, z))) return st;
-    unsigned long long proc = 0;
-    CK(cudaMemcpyAsync(&proc, tg->t_processed, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    r.tiles_processed = proc;
-    r.tiles_total = (uint64_t)nt * r.block_launches;
+    if ((st = tiles_finalize(l, autom ? zslot : -1))) return st;  // the gather also runs the zero check
+    for (auto& sr : slabs) {
+      unsigned long long proc = 0;
+      CK(cudaMemcpyAsync(&proc, sr.g->t_processed, 8, cudaMemcpyDeviceToHost, sr.ctx->stream));
+      CK(cudaStreamSynchronize(sr.ctx->stream));
+      r.tiles_processed += proc;
+    }
+    r.tiles_total = nt * r.block_launches;
   }
   uint32_t used = l, cause = AM_STOP_FIXED;
   if (autom) {
@@ -1019,7 +1057,7 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
     CK(cudaMemsetAsync(g->t_count + 3, 0, 4, s));  // block 0's item fetch counter
     if (r == 2) CK(cudaEventRecord(a, s));
     am::launch_block_tiles(g->g, 16, ctx->sms * am::kTileCtasPerSm, g->val[0], g->val[1], g->srcmask, g->rowsrc,
-                           g->book(), 0, 0, sink, s);
+                           g->book(), 0, 0, sink, true, s);
     ++ctx->launches;
   }
   CK(cudaEventRecord(b, s));

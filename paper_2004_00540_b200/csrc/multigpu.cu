@@ -111,6 +111,25 @@ struct NcclTransport final : Transport {
     NK(nccl().groupEnd());
     return AM_OK;
   }
+  am_status exchange_tiles() override {
+    Comm* cm = ctx->comm;
+    const size_t bytes = (size_t)kK * row_bytes(g);
+    uint8_t* bnd = static_cast<uint8_t*>(g->t_bnd);
+    uint8_t* f0 = static_cast<uint8_t*>(g->val[0]);
+    const uint32_t H = g->g.H;
+    NK(nccl().groupStart());
+    if (cm->rank > 0) {
+      NK(nccl().send(bnd, bytes, ncclUint8, (int)cm->rank - 1, cm->comm, ctx->stream));
+      NK(nccl().recv(f0, bytes, ncclUint8, (int)cm->rank - 1, cm->comm, ctx->stream));
+    }
+    if (cm->rank + 1 < cm->nranks) {
+      NK(nccl().send(bnd + bytes, bytes, ncclUint8, (int)cm->rank + 1, cm->comm, ctx->stream));
+      NK(nccl().recv(f0 + (size_t)(kK + H) * row_bytes(g), bytes, ncclUint8, (int)cm->rank + 1, cm->comm,
+                     ctx->stream));
+    }
+    NK(nccl().groupEnd());
+    return AM_OK;
+  }
   am_status reduce(std::vector<uint32_t*>& words, bool take_max) override {
     NK(nccl().allReduce(words[0], words[0], 1, ncclUint32, take_max ? ncclMax : ncclMin, ctx->comm->comm,
                         ctx->stream));
@@ -142,6 +161,20 @@ struct LocalTransport final : Transport {
         CK(cudaMemcpyAsync(alloc_rows(g, kK + g->g.H), alloc_rows(dn, kK), bytes, cudaMemcpyDeviceToDevice,
                            ctx->stream));
       }
+    }
+    return AM_OK;
+  }
+  am_status exchange_tiles() override {
+    for (size_t i = 0; i < s.size(); ++i) {
+      am_grid* g = s[i].g;
+      const size_t bytes = (size_t)kK * row_bytes(g);
+      uint8_t* f0 = static_cast<uint8_t*>(g->val[0]);
+      if (i > 0)  // the slab above's last rows become this slab's top halo
+        CK(cudaMemcpyAsync(f0, static_cast<uint8_t*>(s[i - 1].g->t_bnd) + bytes, bytes, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+      if (i + 1 < s.size())
+        CK(cudaMemcpyAsync(f0 + (size_t)(kK + g->g.H) * row_bytes(g), s[i + 1].g->t_bnd, bytes,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
     }
     return AM_OK;
   }

@@ -940,6 +940,61 @@ __global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, 
   if ((threadIdx.x & 31) == 0) state[t] = (unsigned long long)(l << 1 | dst) << 32 | (l << 1 | dst);
 }
 
+// Row slabs: the slab's first (side 0) and last (side 1) kK rows at layer l,
+// gathered from each tile's home field with its lag, into bnd[side] (pitched
+// rows, padding columns left as allocated).  One warp per (side, tile band).
+template <int CB>
+__global__ void k_tiles_boundary(Geo g, const unsigned long long* __restrict__ state,
+                                 const typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, uint32_t l,
+                                 typename Cell<CB>::T* __restrict__ bnd) {
+  const uint32_t w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (w >= 2 * g.tbands) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t side = w / g.tbands, b = w % g.tbands;
+  constexpr int kVecCells = 16 / sizeof(typename Cell<CB>::T);
+  constexpr int kVecs = kTileCols / kVecCells;  // vectors per tile row
+  for (int v = lane; v < kVecs * kK; v += 32) {
+    const uint32_t k = v / kVecs, q = v % kVecs;
+    const uint32_t r = side ? g.H - kK + k : k;  // slab row
+    const uint32_t s = (uint32_t)state[(r / kTileRows) * g.tbands + b], home = s & 1u, e = s >> 1;
+    const uint32_t lag = l - e, lagw = CB == 16 ? (lag | lag << 16) : lag;
+    const size_t col = g.pad + b * kTileCols + q * kVecCells;
+    uint4 x = *reinterpret_cast<const uint4*>(f0 + (home ? delta : 0) + (size_t)(r + g.pad) * g.pitch + col);
+    if (lag) {
+      x.x = add_lag<CB>(x.x, lagw);
+      x.y = add_lag<CB>(x.y, lagw);
+      x.z = add_lag<CB>(x.z, lagw);
+      x.w = add_lag<CB>(x.w, lagw);
+    }
+    *reinterpret_cast<uint4*>(bnd + ((size_t)side * kK + k) * g.pitch + col) = x;
+  }
+}
+
+// Row slabs: lists for block blk every boundary tile (first / last chunk) that
+// a frontier cell (a == 1) of the received halo rows lies within kK of.
+template <int CB>
+__global__ void k_tiles_halo_scan(Geo g, const typename Cell<CB>::T* __restrict__ f0, TileBook book, uint32_t blk) {
+  const uint32_t w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (w >= 2 * g.tbands) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const uint32_t side = w / g.tbands, b = w % g.tbands;
+  constexpr int kVecCells = 16 / sizeof(typename Cell<CB>::T);
+  constexpr int kVecs = (kTileCols + 2 * kK) / kVecCells;  // the band's columns plus kK each side
+  const uint32_t frontier = CB == 16 ? (kFlag16 | 1u) : (kFlag32 | 1u);
+  const uint32_t row0 = side ? g.H + kK : 0u;  // allocated halo rows
+  bool any = false;
+  for (int v = lane; v < kVecs * kK; v += 32) {
+    const uint32_t k = v / kVecs, q = v % kVecs;
+    const uint4 x = *reinterpret_cast<const uint4*>(f0 + (size_t)(row0 + k) * g.pitch + b * kTileCols + q * kVecCells);
+    const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      any |= CB == 16 ? ((ws[i] & 0xFFFFu) == frontier || (ws[i] >> 16) == frontier) : ws[i] == frontier;
+  }
+  any = __any_sync(0xffffffffu, any);
+  push_tiles(g, book, blk - 1u, any && lane == 0, side ? (int)g.nchunks - 1 : 0, (int)b);
+}
+
 // Block 0's work list: the 3x3 neighbourhood of every tile holding a source
 // (the layer-0 frontier, a = 1); pushed as block "-1" (lists 0, sched 1).
 __global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, TileBook book) {
@@ -1160,6 +1215,26 @@ void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cuda
   k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, book);
 }
 
+void launch_tiles_boundary(const Geo& g, int cb, const unsigned long long* state, void* f0, void* f1, uint32_t l,
+                           void* bnd, cudaStream_t s) {
+  const uint32_t warps = 2 * g.tbands;
+  if (cb == 16) {
+    auto* a = (const uint16_t*)f0;
+    k_tiles_boundary<16><<<(warps + 3) / 4, 128, 0, s>>>(g, state, a, (const uint16_t*)f1 - a, l, (uint16_t*)bnd);
+  } else {
+    auto* a = (const uint32_t*)f0;
+    k_tiles_boundary<32><<<(warps + 3) / 4, 128, 0, s>>>(g, state, a, (const uint32_t*)f1 - a, l, (uint32_t*)bnd);
+  }
+}
+
+void launch_tiles_halo_scan(const Geo& g, int cb, const void* f0, TileBook book, uint32_t blk, cudaStream_t s) {
+  const uint32_t warps = 2 * g.tbands;
+  if (cb == 16)
+    k_tiles_halo_scan<16><<<(warps + 3) / 4, 128, 0, s>>>(g, (const uint16_t*)f0, book, blk);
+  else
+    k_tiles_halo_scan<32><<<(warps + 3) / 4, 128, 0, s>>>(g, (const uint32_t*)f0, book, blk);
+}
+
 void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer, int home, cudaStream_t s) {
   const uint32_t n = g.ntiles();
   k_tiles_all<<<(n + 255) / 256, 256, 0, s>>>(g, book, blk, layer, (uint32_t)home);
@@ -1167,7 +1242,7 @@ void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer,
 
 // f0/f1: the two fields; book: tile states / lists (block blk reads list[blk & 1])
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag, bool pdl,
                         cudaStream_t s) {
   static bool attr = [] {
     cudaFuncSetAttribute(k_block_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
@@ -1187,7 +1262,7 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_block_tiles<16>, g, a, (ptrdiff_t)((uint16_t*)f1 - a), srcmask, rowsrc, book, blk, l0,
                        flag);
   } else {

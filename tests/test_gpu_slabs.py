@@ -44,6 +44,50 @@ def test_slabs_auto_match_oracle(n):
             s.close()
 
 
+def aligned_split(h, n, tile_rows=32):
+    """am_comm_slab_rows' cuts: tile-chunk multiples, so the slabs run with active-tile skipping."""
+    def cut(k):
+        b = h * k // n
+        if 0 < k < n and h >= 2 * tile_rows * n:
+            b = (b + tile_rows // 2) // tile_rows * tile_rows
+        return b
+    return [(cut(r), cut(r + 1)) for r in range(n)]
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_tile_slabs_match_oracle_and_dense(n):
+    """Slabs meeting at tile-chunk boundaries use active tiles with boundary-row exchange + halo scan."""
+    ctx, dctx = am.default_context(), am.Context(0, dense=True)
+    for seed, (w, h), dens, ns in [(5, (300, 400), 0.3, 4), (6, (517, 700), 0.45, 6), (7, (240, 320), 0.0, 2),
+                                   (8, (1100, 1024), 0.4, 9)]:
+        occ = O.random_maze(w, h, dens, seed)
+        # sources right at the slab boundaries too
+        cuts = [a for a, _ in aligned_split(h, n)][1:]
+        src = np.concatenate([O.sample_free_cells(occ, ns, seed),
+                              np.array([[c, x] for c in cuts for x in range(0, w, 97) if occ[c, x] == 0][:6],
+                                       np.uint32).reshape(-1, 2)])
+        src = np.unique(src, axis=0)
+        sm = O.source_mask(occ, src)
+        slabs = [am.Grid.slab(occ, src, a, b, ctx) for a, b in aligned_split(h, n)]
+        dslabs = [am.Grid.slab(occ, src, a, b, dctx) for a, b in aligned_split(h, n)]
+        for cap in (5, 8, 4 * max(w, h)):
+            r = am.slabs_propagate(slabs, auto_cap=cap)
+            assert r.block_launches == 0 or r.tiles_total > 0, "tile mode expected for aligned slabs"
+            ref, rl, rc = O.propagate_auto(occ, sm, cap, threads=8)
+            assert (r.layers_used, r.cause) == (rl, rc), (n, seed, cap)
+            got = np.concatenate([s.activity() for s in slabs])
+            assert np.array_equal(got, ref), (n, seed, cap)
+            rd = am.slabs_propagate(dslabs, auto_cap=cap)
+            assert rd.tiles_total == 0 and (rd.layers_used, rd.cause) == (rl, rc)
+        for L in (8, 24, 3 * max(w, h) // 2):
+            am.slabs_propagate(slabs, layers=L)
+            got = np.concatenate([s.activity() for s in slabs])
+            assert np.array_equal(got, O.propagate(occ, sm, L)), (n, seed, L)
+        for s in slabs + dslabs:
+            s.close()
+    dctx.close()
+
+
 def test_slabs_gather_then_trace():
     ctx = am.default_context()
     occ = O.random_maze(800, 600, 0.35, 11)

@@ -28,8 +28,14 @@ def free_port():
     return p
 
 
-def slab_rows(h, n, r):
-    return h * r // n, h * (r + 1) // n
+def slab_rows(h, n, r, tile_rows=32):
+    """Mirror of am::slab_rows (am_host.hpp): cuts on tile-chunk multiples when every slab keeps two chunks."""
+    def cut(k):
+        b = h * k // n
+        if 0 < k < n and h >= 2 * tile_rows * n:
+            b = (b + tile_rows // 2) // tile_rows * tile_rows
+        return b
+    return cut(r), cut(r + 1)
 
 
 def termination(start, count, m):
@@ -129,4 +135,8 @@ def test_slab_rows_partition():
             rows = [slab_rows(h, n, r) for r in range(n)]
             assert rows[0][0] == 0 and rows[-1][1] == h
             assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
-            assert max(b - a for a, b in rows) - min(b - a for a, b in rows) <= 1
+            if h >= 64 * n:  # tile-aligned cuts, balanced to within one chunk
+                assert all(a[1] % 32 == 0 for a in rows[:-1])
+                assert max(b - a for a, b in rows) - min(b - a for a, b in rows) <= 32
+            else:
+                assert max(b - a for a, b in rows) - min(b - a for a, b in rows) <= 1
