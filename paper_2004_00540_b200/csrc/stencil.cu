@@ -699,6 +699,17 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
   return acc;
 }
 
+// The rare items whose rows hold a source (the +1 path): kept out of line so
+// the hot loop of k_block_tiles stays small in the instruction cache.
+__device__ __noinline__ uint32_t tile_item16_sources(const Geo& g, uint16_t* f0, const uint8_t* srcmask,
+                                                     const uint8_t* rf, uint32_t b, uint32_t ra, uint32_t lag0,
+                                                     uint32_t lag1, uint32_t lag2, ptrdiff_t delta, uint32_t homes,
+                                                     uint32_t* edge) {
+  return stream_item<16, false, true, kTileStages, kTileWPL, kTileWarpSmem>(g, f0, f0, srcmask, rf, rf, b, ra, b,
+                                                                            ra + kHalfRows, kHalfRows, true, lag0,
+                                                                            lag1, lag2, delta, homes, edge);
+}
+
 // Dense mode: every (band, segment pair) of the grid, one warp each.
 template <int CB, bool SLAB>
 __global__ void __launch_bounds__(kBlockThreads, AM_BLOCK_MINB) k_block(Geo g, const typename Cell<CB>::T* __restrict__ in,
@@ -820,9 +831,8 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
       } else {  // a source in reach: the general path, same halves
         const uint32_t homes = hm[0] | hm[1] << 1 | hm[1] << 2 | hm[1] << 3 | hm[1] << 4 | hm[2] << 5 |
                                out_home << 6 | out_home << 7;
-        acc = stream_item<16, false, true, kTileStages, kTileWPL, kTileWarpSmem>(
-            g, f0, f0, srcmask, rf, rf, bA, ra, bA, ra + kHalfRows, kHalfRows, true, lw[0] | lw[1] << 16,
-            lw[1] | lw[1] << 16, lw[1] | lw[2] << 16, delta, homes, edge);
+        acc = tile_item16_sources(g, f0, srcmask, rf, bA, ra, lw[0] | lw[1] << 16, lw[1] | lw[1] << 16,
+                                  lw[1] | lw[2] << 16, delta, homes, edge);
       }
       auto lo = [](uint32_t v) { return v & 0xFFFFu; };
       auto hi = [](uint32_t v) { return v >> 16; };

@@ -56,6 +56,20 @@ def main():
     print("idle gaps by transition:")
     for k, us in gaps.most_common(4):
         print(f"  {k:55s} {us / 1e3:8.3f} ms")
+    ends = [e["ts"] + e["dur"] for e in dev if e["cat"] == "kernel" and "block_tiles" in e["name"]]
+    if len(ends) > 10:
+        step = [b - a for a, b in zip(ends, ends[1:])]  # per-block span: end-to-end spacing of consecutive blocks
+        print("k_block_tiles end spacing by launch decile (mean us): " +
+              " ".join(f"{sum(x) / len(x):.1f}" for x in (step[i * len(step) // 10:(i + 1) * len(step) // 10]
+                                                          for i in range(10))))
+    tk = [e["dur"] for e in dev if e["cat"] == "kernel" and "block_tiles" in e["name"]]
+    if tk:
+        q = sorted(tk)
+        pct = lambda p: q[min(len(q) - 1, int(p * len(q)))]
+        print(f"k_block_tiles durations: p10 {pct(0.1):.1f} p50 {pct(0.5):.1f} p90 {pct(0.9):.1f} max {q[-1]:.1f} us; "
+              f"by launch index decile (mean us): " +
+              " ".join(f"{sum(tk[i * len(tk) // 10:(i + 1) * len(tk) // 10]) / max(1, len(tk) // 10):.0f}"
+                       for i in range(10)))
     gl = sorted(max(b["ts"] - (a["ts"] + a["dur"]), 0) for a, b in zip(dev, dev[1:]))
     big = [x for x in gl if x > 20]
     print(f"gaps: n={len(gl)} median={gl[len(gl) // 2]:.2f} us p99={gl[int(len(gl) * 0.99)]:.2f} us "
