@@ -351,6 +351,7 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 #define AM_SKEW 1
 #endif
 
+
 constexpr int kStages = AM_STAGES;                 // rows in flight per warp (dense sweep)
 constexpr int kTileStages = AM_TILE_STAGES;        // rows in flight per warp (active tiles: few warps per SM)
 // one stage = one u32 row of the warp's band, or the A+B pair of u16 rows
@@ -647,9 +648,10 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
 // 6 = output field.  Returns the min over covered output cells of a-1 (lo =
 // upper half, hi = lower half); edge[0] / edge[1]: the same over the first /
 // last kK rows of each half (use lo of [0] and hi of [1]).
-__device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta, uint32_t b,
-                                                uint32_t c, const uint32_t (&lw)[3], uint32_t homes,
-                                                uint32_t* edge, uint8_t* buf) {
+// Issues the copies of the tile's rows into buf (two commit groups); the
+// caller may still decide not to run the staged path (then waits them out).
+__device__ __forceinline__ void tile_stage16(const Geo& g, const uint16_t* __restrict__ f0, ptrdiff_t delta,
+                                             uint32_t b, uint32_t c, uint32_t homes, uint8_t* buf) {
   const int lane = threadIdx.x & 31;
   const size_t pitch = g.pitch;
   __syncwarp();  // every lane is done reading the previous item's rows
@@ -671,6 +673,13 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
+}
+
+__device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta, uint32_t b,
+                                                uint32_t c, const uint32_t (&lw)[3], uint32_t homes,
+                                                uint32_t* edge, const uint8_t* buf) {
+  const int lane = threadIdx.x & 31;
+  const size_t pitch = g.pitch;
   uint32_t P0[kK][4], P1[kK][4];
 #pragma unroll
   for (int j = 0; j < kK; ++j)
@@ -808,27 +817,36 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     if (lane == 0) v = atomicAdd(&book.count[3 + blk % 3], 1u);
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  for (uint32_t w = fetch(); w < n; w = fetch()) {
+  // (a static first item per warp packs light blocks onto few SMs: measured slower)
+  uint32_t w = fetch();
+  while (w < n) {
     const uint32_t it = list[w];
     const uint32_t bA = it >> 16, cA = it & 0xFFFFu;
     const uint32_t tA = cA * g.tbands + bA;
+    const uint8_t* rf = rowsrc + g.tile_rowsrc(bA);
+    const uint32_t ra = cA * kTileRows;
+    uint32_t f = 0;  // source rows in reach (loaded alongside the states)
+    if constexpr (CB == 16) {
+      f = rf[ra + lane];
+      if (lane < kStageRows - 32) f |= rf[ra + 32 + lane];
+    }
     const uint32_t sa = state_at_l0(tA);  // own state before the neighbours' (rewritten below)
     uint32_t lw[3], hm[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) lw[d] = region(cA, bA, d - 1, hm[d]);
     const uint32_t out_home = (sa & 1u) ^ 1u;  // own rows go to the field that is not the tile's home
-    const uint8_t* rf = rowsrc + g.tile_rowsrc(bA);
     uint32_t edge[2], acc;
     uint32_t m9;  // frontier regions (bits: any, top, bottom, left, right, tl, tr, bl, br)
     if constexpr (CB == 16) {
       // upper half (lo): tile rows 0-15, lower half (hi): rows 16-31
-      const uint32_t ra = cA * kTileRows;
-      uint32_t f = rf[ra + lane];
-      if (lane < kStageRows - 32) f |= rf[ra + 32 + lane];
+      uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
+      const uint32_t homes16 = hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6;
+      tile_stage16(g, f0, delta, bA, cA, homes16, buf);  // copies in flight during the source vote
       if (!__any_sync(0xffffffffu, f != 0u)) {
-        acc = tile_item16(g, f0, delta, bA, cA, lw, hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6, edge,
-                          smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem);
-      } else {  // a source in reach: the general path, same halves
+        acc = tile_item16(g, f0, delta, bA, cA, lw, homes16, edge, buf);
+      } else {  // a source in reach: the general path, same halves (its ring reuses buf)
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
         const uint32_t homes = hm[0] | hm[1] << 1 | hm[1] << 2 | hm[1] << 3 | hm[1] << 4 | hm[2] << 5 |
                                out_home << 6 | out_home << 7;
         acc = tile_item16_sources(g, f0, srcmask, rf, bA, ra, lw[0] | lw[1] << 16, lw[1] | lw[1] << 16,
@@ -864,6 +882,7 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
       for (int k = 0; k < 9; ++k) m9 |= (vals[k] == 0u ? 1u : 0u) << k;
       gmin = min(gmin, vals[0]);
     }
+    const uint32_t next = fetch();  // the next item's index travels while this item's bookkeeping runs
     // new state (old kept in the high word for this block's readers)
     if (lane == 0) book.state[tA] = (unsigned long long)sa << 32 | (l1 << 1 | out_home);
     // list the next block's candidates: lane k < 9 for the neighbour at (dr, dc) = (k/3-1, k%3-1)
@@ -872,6 +891,7 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
       const bool want = lane < 9 && ((m9 >> kFacing[(lane / 3) % 3][lane % 3]) & 1u);
       push_tiles(g, book, blk, want, (int)cA - dr, (int)bA - dc);
     }
+    w = next;
   }
   publish_flag<true>(flag, gmin, gridDim.x);
 }
