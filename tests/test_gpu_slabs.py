@@ -115,3 +115,24 @@ def test_slab_validation():
         am.Grid.slab(occ, [[0, 0]], 0, 4, ctx)  # fewer rows than the halo depth
     with pytest.raises(am.InvalidInputError):
         am.Grid.slab(occ, [[0, 0]], 10, 50, ctx)
+
+
+def test_tile_slabs_promotion_to_32bit():
+    """Tile-mode slabs across the 16 -> 32-bit promotion: boundary rows, halos and lags stay exact."""
+    occ = O.comb_maze(330, 200)  # serpentine longer than the 16-bit range
+    src = np.array([[0, 329]], np.uint32)
+    sm = O.source_mask(occ, src)
+    ctx = am.default_context()
+    cuts = aligned_split(occ.shape[0], 2)
+    assert cuts[0][1] % 32 == 0
+    slabs = [am.Grid.slab(occ, src, a, b, ctx) for a, b in cuts]
+    r = am.slabs_propagate(slabs, auto_cap=200_000)
+    hops = O.bfs_multi_source(occ, sm)
+    ecc = int(hops[hops != O.UNREACH].max())
+    assert r.cell_bits == 32 and r.tiles_total > 0
+    assert (r.layers_used, r.cause) == (ecc, O.FILLED)
+    got = np.concatenate([s.activity() for s in slabs])
+    bad, _ = O.check_activity(occ, got, hops, r.layers_used)
+    assert bad == 0
+    for s in slabs:
+        s.close()
