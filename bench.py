@@ -144,8 +144,25 @@ def cpu_baseline(occ, src, budget_s=12.0):
     t0 = time.perf_counter()
     O.propagate(occ, sm, L, threads=threads)
     dt = time.perf_counter() - t0
-    return {"value": round(W * H * L / dt / 1e9, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle propagate, full {W}x{H} C4 grid, fixed L={L} slice ({dt:.1f}s), threads={threads}"}
+    t0 = time.perf_counter()
+    O.propagate(occ, sm, 1, threads=1)
+    single = W * H / (time.perf_counter() - t0) / 1e9
+    rate = W * H * L / dt / 1e9
+    return {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(), "single_thread_value": round(single, 4),
+            "sample": f"oracle propagate, full {W}x{H} C4 grid, fixed L={L} slice ({dt:.1f}s), threads={threads}; "
+                      f"single thread: one layer"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, rank, world):
@@ -251,15 +268,23 @@ class Solver:
         self.full.close()
 
 
-def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts):
-    """One end-to-end solve through the C ABI with host buffers (pinned)."""
+def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts, split=None):
+    """One end-to-end solve through the C ABI with host buffers (pinned).  split: dict that receives the
+    wall-clock of the H2D (grid create) and of the full-map D2H."""
     my_tgt = tgt[rank::world]
     if world == 1:
+        t0 = time.perf_counter()
         g = am.Grid(occ, src, ctx)
+        t1 = time.perf_counter()
         g.propagate_auto(AUTO_CAP)
         off, pts, st = g.trace(my_tgt, am.EUCLIDEAN, out=h_pts)
+        t2 = time.perf_counter()
         g.activity(out=h_map)
+        t3 = time.perf_counter()
         g.close()
+        if split is not None:
+            split.setdefault("create_h2d", []).append(t1 - t0)
+            split.setdefault("map_d2h", []).append(t3 - t2)
         return off, pts, st
     r0, r1 = ctx.slab_rows(H)
     s = am.Grid.slab(occ, src, r0, r1, ctx)
@@ -378,13 +403,13 @@ def run_b200(args, rank, world, local_rank):
         h_occ = torch.from_numpy(occ).pin_memory().numpy()
         h_map = torch.empty((H, W), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         h_pts = torch.empty((16 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-        e2e_times = []
+        e2e_times, split = [], {}
         for i in range(3):
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            off2, pts2, st2 = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map, h_pts)
+            off2, pts2, st2 = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map, h_pts, split if i else None)
             ctx.synchronize()
             dt = time.perf_counter() - t0
             if dist:
@@ -399,6 +424,7 @@ def run_b200(args, rank, world, local_rank):
         d2h = W * rows_map * 4 + pts2.nbytes + off2.nbytes + st2.nbytes * 2
         e2e = {"value": round(cell_updates / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "time_to_solve_s": round(e2e_s, 4),
+               "split_ms": {k: round(1000 * statistics.median(v), 2) for k, v in split.items()},
                "api": "am_grid_create(host) + am_propagate(auto) + am_path_counts + am_trace_paths + "
                       "am_activity_download (pinned host buffers)" +
                       ("; per rank: slab grid, NCCL halos, am_comm_gather" if world > 1 else "")}
@@ -406,6 +432,7 @@ def run_b200(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(occ, src)
+        cpu["extrapolated_time_to_solve_s"] = round(cell_updates / (cpu["value"] * 1e9), 1)  # W*H*L_used / rate
 
     if rank == 0:
         line = {
@@ -424,6 +451,10 @@ def run_b200(args, rank, world, local_rank):
             "phase_ms": {"propagate": round(prop_ms, 3), "paths": round(path_ms, 3),
                          "path_share": round(path_ms / max(prop_ms + path_ms, 1e-9), 4)},
             "stencil_gcell_per_s": round(stencil_gcells, 2),
+            "propagate_gcell_per_s": round(cell_updates / (prop_ms / 1000) / 1e9, 1),
+            "cell_updates": {"dense_equivalent_per_step": int(cell_updates),
+                             "executed_per_step": int(tiles_done // args.steps * info["tile_rows"] * info["tile_cols"]
+                                                      * LAYERS_PER_BLOCK) if tiles_all else int(cell_updates)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 3), "traffic": ncu_traffic("tiles" if tile_mode else "dense"),
                          "kernel": kernel, "algorithmic_bytes_per_launch": int(alg_bytes),

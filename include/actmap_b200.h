@@ -201,6 +201,9 @@ am_status am_batch_trace_paths(am_ctx *ctx, am_batch *batch, const uint32_t *tgt
 /* random_maze / comb_maze (grid.hpp:65-76) into a caller buffer of W*H bytes. */
 am_status am_random_maze(uint32_t width, uint32_t height, double density, uint64_t seed, uint8_t *occupancy);
 am_status am_comb_maze(uint32_t width, uint32_t height, uint8_t *occupancy);
+/* benchmark workloads: C2 perfect maze, C3 city blocks (new, not in the reference) */
+am_status am_kruskal_maze(uint32_t width, uint32_t height, uint64_t seed, uint8_t *occupancy);
+am_status am_city_grid(uint32_t width, uint32_t height, uint64_t seed, uint8_t *occupancy);
 /* straighten (reconstruct.hpp:49-58); occupancy may be NULL for the
  * geometric variant; rule 0 = strict, 1 = permissive.  out may alias pts. */
 am_status am_straighten(const uint32_t *pts_rc, uint64_t n, const uint8_t *occupancy, uint32_t width,

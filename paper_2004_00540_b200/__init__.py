@@ -114,6 +114,8 @@ def lib():
             "am_batch_trace_paths": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
             "am_random_maze": (st, [u32, u32, C.c_double, u64, _vp]),
             "am_comb_maze": (st, [u32, u32, _vp]),
+            "am_kruskal_maze": (st, [u32, u32, u64, _vp]),
+            "am_city_grid": (st, [u32, u32, u64, _vp]),
             "am_straighten": (st, [_vp, u64, _vp, u32, u32, u32, _vp, _u64p]),
             "am_path_metrics": (st, [_vp, u64, _u64p, C.POINTER(C.c_double)]),
         }
@@ -600,6 +602,20 @@ def random_maze(width: int, height: int, density: float, seed: int) -> np.ndarra
     """grid.hpp:72-76."""
     occ = np.empty((height, width), np.uint8)
     _check(lib().am_random_maze(width, height, density, seed, _ptr(occ)), None, "random_maze")
+    return occ
+
+
+def kruskal_maze(width: int, height: int, seed: int) -> np.ndarray:
+    """C2 workload: perfect maze on the odd lattice (randomised Kruskal, splitmix64)."""
+    occ = np.empty((height, width), np.uint8)
+    _check(lib().am_kruskal_maze(width, height, seed, _ptr(occ)), None, "kruskal_maze")
+    return occ
+
+
+def city_grid(width: int, height: int, seed: int) -> np.ndarray:
+    """C3 workload: city blocks U[32,96] with streets U[3,8], 10% plazas, 1% clutter."""
+    occ = np.empty((height, width), np.uint8)
+    _check(lib().am_city_grid(width, height, seed, _ptr(occ)), None, "city_grid")
     return occ
 
 

@@ -183,6 +183,85 @@ GridMap random_maze(uint32_t width, uint32_t height, double density, uint64_t se
   return GridMap(width, height, std::move(occ));
 }
 
+// Workload generators of the benchmark configurations.  C2:
+// perfect maze on the odd lattice (corridor cells at odd (r, c), 1-cell
+// walls) by randomised Kruskal: the lattice edges (right / down of each
+// corridor cell) in a splitmix64 Fisher-Yates order, a wall cell opened when
+// its edge joins two components.
+GridMap kruskal_maze(uint32_t width, uint32_t height, uint64_t seed) {
+  if (width < 3 || height < 3 || width > kMaxGridDim || height > kMaxGridDim)
+    throw InvalidInputError("kruskal_maze: bad dimensions");
+  std::vector<uint8_t> occ(static_cast<size_t>(width) * height, 1);
+  const uint32_t cw = (width - 1) / 2, ch = (height - 1) / 2;
+  const uint64_t cells = static_cast<uint64_t>(cw) * ch;
+  for (uint32_t i = 0; i < ch; ++i)
+    for (uint32_t j = 0; j < cw; ++j) occ[static_cast<size_t>(2 * i + 1) * width + 2 * j + 1] = 0;
+  std::vector<uint64_t> edges;  // 2 * cell + (0 right, 1 down)
+  edges.reserve(2 * cells);
+  for (uint64_t c = 0; c < cells; ++c) {
+    if (c % cw + 1 < cw) edges.push_back(2 * c);
+    if (c / cw + 1 < ch) edges.push_back(2 * c + 1);
+  }
+  uint64_t st = seed;
+  for (uint64_t i = edges.size(); i > 1; --i) std::swap(edges[i - 1], edges[bounded(splitmix64(st), i)]);
+  std::vector<uint32_t> parent(cells);
+  for (uint64_t c = 0; c < cells; ++c) parent[c] = static_cast<uint32_t>(c);
+  auto root = [&](uint32_t x) {
+    while (parent[x] != x) x = parent[x] = parent[parent[x]];
+    return x;
+  };
+  for (uint64_t e : edges) {
+    const uint64_t c = e >> 1;
+    const bool down = e & 1;
+    const uint32_t a = root(static_cast<uint32_t>(c)), b = root(static_cast<uint32_t>(down ? c + cw : c + 1));
+    if (a == b) continue;
+    parent[a] = b;
+    const uint32_t i = static_cast<uint32_t>(c / cw), j = static_cast<uint32_t>(c % cw);
+    occ[static_cast<size_t>(2 * i + 1 + (down ? 1 : 0)) * width + 2 * j + 1 + (down ? 0 : 1)] = 0;
+  }
+  return GridMap(width, height, std::move(occ));
+}
+
+// C3: city blocks of side U[32,96] separated by streets of width U[3,8]
+// along both axes; 10% of the blocks are left free as plazas (per-block
+// hash), and 1% single-cell clutter (per-cell hash) everywhere else.
+GridMap city_grid(uint32_t width, uint32_t height, uint64_t seed) {
+  if (width == 0 || height == 0 || width > kMaxGridDim || height > kMaxGridDim)
+    throw InvalidInputError("city_grid: bad dimensions");
+  uint64_t st = seed;
+  auto bands = [&](uint32_t n, std::vector<int64_t>& id) {  // block index per row / column, -1 = street
+    id.assign(n, -1);
+    uint32_t pos = static_cast<uint32_t>(3 + bounded(splitmix64(st), 6)), k = 0;
+    while (pos < n) {
+      const uint32_t b = static_cast<uint32_t>(32 + bounded(splitmix64(st), 65));
+      for (uint32_t x = pos; x < pos + b && x < n; ++x) id[x] = k;
+      ++k;
+      pos += b + static_cast<uint32_t>(3 + bounded(splitmix64(st), 6));
+    }
+    return k;
+  };
+  std::vector<int64_t> rid, cid;
+  bands(height, rid);
+  const uint32_t ncb = bands(width, cid);
+  const uint64_t plaza = splitmix64(st), clutter = splitmix64(st);
+  std::vector<uint8_t> occ(static_cast<size_t>(width) * height);
+  for (uint32_t r = 0; r < height; ++r)
+    for (uint32_t c = 0; c < width; ++c) {
+      const uint64_t idx = static_cast<uint64_t>(r) * width + c;
+      uint8_t ob = 0;
+      if (rid[r] >= 0 && cid[c] >= 0) {
+        uint64_t s = plaza ^ (static_cast<uint64_t>(rid[r]) * ncb + static_cast<uint64_t>(cid[c])) * 0xD1B54A32D192ED03ull;
+        ob = bounded(splitmix64(s), 100) >= 10;
+      }
+      if (!ob) {
+        uint64_t s = clutter ^ idx * 0x9E3779B97F4A7C15ull;
+        ob = bounded(splitmix64(s), 100) < 1;
+      }
+      occ[idx] = ob;
+    }
+  return GridMap(width, height, std::move(occ));
+}
+
 SourceSet::SourceSet(const GridMap& grid, std::span<const Coord> sources) {
   if (sources.empty()) throw InvalidInputError("SourceSet: at least one source is required");
   coords_.assign(sources.begin(), sources.end());
@@ -491,6 +570,32 @@ am_status am_random_maze(uint32_t w, uint32_t h, double density, uint64_t seed, 
   if (!occ) return AM_EINVAL;
   try {
     const auto g = actmap::random_maze(w, h, density, seed);
+    std::memcpy(occ, g.occupancy().data(), g.cell_count());
+    return AM_OK;
+  } catch (const actmap::InvalidInputError&) {
+    return AM_EINVAL;
+  } catch (...) {
+    return AM_EINTERNAL;
+  }
+}
+
+am_status am_kruskal_maze(uint32_t w, uint32_t h, uint64_t seed, uint8_t* occ) {
+  if (!occ) return AM_EINVAL;
+  try {
+    const auto g = actmap::kruskal_maze(w, h, seed);
+    std::memcpy(occ, g.occupancy().data(), g.cell_count());
+    return AM_OK;
+  } catch (const actmap::InvalidInputError&) {
+    return AM_EINVAL;
+  } catch (...) {
+    return AM_EINTERNAL;
+  }
+}
+
+am_status am_city_grid(uint32_t w, uint32_t h, uint64_t seed, uint8_t* occ) {
+  if (!occ) return AM_EINVAL;
+  try {
+    const auto g = actmap::city_grid(w, h, seed);
     std::memcpy(occ, g.occupancy().data(), g.cell_count());
     return AM_OK;
   } catch (const actmap::InvalidInputError&) {

@@ -57,3 +57,13 @@ def test_straighten_and_metrics_match_oracle():
 def test_layer_bound_host():
     for w, h in [(9, 9), (1, 1), (1000, 1000), (23170, 23170), (7, 300)]:
         assert am.layer_bound(w, h) == O.layer_bound(w, h)
+
+
+def test_workload_generators_match_oracle():
+    """am_kruskal_maze / am_city_grid (C2 / C3 workloads) reproduce the oracle's generators exactly."""
+    for w, h, s in [(41, 31, 2), (512, 300, 7), (3, 3, 1), (1025, 77, 11)]:
+        assert np.array_equal(am.kruskal_maze(w, h, s), O.kruskal_maze(w, h, s)), (w, h, s)
+    for w, h, s in [(300, 500, 3), (1000, 700, 9), (5, 5, 1)]:
+        assert np.array_equal(am.city_grid(w, h, s), O.city_grid(w, h, s)), (w, h, s)
+    with pytest.raises(am.InvalidInputError):
+        am.kruskal_maze(2, 10, 0)
