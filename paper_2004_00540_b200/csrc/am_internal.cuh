@@ -126,9 +126,12 @@ void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cuda
 // every tile current at `layer` in field `home`, all listed for block blk
 void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer, int home, cudaStream_t s);
 // pdl: launch with programmatic stream serialization (back-to-back tile blocks on one stream)
+// prev: the previous tile block's word, published (host + re-arm) by this launch; flag.host must be null
 void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag, bool pdl,
-                        cudaStream_t s);
+                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                        FlagSink prev, bool pdl, cudaStream_t s);
+// publishes a word the way the last CTA of a blocked launch would (FlagSink)
+void launch_publish_flag(FlagSink f, cudaStream_t s);
 // zero (nullable): also ORs 1 into *zero if a free cell is still uncovered (fused k_zero_check)
 void launch_tiles_finalize(const Geo& g, int cell_bits, unsigned long long* state, void* f0, void* f1, int dst,
                            uint32_t l, uint32_t* zero, cudaStream_t s);

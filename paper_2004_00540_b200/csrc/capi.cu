@@ -471,6 +471,17 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   for (int i = 0; i < kFlagSlots; ++i) armed[i] = mapped;
   if (mapped) CK(cudaMemsetAsync(slabs[0].g->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), ctx->stream));
   std::deque<PendingBlock> pend;
+  // Mapped tile blocks publish the PREVIOUS block's word (k_block_tiles' prologue); the last one
+  // of a run is published by a one-thread kernel before anything else touches the field.
+  FlagSink unpublished{nullptr, nullptr, nullptr};
+  auto publish_pending = [&]() -> am_status {
+    if (unpublished.host) {
+      launch_publish_flag(unpublished, ctx->stream);
+      CKL();
+      unpublished = FlagSink{nullptr, nullptr, nullptr};
+    }
+    return AM_OK;
+  };
   uint32_t l = 0;       // layers applied so far
   uint32_t lprime = 0;  // first layer without new cells (0 = not found)
   uint64_t nblock = 0;
@@ -510,6 +521,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     const uint32_t kk = blocked ? (uint32_t)K : 1u;
     const bool promoting = slabs[0].g->cell_bits == 16 && (uint64_t)l + kk + 1 > kMax16Activity;
     if ((!blocked || promoting) && (st = close_run())) return st;
+    if ((!blocked || promoting || !tiles) && (st = publish_pending())) return st;
     if (promoting) {
       while (!pend.empty() && !lprime)
         if ((st = drain_one())) return st;
@@ -552,7 +564,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       }
       armed[slot] = mapped && blocked;
       if (mapped && blocked) g->fs->h[slot] = kSlotPending;  // consumed 64 blocks ago (lag < kFlagSlots)
-      const FlagSink sink{flag, g->d_flags + kFlagSlots, mapped ? g->fs->hdev + slot : nullptr};
+      FlagSink sink{flag, g->d_flags + kFlagSlots, mapped ? g->fs->hdev + slot : nullptr};
       void* in = g->val[g->cur];
       void* outp = g->val[g->cur ^ 1];
       if (blocked) {
@@ -568,8 +580,13 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         }
         if (tiles) {
           // the tiles of this block list the next block's tiles themselves (TileBook)
+          const FlagSink prev = unpublished;
+          if (sink.host) {  // published by the next tile launch (or publish_pending)
+            unpublished = sink;
+            sink.host = nullptr;
+          }
           launch_block_tiles(g->g, g->cell_bits, tile_ctas, g->val[0], g->val[1], g->srcmask, g->rowsrc, g->book(),
-                             g->t_blk, l, sink, !halos, s);
+                             g->t_blk, l, sink, prev, !halos, s);
           ++g->t_blk;
         } else {
           launch_block(g->g, g->cell_bits, g->slab != 0, in, outp, g->srcmask, g->rowsrc, sink, s);
@@ -612,6 +629,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       if ((st = drain_one())) return st;
   }
   if ((st = close_run())) return st;
+  if ((st = publish_pending())) return st;
   while (!pend.empty())
     if ((st = drain_one())) return st;
   const int zslot = (int)(nblock % kFlagSlots);
@@ -1057,7 +1075,7 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
     CK(cudaMemsetAsync(g->t_count + 3, 0, 4, s));  // block 0's item fetch counter
     if (r == 2) CK(cudaEventRecord(a, s));
     am::launch_block_tiles(g->g, 16, ctx->sms * am::kTileCtasPerSm, g->val[0], g->val[1], g->srcmask, g->rowsrc,
-                           g->book(), 0, 0, sink, true, s);
+                           g->book(), 0, 0, sink, am::FlagSink{nullptr, nullptr, nullptr}, true, s);
     ++ctx->launches;
   }
   CK(cudaEventRecord(b, s));

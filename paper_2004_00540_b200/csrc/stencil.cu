@@ -769,13 +769,18 @@ __device__ __forceinline__ void push_tiles(const Geo& g, TileBook& book, uint32_
 template <int CB>
 __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
-                  const uint8_t* __restrict__ rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag) {
+                  const uint8_t* __restrict__ rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                  FlagSink prev) {
   extern __shared__ __align__(128) uint8_t smem_tiles[];
   // programmatic dependent launch: this grid may start while the previous
   // block's grid drains; wait for it (memory visible) before touching state,
   // and let the next block's grid get scheduled right away
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
+  // the previous block's fixed-point word is complete now: publish it here
+  // (no arrival counter or fence at the end of every block)
+  if (prev.host && blockIdx.x == 0 && threadIdx.x == 0)
+    *reinterpret_cast<volatile uint32_t*>(prev.host) = atomicExch(prev.word, 0xFFFFFFFFu);
   const uint32_t n = book.count[blk % 3];
   const uint32_t* __restrict__ list = book.list[blk & 1];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1245,6 +1250,12 @@ void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cuda
   k_tiles_init<<<(n + 3) / 4, 128, 0, s>>>(g, srcmask, book);
 }
 
+__global__ void k_publish_flag(FlagSink f) {
+  *reinterpret_cast<volatile uint32_t*>(f.host) = atomicExch(f.word, 0xFFFFFFFFu);
+}
+
+void launch_publish_flag(FlagSink f, cudaStream_t s) { k_publish_flag<<<1, 1, 0, s>>>(f); }
+
 void launch_tiles_boundary(const Geo& g, int cb, const unsigned long long* state, void* f0, void* f1, uint32_t l,
                            void* bnd, cudaStream_t s) {
   const uint32_t warps = 2 * g.tbands;
@@ -1272,8 +1283,8 @@ void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer,
 
 // f0/f1: the two fields; book: tile states / lists (block blk reads list[blk & 1])
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
-                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag, bool pdl,
-                        cudaStream_t s) {
+                        const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
+                        FlagSink prev, bool pdl, cudaStream_t s) {
   static bool attr = [] {
     cudaFuncSetAttribute(k_block_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
     cudaFuncSetAttribute(k_block_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
@@ -1294,11 +1305,11 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_block_tiles<16>, g, a, (ptrdiff_t)((uint16_t*)f1 - a), srcmask, rowsrc, book, blk, l0,
-                       flag);
+                       flag, prev);
   } else {
     auto* a = (uint32_t*)f0;
     k_block_tiles<32><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
-                                                              flag);
+                                                              flag, prev);
   }
 }
 
