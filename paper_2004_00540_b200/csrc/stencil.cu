@@ -350,6 +350,12 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 #ifndef AM_SKEW
 #define AM_SKEW 1
 #endif
+#ifndef AM_QUARTERS
+#define AM_QUARTERS 1  // light blocks run two quarter items per tile
+#endif
+#ifndef AM_QUARTER_SLOTS
+#define AM_QUARTER_SLOTS 1  // quarter items while they fit this many times into the warp slots
+#endif
 
 
 constexpr int kStages = AM_STAGES;                 // rows in flight per warp (dense sweep)
@@ -591,12 +597,13 @@ constexpr int kTileSmem = kWarpsPerCta * kTileWarpSmem;  // dynamic shared memor
 enum { kOutNone = 0, kOutTop = 1, kOutBot = 2 };
 
 // Steps [s0, s1): the upper half reads staged row s, the lower half row s+16.
-template <int OUT>
+// HI: rows between the two u16 streams (16 for tile halves, 8 for quarter items).
+template <int OUT, int HI = kHalfRows>
 __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, uint32_t lagw, bool lag,
                                            uint32_t (&P0)[kK][4], uint32_t (&P1)[kK][4], uint16_t*& oA,
                                            uint16_t*& oB, size_t pitch, bool st, uint32_t& acc, uint32_t& acc_edge) {
   using C = Cell<16>;
-  constexpr int kB = kHalfRows * kTileRowBytes;  // the lower half streams 16 rows further down
+  constexpr int kB = HI * kTileRowBytes;  // the hi stream runs HI rows further down
   auto words = [](uint2 a, uint2 b, uint32_t (&x)[4]) {
     x[0] = __byte_perm(a.x, b.x, 0x5410);
     x[1] = __byte_perm(a.x, b.x, 0x7632);
@@ -708,6 +715,80 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
   return acc;
 }
 
+// ---- light blocks: quarter items (two warps per tile) ---------------------
+//
+// When a block has fewer tiles than half the warp slots it is bound by one
+// item's latency, not by throughput.  Each tile then runs as two items of 16
+// rows (half = 0: rows 0-15, 1: rows 16-31), whose u16 streams carry 8 rows
+// each: 8 + 2K = 24 steps instead of 32.  Both items of a tile do the tile's
+// bookkeeping (state, pushes: idempotent), each with the edge regions it
+// holds.  Staged rows: the 32 rows -8 .. 23 around the item (8 KB).
+constexpr int kQuarterRows = kHalfRows / 2;             // rows per u16 stream
+constexpr int kQuarterSteps = kQuarterRows + 2 * kK;    // 24
+constexpr int kQuarterStage = kHalfRows + 2 * kK;       // 32 rows staged
+static_assert(kQuarterRows == kK, "quarter phase layout assumes 8-row streams with K = 8");
+
+__device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta,
+                                                   uint32_t b, uint32_t c, uint32_t half, const uint32_t (&lw)[3],
+                                                   uint32_t homes, uint32_t* edge, uint8_t* buf) {
+  const int lane = threadIdx.x & 31;
+  const size_t pitch = g.pitch;
+  const uint32_t r0 = half * kHalfRows;  // first tile row of the item
+  __syncwarp();  // every lane is done reading the previous item's rows
+  {
+    const uint32_t ch = __shfl_sync(0xffffffffu, homes, (2 * lane) & 31);
+    const uint32_t col = b * kTileCols + (lane & 15) * 8;
+    const uint16_t* base[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      base[r] = f0 + (((ch >> r) & 1u) ? delta : 0) + ((size_t)c * kTileRows + r0) * pitch + col;
+    uint8_t* dst = buf + (lane & 15) * 16;
+#pragma unroll
+    for (int k = 0; k < kQuarterStage / 2; ++k) {
+      const int row = 2 * k + (lane >> 4);  // staged row = item row + kK
+      const int trow = (int)r0 + row - kK;  // tile row
+      const int reg = trow < 0 ? 0 : (trow < kTileRows ? 1 : 2);
+      cp_async16(dst + row * kTileRowBytes, base[reg] + (size_t)row * pitch);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  uint32_t P0[kK][4], P1[kK][4];
+#pragma unroll
+  for (int j = 0; j < kK; ++j)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) P0[j][w] = P1[j][w] = 0u;
+  uint32_t acc = 0xFFFFFFFFu, accE = 0xFFFFFFFFu;
+  const ptrdiff_t od = ((homes >> 6) & 1u) ? delta : 0;
+  uint16_t* oA = f0 + od + ((size_t)c * kTileRows + r0 + kK) * pitch + b * kTileCols + lane * kTileWPL;
+  uint16_t* oB = oA + (size_t)kQuarterRows * pitch;
+  const bool st = lane >= kK / kTileWPL && lane < 32 - kK / kTileWPL;
+  const uint8_t* rb = buf + lane * 8;
+  // phase lags: [0,8) lo reads rows r0-8.. (above the tile for half 0), hi rows r0..; [8,16) own;
+  // [16,24) hi reads rows r0+16.. (below the tile for half 1)
+  const uint32_t lag0 = (half ? lw[1] : lw[0]) | lw[1] << 16, lag1 = lw[1] | lw[1] << 16,
+                 lag2 = lw[1] | (half ? lw[2] : lw[1]) << 16;
+  const bool l0 = __any_sync(0xffffffffu, lag0 != 0u), l1 = __any_sync(0xffffffffu, lag1 != 0u),
+             l2 = __any_sync(0xffffffffu, lag2 != 0u);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  tile_phase<kOutNone, kQuarterRows>(rb, 0, kK, lag0, l0, P0, P1, oA, oB, pitch, st, acc, accE);
+  tile_phase<kOutNone, kQuarterRows>(rb, kK, 2 * kK, lag1, l1, P0, P1, oA, oB, pitch, st, acc, accE);
+  tile_phase<kOutTop, kQuarterRows>(rb, 2 * kK, kQuarterSteps, lag2, l2, P0, P1, oA, oB, pitch, st, acc, accE);
+  if (!st) acc = accE = 0xFFFFFFFFu;  // halo lanes hold no output
+  edge[0] = edge[1] = accE;  // every output row of a quarter stream is within kK of its item's edge
+  return acc;
+}
+
+// Quarter items next to a source: the general path on two 8-row streams (rows r0.. and r0+8..).
+__device__ __noinline__ uint32_t tile_item16_sources8(const Geo& g, uint16_t* f0, const uint8_t* srcmask,
+                                                      const uint8_t* rf, uint32_t b, uint32_t r0, uint32_t lag0,
+                                                      uint32_t lag1, uint32_t lag2, ptrdiff_t delta, uint32_t homes,
+                                                      uint32_t* edge) {
+  return stream_item<16, false, true, kTileStages, kTileWPL, kTileWarpSmem>(
+      g, f0, f0, srcmask, rf, rf, b, r0, b, r0 + kQuarterRows, kQuarterRows, true, lag0, lag1, lag2, delta, homes,
+      edge);
+}
+
 // The rare items whose rows hold a source (the +1 path): kept out of line so
 // the hot loop of k_block_tiles stays small in the instruction cache.
 __device__ __noinline__ uint32_t tile_item16_sources(const Geo& g, uint16_t* f0, const uint8_t* srcmask,
@@ -816,6 +897,16 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     for (int k = 1; k < kHaloLanes; ++k) m = Cell<CB>::vmin(m, __shfl_sync(0xffffffffu, v, first + k));
     return m;
   };
+  // 9 region bits of the stream in half h (lo 0, hi 1) of a quarter item: every output row of the
+  // stream is within kK of both its top and bottom, so e serves both edges
+  auto regions16q = [&](uint32_t acc, uint32_t e, int h) -> uint32_t {
+    auto part = [h](uint32_t v) { return h ? v >> 16 : v & 0xFFFFu; };
+    const uint32_t a = __reduce_min_sync(0xffffffffu, part(acc)), ee = __reduce_min_sync(0xffffffffu, part(e));
+    const uint32_t l = part(lanes_min(acc, kL)), r = part(lanes_min(acc, kR));
+    const uint32_t el = part(lanes_min(e, kL)), er = part(lanes_min(e, kR));
+    return (a == 0u ? 1u : 0u) | (ee == 0u ? 6u : 0u) | (l == 0u ? 8u : 0u) | (r == 0u ? 16u : 0u) |
+           (el == 0u ? 0xA0u : 0u) | (er == 0u ? 0x140u : 0u);
+  };
   // items are fetched dynamically: a warp that finishes early takes the next one
   auto fetch = [&]() {
     uint32_t v = 0;
@@ -823,17 +914,25 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     return __shfl_sync(0xffffffffu, v, 0);
   };
   // (a static first item per warp packs light blocks onto few SMs: measured slower)
+  // light blocks (at most half a warp slot per tile): two quarter items per tile, shorter latency
+  const bool quarters = CB == 16 && AM_QUARTERS && 2u * n <= (uint32_t)AM_QUARTER_SLOTS * gridDim.x * (kBlockThreads / 32);
+  const uint32_t nitems = quarters ? 2u * n : n;
   uint32_t w = fetch();
-  while (w < n) {
-    const uint32_t it = list[w];
+  while (w < nitems) {
+    const uint32_t it = list[quarters ? w >> 1 : w];
+    const uint32_t half = quarters ? w & 1u : 0u;
     const uint32_t bA = it >> 16, cA = it & 0xFFFFu;
     const uint32_t tA = cA * g.tbands + bA;
     const uint8_t* rf = rowsrc + g.tile_rowsrc(bA);
     const uint32_t ra = cA * kTileRows;
     uint32_t f = 0;  // source rows in reach (loaded alongside the states)
     if constexpr (CB == 16) {
-      f = rf[ra + lane];
-      if (lane < kStageRows - 32) f |= rf[ra + 32 + lane];
+      if (quarters) {
+        f = rf[ra + half * kHalfRows + lane];  // the item's 32 staged rows
+      } else {
+        f = rf[ra + lane];
+        if (lane < kStageRows - 32) f |= rf[ra + 32 + lane];
+      }
     }
     const uint32_t sa = state_at_l0(tA);  // own state before the neighbours' (rewritten below)
     uint32_t lw[3], hm[3];
@@ -842,7 +941,25 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     const uint32_t out_home = (sa & 1u) ^ 1u;  // own rows go to the field that is not the tile's home
     uint32_t edge[2], acc;
     uint32_t m9;  // frontier regions (bits: any, top, bottom, left, right, tl, tr, bl, br)
-    if constexpr (CB == 16) {
+    if (CB == 16 && quarters) {
+      uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
+      const uint32_t r0 = ra + half * kHalfRows;
+      if (!__any_sync(0xffffffffu, f != 0u)) {
+        acc = tile_quarter16(g, reinterpret_cast<uint16_t*>(f0), delta, bA, cA, half, lw,
+                             hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6, edge, buf);
+      } else {  // a source in reach: the general path on the same two 8-row streams
+        const uint32_t up = half ? hm[1] : hm[0], dn = half ? hm[2] : hm[1];
+        const uint32_t homes = up | hm[1] << 1 | hm[1] << 2 | hm[1] << 3 | hm[1] << 4 | dn << 5 | out_home << 6 |
+                               out_home << 7;
+        acc = tile_item16_sources8(g, reinterpret_cast<uint16_t*>(f0), srcmask, rf, bA, r0, (half ? lw[1] : lw[0]) | lw[1] << 16,
+                                   lw[1] | lw[1] << 16, lw[1] | (half ? lw[2] : lw[1]) << 16, delta, homes, edge);
+      }
+      // regions: any / left / right from both streams; the top edge (tl, tr) is the lo stream of half 0,
+      // the bottom edge (bl, br) the hi stream of half 1
+      const uint32_t mlo = regions16q(acc, edge[0], 0), mhi = regions16q(acc, edge[0], 1);
+      m9 = ((mlo | mhi) & 0x19u) | (half == 0 ? (mlo & 0x62u) : 0u) | (half == 1 ? (mhi & 0x184u) : 0u);
+      gmin = min(gmin, min(__reduce_min_sync(0xffffffffu, acc & 0xFFFFu), __reduce_min_sync(0xffffffffu, acc >> 16)));
+    } else if constexpr (CB == 16) {
       // upper half (lo): tile rows 0-15, lower half (hi): rows 16-31
       uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
       const uint32_t homes16 = hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6;
