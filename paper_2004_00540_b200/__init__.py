@@ -447,15 +447,21 @@ class Batch:
         _check(lib().am_batch_download(self.ctx.handle, self.handle, _ptr(out)), self.ctx, "batch download")
         return out
 
-    def trace(self, targets, method=EUCLIDEAN, seed=0):
-        """targets: (k, 3) (maze, row, col) -> (offsets, points (maze-local), status)."""
+    def trace(self, targets, method=EUCLIDEAN, seed=0, out=None):
+        """targets: (k, 3) (maze, row, col) -> (offsets, points (maze-local), status).
+
+        out: optional preallocated (e.g. pinned) uint32 array of shape (>= total, 2) for the points."""
         t = np.ascontiguousarray(np.asarray(targets, np.uint32).reshape(-1, 3))
         off = np.zeros(len(t) + 1, np.uint64)
         st = np.zeros(len(t), np.int32)
         _check(lib().am_batch_path_counts(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
                                           _ptr(st)), self.ctx, "batch counts")
         total = int(off[-1])
-        pts = np.empty((max(total, 1), 2), np.uint32)
+        if out is not None and out.dtype == np.uint32 and out.ndim == 2 and out.shape[1] == 2 and \
+                out.shape[0] >= max(total, 1) and out.flags.c_contiguous:
+            pts = out
+        else:
+            pts = np.empty((max(total, 1), 2), np.uint32)
         _check(lib().am_batch_trace_paths(self.ctx.handle, self.handle, _ptr(t), len(t), method, seed, _ptr(off),
                                           _ptr(pts), total, _ptr(st)), self.ctx, "batch trace")
         return off, pts[:total], st

@@ -140,6 +140,11 @@ struct SlabRef {
   am_grid* g;
 };
 
+// am_trace_paths with an optional maze-local coordinate pass (cell_h/cell_w > 0, am_batch)
+am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
+                           const uint64_t* offsets, uint32_t* pts, uint64_t cap, int32_t* status, uint32_t cell_h,
+                           uint32_t cell_w);
+
 // The propagation driver (capi.cu): runs slabs in lock step, 1 slab = single grid.
 am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t layers, uint32_t auto_cap,
                             uint32_t mode, am_prop_result* res);

@@ -169,5 +169,9 @@ void launch_path_counts(const MapView& m, const uint32_t* tgt_rc, uint64_t n, in
 void launch_scan(const uint64_t* counts, uint64_t n, uint64_t* offsets, cudaStream_t s);
 void launch_trace(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int method, uint64_t seed,
                   const uint64_t* offsets, uint32_t* pts_rc, int32_t* status, cudaStream_t s);
+// paths in a grid of mazes packed on a cell_h x cell_w lattice -> each path's maze-local coordinates
+// (the maze is the one of the path's first point, its target)
+void launch_paths_local(uint32_t* pts_rc, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,
+                        uint32_t cell_w, cudaStream_t s);
 
 }  // namespace am

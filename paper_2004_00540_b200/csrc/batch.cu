@@ -293,18 +293,8 @@ am_status am_batch_trace_paths(am_ctx* ctx, am_batch* b, const uint32_t* tgt, ui
   std::vector<uint32_t> big;
   std::vector<uint8_t> bad;
   batch_targets(ctx, b, tgt, n, big, bad);
-  am_status st = am_trace_paths(ctx, b->grid, big.data(), n, method, seed, offsets, pts, cap, status);
-  if (st) return st;
-  for (uint64_t k = 0; k < n; ++k) {  // back to maze-local coordinates
-    if (status[k] != AM_OK) continue;
-    const uint32_t i = tgt[3 * k];
-    const uint32_t r0 = (i / b->tiles_x) * (b->mh + 1), c0 = (i % b->tiles_x) * (b->mw + 1);
-    for (uint64_t p = offsets[k]; p < offsets[k + 1]; ++p) {
-      pts[2 * p] -= r0;
-      pts[2 * p + 1] -= c0;
-    }
-  }
-  return AM_OK;
+  // maze-local coordinates are produced on the device (mazes sit on a (mh+1) x (mw+1) lattice)
+  return trace_paths_host(ctx, b->grid, big.data(), n, method, seed, offsets, pts, cap, status, b->mh + 1, b->mw + 1);
 }
 
 }  // extern "C"

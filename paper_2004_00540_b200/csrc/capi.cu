@@ -876,6 +876,17 @@ am_status am_path_counts(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t 
 
 am_status am_trace_paths(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
                          const uint64_t* offsets, uint32_t* pts, uint64_t cap, int32_t* status) {
+  return am::trace_paths_host(ctx, g, tgt, n, method, seed, offsets, pts, cap, status, 0, 0);
+}
+
+}  // extern "C"
+
+namespace am {
+// am_trace_paths; cell_h / cell_w > 0: the grid packs mazes on a (cell_h x cell_w) lattice
+// (am_batch) and every path is returned in its maze's local coordinates (device pass before the copy)
+am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
+                           const uint64_t* offsets, uint32_t* pts, uint64_t cap, int32_t* status, uint32_t cell_h,
+                           uint32_t cell_w) {
   if (!ctx || !g || !offsets || (n && (!tgt || !status))) return AM_EINVAL;
   if (!g->have_map) return am::fail(ctx, AM_EINVAL, "no activity map");
   if (g->slab) return am::fail(ctx, AM_EINVAL, "path extraction on a slab: gather the map first");
@@ -901,6 +912,10 @@ am_status am_trace_paths(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t 
   CK(cudaMemcpyAsync(g->d_status, status, n * 4, cudaMemcpyHostToDevice, s));
   am::launch_trace(view_of(g), g->d_tgt, n, (int)method, seed, g->d_offsets, g->d_pts, g->d_status, s);
   CKL();
+  if (cell_h) {
+    am::launch_paths_local(g->d_pts, g->d_offsets, g->d_status, n, cell_h, cell_w, s);
+    CKL();
+  }
   if (total) CK(cudaMemcpyAsync(pts, g->d_pts, total * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(status, g->d_status, n * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -917,6 +932,10 @@ am_status am_trace_paths(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t 
   }
   return AM_OK;
 }
+
+}  // namespace am
+
+extern "C" {
 
 am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, uint64_t n, uint32_t method,
                                 uint64_t seed, uint64_t* d_offsets, uint32_t* d_pts, uint64_t cap,

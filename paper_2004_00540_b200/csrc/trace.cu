@@ -308,6 +308,25 @@ void launch_path_counts(const MapView& m, const uint32_t* tgt, uint64_t n, int m
   k_path_counts<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, counts, status);
 }
 
+__global__ void k_paths_local(uint32_t* __restrict__ pts, const uint64_t* __restrict__ offsets,
+                              const int32_t* __restrict__ status, uint64_t n, uint32_t cell_h, uint32_t cell_w) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= n || status[w] != ST_OK) return;
+  const uint64_t b = offsets[w], e = offsets[w + 1];
+  if (b == e) return;
+  const uint32_t r0 = pts[2 * b] / cell_h * cell_h, c0 = pts[2 * b + 1] / cell_w * cell_w;
+  for (uint64_t p = b + (threadIdx.x & 31); p < e; p += 32) {
+    uint2 v = reinterpret_cast<const uint2*>(pts)[p];
+    reinterpret_cast<uint2*>(pts)[p] = make_uint2(v.x - r0, v.y - c0);
+  }
+}
+
+void launch_paths_local(uint32_t* pts, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,
+                        uint32_t cell_w, cudaStream_t s) {
+  if (!n) return;
+  k_paths_local<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(pts, offsets, status, n, cell_h, cell_w);
+}
+
 void launch_trace(const MapView& m, const uint32_t* tgt, uint64_t n, int method, uint64_t seed,
                   const uint64_t* offsets, uint32_t* pts, int32_t* status, cudaStream_t s) {
   if (!n) return;

