@@ -40,6 +40,8 @@ struct am_ctx {
   am::Comm* comm = nullptr;  // set by am_comm_init
   cudaMemPool_t pool = nullptr;  // every device buffer of the context's grids (am::dmalloc)
   std::vector<am::FlagSet*> flag_sets;  // recycled FlagSets of destroyed grids
+  cudaStream_t copy_stream = nullptr;   // map downloads: D2H copies overlapping the chunk decode
+  cudaEvent_t copy_ev[8] = {};
 };
 
 struct am_grid {

@@ -73,6 +73,9 @@ void am_ctx_destroy(am_ctx* ctx) {
     cudaEventDestroy(t.b);
   }
   for (auto* f : ctx->flag_sets) flag_set_free(f);
+  for (auto& e : ctx->copy_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);  // deferred by the driver while grids still hold memory
   delete ctx;
@@ -746,21 +749,31 @@ static am_status download_impl(am_ctx* ctx, am_grid* g, uint32_t* dst, bool dst_
     CK(cudaStreamSynchronize(s));
     return AM_OK;
   }
-  // decode into the idle ping-pong buffer in row chunks, copy out chunk by chunk
+  // decode into the idle ping-pong buffer in row chunks (ctx stream) while the previous chunk is
+  // copied out on the copy stream: the PCIe copy is the floor, the decode hides behind it
   uint32_t* stage = (uint32_t*)g->val[g->cur ^ 1];
   g->dirty[g->cur ^ 1] = 1;
   const size_t stage_bytes = (size_t)g->g.rows * g->g.pitch * (g->cell_bits / 8);
-  size_t rows_per = stage_bytes / (W * 4 * 2);
+  constexpr int kChunks = 4;  // stage buffers in flight
+  size_t rows_per = std::min(stage_bytes / (W * 4 * kChunks), std::max<size_t>(1, (256u << 20) / (W * 4)));
   if (rows_per < 1) rows_per = 1;
-  uint32_t* bufs[2] = {stage, stage + rows_per * W};
+  if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : ctx->copy_ev)
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   int k = 0;
-  for (size_t r0 = 0; r0 < H; r0 += rows_per, k ^= 1) {
+  for (size_t r0 = 0; r0 < H; r0 += rows_per, k = (k + 1) % kChunks) {
     const size_t r1 = std::min(H, r0 + rows_per);
-    am::launch_decode(g->g, g->cell_bits, g->val[g->cur], rollback, (uint32_t)r0, (uint32_t)r1, bufs[k], s);
+    uint32_t* buf = stage + (size_t)k * rows_per * W;
+    if (r0 >= kChunks * rows_per) CK(cudaStreamWaitEvent(s, ctx->copy_ev[2 * k + 1], 0));  // buffer copied out
+    am::launch_decode(g->g, g->cell_bits, g->val[g->cur], rollback, (uint32_t)r0, (uint32_t)r1, buf, s);
     CKL();
-    CK(cudaMemcpyAsync(dst + r0 * W, bufs[k], (r1 - r0) * W * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ctx->copy_ev[2 * k], s));
+    CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[2 * k], 0));
+    CK(cudaMemcpyAsync(dst + r0 * W, buf, (r1 - r0) * W * 4, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->copy_ev[2 * k + 1], ctx->copy_stream));
   }
-  CK(cudaStreamSynchronize(s));
+  CK(cudaStreamSynchronize(ctx->copy_stream));
+  CK(cudaStreamWaitEvent(s, ctx->copy_ev[2 * ((k + kChunks - 1) % kChunks) + 1], 0));  // later decodes order after
   return AM_OK;
 }
 
