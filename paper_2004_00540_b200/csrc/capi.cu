@@ -2,8 +2,9 @@
 //
 // propagate_auto on the device (propagate.hpp:57-61, pin P3): temporally
 // blocked launches of kK layers each, with the fixed-point signal of block b
-// read back (pinned copy + event) only after block b+1 is already queued, so
-// the GPU never idles on the host.  Coverage growth is monotone
+// read back (a device-mapped pinned slot the kernels write, or a copy +
+// event for slab groups) only blocks after b+1 is queued, so the GPU never
+// idles on the host.  Coverage growth is monotone
 // (new cells at layer l imply new cells at layer l-1), so one number per
 // block -- the smallest activity among covered cells -- locates the first
 // layer without new cells exactly; blocks launched past it are undone by

@@ -1,10 +1,13 @@
 // stencil.cu -- sm_100a kernels for the oMAP layer stack (propagate.hpp:34-68).
 //
-// K1+K2: k_block streams one band of 32*kWPL cells down a row segment and
-// runs kK pool+add+ReLU layers per HBM round trip entirely in registers
-// (per-layer 3-row window, warp-shuffle horizontal halo), then writes the
-// useful middle of the band and folds the fixed-point signal (min over
-// covered cells of a-1) into one atomicMin per warp.  See DESIGN.md §4.
+// K1+K2: a warp streams a band of cells down a run of rows and applies kK
+// pool+add+ReLU layers per HBM round trip entirely in registers (per-layer
+// 3-row window, warp-shuffle horizontal halo), writes the useful middle of
+// the band and folds the fixed-point signal (min over covered cells of a-1)
+// into one atomicMin per warp.  k_block sweeps every band of the grid (dense
+// mode, 240-column bands); k_block_tiles runs only the active 32x112 tiles
+// (exact skipping: quiet tiles advance lazily through a per-tile lag) and
+// lists the next block's tiles itself.  See DESIGN.md §4.
 #include <cstdio>
 
 #include "am_internal.cuh"
@@ -308,32 +311,10 @@ __device__ __forceinline__ void stream_step(uint32_t (&x)[WPL], uint32_t (&P0)[k
   (void)lane;
 }
 
-// ---- TMA bulk-copy staging (cp.async.bulk + mbarrier), one ring per warp ----
+// ---- cp.async staging (per-lane 16 / 8 B pieces into shared memory) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
