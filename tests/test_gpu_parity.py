@@ -25,7 +25,9 @@ def test_spec_kat_on_device(impl, kat):
 
 
 SHAPES = [(1, 1), (1, 300), (300, 1), (7, 5), (37, 1000), (1000, 37), (241, 239), (255, 257), (513, 130),
-          (129, 700), (2000, 64)]
+          (129, 700), (2000, 64),
+          # active-tile geometry edges: 112-column tile bands, 32-row chunks
+          (112, 32), (113, 33), (224, 31), (225, 64), (336, 65), (111, 96)]
 
 
 @pytest.mark.parametrize("w,h", SHAPES)
