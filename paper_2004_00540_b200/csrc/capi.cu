@@ -914,7 +914,16 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   am_status st = ensure_targets(ctx, g, n);
   if (st) return st;
   cudaStream_t s = ctx->stream;
-  if (total > g->pts_cap) {
+  // A pinned (device-mapped) destination takes the points straight from the walkers: the 32-point
+  // warp stores cross PCIe while the walk runs instead of a separate copy afterwards.
+  uint32_t* direct = nullptr;
+  if (!cell_h && total) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, pts) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+      direct = static_cast<uint32_t*>(at.devicePointer);
+    (void)cudaGetLastError();
+  }
+  if (!direct && total > g->pts_cap) {
     am::dfree(ctx, g->d_pts);
     g->d_pts = nullptr;
     g->pts_cap = 0;
@@ -924,13 +933,14 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->d_offsets, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->d_status, status, n * 4, cudaMemcpyHostToDevice, s));
-  am::launch_trace(view_of(g), g->d_tgt, n, (int)method, seed, g->d_offsets, g->d_pts, g->d_status, s);
+  am::launch_trace(view_of(g), g->d_tgt, n, (int)method, seed, g->d_offsets, direct ? direct : g->d_pts,
+                   g->d_status, s);
   CKL();
   if (cell_h) {
     am::launch_paths_local(g->d_pts, g->d_offsets, g->d_status, n, cell_h, cell_w, s);
     CKL();
   }
-  if (total) CK(cudaMemcpyAsync(pts, g->d_pts, total * 8, cudaMemcpyDeviceToHost, s));
+  if (total && !direct) CK(cudaMemcpyAsync(pts, g->d_pts, total * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(status, g->d_status, n * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (g->plain_active && method == AM_METHOD_EUCLIDEAN) {
