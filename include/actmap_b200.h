@@ -197,6 +197,50 @@ am_status am_batch_trace_paths(am_ctx *ctx, am_batch *batch, const uint32_t *tgt
                                uint64_t seed, const uint64_t *offsets, uint32_t *pts_rc, uint64_t pts_capacity,
                                int32_t *status);
 
+/* ---- map / scene text I/O (mapio.hpp:19-38) ------------
+ * The text goes to the device once; newline scan, row validation,
+ * character classes and the source / target lists are computed there (the
+ * occupancy never exists on the host unless downloaded).  Parse failures
+ * return AM_EINVAL and fill am_parse_info: error_line / error_column
+ * (1-based, 0 when the error has no position) map to actmap::ParseError,
+ * otherwise to InvalidInputError (errors.hpp:23-38). */
+enum { AM_FORMAT_MOVINGAI = 0, AM_FORMAT_ASCII_SCENE = 1 };
+typedef struct am_parse_info {
+  uint32_t width, height;
+  uint64_t n_sources, n_targets, obstacles;
+  uint64_t error_line, error_column;
+  char error[160];
+} am_parse_info;
+typedef struct am_scene am_scene;
+/* Moving AI header only (host, no device): width/height and the byte offset
+ * of the first map row.  parse_movingai's header rules (mapio.hpp:19-22). */
+am_status am_movingai_header(const char *text, uint64_t len, am_parse_info *info, uint64_t *body_offset);
+/* parse_movingai (mapio.hpp:23) / parse_ascii_scene (mapio.hpp:30) into a
+ * device-resident scene: occupancy, and for ASCII scenes the 'S' sources and
+ * 'T' targets in row-major order. */
+am_status am_scene_parse(am_ctx *ctx, const char *text, uint64_t len, uint32_t format, am_scene **out,
+                         am_parse_info *info);
+am_status am_scene_destroy(am_ctx *ctx, am_scene *scene);
+/* any pointer may be NULL; sizes: W*H bytes and 2*n u32 (see am_parse_info) */
+am_status am_scene_download(am_ctx *ctx, const am_scene *scene, uint8_t *occupancy, uint32_t *src_rc,
+                            uint32_t *tgt_rc);
+/* build_grid + SourceSet straight from a parsed scene (no host occupancy);
+ * src_rc NULL = the scene's own sources, else n_src host (row, col) pairs
+ * (sources given by the caller override the file). */
+am_status am_grid_create_scene(am_ctx *ctx, const am_scene *scene, const uint32_t *src_rc, uint64_t n_src,
+                               am_grid **out);
+/* emit_movingai (mapio.hpp:26) / emit_ascii_scene (mapio.hpp:32): the text of
+ * a grid ('.'/'@' or '.'/'#' plus 'S'/'T').  out NULL: *length only. */
+am_status am_emit_text(am_ctx *ctx, uint32_t format, uint32_t width, uint32_t height, const uint8_t *occupancy,
+                       const uint32_t *src_rc, uint64_t n_src, const uint32_t *tgt_rc, uint64_t n_tgt, char *out,
+                       uint64_t capacity, uint64_t *length);
+/* export_pgm (mapio.hpp:35-38): binary P5 of the grid's map (device-resident)
+ * or of a host map; maxval 255, or 65535 when the maximum exceeds 255.  out
+ * NULL: *length only. */
+am_status am_activity_export_pgm(am_ctx *ctx, am_grid *grid, uint8_t *out, uint64_t capacity, uint64_t *length);
+am_status am_export_pgm(am_ctx *ctx, uint32_t width, uint32_t height, const uint32_t *values, uint8_t *out,
+                        uint64_t capacity, uint64_t *length);
+
 /* ---- host helpers of the planner API (no device work) ------------------ */
 /* random_maze / comb_maze (grid.hpp:65-76) into a caller buffer of W*H bytes. */
 am_status am_random_maze(uint32_t width, uint32_t height, double density, uint64_t seed, uint8_t *occupancy);

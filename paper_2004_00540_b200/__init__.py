@@ -25,6 +25,7 @@ FILLED, STALLED, CAP, FIXED = 0, 1, 2, 3          # AutoStop (propagate.hpp:45-4
 BATCHED, ITERATIVE = 0, 1                          # Mode (propagate.hpp:22)
 SIMPLE, EUCLIDEAN = 0, 1                           # Method (report.hpp:15)
 STRICT, PERMISSIVE = 0, 1                          # CornerRule (reconstruct.hpp:14)
+MOVINGAI, ASCII_SCENE = 0, 1                      # text formats (mapio.hpp:19-33)
 CTX_TIMING = 1
 CTX_DENSE = 2
 K_MAX_LAYERS = 2147483646                          # propagate.hpp:15-16
@@ -43,6 +44,15 @@ class UncoveredTargetError(Error):
     """actmap::UncoveredTargetError (errors.hpp:41)."""
 
 
+class ParseError(InvalidInputError):
+    """actmap::ParseError (errors.hpp:23-38): malformed map / scene text, 1-based position."""
+
+    def __init__(self, msg: str, line: int, column: int):
+        super().__init__(f"{msg} (line {line}, column {column})")
+        self.line = line
+        self.column = column
+
+
 class _PropResult(C.Structure):
     _fields_ = [("layers_used", C.c_uint32), ("cause", C.c_uint32), ("layers_computed", C.c_uint32),
                 ("cell_bits", C.c_uint32), ("block_launches", C.c_uint64), ("layer_launches", C.c_uint64),
@@ -57,6 +67,12 @@ class _GridInfo(C.Structure):
 
 class _CtxOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("flags", C.c_uint32)]
+
+
+class _ParseInfo(C.Structure):
+    _fields_ = [("width", C.c_uint32), ("height", C.c_uint32), ("n_sources", C.c_uint64),
+                ("n_targets", C.c_uint64), ("obstacles", C.c_uint64), ("error_line", C.c_uint64),
+                ("error_column", C.c_uint64), ("error", C.c_char * 160)]
 
 
 class _Stats(C.Structure):
@@ -112,6 +128,14 @@ def lib():
             "am_batch_download": (st, [_vp, _vp, _vp]),
             "am_batch_path_counts": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp]),
             "am_batch_trace_paths": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
+            "am_movingai_header": (st, [C.c_char_p, u64, C.POINTER(_ParseInfo), _u64p]),
+            "am_scene_parse": (st, [_vp, C.c_char_p, u64, u32, C.POINTER(_vp), C.POINTER(_ParseInfo)]),
+            "am_scene_destroy": (st, [_vp, _vp]),
+            "am_scene_download": (st, [_vp, _vp, _vp, _vp, _vp]),
+            "am_grid_create_scene": (st, [_vp, _vp, _vp, u64, C.POINTER(_vp)]),
+            "am_emit_text": (st, [_vp, u32, u32, u32, _vp, _vp, u64, _vp, u64, _vp, u64, _u64p]),
+            "am_activity_export_pgm": (st, [_vp, _vp, _vp, u64, _u64p]),
+            "am_export_pgm": (st, [_vp, u32, u32, _vp, _vp, u64, _u64p]),
             "am_random_maze": (st, [u32, u32, C.c_double, u64, _vp]),
             "am_comb_maze": (st, [u32, u32, _vp]),
             "am_kruskal_maze": (st, [u32, u32, u64, _vp]),
@@ -399,6 +423,15 @@ class Grid:
             out.append((OK, p[keep]))
         return out
 
+    def export_pgm(self) -> bytes:
+        """export_pgm (mapio.hpp:35-38) of this grid's map, rescaled on the device."""
+        n = C.c_uint64(0)
+        _check(lib().am_activity_export_pgm(self.ctx.handle, self.handle, None, 0, C.byref(n)), self.ctx, "pgm")
+        buf = np.empty(n.value, dtype=np.uint8)
+        _check(lib().am_activity_export_pgm(self.ctx.handle, self.handle, _ptr(buf), n.value, C.byref(n)), self.ctx,
+               "pgm")
+        return buf.tobytes()
+
 
 class Batch:
     """Many independent small mazes solved in one device run (config C5)."""
@@ -602,6 +635,143 @@ def path_metrics(points):
     s, length = C.c_uint64(0), C.c_double(0.0)
     _check(lib().am_path_metrics(_ptr(p), len(p), C.byref(s), C.byref(length)), None, "path_metrics")
     return s.value, length.value
+
+
+# ---------------------------------------------------------------- map / scene text (mapio.hpp)
+def _text(text) -> bytes:
+    return text.encode() if isinstance(text, str) else bytes(text)
+
+
+def _parse_fail(st, info: _ParseInfo, ctx):
+    msg = info.error.decode(errors="replace")
+    if st == EINVAL and info.error_line:
+        raise ParseError(msg, int(info.error_line), int(info.error_column))
+    if st == EINVAL and msg:
+        raise InvalidInputError(msg)
+    _raise(st, ctx, "parse")
+
+
+class Scene:
+    """A parsed map / scene resident on the device (am_scene): occupancy plus, for
+    ASCII scenes, the 'S' sources and 'T' targets (mapio.hpp:13-17)."""
+
+    def __init__(self, text, fmt: int = ASCII_SCENE, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        t = _text(text)
+        info = _ParseInfo()
+        h = C.c_void_p()
+        st = lib().am_scene_parse(self.ctx.handle, t, len(t), fmt, C.byref(h), C.byref(info))
+        if st != OK:
+            _parse_fail(st, info, self.ctx)
+        self.handle = h
+        self.ctx._own(self)
+        self.width, self.height = info.width, info.height
+        self.n_sources, self.n_targets, self.obstacles = info.n_sources, info.n_targets, info.obstacles
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().am_scene_destroy(self.ctx.handle, self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def download(self):
+        """(occupancy (H, W) uint8, sources (n, 2) uint32, targets (m, 2) uint32), row-major order."""
+        occ = np.empty((self.height, self.width), dtype=np.uint8)
+        src = np.empty((self.n_sources, 2), dtype=np.uint32)
+        tgt = np.empty((self.n_targets, 2), dtype=np.uint32)
+        _check(lib().am_scene_download(self.ctx.handle, self.handle, _ptr(occ), _ptr(src), _ptr(tgt)), self.ctx,
+               "scene download")
+        return occ, src, tgt
+
+    def grid(self, sources=None) -> Grid:
+        """Grid straight from the device-resident scene; sources override the file's 'S' cells."""
+        g = Grid.__new__(Grid)
+        g.ctx = self.ctx
+        g.occ = None
+        g.width, g.height = self.width, self.height
+        h = C.c_void_p()
+        if sources is None:
+            st = lib().am_grid_create_scene(self.ctx.handle, self.handle, None, 0, C.byref(h))
+        else:
+            src = _rc(sources)
+            st = lib().am_grid_create_scene(self.ctx.handle, self.handle, _ptr(src), len(src), C.byref(h))
+        _check(st, self.ctx, "SourceSet/grid")
+        g.handle = h
+        self.ctx._own(g)
+        g.layers = 0
+        return g
+
+
+def movingai_header(text):
+    """Host-side Moving AI header check: (width, height, body offset) or ParseError."""
+    t = _text(text)
+    info = _ParseInfo()
+    off = C.c_uint64(0)
+    st = lib().am_movingai_header(t, len(t), C.byref(info), C.byref(off))
+    if st != OK:
+        _parse_fail(st, info, None)
+    return info.width, info.height, off.value
+
+
+def parse_movingai(text, ctx: Context | None = None) -> np.ndarray:
+    """parse_movingai (mapio.hpp:23): the occupancy grid (nonzero = obstacle)."""
+    sc = Scene(text, MOVINGAI, ctx)
+    try:
+        return sc.download()[0]
+    finally:
+        sc.close()
+
+
+def parse_ascii_scene(text, ctx: Context | None = None):
+    """parse_ascii_scene (mapio.hpp:30): (occupancy, sources, targets)."""
+    sc = Scene(text, ASCII_SCENE, ctx)
+    try:
+        return sc.download()
+    finally:
+        sc.close()
+
+
+def _emit(fmt, occupancy, sources, targets, ctx):
+    ctx = ctx or default_context()
+    occ = _occ(occupancy)
+    h, w = occ.shape
+    src = _rc(sources if sources is not None else np.zeros((0, 2)))
+    tgt = _rc(targets if targets is not None else np.zeros((0, 2)))
+    n = C.c_uint64(0)
+    args = (ctx.handle, fmt, w, h, _ptr(occ), _ptr(src), len(src), _ptr(tgt), len(tgt))
+    _check(lib().am_emit_text(*args, None, 0, C.byref(n)), ctx, "emit")
+    buf = np.empty(n.value, dtype=np.uint8)
+    _check(lib().am_emit_text(*args, _ptr(buf), n.value, C.byref(n)), ctx, "emit")
+    return buf.tobytes()
+
+
+def emit_movingai(occupancy, ctx: Context | None = None) -> bytes:
+    """emit_movingai (mapio.hpp:26): canonical `.` / `@` text."""
+    return _emit(MOVINGAI, occupancy, None, None, ctx)
+
+
+def emit_ascii_scene(occupancy, sources, targets=(), ctx: Context | None = None) -> bytes:
+    """emit_ascii_scene (mapio.hpp:32)."""
+    return _emit(ASCII_SCENE, occupancy, sources, targets, ctx)
+
+
+def export_pgm(values, ctx: Context | None = None) -> bytes:
+    """export_pgm (mapio.hpp:35-38) of a host map (H, W) uint32."""
+    ctx = ctx or default_context()
+    v = np.ascontiguousarray(values, dtype=np.uint32)
+    if v.ndim != 2:
+        raise InvalidInputError("activity map must be a 2-D (height, width) array")
+    h, w = v.shape
+    n = C.c_uint64(0)
+    _check(lib().am_export_pgm(ctx.handle, w, h, _ptr(v), None, 0, C.byref(n)), ctx, "pgm")
+    buf = np.empty(n.value, dtype=np.uint8)
+    _check(lib().am_export_pgm(ctx.handle, w, h, _ptr(v), _ptr(buf), n.value, C.byref(n)), ctx, "pgm")
+    return buf.tobytes()
 
 
 def random_maze(width: int, height: int, density: float, seed: int) -> np.ndarray:

@@ -13,6 +13,7 @@
 
 #include "actmap/b200.hpp"
 #include "actmap/errors.hpp"
+#include "actmap/mapio.hpp"
 #include "actmap/propagate.hpp"
 #include "actmap/reconstruct.hpp"
 #include "actmap_b200.h"
@@ -560,6 +561,105 @@ std::vector<PlannedPath> Planner::reconstruct_all(std::span<const Coord> targets
 }
 
 }  // namespace b200
+
+// ---------------------------------------------------------------- map / scene text (mapio.hpp)
+
+namespace {
+
+// device parse of `text`; the scene handle is released on every path
+struct ParsedScene {
+  am_ctx* ctx = nullptr;
+  am_scene* sc = nullptr;
+  am_parse_info info{};
+  ~ParsedScene() {
+    if (sc) am_scene_destroy(ctx, sc);
+  }
+};
+
+void parse_text(std::string_view text, uint32_t format, ParsedScene& ps) {
+  ps.ctx = default_ctx();
+  const am_status st = am_scene_parse(ps.ctx, text.data(), text.size(), format, &ps.sc, &ps.info);
+  if (st == AM_OK) return;
+  if (st == AM_EINVAL && ps.info.error_line)
+    throw ParseError(ps.info.error, ps.info.error_line, ps.info.error_column);
+  if (st == AM_EINVAL && ps.info.error[0]) throw InvalidInputError(ps.info.error);
+  throw_status(st, ps.ctx, "parse");
+}
+
+std::string emit_text(uint32_t format, const GridMap& grid, const std::vector<uint32_t>& src,
+                      const std::vector<uint32_t>& tgt) {
+  am_ctx* ctx = default_ctx();
+  uint64_t n = 0;
+  const auto occ = grid.occupancy();
+  check(am_emit_text(ctx, format, grid.width(), grid.height(), occ.data(), src.data(), src.size() / 2, tgt.data(),
+                     tgt.size() / 2, nullptr, 0, &n),
+        ctx, "emit");
+  std::string out(n, '\0');
+  check(am_emit_text(ctx, format, grid.width(), grid.height(), occ.data(), src.data(), src.size() / 2, tgt.data(),
+                     tgt.size() / 2, out.data(), n, &n),
+        ctx, "emit");
+  return out;
+}
+
+}  // namespace
+
+GridMap parse_movingai(std::string_view text) {
+  std::lock_guard<std::mutex> lk(api_mutex());
+  ParsedScene ps;
+  parse_text(text, AM_FORMAT_MOVINGAI, ps);
+  std::vector<uint8_t> occ(static_cast<size_t>(ps.info.width) * ps.info.height);
+  check(am_scene_download(ps.ctx, ps.sc, occ.data(), nullptr, nullptr), ps.ctx, "scene download");
+  return GridMap(ps.info.width, ps.info.height, std::move(occ));
+}
+
+std::string emit_movingai(const GridMap& grid) {
+  std::lock_guard<std::mutex> lk(api_mutex());
+  return emit_text(AM_FORMAT_MOVINGAI, grid, {}, {});
+}
+
+Scene parse_ascii_scene(std::string_view text) {
+  std::unique_lock<std::mutex> lk(api_mutex());
+  ParsedScene ps;
+  parse_text(text, AM_FORMAT_ASCII_SCENE, ps);
+  std::vector<uint8_t> occ(static_cast<size_t>(ps.info.width) * ps.info.height);
+  std::vector<uint32_t> src(2 * ps.info.n_sources), tgt(2 * ps.info.n_targets);
+  check(am_scene_download(ps.ctx, ps.sc, occ.data(), src.data(), tgt.data()), ps.ctx, "scene download");
+  lk.unlock();
+  std::vector<Coord> s(ps.info.n_sources), t(ps.info.n_targets);
+  for (size_t i = 0; i < s.size(); ++i) s[i] = Coord{src[2 * i], src[2 * i + 1]};
+  for (size_t i = 0; i < t.size(); ++i) t[i] = Coord{tgt[2 * i], tgt[2 * i + 1]};
+  GridMap g(ps.info.width, ps.info.height, std::move(occ));
+  SourceSet set(g, s);
+  return Scene{std::move(g), std::move(set), std::move(t)};
+}
+
+std::string emit_ascii_scene(const Scene& scene) {
+  std::lock_guard<std::mutex> lk(api_mutex());
+  return emit_text(AM_FORMAT_ASCII_SCENE, scene.grid, flatten(scene.sources.coords()), flatten(scene.targets));
+}
+
+std::string export_pgm(const ActivityMap& activity) {
+  const auto& dev = activity.device_map();
+  if (dev) {
+    std::lock_guard<std::mutex> lk(api_mutex());
+    uint64_t n = 0;
+    check(am_activity_export_pgm(dev->ctx, dev->grid, nullptr, 0, &n), dev->ctx, "export_pgm");
+    std::string out(n, '\0');
+    check(am_activity_export_pgm(dev->ctx, dev->grid, reinterpret_cast<uint8_t*>(out.data()), n, &n), dev->ctx,
+          "export_pgm");
+    return out;
+  }
+  const auto vals = activity.values();
+  std::lock_guard<std::mutex> lk(api_mutex());
+  am_ctx* ctx = default_ctx();
+  uint64_t n = 0;
+  check(am_export_pgm(ctx, activity.width(), activity.height(), vals.data(), nullptr, 0, &n), ctx, "export_pgm");
+  std::string out(n, '\0');
+  check(am_export_pgm(ctx, activity.width(), activity.height(), vals.data(), reinterpret_cast<uint8_t*>(out.data()), n,
+                      &n),
+        ctx, "export_pgm");
+  return out;
+}
 
 }  // namespace actmap
 

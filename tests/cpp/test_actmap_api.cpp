@@ -8,6 +8,7 @@
 
 #include "actmap/b200.hpp"
 #include "actmap/errors.hpp"
+#include "actmap/mapio.hpp"
 #include "actmap/propagate.hpp"
 #include "actmap/reconstruct.hpp"
 
@@ -124,6 +125,48 @@ int main() {
       ++ok;
     }
     CHECK(ok > 10);
+  }
+  // map / scene text (mapio.hpp)
+  {
+    const GridMap g = parse_movingai("type octile\nheight 2\nwidth 2\nmap\n.@\n@.\n");
+    CHECK(g.width() == 2 && g.height() == 2 && g.is_obstacle({0, 1}) && g.is_obstacle({1, 0}) && g.is_free({0, 0}));
+    CHECK(emit_movingai(g) == "type octile\nheight 2\nwidth 2\nmap\n.@\n@.\n");
+    bool pos = false;
+    try {
+      parse_movingai("type octile\nheight 3\nwidth 2\nmap\n..\n..\n");
+    } catch (const ParseError& e) {
+      pos = e.line() == 7 && e.column() == 1;
+    }
+    CHECK(pos);
+    pos = false;
+    try {
+      parse_movingai("type octile\nheight 2\nwidth 2\nmap\n.@\n@x\n");
+    } catch (const ParseError& e) {
+      pos = e.line() == 6 && e.column() == 2;
+    }
+    CHECK(pos);
+    const Scene sc = parse_ascii_scene("S.\n.T\n");
+    CHECK(sc.grid.width() == 2 && sc.sources.size() == 1 && sc.sources.coords()[0] == (Coord{0, 0}));
+    CHECK(sc.targets.size() == 1 && sc.targets[0] == (Coord{1, 1}));
+    CHECK(emit_ascii_scene(sc) == "S.\n.T\n");
+    const Scene dis = parse_ascii_scene("S#\n#T");
+    CHECK(throws<UncoveredTargetError>([&] {
+      reconstruct_euclidean(propagate(dis.grid, dis.sources, 4), dis.grid, dis.sources, dis.targets[0]);
+    }));
+    CHECK(throws<ParseError>([&] { parse_ascii_scene("S.\n.T.\n"); }));
+    CHECK(throws<InvalidInputError>([&] { parse_ascii_scene("..\n.T\n"); }));
+    const std::string p1 = export_pgm(ActivityMap(1, 1, std::vector<uint32_t>{2}, 1));
+    CHECK(p1 == std::string("P5\n1 1\n255\n\xff", 13));
+    const std::string p0 = export_pgm(ActivityMap(2, 1, std::vector<uint32_t>{0, 0}, 1));
+    CHECK(p0 == std::string("P5\n2 1\n255\n\0\0", 13));
+    // device-resident map: same bytes as the host-map path
+    const GridMap e = build_grid(9, 9, {});
+    const std::vector<Coord> cs{{4, 4}};
+    const SourceSet src(e, cs);
+    const ActivityMap m = propagate(e, src, 300);
+    const ActivityMap host(9, 9, std::vector<uint32_t>(m.values().begin(), m.values().end()), 300);
+    const std::string pd = export_pgm(m), ph = export_pgm(host);
+    CHECK(pd == ph && pd.size() == std::string("P5\n9 9\n65535\n").size() + 162);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
