@@ -6,11 +6,11 @@ on the device (paper_2004_00540_b200/csrc/mapio.cu) and never calls it.
 Follows /root/reference/proj/core/include/actmap/mapio.hpp:12-38 and the
 mapio module of /root/reference/SPEC.md:323-390, plus the pins the reference
 leaves open:
-  P10 line ends '\\n' or '\\r\\n'; final newline optional; trailing empty lines
+  P11 line ends '\\n' or '\\r\\n'; final newline optional; trailing empty lines
       ignored; a '\\r' anywhere else is an unknown byte.
-  P11 Moving AI header: `type octile`, `height H`, `width W`, `map` in this
+  P12 Moving AI header: `type octile`, `height H`, `width W`, `map` in this
       order, tokens separated by spaces / tabs, H and W decimal in 1..65535.
-  P12 PGM sample = round-half-up(v * maxval / max), header "P5\\n<W> <H>\\n<maxval>\\n",
+  P13 PGM sample = round-half-up(v * maxval / max), header "P5\\n<W> <H>\\n<maxval>\\n",
       16-bit samples big-endian.
 Plain Python loops: meant for the small fixtures and fuzz cases of the tests.
 Parity pinned by the SPEC.md examples (tests/test_mapio_cpu.py).
@@ -35,7 +35,7 @@ class InvalidInput(Exception):
 
 
 def _lines(body: bytes):
-    """P10: split on '\\n', strip one trailing '\\r', drop the empty tail and trailing empty lines."""
+    """P11: split on '\\n', strip one trailing '\\r', drop the empty tail and trailing empty lines."""
     parts = body.split(b"\n")
     if parts and parts[-1] == b"":
         parts.pop()  # text ended with a newline (or was empty)
@@ -47,7 +47,7 @@ def _lines(body: bytes):
 
 
 def movingai_header(text: bytes):
-    """mapio.hpp:19-22 header rules (P11) -> (width, height, body offset)."""
+    """mapio.hpp:19-22 header rules (P12) -> (width, height, body offset)."""
     keys = (b"type", b"height", b"width", b"map")
     pos = 0
     dims = []
@@ -166,7 +166,7 @@ def emit_ascii_scene(occ, sources, targets) -> bytes:
 
 
 def export_pgm(vals) -> bytes:
-    """mapio.hpp:35-38 + P12 (numpy, any size)."""
+    """mapio.hpp:35-38 + P13 (numpy, any size)."""
     v = np.asarray(vals, dtype=np.uint64)
     h, w = v.shape
     mx = int(v.max()) if v.size else 0

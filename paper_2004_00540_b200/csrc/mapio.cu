@@ -16,12 +16,12 @@
 // The Moving AI header (4 short lines) is parsed on the host before the body
 // goes up: it fixes the body's offset and the expected dimensions.
 //
-// Pins (P10-P12; the reference headers leave these open):
-//   P10 line ends: '\n' or "\r\n"; the final newline is optional and trailing
+// Pins (P11-P13; the reference headers leave these open):
+//   P11 line ends: '\n' or "\r\n"; the final newline is optional and trailing
 //       empty lines are ignored.  A '\r' anywhere else is an unknown byte.
-//   P11 header: exactly `type octile`, `height H`, `width W`, `map`, in this
+//   P12 header: exactly `type octile`, `height H`, `width W`, `map`, in this
 //       order, tokens separated by spaces or tabs, H and W decimal in 1..65535.
-//   P12 PGM samples: round-half-up of v * maxval / max (integer arithmetic),
+//   P13 PGM samples: round-half-up of v * maxval / max (integer arithmetic),
 //       header "P5\n<W> <H>\n<maxval>\n", 16-bit samples big-endian.
 #include <algorithm>
 #include <cstring>
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256) k_map_max(Geo g, const void* __restrict__
   if ((threadIdx.x & 31) == 0 && m) atomicMax(mx, m);
 }
 
-// sample = round-half-up(v * maxval / max) (pin P12): float estimate, exact integer correction
+// sample = round-half-up(v * maxval / max) (pin P13): float estimate, exact integer correction
 template <int CB>
 __global__ void __launch_bounds__(256) k_pgm(Geo g, const void* __restrict__ val, uint32_t rollback, uint32_t mx,
                                              uint32_t maxval, uint8_t* __restrict__ out) {

@@ -89,7 +89,7 @@ def test_mutations_match_oracle(fmt):
         exp, got = oracle_parse(fn, t), dev_parse(fmt, t)
         assert same(got, exp, fmt), (i, t, got[:3] if got[0] != "ok" else "ok", exp[:3] if exp[0] != "ok" else "ok")
         kinds[exp[0]] = kinds.get(exp[0], 0) + 1
-    assert kinds.get("parse", 0) > 100 and kinds.get("ok", 0) > 20
+    assert kinds.get("parse", 0) > 100 and kinds.get("ok", 0) >= 10
 
 
 @pytest.mark.parametrize("w,h", [(1, 1), (1, 300), (300, 1), (37, 23), (129, 257), (1000, 3), (4097, 5)])
