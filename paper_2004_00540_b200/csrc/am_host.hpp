@@ -73,7 +73,10 @@ struct am_grid {
   unsigned long long* t_processed = nullptr; // tiles processed (statistics)
   uint32_t t_blk = 0;                        // index of the next tile block (list / counter selection)
   void* t_bnd = nullptr;                     // slabs: first / last kK rows gathered for the neighbours (2 x kK x pitch)
-  am::TileBook book() const { return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed}; }
+  uint8_t* t_src = nullptr;                  // per tile: a source in its staged rows (TileBook::tsrc)
+  am::TileBook book() const {
+    return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed, t_src};
+  }
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;
   uint64_t* d_counts = nullptr;
@@ -135,6 +138,9 @@ struct Transport {
   virtual am_status reduce(std::vector<uint32_t*>& words, bool take_max) = 0;
   // local values must still be combined on the host (in-process groups)
   virtual bool host_combine() const = 0;
+  // a one-slab-per-process transport whose slab has a neighbour below it
+  // (its bottom halo holds that neighbour's rows, not padding)
+  virtual bool lower_neighbour() const { return false; }
 };
 
 struct SlabRef {

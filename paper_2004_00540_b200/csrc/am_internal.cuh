@@ -108,7 +108,12 @@ struct TileBook {
   uint32_t* list[2];
   uint32_t* count;                // [6]: list lengths [0..2], item fetch counters [3..5] (both by block mod 3)
   unsigned long long* processed;  // tiles processed (statistics)
+  const uint8_t* tsrc;            // per tile: a source lies in the rows its items stage (static)
 };
+// list entries: band << 16 | chunk, plus kListSrc when the tile's tsrc is set (the item takes the source path
+// without reading the per-row flags first)
+constexpr uint32_t kListSrc = 1u << 31;
+constexpr uint32_t kListBand = 0x7FFFu;
 
 // ---- kernels (stencil.cu) ----
 void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcmask, void* d_val,
@@ -123,6 +128,8 @@ void launch_layer(const Geo& g, int cell_bits, const void* in, void* out, const 
 // active-tile skipping (stencil.cu)
 // lists the tiles of block 0: the 3x3 tile neighbourhood of every tile holding a source
 void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cudaStream_t s);
+// TileBook::tsrc from the per-band source-row flags (after launch_srcmask_rows)
+void launch_tile_src(const Geo& g, const uint8_t* rowsrc, uint8_t* tsrc, cudaStream_t s);
 // every tile current at `layer` in field `home`, all listed for block blk
 void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer, int home, cudaStream_t s);
 // pdl: launch with programmatic stream serialization (back-to-back tile blocks on one stream)

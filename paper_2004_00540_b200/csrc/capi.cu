@@ -166,6 +166,7 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->t_count);
   am::dfree(ctx, g->t_bnd);
   am::dfree(ctx, g->t_processed);
+  am::dfree(ctx, g->t_src);
   delete g;
 }
 
@@ -218,6 +219,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
     if (slab && !e) e = am::dmalloc(ctx, &g->t_bnd, (size_t)2 * kK * g->g.pitch * 4);  // room for 32-bit cells
     if (slab && !e) e = cudaMemsetAsync(g->t_bnd, 0, (size_t)2 * kK * g->g.pitch * 4, s);
     if (!e) e = am::dmalloc(ctx, &g->t_processed, 8);
+    if (!e) e = am::dmalloc(ctx, &g->t_src, nt);
   }
   if (!e) e = cudaMemsetAsync(g->val[0], 0, cells * 2, s);
   if (!e) e = cudaMemsetAsync(g->val[1], 0, cells * 2, s);
@@ -238,7 +240,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) {
     launch_srcmask_rows(g->g, H_total, row0, d_src, n_src, g->srcmask_dense, g->occ, g->srcmask, g->rowsrc, d_err,
                         s);
-    ++ctx->launches;
+    launch_tile_src(g->g, g->rowsrc, g->t_src, s);
+    ctx->launches += 2;
     e = cudaPeekAtLastError();
   }
   if (!e) e = cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
@@ -414,6 +417,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     tiles = tiles && slabs[i].g->t_state;
     if (i + 1 < slabs.size()) tiles = tiles && slabs[i].g->g.H % kTileRows == 0;
   }
+  // one slab per process: the same rule for a rank with a lower neighbour (the
+  // other ranks may still use tiles: both exchanges move the same rows)
+  if (tr && tr->lower_neighbour()) tiles = tiles && slabs[0].g->g.H % kTileRows == 0;
   const bool halos = tiles && (slabs.size() > 1 || tr);  // boundary exchange + halo scan every block
   uint64_t nt = 0;
   for (auto& sr : slabs) nt += tiles ? sr.g->g.ntiles() : 0;

@@ -136,6 +136,7 @@ struct NcclTransport final : Transport {
     return AM_OK;
   }
   bool host_combine() const override { return false; }
+  bool lower_neighbour() const override { return ctx->comm->rank + 1 < ctx->comm->nranks; }
 };
 
 Transport* make_nccl_transport(am_ctx* ctx, am_grid* g) {

@@ -334,6 +334,12 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 #ifndef AM_QUARTERS
 #define AM_QUARTERS 1  // light blocks run two quarter items per tile
 #endif
+#ifndef AM_PAIRS
+#define AM_PAIRS 1  // heavy blocks (more tiles than warps) run two whole tiles per item
+#endif
+#ifndef AM_PAIR_MIN4
+#define AM_PAIR_MIN4 6  // pairs from this many quarter warp slots of tiles on (below: halves, shorter latency)
+#endif
 #ifndef AM_QUARTER_SLOTS
 #define AM_QUARTER_SLOTS 1  // quarter items while they fit this many times into the warp slots
 #endif
@@ -570,12 +576,18 @@ constexpr int kTileSteps = kHalfRows + 2 * kK;             // steps per item
 constexpr int kStageRows = kTileRows + 2 * kK;             // rows staged (-K .. kTileRows+K-1)
 constexpr int kTileRowBytes = 32 * kTileWPL * 2;           // one u16 row of the warp's band
 constexpr int kTileBufBytes = kStageRows * kTileRowBytes;  // 12 KB
+constexpr int kPairSteps = kTileRows + 2 * kK;             // steps of a pair item (48)
 static_assert(kTileWPL == 4, "the staged item path loads 8 B per lane and tile row");
 static_assert(kHalfRows == 2 * kK, "phase layout: 16-row halves with K = 8");
-constexpr int kTileWarpSmem = kTileBufBytes > kTileWarpSmemRing ? kTileBufBytes : kTileWarpSmemRing;
+// heavy blocks, pairs of tiles (see tile_pair16): 32 staged rows of A + B (a ring over 48 steps)
+constexpr int kPairRowBytes = 2 * kTileRowBytes;        // tile A's row, then tile B's row
+constexpr int kPairSlots = kTileRows;                   // ring slots
+constexpr int kPairBufBytes = kPairSlots * kPairRowBytes;  // 16 KB
+constexpr int kTileWarpSmem0 = kTileBufBytes > kTileWarpSmemRing ? kTileBufBytes : kTileWarpSmemRing;
+constexpr int kTileWarpSmem = AM_PAIRS && kPairBufBytes > kTileWarpSmem0 ? kPairBufBytes : kTileWarpSmem0;
 constexpr int kTileSmem = kWarpsPerCta * kTileWarpSmem;  // dynamic shared memory of k_block_tiles
 
-enum { kOutNone = 0, kOutTop = 1, kOutBot = 2 };
+enum { kOutNone = 0, kOutTop = 1, kOutBot = 2, kOutMid = 3 };  // kOutMid: outputs feed acc only
 
 // Steps [s0, s1): the upper half reads staged row s, the lower half row s+16.
 // HI: rows between the two u16 streams (16 for tile halves, 8 for quarter items).
@@ -584,7 +596,8 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
                                            uint32_t (&P0)[kK][4], uint32_t (&P1)[kK][4], uint16_t*& oA,
                                            uint16_t*& oB, size_t pitch, bool st, uint32_t& acc, uint32_t& acc_edge) {
   using C = Cell<16>;
-  constexpr int kB = HI * kTileRowBytes;  // the hi stream runs HI rows further down
+  constexpr int kRow = HI < 0 ? kPairRowBytes : kTileRowBytes;   // HI < 0: pair buffer (see fill_pair)
+  constexpr int kB = HI < 0 ? kTileRowBytes : HI * kTileRowBytes;  // the hi stream runs HI rows further down
   auto words = [](uint2 a, uint2 b, uint32_t (&x)[4]) {
     x[0] = __byte_perm(a.x, b.x, 0x5410);
     x[1] = __byte_perm(a.x, b.x, 0x7632);
@@ -602,15 +615,14 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
 #pragma unroll
     for (int w = 0; w < 4; ++w) rm = C::acc_min(x[w], rm);
     acc = C::vmin(acc, rm);
-    acc_edge = C::vmin(acc_edge, rm);
+    if (OUT != kOutMid) acc_edge = C::vmin(acc_edge, rm);
   };
 #pragma unroll 1
   for (int s = s0; s < s1; s += 2) {
-    const uint8_t* r = buf + s * kTileRowBytes;
+    const uint8_t* r = buf + (HI < 0 ? s % kPairSlots : s) * kRow;
     uint32_t x0[4], x1[4];
     words(*reinterpret_cast<const uint2*>(r), *reinterpret_cast<const uint2*>(r + kB), x0);
-    words(*reinterpret_cast<const uint2*>(r + kTileRowBytes), *reinterpret_cast<const uint2*>(r + kB + kTileRowBytes),
-          x1);
+    words(*reinterpret_cast<const uint2*>(r + kRow), *reinterpret_cast<const uint2*>(r + kB + kRow), x1);
     if (lag) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
@@ -629,6 +641,73 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
       emit(x1);
     }
   }
+}
+
+// Pipeline fill (steps 0 .. 2K-1) without the work that cannot reach an
+// output.  Layer j+1 of row t-j-1 is produced at step t; the K-layer result
+// is needed on rows [K, steps) only, so layer j+1 is needed on rows >= j+1,
+// i.e. from step 2j+2 on.  At steps 2j and 2j+1 layer j's input rows only
+// have to enter the window (P0 / P1 slot of the step's parity); before that
+// the iteration does nothing.  Step pair m (steps 2m, 2m+1) therefore runs
+// iterations j < m, stores j == m and skips the rest: 56 of the 128 layer
+// updates of the fill (a tile item: 184 instead of 256 per u16 stream).
+#ifndef AM_TRIM
+#define AM_TRIM 1
+#endif
+#ifndef AM_STATIC_FIRST
+#define AM_STATIC_FIRST 1
+#endif
+// HI: rows between the lo and hi streams of a staged buffer of kTileRowBytes rows; or HI < 0: pair
+// buffers (rows of kPairRowBytes, the hi stream's row right after the lo stream's)
+template <int M, int HI>
+__device__ __forceinline__ void fill_pair(const uint8_t* buf, uint32_t lagw, bool lag, uint32_t (&P0)[kK][4],
+                                          uint32_t (&P1)[kK][4]) {
+  constexpr int kRow = HI < 0 ? kPairRowBytes : kTileRowBytes;
+  constexpr int kB = HI < 0 ? kTileRowBytes : HI * kTileRowBytes;
+  const uint8_t* r = buf + 2 * M * kRow;
+  const uint2 a0 = *reinterpret_cast<const uint2*>(r), b0 = *reinterpret_cast<const uint2*>(r + kB);
+  const uint2 a1 = *reinterpret_cast<const uint2*>(r + kRow), b1 = *reinterpret_cast<const uint2*>(r + kB + kRow);
+  uint32_t x0[4] = {__byte_perm(a0.x, b0.x, 0x5410), __byte_perm(a0.x, b0.x, 0x7632),
+                    __byte_perm(a0.y, b0.y, 0x5410), __byte_perm(a0.y, b0.y, 0x7632)};
+  uint32_t x1[4] = {__byte_perm(a1.x, b1.x, 0x5410), __byte_perm(a1.x, b1.x, 0x7632),
+                    __byte_perm(a1.y, b1.y, 0x5410), __byte_perm(a1.y, b1.y, 0x7632)};
+  if (lag) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      x0[w] = add_lag<16>(x0[w], lagw);
+      x1[w] = add_lag<16>(x1[w], lagw);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j <= M + 1; ++j) {  // skewed as in stream_step2
+    if (j < M) {
+      stream_layer<16, 0, 4>(j, x0, P0, P1);
+    } else if (j == M) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) P0[M][w] = x0[w];
+    }
+    if (j >= 1 && j - 1 < M) {
+      stream_layer<16, 1, 4>(j - 1, x1, P0, P1);
+    } else if (j >= 1 && j - 1 == M) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) P1[M][w] = x1[w];
+    }
+  }
+}
+
+// steps [0, K) read with lag a, [K, 2K) with lag b
+template <int HI>
+__device__ __forceinline__ void tile_fill(const uint8_t* buf, uint32_t lag_a, bool la, uint32_t lag_b, bool lb,
+                                          uint32_t (&P0)[kK][4], uint32_t (&P1)[kK][4]) {
+  static_assert(kK == 8, "fill schedule written for K = 8");
+  fill_pair<0, HI>(buf, lag_a, la, P0, P1);
+  fill_pair<1, HI>(buf, lag_a, la, P0, P1);
+  fill_pair<2, HI>(buf, lag_a, la, P0, P1);
+  fill_pair<3, HI>(buf, lag_a, la, P0, P1);
+  fill_pair<4, HI>(buf, lag_b, lb, P0, P1);
+  fill_pair<5, HI>(buf, lag_b, lb, P0, P1);
+  fill_pair<6, HI>(buf, lag_b, lb, P0, P1);
+  fill_pair<7, HI>(buf, lag_b, lb, P0, P1);
 }
 
 // Tile (band b, chunk c) without source rows; lw / homes: this lane's lag and
@@ -669,10 +748,12 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
   const int lane = threadIdx.x & 31;
   const size_t pitch = g.pitch;
   uint32_t P0[kK][4], P1[kK][4];
+#if !AM_TRIM
 #pragma unroll
   for (int j = 0; j < kK; ++j)
 #pragma unroll
     for (int w = 0; w < 4; ++w) P0[j][w] = P1[j][w] = 0u;
+#endif
   uint32_t acc = 0xFFFFFFFFu, accTop = 0xFFFFFFFFu, accBot = 0xFFFFFFFFu;
   const ptrdiff_t od = ((homes >> 6) & 1u) ? delta : 0;
   uint16_t* oA = f0 + od + (size_t)(c * kTileRows + kK) * pitch + b * kTileCols + lane * kTileWPL;  // tile row 0
@@ -684,12 +765,79 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
              l_dn = __any_sync(0xffffffffu, lag_dn != 0u);
   asm volatile("cp.async.wait_group 1;" ::: "memory");
   __syncwarp();
+#if AM_TRIM
+  tile_fill<kHalfRows>(rb, lag_up, l_up, lag_in, l_in, P0, P1);
+#else
   tile_phase<kOutNone>(rb, 0, kK, lag_up, l_up, P0, P1, oA, oB, pitch, st, acc, accTop);
   tile_phase<kOutNone>(rb, kK, 2 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
+#endif
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
   tile_phase<kOutTop>(rb, 2 * kK, 3 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
   tile_phase<kOutBot>(rb, 3 * kK, kTileSteps, lag_dn, l_dn, P0, P1, oA, oB, pitch, st, acc, accBot);
+  if (!st) acc = accTop = accBot = 0xFFFFFFFFu;  // halo lanes hold no output
+  edge[0] = accTop;
+  edge[1] = accBot;
+  return acc;
+}
+
+// ---- heavy blocks: pairs of tiles (lo = tile A, hi = tile B) ----------------
+//
+// With more active tiles than warps the kernel is throughput bound, and the
+// halves layout pays 2 x 2K halo rows per 32-row tile.  A pair item streams
+// two whole tiles side by side instead (any two listed tiles: the u16 streams
+// are independent): 32 + 2K = 48 steps for 64 tile rows, 156 instead of 184
+// layer updates per tile after the trimmed fill.  Staged rows live in a
+// 32-slot ring (16 KB per warp): rows 0-31 up front, rows 32-47 into the slots
+// of rows 0-15 once the fill has consumed them.
+// copies staged rows [r0, r1) (staged row = tile row + kK) into ring slot row % kPairSlots;
+// lanes 0-15 copy tile A's 256 B of the row, lanes 16-31 tile B's
+__device__ __forceinline__ void pair_stage(const Geo& g, const uint16_t* __restrict__ f0, ptrdiff_t delta,
+                                           const uint16_t* baseA, const uint16_t* baseB, uint32_t homesA,
+                                           uint32_t homesB, uint8_t* buf, int r0, int r1) {
+  const int lane = threadIdx.x & 31;
+  const size_t pitch = g.pitch;
+  const uint32_t hA = __shfl_sync(0xffffffffu, homesA, (2 * lane) & 31);
+  const uint32_t hB = __shfl_sync(0xffffffffu, homesB, (2 * lane) & 31);
+  const uint32_t ch = lane < 16 ? hA : hB;
+  const uint16_t* base = (lane < 16 ? baseA : baseB) + (lane & 15) * 8;  // tile row -kK, this lane's 8 cells
+  uint8_t* dst = buf + (lane >> 4) * kTileRowBytes + (lane & 15) * 16;
+  for (int row = r0; row < r1; ++row) {
+    const int reg = row < kK ? 0 : (row < kK + kTileRows ? 1 : 2);
+    cp_async16(dst + (row % kPairSlots) * kPairRowBytes, base + (((ch >> reg) & 1u) ? delta : 0) + (size_t)row * pitch);
+  }
+}
+
+// lwA / lwB: this lane's lag of the regions above / inside / below tile A / B; homes bit 6: output field.
+// Returns the min over covered output cells of a-1 (lo = A, hi = B); edge[0] / edge[1]: the same over the
+// tiles' first / last kK rows.  The caller has issued pair_stage of rows [0, 16) and [16, 32) (two groups).
+__device__ __forceinline__ uint32_t tile_pair16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta,
+                                                const uint16_t* baseA, const uint16_t* baseB, const uint32_t (&lwA)[3],
+                                                const uint32_t (&lwB)[3], uint32_t homesA, uint32_t homesB,
+                                                uint16_t* oA, uint16_t* oB, uint32_t* edge, uint8_t* buf) {
+  const int lane = threadIdx.x & 31;
+  const size_t pitch = g.pitch;
+  uint32_t P0[kK][4], P1[kK][4];
+  uint32_t acc = 0xFFFFFFFFu, accTop = 0xFFFFFFFFu, accBot = 0xFFFFFFFFu, dummy = 0u;
+  const bool st = lane >= kK / kTileWPL && lane < 32 - kK / kTileWPL;
+  const uint8_t* rb = buf + lane * 8;
+  const uint32_t lag_up = lwA[0] | lwB[0] << 16, lag_in = lwA[1] | lwB[1] << 16, lag_dn = lwA[2] | lwB[2] << 16;
+  const bool l_up = __any_sync(0xffffffffu, lag_up != 0u), l_in = __any_sync(0xffffffffu, lag_in != 0u),
+             l_dn = __any_sync(0xffffffffu, lag_dn != 0u);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncwarp();
+  tile_fill<-1>(rb, lag_up, l_up, lag_in, l_in, P0, P1);  // steps 0-15: staged rows 0-15
+  __syncwarp();                                            // every lane is done with slots 0-15
+  pair_stage(g, f0, delta, baseA, baseB, homesA, homesB, buf, kPairSlots, kPairSteps);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 1;" ::: "memory");  // rows 16-31
+  __syncwarp();
+  tile_phase<kOutTop, -1>(rb, 2 * kK, 3 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
+  tile_phase<kOutMid, -1>(rb, 3 * kK, 4 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, dummy);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // rows 32-47
+  __syncwarp();
+  tile_phase<kOutMid, -1>(rb, 4 * kK, 5 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, dummy);
+  tile_phase<kOutBot, -1>(rb, 5 * kK, kPairSteps, lag_dn, l_dn, P0, P1, oA, oB, pitch, st, acc, accBot);
   if (!st) acc = accTop = accBot = 0xFFFFFFFFu;  // halo lanes hold no output
   edge[0] = accTop;
   edge[1] = accBot;
@@ -734,10 +882,12 @@ __device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __res
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   uint32_t P0[kK][4], P1[kK][4];
+#if !AM_TRIM
 #pragma unroll
   for (int j = 0; j < kK; ++j)
 #pragma unroll
     for (int w = 0; w < 4; ++w) P0[j][w] = P1[j][w] = 0u;
+#endif
   uint32_t acc = 0xFFFFFFFFu, accE = 0xFFFFFFFFu;
   const ptrdiff_t od = ((homes >> 6) & 1u) ? delta : 0;
   uint16_t* oA = f0 + od + ((size_t)c * kTileRows + r0 + kK) * pitch + b * kTileCols + lane * kTileWPL;
@@ -752,8 +902,12 @@ __device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __res
              l2 = __any_sync(0xffffffffu, lag2 != 0u);
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
+#if AM_TRIM
+  tile_fill<kQuarterRows>(rb, lag0, l0, lag1, l1, P0, P1);
+#else
   tile_phase<kOutNone, kQuarterRows>(rb, 0, kK, lag0, l0, P0, P1, oA, oB, pitch, st, acc, accE);
   tile_phase<kOutNone, kQuarterRows>(rb, kK, 2 * kK, lag1, l1, P0, P1, oA, oB, pitch, st, acc, accE);
+#endif
   tile_phase<kOutTop, kQuarterRows>(rb, 2 * kK, kQuarterSteps, lag2, l2, P0, P1, oA, oB, pitch, st, acc, accE);
   if (!st) acc = accE = 0xFFFFFFFFu;  // halo lanes hold no output
   edge[0] = edge[1] = accE;  // every output row of a quarter stream is within kK of its item's edge
@@ -809,14 +963,21 @@ __constant__ uint8_t kFacing[3][3] = {{8, 2, 7}, {4, 0, 3}, {6, 1, 5}};
 __device__ __forceinline__ void push_tiles(const Geo& g, TileBook& book, uint32_t blk, bool want, int c, int b) {
   const bool in = want && c >= 0 && b >= 0 && c < (int)g.nchunks && b < (int)g.tbands;
   bool add = false;
-  if (in) add = atomicMax(&book.sched[(uint32_t)c * g.tbands + (uint32_t)b], blk + 2) < blk + 2;
+  uint32_t src = 0;
+  if (in) {
+    const uint32_t t = (uint32_t)c * g.tbands + (uint32_t)b;
+    src = book.tsrc[t];  // independent of the atomic: no added latency
+    add = atomicMax(&book.sched[t], blk + 2) < blk + 2;
+  }
   const uint32_t m = __ballot_sync(0xffffffffu, add);
   if (!m) return;
   const int lane = threadIdx.x & 31;
   uint32_t base = 0;
   if (lane == __ffs(m) - 1) base = atomicAdd(&book.count[(blk + 1) % 3], (uint32_t)__popc(m));
   base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-  if (add) book.list[(blk + 1) & 1][base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)b << 16 | (uint32_t)c;
+  if (add)
+    book.list[(blk + 1) & 1][base + __popc(m & ((1u << lane) - 1u))] =
+        (uint32_t)b << 16 | (uint32_t)c | (src ? kListSrc : 0u);
 }
 
 // Active-tile mode: the warps walk the block's work list (items = band << 16
@@ -888,27 +1049,122 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
     return (a == 0u ? 1u : 0u) | (ee == 0u ? 6u : 0u) | (l == 0u ? 8u : 0u) | (r == 0u ? 16u : 0u) |
            (el == 0u ? 0xA0u : 0u) | (er == 0u ? 0x140u : 0u);
   };
+  // light blocks (at most half a warp slot per tile): two quarter items per tile, shorter latency
+  const uint32_t nwarps = gridDim.x * (kBlockThreads / 32);
+  const bool quarters = CB == 16 && AM_QUARTERS && 2u * n <= (uint32_t)AM_QUARTER_SLOTS * nwarps;
+  // heavy blocks (more tiles than warps): two whole tiles per item (tile_pair16)
+  const bool pairs = CB == 16 && AM_PAIRS && !quarters && 4u * n > (uint32_t)AM_PAIR_MIN4 * nwarps;
+  const uint32_t nitems = quarters ? 2u * n : (pairs ? (n + 1) / 2 : n);
+#if AM_STATIC_FIRST
+  // Every warp's first item is static, spread over the CTAs (item i -> CTA i mod grid, so consecutive items
+  // land on different SMs); only items past the warp count are fetched dynamically (a warp that finishes
+  // early takes the next one).  A light block then runs without a single fetch atomic, and a heavy block
+  // saves one same-address atomic per warp.
+  const bool light = nitems <= nwarps;
+  auto fetch = [&]() {
+    if (AM_STATIC_FIRST == 2 ? light : AM_STATIC_FIRST == 1 && light) return 0xFFFFFFFFu;
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(&book.count[3 + blk % 3], 1u) + (AM_STATIC_FIRST == 2 ? nwarps : 0u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  // 1: static items in light blocks only (heavy blocks fetch every item); 2: static first item everywhere
+  uint32_t w = (AM_STATIC_FIRST == 2 || light) ? (threadIdx.x >> 5) * gridDim.x + blockIdx.x : fetch();
+#else
   // items are fetched dynamically: a warp that finishes early takes the next one
   auto fetch = [&]() {
     uint32_t v = 0;
     if (lane == 0) v = atomicAdd(&book.count[3 + blk % 3], 1u);
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  // (a static first item per warp packs light blocks onto few SMs: measured slower)
-  // light blocks (at most half a warp slot per tile): two quarter items per tile, shorter latency
-  const bool quarters = CB == 16 && AM_QUARTERS && 2u * n <= (uint32_t)AM_QUARTER_SLOTS * gridDim.x * (kBlockThreads / 32);
-  const uint32_t nitems = quarters ? 2u * n : n;
   uint32_t w = fetch();
-  while (w < nitems) {
-    const uint32_t it = list[quarters ? w >> 1 : w];
-    const uint32_t half = quarters ? w & 1u : 0u;
-    const uint32_t bA = it >> 16, cA = it & 0xFFFFu;
+#endif
+  constexpr uint32_t kNone = 0xFFFFFFFFu;
+  uint32_t solo = kNone;  // the second tile of a pair item that takes the single-tile path
+  while (w < nitems || solo != kNone) {
+    uint32_t it, half = 0;
+    bool fetch_next = true;
+    if (solo != kNone) {
+      it = solo;
+      solo = kNone;
+    } else if (CB == 16 && pairs) {
+      const uint32_t itA = list[2 * w], itB = 2 * w + 1 < n ? list[2 * w + 1] : kNone;
+      if constexpr (CB == 16) {
+        if (itB != kNone) {
+          const uint32_t bA = (itA >> 16) & kListBand, cA = itA & 0xFFFFu, bB = (itB >> 16) & kListBand,
+                         cB = itB & 0xFFFFu;
+          if (!((itA | itB) & kListSrc)) {  // no source in reach of either tile
+            const uint32_t tA = cA * g.tbands + bA, tB = cB * g.tbands + bB;
+            const uint32_t sA = state_at_l0(tA), sB = state_at_l0(tB);
+            uint32_t lwA[3], hmA[3], lwB[3], hmB[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              lwA[d] = region(cA, bA, d - 1, hmA[d]);
+              lwB[d] = region(cB, bB, d - 1, hmB[d]);
+            }
+            const uint32_t ohA = (sA & 1u) ^ 1u, ohB = (sB & 1u) ^ 1u;
+            const uint32_t homesA = hmA[0] | hmA[1] << 1 | hmA[2] << 2, homesB = hmB[0] | hmB[1] << 1 | hmB[2] << 2;
+            uint16_t* f16 = reinterpret_cast<uint16_t*>(f0);
+            const size_t pitch = g.pitch;
+            const uint16_t* baseA = f16 + (size_t)cA * kTileRows * pitch + bA * kTileCols;
+            const uint16_t* baseB = f16 + (size_t)cB * kTileRows * pitch + bB * kTileCols;
+            uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
+            __syncwarp();  // every lane is done reading the previous item's rows
+            pair_stage(g, f16, delta, baseA, baseB, homesA, homesB, buf, 0, kHalfRows);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            pair_stage(g, f16, delta, baseA, baseB, homesA, homesB, buf, kHalfRows, kTileRows);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            uint16_t* oA = f16 + (ohA ? delta : 0) + (size_t)(cA * kTileRows + kK) * pitch + bA * kTileCols + lane * kTileWPL;
+            uint16_t* oB = f16 + (ohB ? delta : 0) + (size_t)(cB * kTileRows + kK) * pitch + bB * kTileCols + lane * kTileWPL;
+            uint32_t edge[2];
+            const uint32_t acc = tile_pair16(g, f16, delta, baseA, baseB, lwA, lwB, homesA, homesB, oA, oB, edge, buf);
+            const uint32_t next = fetch();
+            // frontier regions of A (lo) and B (hi)
+            auto m9_of = [&](int h) -> uint32_t {
+              auto part = [h](uint32_t v) { return h ? v >> 16 : v & 0xFFFFu; };
+              const uint32_t vals[9] = {__reduce_min_sync(0xffffffffu, part(acc)),
+                                        __reduce_min_sync(0xffffffffu, part(edge[0])),
+                                        __reduce_min_sync(0xffffffffu, part(edge[1])),
+                                        part(lanes_min(acc, kL)),
+                                        part(lanes_min(acc, kR)),
+                                        part(lanes_min(edge[0], kL)),
+                                        part(lanes_min(edge[0], kR)),
+                                        part(lanes_min(edge[1], kL)),
+                                        part(lanes_min(edge[1], kR))};
+              uint32_t m = 0;
+#pragma unroll
+              for (int k = 0; k < 9; ++k) m |= (vals[k] == 0u ? 1u : 0u) << k;
+              gmin = min(gmin, vals[0]);
+              return m;
+            };
+            const uint32_t mA = m9_of(0), mB = m9_of(1);
+            if (lane == 0) {
+              book.state[tA] = (unsigned long long)sA << 32 | (l1 << 1 | ohA);
+              book.state[tB] = (unsigned long long)sB << 32 | (l1 << 1 | ohB);
+            }
+            const int dr = lane / 3 - 1, dc = lane % 3 - 1;
+            const int fk = kFacing[(lane / 3) % 3][lane % 3];
+            push_tiles(g, book, blk, lane < 9 && ((mA >> fk) & 1u), (int)cA - dr, (int)bA - dc);
+            push_tiles(g, book, blk, lane < 9 && ((mB >> fk) & 1u), (int)cB - dr, (int)bB - dc);
+            w = next;
+            continue;
+          }
+        }
+      }
+      it = itA;  // a source in reach or no partner: the single-tile path, one tile after the other
+      solo = itB;
+      fetch_next = itB == kNone;
+    } else {
+      it = list[quarters ? w >> 1 : w];
+      half = quarters ? w & 1u : 0u;
+    }
+    const uint32_t bA = (it >> 16) & kListBand, cA = it & 0xFFFFu;
     const uint32_t tA = cA * g.tbands + bA;
     const uint8_t* rf = rowsrc + g.tile_rowsrc(bA);
     const uint32_t ra = cA * kTileRows;
-    uint32_t f = 0;  // source rows in reach (loaded alongside the states)
+    uint32_t f = 0;  // source rows in reach (read only for tiles listed with kListSrc)
     if constexpr (CB == 16) {
-      if (quarters) {
+      if (!(it & kListSrc)) {
+      } else if (quarters) {
         f = rf[ra + half * kHalfRows + lane];  // the item's 32 staged rows
       } else {
         f = rf[ra + lane];
@@ -985,7 +1241,7 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
       for (int k = 0; k < 9; ++k) m9 |= (vals[k] == 0u ? 1u : 0u) << k;
       gmin = min(gmin, vals[0]);
     }
-    const uint32_t next = fetch();  // the next item's index travels while this item's bookkeeping runs
+    const uint32_t next = fetch_next ? fetch() : w;  // the next item's index travels while the bookkeeping runs
     // new state (old kept in the high word for this block's readers)
     if (lane == 0) book.state[tA] = (unsigned long long)sa << 32 | (l1 << 1 | out_home);
     // list the next block's candidates: lane k < 9 for the neighbour at (dr, dc) = (k/3-1, k%3-1)
@@ -1162,7 +1418,7 @@ __global__ void k_tiles_all(Geo g, TileBook book, uint32_t blk, uint32_t layer, 
   const uint32_t cur = layer << 1 | home;
   book.state[t] = (unsigned long long)cur << 32 | cur;
   book.sched[t] = blk + 1;
-  book.list[blk & 1][t] = (t % g.tbands) << 16 | (t / g.tbands);
+  book.list[blk & 1][t] = (t % g.tbands) << 16 | (t / g.tbands) | (book.tsrc[t] ? kListSrc : 0u);
 }
 
 // -------------------------------------------------------- single layer
@@ -1341,6 +1597,22 @@ void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, co
     k_block<32, false><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
   else
     k_block<32, true><<<blocks, kBlockThreads, kBlockSmem, s>>>(g, i32, (uint32_t*)out, srcmask, rowsrc, flag);
+}
+
+// TileBook::tsrc: one thread per tile, OR of its band's source-row flags over the rows its items stage
+__global__ void k_tile_src(Geo g, const uint8_t* __restrict__ rowsrc, uint8_t* __restrict__ tsrc) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.ntiles()) return;
+  const uint32_t b = t % g.tbands, c = t / g.tbands;
+  const uint8_t* rf = rowsrc + g.tile_rowsrc(b);
+  uint32_t any = 0;
+  for (uint32_t r = c * kTileRows; r < c * kTileRows + kTileRows + 2 * kK && r < g.rows; ++r) any |= rf[r];
+  tsrc[t] = any ? 1 : 0;
+}
+
+void launch_tile_src(const Geo& g, const uint8_t* rowsrc, uint8_t* tsrc, cudaStream_t s) {
+  const uint32_t n = g.ntiles();
+  if (n) k_tile_src<<<(n + 255) / 256, 256, 0, s>>>(g, rowsrc, tsrc);
 }
 
 void launch_tiles_init(const Geo& g, const uint8_t* srcmask, TileBook book, cudaStream_t s) {

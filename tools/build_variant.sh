@@ -11,7 +11,7 @@ NVCC=/usr/local/cuda/bin/nvcc
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -ccbin g++ -I$ROOT/include $EXTRA"
 pids=()
-for f in stencil trace capi multigpu batch; do
+for f in stencil trace capi multigpu batch mapio; do
   $NVCC $FLAGS -c $SRC/$f.cu -o $OUT/$f.o & pids+=($!)
 done
 g++ -std=c++20 -O2 -fPIC -I$ROOT/include -c $SRC/actmap_api.cpp -o $OUT/actmap_api.o & pids+=($!)

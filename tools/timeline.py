@@ -59,6 +59,7 @@ def main():
     ends = [e["ts"] + e["dur"] for e in dev if e["cat"] == "kernel" and "block_tiles" in e["name"]]
     if len(ends) > 10:
         step = [b - a for a, b in zip(ends, ends[1:])]  # per-block span: end-to-end spacing of consecutive blocks
+        print("last 32 end spacings (us): " + " ".join(f"{x:.1f}" for x in step[-32:]))
         print("k_block_tiles end spacing by launch decile (mean us): " +
               " ".join(f"{sum(x) / len(x):.1f}" for x in (step[i * len(step) // 10:(i + 1) * len(step) // 10]
                                                           for i in range(10))))
