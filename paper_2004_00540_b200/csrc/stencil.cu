@@ -335,7 +335,7 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 #define AM_QUARTERS 1  // light blocks run two quarter items per tile
 #endif
 #ifndef AM_PAIRS
-#define AM_PAIRS 1  // heavy blocks (more tiles than warps) run two whole tiles per item
+#define AM_PAIRS 0  // 1: heavy blocks run two whole tiles per item (C4 -1.4%, C5 +50%: source tiles serialise)
 #endif
 #ifndef AM_PAIR_MIN4
 #define AM_PAIR_MIN4 6  // pairs from this many quarter warp slots of tiles on (below: halves, shorter latency)
