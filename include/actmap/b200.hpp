@@ -11,6 +11,7 @@
 
 #include "actmap/propagate.hpp"
 #include "actmap/reconstruct.hpp"
+#include "actmap/report.hpp"
 
 namespace actmap::b200 {
 
@@ -52,6 +53,11 @@ class Planner {
   /// invalid targets are reported per target, not thrown.
   std::vector<PlannedPath> reconstruct_all(std::span<const Coord> targets, Method method, std::uint64_t seed = 0,
                                            CornerRule rule = CornerRule::kStrict);
+  /// RunReport path entries (report.hpp TargetReport) for a target batch from one batched
+  /// device trace: covered, reached source, steps, Euclidean length and (emit_points) the
+  /// points; throws InvalidInputError for a target out of bounds or on an obstacle.
+  std::vector<TargetReport> target_reports(std::span<const Coord> targets, Method method, std::uint64_t seed = 0,
+                                           bool emit_points = true, CornerRule rule = CornerRule::kStrict);
   const PropagationStats& last_stats() const noexcept { return stats_; }
 
  private:

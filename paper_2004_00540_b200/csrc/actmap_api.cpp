@@ -405,6 +405,7 @@ std::vector<Path> trace_batch(detail::DeviceMap& dev, std::span<const Coord> tar
   for (size_t i = 0; i < n; ++i) {
     if (status[i] != AM_OK) continue;
     auto& p = paths[i].points;
+    p.reserve(off[i + 1] - off[i]);
     for (uint64_t k = off[i]; k < off[i + 1]; ++k) {
       if (pts[2 * k] == 0xFFFFFFFFu) break;  // removed by device-side straightening of uploaded maps
       p.push_back(Coord{pts[2 * k], pts[2 * k + 1]});
@@ -554,8 +555,32 @@ std::vector<PlannedPath> Planner::reconstruct_all(std::span<const Coord> targets
   for (size_t i = 0; i < targets.size(); ++i) {
     out[i].target = targets[i];
     out[i].status = static_cast<TargetStatus>(st[i]);
-    if (st[i] == AM_OK)
-      out[i].path = method == Method::kEuclidean ? straighten(paths[i], *p->grid, rule) : std::move(paths[i]);
+    // the map is the device propagation's, so Euclidean paths are already straight (pin P1': two +1 moves
+    // cannot span a sqrt(2) pair when 8-adjacent free cells differ by <= 1): no host straightening
+    (void)rule;
+    if (st[i] == AM_OK) out[i].path = std::move(paths[i]);
+  }
+  return out;
+}
+
+std::vector<TargetReport> Planner::target_reports(std::span<const Coord> targets, Method method, uint64_t seed,
+                                                  bool emit_points, CornerRule rule) {
+  auto planned = reconstruct_all(targets, method, seed, rule);
+  std::vector<TargetReport> out(planned.size());
+  for (size_t i = 0; i < planned.size(); ++i) {
+    TargetReport& t = out[i];
+    t.target = planned[i].target;
+    if (planned[i].status == TargetStatus::kInvalid)
+      throw InvalidInputError("target out of bounds or on an obstacle " + to_string(t.target));
+    if (planned[i].status == TargetStatus::kInternal)
+      throw Error("activity map has no ascending neighbour on the path from " + to_string(t.target));
+    if (planned[i].status != TargetStatus::kOk) continue;  // uncovered: recorded, not thrown (validate.hpp:76-77)
+    const Path& path = planned[i].path;
+    t.covered = true;
+    t.reached_source = path.source();
+    t.steps = path.steps();
+    t.euclidean_length = path_metrics(path).euclidean_length;
+    if (emit_points) t.points = std::move(planned[i].path.points);
   }
   return out;
 }

@@ -9,6 +9,7 @@
 #include "actmap/b200.hpp"
 #include "actmap/errors.hpp"
 #include "actmap/mapio.hpp"
+#include "actmap/report.hpp"
 #include "actmap/propagate.hpp"
 #include "actmap/reconstruct.hpp"
 
@@ -125,6 +126,29 @@ int main() {
       ++ok;
     }
     CHECK(ok > 10);
+    // RunReport path entries from the same device trace (report.hpp), serialised and read back
+    RunReport rep;
+    rep.command = "plan";
+    rep.scene = SceneSummary{g.width(), g.height(), g.obstacle_count(), src.size(), targets.size()};
+    rep.config.auto_cap = 2400;
+    rep.layers_used = a.layers_used;
+    rep.termination = a.cause == AutoStop::kFilled ? "filled" : a.cause == AutoStop::kStalled ? "stalled" : "cap";
+    rep.max_activity = a.layers_used + 1;
+    rep.bounds = layer_bound(g);
+    rep.paths = planner.target_reports(targets, b200::Method::kEuclidean);
+    CHECK(rep.paths.size() == targets.size());
+    for (size_t i = 0; i < rep.paths.size(); ++i) {
+      const TargetReport& t = rep.paths[i];
+      CHECK(t.target == targets[i]);
+      CHECK(t.covered == (paths[i].status == b200::TargetStatus::kOk));
+      if (!t.covered) continue;
+      CHECK(t.points == paths[i].path.points && t.steps + 1 == t.points.size());
+      CHECK(t.reached_source && src.contains(*t.reached_source));
+      CHECK(t.euclidean_length == path_metrics(paths[i].path).euclidean_length);
+    }
+    CHECK(parse_run_report(serialize_run_report(rep)) == rep);
+    const auto no_pts = planner.target_reports(targets, b200::Method::kEuclidean, 0, false);
+    CHECK(no_pts.size() == targets.size() && no_pts[0].points.empty() && no_pts[0].steps == rep.paths[0].steps);
   }
   // map / scene text (mapio.hpp)
   {

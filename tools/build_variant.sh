@@ -14,7 +14,9 @@ pids=()
 for f in stencil trace capi multigpu batch mapio; do
   $NVCC $FLAGS -c $SRC/$f.cu -o $OUT/$f.o & pids+=($!)
 done
-g++ -std=c++20 -O2 -fPIC -I$ROOT/include -c $SRC/actmap_api.cpp -o $OUT/actmap_api.o & pids+=($!)
+for f in actmap_api report; do
+  g++ -std=c++20 -O2 -fPIC -I$ROOT/include -c $SRC/$f.cpp -o $OUT/$f.o & pids+=($!)
+done
 for p in "${pids[@]}"; do wait $p; done
 $NVCC $ARCH -shared -cudart static -o $ROOT/build_ab/$NAME.so $OUT/*.o -ldl
 rm -rf "$OUT"
