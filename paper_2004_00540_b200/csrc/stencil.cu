@@ -654,6 +654,9 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
 #ifndef AM_TRIM
 #define AM_TRIM 1
 #endif
+#ifndef AM_FIN_BATCH
+#define AM_FIN_BATCH 1
+#endif
 #ifndef AM_STATIC_FIRST
 #define AM_STATIC_FIRST 1
 #endif
@@ -1308,8 +1311,31 @@ __global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, 
     // fused fixed-point zero check (k_zero_check): a free cell still at a = 0 is the bare flag
     const uint32_t bare = CB == 16 ? 0x80008000u : kFlag32;
     bool z = false;
+#if AM_FIN_BATCH
+    // all of this lane's vectors in flight at once (memory-level parallelism), then processed
+    constexpr int kVecCells = 16 / sizeof(typename Cell<CB>::T);
+    constexpr int kVecs = kTileCols / kVecCells;
+    constexpr int kPer = kVecs * kTileRows / 32;
+    static_assert(kVecs * kTileRows % 32 == 0, "vectors per lane");
+    const int lane = threadIdx.x & 31;
+    const uint32_t band = t % g.tbands, chunk = t / g.tbands;
+    size_t at[kPer];
+    uint4 vv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int v = lane + 32 * k;
+      const uint32_t r = v / kVecs, q = v % kVecs;
+      at[k] = (size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kTileCols + q * kVecCells;
+      vv[k] = *reinterpret_cast<const uint4*>(src + at[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      uint4 v = vv[k];
+      const size_t i = at[k];
+#else
     tile_rows_foreach<CB>(g, t % g.tbands, t / g.tbands, [&](size_t i) {
       uint4 v = *reinterpret_cast<const uint4*>(src + i);
+#endif
       if (lag) {
         v.x = add_lag<CB>(v.x, lagw);
         v.y = add_lag<CB>(v.y, lagw);
@@ -1322,7 +1348,11 @@ __global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, 
         for (int k = 0; k < 4; ++k) z |= CB == 16 ? ((w[k] & 0xFFFFu) == 0u || (w[k] >> 16) == 0u) : w[k] == 0u;
       }
       if (move) *reinterpret_cast<uint4*>(out + i) = v;
+#if AM_FIN_BATCH
+    }
+#else
     });
+#endif
     if (zero && __any_sync(0xffffffffu, z) && (threadIdx.x & 31) == 0) atomicOr(zero, 1u);
   }
   __syncwarp();
