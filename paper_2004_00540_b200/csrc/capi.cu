@@ -1103,10 +1103,12 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
   g->have_map = 0;
   const uint32_t nt = (uint32_t)g->g.ntiles();
   const uint32_t n = std::min<uint64_t>((uint64_t)items * 2, nt);
+  std::vector<uint8_t> tsrc(nt);
+  CK(cudaMemcpy(tsrc.data(), g->t_src, nt, cudaMemcpyDeviceToHost));
   std::vector<uint32_t> list(n);
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t t = (uint32_t)(((uint64_t)i * stride) % nt);
-    list[i] = (t % g->g.nbands) << 16 | (t / g->g.nbands);
+    list[i] = (t % g->g.tbands) << 16 | (t / g->g.tbands) | (tsrc[t] ? am::kListSrc : 0u);
   }
   cudaStream_t s = ctx->stream;
   // block 0 every launch: list[0] / count[0] stay, the pushes for block 1 are deduplicated away
