@@ -11,7 +11,6 @@
 #include "am_internal.cuh"
 
 namespace am {
-constexpr int kFlagSlots = 64;
 constexpr int kLag = 2;        // blocks in flight before the host reads a fixed-point flag (dense)
 constexpr int kLagTiles = 24;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
@@ -53,7 +52,7 @@ struct am_grid {
   uint8_t* rowsrc = nullptr;         // per band and allocated row: a source in the band's columns (Geo::rowsrc_bytes)
   uint8_t* occ = nullptr;            // dense owned rows (re-initialisation / plain maps)
   uint8_t* srcmask_dense = nullptr;  // dense owned rows (plain maps)
-  uint32_t* d_flags = nullptr;       // kFlagSlots fixed-point slots + 1 CTA arrival counter (FlagSink::done)
+  uint32_t* d_flags = nullptr;       // kFlagWords: fixed-point slots, CTA arrival counter, neighbour receive rings
   am::FlagSet* fs = nullptr;         // host mirror + events of the slots (borrowed from the context)
   uint32_t* plain = nullptr;         // caller-uploaded dense map
   int plain_active = 0;
@@ -136,6 +135,14 @@ struct Transport {
   virtual am_status exchange_tiles() = 0;
   // make the per-slab device word *w (one per local slab) global: min or max over all slabs
   virtual am_status reduce(std::vector<uint32_t*>& words, bool take_max) = 0;
+  // The per-block fixed-point words travel with the halo rows instead of an
+  // all-reduce per block: exchange() / exchange_tiles() also send every slab's
+  // kFlagSlots slot words to both neighbours and fold the neighbours' words in
+  // (d_flags receive rings + launch_flags_merge), one hop per exchange, so a
+  // block's word is the minimum over all slabs after span() - 1 further
+  // exchanges.  exchange_flags() is such an exchange without the rows.
+  virtual uint32_t span() const = 0;  // slabs in the chain
+  virtual am_status exchange_flags() = 0;
   // local values must still be combined on the host (in-process groups)
   virtual bool host_combine() const = 0;
   // a one-slab-per-process transport whose slab has a neighbour below it

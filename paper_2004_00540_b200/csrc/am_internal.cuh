@@ -57,6 +57,15 @@ constexpr int kTileCols = 32 * kTileWPL - 2 * kK;  // useful columns of a tile b
 #endif
 constexpr int kTileCtasPerSm = AM_TILE_CTAS;  // k_block_tiles is persistent: this many CTAs per SM
 
+// Fixed-point word slots per grid (a ring the host reads lagged).  A grid's
+// d_flags holds the slots, the CTA arrival counter (FlagSink::done), and two
+// receive rings for the neighbours' slots (row slabs: the words travel with the
+// halo rows, see Transport in am_host.hpp).
+constexpr int kFlagSlots = 64;
+constexpr int kFlagRecvUp = kFlagSlots + 1;
+constexpr int kFlagRecvDn = 2 * kFlagSlots + 1;
+constexpr int kFlagWords = 3 * kFlagSlots + 1;
+
 struct Geo {
   uint32_t W, H;          // grid extent (cells)
   uint32_t pad;           // = kK: rows above / cols left of the grid
@@ -139,6 +148,8 @@ void launch_block_tiles(const Geo& g, int cell_bits, int ctas, void* f0, void* f
                         FlagSink prev, bool pdl, cudaStream_t s);
 // publishes a word the way the last CTA of a blocked launch would (FlagSink)
 void launch_publish_flag(FlagSink f, cudaStream_t s);
+// slots[k] = min(slots[k], received from above[k], received from below[k]) for every slot
+void launch_flags_merge(uint32_t* d_flags, cudaStream_t s);
 // zero (nullable): also ORs 1 into *zero if a free cell is still uncovered (fused k_zero_check)
 void launch_tiles_finalize(const Geo& g, int cell_bits, unsigned long long* state, void* f0, void* f1, int dst,
                            uint32_t l, uint32_t* zero, cudaStream_t s);

@@ -207,7 +207,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = am::dmalloc(ctx, &g->rowsrc, g->g.rowsrc_bytes());
   if (!e) e = am::dmalloc(ctx, &g->occ, dense);
   if (!e) e = am::dmalloc(ctx, &g->srcmask_dense, dense);
-  if (!e) e = am::dmalloc(ctx, &g->d_flags, (kFlagSlots + 1) * sizeof(uint32_t));
+  if (!e) e = am::dmalloc(ctx, &g->d_flags, kFlagWords * sizeof(uint32_t));
   if (!e) e = take_flag_set(ctx, &g->fs);
   {  // active-tile skipping state
     const size_t nt = g->g.ntiles();
@@ -227,6 +227,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = cudaMemsetAsync(g->rowsrc, 0, g->g.rowsrc_bytes(), s);
   if (!e) e = cudaMemsetAsync(g->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), s);  // armed slots
   if (!e) e = cudaMemsetAsync(g->d_flags + kFlagSlots, 0, sizeof(uint32_t), s);     // arrival counter
+  if (!e) e = cudaMemsetAsync(g->d_flags + kFlagRecvUp, 0xFF, 2 * kFlagSlots * sizeof(uint32_t), s);  // no neighbour
   if (!e) e = cudaMemsetAsync(g->srcmask_dense, 0, dense, s);
   if (!e)
     e = cudaMemcpyAsync(g->occ, occ_full + (size_t)row0 * W, dense,
@@ -498,10 +499,46 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   const int K = kK;
   std::vector<uint32_t*> words(slabs.size());
 
+  // Row slabs: a block's word is global once span - 1 exchanges have carried it (Transport); until then
+  // the block waits here, then its word is copied to the host and it joins `pend`.
+  const bool diffuse = autom && tr != nullptr;
+  const uint32_t hops = diffuse ? tr->span() - 1 : 0;
+  struct Awaiting {
+    PendingBlock b;
+    uint32_t done;  // exchanges since the block
+  };
+  std::deque<Awaiting> awaiting;
+  auto copy_out = [&](const PendingBlock& b) -> am_status {
+    for (auto& sr : slabs) {
+      am_ctx* c = sr.ctx;
+      if (b.polled) continue;  // the kernel writes the mapped slot itself
+      cudaError_t e = cudaMemcpyAsync(sr.g->fs->h + b.slot, sr.g->d_flags + b.slot, sizeof(uint32_t),
+                                      cudaMemcpyDeviceToHost, c->stream);
+      if (!e) e = cudaEventRecord(sr.g->fs->ev[b.slot], c->stream);
+      if (e) return fail(c, AM_ECUDA, "flag copy: %s", cudaGetErrorString(e));
+    }
+    pend.push_back(b);
+    return AM_OK;
+  };
+  auto after_exchange = [&]() -> am_status {
+    for (auto& a : awaiting) ++a.done;
+    while (!awaiting.empty() && awaiting.front().done >= hops) {
+      if (am_status s2 = copy_out(awaiting.front().b)) return s2;
+      awaiting.pop_front();
+    }
+    return AM_OK;
+  };
+  auto flush_flags = [&]() -> am_status {  // flag-only exchanges until every launched block's word is global
+    while (!awaiting.empty()) {
+      if (am_status s2 = tr->exchange_flags()) return s2;
+      if (am_status s2 = after_exchange()) return s2;
+    }
+    return AM_OK;
+  };
   auto drain_one = [&]() -> am_status {
     PendingBlock b = pend.front();
     pend.pop_front();
-    uint32_t m = 0xFFFFFFFFu;
+    uint32_t m = 0xFFFFFFFFu, mx = 0u;
     for (auto& s : slabs) {
       am_ctx* c = s.ctx;
       volatile uint32_t* h = s.g->fs->h + b.slot;
@@ -518,7 +555,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         if (e) return fail(c, AM_ECUDA, "flag event: %s", cudaGetErrorString(e));
       }
       m = std::min(m, (uint32_t)*h);
+      mx = std::max(mx, (uint32_t)*h);
     }
+    if (diffuse && m != mx) return fail(ctx, AM_EINTERNAL, "slab fixed-point words disagree after %u exchanges", hops);
     if (!lprime) {
       const uint32_t t = block_termination(b, m);
       if (t) lprime = t;
@@ -533,6 +572,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     if ((!blocked || promoting) && (st = close_run())) return st;
     if ((!blocked || promoting || !tiles) && (st = publish_pending())) return st;
     if (promoting) {
+      if (diffuse && (st = flush_flags())) return st;
       while (!pend.empty() && !lprime)
         if ((st = drain_one())) return st;
       pend.clear();
@@ -552,13 +592,15 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
         CKL();
       }
       if (tr && (st = tr->exchange_tiles())) return st;  // (a lone slab has no neighbours: halos stay padding)
+      if (diffuse && (st = after_exchange())) return st;
       for (auto& sr : slabs) {  // boundary tiles the received frontier reaches
         am_grid* g = sr.g;
         launch_tiles_halo_scan(g->g, g->cell_bits, g->val[0], g->book(), g->t_blk, sr.ctx->stream);
         CKL();
       }
-    } else if (tr && (st = tr->exchange())) {  // dense blocks / single layers (tiles gathered into val[0])
-      return st;
+    } else if (tr) {  // dense blocks / single layers (tiles gathered into val[0])
+      if ((st = tr->exchange())) return st;
+      if (diffuse && (st = after_exchange())) return st;
     }
     const int slot = (int)(nblock % kFlagSlots);
     for (size_t i = 0; i < slabs.size(); ++i) {
@@ -614,16 +656,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     }
     if (tiles && !blocked && (st = tiles_all_active(l + kk))) return st;
     if (autom) {
-      if (tr && (st = tr->reduce(words, false))) return st;
-      for (auto& sr : slabs) {
-        am_ctx* c = sr.ctx;
-        if (mapped && blocked) continue;  // polled
-        cudaError_t e = cudaMemcpyAsync(sr.g->fs->h + slot, sr.g->d_flags + slot, sizeof(uint32_t),
-                                        cudaMemcpyDeviceToHost, c->stream);
-        if (!e) e = cudaEventRecord(sr.g->fs->ev[slot], c->stream);
-        if (e) return fail(c, AM_ECUDA, "flag copy: %s", cudaGetErrorString(e));
-      }
-      pend.push_back(PendingBlock{slot, l, kk, slabs[0].g->cell_bits, mapped && blocked});
+      const PendingBlock pb{slot, l, kk, slabs[0].g->cell_bits, mapped && blocked};
+      if (hops) awaiting.push_back(Awaiting{pb, 0});
+      else if ((st = copy_out(pb))) return st;
     }
     l += kk;
     ++nblock;
@@ -640,6 +675,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   }
   if ((st = close_run())) return st;
   if ((st = publish_pending())) return st;
+  if (diffuse && (st = flush_flags())) return st;
   while (!pend.empty())
     if ((st = drain_one())) return st;
   const int zslot = (int)(nblock % kFlagSlots);

@@ -95,6 +95,26 @@ struct NcclTransport final : Transport {
   am_ctx* ctx;
   am_grid* g;
   NcclTransport(am_ctx* c, am_grid* gg) : ctx(c), g(gg) {}
+  // the slot words to / from both neighbours (inside the caller's group), then folded in
+  am_status flags_p2p() {
+    Comm* cm = ctx->comm;
+    const size_t n = kFlagSlots;
+    if (cm->rank > 0) {
+      NK(nccl().send(g->d_flags, n, ncclUint32, (int)cm->rank - 1, cm->comm, ctx->stream));
+      NK(nccl().recv(g->d_flags + kFlagRecvUp, n, ncclUint32, (int)cm->rank - 1, cm->comm, ctx->stream));
+    }
+    if (cm->rank + 1 < cm->nranks) {
+      NK(nccl().send(g->d_flags, n, ncclUint32, (int)cm->rank + 1, cm->comm, ctx->stream));
+      NK(nccl().recv(g->d_flags + kFlagRecvDn, n, ncclUint32, (int)cm->rank + 1, cm->comm, ctx->stream));
+    }
+    return AM_OK;
+  }
+  am_status merge() {
+    launch_flags_merge(g->d_flags, ctx->stream);
+    ++ctx->launches;
+    if (cudaError_t e = cudaPeekAtLastError()) return fail(ctx, AM_ECUDA, "flags merge: %s", cudaGetErrorString(e));
+    return AM_OK;
+  }
   am_status exchange() override {
     Comm* cm = ctx->comm;
     const size_t bytes = (size_t)kK * row_bytes(g);
@@ -108,9 +128,17 @@ struct NcclTransport final : Transport {
       NK(nccl().send(alloc_rows(g, H), bytes, ncclUint8, (int)cm->rank + 1, cm->comm, ctx->stream));
       NK(nccl().recv(alloc_rows(g, kK + H), bytes, ncclUint8, (int)cm->rank + 1, cm->comm, ctx->stream));
     }
+    if (am_status st = flags_p2p()) return st;
     NK(nccl().groupEnd());
-    return AM_OK;
+    return merge();
   }
+  am_status exchange_flags() override {
+    NK(nccl().groupStart());
+    if (am_status st = flags_p2p()) return st;
+    NK(nccl().groupEnd());
+    return merge();
+  }
+  uint32_t span() const override { return ctx->comm->nranks; }
   am_status exchange_tiles() override {
     Comm* cm = ctx->comm;
     const size_t bytes = (size_t)kK * row_bytes(g);
@@ -127,8 +155,9 @@ struct NcclTransport final : Transport {
       NK(nccl().recv(f0 + (size_t)(kK + H) * row_bytes(g), bytes, ncclUint8, (int)cm->rank + 1, cm->comm,
                      ctx->stream));
     }
+    if (am_status st = flags_p2p()) return st;
     NK(nccl().groupEnd());
-    return AM_OK;
+    return merge();
   }
   am_status reduce(std::vector<uint32_t*>& words, bool take_max) override {
     NK(nccl().allReduce(words[0], words[0], 1, ncclUint32, take_max ? ncclMax : ncclMin, ctx->comm->comm,
@@ -149,6 +178,26 @@ struct LocalTransport final : Transport {
   am_ctx* ctx;
   std::vector<SlabRef>& s;
   LocalTransport(am_ctx* c, std::vector<SlabRef>& v) : ctx(c), s(v) {}
+  // every slab's slot words into its neighbours' receive rings (all copies before any merge, as
+  // the NCCL exchange delivers them), then each slab folds them in
+  am_status flags() {
+    const size_t bytes = kFlagSlots * sizeof(uint32_t);
+    for (size_t i = 0; i < s.size(); ++i) {
+      if (i > 0) CK(cudaMemcpyAsync(s[i].g->d_flags + kFlagRecvUp, s[i - 1].g->d_flags, bytes, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+      if (i + 1 < s.size())
+        CK(cudaMemcpyAsync(s[i].g->d_flags + kFlagRecvDn, s[i + 1].g->d_flags, bytes, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+    }
+    for (size_t i = 0; i < s.size(); ++i) {
+      launch_flags_merge(s[i].g->d_flags, ctx->stream);
+      ++ctx->launches;
+    }
+    CK(cudaPeekAtLastError());
+    return AM_OK;
+  }
+  am_status exchange_flags() override { return flags(); }
+  uint32_t span() const override { return (uint32_t)s.size(); }
   am_status exchange() override {
     for (size_t i = 0; i < s.size(); ++i) {
       am_grid* g = s[i].g;
@@ -163,7 +212,7 @@ struct LocalTransport final : Transport {
                            ctx->stream));
       }
     }
-    return AM_OK;
+    return flags();
   }
   am_status exchange_tiles() override {
     for (size_t i = 0; i < s.size(); ++i) {
@@ -177,7 +226,7 @@ struct LocalTransport final : Transport {
         CK(cudaMemcpyAsync(f0 + (size_t)(kK + g->g.H) * row_bytes(g), s[i + 1].g->t_bnd, bytes,
                            cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    return AM_OK;
+    return flags();
   }
   am_status reduce(std::vector<uint32_t*>&, bool) override { return AM_OK; }
   bool host_combine() const override { return true; }

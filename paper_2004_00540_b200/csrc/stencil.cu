@@ -1640,6 +1640,13 @@ __global__ void k_tile_src(Geo g, const uint8_t* __restrict__ rowsrc, uint8_t* _
   tsrc[t] = any ? 1 : 0;
 }
 
+__global__ void k_flags_merge(uint32_t* __restrict__ f) {
+  const int k = threadIdx.x;
+  if (k < kFlagSlots) f[k] = min(f[k], min(f[kFlagRecvUp + k], f[kFlagRecvDn + k]));
+}
+
+void launch_flags_merge(uint32_t* d_flags, cudaStream_t s) { k_flags_merge<<<1, kFlagSlots, 0, s>>>(d_flags); }
+
 void launch_tile_src(const Geo& g, const uint8_t* rowsrc, uint8_t* tsrc, cudaStream_t s) {
   const uint32_t n = g.ntiles();
   if (n) k_tile_src<<<(n + 255) / 256, 256, 0, s>>>(g, rowsrc, tsrc);
