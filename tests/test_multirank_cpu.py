@@ -2,8 +2,10 @@
 
 Mirrors the device driver (capi.cu drive_propagation + multigpu.cu
 NcclTransport) with the oracle as the per-slab compute: K-row halo
-send/recv between neighbouring ranks before every block, per-block minimum
-covered activity all-reduced with MIN, termination from that number,
+send/recv between neighbouring ranks before every block, carrying the ring of
+per-block minimum covered activities (merged with MIN on receipt: a block's
+word is global after world-1 exchanges, checked against an all-reduce),
+termination from those words, flag-only exchanges to flush the last blocks,
 filled/stalled from an all-reduced zero check, exact rollback of the
 overshoot.  The assembled map must equal the single-process oracle."""
 import os
@@ -61,37 +63,78 @@ def worker(rank, world, port, occ, src, cap, out_path):
     A = np.zeros((Hl + 2 * K, W), np.uint32)
     A[K:K + Hl] = O.initial(occ[f:l], sm_full[f:l])
 
-    def exchange():
+    NS = 64  # kFlagSlots
+    slots = np.full(NS, 0xFFFFFFFF, np.int64)
+    hops = world - 1
+    awaiting = []  # [slot, start, count, exchanges so far, all-reduced word (check)]
+    ready = []
+
+    def exchange(rows=True):
+        nonlocal slots
         reqs = []
         up_recv = torch.zeros((K, W), dtype=torch.int64)
         dn_recv = torch.zeros((K, W), dtype=torch.int64)
+        up_s = torch.full((NS,), 0xFFFFFFFF, dtype=torch.int64)
+        dn_s = torch.full((NS,), 0xFFFFFFFF, dtype=torch.int64)
+        mine = torch.from_numpy(slots.copy())
         if rank > 0:
-            reqs.append(dist.isend(torch.from_numpy(A[K:2 * K].astype(np.int64)), rank - 1))
-            reqs.append(dist.irecv(up_recv, rank - 1))
+            if rows:
+                reqs.append(dist.isend(torch.from_numpy(A[K:2 * K].astype(np.int64)), rank - 1))
+                reqs.append(dist.irecv(up_recv, rank - 1))
+            reqs.append(dist.isend(mine, rank - 1))
+            reqs.append(dist.irecv(up_s, rank - 1))
         if rank + 1 < world:
-            reqs.append(dist.isend(torch.from_numpy(A[Hl:Hl + K].astype(np.int64)), rank + 1))
-            reqs.append(dist.irecv(dn_recv, rank + 1))
+            if rows:
+                reqs.append(dist.isend(torch.from_numpy(A[Hl:Hl + K].astype(np.int64)), rank + 1))
+                reqs.append(dist.irecv(dn_recv, rank + 1))
+            reqs.append(dist.isend(mine, rank + 1))
+            reqs.append(dist.irecv(dn_s, rank + 1))
         for q in reqs:
             q.wait()
-        if rank > 0:
+        if rows and rank > 0:
             A[0:K] = up_recv.numpy().astype(np.uint32)
-        if rank + 1 < world:
+        if rows and rank + 1 < world:
             A[K + Hl:] = dn_recv.numpy().astype(np.uint32)
+        slots = np.minimum(slots, np.minimum(up_s.numpy(), dn_s.numpy()))  # launch_flags_merge
+        for a in awaiting:
+            a[3] += 1
+        while awaiting and awaiting[0][3] >= hops:
+            sl, start, count, _, check = awaiting.pop(0)
+            assert slots[sl] == check, "the word is global after world-1 exchanges"
+            ready.append((start, count, int(slots[sl])))
 
-    done, lprime = 0, 0
+    done, lprime, nblock = 0, 0, 0
+
+    def consume():
+        nonlocal lprime
+        while ready:
+            start, count, m = ready.pop(0)
+            t = termination(start, count, m)
+            if t and not lprime:
+                lprime = t
+
     while done < cap and not lprime:
         kk = K if cap - done >= K else 1
         exchange()
+        consume()
         for _ in range(kk):
             A = O.propagate_layer(ext_occ, ext_sm, A)
         own = A[K:K + Hl]
         cov = own[own > 0]
-        m = torch.tensor([int(cov.min()) - 1 if cov.size else 0xFFFFFFFF], dtype=torch.int64)
-        dist.all_reduce(m, op=dist.ReduceOp.MIN)
-        t = termination(done, kk, int(m.item()))
+        m = int(cov.min()) - 1 if cov.size else 0xFFFFFFFF
+        sl = nblock % NS
+        slots[sl] = m  # re-armed slot + this block's local minimum
+        check = torch.tensor([m], dtype=torch.int64)
+        dist.all_reduce(check, op=dist.ReduceOp.MIN)  # test-only reference value
+        awaiting.append([sl, done, kk, 0, int(check.item())])
+        if hops == 0:
+            exchange(rows=False)
         done += kk
-        if t:
-            lprime = t
+        nblock += 1
+        consume()
+    while awaiting:  # flush: flag-only exchanges
+        exchange(rows=False)
+    consume()
     own = A[K:K + Hl].copy()
     z = torch.tensor([int(((own == 0) & (occ[f:l] == 0)).any())], dtype=torch.int64)
     dist.all_reduce(z, op=dist.ReduceOp.MAX)
