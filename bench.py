@@ -94,14 +94,16 @@ class ClockSampler:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
-    def stop(self):
+    def stop(self, window=None):
+        """Median SM clock and throttle reasons of the samples taken inside `window` (wall-clock (t0, t1) of
+        the timed region; the sampler starts before the warm-up so nvidia-smi is polling by then)."""
         if not self.p:
             return None
         self.p.terminate()
@@ -110,24 +112,30 @@ class ClockSampler:
         except Exception:
             self.p.kill()
         self.f.close()
-        sm, mx, reasons = [], 0, set()
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         with open(self.path) as f:
             for line in f:
                 parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 7:
+                if len(parts) < 8:
                     continue
                 try:
-                    sm.append(float(parts[0]))
-                    mx = max(mx, float(parts[1]))
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((ts, float(parts[1]), float(parts[2]), parts[4:8]))
                 except ValueError:
                     continue
-                for n, v in zip(names, parts[3:7]):
-                    if v.lower().startswith("active"):
-                        reasons.add(n)
-        if not sm:
+        inside = [r for r in rows if window is None or window[0] <= r[0] <= window[1]]
+        scope = "timed region"
+        if not inside and rows and window is not None:  # region shorter than the polling interval
+            mid = 0.5 * (window[0] + window[1])
+            inside = [min(rows, key=lambda r: abs(r[0] - mid))]
+            scope = "nearest sample to the timed region"
+        if not inside:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted({n for r in inside for n, v in zip(names, r[3]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": reasons, "samples": len(inside), "scope": scope}
 
 
 def cpu_baseline(occ, src, budget_s=12.0):
@@ -333,6 +341,7 @@ def run_b200(args, rank, world, local_rank):
     sol = Solver(am, torch, ctx, occ, src, tgt, rank, world, local_rank)
     stream = sol.stream
 
+    clocks = ClockSampler(local_rank) if rank == 0 else None  # polling well before the timed region
     for _ in range(args.warmup):
         sol.step()
     ctx.synchronize()
@@ -347,12 +356,12 @@ def run_b200(args, rank, world, local_rank):
     prop_ms, path_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
 
     launches0 = ctx.kernel_launches()
-    clocks = ClockSampler(local_rank) if rank == 0 else None
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ctx.synchronize()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
     t_start.record(stream)
     stencil_ms, blocks, res, tiles_done, tiles_all = 0.0, 0, None, 0, 0
     for _ in range(args.steps):
@@ -367,8 +376,9 @@ def run_b200(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     ms_total = t_start.elapsed_time(t_end)
+    wall1 = time.time()
     launches = ctx.kernel_launches() - launches0
-    clk = clocks.stop() if clocks else None
+    clk = clocks.stop((wall0, wall1)) if clocks else None
     if dist:
         t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
