@@ -56,6 +56,10 @@ constexpr int kTileCols = 32 * kTileWPL - 2 * kK;  // useful columns of a tile b
 #define AM_TILE_CTAS 3  // 4 warps x 12 KB staged tiles each, <= 168 registers
 #endif
 constexpr int kTileCtasPerSm = AM_TILE_CTAS;  // k_block_tiles is persistent: this many CTAs per SM
+#ifndef AM_TILE_THREADS
+#define AM_TILE_THREADS 128
+#endif
+constexpr int kTileThreads = AM_TILE_THREADS;  // threads per k_block_tiles CTA (one item per warp)
 
 // Fixed-point word slots per grid (a ring the host reads lagged).  A grid's
 // d_flags holds the slots, the CTA arrival counter (FlagSink::done), and two

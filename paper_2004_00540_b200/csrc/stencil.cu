@@ -585,7 +585,7 @@ constexpr int kPairSlots = kTileRows;                   // ring slots
 constexpr int kPairBufBytes = kPairSlots * kPairRowBytes;  // 16 KB
 constexpr int kTileWarpSmem0 = kTileBufBytes > kTileWarpSmemRing ? kTileBufBytes : kTileWarpSmemRing;
 constexpr int kTileWarpSmem = AM_PAIRS && kPairBufBytes > kTileWarpSmem0 ? kPairBufBytes : kTileWarpSmem0;
-constexpr int kTileSmem = kWarpsPerCta * kTileWarpSmem;  // dynamic shared memory of k_block_tiles
+constexpr int kTileSmem = kTileThreads / 32 * kTileWarpSmem;  // dynamic shared memory of k_block_tiles
 
 enum { kOutNone = 0, kOutTop = 1, kOutBot = 2, kOutMid = 3 };  // kOutMid: outputs feed acc only
 
@@ -993,7 +993,7 @@ __device__ __forceinline__ void push_tiles(const Geo& g, TileBook& book, uint32_
 // and the neighbours its frontier (cells covered in the block's last layer)
 // can reach within kK cells.
 template <int CB>
-__global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
+__global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
                   const uint8_t* __restrict__ rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
                   FlagSink prev) {
@@ -1053,7 +1053,7 @@ __global__ void __launch_bounds__(kBlockThreads, kTileCtasPerSm)
            (el == 0u ? 0xA0u : 0u) | (er == 0u ? 0x140u : 0u);
   };
   // light blocks (at most half a warp slot per tile): two quarter items per tile, shorter latency
-  const uint32_t nwarps = gridDim.x * (kBlockThreads / 32);
+  const uint32_t nwarps = gridDim.x * (kTileThreads / 32);
   const bool quarters = CB == 16 && AM_QUARTERS && 2u * n <= (uint32_t)AM_QUARTER_SLOTS * nwarps;
   // heavy blocks (more tiles than warps): two whole tiles per item (tile_pair16)
   const bool pairs = CB == 16 && AM_PAIRS && !quarters && 4u * n > (uint32_t)AM_PAIR_MIN4 * nwarps;
@@ -1703,7 +1703,7 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
     // programmatic stream serialization: the launch overlaps the previous block's tail (griddepcontrol.wait)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctas);
-    cfg.blockDim = dim3(kBlockThreads);
+    cfg.blockDim = dim3(kTileThreads);
     cfg.dynamicSmemBytes = kTileSmem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -1715,7 +1715,7 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
                        flag, prev);
   } else {
     auto* a = (uint32_t*)f0;
-    k_block_tiles<32><<<ctas, kBlockThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
+    k_block_tiles<32><<<ctas, kTileThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
                                                               flag, prev);
   }
 }
