@@ -157,6 +157,9 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
 // reference enumerations: row-major for the simple rule (pin P2), axis order
 // L,R,U,D then the diagonals for the Euclidean rule (pin P1).  Points are
 // gathered 32 at a time and written by the whole warp.
+#ifndef AM_TRACE_LAW
+#define AM_TRACE_LAW 1
+#endif
 #ifndef AM_TWR
 #define AM_TWR 32  // 16-bit window rows
 #endif
@@ -220,6 +223,25 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
     const uint32_t v = lane < 8 ? (uint32_t)win[((int)r - wr + dr) * WC + ((int)c - wc + dc)] : 0u;
     int sel = -1;
     uint32_t best;
+#if AM_TRACE_LAW
+    // Maps from the device propagation obey the law (8-adjacent free cells differ by <= 1, every
+    // ascent is exactly +1), so the maxima the rules look for are exactly the cells at cur + 1:
+    // one vote per step, no max-reduction on the dependent chain.
+    best = cur + 1u;
+    if (method == 0) {  // simple: the row-major candidates at cur + 1, seeded tie-break (pin P2)
+      uint32_t mask = __ballot_sync(0xffffffffu, lane < 8 && v == best);
+      if (mask) {
+        const int cnt = __popc(mask);
+        int pick = 0;
+        if (cnt >= 2) pick = (int)__umul64hi(splitmix64(rng), (uint64_t)cnt);
+        for (int k = 0; k < pick; ++k) mask &= mask - 1;
+        sel = __ffs(mask) - 1;
+      }
+    } else {  // Euclidean: first of L,R,U,D at cur + 1, else the first diagonal (pin P1)
+      const uint32_t mask = __ballot_sync(0xffffffffu, lane < 8 && v == best);
+      sel = (mask & 0xFu) ? __ffs(mask & 0xFu) - 1 : (mask ? __ffs(mask) - 1 : -1);
+    }
+#else
     if (method == 0) {  // simple: 8-neighbour argmax, seeded tie-break (pin P2)
       best = __reduce_max_sync(0xffffffffu, v);
       uint32_t mask = __ballot_sync(0xffffffffu, lane < 8 && v == best);
@@ -239,6 +261,7 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
         if (best > cur) sel = __ffs(__ballot_sync(0xffffffffu, lane >= 4 && lane < 8 && v == best)) - 1;
       }
     }
+#endif
     if (sel < 0) {
       *st = ST_EINTERNAL;  // no ascending neighbour
       return 0;
