@@ -278,6 +278,103 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
   return n;
 }
 
+// Euclidean walk, two steps per iteration (law-abiding device maps, see walk_smem):
+// lanes 0-24 read the 5x5 cells around the current cell, one ballot marks the
+// cells at cur + 1 and one the cells at cur + 2; the first step is the first
+// of L, R, U, D (else of the diagonals) at cur + 1, the second the same rule
+// among the chosen cell's neighbours at cur + 2 -- both decided from the two
+// masks, so two steps cost one shared-memory read and two votes.
+#ifndef AM_TRACE_2STEP
+#define AM_TRACE_2STEP 1
+#endif
+// first set bit of m among lanes base + {-1, +1, -5, +5} (L, R, U, D), else base + {-6, -4, +4, +6}
+__device__ __forceinline__ int eucl_pick5(uint32_t m, int base) {
+  const int ax[4] = {-1, 1, -5, 5}, dg[4] = {-6, -4, 4, 6};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((m >> (base + ax[k])) & 1u) return base + ax[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((m >> (base + dg[k])) & 1u) return base + dg[k];
+  return -1;
+}
+
+template <typename T, int WR, int WC>
+__device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_t limit, uint32_t* out, int32_t* st,
+                               T* win) {
+  static_assert(WR * WC * sizeof(T) <= kWinBytes && WR % 32 == 0, "window");
+  constexpr int kVec = 16 / sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const MapView& m = rd.m;
+  const int pad = (int)m.g.pad, pitch = (int)m.g.pitch;
+  const int rmax = (int)m.g.rows - pad - WR;
+  const T* field = static_cast<const T*>(m.val);
+  const uint32_t flag = sizeof(T) == 2 ? kFlag16 : kFlag32;
+  const uint32_t top = flag | (m.layers + 1);  // raw value of a source
+  const int dr = lane / 5 - 2, dc = lane % 5 - 2;  // this lane's cell of the 5x5 (lanes < 25)
+  int wr = 0, wc = 0;
+  bool loaded = false;
+  auto stage = [&]() {
+    wr = min(max((int)r - WR / 2, -pad), rmax);
+    const int ac = min(max(((int)c + pad - WC / 2) & ~(kVec - 1), 0), pitch - WC);
+    wc = ac - pad;
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < WR / 32; ++h) {
+      const int row = lane + 32 * h;
+      const uint4* p = reinterpret_cast<const uint4*>(field + (size_t)(wr + row + pad) * pitch + ac);
+      uint4* o = reinterpret_cast<uint4*>(win + row * WC);
+#pragma unroll
+      for (int q = 0; q < WC / kVec; ++q) o[q] = p[q];
+    }
+    __syncwarp();
+    loaded = true;
+  };
+  uint32_t cur = field[m.g.idx(r, c)];
+  uint64_t n = 0;
+  uint32_t keep_r = 0, keep_c = 0;
+  auto record = [&]() {
+    if ((int)(n & 31) == lane) keep_r = r, keep_c = c;
+    if ((n & 31) == 31) reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r, keep_c);
+    ++n;
+  };
+  record();
+  while (cur != top) {
+    if (n >= limit) {
+      *st = ST_EINTERNAL;
+      return 0;
+    }
+    const int pr = (int)r - wr, pc = (int)c - wc;
+    if (!loaded || pr < 2 || pr > WR - 3 || pc < 2 || pc > WC - 3) stage();
+    const uint32_t v = lane < 25 ? (uint32_t)win[((int)r - wr + dr) * WC + ((int)c - wc + dc)] : 0u;
+    const uint32_t m1 = __ballot_sync(0xffffffffu, lane < 25 && v == cur + 1u);
+    const uint32_t m2 = __ballot_sync(0xffffffffu, lane < 25 && v == cur + 2u);
+    const int s1 = eucl_pick5(m1, 12);
+    if (s1 < 0) {
+      *st = ST_EINTERNAL;  // no ascending neighbour
+      return 0;
+    }
+    r = (uint32_t)((int)r + s1 / 5 - 2);
+    c = (uint32_t)((int)c + s1 % 5 - 2);
+    cur += 1u;
+    record();
+    if (cur == top || n >= limit) continue;  // reached a source (or the count says so: checked above)
+    const int s2 = eucl_pick5(m2, s1);
+    if (s2 < 0) {
+      *st = ST_EINTERNAL;
+      return 0;
+    }
+    r = (uint32_t)((int)r + s2 / 5 - s1 / 5);
+    c = (uint32_t)((int)c + s2 % 5 - s1 % 5);
+    cur += 1u;
+    record();
+  }
+  const uint64_t base = n & ~(uint64_t)31;
+  if (base + lane < n) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(keep_r, keep_c);
+  if (!rd.source(r, c)) *st = ST_EINTERNAL;
+  return n;
+}
+
 // Encoded maps: closed-form count L+2-A(t).  Plain maps: a counting walk.
 __global__ void k_path_counts(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method,
                               uint64_t seed, uint64_t* __restrict__ counts, int32_t* __restrict__ status) {
@@ -312,7 +409,10 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
   int32_t st = ST_OK;
   __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
   uint8_t* win = wins[(threadIdx.x >> 5) & 3];
-  const uint64_t got = m.cell_bits == 16 ? walk_smem<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed,
+  const uint64_t got = AM_TRACE_2STEP && method == 1 && m.cell_bits == 16
+                           ? walk_eucl2<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], limit, pts + 2 * off,
+                                                                  &st, (uint16_t*)win)
+                       : m.cell_bits == 16 ? walk_smem<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed,
                                                                        limit, pts + 2 * off, &st, (uint16_t*)win)
                        : m.cell_bits == 32
                            ? walk_smem<uint32_t, 32, 32>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed, limit,
