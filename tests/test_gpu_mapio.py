@@ -150,6 +150,18 @@ def test_pgm_matches_oracle(w, h, layers):
     g.close()
 
 
+def test_pgm_large_map_matches_oracle():
+    """4096^2 maze, 64 sources, fixed point (16-bit samples): device export == oracle export of the downloaded map."""
+    occ = O.random_maze(4096, 4096, 0.35, 77)
+    src = O.sample_free_cells(occ, 64, 78)
+    g = am.Grid(occ, src)
+    r = g.propagate_auto(4 * 4096)
+    vals = g.activity()
+    assert int(vals.max()) == r.layers_used + 1 > 255
+    assert g.export_pgm() == M.export_pgm(vals)
+    g.close()
+
+
 def test_pgm_rounding_and_zero():
     v = np.array([[0, 1, 300, 599, 600, 2**31 - 1]], np.uint32)
     assert am.export_pgm(v) == M.export_pgm(v)
