@@ -917,6 +917,77 @@ __device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __res
   return acc;
 }
 
+// ---- very light blocks: eighth items (four warps per tile) ------------------
+//
+// When a block has at most a quarter warp slot per tile, each tile runs as
+// four items of 8 rows (part p: tile rows 8p .. 8p+7) whose u16 streams carry
+// 4 rows each: 4 + 2K = 20 steps.  Staged: the 24 rows 8p-8 .. 8p+15.  The lo
+// stream reads staged row s, the hi stream row s+4; every 4-step phase reads
+// one region (above / inside / below the tile) per stream, so a phase has one
+// lag word.  Items of tiles with a source in reach run as quarter items (parts
+// 0 and 2; parts 1 and 3 then do nothing).
+#ifndef AM_EIGHTHS
+#define AM_EIGHTHS 0  // 1: C2 -2%, C4 +0.9% (code growth in the heavy path)
+#endif
+constexpr int kEighthRows = 4;                          // rows per u16 stream
+constexpr int kEighthSteps = kEighthRows + 2 * kK;      // 20
+constexpr int kEighthStage = 2 * kEighthRows + 2 * kK;  // 24 rows staged
+static_assert(kEighthStage % 2 == 0 && kTileRows == 4 * 2 * kEighthRows, "eighth layout");
+
+__device__ __forceinline__ uint32_t tile_eighth16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta,
+                                                  uint32_t b, uint32_t c, uint32_t part, const uint32_t (&lw)[3],
+                                                  uint32_t homes, uint32_t* edge, uint8_t* buf) {
+  const int lane = threadIdx.x & 31;
+  const size_t pitch = g.pitch;
+  const int r0 = (int)part * 2 * kEighthRows;  // first tile row of the item
+  auto region = [](int trow) { return trow < 0 ? 0 : (trow < kTileRows ? 1 : 2); };
+  __syncwarp();  // every lane is done reading the previous item's rows
+  {
+    const uint32_t ch = __shfl_sync(0xffffffffu, homes, (2 * lane) & 31);
+    const uint32_t col = b * kTileCols + (lane & 15) * 8;
+    const uint16_t* base[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      base[r] = f0 + (((ch >> r) & 1u) ? delta : 0) + ((size_t)c * kTileRows + r0) * pitch + col;
+    uint8_t* dst = buf + (lane & 15) * 16;
+#pragma unroll
+    for (int k = 0; k < kEighthStage / 2; ++k) {
+      const int row = 2 * k + (lane >> 4);  // staged row = item row + kK
+      cp_async16(dst + row * kTileRowBytes, base[region(r0 + row - kK)] + (size_t)row * pitch);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  uint32_t P0[kK][4], P1[kK][4];
+  uint32_t acc = 0xFFFFFFFFu, accE = 0xFFFFFFFFu;
+  const ptrdiff_t od = ((homes >> 6) & 1u) ? delta : 0;
+  uint16_t* oA = f0 + od + ((size_t)c * kTileRows + r0 + kK) * pitch + b * kTileCols + lane * kTileWPL;
+  uint16_t* oB = oA + (size_t)kEighthRows * pitch;
+  const bool st = lane >= kK / kTileWPL && lane < 32 - kK / kTileWPL;
+  const uint8_t* rb = buf + lane * 8;
+  // phase q (steps 4q .. 4q+3): lo reads tile rows r0-8+4q.., hi rows r0-4+4q..
+  uint32_t lag[5];
+  bool lg[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    lag[q] = lw[region(r0 - kK + 4 * q)] | lw[region(r0 - kK + kEighthRows + 4 * q)] << 16;
+    lg[q] = __any_sync(0xffffffffu, lag[q] != 0u);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  fill_pair<0, kEighthRows>(rb, lag[0], lg[0], P0, P1);
+  fill_pair<1, kEighthRows>(rb, lag[0], lg[0], P0, P1);
+  fill_pair<2, kEighthRows>(rb, lag[1], lg[1], P0, P1);
+  fill_pair<3, kEighthRows>(rb, lag[1], lg[1], P0, P1);
+  fill_pair<4, kEighthRows>(rb, lag[2], lg[2], P0, P1);
+  fill_pair<5, kEighthRows>(rb, lag[2], lg[2], P0, P1);
+  fill_pair<6, kEighthRows>(rb, lag[3], lg[3], P0, P1);
+  fill_pair<7, kEighthRows>(rb, lag[3], lg[3], P0, P1);
+  tile_phase<kOutTop, kEighthRows>(rb, 2 * kK, kEighthSteps, lag[4], lg[4], P0, P1, oA, oB, pitch, st, acc, accE);
+  if (!st) acc = accE = 0xFFFFFFFFu;  // halo lanes hold no output
+  edge[0] = edge[1] = accE;
+  return acc;
+}
+
 // Quarter items next to a source: the general path on two 8-row streams (rows r0.. and r0+8..).
 __device__ __noinline__ uint32_t tile_item16_sources8(const Geo& g, uint16_t* f0, const uint8_t* srcmask,
                                                       const uint8_t* rf, uint32_t b, uint32_t r0, uint32_t lag0,
@@ -1055,9 +1126,10 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
   // light blocks (at most half a warp slot per tile): two quarter items per tile, shorter latency
   const uint32_t nwarps = gridDim.x * (kTileThreads / 32);
   const bool quarters = CB == 16 && AM_QUARTERS && 2u * n <= (uint32_t)AM_QUARTER_SLOTS * nwarps;
+  const bool eighths = quarters && AM_EIGHTHS && 4u * n <= nwarps;  // four items per tile (tile_eighth16)
   // heavy blocks (more tiles than warps): two whole tiles per item (tile_pair16)
   const bool pairs = CB == 16 && AM_PAIRS && !quarters && 4u * n > (uint32_t)AM_PAIR_MIN4 * nwarps;
-  const uint32_t nitems = quarters ? 2u * n : (pairs ? (n + 1) / 2 : n);
+  const uint32_t nitems = eighths ? 4u * n : quarters ? 2u * n : (pairs ? (n + 1) / 2 : n);
 #if AM_STATIC_FIRST
   // Every warp's first item is static, spread over the CTAs (item i -> CTA i mod grid, so consecutive items
   // land on different SMs); only items past the warp count are fetched dynamically (a warp that finishes
@@ -1157,8 +1229,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
       solo = itB;
       fetch_next = itB == kNone;
     } else {
-      it = list[quarters ? w >> 1 : w];
-      half = quarters ? w & 1u : 0u;
+      it = list[eighths ? w >> 2 : (quarters ? w >> 1 : w)];
+      half = eighths ? (w & 3u) : (quarters ? w & 1u : 0u);  // eighths: the part (0-3)
     }
     const uint32_t bA = (it >> 16) & kListBand, cA = it & 0xFFFFu;
     const uint32_t tA = cA * g.tbands + bA;
@@ -1166,7 +1238,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
     const uint32_t ra = cA * kTileRows;
     uint32_t f = 0;  // source rows in reach (read only for tiles listed with kListSrc)
     if constexpr (CB == 16) {
-      if (!(it & kListSrc)) {
+      if (!(it & kListSrc) || eighths) {  // (eighths: the quarter fallback below reads its own rows)
       } else if (quarters) {
         f = rf[ra + half * kHalfRows + lane];  // the item's 32 staged rows
       } else {
@@ -1181,7 +1253,23 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
     const uint32_t out_home = (sa & 1u) ^ 1u;  // own rows go to the field that is not the tile's home
     uint32_t edge[2], acc;
     uint32_t m9;  // frontier regions (bits: any, top, bottom, left, right, tl, tr, bl, br)
-    if (CB == 16 && quarters) {
+    if (CB == 16 && eighths && !(it & kListSrc)) {
+      uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
+      acc = tile_eighth16(g, reinterpret_cast<uint16_t*>(f0), delta, bA, cA, half, lw,
+                          hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6, edge, buf);
+      // any / left / right from both streams; top (bottom) edge bits when the item holds tile rows 0-7 (24-31)
+      const uint32_t m2 = regions16q(acc, edge[0], 0) | regions16q(acc, edge[0], 1);
+      m9 = (m2 & 0x19u) | (half == 0 ? (m2 & 0x62u) : 0u) | (half == 3 ? (m2 & 0x184u) : 0u);
+      gmin = min(gmin, min(__reduce_min_sync(0xffffffffu, acc & 0xFFFFu), __reduce_min_sync(0xffffffffu, acc >> 16)));
+    } else if (CB == 16 && quarters) {
+      if (eighths) {  // a tile with a source in reach: quarter items (parts 0 and 2), parts 1 and 3 idle
+        if (half & 1u) {
+          w = fetch_next ? fetch() : w;
+          continue;
+        }
+        half >>= 1;
+        f = rf[ra + half * kHalfRows + lane];  // the quarter's 32 staged rows (the eighth read no flags)
+      }
       uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
       const uint32_t r0 = ra + half * kHalfRows;
       if (!__any_sync(0xffffffffu, f != 0u)) {
