@@ -190,3 +190,33 @@ def test_full_size_movingai_round_trip():
     back, _, _ = sc.download()
     assert np.array_equal(back, occ)
     sc.close()
+
+
+def test_c_abi_rejections():
+    """Capacity, format and handle checks of the text / PGM entry points (status codes, no crash)."""
+    import ctypes as C
+    L, ctx = am.lib(), am.default_context()
+    occ = np.zeros((3, 4), np.uint8)
+    n = C.c_uint64(0)
+    args = (ctx.handle, am.MOVINGAI, 4, 3, occ.ctypes.data_as(C.c_void_p), None, 0, None, 0)
+    assert L.am_emit_text(*args, None, 0, C.byref(n)) == am.OK and n.value == len(b"type octile\nheight 3\nwidth 4\nmap\n") + 15
+    small = np.empty(n.value - 1, np.uint8)
+    assert L.am_emit_text(*args, small.ctypes.data_as(C.c_void_p), n.value - 1, C.byref(n)) == am.EINVAL
+    assert L.am_emit_text(ctx.handle, 7, 4, 3, occ.ctypes.data_as(C.c_void_p), None, 0, None, 0, None, 0,
+                          C.byref(n)) == am.EINVAL
+    info, h = am._ParseInfo(), C.c_void_p()
+    assert L.am_scene_parse(ctx.handle, b"S.", 2, 9, C.byref(h), C.byref(info)) == am.EINVAL
+    v = np.array([[1, 2]], np.uint32)
+    assert L.am_export_pgm(ctx.handle, 2, 1, v.ctypes.data_as(C.c_void_p), None, 0, C.byref(n)) == am.OK
+    out = np.empty(n.value - 1, np.uint8)
+    assert L.am_export_pgm(ctx.handle, 2, 1, v.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p),
+                           n.value - 1, C.byref(n)) == am.EINVAL
+    g = am.Grid(occ, [(0, 0)])
+    assert L.am_activity_export_pgm(ctx.handle, g.handle, None, 0, C.byref(n)) == am.EINVAL  # no map yet
+    g.propagate(2)
+    assert g.export_pgm() == M.export_pgm(g.activity())
+    sc = am.Scene(b"S.\n.T\n")
+    with pytest.raises(am.InvalidInputError):
+        sc.grid(sources=[(0, 5)])  # out of bounds source
+    g.close()
+    sc.close()
