@@ -12,7 +12,10 @@
 
 namespace am {
 constexpr int kLag = 2;        // blocks in flight before the host reads a fixed-point flag (dense)
-constexpr int kLagTiles = 24;  // same, active-tile mode (< kFlagSlots)
+#ifndef AM_LAG_TILES
+#define AM_LAG_TILES 24
+#endif
+constexpr int kLagTiles = AM_LAG_TILES;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
 // Host side of a grid's fixed-point slots: pinned device-mapped mirror + one
 // event per slot.  Pinning and event creation are slow, so contexts recycle

@@ -1358,13 +1358,17 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
 
 // Covered cells (flag set, a > 0) are exactly the halves above the bare flag:
 // adds `lagw` (per-half lag) to them, leaving uncovered and obstacle cells.
+// Obstacle and padding cells are unflagged but keep junk low bits (the layer
+// step only clears their flag), so the test must include the flag: lag added
+// to junk would grow it across layers and runs until it carried into the flag
+// bit and turned a wall or padding cell into a covered one.
 template <int CB>
 __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
   if constexpr (CB == 16) {
-    // a half is covered iff its low 15 bits are nonzero: adding 0x7FFF then
-    // carries into bit 15 (never out of the half); PRMT replicates that bit
+    // a half's low 15 bits are nonzero iff adding 0x7FFF carries into bit 15
+    // (never out of the half); AND with w keeps flagged halves; PRMT replicates bit 15
     uint32_t cov;  // prmt's sign-replicate selectors (__byte_perm drops the selector msb)
-    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(cov) : "r"((w & 0x7FFF7FFFu) + 0x7FFF7FFFu));
+    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(cov) : "r"(((w & 0x7FFF7FFFu) + 0x7FFF7FFFu) & w));
     return w + (cov & lagw);
   } else return w + (w > kFlag32 ? lagw : 0u);
 }

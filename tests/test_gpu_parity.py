@@ -168,3 +168,20 @@ def test_repeat_after_download_and_mixed_calls():
     g.propagate(20)
     assert np.array_equal(g.activity(), O.propagate(occ, sm, 20))
     g.close()
+
+
+def test_repeated_runs_on_one_grid_are_identical():
+    """Many propagate_auto calls on the same grid (as a planner session or the bench does): every run
+    equals the oracle.  Regression: lag was once added to the junk low bits of wall / padding cells,
+    which grew across runs until it carried into the flag bit (intermittent wrong maps / causes)."""
+    occ = O.kruskal_maze(1024, 1024, 5)
+    src = O.sample_free_cells(occ, 16, 5)
+    sm = O.source_mask(occ, src)
+    ref, rl, rc = O.propagate_auto(occ, sm, 20000)
+    g = am.Grid(occ, src)
+    for run in range(24):
+        r = g.propagate_auto(20000)
+        assert (r.layers_used, r.cause) == (rl, rc), run
+        if run % 4 == 3:
+            assert np.array_equal(g.activity(), ref), run
+    g.close()
