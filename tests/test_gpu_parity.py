@@ -185,3 +185,39 @@ def test_repeated_runs_on_one_grid_are_identical():
         if run % 4 == 3:
             assert np.array_equal(g.activity(), ref), run
     g.close()
+
+
+def test_repeated_runs_slabs_batch_dense_are_identical():
+    """The same repeated-run check for in-process row slabs, the small-maze batch and the dense sweep."""
+    occ = O.kruskal_maze(512, 640, 9)
+    src = O.sample_free_cells(occ, 8, 9)
+    sm = O.source_mask(occ, src)
+    ref, rl, rc = O.propagate_auto(occ, sm, 8000)
+    H = occ.shape[0]
+    cuts = [0, 192, 448, H]
+    slabs = [am.Grid.slab(occ, src, cuts[k], cuts[k + 1]) for k in range(3)]
+    full = am.Grid(occ, src)
+    dctx = am.Context(0, dense=True)
+    gd = am.Grid(occ, src, dctx)
+    mazes = np.stack([O.random_maze(64, 64, 0.3, 300 + i) for i in range(16)])
+    msrc = [O.sample_free_cells(mazes[i], 1, 400 + i) for i in range(16)]
+    bref = [O.propagate_auto(mazes[i], O.source_mask(mazes[i], msrc[i]), 1024) for i in range(16)]
+    b = am.Batch(mazes, msrc)
+    for run in range(12):
+        r = am.slabs_propagate(slabs, 0, 8000)
+        assert (r.layers_used, r.cause) == (rl, rc), ("slabs", run)
+        rd = gd.propagate_auto(8000)
+        assert (rd.layers_used, rd.cause) == (rl, rc), ("dense", run)
+        used, cause, _ = b.propagate(auto_cap=1024)
+        assert [(int(u), int(c)) for u, c in zip(used, cause)] == [(x[1], x[2]) for x in bref], ("batch", run)
+        if run % 4 == 3:
+            am.slabs_gather(slabs, full)
+            assert np.array_equal(full.activity(), ref), ("slabs map", run)
+            assert np.array_equal(gd.activity(), ref), ("dense map", run)
+            maps = b.activity()
+            for i in range(16):
+                assert np.array_equal(maps[i], bref[i][0]), ("batch map", run, i)
+    for x in slabs + [full, gd]:
+        x.close()
+    b.close()
+    dctx.close()
