@@ -1365,10 +1365,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
 template <int CB>
 __device__ __forceinline__ uint32_t add_lag(uint32_t w, uint32_t lagw) {
   if constexpr (CB == 16) {
-    // a half's low 15 bits are nonzero iff adding 0x7FFF carries into bit 15
-    // (never out of the half); AND with w keeps flagged halves; PRMT replicates bit 15
+    // covered <=> half > 0x8000: after a per-half max with 0x8000 every half is >= 0x8000, so
+    // subtracting 1 per half cannot borrow across halves and leaves bit 15 set exactly for
+    // covered halves; PRMT replicates bit 15 (VIMNMX + IADD + PRMT)
     uint32_t cov;  // prmt's sign-replicate selectors (__byte_perm drops the selector msb)
-    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(cov) : "r"(((w & 0x7FFF7FFFu) + 0x7FFF7FFFu) & w));
+    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(cov) : "r"(__vmaxu2(w, 0x80008000u) - 0x00010001u));
     return w + (cov & lagw);
   } else return w + (w > kFlag32 ? lagw : 0u);
 }
