@@ -65,3 +65,48 @@ def test_random_grid_matches_oracle(seed):
                 assert st == ost == 0, (seed, method, tuple(t))
                 assert np.array_equal(pts, opts), (seed, method, tuple(t))
     g.close()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_slabs_and_batches_match_oracle(seed):
+    rng = np.random.default_rng(5000 + seed)
+    w, h = int(rng.integers(8, 700)), int(rng.integers(40, 900))
+    occ = O.random_maze(w, h, float(rng.choice([0.0, 0.2, 0.35, 0.5])), seed)
+    if (occ == 0).sum() < 4:
+        pytest.skip("too few free cells")
+    src = O.sample_free_cells(occ, int(rng.integers(1, 6)), seed)
+    sm = O.source_mask(occ, src)
+    cap = 4 * max(w, h) + 8
+    ref, rl, rc = O.propagate_auto(occ, sm, cap)
+    # row slabs: random cut count, cuts from the library's rule or random (>= K rows each)
+    n = int(rng.integers(2, 6))
+    if h < 8 * n:
+        n = 2
+    cuts = sorted(set([0, h] + [int(x) for x in rng.choice(np.arange(8, h - 7), size=n - 1, replace=False)]))
+    if any(b - a < 8 for a, b in zip(cuts, cuts[1:])):
+        cuts = [0, h // 2, h]
+    slabs = [am.Grid.slab(occ, src, a, b) for a, b in zip(cuts, cuts[1:])]
+    full = am.Grid(occ, src)
+    for run in range(2):
+        r = am.slabs_propagate(slabs, 0, cap)
+        assert (r.layers_used, r.cause) == (rl, rc), (seed, run, cuts)
+        am.slabs_gather(slabs, full)
+        assert np.array_equal(full.activity(), ref), (seed, run, cuts)
+    for x in slabs + [full]:
+        x.close()
+    # small-maze batch of random size
+    mw, mh, nb = int(rng.integers(4, 90)), int(rng.integers(4, 90)), int(rng.integers(1, 40))
+    mazes = np.stack([O.random_maze(mw, mh, 0.3, 7000 + seed * 64 + i) for i in range(nb)])
+    keep = [i for i in range(nb) if (mazes[i] == 0).sum() > 0]
+    mazes = mazes[keep]
+    if len(mazes) == 0:
+        return
+    msrc = [O.sample_free_cells(m, 1, seed + i) for i, m in enumerate(mazes)]
+    b = am.Batch(mazes, msrc)
+    used, cause, _ = b.propagate(auto_cap=512)
+    maps = b.activity()
+    for i, m in enumerate(mazes):
+        mref, ml, mc = O.propagate_auto(m, O.source_mask(m, msrc[i]), 512)
+        assert (int(used[i]), int(cause[i])) == (ml, mc), (seed, i)
+        assert np.array_equal(maps[i], mref), (seed, i)
+    b.close()
