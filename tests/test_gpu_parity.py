@@ -144,8 +144,24 @@ def test_promotion_to_32bit_cells():
     ecc = int(hops[hops != O.UNREACH].max())
     assert ecc > 32767 and r.cell_bits == 32
     assert (r.layers_used, r.cause) == (ecc, O.FILLED)
-    bad, _ = O.check_activity(occ, g.activity(), hops, r.layers_used)
+    vals = g.activity()
+    bad, _ = O.check_activity(occ, vals, hops, r.layers_used)
     assert bad == 0
+    # paths on the 32-bit map (the 32-bit walk), both methods, against the oracle on the downloaded map
+    far = np.argwhere(hops == ecc)[:1]
+    mid = np.argwhere((hops > 16000) & (hops < 16010))[:2]
+    tg = np.concatenate([far, mid]).astype(np.uint32)
+    for method in (am.EUCLIDEAN, am.SIMPLE):
+        for (st, pts), t in zip(g.paths(tg, method, seed=5), tg):
+            if method == am.EUCLIDEAN:
+                ost, opts = O.reconstruct_euclidean(occ, sm, vals, t)
+            else:
+                ost, opts = O.reconstruct_simple(occ, sm, vals, t, 5)
+            assert st == ost == 0 and np.array_equal(pts, opts), (method, tuple(t))
+    # the next solve on the same grid starts over in 16-bit cells and promotes again
+    r2 = g.propagate_auto(200_000)
+    assert (r2.layers_used, r2.cause, r2.cell_bits) == (r.layers_used, r.cause, 32)
+    assert np.array_equal(g.activity(), vals)
     # fixed L beyond 16 bits starts in 32-bit cells
     occ2 = O.random_maze(64, 48, 0.2, 3)
     src2 = O.sample_free_cells(occ2, 2, 3)
