@@ -1507,22 +1507,17 @@ __global__ void k_tiles_halo_scan(Geo g, const typename Cell<CB>::T* __restrict_
   push_tiles(g, book, blk - 1u, any && lane == 0, side ? (int)g.nchunks - 1 : 0, (int)b);
 }
 
-// Block 0's work list: the 3x3 neighbourhood of every tile holding a source
-// (the layer-0 frontier, a = 1); pushed as block "-1" (lists 0, sched 1).
+// Block 0's work list: the 3x3 neighbourhood of every tile with a source in
+// reach (the layer-0 frontier, a = 1; TileBook::tsrc, a superset of the tiles
+// holding one -- listing a tile that cannot change is harmless); pushed as
+// block "-1" (lists 0, sched 1).
 __global__ void k_tiles_init(Geo g, const uint8_t* __restrict__ srcmask, TileBook book) {
+  (void)srcmask;
   const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= g.ntiles()) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const uint32_t chunk = t / g.tbands, band = t % g.tbands;
-  bool any = false;
-  if (lane < kTileCols / 8)
-    for (uint32_t r = 0; r < (uint32_t)kTileRows; ++r) {
-      const size_t base = (size_t)(chunk * kTileRows + r + g.pad) * g.pitch + g.pad + band * kTileCols + lane * 8;
-      const uint2 m = *reinterpret_cast<const uint2*>(srcmask + base);
-      any |= (m.x | m.y) != 0;
-    }
-  any = __any_sync(0xffffffffu, any);
-  if (!any) return;
+  if (!book.tsrc[t]) return;  // warp-uniform
   const int dr = lane / 3 - 1, dc = lane % 3 - 1;
   push_tiles(g, book, 0xFFFFFFFFu, lane < 9, (int)chunk + dr, (int)band + dc);
 }
