@@ -54,6 +54,8 @@ struct am_grid {
   uint8_t* srcmask = nullptr;        // pitched 0/1 (owned rows + halo rows for slabs)
   uint8_t* rowsrc = nullptr;         // per band and allocated row: a source in the band's columns (Geo::rowsrc_bytes)
   uint8_t* occ = nullptr;            // dense owned rows (re-initialisation / plain maps)
+  uint32_t* src_rc = nullptr;        // the SourceSet, global (row, col) pairs (re-initialisation)
+  uint64_t n_src = 0;
   uint8_t* srcmask_dense = nullptr;  // dense owned rows (plain maps)
   uint32_t* d_flags = nullptr;       // kFlagWords: fixed-point slots, CTA arrival counter, neighbour receive rings
   am::FlagSet* fs = nullptr;         // host mirror + events of the slots (borrowed from the context)

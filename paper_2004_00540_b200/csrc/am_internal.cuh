@@ -129,8 +129,11 @@ constexpr uint32_t kListSrc = 1u << 31;
 constexpr uint32_t kListBand = 0x7FFFu;
 
 // ---- kernels (stencil.cu) ----
-void launch_init(const Geo& g, const uint8_t* d_occ_dense, const uint8_t* d_srcmask, void* d_val,
-                 int cell_bits, cudaStream_t s);
+// layer 0 (initial, activity.hpp:21): flag on free cells; then +1 at the sources of rows
+// [row0, row0 + g.H) (src_rc: n global (row, col) pairs, already validated)
+void launch_init(const Geo& g, const uint8_t* d_occ_dense, void* d_val, int cell_bits, cudaStream_t s);
+void launch_src_init(const Geo& g, const uint32_t* src_rc, uint64_t n, uint32_t row0, void* d_val, int cell_bits,
+                     cudaStream_t s);
 void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const uint32_t* d_src_rc, uint64_t n,
                          uint8_t* d_dense, const uint8_t* d_occ, uint8_t* d_srcmask, uint8_t* d_rowsrc, int* d_err,
                          cudaStream_t s);

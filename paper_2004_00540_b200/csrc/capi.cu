@@ -150,6 +150,7 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->srcmask);
   am::dfree(ctx, g->rowsrc);
   am::dfree(ctx, g->occ);
+  am::dfree(ctx, g->src_rc);
   am::dfree(ctx, g->srcmask_dense);
   am::dfree(ctx, g->d_flags);
   if (g->fs) ctx->flag_sets.push_back(g->fs);
@@ -247,7 +248,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   }
   if (!e) e = cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);
-  am::dfree(ctx, d_src);
+  g->src_rc = d_src;  // kept: the sources of every re-initialisation (freed with the grid)
+  g->n_src = n_src;
   am::dfree(ctx, d_err);
   if (e) {
     (void)cudaGetLastError();
@@ -386,7 +388,9 @@ static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
   am_status st = set_cell_bits(ctx, g, cell_bits);
   if (st) return st;
   g->cur = 0;
-  launch_init(g->g, g->occ, g->srcmask, g->val[0], cell_bits, ctx->stream);
+  launch_init(g->g, g->occ, g->val[0], cell_bits, ctx->stream);
+  CKL();
+  launch_src_init(g->g, g->src_rc, g->n_src, g->row0, g->val[0], cell_bits, ctx->stream);
   CKL();
   g->plain_active = 0;
   g->computed = g->layers_used = 0;

@@ -144,21 +144,16 @@ __global__ void k_srcmask_rows(Geo g, uint32_t total_h, uint32_t row0, const uin
 // 8 cells per thread (one 16 B / 32 B store); cells past the grid edge are
 // written as padding (0).
 template <int CB>
-__global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __restrict__ srcmask,
-                       typename Cell<CB>::T* __restrict__ val) {
+__global__ void k_init(Geo g, const uint8_t* __restrict__ occ, typename Cell<CB>::T* __restrict__ val) {
   const uint32_t c0 = 8 * (blockIdx.x * blockDim.x + threadIdx.x);
   const uint32_t r = blockIdx.y;
   if (c0 >= g.W) return;
   const uint8_t* o = occ + (size_t)r * g.W + c0;
   const size_t i = g.idx(r, c0);
-  const uint2 sm = *reinterpret_cast<const uint2*>(srcmask + i);
   const uint32_t flag = CB == 16 ? kFlag16 : kFlag32;
   uint32_t v[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t s = ((k < 4 ? sm.x : sm.y) >> (8 * (k & 3))) & 0xFFu;
-    v[k] = (c0 + k < g.W && !o[k]) ? (flag | s) : 0u;
-  }
+  for (int k = 0; k < 8; ++k) v[k] = (c0 + k < g.W && !o[k]) ? flag : 0u;
   if constexpr (CB == 16) {
     *reinterpret_cast<uint4*>(val + i) =
         make_uint4(v[0] | v[1] << 16, v[2] | v[3] << 16, v[4] | v[5] << 16, v[6] | v[7] << 16);
@@ -166,6 +161,17 @@ __global__ void k_init(Geo g, const uint8_t* __restrict__ occ, const uint8_t* __
     reinterpret_cast<uint4*>(val + i)[0] = make_uint4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<uint4*>(val + i)[1] = make_uint4(v[4], v[5], v[6], v[7]);
   }
+}
+
+// the sources of the grid's rows start at 1 (free cells: validated at grid creation)
+template <int CB>
+__global__ void k_src_init(Geo g, const uint32_t* __restrict__ rc, uint64_t n, uint32_t row0,
+                           typename Cell<CB>::T* __restrict__ val) {
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t r = rc[2 * k], c = rc[2 * k + 1];
+  if (r < row0 || r >= row0 + g.H) return;
+  val[g.idx(r - row0, c)] = (CB == 16 ? kFlag16 : kFlag32) | 1u;
 }
 
 // ----------------------------------------------------------- K1+K2 block
@@ -1691,13 +1697,22 @@ void launch_srcmask_rows(const Geo& g, uint32_t total_h, uint32_t row0, const ui
                                                              d_srcmask, d_rowsrc, d_err);
 }
 
-void launch_init(const Geo& g, const uint8_t* d_occ, const uint8_t* d_srcmask, void* d_val, int cb,
-                 cudaStream_t s) {
+void launch_init(const Geo& g, const uint8_t* d_occ, void* d_val, int cb, cudaStream_t s) {
   const dim3 grid((g.W + 8 * 128 - 1) / (8 * 128), g.H);
   if (cb == 16)
-    k_init<16><<<grid, 128, 0, s>>>(g, d_occ, d_srcmask, (uint16_t*)d_val);
+    k_init<16><<<grid, 128, 0, s>>>(g, d_occ, (uint16_t*)d_val);
   else
-    k_init<32><<<grid, 128, 0, s>>>(g, d_occ, d_srcmask, (uint32_t*)d_val);
+    k_init<32><<<grid, 128, 0, s>>>(g, d_occ, (uint32_t*)d_val);
+}
+
+void launch_src_init(const Geo& g, const uint32_t* rc, uint64_t n, uint32_t row0, void* d_val, int cb,
+                     cudaStream_t s) {
+  if (!n) return;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (cb == 16)
+    k_src_init<16><<<blocks, 256, 0, s>>>(g, rc, n, row0, (uint16_t*)d_val);
+  else
+    k_src_init<32><<<blocks, 256, 0, s>>>(g, rc, n, row0, (uint32_t*)d_val);
 }
 
 void launch_block(const Geo& g, int cb, bool slab, const void* in, void* out, const uint8_t* srcmask,
