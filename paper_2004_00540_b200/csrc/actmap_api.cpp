@@ -499,6 +499,12 @@ struct PlannerImpl {
   std::shared_ptr<detail::DeviceMap> dev;
   uint32_t width, height;
   const GridMap* grid;
+  std::vector<Coord> sources;
+  // A map returned earlier still refers to `dev` (ActivityMap fetches its values lazily): before the
+  // next propagation overwrites the device map, give the planner a fresh one so that map keeps its values.
+  void own_map() {
+    if (dev.use_count() > 1) dev = std::make_shared<detail::DeviceMap>(*grid, SourceSet(*grid, sources));
+  }
 };
 
 Planner::Planner(const GridMap& grid, const SourceSet& sources, DeviceOptions options) {
@@ -509,6 +515,7 @@ Planner::Planner(const GridMap& grid, const SourceSet& sources, DeviceOptions op
   impl->width = grid.width();
   impl->height = grid.height();
   impl->grid = &grid;
+  impl->sources = sources.coords();
   impl_ = impl;
 }
 
@@ -518,6 +525,7 @@ AutoResult Planner::propagate_auto(uint32_t auto_cap) {
   if (auto_cap == 0 || auto_cap > kMaxLayers) throw InvalidInputError("propagate_auto: auto_cap out of range");
   auto* p = static_cast<PlannerImpl*>(impl_.get());
   std::lock_guard<std::mutex> lk(api_mutex());
+  p->own_map();
   am_prop_result r{};
   check(am_propagate(p->dev->ctx, p->dev->grid, 0, auto_cap, AM_MODE_BATCHED, &r), p->dev->ctx, "propagate_auto");
   p->dev->layers = r.layers_used;
@@ -525,7 +533,7 @@ AutoResult Planner::propagate_auto(uint32_t auto_cap) {
   const AutoStop cause = r.cause == AM_STOP_FILLED ? AutoStop::kFilled
                          : r.cause == AM_STOP_STALLED ? AutoStop::kStalled
                                                       : AutoStop::kCapReached;
-  // the returned map shares the planner's device map: it reflects this propagation
+  // the returned map shares the planner's device map until the next propagation (own_map)
   return AutoResult{ActivityMap(p->width, p->height, r.layers_used, p->dev), r.layers_used, cause};
 }
 
@@ -533,6 +541,7 @@ ActivityMap Planner::propagate(uint32_t layers, Mode mode) {
   if (layers == 0 || layers > kMaxLayers) throw InvalidInputError("propagate: L out of range");
   auto* p = static_cast<PlannerImpl*>(impl_.get());
   std::lock_guard<std::mutex> lk(api_mutex());
+  p->own_map();
   am_prop_result r{};
   check(am_propagate(p->dev->ctx, p->dev->grid, layers, 0, mode == Mode::kBatched ? AM_MODE_BATCHED : AM_MODE_ITERATIVE,
                      &r),

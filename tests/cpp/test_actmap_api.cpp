@@ -150,6 +150,20 @@ int main() {
     const auto no_pts = planner.target_reports(targets, b200::Method::kEuclidean, 0, false);
     CHECK(no_pts.size() == targets.size() && no_pts[0].points.empty() && no_pts[0].steps == rep.paths[0].steps);
   }
+  // a planner's earlier maps keep their values across later propagations (value semantics)
+  {
+    const GridMap g = build_grid(9, 9, {});
+    const std::vector<Coord> s{{4, 4}};
+    const SourceSet src(g, s);
+    b200::Planner planner(g, src);
+    const ActivityMap a = planner.propagate(3);
+    const ActivityMap b = planner.propagate(5);
+    const AutoResult c = planner.propagate_auto(100);
+    CHECK(a.at(4, 4) == 4 && a.layers_applied() == 3);
+    CHECK(b.at(4, 4) == 6 && b.layers_applied() == 5);
+    CHECK(c.layers_used == 4 && c.map.at(4, 4) == 5 && c.map.at(0, 0) == 1);
+    CHECK(a == propagate(g, src, 3) && b == propagate(g, src, 5));
+  }
   // map / scene text (mapio.hpp)
   {
     const GridMap g = parse_movingai("type octile\nheight 2\nwidth 2\nmap\n.@\n@.\n");
