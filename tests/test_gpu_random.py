@@ -1,6 +1,8 @@
 """Randomised differential suite: seeded random grids (shape, density, generator, sources, layer mode)
 through the device path twice on the same grid, against the CPU oracle -- maps, layers_used / cause,
 and the point sequences of sampled targets for both reconstruction methods, bit for bit."""
+import os
+
 import numpy as np
 import pytest
 
@@ -32,7 +34,7 @@ def case(seed):
     return occ, src, mode, layers, cap, rng
 
 
-@pytest.mark.parametrize("seed", range(160))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("AM_RANDOM_CASES", "160"))))
 def test_random_grid_matches_oracle(seed):
     c = case(1000 + seed)
     if c is None:
@@ -67,7 +69,7 @@ def test_random_grid_matches_oracle(seed):
     g.close()
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("AM_RANDOM_CASES", "160")) // 4))
 def test_random_slabs_and_batches_match_oracle(seed):
     rng = np.random.default_rng(5000 + seed)
     w, h = int(rng.integers(8, 700)), int(rng.integers(40, 900))
