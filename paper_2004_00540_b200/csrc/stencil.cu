@@ -660,6 +660,9 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
 #ifndef AM_TRIM
 #define AM_TRIM 1
 #endif
+#ifndef AM_SPEC_LIST
+#define AM_SPEC_LIST 1
+#endif
 #ifndef AM_FIN_BATCH
 #define AM_FIN_BATCH 1
 #endif
@@ -1086,6 +1089,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
     *reinterpret_cast<volatile uint32_t*>(prev.host) = atomicExch(prev.word, 0xFFFFFFFFu);
   const uint32_t n = book.count[blk % 3];
   const uint32_t* __restrict__ list = book.list[blk & 1];
+#if AM_SPEC_LIST
+  // Light blocks take static quarter items (w -> tile w / 2): the list entry of this warp's first
+  // item is loaded alongside the list length instead of after it (one L2 round trip less per block)
+  const uint32_t w_static = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const uint32_t spec_entry = (w_static >> 1) < g.ntiles() ? list[w_static >> 1] : 0u;
+#endif
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     book.count[(blk + 2) % 3] = 0;
     book.count[3 + (blk + 2) % 3] = 0;
@@ -1235,7 +1244,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
       solo = itB;
       fetch_next = itB == kNone;
     } else {
+#if AM_SPEC_LIST
+      it = (quarters && !eighths && w == w_static) ? spec_entry : list[eighths ? w >> 2 : (quarters ? w >> 1 : w)];
+#else
       it = list[eighths ? w >> 2 : (quarters ? w >> 1 : w)];
+#endif
       half = eighths ? (w & 3u) : (quarters ? w & 1u : 0u);  // eighths: the part (0-3)
     }
     const uint32_t bA = (it >> 16) & kListBand, cA = it & 0xFFFFu;
