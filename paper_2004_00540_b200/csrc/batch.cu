@@ -49,15 +49,18 @@ __global__ void k_batch_stats(Geo g, const void* __restrict__ val, uint32_t mw, 
   const uint32_t tx = i % tiles_x, ty = i / tiles_x;
   const uint32_t flag = CB == 16 ? kFlag16 : kFlag32, low = CB == 16 ? 0x7FFFu : kLow32;
   uint32_t m = 0xFFFFFFFFu, z = 0;
-  const uint64_t cells = (uint64_t)mw * mh;
-  for (uint64_t k = threadIdx.x; k < cells; k += blockDim.x) {
-    const uint32_t r = ty * (mh + 1) + (uint32_t)(k / mw), c = tx * (mw + 1) + (uint32_t)(k % mw);
-    const size_t idx = g.idx(r, c);
-    const uint32_t v = CB == 16 ? (uint32_t) static_cast<const uint16_t*>(val)[idx] : static_cast<const uint32_t*>(val)[idx];
-    if (v & flag) {
-      const uint32_t a = v & low;
-      if (a == 0) z = 1;
-      else m = a < m ? a : m;
+  // a warp per maze row (coalesced), no per-cell division
+  const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (uint32_t rr = threadIdx.x >> 5; rr < mh; rr += nw) {
+    const size_t base = g.idx(ty * (mh + 1) + rr, tx * (mw + 1));
+    for (uint32_t cc = lane; cc < mw; cc += 32) {
+      const uint32_t v = CB == 16 ? (uint32_t) static_cast<const uint16_t*>(val)[base + cc]
+                                  : static_cast<const uint32_t*>(val)[base + cc];
+      if (v & flag) {
+        const uint32_t a = v & low;
+        if (a == 0) z = 1;
+        else m = a < m ? a : m;
+      }
     }
   }
   m = __reduce_min_sync(0xffffffffu, m);
