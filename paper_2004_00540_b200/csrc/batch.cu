@@ -91,9 +91,10 @@ __global__ void k_batch_decode(Geo g, const void* __restrict__ val, uint32_t mw,
   const uint32_t tx = i % tiles_x, ty = i / tiles_x;
   const uint32_t flag = CB == 16 ? kFlag16 : kFlag32, low = CB == 16 ? 0x7FFFu : kLow32;
   const uint32_t rb = computed - used[i];
-  const uint64_t cells = (uint64_t)mw * mh;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < cells; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = ty * (mh + 1) + (uint32_t)(k / mw), c = tx * (mw + 1) + (uint32_t)(k % mw);
+  const uint32_t cells = mw * mh;  // <= 65535^2 < 2^32: 32-bit index arithmetic
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cells; k += gridDim.x * blockDim.x) {
+    const uint32_t kr = k / mw;
+    const uint32_t r = ty * (mh + 1) + kr, c = tx * (mw + 1) + (k - kr * mw);
     const size_t idx = g.idx(r, c);
     const uint32_t v = CB == 16 ? (uint32_t) static_cast<const uint16_t*>(val)[idx] : static_cast<const uint32_t*>(val)[idx];
     const uint32_t a = v & low;
