@@ -32,10 +32,10 @@ namespace am {
 __global__ void k_batch_pack(const uint8_t* __restrict__ mazes, uint32_t n, uint32_t mw, uint32_t mh,
                              uint32_t tiles_x, uint32_t W, uint8_t* __restrict__ big) {
   const uint32_t i = blockIdx.y;  // maze
-  const uint64_t cells = (uint64_t)mw * mh;
+  const uint32_t cells = mw * mh;  // <= 65535^2 < 2^32
   const uint32_t tx = i % tiles_x, ty = i / tiles_x;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < cells; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = (uint32_t)(k / mw), c = (uint32_t)(k % mw);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cells; k += gridDim.x * blockDim.x) {
+    const uint32_t r = k / mw, c = k - r * mw;
     big[(size_t)(ty * (mh + 1) + r) * W + tx * (mw + 1) + c] = mazes[(size_t)i * cells + k];
   }
   (void)n;
