@@ -14,10 +14,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <map>
 #include <memory>
 #include <string>
-#include <variant>
 
 #include "actmap/errors.hpp"
 #include "actmap/report.hpp"
