@@ -8,12 +8,24 @@ region starts (the 1 GiB activity field is far larger than L2, so no flush is
 needed).  value = W*H*L_used / time-to-solve.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--no-cpu-baseline] [--no-e2e] [--no-parity] [--no-configs]
+
+After the timed region (rank 0, N=1) the line also carries
+  * "parity": the benchmarked instance checked by the CPU oracle (the checker,
+    never the thing measured): the closed-form law against a CPU BFS on every
+    cell, the auto-L outcome predicted from the BFS, and 256 of the timed
+    step's own paths against the oracle's reconstruction on the device map;
+  * "configs": the other BASELINE.json configurations (C2, C3, C4-fixed L=1024,
+    C5) timed the same way, each with its own parity flags.
 
 --impl reference times the CPU restatement of the reference planner
 (oracle/, the reference ships no implementation) on the host cores, same
-config and metric, one bounded fixed-L slice per step.
+config and metric: each step one fixed-L slice of layers over the full C4 grid
+with preallocated buffers (the same measurement as the GPU arm's
+cpu_baseline), plus full CPU solves of C1 and C2.
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -34,12 +46,15 @@ N_SOURCES, N_TARGETS, PT_SEED = 64, 4096, 4
 AUTO_CAP = 4 * max(W, H)
 BYTES_PER_CELL_UPDATE = 9  # 4 B read + 4 B write of uint32 activity + 1 B mask (activity.hpp:51, grid.hpp:56)
 LAYERS_PER_BLOCK = 8       # am::kK
+CPU_SLICE_LAYERS = 8       # layers per CPU timing slice (both CPU legs)
+PARITY_PATHS = 256         # paths of the timed step re-derived by the oracle
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# ------------------------------------------------------------------ workloads
 def sample_points(occ, n, seed, exclude=None):
     """n distinct free cells (deterministic); exclude: set of (r, c)."""
     rng = np.random.default_rng(seed)
@@ -57,15 +72,45 @@ def sample_points(occ, n, seed, exclude=None):
     return np.array(out, np.uint32)
 
 
-def make_workload(am):
+def points_for(occ, n_src, n_tgt, seed):
+    src = sample_points(occ, n_src, seed)
+    tgt = sample_points(occ, n_tgt, seed + 1, exclude={tuple(x) for x in src.tolist()})
+    return src, tgt
+
+
+def make_workload(gen):
+    """C4; gen = a random_maze implementation (the product's am.random_maze or the oracle's -- equal, tested)."""
     t0 = time.perf_counter()
-    occ = am.random_maze(W, H, DENSITY, GRID_SEED)
-    src = sample_points(occ, N_SOURCES, PT_SEED)
-    tgt = sample_points(occ, N_TARGETS, PT_SEED + 1, exclude={tuple(x) for x in src.tolist()})
+    occ = gen(W, H, DENSITY, GRID_SEED)
+    src, tgt = points_for(occ, N_SOURCES, N_TARGETS, PT_SEED)
     log(f"workload generated in {time.perf_counter() - t0:.1f}s (obstacles {occ.mean():.4f})")
     return occ, src, tgt
 
 
+def c2_workload(am):
+    occ = am.kruskal_maze(4096, 4096, 2)
+    src, tgt = points_for(occ, 16, 16, 2)
+    return occ, src, tgt, 4096 * 4096  # perfect-maze corridors: cap at the cell count
+
+
+def c3_workload(am):
+    occ = am.city_grid(16384, 16384, 3)
+    src, tgt = points_for(occ, 64, 1000, 3)
+    return occ, src, tgt, 4 * 16384
+
+
+def c5_workload(am, n=4096):
+    """n x 256^2 random mazes (0.30, seeds 5000+i), 1 source + 8 targets each, cap 1024."""
+    mazes = np.stack([am.random_maze(256, 256, 0.30, 5000 + i) for i in range(n)])
+    srcs, tg = [], []
+    for i in range(n):
+        s, t = points_for(mazes[i], 1, 8, 5000 + 7 * i)
+        srcs.append(s)
+        tg.append(np.column_stack([np.full(8, i, np.uint32), t]))
+    return mazes, srcs, np.concatenate(tg).astype(np.uint32), 1024
+
+
+# ------------------------------------------------------------------ measurement helpers
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -138,38 +183,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside), "scope": scope}
 
 
-def cpu_baseline(occ, src, budget_s=12.0):
-    """Oracle (CPU restatement, all host threads) on a bounded fixed-L slice of the same grid."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-
-    threads = os.cpu_count() or 1
-    sm = O.source_mask(occ, src)
-    t0 = time.perf_counter()
-    O.propagate(occ, sm, 1, threads=threads)
-    one = time.perf_counter() - t0
-    L = max(1, min(64, int(budget_s / max(one, 1e-3))))
-    t0 = time.perf_counter()
-    O.propagate(occ, sm, L, threads=threads)
-    dt = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.propagate(occ, sm, 1, threads=1)
-    single = W * H / (time.perf_counter() - t0) / 1e9
-    rate = W * H * L / dt / 1e9
-    return {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "cpu_model": cpu_model(), "single_thread_value": round(single, 4),
-            "sample": f"oracle propagate, full {W}x{H} C4 grid, fixed L={L} slice ({dt:.1f}s), threads={threads}; "
-                      f"single thread: one layer"}
-
-
-def bench_config(world):
-    return {"workload": f"C4: {W}x{H} random_maze(density 0.40, seed 4), {N_SOURCES} sources, "
-                        f"{N_TARGETS} targets, propagate_auto(cap {AUTO_CAP}) + Euclidean paths to host",
-            "grid": [W, H], "sources": N_SOURCES, "targets": N_TARGETS, "auto_cap": AUTO_CAP,
-            "parallelism": "single GPU" if world == 1 else f"row slabs x{world} (NCCL K=8 halos)",
-            "l2": "inputs larger than L2 (1.07 GB 16-bit field vs 126 MB L2), no flush"}
-
-
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -181,43 +194,154 @@ def cpu_model():
     return "unknown"
 
 
+# ------------------------------------------------------------------ CPU side (oracle: checker + baseline only)
+_ORACLE = None
+
+
+def load_oracle():
+    """The CPU restatement (oracle/), built for THIS host (-march=native) when gcc can; else the portable
+    x86-64-v3 build.  Returns (module, isa)."""
+    global _ORACLE
+    if _ORACLE is None:
+        isa = "x86-64-v3 (portable build)"
+        try:
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "native"], check=True,
+                           stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=120)
+            os.environ["ORACLE_LIB"] = os.path.join(ROOT, "oracle", "liboracle_native.so")
+            isa = "-march=native (built on this host)"
+        except Exception:
+            pass
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        O.lib()
+        _ORACLE = (O, isa)
+    return _ORACLE
+
+
+def cpu_slices(O, occ, src, layers, reps, threads):
+    """Times `reps` slices of `layers` oracle layers (propagate_layer ping-pong over the full grid, buffers
+    allocated and first-touched outside the timer).  Returns per-slice seconds."""
+    sm = O.source_mask(occ, src)
+    a = O.initial(occ, sm)
+    b = np.zeros_like(a)
+    O.propagate_layer(occ, sm, a, threads=threads, out=b)  # warm: page-in + OpenMP pool
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for _ in range(layers):
+            O.propagate_layer(occ, sm, a, threads=threads, out=b)
+            a, b = b, a
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_baseline(occ, src, L_used):
+    """Oracle on all host threads: fixed-L slices of the full C4 grid, same measurement as
+    the --impl reference arm; plus a single-thread layer."""
+    O, isa = load_oracle()
+    threads = os.cpu_count() or 1
+    ts = cpu_slices(O, occ, src, CPU_SLICE_LAYERS, 3, threads)
+    dt = statistics.median(ts)
+    rate = W * H * CPU_SLICE_LAYERS / dt / 1e9
+    single = W * H / statistics.median(cpu_slices(O, occ, src, 1, 1, 1)) / 1e9
+    return {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+            "isa": isa, "single_thread_value": round(single, 4),
+            "sample": f"oracle propagate_layer x {CPU_SLICE_LAYERS} layers over the full {W}x{H} C4 grid, "
+                      f"median of 3 slices ({dt:.2f} s each), threads={threads}, buffers preallocated; "
+                      f"single thread: one layer",
+            "extrapolated_time_to_solve_s": round(W * H * L_used / (rate * 1e9), 1)}
+
+
+def predicted_auto(O, occ, hops, cap):
+    """propagate_auto's (L_used, cause) from the BFS alone (pin P3)."""
+    reach = hops != O.UNREACH
+    maxd = int(hops[reach].max())
+    unreachable_free = bool(((occ == 0) & ~reach).any())
+    lu, cause = (max(1, maxd), O.FILLED) if not unreachable_free else (maxd + 1, O.STALLED)
+    if lu > cap:
+        lu, cause = cap, (O.FILLED if (not unreachable_free and maxd <= cap) else O.CAP)
+    return lu, cause
+
+
+def check_grid(O, occ, src, amap, L, cap, tgt, off, pts, st, n_paths, hops=None):
+    """Oracle check of one solved grid: law on every cell, auto outcome, and n_paths of the device paths
+    (offsets / points / status of the traced targets) against oracle reconstruct_euclidean."""
+    sm = O.source_mask(occ, src)
+    if hops is None:
+        hops = O.bfs_multi_source(occ, sm)
+    bad, _ = O.check_activity(occ, amap, hops, L)
+    out = {"cells_checked": int(occ.size), "law_violations": int(bad)}
+    if cap is not None:
+        out["auto_outcome_matches_bfs"] = predicted_auto(O, occ, hops, cap)[0] == L
+    idx = np.linspace(0, len(tgt) - 1, min(n_paths, len(tgt))).astype(np.int64) if len(tgt) else []
+    mism = 0
+    for k in idx:
+        ost, opts = O.reconstruct_euclidean(occ, sm, amap, tgt[k], cap=L + 2)
+        if int(st[k]) != ost or (ost == 0 and not np.array_equal(pts[int(off[k]):int(off[k + 1])], opts)):
+            mism += 1
+    out["paths_checked"] = int(len(idx))
+    out["path_mismatches"] = mism
+    return out, hops
+
+
+def parity_ok(p):
+    return p["law_violations"] == 0 and p["path_mismatches"] == 0 and p.get("auto_outcome_matches_bfs", True)
+
+
+def bench_config(world):
+    return {"workload": f"C4: {W}x{H} random_maze(density 0.40, seed 4), {N_SOURCES} sources, "
+                        f"{N_TARGETS} targets, propagate_auto(cap {AUTO_CAP}) + Euclidean paths to host",
+            "grid": [W, H], "sources": N_SOURCES, "targets": N_TARGETS, "auto_cap": AUTO_CAP,
+            "parallelism": "single GPU" if world == 1 else f"row slabs x{world} (NCCL K=8 halos)",
+            "l2": "inputs larger than L2 (1.07 GB 16-bit field vs 126 MB L2), no flush"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: CPU restatement on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-
-    occ = O.random_maze(W, H, DENSITY, GRID_SEED)
-    src = sample_points(occ, N_SOURCES, PT_SEED)
-    sm = O.source_mask(occ, src)
+    O, isa = load_oracle()
+    occ, src, tgt = make_workload(O.random_maze)
     threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    O.propagate(occ, sm, 1, threads=threads)
-    one = time.perf_counter() - t0
-    L = max(1, min(64, int(15.0 / max(one, 1e-3) / max(1, args.steps + args.warmup))))
-    for _ in range(args.warmup):
-        O.propagate(occ, sm, L, threads=threads)
-    times = []
-    for _ in range(args.steps):
+    sm = O.source_mask(occ, src)
+    times = cpu_slices(O, occ, src, CPU_SLICE_LAYERS, args.warmup + args.steps, threads)[args.warmup:]
+    ms = 1000 * statistics.mean(times)
+    value = W * H * CPU_SLICE_LAYERS / (ms / 1000) / 1e9
+    hops = O.bfs_multi_source(occ, sm)
+    L_used, _ = predicted_auto(O, occ, hops, AUTO_CAP)
+    del hops
+    # full CPU solves of the two configurations that finish in seconds on the host (SURVEY.md §8d)
+    full = []
+    c1 = O.random_maze(1024, 1024, 0.30, 1)
+    s1 = O.sample_free_cells(c1, 1, 1)
+    for name, occ_c, src_c, cap in (("C1 1024^2 random 0.30, 1 source", c1, s1, 4 * 1024),
+                                    ("C2 4096^2 Kruskal maze, 16 sources", O.kruskal_maze(4096, 4096, 2), None,
+                                     4096 * 4096)):
+        if src_c is None:
+            src_c, _ = points_for(occ_c, 16, 16, 2)
         t0 = time.perf_counter()
-        O.propagate(occ, sm, L, threads=threads)
-        times.append(time.perf_counter() - t0)
-    ms = 1000 * sum(times) / len(times)
-    value = W * H * L / (ms / 1000) / 1e9
+        _, lu, cause = O.propagate_auto(occ_c, O.source_mask(occ_c, src_c), cap, threads=threads)
+        dt = time.perf_counter() - t0
+        full.append({"config": name, "time_to_solve_s": round(dt, 3), "layers_used": lu, "cause": cause,
+                     "gcell_per_s": round(occ_c.size * lu / dt / 1e9, 3)})
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": bench_config(world),
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                             "cpu_model": cpu_model(),
-                             "sample": f"oracle propagate (the CPU restatement; the reference has no buildable "
-                                       f"sources), fixed L={L} slice over the full C4 grid per step"},
+                             "cpu_model": cpu_model(), "isa": isa,
+                             "sample": f"oracle propagate_layer x {CPU_SLICE_LAYERS} layers over the full C4 grid "
+                                       f"per step (buffers preallocated; the reference has no buildable sources)",
+                             "extrapolated_time_to_solve_s": round(W * H * L_used / (value * 1e9), 1),
+                             "layers_used_bfs": L_used},
+            "full_solves": full,
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ GPU arm
 class Solver:
     """One timed step = propagate_auto to the fixed point + Euclidean paths of this rank's targets to the host.
 
@@ -276,10 +400,16 @@ class Solver:
             self.h_status.copy_(self.d_status, non_blocking=True)
         return r
 
+    def host_paths(self):
+        """(offsets, points (total, 2), status) of the last step, from the pinned host copies."""
+        self.ctx.synchronize()
+        return (self.h_off.numpy().view(np.uint64), self.h_pts.numpy().view(np.uint32).reshape(-1, 2),
+                self.h_status.numpy())
+
     def close(self):
-        del self.h_pts, self.h_off, self.h_status, self.d_pts, self.d_off, self.d_status, self.d_tgt
         self.torch.cuda.synchronize()
         self.ctx.synchronize()
+        del self.h_pts, self.h_off, self.h_status, self.d_pts, self.d_off, self.d_status, self.d_tgt
         if self.slab is not None:
             self.slab.close()
         self.full.close()
@@ -322,6 +452,95 @@ def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts, split=None):
     return off, pts, st, t2 - t0
 
 
+def timed_median(fn, reps=3):
+    fn()  # warm-up
+    ts, out = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), out
+
+
+def run_configs(am, torch, ctx, info_c4, occ4, src4, hops4, parity):
+    """The other BASELINE.json configurations on one GPU, inputs resident in HBM, paths to pinned host
+    memory, median of 3 solves after a warm-up (host wall clock around synchronous library calls)."""
+    out = []
+    O = load_oracle()[0] if parity else None
+    h_pts = torch.empty((8 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    tile_cells = info_c4["tile_rows"] * info_c4["tile_cols"] * LAYERS_PER_BLOCK
+
+    def grid_cfg(name, occ, src, tgt, cap, fixed=None, hops=None):
+        hh, ww = occ.shape
+        g = am.Grid(occ, src, ctx)
+
+        def run():
+            r = g.propagate(fixed) if fixed else g.propagate_auto(cap)
+            if not len(tgt):
+                return r, np.zeros(1, np.uint64), h_pts[:0], np.zeros(0, np.int32)
+            off, pts, st = g.trace(tgt, am.EUCLIDEAN, out=h_pts)
+            return r, off, pts, st
+        t, (r, off, pts, st) = timed_median(run)
+        L = fixed or r.layers_used
+        e = {"config": name, "grid": [ww, hh], "sources": len(src), "targets": len(tgt),
+             "time_to_solve_s": round(t, 5), "layers_used": r.layers_used,
+             "termination": ["filled", "stalled", "cap", "fixed"][r.cause if not fixed else 3],
+             "dense_equivalent_gcell_per_s": round(ww * hh * L / t / 1e9, 1),
+             "executed_gcell_per_s": round(r.tiles_processed * tile_cells / t / 1e9, 1) if r.tiles_total else None,
+             "paths_covered": int((st == 0).sum())}
+        if parity:
+            p, _ = check_grid(O, occ, src, g.activity(), L, None if fixed else cap, tgt, off, pts, st, PARITY_PATHS,
+                              hops)
+            e["parity"] = p
+            e["parity_ok"] = parity_ok(p)
+        g.close()
+        log(f"config {name}: {json.dumps(e)}")
+        return e
+
+    occ, src, tgt, cap = c2_workload(am)
+    out.append(grid_cfg("C2 4096^2 Kruskal maze, 16 sources / 16 targets, auto", occ, src, tgt, cap))
+    occ, src, tgt, cap = c3_workload(am)
+    out.append(grid_cfg("C3 16384^2 city grid, 64 sources / 1000 targets, auto", occ, src, tgt, cap))
+    del occ
+    out.append(grid_cfg("C4-fixed: the C4 grid, fixed L=1024", occ4, src4, np.zeros((0, 2), np.uint32), None,
+                        fixed=1024, hops=hops4))
+    mazes, srcs, tg, cap = c5_workload(am)
+    b = am.Batch(mazes, srcs, ctx)
+
+    def run5():
+        used, cause, r = b.propagate(auto_cap=cap)
+        off, pts, st = b.trace(tg, am.EUCLIDEAN, out=h_pts)
+        return used, cause, r, off, pts, st
+    t, (used, cause, r, off, pts, st) = timed_median(run5)
+    n = len(mazes)
+    cells = int(256 * 256 * np.asarray(used, np.int64).sum())
+    e = {"config": f"C5 {n} x 256^2 random mazes (0.30), 1 source + 8 targets each, cap {cap}",
+         "time_to_solve_s": round(t, 5), "mazes_per_s": round(n / t, 1),
+         "dense_equivalent_gcell_per_s": round(cells / t / 1e9, 1), "paths": int(len(tg)),
+         "paths_covered": int((st == 0).sum()), "kernel": getattr(r, "kernel", None)}
+    if parity:
+        maps = b.activity()
+        bad = mism = wrong_auto = 0
+        for i in range(n):
+            sm = O.source_mask(mazes[i], srcs[i])
+            hops = O.bfs_multi_source(mazes[i], sm)
+            bad += O.check_activity(mazes[i], maps[i], hops, int(used[i]))[0]
+            wrong_auto += predicted_auto(O, mazes[i], hops, cap) != (int(used[i]), int(cause[i]))
+        for k, (i, rr, cc) in enumerate(tg):
+            sm = O.source_mask(mazes[i], srcs[i])
+            ost, opts = O.reconstruct_euclidean(mazes[i], sm, maps[i], (rr, cc), cap=int(used[i]) + 2)
+            if int(st[k]) != ost or (ost == 0 and not np.array_equal(pts[int(off[k]):int(off[k + 1])], opts)):
+                mism += 1
+        p = {"mazes_checked": n, "cells_checked": int(mazes.size), "law_violations": int(bad),
+             "auto_outcome_mismatches": int(wrong_auto), "paths_checked": int(len(tg)), "path_mismatches": mism}
+        e["parity"] = p
+        e["parity_ok"] = bad == 0 and mism == 0 and wrong_auto == 0
+    b.close()
+    log(f"config C5: {json.dumps(e)}")
+    out.append(e)
+    return out
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
 
@@ -332,7 +551,7 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
 
-    occ, src, tgt = make_workload(am)
+    occ, src, tgt = make_workload(am.random_maze)
     ctx = am.Context(local_rank, timing=True)
     if world > 1:
         uid = [am.comm_unique_id() if rank == 0 else None]
@@ -417,20 +636,22 @@ def run_b200(args, rank, world, local_rank):
             ms = rr.stencil_ms / max(rr.block_launches, 1)
             best = ms if best is None else min(best, ms)
         dg.close()
+        dctx.close()
         dbytes = BYTES_PER_CELL_UPDATE * W * H * LAYERS_PER_BLOCK
         dense = {"kernel": "am::k_block<16> (dense, fixed L=64 on the C4 grid)", "mean_launch_ms": round(best, 4),
                  "gcell_per_s": round(W * H * LAYERS_PER_BLOCK / (best / 1000) / 1e9, 1),
                  "achieved": round(dbytes / (best / 1000) / 1e9, 1), "peak": peak, "unit": "GB/s",
                  "frac": round(dbytes / (best / 1000) / 1e9 / peak, 3), "traffic": ncu_traffic("dense")}
 
-    # end-to-end through the C ABI with host buffers (H2D of the grid, D2H of map + paths inside the timing)
+    # end-to-end through the C ABI with host buffers (H2D of the grid, D2H of map + paths inside the timing):
+    # one warm-up solve, then the median of 3
     e2e = None
     if not args.no_e2e:
         h_occ = torch.from_numpy(occ).pin_memory().numpy()
         h_map = torch.empty((H, W), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         h_pts = torch.empty((16 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         e2e_times, full_times, split = [], [], {}
-        for i in range(3):
+        for i in range(4):
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -449,7 +670,7 @@ def run_b200(args, rank, world, local_rank):
         h2d = occ.nbytes + src.nbytes + tgt.nbytes * 2 // world + off2.nbytes + st2.nbytes
         d2h = pts2.nbytes + off2.nbytes + st2.nbytes * 2
         e2e = {"value": round(cell_updates / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "time_to_solve_s": round(e2e_s, 4),
+               "d2h_bytes_per_step": int(d2h), "time_to_solve_s": round(e2e_s, 4), "runs": len(e2e_times),
                "split_ms": {k: round(1000 * statistics.median(v), 2) for k, v in split.items()},
                "with_full_map_download": {"value": round(cell_updates / full_s / 1e9, 3),
                                           "time_to_solve_s": round(full_s, 4),
@@ -458,11 +679,25 @@ def run_b200(args, rank, world, local_rank):
                       "am_trace_paths (every path to pinned host memory); the uint32 activity map stays on the "
                       "device (the C++ ActivityMap fetches it lazily) and its download is reported separately" +
                       ("; per rank: slab grid, NCCL halos, am_comm_gather" if world > 1 else "")}
+        del h_occ, h_map, h_pts
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(occ, src)
-        cpu["extrapolated_time_to_solve_s"] = round(cell_updates / (cpu["value"] * 1e9), 1)  # W*H*L_used / rate
+    # ---- CPU leg (rank 0, N=1): the oracle as baseline and as the checker of what was just timed ----
+    cpu = parity = configs = None
+    hops4 = None
+    solo = rank == 0 and world == 1
+    if solo and not args.no_cpu_baseline:
+        cpu = cpu_baseline(occ, src, L)
+    if solo and not args.no_parity:
+        O = load_oracle()[0]
+        off_h, pts_h, st_h = sol.host_paths()
+        parity, hops4 = check_grid(O, occ, src, sol.full.activity(), L, AUTO_CAP, sol.tgt, off_h, pts_h, st_h,
+                                   PARITY_PATHS)
+        parity["auto_outcome_matches_bfs"] = predicted_auto(O, occ, hops4, AUTO_CAP) == (L, res.cause)
+        parity["ok"] = parity_ok(parity)
+        parity["instance"] = "the timed C4 instance (bench.py's own grid, sources and targets)"
+        log(f"parity: {json.dumps(parity)}")
+    if solo and not args.no_configs:
+        configs = run_configs(am, torch, ctx, info, occ, src, hops4, not args.no_parity)
 
     if rank == 0:
         line = {
@@ -495,12 +730,17 @@ def run_b200(args, rank, world, local_rank):
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     # teardown order: torch's pinned-memory allocator records events on the context stream when these
     # buffers die, so release them (and sync) before the context and its stream go away
     sol.close()
-    return ctx
+    del sol
+    gc.collect()
+    torch.cuda.synchronize()
+    ctx.close()
 
 
 def main():
@@ -511,6 +751,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed instance")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C4-fixed/C5 block")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -524,14 +766,13 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
-    keep = run_b200(args, rank, world, local_rank)
+    run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
     sys.stdout.flush()
     sys.stderr.flush()
-    os._exit(0)  # skip interpreter teardown (ctx/stream vs torch caching allocators)
 
 
 if __name__ == "__main__":

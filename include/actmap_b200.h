@@ -102,6 +102,9 @@ am_status am_grid_create(am_ctx *ctx, uint32_t width, uint32_t height, const uin
 am_status am_grid_create_device(am_ctx *ctx, uint32_t width, uint32_t height, const uint8_t *d_occupancy,
                                 const uint32_t *d_src_rc, uint64_t n_src, am_grid **out);
 am_status am_grid_destroy(am_ctx *ctx, am_grid *grid);
+/* A new grid with the same occupancy and SourceSet, built on the device from
+ * `grid`'s resident copies (no host data; `grid` may be destroyed after). */
+am_status am_grid_clone(am_ctx *ctx, const am_grid *grid, am_grid **out);
 am_status am_grid_get_info(const am_grid *grid, am_grid_info *out);
 
 /* ---- propagation (propagate.hpp:40-61) ---------------------------------
@@ -134,7 +137,8 @@ am_status am_trace_paths(am_ctx *ctx, am_grid *grid, const uint32_t *tgt_rc, uin
                          int32_t *status);
 /* Device-resident variant: targets, offsets (n+1), points and status are
  * device pointers; counts, scan and trace run back to back on the stream
- * with no host round trip.  pts capacity must be >= the total. */
+ * with no host round trip.  A target whose points would end past
+ * pts_capacity gets status AM_EINVAL and nothing is written for it. */
 am_status am_trace_paths_device(am_ctx *ctx, am_grid *grid, const uint32_t *d_tgt_rc, uint64_t n,
                                 uint32_t method, uint64_t seed, uint64_t *d_offsets, uint32_t *d_pts_rc,
                                 uint64_t pts_capacity, int32_t *d_status);

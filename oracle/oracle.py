@@ -14,7 +14,9 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# ORACLE_LIB: an alternative build of the same sources (bench.py builds `make native`, -march=native, on the
+# host it times; the default .so is portable x86-64-v3)
+_LIB_PATH = os.environ.get("ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
 
 OK, EINVAL, EUNCOVERED, EINTERNAL = 0, 1, 2, 6
 UNREACH = 0xFFFFFFFF
@@ -157,10 +159,12 @@ def initial(occ, srcmask):
     return out
 
 
-def propagate_layer(occ, srcmask, act, threads=1):
+def propagate_layer(occ, srcmask, act, threads=1, out=None):
+    """out: optional preallocated (h, w) uint32 C-contiguous buffer (no allocation inside a timed loop)."""
     occ, sm, a = _u8(occ), _u8(srcmask), _u32(act)
     h, w = occ.shape
-    out = np.empty((h, w), np.uint32)
+    if out is None or out.shape != (h, w) or out.dtype != np.uint32 or not out.flags.c_contiguous:
+        out = np.empty((h, w), np.uint32)
     _chk(lib().or_propagate_layer(w, h, _p(occ, _u8p), _p(sm, _u8p), _p(a, _u32p), _p(out, _u32p), threads))
     return out
 

@@ -10,6 +10,7 @@ CPU fallback -- importing works without a GPU, the first device call raises
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import threading
@@ -105,6 +106,7 @@ def lib():
             "am_grid_create": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
             "am_grid_create_device": (st, [_vp, u32, u32, _vp, _vp, u64, C.POINTER(_vp)]),
             "am_grid_destroy": (st, [_vp, _vp]),
+            "am_grid_clone": (st, [_vp, _vp, C.POINTER(_vp)]),
             "am_grid_get_info": (st, [_vp, C.POINTER(_GridInfo)]),
             "am_propagate": (st, [_vp, _vp, u32, u32, u32, C.POINTER(_PropResult)]),
             "am_activity_download": (st, [_vp, _vp, _vp]),
@@ -185,6 +187,7 @@ class Context:
         self.handle = h
         self.device = device
         self._owned = weakref.WeakSet()  # grids / batches: closed before the context
+        _live_contexts.add(self)
 
     def _own(self, obj):
         self._owned.add(obj)
@@ -249,6 +252,18 @@ class Context:
 
 
 _default = None
+_live_contexts = weakref.WeakSet()
+
+
+@atexit.register
+def _close_contexts():
+    """Destroy every live context (its grids first) while the CUDA runtime is still up: a context left to the
+    garbage collector at interpreter teardown would release its stream and pool after torch / cudart shut down."""
+    for c in list(_live_contexts):
+        try:
+            c.close()
+        except Exception:
+            pass
 
 
 def default_context() -> Context:

@@ -109,6 +109,13 @@ struct DeviceMap {
     check(am_grid_create(ctx, width, height, g.occupancy().data(), rc.data(), sources.size(), &grid), ctx,
           "grid upload");
   }
+  // same grid and sources, built on the device from `from`'s resident copies (no host GridMap needed)
+  explicit DeviceMap(const DeviceMap& from)
+      : ctx(from.ctx), width(from.width), height(from.height), occ_ptr(from.occ_ptr), obstacles(from.obstacles),
+        occ_hash(from.occ_hash), sources(from.sources) {
+    check(am_grid_clone(ctx, from.grid, &grid), ctx, "grid clone");
+  }
+  DeviceMap& operator=(const DeviceMap&) = delete;
   ~DeviceMap() {
     if (grid) am_grid_destroy(ctx, grid);
   }
@@ -327,11 +334,11 @@ uint64_t ActivityMap::zero_free_cells(const GridMap& grid) const {
 ActivityMap propagate_layer(const ActivityMap& activity, const GridMap& grid, const SourceSet& sources, unsigned) {
   if (activity.width() != grid.width() || activity.height() != grid.height())
     throw InvalidInputError("propagate_layer: activity/grid dimension mismatch");
+  const auto in = activity.values();  // before taking the API lock (a lazy download takes it)
   std::lock_guard<std::mutex> lk(api_mutex());
   am_ctx* ctx = default_ctx();
   const auto rc = flatten(sources.coords());
   std::vector<uint32_t> out(grid.cell_count());
-  const auto in = activity.values();
   check(am_propagate_layer(ctx, grid.width(), grid.height(), grid.occupancy().data(), rc.data(), sources.size(),
                            in.data(), out.data()),
         ctx, "propagate_layer");
@@ -498,12 +505,12 @@ namespace b200 {
 struct PlannerImpl {
   std::shared_ptr<detail::DeviceMap> dev;
   uint32_t width, height;
-  const GridMap* grid;
-  std::vector<Coord> sources;
   // A map returned earlier still refers to `dev` (ActivityMap fetches its values lazily): before the
   // next propagation overwrites the device map, give the planner a fresh one so that map keeps its values.
+  // The fresh grid is cloned on the device, so the planner never touches the caller's GridMap after
+  // construction (it may die first).
   void own_map() {
-    if (dev.use_count() > 1) dev = std::make_shared<detail::DeviceMap>(*grid, SourceSet(*grid, sources));
+    if (dev.use_count() > 1) dev = std::make_shared<detail::DeviceMap>(*dev);
   }
 };
 
@@ -514,8 +521,6 @@ Planner::Planner(const GridMap& grid, const SourceSet& sources, DeviceOptions op
   impl->dev = std::make_shared<detail::DeviceMap>(grid, sources);
   impl->width = grid.width();
   impl->height = grid.height();
-  impl->grid = &grid;
-  impl->sources = sources.coords();
   impl_ = impl;
 }
 

@@ -193,7 +193,8 @@ void launch_path_counts(const MapView& m, const uint32_t* tgt_rc, uint64_t n, in
                         uint64_t* counts, int32_t* status, cudaStream_t s);
 void launch_scan(const uint64_t* counts, uint64_t n, uint64_t* offsets, cudaStream_t s);
 void launch_trace(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int method, uint64_t seed,
-                  const uint64_t* offsets, uint32_t* pts_rc, int32_t* status, cudaStream_t s);
+                  const uint64_t* offsets, uint32_t* pts_rc, int32_t* status, cudaStream_t s,
+                  uint64_t pts_capacity = ~0ull);
 // paths in a grid of mazes packed on a cell_h x cell_w lattice -> each path's maze-local coordinates
 // (the maze is the one of the path's first point, its target)
 void launch_paths_local(uint32_t* pts_rc, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,

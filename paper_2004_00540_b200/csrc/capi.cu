@@ -279,6 +279,12 @@ am_status am_grid_create_device(am_ctx* ctx, uint32_t W, uint32_t H, const uint8
   return am::grid_create_rows(ctx, W, H, 0, H, occ, src, n_src, true, false, out);
 }
 
+am_status am_grid_clone(am_ctx* ctx, const am_grid* g, am_grid** out) {
+  if (!ctx || !g || !out) return AM_EINVAL;
+  if (g->slab) return am::fail(ctx, AM_EINVAL, "am_grid_clone: slab grids are not cloneable");
+  return am::grid_create_rows(ctx, g->g.W, g->g.H, 0, g->g.H, g->occ, g->src_rc, g->n_src, true, false, out);
+}
+
 am_status am_grid_destroy(am_ctx* ctx, am_grid* g) {
   if (!g) return AM_OK;
   if (!ctx) return AM_EINVAL;  // the grid's buffers belong to the context's pool
@@ -1015,8 +1021,8 @@ am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, 
   if (g->plain_active) return am::fail(ctx, AM_EINVAL, "device path tracing needs a propagated map");
   if (g->slab) return am::fail(ctx, AM_EINVAL, "path extraction on a slab: gather the map first");
   if (method > 1) return am::fail(ctx, AM_EINVAL, "bad method");
-  (void)cap;
   if (!n) return AM_OK;
+  if (!d_pts && cap) return am::fail(ctx, AM_EINVAL, "null point buffer");
   CK(cudaSetDevice(ctx->device));
   am_status st = ensure_targets(ctx, g, n);
   if (st) return st;
@@ -1026,7 +1032,7 @@ am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, 
   CKL();
   am::launch_scan(g->d_counts, n, d_offsets, s);
   CKL();
-  am::launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, s);
+  am::launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, s, cap);  // paths past cap: AM_EINVAL
   CKL();
   return AM_OK;
 }

@@ -482,6 +482,9 @@ const Value& field(const Value& o, const char* k) {
   bad(std::string("missing field \"") + k + "\"");
 }
 const Array& arr(const Value& v, const char* what) {
+  // "[]" under a "points" / "samples" key reads as an empty coordinate array: it is also an empty array
+  static const Array kEmpty;
+  if (v.kind == Value::kCoords && v.pairs->empty()) return kEmpty;
   if (v.kind != Value::kArray) bad(std::string(what) + " must be an array");
   return *v.arr;
 }

@@ -400,12 +400,16 @@ __global__ void k_path_counts(MapView m, const uint32_t* __restrict__ tgt, uint6
 
 __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method, uint64_t seed,
                         const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pts,
-                        int32_t* __restrict__ status) {
+                        int32_t* __restrict__ status, uint64_t cap) {
   const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= n) return;
   if (status[w] != ST_OK) return;
   Reader rd{m};
   const uint64_t off = offsets[w], limit = offsets[w + 1] - off;
+  if (offsets[w + 1] > cap) {  // the caller's point buffer ends before this path: report, never write past it
+    if ((threadIdx.x & 31) == 0) status[w] = ST_EINVAL;
+    return;
+  }
   int32_t st = ST_OK;
   __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
   uint8_t* win = wins[(threadIdx.x >> 5) & 3];
@@ -451,10 +455,10 @@ void launch_paths_local(uint32_t* pts, const uint64_t* offsets, const int32_t* s
 }
 
 void launch_trace(const MapView& m, const uint32_t* tgt, uint64_t n, int method, uint64_t seed,
-                  const uint64_t* offsets, uint32_t* pts, int32_t* status, cudaStream_t s) {
+                  const uint64_t* offsets, uint32_t* pts, int32_t* status, cudaStream_t s, uint64_t cap) {
   if (!n) return;
   const unsigned blocks = (unsigned)((n * 32 + 127) / 128);
-  k_trace<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status);
+  k_trace<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap);
 }
 
 }  // namespace am

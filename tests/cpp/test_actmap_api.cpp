@@ -3,6 +3,7 @@
 // tests/test_cpp_api.py; prints one line per check, exits nonzero on failure.
 #include <cmath>
 #include <cstdio>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -163,6 +164,30 @@ int main() {
     CHECK(b.at(4, 4) == 6 && b.layers_applied() == 5);
     CHECK(c.layers_used == 4 && c.map.at(4, 4) == 5 && c.map.at(0, 0) == 1);
     CHECK(a == propagate(g, src, 3) && b == propagate(g, src, 5));
+    // a device-backed (not yet downloaded) map fed to propagate_layer: the lazy download must not
+    // re-enter the API lock
+    const ActivityMap d3 = propagate(g, src, 3);
+    CHECK(propagate_layer(d3, g, src) == propagate(g, src, 4));
+    const ActivityMap p3 = planner.propagate(3);
+    CHECK(propagate_layer(p3, g, src) == b200::Planner(g, src).propagate(4));
+  }
+  // the planner does not depend on the caller's GridMap after construction (it may die first)
+  {
+    auto g = std::make_unique<GridMap>(random_maze(64, 48, 0.3, 11));
+    const std::vector<Coord> s{{0, 0}, {47, 63}};
+    std::vector<Coord> free_s;
+    for (Coord c : s)
+      if (g->is_free(c)) free_s.push_back(c);
+    if (free_s.empty()) free_s.push_back(Coord{1, 1});
+    const GridMap copy = *g;
+    const SourceSet src(*g, free_s);
+    b200::Planner planner(*g, src);
+    const SourceSet src_copy(copy, free_s);
+    g.reset();  // the planner's grid is gone
+    const ActivityMap a = planner.propagate(7);      // shares the planner's device map
+    const AutoResult b = planner.propagate_auto(400);  // a is alive: the planner clones its grid on the device
+    CHECK(a == propagate(copy, src_copy, 7));
+    CHECK(b.map == propagate_auto(copy, src_copy, 400).map);
   }
   // map / scene text (mapio.hpp)
   {

@@ -103,6 +103,15 @@ int main() {
   const size_t cut = j.find("\"timing\":");
   CHECK(cut != std::string::npos && j.compare(0, cut, j2, 0, cut) == 0 && j != j2);
   CHECK(j.find("\"timing\":") > j.find("\"bench\":"));
+  // empty sample lists ("samples": [] reads like an empty coordinate array) round-trip exactly
+  {
+    RunReport e = r;
+    e.bench = BenchReport{};
+    e.validation->activity.samples.clear();
+    const std::string je = serialize_run_report(e);
+    CHECK(parse_run_report(je) == e);
+    CHECK(serialize_run_report(parse_run_report(je)) == je);
+  }
   // rejections
   {
     std::string bad = j;

@@ -56,12 +56,50 @@ def test_batch_small_mixed_outcomes():
     b.close()
 
 
-def test_batch_c5_shape():
-    """4096 x 256^2 (config C5), checked on a sample of mazes."""
-    n = 4096
-    occ, src = make_batch(n, 256, 256, 5000)
+def predicted_auto(occ, hops, cap):
+    """propagate_auto's (L_used, cause) from the BFS alone (pin P3)."""
+    reach = hops != O.UNREACH
+    maxd = int(hops[reach].max())
+    unreachable_free = bool(((occ == 0) & ~reach).any())
+    lu, cause = (max(1, maxd), O.FILLED) if not unreachable_free else (maxd + 1, O.STALLED)
+    if lu > cap:
+        lu, cause = cap, (O.FILLED if (not unreachable_free and maxd <= cap) else O.CAP)
+    return lu, cause
+
+
+def c5_workload(n=4096):
+    """config C5 exactly as bench.py runs it (bench.c5_workload): 256^2 random mazes (0.30, seeds 5000+i),
+    1 source and 8 targets each"""
+    import bench
+
+    occ, src, tg, cap = bench.c5_workload(am, n)
+    assert cap == 1024
+    return occ, src, tg
+
+
+def test_batch_c5_every_maze():
+    """4096 x 256^2 (config C5): EVERY maze's map (closed-form law against a CPU BFS: all cells), L_used and
+    cause (predicted from the BFS), and every one of the 32768 Euclidean paths against the oracle's
+    reconstruction on the device map; a sample of mazes also against the oracle's full propagate_auto."""
+    n, cap = 4096, 1024
+    occ, src, tg = c5_workload(n)
     b = am.Batch(occ, src)
-    check(b, occ, src, 1024, list(range(0, n, 257)) + [n - 1])
+    lu, cause, _ = b.propagate(auto_cap=cap)
+    maps = b.activity()
+    for i in range(n):
+        sm = O.source_mask(occ[i], src[i])
+        hops = O.bfs_multi_source(occ[i], sm)
+        assert (int(lu[i]), int(cause[i])) == predicted_auto(occ[i], hops, cap), i
+        bad, where = O.check_activity(occ[i], maps[i], hops, int(lu[i]))
+        assert bad == 0, (i, where)
+    off, pts, st = b.trace(tg, am.EUCLIDEAN, 0)
+    for k, (i, r, c) in enumerate(tg):
+        sm = O.source_mask(occ[i], src[i])
+        ost, opts = O.reconstruct_euclidean(occ[i], sm, maps[i], (r, c), cap=int(lu[i]) + 2)
+        assert st[k] == ost, (i, r, c)
+        if ost == 0:
+            assert np.array_equal(pts[off[k]:off[k + 1]], opts), (i, r, c)
+    check(b, occ, src, cap, list(range(0, n, 257)) + [n - 1])
     b.close()
 
 

@@ -80,13 +80,13 @@ def test_c3_city_16384():
 
 
 def test_c4_dense_23170():
+    """The exact instance bench.py times (its own grid, sources and 4096 targets)."""
+    import bench
+
     n = 23170
-    occ = am.random_maze(n, n, 0.40, 4)
+    occ, src, tg = bench.make_workload(am.random_maze)
     assert np.array_equal(occ[:64], O.random_maze(n, n, 0.40, 4)[:64])
-    src = O.sample_free_cells(occ, 64, 4)
-    sm = O.source_mask(occ, src)
-    tg = O.sample_free_cells(occ, 4096, 5, exclude=sm)
-    r = run_config(occ, src, tg, 4 * n, fixed_slice=64)
+    r = run_config(occ, src, tg, bench.AUTO_CAP, fixed_slice=64)
     assert r.cell_bits == 16 and r.block_launches > 0
 
 

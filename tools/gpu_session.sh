@@ -18,7 +18,7 @@ if [[ "$ARGS" == *" bench "* ]]; then
   cat gpurun_out/bench.json; grep -v "^frame" gpurun_out/bench.err | tail -4
 fi
 if [[ "$ARGS" == *" ncu "* ]]; then
-  CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+  CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-parity --no-configs"
   timeout 300 $CMD > gpurun_out/plain.log 2>&1; rc=$?; echo "plain_rc=$rc"
   if [ $rc -eq 0 ]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 2200 -c 2000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo "ncu_list_rc=$?"
