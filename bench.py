@@ -401,10 +401,11 @@ class Solver:
         return r
 
     def host_paths(self):
-        """(offsets, points (total, 2), status) of the last step, from the pinned host copies."""
+        """(offsets, points (total, 2), status) of the last step, copied out of the pinned buffers (a numpy view
+        would keep torch's pinned block alive past the context's stream, which its allocator records on)."""
         self.ctx.synchronize()
-        return (self.h_off.numpy().view(np.uint64), self.h_pts.numpy().view(np.uint32).reshape(-1, 2),
-                self.h_status.numpy())
+        return (self.h_off.numpy().view(np.uint64).copy(),
+                self.h_pts.numpy().view(np.uint32).reshape(-1, 2)[: self.total].copy(), self.h_status.numpy().copy())
 
     def close(self):
         self.torch.cuda.synchronize()
@@ -517,7 +518,8 @@ def run_configs(am, torch, ctx, info_c4, occ4, src4, hops4, parity):
     e = {"config": f"C5 {n} x 256^2 random mazes (0.30), 1 source + 8 targets each, cap {cap}",
          "time_to_solve_s": round(t, 5), "mazes_per_s": round(n / t, 1),
          "dense_equivalent_gcell_per_s": round(cells / t / 1e9, 1), "paths": int(len(tg)),
-         "paths_covered": int((st == 0).sum()), "kernel": getattr(r, "kernel", None)}
+         "paths_covered": int((st == 0).sum()), "layers_used_max": int(np.max(used)),
+         "layers_used_mean": round(float(np.mean(used)), 1)}
     if parity:
         maps = b.activity()
         bad = mism = wrong_auto = 0

@@ -14,6 +14,7 @@
 // paths are traced on the packed field directly.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -25,6 +26,8 @@ struct am_batch {
   uint32_t n = 0, mw = 0, mh = 0, tiles_x = 0, tiles_y = 0;
   std::vector<uint32_t> layers_used, cause;  // per maze, after am_batch_propagate
   int have = 0;
+  uint64_t* d_src_off = nullptr;  // K5: per-maze offsets into grid->src_rc (n + 1)
+  uint32_t* d_k5 = nullptr;       // K5 scratch: used[n], cause[n], fetch counter
 };
 
 namespace am {
@@ -102,6 +105,206 @@ __global__ void k_batch_decode(Geo g, const void* __restrict__ val, uint32_t mw,
   }
 }
 
+// ---- K5: one CTA per maze, the whole maze on chip ------------------------------------------------------
+//
+// A layer's output differs from "every covered cell +1" (propagate.hpp:34-38 applied to a map whose covered
+// cells already gained their +1) only at free, uncovered cells whose 3x3 neighbourhood holds a
+// cell covered in the previous layer: there max3x3(A) = 1 > 0 and the ReLU output turns positive.  K5 runs
+// the layer stack of one maze per CTA on that indicator, bit-parallel: the maze is held as bit planes (free,
+// covered, last layer's new cells; 32 cells per word) in REGISTERS -- thread (g, k) owns word column k of
+// the R rows [g*R, g*R+R) -- and a layer is, per word, the 3x3 max of the new-cell indicator (OR of the
+// three rows: registers plus one halo word above and below published through shared memory; x | x<<1 |
+// x>>1 plus the carries of the neighbour words: two lane shuffles), masked by free & ~covered.  Every
+// other cell's value follows lazily: a cell covered at layer t holds L+1-t after L layers.  HBM is
+// touched once for the occupancy (read) and once per cell for its encoded value (written into the packed
+// field the trace and the download read, relative to L_ref = the cap / fixed L, so a maze's rollback is
+// the existing `computed - layers_used` shift).  The per-layer count of new cells (one CTA barrier per
+// layer) gives each maze's own auto-L outcome (pin P3) exactly.  CTAs fetch mazes dynamically.
+constexpr int kWaveThreads = 256;
+
+struct WaveArgs {
+  Geo g;
+  const uint8_t* occ;       // packed dense occupancy (g.W x g.H, row stride g.W)
+  uint16_t* field;          // packed encoded field (16-bit cells)
+  const uint32_t* src_rc;   // packed-field coordinates of every maze's sources, maze by maze
+  const uint64_t* src_off;  // n + 1 offsets into src_rc (pairs)
+  uint32_t n, mw, mh, tiles_x;
+  uint32_t ww;              // words per maze row (ceil(mw / 32)); lanes per row group: wwp = pow2 >= ww
+  uint32_t wwp_log2;
+  uint32_t limit;           // auto: cap; fixed: L
+  int autom;
+  uint32_t lref;            // encoded values are lref + 1 - t
+  uint32_t* used;           // per maze layers_used
+  uint32_t* cause;          // per maze AM_STOP_*
+  uint32_t* next;           // maze fetch counter (0 at launch)
+};
+
+// R rows per thread; shared memory: two staging planes (mh x ww words: free cells, sources) and the
+// double-buffered halo rows (2 x groups x {top, bottom} x wwp words)
+template <int R, int T>
+__global__ void __launch_bounds__(T, (R * T) <= 2048 ? 1024 / T : ((R * T) <= 4096 ? 512 / T : 1)) k_batch_wave(WaveArgs a) {
+  extern __shared__ uint32_t wsm[];
+  const uint32_t ww = a.ww, wwp = 1u << a.wwp_log2, groups = T >> a.wwp_log2;
+  const uint32_t nwords = a.mh * ww;
+  uint32_t* s_free = wsm;
+  uint32_t* s_src = s_free + nwords;
+  uint32_t* halo = s_src + nwords;  // [2][groups][2][wwp]
+  __shared__ uint32_t s_maze, s_cnt, s_new[3];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t k = tid & (wwp - 1), grp = tid >> a.wwp_log2, row0 = grp * R;
+  const bool kin = k < ww;
+  for (;;) {
+    if (tid == 0) {
+      s_maze = atomicAdd(a.next, 1u);
+      s_cnt = 0;
+      s_new[0] = s_new[1] = s_new[2] = 0;
+    }
+    for (uint32_t q = tid; q < nwords; q += T) s_src[q] = 0;
+    __syncthreads();
+    const uint32_t i = s_maze;
+    if (i >= a.n) break;
+    const uint32_t r0 = (i / a.tiles_x) * (a.mh + 1), c0 = (i % a.tiles_x) * (a.mw + 1);
+    // occupancy -> free plane (a warp per row, one ballot per 32 cells, the row's loads issued together)
+    // + the maze's layer-0 values in the field (free: flag, obstacle: 0)
+    uint32_t nfree = 0;
+    for (uint32_t r = warp; r < a.mh; r += T / 32) {
+      const uint8_t* orow = a.occ + (size_t)(r0 + r) * a.g.W + c0;
+      const size_t frow = a.g.idx(r0 + r, c0);
+      for (uint32_t kb = 0; kb < ww; kb += 8) {
+        uint8_t o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t c = 32 * (kb + u) + lane;
+          o[u] = (kb + u < ww && c < a.mw) ? orow[c] : 1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t c = 32 * (kb + u) + lane;
+          if (kb + u < ww && c < a.mw) a.field[frow + c] = o[u] ? (uint16_t)0 : (uint16_t)kFlag16;
+          const uint32_t word = __ballot_sync(0xffffffffu, o[u] == 0);
+          if (lane == 0 && kb + u < ww) {
+            s_free[r * ww + kb + u] = word;
+            nfree += __popc(word);
+          }
+        }
+      }
+    }
+    if (lane == 0 && nfree) atomicAdd(&s_cnt, nfree);
+    // sources (layer 0): value lref + 1
+    const uint16_t vsrc = (uint16_t)(kFlag16 | (a.lref + 1));
+    for (uint64_t s = a.src_off[i] + tid; s < a.src_off[i + 1]; s += T) {
+      const uint32_t r = a.src_rc[2 * s] - r0, c = a.src_rc[2 * s + 1] - c0;
+      atomicOr(&s_src[r * ww + (c >> 5)], 1u << (c & 31));
+    }
+    __syncthreads();
+    // planes into registers; layer-0 new cells = the sources
+    uint32_t fr[R], cv[R], nw[R];
+    uint32_t nsrc = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const uint32_t r = row0 + j;
+      const bool in = kin && r < a.mh;
+      fr[j] = in ? s_free[r * ww + k] : 0u;
+      cv[j] = in ? s_src[r * ww + k] : 0u;
+      nw[j] = cv[j];
+      nsrc += __popc(cv[j]);
+      if (cv[j]) {
+        const size_t base = a.g.idx(r0 + r, c0 + 32 * k);
+        for (uint32_t m = cv[j]; m; m &= m - 1) a.field[base + (__ffs(m) - 1)] = vsrc;
+      }
+    }
+    nsrc = __reduce_add_sync(0xffffffffu, nsrc);
+    if (lane == 0 && nsrc) atomicAdd(&s_new[0], nsrc);
+    halo[(grp * 2) * wwp + k] = nw[0];  // layer 0's halo rows: plane 0
+    halo[(grp * 2 + 1) * wwp + k] = nw[R - 1];
+    __syncthreads();
+    const uint32_t free_total = s_cnt;
+    uint32_t covered = s_new[0];
+    uint32_t used = 0, why = AM_STOP_FIXED;
+    const uint32_t hstride = groups * 2 * wwp;
+    // per-thread constants of the layer loop: halo slots (read: the neighbours' rows of the other parity,
+    // write: this group's top / bottom row) and the field address of the thread's first row
+    const uint32_t* rd_up = halo + ((grp - 1) * 2 + 1) * wwp + k;  // + plane * hstride
+    const uint32_t* rd_dn = halo + ((grp + 1) * 2) * wwp + k;
+    uint32_t* wr_top = halo + (grp * 2) * wwp + k;
+    const bool has_up = grp != 0, has_dn = grp + 1 < groups, kfirst = k == 0, klast = k + 1 == wwp;
+    uint16_t* const mz = a.field + a.g.idx(r0 + row0, c0 + 32 * k);
+    const uint32_t pitch = a.g.pitch;
+    for (uint32_t l = 1;; ++l) {
+      const uint32_t rp = (l - 1) & 1, wp = l & 1;  // halo plane read (last layer's) / written
+      if (tid == 0) s_new[(l + 1) % 3] = 0;
+      const uint32_t up = has_up ? rd_up[rp * hstride] : 0u;
+      const uint32_t dn = has_dn ? rd_dn[rp * hstride] : 0u;
+      uint32_t any = up | dn;
+#pragma unroll
+      for (int j = 0; j < R; ++j) any |= nw[j];
+      uint32_t newc = 0;
+      if (__any_sync(0xffffffffu, any)) {
+        const uint16_t val = (uint16_t)(kFlag16 | (a.lref + 1 - l));
+        uint32_t prev = up, v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {  // vertical 3-row OR of last layer's new cells
+          const uint32_t below = j + 1 < R ? nw[j + 1] : dn;
+          v[j] = prev | nw[j] | below;
+          prev = nw[j];
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {  // horizontal: the word itself and the carries of its row neighbours
+          uint32_t lft = __shfl_up_sync(0xffffffffu, v[j], 1);
+          uint32_t rgt = __shfl_down_sync(0xffffffffu, v[j], 1);
+          if (kfirst) lft = 0;
+          if (klast) rgt = 0;
+          const uint32_t h = v[j] | (v[j] << 1) | (v[j] >> 1) | (lft >> 31) | (rgt << 31);
+          const uint32_t n = h & fr[j] & ~cv[j];
+          cv[j] |= n;
+          nw[j] = n;
+          newc += __popc(n);
+        }
+        // the new cells' values
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          uint16_t* row = mz + j * pitch;
+          for (uint32_t m = nw[j]; m; m &= m - 1) row[__ffs(m) - 1] = val;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) nw[j] = 0;
+      }
+      wr_top[wp * hstride] = nw[0];
+      wr_top[wp * hstride + wwp] = nw[R - 1];
+      newc = __reduce_add_sync(0xffffffffu, newc);
+      if (lane == 0 && newc) atomicAdd(&s_new[l % 3], newc);
+      __syncthreads();
+      const uint32_t got = s_new[l % 3];
+      covered += got;
+      // pin P3: filled, else stalled, else cap; fixed L: stop at L (or once nothing moves:
+      // the remaining layers only add the lazy +1, already in the values)
+      if (a.autom) {
+        if (covered == free_total) { used = l; why = AM_STOP_FILLED; break; }
+        if (got == 0) { used = l; why = AM_STOP_STALLED; break; }
+        if (l >= a.limit) { used = a.limit; why = AM_STOP_CAP; break; }
+      } else if (l >= a.limit || got == 0) {
+        used = a.limit;
+        break;
+      }
+    }
+    if (tid == 0) {
+      a.used[i] = used;
+      a.cause[i] = why;
+    }
+    __syncthreads();  // shared planes reused by the next maze
+  }
+}
+
+// rows per thread for a maze of mh rows with 2^wwp_log2 lanes per row group (0: no instantiation fits)
+inline int wave_rows(uint32_t mh, uint32_t wwp_log2, uint32_t threads) {
+  const uint32_t groups = threads >> wwp_log2;
+  const uint32_t need = (mh + groups - 1) / groups;
+  for (int r = 1; r <= 32; r *= 2)
+    if ((uint32_t)r >= need) return r;
+  return 0;
+}
+
 }  // namespace am
 
 using namespace am;
@@ -163,7 +366,19 @@ am_status am_batch_create(am_ctx* ctx, uint32_t n, uint32_t mw, uint32_t mh, con
   am::dfree(ctx, d_src);
   am::dfree(ctx, d_m);
   am::dfree(ctx, d_big);
+  if (!st) {  // K5 bookkeeping: where each maze's sources start in the packed list
+    std::vector<uint64_t> off(src_off, src_off + n + 1);
+    for (auto& o : off) o -= src_off[0];
+    e = am::dmalloc(ctx, &b->d_src_off, (n + 1) * 8);
+    if (!e) e = am::dmalloc(ctx, &b->d_k5, (2 * (size_t)n + 4) * 4);
+    if (!e) e = cudaMemcpyAsync(b->d_src_off, off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream);
+    if (!e) e = cudaStreamSynchronize(ctx->stream);
+    if (e) st = fail(ctx, AM_ECUDA, "batch: %s", cudaGetErrorString(e));
+  }
   if (st) {
+    if (b->grid) am_grid_destroy(ctx, b->grid);
+    am::dfree(ctx, b->d_src_off);
+    am::dfree(ctx, b->d_k5);
     delete b;
     return st;
   }
@@ -174,13 +389,171 @@ am_status am_batch_create(am_ctx* ctx, uint32_t n, uint32_t mw, uint32_t mh, con
 am_status am_batch_destroy(am_ctx* ctx, am_batch* b) {
   if (!b) return AM_OK;
   am_grid_destroy(ctx, b->grid);
+  am::dfree(ctx, b->d_src_off);
+  am::dfree(ctx, b->d_k5);
   delete b;
   return AM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+struct WaveShape {
+  uint32_t ww, wwp_log2;
+  int rows;     // rows per thread (template instance), 0: the batch does not fit K5
+  size_t smem;  // dynamic shared memory per CTA
+  uint32_t threads;
+};
+
+// CTA size (A/B: AM_K5_THREADS = 128 / 256 / 512)
+uint32_t wave_threads() {
+  static const uint32_t t = [] {
+    const char* e = std::getenv("AM_K5_THREADS");
+    const int v = e ? std::atoi(e) : kWaveThreads;
+    return (uint32_t)(v == 128 || v == 512 ? v : kWaveThreads);
+  }();
+  return t;
+}
+
+WaveShape wave_shape(const am_batch* b) {
+  WaveShape w{};
+  w.threads = wave_threads();
+  w.ww = (b->mw + 31) / 32;
+  if (w.ww > 32) return w;
+  while ((1u << w.wwp_log2) < w.ww) ++w.wwp_log2;
+  w.rows = wave_rows(b->mh, w.wwp_log2, w.threads);
+  const uint32_t groups = w.threads >> w.wwp_log2;
+  w.smem = (size_t)2 * b->mh * w.ww * 4 + (size_t)2 * groups * 2 * (1u << w.wwp_log2) * 4;
+  if (w.smem > 200 * 1024) w.rows = 0;
+  return w;
+}
+
+bool wave_eligible(const am_batch* b, uint32_t lref) {
+  static const bool off = [] {
+    const char* e = std::getenv("AM_BATCH_TILES");  // A/B: the packed tile path for every batch
+    return e && *e == '1';
+  }();
+  return !off && (uint64_t)lref + 1 <= kMax16Activity && wave_shape(b).rows > 0;
+}
+
+template <int R, int T>
+cudaError_t wave_launch_t(const WaveArgs& a, size_t smem, int sms, uint32_t n, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_batch_wave<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e) return e;
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_batch_wave<R, T>, T, smem);
+  if (e) return e;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(n, (uint64_t)std::max(per_sm, 1) * sms);
+  k_batch_wave<R, T><<<grid, T, smem, s>>>(a);
+  return cudaPeekAtLastError();
+}
+
+template <int R>
+cudaError_t wave_launch(const WaveArgs& a, size_t smem, int sms, uint32_t n, uint32_t threads, cudaStream_t s) {
+  if (threads == 128) return wave_launch_t<R, 128>(a, smem, sms, n, s);
+  if (threads == 512) return wave_launch_t<R, 512>(a, smem, sms, n, s);
+  return wave_launch_t<R, kWaveThreads>(a, smem, sms, n, s);
+}
+
+// K5: the whole batch in one launch, per-maze layers_used / cause straight from the wavefronts
+am_status wave_propagate(am_ctx* ctx, am_batch* b, uint32_t layers, uint32_t auto_cap, uint32_t lref,
+                         am_prop_result* r) {
+  am_grid* g = b->grid;
+  am_status st = set_cell_bits(ctx, g, 16);
+  if (st) return st;
+  cudaStream_t s = ctx->stream;
+  const WaveShape w = wave_shape(b);
+  uint32_t* used = b->d_k5;
+  uint32_t* cause = used + b->n;
+  uint32_t* next = cause + b->n;
+  CK(cudaMemsetAsync(next, 0, 4, s));
+  WaveArgs a{};
+  a.g = g->g;
+  a.occ = g->occ;
+  a.field = static_cast<uint16_t*>(g->val[g->cur]);
+  a.src_rc = g->src_rc;
+  a.src_off = b->d_src_off;
+  a.n = b->n;
+  a.mw = b->mw;
+  a.mh = b->mh;
+  a.tiles_x = b->tiles_x;
+  a.ww = w.ww;
+  a.wwp_log2 = w.wwp_log2;
+  a.autom = layers == 0;
+  a.limit = layers ? layers : auto_cap;
+  a.lref = lref;
+  a.used = used;
+  a.cause = cause;
+  a.next = next;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const bool timing = ctx->flags & AM_CTX_TIMING;
+  if (timing) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+  }
+  switch (w.rows) {
+    case 1: CK(wave_launch<1>(a, w.smem, ctx->sms, b->n, w.threads, s)); break;
+    case 2: CK(wave_launch<2>(a, w.smem, ctx->sms, b->n, w.threads, s)); break;
+    case 4: CK(wave_launch<4>(a, w.smem, ctx->sms, b->n, w.threads, s)); break;
+    case 8: CK(wave_launch<8>(a, w.smem, ctx->sms, b->n, w.threads, s)); break;
+    case 16: CK(wave_launch<16>(a, w.smem, ctx->sms, b->n, w.threads, s)); break;
+    default: CK(wave_launch<32>(a, w.smem, ctx->sms, b->n, w.threads, s)); break;
+  }
+  ++ctx->launches;
+  if (timing) CK(cudaEventRecord(e1, s));
+  b->layers_used.resize(b->n);
+  b->cause.resize(b->n);
+  CK(cudaMemcpyAsync(b->layers_used.data(), used, b->n * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(b->cause.data(), cause, b->n * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  if (timing) {
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  g->computed = g->layers_used = lref;  // values are lref + 1 - t; maze i's rollback is lref - used[i]
+  g->plain_active = 0;
+  g->have_map = 1;
+  uint32_t maxl = 0;
+  for (uint32_t u : b->layers_used) maxl = std::max(maxl, u);
+  *r = am_prop_result{};
+  r->layers_used = maxl;
+  r->cause = layers ? AM_STOP_FIXED : AM_STOP_CAP;
+  r->layers_computed = maxl;
+  r->cell_bits = 16;
+  r->block_launches = 1;
+  r->stencil_ms = ms;
+  return AM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 am_status am_batch_propagate(am_ctx* ctx, am_batch* b, uint32_t layers, uint32_t auto_cap, uint32_t* layers_used,
                              uint32_t* cause, am_prop_result* global) {
   if (!ctx || !b) return AM_EINVAL;
+  if (layers == 0 && auto_cap == 0) return fail(ctx, AM_EINVAL, "auto_cap must be >= 1");
+  if (layers > kMaxLayers || auto_cap > kMaxLayers) return fail(ctx, AM_EINVAL, "layer count exceeds kMaxLayers");
+  CK(cudaSetDevice(ctx->device));
+  const uint32_t lref = layers ? layers : auto_cap;
+  if (wave_eligible(b, lref)) {
+    am_prop_result r{};
+    am_status st = wave_propagate(ctx, b, layers, auto_cap, lref, &r);
+    if (st) return st;
+    if (layers_used) memcpy(layers_used, b->layers_used.data(), b->n * 4);
+    if (cause) memcpy(cause, b->cause.data(), b->n * 4);
+    if (global) *global = r;
+    b->have = 1;
+    return AM_OK;
+  }
   std::vector<SlabRef> one{{ctx, b->grid}};
   am_prop_result r{};
   am_status st = drive_propagation(one, nullptr, layers, auto_cap, AM_MODE_BATCHED, &r);
