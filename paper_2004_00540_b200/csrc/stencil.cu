@@ -8,9 +8,20 @@
 // mode, 240-column bands); k_block_tiles runs only the active 32x112 tiles
 // (exact skipping: quiet tiles advance lazily through a per-tile lag) and
 // lists the next block's tiles itself.  See DESIGN.md §4.
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
+
 #include <cstdio>
+#include <cstdlib>
 
 #include "am_internal.cuh"
+
+// AM_TMA=1: the active-tile items stage their rows with TMA (cp.async.bulk.tensor.2d, one 128 x 8 box of
+// 16-bit cells per 8-row slot, completion on a per-warp mbarrier) wherever all 128 columns of a slot's
+// region live in the same ping-pong field; regions split across fields (the neighbour bands' halo columns
+// in the other field) keep the per-lane 16 B cp.async.  AM_TMA=0: cp.async only (the A/B baseline).
+#ifndef AM_TMA
+#define AM_TMA 0  // measured: +2-4% on C4 / C2 / C3; tools/build_variant.sh tma "-DAM_TMA=1"
+#endif
 
 namespace am {
 
@@ -326,6 +337,73 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// ---- TMA staging (active tiles, 16-bit cells) ----
+struct TileMaps {
+  CUtensorMap box8[2];  // field 0 / field 1: 2-D (pitch x rows) u16, box = 128 columns x 8 rows (2 KB)
+};
+constexpr int kSlotRows = 8;
+constexpr int kSlotBytes = kSlotRows * 32 * kTileWPL * 2;  // one 8-row slot of the warp's 128-column band
+
+struct TmaStage {
+  const TileMaps* tm;  // the kernel's __grid_constant__ descriptors
+  uint32_t mbA, mbB;   // this warp's mbarriers (shared addresses): rows 0..31 / rows 32..47 of a staging
+  uint32_t parity;     // phase parity of the current staging (every staging arrives on both exactly once)
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "MBAR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// one 128-column x 8-row box of a field into shared memory, completing on bar
+__device__ __forceinline__ void tma_box8(uint32_t dst, const CUtensorMap* map, uint32_t x, uint32_t y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// Issue the TMA part of a staging of `nslots` (<= 6) 8-row slots (slot s = staged rows 8s..8s+7, band
+// column x, allocated row y0 + 8s) into buf; slot s reads region reg(s).  A region goes through TMA when
+// all 32 compute lanes' homes (bit r of `homes`) agree; returns the mask of TMA regions.  Lanes 0-3 arrive
+// on mbA (init count 4) and lanes 4-5 on mbB (count 2), each with its own slot's bytes (0 when the slot
+// is absent or copied by cp.async), so every staging completes one phase of each barrier and no lane
+// waits for another before issuing.
+template <class Reg>
+__device__ __forceinline__ uint32_t tma_stage(const TmaStage& ts, uint32_t homes, uint8_t* buf, uint32_t x, uint32_t y0,
+                                              int nslots, Reg reg) {
+  const int lane = threadIdx.x & 31;
+  uint32_t tmask = 0, fld = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const uint32_t m = __ballot_sync(0xffffffffu, (homes >> r) & 1u);
+    if (m == 0u || m == 0xffffffffu) tmask |= 1u << r;
+    if (m) fld |= 1u << r;
+  }
+  if (lane < 6) {
+    const int r = lane < nslots ? reg(lane) : 0;
+    const bool tma = lane < nslots && ((tmask >> r) & 1u);
+    const uint32_t bar = lane < 4 ? ts.mbA : ts.mbB;
+    // the previous item's generic-proxy reads of buf (ordered by the caller's __syncwarp) come first
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect(bar, tma ? kSlotBytes : 0u);
+    if (tma)
+      tma_box8(smem_u32(buf) + lane * kSlotBytes, &ts.tm->box8[(fld >> r) & 1u], x, y0 + kSlotRows * lane, bar);
+  }
+  return tmask;
 }
 
 #ifndef AM_STAGES
@@ -730,10 +808,19 @@ __device__ __forceinline__ void tile_fill(const uint8_t* buf, uint32_t lag_a, bo
 // Issues the copies of the tile's rows into buf (two commit groups); the
 // caller may still decide not to run the staged path (then waits them out).
 __device__ __forceinline__ void tile_stage16(const Geo& g, const uint16_t* __restrict__ f0, ptrdiff_t delta,
-                                             uint32_t b, uint32_t c, uint32_t homes, uint8_t* buf) {
+                                             uint32_t b, uint32_t c, uint32_t homes, uint8_t* buf,
+                                             const TmaStage& ts) {
   const int lane = threadIdx.x & 31;
   const size_t pitch = g.pitch;
   __syncwarp();  // every lane is done reading the previous item's rows
+  uint32_t tmask = 0;
+#if AM_TMA
+  // slots: staged rows 0-7 above the tile, 8-39 inside, 40-47 below
+  tmask = tma_stage(ts, homes, buf, b * kTileCols, c * kTileRows, kStageRows / kSlotRows,
+                    [](int sl) { return sl == 0 ? 0 : (sl == kStageRows / kSlotRows - 1 ? 2 : 1); });
+#else
+  (void)ts;
+#endif
   {
     // the 8 cells this lane copies belong to compute lanes 2*(lane&15) and +1: their band's homes
     const uint32_t ch = __shfl_sync(0xffffffffu, homes, (2 * lane) & 31);
@@ -747,7 +834,7 @@ __device__ __forceinline__ void tile_stage16(const Geo& g, const uint16_t* __res
     for (int k = 0; k < kStageRows / 2; ++k) {
       const int row = 2 * k + half;  // staged row = tile row + kK
       const int reg = row < kK ? 0 : (row < kK + kTileRows ? 1 : 2);
-      cp_async16(dst + row * kTileRowBytes, base[reg] + (size_t)row * pitch);
+      if (!((tmask >> reg) & 1u)) cp_async16(dst + row * kTileRowBytes, base[reg] + (size_t)row * pitch);
       if (k == kHalfRows - 1) asm volatile("cp.async.commit_group;" ::: "memory");  // rows 0..31: phases 0-1
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -756,7 +843,7 @@ __device__ __forceinline__ void tile_stage16(const Geo& g, const uint16_t* __res
 
 __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta, uint32_t b,
                                                 uint32_t c, const uint32_t (&lw)[3], uint32_t homes,
-                                                uint32_t* edge, const uint8_t* buf) {
+                                                uint32_t* edge, const uint8_t* buf, const TmaStage& ts) {
   const int lane = threadIdx.x & 31;
   const size_t pitch = g.pitch;
   uint32_t P0[kK][4], P1[kK][4];
@@ -776,6 +863,11 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
   const bool l_up = __any_sync(0xffffffffu, lag_up != 0u), l_in = __any_sync(0xffffffffu, lag_in != 0u),
              l_dn = __any_sync(0xffffffffu, lag_dn != 0u);
   asm volatile("cp.async.wait_group 1;" ::: "memory");
+#if AM_TMA
+  mbar_wait(ts.mbA, ts.parity);
+#else
+  (void)ts;
+#endif
   __syncwarp();
 #if AM_TRIM
   tile_fill<kHalfRows>(rb, lag_up, l_up, lag_in, l_in, P0, P1);
@@ -784,6 +876,9 @@ __device__ __forceinline__ uint32_t tile_item16(const Geo& g, uint16_t* __restri
   tile_phase<kOutNone>(rb, kK, 2 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
 #endif
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+#if AM_TMA
+  mbar_wait(ts.mbB, ts.parity);
+#endif
   __syncwarp();
   tile_phase<kOutTop>(rb, 2 * kK, 3 * kK, lag_in, l_in, P0, P1, oA, oB, pitch, st, acc, accTop);
   tile_phase<kOutBot>(rb, 3 * kK, kTileSteps, lag_dn, l_dn, P0, P1, oA, oB, pitch, st, acc, accBot);
@@ -871,11 +966,17 @@ static_assert(kQuarterRows == kK, "quarter phase layout assumes 8-row streams wi
 
 __device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __restrict__ f0, ptrdiff_t delta,
                                                    uint32_t b, uint32_t c, uint32_t half, const uint32_t (&lw)[3],
-                                                   uint32_t homes, uint32_t* edge, uint8_t* buf) {
+                                                   uint32_t homes, uint32_t* edge, uint8_t* buf, TmaStage& ts) {
   const int lane = threadIdx.x & 31;
   const size_t pitch = g.pitch;
   const uint32_t r0 = half * kHalfRows;  // first tile row of the item
   __syncwarp();  // every lane is done reading the previous item's rows
+  uint32_t tmask = 0;
+#if AM_TMA
+  // slots (staged rows 8s..8s+7 = tile rows r0-8+8s..): half 0: above, inside x 3; half 1: inside x 3, below
+  tmask = tma_stage(ts, homes, buf, b * kTileCols, c * kTileRows + r0, kQuarterStage / kSlotRows,
+                    [half](int sl) { return half ? (sl == 3 ? 2 : 1) : (sl == 0 ? 0 : 1); });
+#endif
   {
     const uint32_t ch = __shfl_sync(0xffffffffu, homes, (2 * lane) & 31);
     const uint32_t col = b * kTileCols + (lane & 15) * 8;
@@ -889,7 +990,7 @@ __device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __res
       const int row = 2 * k + (lane >> 4);  // staged row = item row + kK
       const int trow = (int)r0 + row - kK;  // tile row
       const int reg = trow < 0 ? 0 : (trow < kTileRows ? 1 : 2);
-      cp_async16(dst + row * kTileRowBytes, base[reg] + (size_t)row * pitch);
+      if (!((tmask >> reg) & 1u)) cp_async16(dst + row * kTileRowBytes, base[reg] + (size_t)row * pitch);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
@@ -913,6 +1014,12 @@ __device__ __forceinline__ uint32_t tile_quarter16(const Geo& g, uint16_t* __res
   const bool l0 = __any_sync(0xffffffffu, lag0 != 0u), l1 = __any_sync(0xffffffffu, lag1 != 0u),
              l2 = __any_sync(0xffffffffu, lag2 != 0u);
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+#if AM_TMA
+  mbar_wait(ts.mbA, ts.parity);  // (mbB completed on its zero-byte arrive)
+  ts.parity ^= 1u;
+#else
+  (void)ts;
+#endif
   __syncwarp();
 #if AM_TRIM
   tile_fill<kQuarterRows>(rb, lag0, l0, lag1, l1, P0, P1);
@@ -1076,8 +1183,19 @@ template <int CB>
 __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
     k_block_tiles(Geo g, typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, const uint8_t* __restrict__ srcmask,
                   const uint8_t* __restrict__ rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
-                  FlagSink prev) {
+                  FlagSink prev, const __grid_constant__ TileMaps tmaps) {
   extern __shared__ __align__(128) uint8_t smem_tiles[];
+  // this warp's two staging mbarriers live after the per-warp buffers
+  TmaStage ts{&tmaps, smem_u32(smem_tiles + kTileSmem + (threadIdx.x >> 5) * 16),
+              smem_u32(smem_tiles + kTileSmem + (threadIdx.x >> 5) * 16 + 8), 0u};
+#if AM_TMA
+  if (CB == 16 && (threadIdx.x & 31) == 0) {
+    mbar_init(ts.mbA, 4);  // slot lanes 0-3
+    mbar_init(ts.mbB, 2);  // slot lanes 4-5
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+#endif
   // programmatic dependent launch: this grid may start while the previous
   // block's grid drains; wait for it (memory visible) before touching state,
   // and let the next block's grid get scheduled right away
@@ -1293,7 +1411,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
       const uint32_t r0 = ra + half * kHalfRows;
       if (!__any_sync(0xffffffffu, f != 0u)) {
         acc = tile_quarter16(g, reinterpret_cast<uint16_t*>(f0), delta, bA, cA, half, lw,
-                             hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6, edge, buf);
+                             hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6, edge, buf, ts);
       } else {  // a source in reach: the general path on the same two 8-row streams
         const uint32_t up = half ? hm[1] : hm[0], dn = half ? hm[2] : hm[1];
         const uint32_t homes = up | hm[1] << 1 | hm[1] << 2 | hm[1] << 3 | hm[1] << 4 | dn << 5 | out_home << 6 |
@@ -1310,11 +1428,19 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm)
       // upper half (lo): tile rows 0-15, lower half (hi): rows 16-31
       uint8_t* buf = smem_tiles + (threadIdx.x >> 5) * kTileWarpSmem;
       const uint32_t homes16 = hm[0] | hm[1] << 1 | hm[2] << 2 | out_home << 6;
-      tile_stage16(g, f0, delta, bA, cA, homes16, buf);  // copies in flight during the source vote
+      tile_stage16(g, f0, delta, bA, cA, homes16, buf, ts);  // copies in flight during the source vote
       if (!__any_sync(0xffffffffu, f != 0u)) {
-        acc = tile_item16(g, f0, delta, bA, cA, lw, homes16, edge, buf);
+        acc = tile_item16(g, f0, delta, bA, cA, lw, homes16, edge, buf, ts);
+#if AM_TMA
+        ts.parity ^= 1u;
+#endif
       } else {  // a source in reach: the general path, same halves (its ring reuses buf)
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+#if AM_TMA
+        mbar_wait(ts.mbA, ts.parity);
+        mbar_wait(ts.mbB, ts.parity);
+        ts.parity ^= 1u;
+#endif
         __syncwarp();
         const uint32_t homes = hm[0] | hm[1] << 1 | hm[1] << 2 | hm[1] << 3 | hm[1] << 4 | hm[2] << 5 |
                                out_home << 6 | out_home << 7;
@@ -1805,22 +1931,72 @@ void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer,
 }
 
 // f0/f1: the two fields; book: tile states / lists (block blk reads list[blk & 1])
+// TMA descriptors of the two 16-bit fields (box: one 8-row slot of a 128-column tile band), encoded
+// through the driver entry point the runtime exposes; cached for the last (f0, f1, geometry).
+static bool tile_maps(const Geo& g, void* f0, void* f1, TileMaps* out) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<Encode>(fn);
+  }();
+  static TileMaps cached{};
+  static const void* key[2] = {nullptr, nullptr};
+  static uint32_t key_pitch = 0, key_rows = 0;
+  if (!encode) return false;
+  if (key[0] != f0 || key[1] != f1 || key_pitch != g.pitch || key_rows != g.rows) {
+    void* f[2] = {f0, f1};
+    for (int i = 0; i < 2; ++i) {
+      const cuuint64_t dims[2] = {g.pitch, g.rows};
+      const cuuint64_t strides[1] = {(cuuint64_t)g.pitch * 2};
+      const cuuint32_t box[2] = {32 * kTileWPL, kSlotRows};
+      const cuuint32_t estr[2] = {1, 1};
+      if (encode(&cached.box8[i], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, f[i], dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        key[0] = key[1] = nullptr;
+        return false;
+      }
+    }
+    key[0] = f0;
+    key[1] = f1;
+    key_pitch = g.pitch;
+    key_rows = g.rows;
+  }
+  *out = cached;
+  return true;
+}
+
+constexpr int kTileSmemTotal = kTileSmem + kTileThreads / 32 * 16;  // + two mbarriers per warp
+
 void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, const uint8_t* srcmask,
                         const uint8_t* rowsrc, TileBook book, uint32_t blk, uint32_t l0, FlagSink flag,
                         FlagSink prev, bool pdl, cudaStream_t s) {
   static bool attr = [] {
-    cudaFuncSetAttribute(k_block_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
-    cudaFuncSetAttribute(k_block_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+    cudaFuncSetAttribute(k_block_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemTotal);
+    cudaFuncSetAttribute(k_block_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemTotal);
     return true;
   }();
   (void)attr;
+  TileMaps maps{};
   if (cb == 16) {
+#if AM_TMA
+    if (!tile_maps(g, f0, f1, &maps)) {
+      fprintf(stderr, "actmap: cuTensorMapEncodeTiled unavailable (driver too old for TMA staging)\n");
+      abort();
+    }
+#endif
     auto* a = (uint16_t*)f0;
     // programmatic stream serialization: the launch overlaps the previous block's tail (griddepcontrol.wait)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctas);
     cfg.blockDim = dim3(kTileThreads);
-    cfg.dynamicSmemBytes = kTileSmem;
+    cfg.dynamicSmemBytes = kTileSmemTotal;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1828,11 +2004,11 @@ void launch_block_tiles(const Geo& g, int cb, int ctas, void* f0, void* f1, cons
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_block_tiles<16>, g, a, (ptrdiff_t)((uint16_t*)f1 - a), srcmask, rowsrc, book, blk, l0,
-                       flag, prev);
+                       flag, prev, maps);
   } else {
     auto* a = (uint32_t*)f0;
-    k_block_tiles<32><<<ctas, kTileThreads, kTileSmem, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk, l0,
-                                                              flag, prev);
+    k_block_tiles<32><<<ctas, kTileThreads, kTileSmemTotal, s>>>(g, a, (uint32_t*)f1 - a, srcmask, rowsrc, book, blk,
+                                                                   l0, flag, prev, maps);
   }
 }
 

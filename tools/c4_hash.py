@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2004_00540_b200 as am  # noqa: E402
 
-occ, src, tgt = bench.make_workload(am)
+occ, src, tgt = bench.make_workload(am.random_maze)
 ctx = am.Context(0)
 g = am.Grid(occ, src, ctx)
 r = g.propagate_auto(bench.AUTO_CAP)

@@ -49,7 +49,7 @@ def main():
     src, tgt = bench.sample_points(occ, 64, 3), bench.sample_points(occ, 1000, 4)
     out.append(grid_solve("C3 16384^2 city", occ, src, tgt, 4 * 16384, ctx))
     # C4-fixed and E: fixed L = 1024 on the C4 grid / an empty 23170^2 grid with a centred source
-    occ4, src4, _ = bench.make_workload(am)
+    occ4, src4, _ = bench.make_workload(am.random_maze)
     for name, occ, src in (("C4-fixed L=1024", occ4, src4),
                            ("E 23170^2 empty, centred source, L=1024",
                             np.zeros((23170, 23170), np.uint8), np.array([[11585, 11585]], np.uint32))):

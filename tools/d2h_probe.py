@@ -24,7 +24,7 @@ def t(fn, reps=3):
     return best * 1e3
 
 
-occ, src, _ = bench.make_workload(am)
+occ, src, _ = bench.make_workload(am.random_maze)
 H, W = occ.shape
 ctx = am.Context(0)
 g = am.Grid(occ, src, ctx)

@@ -19,7 +19,7 @@ import paper_2004_00540_b200 as am  # noqa: E402
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     torch.cuda.set_device(0)
-    occ, src, tgt = bench.make_workload(am)
+    occ, src, tgt = bench.make_workload(am.random_maze)
     H, W = occ.shape
     ctx = am.Context(0, timing=True)
     h_occ = torch.from_numpy(occ).pin_memory()

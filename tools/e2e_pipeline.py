@@ -19,7 +19,7 @@ import paper_2004_00540_b200 as am  # noqa: E402
 def main():
     k = int(sys.argv[1]) if len(sys.argv) > 1 else 6
     torch.cuda.set_device(0)
-    occ, src, tgt = bench.make_workload(am)
+    occ, src, tgt = bench.make_workload(am.random_maze)
     h_occ = torch.from_numpy(occ).pin_memory().numpy()
     ctxs = [am.Context(0), am.Context(0)]
     outs = [torch.empty((16 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32) for _ in ctxs]

@@ -18,7 +18,7 @@ import paper_2004_00540_b200 as am  # noqa: E402
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     torch.cuda.set_device(0)
-    occ, src, tgt = bench.make_workload(am)
+    occ, src, tgt = bench.make_workload(am.random_maze)
     ctx = am.Context(0)
     text = am.emit_movingai(occ, ctx)
     h_text = torch.empty(len(text), dtype=torch.uint8, pin_memory=True)

@@ -13,7 +13,7 @@ from tests.test_gpu_slabs import aligned_split  # noqa: E402
 
 def main():
     ns = [int(a) for a in sys.argv[1:]] or [1, 2, 4]
-    occ, src, _ = bench.make_workload(am)
+    occ, src, _ = bench.make_workload(am.random_maze)
     H = occ.shape[0]
     ctx = am.Context(0)
     for n in ns:

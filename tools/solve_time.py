@@ -14,7 +14,7 @@ import paper_2004_00540_b200 as am  # noqa: E402
 from bench import AUTO_CAP, H, W, make_workload  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-occ, src, tgt = make_workload(am)
+occ, src, tgt = make_workload(am.random_maze)
 out = {}
 maps = {}
 modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["dense", "tiles"]

@@ -13,7 +13,7 @@ import paper_2004_00540_b200 as am  # noqa: E402
 
 
 def main():
-    occ, src, _ = bench.make_workload(am)
+    occ, src, _ = bench.make_workload(am.random_maze)
     ctx = am.Context(0)
     g = am.Grid(occ, src, ctx)
     nt = g.info()["tiles"]

@@ -22,7 +22,7 @@ def main():
     timing = bool(int(sys.argv[1])) if len(sys.argv) > 1 else False
     dense = bool(int(sys.argv[2])) if len(sys.argv) > 2 else False
     torch.cuda.set_device(0)
-    occ, src, tgt = bench.make_workload(am)
+    occ, src, tgt = bench.make_workload(am.random_maze)
     ctx = am.Context(0, timing=timing, dense=dense)
     g = am.Grid(occ, src, ctx)
     g.propagate_auto(bench.AUTO_CAP)
