@@ -344,13 +344,15 @@ struct TileMaps {
   CUtensorMap box8[2];  // field 0 / field 1: 2-D (pitch x rows) u16, box = 128 columns x 8 rows (2 KB)
 };
 constexpr int kSlotRows = 8;
-constexpr int kSlotBytes = kSlotRows * 32 * kTileWPL * 2;  // one 8-row slot of the warp's 128-column band
 
 struct TmaStage {
   const TileMaps* tm;  // the kernel's __grid_constant__ descriptors
   uint32_t mbA, mbB;   // this warp's mbarriers (shared addresses): rows 0..31 / rows 32..47 of a staging
   uint32_t parity;     // phase parity of the current staging (every staging arrives on both exactly once)
 };
+
+#if AM_TMA
+constexpr int kSlotBytes = kSlotRows * 32 * kTileWPL * 2;  // one 8-row slot of the warp's 128-column band
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -405,6 +407,7 @@ __device__ __forceinline__ uint32_t tma_stage(const TmaStage& ts, uint32_t homes
   }
   return tmask;
 }
+#endif  // AM_TMA
 
 #ifndef AM_STAGES
 #define AM_STAGES 4
@@ -1931,6 +1934,7 @@ void launch_tiles_all(const Geo& g, TileBook book, uint32_t blk, uint32_t layer,
 }
 
 // f0/f1: the two fields; book: tile states / lists (block blk reads list[blk & 1])
+#if AM_TMA
 // TMA descriptors of the two 16-bit fields (box: one 8-row slot of a 128-column tile band), encoded
 // through the driver entry point the runtime exposes; cached for the last (f0, f1, geometry).
 static bool tile_maps(const Geo& g, void* f0, void* f1, TileMaps* out) {
@@ -1971,6 +1975,7 @@ static bool tile_maps(const Geo& g, void* f0, void* f1, TileMaps* out) {
   *out = cached;
   return true;
 }
+#endif  // AM_TMA
 
 constexpr int kTileSmemTotal = kTileSmem + kTileThreads / 32 * 16;  // + two mbarriers per warp
 
