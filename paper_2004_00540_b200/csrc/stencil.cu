@@ -343,7 +343,6 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 struct TileMaps {
   CUtensorMap box8[2];  // field 0 / field 1: 2-D (pitch x rows) u16, box = 128 columns x 8 rows (2 KB)
 };
-constexpr int kSlotRows = 8;
 
 struct TmaStage {
   const TileMaps* tm;  // the kernel's __grid_constant__ descriptors
@@ -352,6 +351,7 @@ struct TmaStage {
 };
 
 #if AM_TMA
+constexpr int kSlotRows = 8;
 constexpr int kSlotBytes = kSlotRows * 32 * kTileWPL * 2;  // one 8-row slot of the warp's 128-column band
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
