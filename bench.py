@@ -293,7 +293,7 @@ def bench_config(world):
     return {"workload": f"C4: {W}x{H} random_maze(density 0.40, seed 4), {N_SOURCES} sources, "
                         f"{N_TARGETS} targets, propagate_auto(cap {AUTO_CAP}) + Euclidean paths to host",
             "grid": [W, H], "sources": N_SOURCES, "targets": N_TARGETS, "auto_cap": AUTO_CAP,
-            "parallelism": "single GPU" if world == 1 else f"row slabs x{world} (NCCL K=8 halos)",
+            "parallelism": "single GPU" if world == 1 else f"row slabs x{world} (K=8 halos through peer memory)",
             "l2": "inputs larger than L2 (1.07 GB 16-bit field vs 126 MB L2), no flush"}
 
 
@@ -349,7 +349,7 @@ class Solver:
     N > 1: row slabs (one per rank, NCCL halo exchange per block), the fixed-point map all-gathered into a
     full-size field on every rank, each rank tracing targets[rank::N]."""
 
-    def __init__(self, am, torch, ctx, occ, src, tgt, rank, world, local_rank):
+    def __init__(self, am, torch, ctx, occ, src, tgt, rank, world, local_rank, transport="peer"):
         self.am, self.torch, self.ctx, self.world, self.rank = am, torch, ctx, world, rank
         dev = torch.device(f"cuda:{local_rank}")
         self.stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
@@ -361,9 +361,9 @@ class Solver:
         torch.cuda.synchronize()
         self.full = am.Grid.from_device(W, H, d_occ.data_ptr(), d_src.data_ptr(), len(src), ctx)
         self.slab = None
+        self.transport = transport
         if world > 1:
-            r0, r1 = ctx.slab_rows(H)
-            self.slab = am.Grid.slab(occ, src, r0, r1, ctx)
+            self.slab = make_slab(am, ctx, occ, src, rank, world, transport)
         del d_occ, d_src
         n = len(my_tgt)
         self.n = n
@@ -384,7 +384,7 @@ class Solver:
         if self.slab is None:
             return self.full.propagate_auto(AUTO_CAP)
         r = self.slab.propagate_auto(AUTO_CAP)
-        self.ctx.comm_gather(self.slab, self.full)
+        gather(self.am, self.ctx, self.slab, self.full, self.transport)
         return r
 
     def trace(self):
@@ -416,7 +416,30 @@ class Solver:
         self.full.close()
 
 
-def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts, split=None):
+def make_slab(am, ctx, occ, src, rank, world, transport):
+    """This rank's row slab; peer transport: IPC handles shared with every rank (torch.distributed carries
+    the 1 KB blobs), halos then move through peer memory with no NCCL call per block."""
+    if transport == "nccl":
+        r0, r1 = ctx.slab_rows(H)
+        return am.Grid.slab(occ, src, r0, r1, ctx)
+    import torch.distributed as dist
+
+    r0, r1 = am.slab_rows(H, world, rank)
+    slab = am.Grid.slab(occ, src, r0, r1, ctx)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, am.peer_export(slab))
+    am.peer_connect(slab, world, rank, blobs)
+    return slab
+
+
+def gather(am, ctx, slab, full, transport):
+    if transport == "nccl":
+        ctx.comm_gather(slab, full)
+    else:
+        am.peer_gather(slab, full)
+
+
+def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts, split=None, transport="peer"):
     """One end-to-end solve through the C ABI with host buffers (pinned): occupancy + sources H2D, propagate
     to the fixed point, every path to the host.  Returns (offsets, points, status, seconds); the full activity
     map is then downloaded too, outside that time (SURVEY.md §8d reports it separately), and split receives
@@ -437,11 +460,11 @@ def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts, split=None):
             split.setdefault("map_d2h", []).append(t3 - t2)
         return off, pts, st, t2 - t0
     t0 = time.perf_counter()
-    r0, r1 = ctx.slab_rows(H)
-    s = am.Grid.slab(occ, src, r0, r1, ctx)
+    s = make_slab(am, ctx, occ, src, rank, world, transport)
+    r0, r1 = s.row0, s.row0 + s.height
     s.propagate_auto(AUTO_CAP)
     full = am.Grid(occ, src, ctx)
-    ctx.comm_gather(s, full)
+    gather(am, ctx, s, full, transport)
     off, pts, st = full.trace(my_tgt, am.EUCLIDEAN, out=h_pts)
     t2 = time.perf_counter()
     s.activity(out=h_map[r0:r1])
@@ -543,6 +566,11 @@ def run_configs(am, torch, ctx, info_c4, occ4, src4, hops4, parity):
     return out
 
 
+def reduce_device(dist, local_rank):
+    """Where the max-over-ranks timing reductions run (gloo: host tensors)."""
+    return "cpu" if dist.get_backend() == "gloo" else f"cuda:{local_rank}"
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
 
@@ -555,11 +583,11 @@ def run_b200(args, rank, world, local_rank):
 
     occ, src, tgt = make_workload(am.random_maze)
     ctx = am.Context(local_rank, timing=True)
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         uid = [am.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.comm_init(world, rank, uid[0])
-    sol = Solver(am, torch, ctx, occ, src, tgt, rank, world, local_rank)
+    sol = Solver(am, torch, ctx, occ, src, tgt, rank, world, local_rank, args.transport)
     stream = sol.stream
 
     clocks = ClockSampler(local_rank) if rank == 0 else None  # polling well before the timed region
@@ -601,7 +629,7 @@ def run_b200(args, rank, world, local_rank):
     launches = ctx.kernel_launches() - launches0
     clk = clocks.stop((wall0, wall1)) if clocks else None
     if dist:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local_rank}")
+        t = torch.tensor([ms_total], dtype=torch.float64, device=reduce_device(dist, local_rank))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -658,11 +686,12 @@ def run_b200(args, rank, world, local_rank):
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            off2, pts2, st2, dt = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map, h_pts, split if i else None)
+            off2, pts2, st2, dt = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map, h_pts, split if i else None,
+                                            args.transport)
             ctx.synchronize()
             dfull = time.perf_counter() - t0  # including the full map download
             if dist:
-                t = torch.tensor([dt, dfull], dtype=torch.float64, device=f"cuda:{local_rank}")
+                t = torch.tensor([dt, dfull], dtype=torch.float64, device=reduce_device(dist, local_rank))
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 dt, dfull = (float(x) for x in t.tolist())
             if i:
@@ -680,7 +709,7 @@ def run_b200(args, rank, world, local_rank):
                "api": "am_grid_create(host occupancy + sources, pinned) + am_propagate(auto) + am_path_counts + "
                       "am_trace_paths (every path to pinned host memory); the uint32 activity map stays on the "
                       "device (the C++ ActivityMap fetches it lazily) and its download is reported separately" +
-                      ("; per rank: slab grid, NCCL halos, am_comm_gather" if world > 1 else "")}
+                      ("; per rank: slab grid, peer-memory halos, am_peer_gather" if world > 1 else "")}
         del h_occ, h_map, h_pts
 
     # ---- CPU leg (rank 0, N=1): the oracle as baseline and as the checker of what was just timed ----
@@ -755,10 +784,18 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed instance")
     ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C4-fixed/C5 block")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 halo transport: peer memory (CUDA IPC, default) or NCCL send/recv")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # AM_BENCH_SHARED_GPU=1 (code-path check only, the numbers mean nothing): every rank on cuda:0, gloo for
+    # the host-side collectives; the peer transport's cross-rank dependencies are stream waits, so ranks may
+    # share a GPU
+    shared = os.environ.get("AM_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -767,7 +804,7 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if shared else "nccl")
     run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

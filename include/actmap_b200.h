@@ -180,6 +180,27 @@ am_status am_comm_unique_id(uint8_t *id_out /* 128 bytes */);
 am_status am_comm_init(am_ctx *ctx, uint32_t nranks, uint32_t rank, const uint8_t *id /* 128 bytes */);
 am_status am_comm_slab_rows(const am_ctx *ctx, uint32_t height, uint32_t *row0, uint32_t *row1);
 am_status am_comm_gather(am_ctx *ctx, am_grid *slab, am_grid *full);
+/* rows [row0, row1) of slab `rank` of `nranks` over `height` rows (the cut
+ * am_comm_slab_rows uses; no communicator needed). */
+am_status am_slab_rows(uint32_t height, uint32_t nranks, uint32_t rank, uint32_t *row0, uint32_t *row1);
+
+/* ---- peer-memory slab transport (no NCCL call on the per-block path) -----
+ * One process per GPU (or several on one GPU).  Each rank's slab exports a
+ * blob (CUDA IPC handles of its halo inbox, its publish buffer and its block
+ * events); the caller shares the blobs (any host channel, e.g.
+ * torch.distributed all_gather_object) and connects.  Per block, the
+ * boundary kernel stores the slab's first / last K rows straight into the
+ * neighbours' inboxes through the mapped peer pointers (NVLink / NVSwitch
+ * P2P stores across GPUs), records an IPC event, and the neighbours' streams
+ * wait on it (stream-ordered: no kernel spins on another rank).  The
+ * fixed-point words ride along as in the NCCL transport.  am_propagate on a
+ * connected slab uses this transport; am_peer_gather assembles the full map
+ * from the peers' published slabs with peer-to-peer copies. */
+#define AM_PEER_BLOB_BYTES 1024
+am_status am_peer_export(am_ctx *ctx, am_grid *slab, uint8_t *blob /* AM_PEER_BLOB_BYTES */);
+am_status am_peer_connect(am_ctx *ctx, am_grid *slab, uint32_t nranks, uint32_t rank,
+                          const uint8_t *blobs /* nranks x AM_PEER_BLOB_BYTES, rank order */);
+am_status am_peer_gather(am_ctx *ctx, am_grid *slab, am_grid *full);
 
 /* ---- small-grid batch (BASELINE.json config 5) ---------------------------
  * n independent width x height mazes solved in one device run: the

@@ -124,6 +124,10 @@ def lib():
             "am_comm_init": (st, [_vp, u32, u32, _vp]),
             "am_comm_slab_rows": (st, [_vp, u32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
             "am_comm_gather": (st, [_vp, _vp, _vp]),
+            "am_slab_rows": (st, [u32, u32, u32, C.POINTER(u32), C.POINTER(u32)]),
+            "am_peer_export": (st, [_vp, _vp, _vp]),
+            "am_peer_connect": (st, [_vp, _vp, u32, u32, _vp]),
+            "am_peer_gather": (st, [_vp, _vp, _vp]),
             "am_batch_create": (st, [_vp, u32, u32, u32, _vp, _vp, _vp, C.POINTER(_vp)]),
             "am_batch_destroy": (st, [_vp, _vp]),
             "am_batch_propagate": (st, [_vp, _vp, u32, u32, _vp, _vp, C.POINTER(_PropResult)]),
@@ -534,6 +538,41 @@ def slabs_propagate(slabs, layers: int = 0, auto_cap: int = 0, mode: int = BATCH
     for s in slabs:
         s.layers = r.layers_used
     return PropResult(r)
+
+
+PEER_BLOB_BYTES = 1024  # AM_PEER_BLOB_BYTES
+
+
+def slab_rows(height: int, nranks: int, rank: int):
+    """Rows [row0, row1) of slab `rank` of `nranks` (am_slab_rows)."""
+    a, b = C.c_uint32(0), C.c_uint32(0)
+    st = lib().am_slab_rows(height, nranks, rank, C.byref(a), C.byref(b))
+    if st != OK:
+        raise InvalidInputError(f"slab_rows({height}, {nranks}, {rank})")
+    return a.value, b.value
+
+
+def peer_export(slab: Grid) -> bytes:
+    """This rank's slab handles for the peer-memory transport (share with every rank, then peer_connect)."""
+    buf = (C.c_uint8 * PEER_BLOB_BYTES)()
+    _check(lib().am_peer_export(slab.ctx.handle, slab.handle, C.cast(buf, C.c_void_p)), slab.ctx, "peer_export")
+    return bytes(buf)
+
+
+def peer_connect(slab: Grid, nranks: int, rank: int, blobs):
+    """Connect this rank's slab to the others (blobs: every rank's peer_export, in rank order); am_propagate on
+    the slab then exchanges halos through peer memory."""
+    if len(blobs) != nranks or any(len(b) != PEER_BLOB_BYTES for b in blobs):
+        raise InvalidInputError("peer_connect: one blob of PEER_BLOB_BYTES per rank")
+    buf = (C.c_uint8 * (PEER_BLOB_BYTES * nranks)).from_buffer_copy(b"".join(blobs))
+    _check(lib().am_peer_connect(slab.ctx.handle, slab.handle, nranks, rank, C.cast(buf, C.c_void_p)), slab.ctx,
+           "peer_connect")
+
+
+def peer_gather(slab: Grid, full: Grid):
+    """Every rank's slab into `full` (full-size grid on this rank) by peer-to-peer copies."""
+    _check(lib().am_peer_gather(slab.ctx.handle, slab.handle, full.handle), slab.ctx, "peer_gather")
+    full.layers = slab.layers
 
 
 def slabs_gather(slabs, full: Grid):

@@ -17,6 +17,8 @@ constexpr int kLag = 2;        // blocks in flight before the host reads a fixed
 #endif
 constexpr int kLagTiles = AM_LAG_TILES;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
+struct PeerLink;         // peer-memory slab transport state (multigpu.cu)
+void peer_destroy(PeerLink* p);
 // Host side of a grid's fixed-point slots: pinned device-mapped mirror + one
 // event per slot.  Pinning and event creation are slow, so contexts recycle
 // these across grids.
@@ -78,6 +80,7 @@ struct am_grid {
   uint32_t t_blk = 0;                        // index of the next tile block (list / counter selection)
   void* t_bnd = nullptr;                     // slabs: first / last kK rows gathered for the neighbours (2 x kK x pitch)
   uint8_t* t_src = nullptr;                  // per tile: a source in its staged rows (TileBook::tsrc)
+  am::PeerLink* peer = nullptr;              // slabs: peer-memory transport (am_peer_connect)
   am::TileBook book() const {
     return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed, t_src};
   }
@@ -153,6 +156,12 @@ struct Transport {
   // a one-slab-per-process transport whose slab has a neighbour below it
   // (its bottom halo holds that neighbour's rows, not padding)
   virtual bool lower_neighbour() const { return false; }
+  // every slab of the chain (all ranks) meets its lower neighbour on a tile-chunk boundary, so every
+  // rank runs the same mode (active tiles or dense) and issues the same sequence of exchanges
+  virtual bool chain_tiles_ok() const { return true; }
+  // where the boundary kernel stores the slab's first (side 0) / last (side 1) kK rows for the next
+  // exchange_tiles(); nullptr: the slab's own t_bnd (the transport moves them)
+  virtual void* boundary_dst(int side) { (void)side; return nullptr; }
 };
 
 struct SlabRef {
@@ -164,6 +173,8 @@ struct SlabRef {
 am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t n, uint32_t method, uint64_t seed,
                            const uint64_t* offsets, uint32_t* pts, uint64_t cap, int32_t* status, uint32_t cell_h,
                            uint32_t cell_w);
+
+Transport* make_peer_transport(am_ctx* ctx, am_grid* g);
 
 // The propagation driver (capi.cu): runs slabs in lock step, 1 slab = single grid.
 am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t layers, uint32_t auto_cap,

@@ -164,7 +164,9 @@ void launch_tiles_finalize(const Geo& g, int cell_bits, unsigned long long* stat
 // bnd (2 x kK x pitch, the halo rows its neighbours read), and the list entry
 // of every boundary tile a frontier cell in the received halo rows can reach
 void launch_tiles_boundary(const Geo& g, int cell_bits, const unsigned long long* state, void* f0, void* f1,
-                           uint32_t l, void* bnd, cudaStream_t s);
+                           uint32_t l, void* dst_top, void* dst_bottom, cudaStream_t s);
+// min (take_max = 0) or max over n words into *out
+void launch_peer_reduce(const uint32_t* vals, uint32_t n, int take_max, uint32_t* out, cudaStream_t s);
 void launch_tiles_halo_scan(const Geo& g, int cell_bits, const void* f0, TileBook book, uint32_t blk, cudaStream_t s);
 void launch_promote(const Geo& g, const uint16_t* in, uint32_t* out, cudaStream_t s);
 void launch_zero_check(const Geo& g, int cell_bits, const void* val, uint32_t* flag, cudaStream_t s);

@@ -168,6 +168,7 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->t_bnd);
   am::dfree(ctx, g->t_processed);
   am::dfree(ctx, g->t_src);
+  am::peer_destroy(g->peer);
   delete g;
 }
 
@@ -428,9 +429,9 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     tiles = tiles && slabs[i].g->t_state;
     if (i + 1 < slabs.size()) tiles = tiles && slabs[i].g->g.H % kTileRows == 0;
   }
-  // one slab per process: the same rule for a rank with a lower neighbour (the
-  // other ranks may still use tiles: both exchanges move the same rows)
-  if (tr && tr->lower_neighbour()) tiles = tiles && slabs[0].g->g.H % kTileRows == 0;
+  // one slab per process: the same rule for every rank of the chain, so all ranks take the same mode
+  // (and the same number of exchanges: the transports pair them up in lock step)
+  if (tr) tiles = tiles && tr->chain_tiles_ok();
   const bool halos = tiles && (slabs.size() > 1 || tr);  // boundary exchange + halo scan every block
   uint64_t nt = 0;
   for (auto& sr : slabs) nt += tiles ? sr.g->g.ntiles() : 0;
@@ -598,7 +599,11 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     if (halos && blocked) {
       for (auto& sr : slabs) {  // boundary rows at layer l from the tiles' homes
         am_grid* g = sr.g;
-        launch_tiles_boundary(g->g, g->cell_bits, g->t_state, g->val[0], g->val[1], l, g->t_bnd, sr.ctx->stream);
+        void* top = tr ? tr->boundary_dst(0) : nullptr;
+        void* bot = tr ? tr->boundary_dst(1) : nullptr;
+        if (!top) top = g->t_bnd;
+        if (!bot) bot = static_cast<uint8_t*>(g->t_bnd) + (size_t)kK * g->g.pitch * (g->cell_bits / 8);
+        launch_tiles_boundary(g->g, g->cell_bits, g->t_state, g->val[0], g->val[1], l, top, bot, sr.ctx->stream);
         CKL();
       }
       if (tr && (st = tr->exchange_tiles())) return st;  // (a lone slab has no neighbours: halos stay padding)
@@ -769,8 +774,11 @@ am_status am_propagate(am_ctx* ctx, am_grid* g, uint32_t layers, uint32_t auto_c
   if (!ctx || !g) return AM_EINVAL;
   std::vector<am::SlabRef> one{{ctx, g}};
   am::Transport* tr = nullptr;
-  if (g->slab) {
-    if (!ctx->comm) return am::fail(ctx, AM_EINVAL, "slab grid: call am_comm_init or use am_slabs_propagate");
+  if (g->slab && g->peer) {
+    tr = am::make_peer_transport(ctx, g);
+  } else if (g->slab) {
+    if (!ctx->comm)
+      return am::fail(ctx, AM_EINVAL, "slab grid: call am_peer_connect / am_comm_init or use am_slabs_propagate");
     tr = am::make_nccl_transport(ctx, g);
     if (!tr) return am::fail(ctx, AM_ENCCL, "cannot build the NCCL halo transport");
   }

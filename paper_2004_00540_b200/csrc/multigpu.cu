@@ -13,13 +13,31 @@
 //    boundary rows over NVLink, ncclAllReduce(min/max) for the flags.
 //    libnccl.so.2 is opened at am_comm_init time (the process may already
 //    hold torch's copy), so the library has no link-time NCCL dependency.
+//  * peer memory (am_peer_*, one process per GPU or several on one GPU): the
+//    boundary kernel stores a slab's first / last K rows straight into the
+//    neighbours' halo inboxes through CUDA-IPC-mapped peer pointers (P2P
+//    stores over NVLink / NVSwitch), the slot words follow with one small
+//    peer copy, and the neighbour's stream waits on the writer's IPC event
+//    (a stream-ordered dependency: no kernel ever spins on another rank, so
+//    ranks sharing one GPU are safe).  A shared-memory counter per rank tells
+//    a host that the peer's event record for an exchange has been issued.
+//    No NCCL call and no collective sits on the per-block path.
 //  * in-process groups on one device (am_slabs_*): device-to-device copies
 //    on the shared stream.  They run the identical decomposition, so the
 //    slab logic is tested on a single GPU against the oracle.
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sched.h>
 #include <nccl.h>
+#include <sys/mman.h>
+#include <time.h>
+#include <unistd.h>
 
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
+#include <new>
 
 #include "am_host.hpp"
 
@@ -166,6 +184,14 @@ struct NcclTransport final : Transport {
   }
   bool host_combine() const override { return false; }
   bool lower_neighbour() const override { return ctx->comm->rank + 1 < ctx->comm->nranks; }
+  bool chain_tiles_ok() const override {
+    for (uint32_t r = 0; r + 1 < ctx->comm->nranks; ++r) {
+      uint32_t a = 0, z = 0;
+      slab_rows(g->total_h, ctx->comm->nranks, r, &a, &z);
+      if ((z - a) % kTileRows) return false;
+    }
+    return true;
+  }
 };
 
 Transport* make_nccl_transport(am_ctx* ctx, am_grid* g) {
@@ -232,6 +258,192 @@ struct LocalTransport final : Transport {
   bool host_combine() const override { return true; }
 };
 
+// ---------------------------------------------------------------- peer-memory transport
+//
+// Inbox of a slab (cudaMalloc, exported with cudaIpcGetMemHandle), by exchange parity p:
+//   rows from the slab above (its last kK rows)  -> from_up[p]   (kK rows x pitch x 4 B: room for 32-bit cells)
+//   rows from the slab below (its first kK rows) -> from_dn[p]
+//   slot words from above / below               -> words_up[p], words_dn[p] (kFlagSlots u32)
+//   one word per rank for reductions            -> red[p][kPeerMaxRanks]
+// Publish buffer: the slab's own rows for am_peer_gather (rows x pitch x 4 B).
+constexpr uint32_t kPeerMaxRanks = 64;
+constexpr uint32_t kPeerMagic = 0x41504545u;  // "EEPA"
+enum { kEvX0, kEvX1, kEvA0, kEvA1, kEvD0, kEvD1, kPeerEvents };
+enum { kChX, kChA, kChD, kPeerChannels };  // shm counters: exchanges, aux (reduce / publish), gather done
+
+struct PeerBlob {
+  uint32_t magic, rank_hint, pitch, rows;
+  uint64_t token;
+  cudaIpcMemHandle_t inbox, publish;
+  cudaIpcEventHandle_t ev[kPeerEvents];
+};
+static_assert(sizeof(PeerBlob) <= AM_PEER_BLOB_BYTES, "peer blob size");
+
+struct PeerLink {
+  // local, exported
+  uint8_t* inbox = nullptr;
+  uint8_t* publish = nullptr;
+  size_t halo_bytes = 0, inbox_bytes = 0, publish_bytes = 0;
+  cudaEvent_t ev[kPeerEvents] = {};
+  uint64_t token = 0;
+  // connection
+  bool connected = false;
+  uint32_t nranks = 1, rank = 0;
+  std::vector<uint8_t*> p_inbox, p_publish;          // per rank (own entry: local pointers)
+  std::vector<std::vector<cudaEvent_t>> p_ev;        // per rank x kPeerEvents (own entry: local events)
+  std::vector<uint32_t> row0, rows;                  // slab rows of every rank
+  std::atomic<uint64_t>* shm = nullptr;              // nranks x kPeerChannels counters (64 B apart)
+  size_t shm_bytes = 0;
+  char shm_name[64] = {};
+  uint64_t n[kPeerChannels] = {};                    // operations issued on each channel
+  int device = 0;
+
+  size_t off_from_up(uint32_t p) const { return p * halo_bytes; }
+  size_t off_from_dn(uint32_t p) const { return (2 + p) * halo_bytes; }
+  size_t off_words_up(uint32_t p) const { return 4 * halo_bytes + p * kFlagSlots * 4; }
+  size_t off_words_dn(uint32_t p) const { return 4 * halo_bytes + (2 + p) * kFlagSlots * 4; }
+  size_t off_red(uint32_t p) const { return 4 * halo_bytes + 4 * kFlagSlots * 4 + p * kPeerMaxRanks * 4; }
+  std::atomic<uint64_t>& counter(uint32_t r, int ch) { return shm[(r * kPeerChannels + ch) * 8]; }
+};
+
+void peer_destroy(PeerLink* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (uint32_t r = 0; r < p->p_inbox.size(); ++r) {
+    if (r == p->rank) continue;
+    if (p->p_inbox[r]) cudaIpcCloseMemHandle(p->p_inbox[r]);
+    if (p->p_publish[r]) cudaIpcCloseMemHandle(p->p_publish[r]);
+    for (cudaEvent_t e : p->p_ev[r])
+      if (e) cudaEventDestroy(e);
+  }
+  for (cudaEvent_t e : p->ev)
+    if (e) cudaEventDestroy(e);
+  if (p->inbox) cudaFree(p->inbox);
+  if (p->publish) cudaFree(p->publish);
+  if (p->shm) munmap(p->shm, p->shm_bytes);
+  if (p->shm && p->rank == 0 && p->shm_name[0]) shm_unlink(p->shm_name);
+  (void)cudaGetLastError();
+  delete p;
+}
+
+// Host side of "rank r has issued the record of its op number `target` on channel ch".
+static am_status peer_await(am_ctx* ctx, PeerLink* p, uint32_t r, int ch, uint64_t target) {
+  std::atomic<uint64_t>& c = p->counter(r, ch);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t spin = 0; c.load(std::memory_order_acquire) < target; ++spin) {
+    if ((spin & 1023) == 1023) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+        return fail(ctx, AM_EINTERNAL, "peer transport: rank %u never reached op %llu on channel %d", r,
+                    (unsigned long long)target, ch);
+      sched_yield();
+    }
+  }
+  return AM_OK;
+}
+
+// Record this rank's event for op `idx` on channel ch (event parity idx & 1) and announce it.
+static am_status peer_signal(am_ctx* ctx, PeerLink* p, int ch, int ev0, uint64_t idx) {
+  CK(cudaEventRecord(p->ev[ev0 + (idx & 1)], ctx->stream));
+  p->counter(p->rank, ch).store(idx + 1, std::memory_order_release);
+  return AM_OK;
+}
+
+// Make ctx's stream wait for rank r's op `idx` on channel ch.
+static am_status peer_wait(am_ctx* ctx, PeerLink* p, uint32_t r, int ch, int ev0, uint64_t idx) {
+  if (am_status st = peer_await(ctx, p, r, ch, idx + 1)) return st;
+  CK(cudaStreamWaitEvent(ctx->stream, p->p_ev[r][ev0 + (idx & 1)], 0));
+  return AM_OK;
+}
+
+struct PeerTransport final : Transport {
+  am_ctx* ctx;
+  am_grid* g;
+  PeerLink* p;
+  PeerTransport(am_ctx* c, am_grid* gg) : ctx(c), g(gg), p(gg->peer) {}
+  bool has_up() const { return p->rank > 0; }
+  bool has_dn() const { return p->rank + 1 < p->nranks; }
+  uint32_t parity() const { return (uint32_t)(p->n[kChX] & 1); }
+  void* boundary_dst(int side) override {
+    if (side == 0) return has_up() ? p->p_inbox[p->rank - 1] + p->off_from_dn(parity()) : nullptr;
+    return has_dn() ? p->p_inbox[p->rank + 1] + p->off_from_up(parity()) : nullptr;
+  }
+  // rows: copy this slab's boundary rows into the neighbours' inboxes (dense exchange; the tile exchange
+  // stored them from the boundary kernel already); always the slot words; then signal, wait, consume
+  am_status exchange_impl(bool rows_dense, bool rows_tiles) {
+    const uint32_t q = parity();
+    const uint64_t idx = p->n[kChX];
+    const size_t rb = row_bytes(g), bytes = (size_t)kK * rb;
+    uint8_t* cur = static_cast<uint8_t*>(g->val[rows_tiles ? 0 : g->cur]);
+    const uint32_t H = g->g.H;
+    if (has_up()) {
+      uint8_t* dst = p->p_inbox[p->rank - 1];
+      if (rows_dense)
+        CK(cudaMemcpyAsync(dst + p->off_from_dn(q), cur + (size_t)kK * rb, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(dst + p->off_words_dn(q), g->d_flags, kFlagSlots * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (has_dn()) {
+      uint8_t* dst = p->p_inbox[p->rank + 1];
+      if (rows_dense)
+        CK(cudaMemcpyAsync(dst + p->off_from_up(q), cur + (size_t)H * rb, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(dst + p->off_words_up(q), g->d_flags, kFlagSlots * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (am_status st = peer_signal(ctx, p, kChX, kEvX0, idx)) return st;
+    if (has_up())
+      if (am_status st = peer_wait(ctx, p, p->rank - 1, kChX, kEvX0, idx)) return st;
+    if (has_dn())
+      if (am_status st = peer_wait(ctx, p, p->rank + 1, kChX, kEvX0, idx)) return st;
+    if (has_up()) {
+      if (rows_dense || rows_tiles)
+        CK(cudaMemcpyAsync(cur, p->inbox + p->off_from_up(q), bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(g->d_flags + kFlagRecvUp, p->inbox + p->off_words_up(q), kFlagSlots * 4,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (has_dn()) {
+      if (rows_dense || rows_tiles)
+        CK(cudaMemcpyAsync(cur + (size_t)(kK + H) * rb, p->inbox + p->off_from_dn(q), bytes, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+      CK(cudaMemcpyAsync(g->d_flags + kFlagRecvDn, p->inbox + p->off_words_dn(q), kFlagSlots * 4,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ++p->n[kChX];
+    launch_flags_merge(g->d_flags, ctx->stream);
+    ++ctx->launches;
+    if (cudaError_t e = cudaPeekAtLastError()) return fail(ctx, AM_ECUDA, "flags merge: %s", cudaGetErrorString(e));
+    return AM_OK;
+  }
+  am_status exchange() override { return exchange_impl(true, false); }
+  am_status exchange_tiles() override { return exchange_impl(false, true); }
+  am_status exchange_flags() override { return exchange_impl(false, false); }
+  uint32_t span() const override { return p->nranks; }
+  am_status reduce(std::vector<uint32_t*>& words, bool take_max) override {
+    const uint64_t idx = p->n[kChA];
+    const uint32_t q = (uint32_t)(idx & 1);
+    for (uint32_t r = 0; r < p->nranks; ++r)
+      CK(cudaMemcpyAsync(p->p_inbox[r] + p->off_red(q) + 4 * p->rank, words[0], 4, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+    if (am_status st = peer_signal(ctx, p, kChA, kEvA0, idx)) return st;
+    for (uint32_t r = 0; r < p->nranks; ++r)
+      if (r != p->rank)
+        if (am_status st = peer_wait(ctx, p, r, kChA, kEvA0, idx)) return st;
+    ++p->n[kChA];
+    launch_peer_reduce(reinterpret_cast<const uint32_t*>(p->inbox + p->off_red(q)), p->nranks, take_max ? 1 : 0,
+                       words[0], ctx->stream);
+    ++ctx->launches;
+    CK(cudaPeekAtLastError());
+    return AM_OK;
+  }
+  bool host_combine() const override { return false; }
+  bool lower_neighbour() const override { return has_dn(); }
+  bool chain_tiles_ok() const override {
+    for (uint32_t r = 0; r + 1 < p->nranks; ++r)
+      if (p->rows[r] % kTileRows) return false;
+    return true;
+  }
+};
+
+Transport* make_peer_transport(am_ctx* ctx, am_grid* g) { return new PeerTransport(ctx, g); }
+
 // Places a propagated slab's own rows into the full grid's field.
 static am_status adopt_full(am_ctx* ctx, am_grid* full, const am_grid* like) {
   am_status st = set_cell_bits(ctx, full, like->cell_bits);
@@ -282,6 +494,146 @@ am_status am_slabs_gather(am_ctx* ctx, am_grid** slabs, uint32_t n, am_grid* ful
     CK(cudaMemcpyAsync(static_cast<uint8_t*>(full->val[0]) + (size_t)(kK + s->row0) * rb, alloc_rows(s, kK),
                        (size_t)s->g.H * rb, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return AM_OK;
+}
+
+am_status am_slab_rows(uint32_t height, uint32_t nranks, uint32_t rank, uint32_t* row0, uint32_t* row1) {
+  if (!row0 || !row1 || nranks == 0 || rank >= nranks) return AM_EINVAL;
+  slab_rows(height, nranks, rank, row0, row1);
+  return AM_OK;
+}
+
+am_status am_peer_export(am_ctx* ctx, am_grid* g, uint8_t* blob) {
+  if (!ctx || !g || !blob) return AM_EINVAL;
+  if (!g->slab) return fail(ctx, AM_EINVAL, "am_peer_export: not a slab grid");
+  CK(cudaSetDevice(ctx->device));
+  peer_destroy(g->peer);
+  g->peer = nullptr;
+  PeerLink* p = new (std::nothrow) PeerLink();
+  if (!p) return AM_EOOM;
+  p->device = ctx->device;
+  const size_t rb4 = (size_t)g->g.pitch * 4;
+  p->halo_bytes = (size_t)kK * rb4;
+  p->inbox_bytes = p->off_red(2);
+  p->publish_bytes = (size_t)g->g.H * rb4;
+  cudaError_t e = cudaMalloc(&p->inbox, p->inbox_bytes);
+  if (!e) e = cudaMalloc(&p->publish, p->publish_bytes);
+  if (!e) e = cudaMemset(p->inbox, 0, p->inbox_bytes);
+  for (int i = 0; i < kPeerEvents && !e; ++i)
+    e = cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming | cudaEventInterprocess);
+  PeerBlob b{};
+  b.magic = kPeerMagic;
+  b.pitch = g->g.pitch;
+  b.rows = g->g.H;
+  {
+    timespec ts{};
+    clock_gettime(CLOCK_REALTIME, &ts);
+    p->token = ((uint64_t)getpid() << 40) ^ (uint64_t)ts.tv_nsec ^ ((uint64_t)ts.tv_sec << 20) ^
+               reinterpret_cast<uintptr_t>(p);
+  }
+  b.token = p->token;
+  if (!e) e = cudaIpcGetMemHandle(&b.inbox, p->inbox);
+  if (!e) e = cudaIpcGetMemHandle(&b.publish, p->publish);
+  for (int i = 0; i < kPeerEvents && !e; ++i) e = cudaIpcGetEventHandle(&b.ev[i], p->ev[i]);
+  if (e) {
+    peer_destroy(p);
+    (void)cudaGetLastError();
+    return fail(ctx, e == cudaErrorMemoryAllocation ? AM_EOOM : AM_ECUDA, "am_peer_export: %s", cudaGetErrorString(e));
+  }
+  memset(blob, 0, AM_PEER_BLOB_BYTES);
+  memcpy(blob, &b, sizeof b);
+  g->peer = p;
+  return AM_OK;
+}
+
+am_status am_peer_connect(am_ctx* ctx, am_grid* g, uint32_t nranks, uint32_t rank, const uint8_t* blobs) {
+  if (!ctx || !g || !blobs || nranks == 0 || rank >= nranks || nranks > kPeerMaxRanks) return AM_EINVAL;
+  PeerLink* p = g->peer;
+  if (!p || p->connected) return fail(ctx, AM_EINVAL, "am_peer_connect: export this slab (once) first");
+  uint32_t r0 = 0, r1 = 0;
+  slab_rows(g->total_h, nranks, rank, &r0, &r1);
+  if (r0 != g->row0 || r1 - r0 != g->g.H)
+    return fail(ctx, AM_EINVAL, "am_peer_connect: slab rows [%u, %u) are not rank %u's share [%u, %u)", g->row0,
+                g->row0 + g->g.H, rank, r0, r1);
+  CK(cudaSetDevice(ctx->device));
+  std::vector<PeerBlob> b(nranks);
+  for (uint32_t r = 0; r < nranks; ++r) {
+    memcpy(&b[r], blobs + (size_t)r * AM_PEER_BLOB_BYTES, sizeof(PeerBlob));
+    if (b[r].magic != kPeerMagic || b[r].pitch != g->g.pitch)
+      return fail(ctx, AM_EINVAL, "am_peer_connect: blob %u is not a slab of this grid", r);
+  }
+  if (b[rank].token != p->token) return fail(ctx, AM_EINVAL, "am_peer_connect: blob %u is not this slab's", rank);
+  p->nranks = nranks;
+  p->rank = rank;
+  p->p_inbox.assign(nranks, nullptr);
+  p->p_publish.assign(nranks, nullptr);
+  p->p_ev.assign(nranks, std::vector<cudaEvent_t>(kPeerEvents, nullptr));
+  p->row0.resize(nranks);
+  p->rows.resize(nranks);
+  for (uint32_t r = 0; r < nranks; ++r) {
+    uint32_t a = 0, z = 0;
+    slab_rows(g->total_h, nranks, r, &a, &z);
+    p->row0[r] = a;
+    p->rows[r] = z - a;
+    if (r == rank) {
+      p->p_inbox[r] = p->inbox;
+      p->p_publish[r] = p->publish;
+      for (int i = 0; i < kPeerEvents; ++i) p->p_ev[r][i] = p->ev[i];
+      continue;
+    }
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, b[r].inbox, cudaIpcMemLazyEnablePeerAccess);
+    p->p_inbox[r] = static_cast<uint8_t*>(ptr);
+    if (!e) e = cudaIpcOpenMemHandle(&ptr, b[r].publish, cudaIpcMemLazyEnablePeerAccess);
+    if (!e) p->p_publish[r] = static_cast<uint8_t*>(ptr);
+    for (int i = 0; i < kPeerEvents && !e; ++i) e = cudaIpcOpenEventHandle(&p->p_ev[r][i], b[r].ev[i]);
+    if (e) {
+      (void)cudaGetLastError();
+      return fail(ctx, AM_ECUDA, "am_peer_connect: rank %u handles: %s", r, cudaGetErrorString(e));
+    }
+  }
+  // host counters shared by the ranks (one node): named after rank 0's token
+  snprintf(p->shm_name, sizeof p->shm_name, "/actmap_peer_%016llx", (unsigned long long)b[0].token);
+  p->shm_bytes = (size_t)nranks * kPeerChannels * 64;
+  const int fd = shm_open(p->shm_name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0) return fail(ctx, AM_EINTERNAL, "am_peer_connect: shm_open(%s) failed", p->shm_name);
+  if (ftruncate(fd, (off_t)p->shm_bytes) != 0) {
+    close(fd);
+    return fail(ctx, AM_EINTERNAL, "am_peer_connect: ftruncate failed");
+  }
+  void* m = mmap(nullptr, p->shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (m == MAP_FAILED) return fail(ctx, AM_EINTERNAL, "am_peer_connect: mmap failed");
+  p->shm = static_cast<std::atomic<uint64_t>*>(m);
+  p->connected = true;
+  return AM_OK;
+}
+
+am_status am_peer_gather(am_ctx* ctx, am_grid* slab, am_grid* full) {
+  if (!ctx || !slab || !full) return AM_EINVAL;
+  PeerLink* p = slab->peer;
+  if (!p || !p->connected) return fail(ctx, AM_EINVAL, "am_peer_gather: slab not connected");
+  if (full->slab || full->g.pitch != slab->g.pitch || full->g.H != slab->total_h)
+    return fail(ctx, AM_EINVAL, "am_peer_gather: full grid does not match the slab");
+  CK(cudaSetDevice(ctx->device));
+  am_status st = adopt_full(ctx, full, slab);
+  if (st) return st;
+  const size_t rb = row_bytes(slab);
+  const uint64_t ia = p->n[kChA], id = p->n[kChD];
+  if (id > 0)  // every peer finished reading this rank's previous publish
+    for (uint32_t r = 0; r < p->nranks; ++r)
+      if (r != p->rank && (st = peer_wait(ctx, p, r, kChD, kEvD0, id - 1))) return st;
+  CK(cudaMemcpyAsync(p->publish, alloc_rows(slab, kK), (size_t)slab->g.H * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((st = peer_signal(ctx, p, kChA, kEvA0, ia))) return st;
+  for (uint32_t r = 0; r < p->nranks; ++r)
+    if (r != p->rank && (st = peer_wait(ctx, p, r, kChA, kEvA0, ia))) return st;
+  for (uint32_t r = 0; r < p->nranks; ++r)  // peer-to-peer copies of every slab into the full field
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(full->val[0]) + (size_t)(kK + p->row0[r]) * rb, p->p_publish[r],
+                       (size_t)p->rows[r] * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((st = peer_signal(ctx, p, kChD, kEvD0, id))) return st;
+  ++p->n[kChA];
+  ++p->n[kChD];
   CK(cudaStreamSynchronize(ctx->stream));
   return AM_OK;
 }

@@ -1606,7 +1606,7 @@ __global__ void k_tiles_finalize(Geo g, unsigned long long* __restrict__ state, 
 template <int CB>
 __global__ void k_tiles_boundary(Geo g, const unsigned long long* __restrict__ state,
                                  const typename Cell<CB>::T* __restrict__ f0, ptrdiff_t delta, uint32_t l,
-                                 typename Cell<CB>::T* __restrict__ bnd) {
+                                 typename Cell<CB>::T* __restrict__ dst0, typename Cell<CB>::T* __restrict__ dst1) {
   const uint32_t w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (w >= 2 * g.tbands) return;
   const int lane = threadIdx.x & 31;
@@ -1626,7 +1626,7 @@ __global__ void k_tiles_boundary(Geo g, const unsigned long long* __restrict__ s
       x.z = add_lag<CB>(x.z, lagw);
       x.w = add_lag<CB>(x.w, lagw);
     }
-    *reinterpret_cast<uint4*>(bnd + ((size_t)side * kK + k) * g.pitch + col) = x;
+    *reinterpret_cast<uint4*>((side ? dst1 : dst0) + (size_t)k * g.pitch + col) = x;  // (peer memory: P2P store)
   }
 }
 
@@ -1909,15 +1909,28 @@ __global__ void k_publish_flag(FlagSink f) {
 void launch_publish_flag(FlagSink f, cudaStream_t s) { k_publish_flag<<<1, 1, 0, s>>>(f); }
 
 void launch_tiles_boundary(const Geo& g, int cb, const unsigned long long* state, void* f0, void* f1, uint32_t l,
-                           void* bnd, cudaStream_t s) {
+                           void* dst_top, void* dst_bottom, cudaStream_t s) {
   const uint32_t warps = 2 * g.tbands;
   if (cb == 16) {
     auto* a = (const uint16_t*)f0;
-    k_tiles_boundary<16><<<(warps + 3) / 4, 128, 0, s>>>(g, state, a, (const uint16_t*)f1 - a, l, (uint16_t*)bnd);
+    k_tiles_boundary<16><<<(warps + 3) / 4, 128, 0, s>>>(g, state, a, (const uint16_t*)f1 - a, l, (uint16_t*)dst_top,
+                                                         (uint16_t*)dst_bottom);
   } else {
     auto* a = (const uint32_t*)f0;
-    k_tiles_boundary<32><<<(warps + 3) / 4, 128, 0, s>>>(g, state, a, (const uint32_t*)f1 - a, l, (uint32_t*)bnd);
+    k_tiles_boundary<32><<<(warps + 3) / 4, 128, 0, s>>>(g, state, a, (const uint32_t*)f1 - a, l, (uint32_t*)dst_top,
+                                                         (uint32_t*)dst_bottom);
   }
+}
+
+__global__ void k_peer_reduce(const uint32_t* __restrict__ vals, uint32_t n, int take_max, uint32_t* out) {
+  uint32_t m = take_max ? 0u : 0xFFFFFFFFu;
+  for (uint32_t i = threadIdx.x; i < n; i += 32) m = take_max ? max(m, vals[i]) : min(m, vals[i]);
+  m = take_max ? __reduce_max_sync(0xffffffffu, m) : __reduce_min_sync(0xffffffffu, m);
+  if (threadIdx.x == 0) *out = m;
+}
+
+void launch_peer_reduce(const uint32_t* vals, uint32_t n, int take_max, uint32_t* out, cudaStream_t s) {
+  k_peer_reduce<<<1, 32, 0, s>>>(vals, n, take_max, out);
 }
 
 void launch_tiles_halo_scan(const Geo& g, int cb, const void* f0, TileBook book, uint32_t blk, cudaStream_t s) {

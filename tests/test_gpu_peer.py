@@ -1,0 +1,75 @@
+"""Peer-memory slab transport (am_peer_export / am_peer_connect / am_peer_gather, multigpu.cu) with 2 and
+3 processes sharing cuda:0, against the CPU oracle: the map every rank assembles equals
+oracle propagate / propagate_auto bit for bit, and every rank reports the same layers_used / cause.
+The ranks' only cross-process dependencies are stream waits on IPC events, so sharing one
+GPU is safe; the same code drives one process per GPU over NVLink."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.oracle_adapter import O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run_ranks(tmp_path, n, **kw):
+    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+            os.path.join(ROOT, "tests", "workers", "peer_worker.py"), "--out", str(tmp_path)]
+    for k, v in kw.items():
+        args += [f"--{k}", str(v)]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    out = subprocess.run(args, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    ranks = [json.load(open(os.path.join(tmp_path, f"rank{r}.json"))) for r in range(n)]
+    return ranks
+
+
+CASES = [  # (nranks, generator, w, h, density, sources, layers (0 auto), cap)
+    (2, "random", 700, 600, 0.3, 3, 0, 4 * 700),      # active tiles across the cut (slabs on 32-row chunks)
+    (3, "random", 500, 900, 0.35, 5, 0, 4 * 900),
+    (2, "random", 300, 50, 0.2, 2, 0, 4 * 300),       # short slabs: dense exchange
+    (3, "random", 640, 640, 0.3, 4, 77, 0),           # fixed L (not a multiple of the block depth)
+    (2, "comb", 128, 600, 0.0, 1, 0, 128 * 600),      # comb maze: > 32767 layers, 16 -> 32-bit promotion
+]
+
+
+@pytest.mark.parametrize("n,gen,w,h,dens,ns,layers,cap", CASES)
+def test_peer_slabs_match_oracle(tmp_path, n, gen, w, h, dens, ns, layers, cap):
+    ranks = run_ranks(tmp_path, n, gen=gen, w=w, h=h, density=dens, seed=11 + n, sources=ns, layers=layers,
+                      cap=cap, reps=2)
+    if gen == "comb":
+        occ = O.comb_maze(w, h)
+        src = np.array([[h - 1, 0]], np.uint32)
+    else:
+        occ = O.random_maze(w, h, dens, 11 + n)
+        rng = np.random.default_rng(11 + n)
+        free = np.argwhere(occ == 0)
+        src = free[rng.choice(len(free), size=min(ns, len(free)), replace=False)].astype(np.uint32)
+    sm = O.source_mask(occ, src)
+    if layers:
+        ref, want = O.propagate(occ, sm, layers, threads=os.cpu_count() or 1), (layers, 3)
+    else:
+        ref, lu, cause = O.propagate_auto(occ, sm, cap, threads=os.cpu_count() or 1)
+        want = (lu, cause)
+    rows = sorted(tuple(r["rows"]) for r in ranks)
+    assert rows[0][0] == 0 and rows[-1][1] == h and all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+    for rep in range(2):
+        for r in ranks:
+            got = r["results"][rep]
+            assert (got["layers_used"], got["cause"]) == want, (r["rank"], rep, got, want)
+        assert np.array_equal(np.load(os.path.join(tmp_path, f"map_{rep}.npy")), ref), rep
+    if gen == "comb":
+        assert ranks[0]["results"][0]["cell_bits"] == 32
