@@ -87,6 +87,12 @@ def make_workload(gen):
     return occ, src, tgt
 
 
+def c1_workload(am):
+    occ = am.random_maze(1024, 1024, 0.30, 1)
+    src, tgt = points_for(occ, 1, 1, 1)
+    return occ, src, tgt, 4 * 1024
+
+
 def c2_workload(am):
     occ = am.kruskal_maze(4096, 4096, 2)
     src, tgt = points_for(occ, 16, 16, 2)
@@ -314,7 +320,7 @@ def run_reference(args, rank, world):
     # full CPU solves of the two configurations that finish in seconds on the host
     full = []
     c1 = O.random_maze(1024, 1024, 0.30, 1)
-    s1 = O.sample_free_cells(c1, 1, 1)
+    s1, _ = points_for(c1, 1, 1, 1)
     for name, occ_c, src_c, cap in (("C1 1024^2 random 0.30, 1 source", c1, s1, 4 * 1024),
                                     ("C2 4096^2 Kruskal maze, 16 sources", O.kruskal_maze(4096, 4096, 2), None,
                                      4096 * 4096)):
@@ -346,33 +352,46 @@ class Solver:
     """One timed step = propagate_auto to the fixed point + Euclidean paths of this rank's targets to the host.
 
     N == 1: the whole C4 grid on one GPU (inputs resident in HBM).
-    N > 1: row slabs (one per rank, NCCL halo exchange per block), the fixed-point map all-gathered into a
-    full-size field on every rank, each rank tracing targets[rank::N]."""
+    N > 1, peer transport: row slabs (one per rank, halos through peer memory every block); each rank traces
+    targets[rank::N] on the distributed map, its walkers reading across slab edges through the peers'
+    published rows (no gather).  N > 1, NCCL transport: the map is all-gathered into a full-size field on
+    every rank first."""
 
     def __init__(self, am, torch, ctx, occ, src, tgt, rank, world, local_rank, transport="peer"):
         self.am, self.torch, self.ctx, self.world, self.rank = am, torch, ctx, world, rank
         dev = torch.device(f"cuda:{local_rank}")
         self.stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
-        d_occ = torch.from_numpy(occ).to(dev)
-        d_src = torch.from_numpy(src.astype(np.int32)).to(dev)
+        self.peer = world > 1 and transport == "peer"
         my_tgt = tgt[rank::world]
         self.tgt = my_tgt
         self.d_tgt = torch.from_numpy(my_tgt.astype(np.int32)).to(dev)
-        torch.cuda.synchronize()
-        self.full = am.Grid.from_device(W, H, d_occ.data_ptr(), d_src.data_ptr(), len(src), ctx)
+        self.full = None
+        if not self.peer:
+            d_occ = torch.from_numpy(occ).to(dev)
+            d_src = torch.from_numpy(src.astype(np.int32)).to(dev)
+            torch.cuda.synchronize()
+            self.full = am.Grid.from_device(W, H, d_occ.data_ptr(), d_src.data_ptr(), len(src), ctx)
+            del d_occ, d_src
         self.slab = None
         self.transport = transport
         if world > 1:
             self.slab = make_slab(am, ctx, occ, src, rank, world, transport)
-        del d_occ, d_src
         n = len(my_tgt)
         self.n = n
         self.d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
         self.d_status = torch.zeros(n, dtype=torch.int32, device=dev)
         r = self.propagate()
-        off, st = self.full.path_counts(my_tgt, am.EUCLIDEAN)
-        self.total = int(off[-1])
-        self.covered = int((st == 0).sum())
+        if self.peer:  # point counts come with the first trace (an upper-bound buffer), then the exact one
+            self.total = max(n, 1) * (r.layers_computed + 2)
+            self.d_pts = torch.empty(2 * self.total, dtype=torch.int32, device=dev)
+            self.trace()
+            ctx.synchronize()
+            self.total = int(self.d_off[-1].item())
+            self.covered = int((self.d_status == 0).sum().item())
+        else:
+            off, st = self.full.path_counts(my_tgt, am.EUCLIDEAN)
+            self.total = int(off[-1])
+            self.covered = int((st == 0).sum())
         self.d_pts = torch.empty(2 * max(self.total, 1), dtype=torch.int32, device=dev)
         self.h_pts = torch.empty(2 * max(self.total, 1), dtype=torch.int32, pin_memory=True)
         self.h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
@@ -380,16 +399,25 @@ class Solver:
         log(f"[rank {rank}] L_used={r.layers_used} cause={r.cause} computed={r.layers_computed} bits={r.cell_bits} "
             f"blocks={r.block_launches} paths: points={self.total}, covered={self.covered}/{n}")
 
+    def grid(self):
+        return self.full if self.full is not None else self.slab
+
     def propagate(self):
         if self.slab is None:
             return self.full.propagate_auto(AUTO_CAP)
         r = self.slab.propagate_auto(AUTO_CAP)
-        gather(self.am, self.ctx, self.slab, self.full, self.transport)
+        if not self.peer:
+            gather(self.am, self.ctx, self.slab, self.full, self.transport)
         return r
 
     def trace(self):
-        self.ctx.trace_device(self.full, self.d_tgt.data_ptr(), self.n, self.am.EUCLIDEAN, 0, self.d_off.data_ptr(),
-                              self.d_pts.data_ptr(), self.total, self.d_status.data_ptr())
+        if self.peer:
+            self.am.peer_trace_device(self.slab, self.d_tgt.data_ptr(), self.n, self.am.EUCLIDEAN, 0,
+                                      self.d_off.data_ptr(), self.d_pts.data_ptr(), self.total,
+                                      self.d_status.data_ptr())
+        else:
+            self.ctx.trace_device(self.full, self.d_tgt.data_ptr(), self.n, self.am.EUCLIDEAN, 0,
+                                  self.d_off.data_ptr(), self.d_pts.data_ptr(), self.total, self.d_status.data_ptr())
 
     def step(self):
         r = self.propagate()
@@ -413,7 +441,8 @@ class Solver:
         del self.h_pts, self.h_off, self.h_status, self.d_pts, self.d_off, self.d_status, self.d_tgt
         if self.slab is not None:
             self.slab.close()
-        self.full.close()
+        if self.full is not None:
+            self.full.close()
 
 
 def make_slab(am, ctx, occ, src, rank, world, transport):
@@ -462,17 +491,39 @@ def e2e_solve(am, ctx, occ, src, tgt, rank, world, h_map, h_pts, split=None, tra
     t0 = time.perf_counter()
     s = make_slab(am, ctx, occ, src, rank, world, transport)
     r0, r1 = s.row0, s.row0 + s.height
-    s.propagate_auto(AUTO_CAP)
-    full = am.Grid(occ, src, ctx)
-    gather(am, ctx, s, full, transport)
-    off, pts, st = full.trace(my_tgt, am.EUCLIDEAN, out=h_pts)
+    r = s.propagate_auto(AUTO_CAP)
+    if transport == "peer":  # paths on the distributed map: targets up, points down (torch device buffers)
+        import torch
+
+        dev = torch.device(f"cuda:{ctx.device}")
+        n = len(my_tgt)
+        cap = max(n, 1) * (r.layers_computed + 2)
+        d_t = torch.from_numpy(my_tgt.astype(np.int32)).to(dev)
+        d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        d_st = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        d_pts = torch.empty(2 * cap, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        am.peer_trace_device(s, d_t.data_ptr(), n, am.EUCLIDEAN, 0, d_off.data_ptr(), d_pts.data_ptr(), cap,
+                             d_st.data_ptr())
+        ctx.synchronize()
+        off = d_off.cpu().numpy().view(np.uint64)
+        total = int(off[-1])
+        pts = h_pts[:total]
+        pts[:] = d_pts[: 2 * total].cpu().numpy().view(np.uint32).reshape(-1, 2)
+        st = d_st[:n].cpu().numpy()
+        full = None
+    else:
+        full = am.Grid(occ, src, ctx)
+        gather(am, ctx, s, full, transport)
+        off, pts, st = full.trace(my_tgt, am.EUCLIDEAN, out=h_pts)
     t2 = time.perf_counter()
     s.activity(out=h_map[r0:r1])
     t3 = time.perf_counter()
     if split is not None:
         split.setdefault("map_d2h", []).append(t3 - t2)
     s.close()
-    full.close()
+    if full is not None:
+        full.close()
     return off, pts, st, t2 - t0
 
 
@@ -521,6 +572,8 @@ def run_configs(am, torch, ctx, info_c4, occ4, src4, hops4, parity):
         log(f"config {name}: {json.dumps(e)}")
         return e
 
+    occ, src, tgt, cap = c1_workload(am)
+    out.append(grid_cfg("C1 1024^2 random maze (0.30), 1 source / 1 target, auto", occ, src, tgt, cap))
     occ, src, tgt, cap = c2_workload(am)
     out.append(grid_cfg("C2 4096^2 Kruskal maze, 16 sources / 16 targets, auto", occ, src, tgt, cap))
     occ, src, tgt, cap = c3_workload(am)
@@ -645,7 +698,7 @@ def run_b200(args, rank, world, local_rank):
     rows_here = (sol.slab.height if sol.slab is not None else H)
     per_launch_ms = stencil_ms / max(blocks, 1)
     tile_mode = tiles_all > 0
-    info = sol.full.info()
+    info = sol.grid().info()
     if tile_mode:
         cells_per_launch = tiles_done * info["tile_rows"] * info["tile_cols"] * LAYERS_PER_BLOCK / max(blocks, 1)
         kernel = "am::k_block_tiles<16>"

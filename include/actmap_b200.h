@@ -201,6 +201,14 @@ am_status am_peer_export(am_ctx *ctx, am_grid *slab, uint8_t *blob /* AM_PEER_BL
 am_status am_peer_connect(am_ctx *ctx, am_grid *slab, uint32_t nranks, uint32_t rank,
                           const uint8_t *blobs /* nranks x AM_PEER_BLOB_BYTES, rank order */);
 am_status am_peer_gather(am_ctx *ctx, am_grid *slab, am_grid *full);
+/* am_trace_paths_device on the map distributed over the connected slabs: every
+ * rank publishes its rows, then the walkers read across slab edges through
+ * the peer-mapped publish buffers (no full-map gather).  Any rank may trace
+ * any target (grid coordinates); every rank must call it (the publish is a
+ * rendezvous), with n = 0 if it has no targets. */
+am_status am_peer_trace_paths_device(am_ctx *ctx, am_grid *slab, const uint32_t *d_tgt_rc, uint64_t n,
+                                     uint32_t method, uint64_t seed, uint64_t *d_offsets, uint32_t *d_pts_rc,
+                                     uint64_t pts_capacity, int32_t *d_status);
 
 /* ---- small-grid batch (BASELINE.json config 5) ---------------------------
  * n independent width x height mazes solved in one device run: the

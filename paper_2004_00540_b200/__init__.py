@@ -128,6 +128,7 @@ def lib():
             "am_peer_export": (st, [_vp, _vp, _vp]),
             "am_peer_connect": (st, [_vp, _vp, u32, u32, _vp]),
             "am_peer_gather": (st, [_vp, _vp, _vp]),
+            "am_peer_trace_paths_device": (st, [_vp, _vp, _vp, u64, u32, u64, _vp, _vp, u64, _vp]),
             "am_batch_create": (st, [_vp, u32, u32, u32, _vp, _vp, _vp, C.POINTER(_vp)]),
             "am_batch_destroy": (st, [_vp, _vp]),
             "am_batch_propagate": (st, [_vp, _vp, u32, u32, _vp, _vp, C.POINTER(_PropResult)]),
@@ -573,6 +574,15 @@ def peer_gather(slab: Grid, full: Grid):
     """Every rank's slab into `full` (full-size grid on this rank) by peer-to-peer copies."""
     _check(lib().am_peer_gather(slab.ctx.handle, slab.handle, full.handle), slab.ctx, "peer_gather")
     full.layers = slab.layers
+
+
+def peer_trace_device(slab: Grid, d_tgt: int, n: int, method: int, seed: int, d_offsets: int, d_pts: int,
+                      cap: int, d_status: int):
+    """am_peer_trace_paths_device: trace targets (device pointers, grid coordinates) on the map distributed
+    over the connected slabs, reading across slab edges through peer memory.  Every rank must call it."""
+    _check(lib().am_peer_trace_paths_device(slab.ctx.handle, slab.handle, C.c_void_p(d_tgt), n, method, seed,
+                                            C.c_void_p(d_offsets), C.c_void_p(d_pts), cap, C.c_void_p(d_status)),
+           slab.ctx, "peer_trace")
 
 
 def slabs_gather(slabs, full: Grid):

@@ -175,6 +175,8 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
                            uint32_t cell_w);
 
 Transport* make_peer_transport(am_ctx* ctx, am_grid* g);
+// per-grid path-extraction scratch (targets, counts, offsets, status) for n targets
+am_status trace_scratch(am_ctx* ctx, am_grid* g, uint64_t n);
 
 // The propagation driver (capi.cu): runs slabs in lock step, 1 slab = single grid.
 am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t layers, uint32_t auto_cap,

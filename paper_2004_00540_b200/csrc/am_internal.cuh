@@ -183,6 +183,16 @@ void launch_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* d_src_rc, uint
                           const uint8_t* d_occ, int* d_err, cudaStream_t s);
 
 // ---- path extraction (trace.cu) ----
+// A map distributed over row slabs (peer transport): grid row r lives in slab s with row0[s] <= r <
+// row0[s+1], at base[s] + (r - row0[s]) * pitch cells (base: the slabs' published rows, peer-mapped);
+// rows outside the grid read the zero row.  Device memory, built by am_peer_connect.
+constexpr uint32_t kSlabDirMax = 64;
+struct SlabDir {
+  uint32_t n;
+  uint32_t row0[kSlabDirMax + 1];
+  const void* base[kSlabDirMax];
+  const void* zero;  // one zero row (pitch cells of either width)
+};
 struct MapView {
   const void* val;        // encoded pitched field (cell_bits 16/32) or plain dense uint32 (cell_bits 0)
   const uint8_t* srcmask; // pitched (encoded) or dense (plain)
@@ -190,6 +200,17 @@ struct MapView {
   int cell_bits;          // 16, 32, or 0 = plain dense uint32 + dense occupancy
   const uint8_t* occ;     // plain mode only: dense occupancy
   uint32_t layers;        // layers represented by the values (for point counts)
+  const SlabDir* dir = nullptr;  // encoded maps only: the field is distributed over row slabs (val unused)
+  // allocated row arow of an encoded field (cell 0 = allocated column 0)
+  template <typename T>
+  __device__ __forceinline__ const T* row(int arow) const {
+    if (!dir) return static_cast<const T*>(val) + (size_t)arow * g.pitch;
+    const int r = arow - (int)g.pad;
+    if (r < 0 || r >= (int)g.H) return static_cast<const T*>(dir->zero);
+    uint32_t s = 0;
+    while (s + 1 < dir->n && (uint32_t)r >= dir->row0[s + 1]) ++s;
+    return static_cast<const T*>(dir->base[s]) + (size_t)((uint32_t)r - dir->row0[s]) * g.pitch;
+  }
 };
 void launch_path_counts(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int method, uint64_t seed,
                         uint64_t* counts, int32_t* status, cudaStream_t s);

@@ -901,6 +901,10 @@ static am_status ensure_targets(am_ctx* ctx, am_grid* g, uint64_t n) {
   return AM_OK;
 }
 
+namespace am {
+am_status trace_scratch(am_ctx* ctx, am_grid* g, uint64_t n) { return ensure_targets(ctx, g, n); }
+}  // namespace am
+
 // Host straighten (reconstruct.hpp:54-58, pin P4, strict rule) -- only needed
 // for caller-uploaded maps; see the header.
 static uint64_t straighten_strict(uint32_t* p, uint64_t n, const std::vector<uint8_t>& occ, uint32_t W) {

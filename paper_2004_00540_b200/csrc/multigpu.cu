@@ -297,6 +297,8 @@ struct PeerLink {
   char shm_name[64] = {};
   uint64_t n[kPeerChannels] = {};                    // operations issued on each channel
   int device = 0;
+  SlabDir* dir = nullptr;                            // device: every rank's published rows (peer traces)
+  void* zero_row = nullptr;                          // device: one zero row (pitch x 4 B)
 
   size_t off_from_up(uint32_t p) const { return p * halo_bytes; }
   size_t off_from_dn(uint32_t p) const { return (2 + p) * halo_bytes; }
@@ -319,6 +321,8 @@ void peer_destroy(PeerLink* p) {
   }
   for (cudaEvent_t e : p->ev)
     if (e) cudaEventDestroy(e);
+  if (p->dir) cudaFree(p->dir);
+  if (p->zero_row) cudaFree(p->zero_row);
   if (p->inbox) cudaFree(p->inbox);
   if (p->publish) cudaFree(p->publish);
   if (p->shm) munmap(p->shm, p->shm_bytes);
@@ -606,9 +610,54 @@ am_status am_peer_connect(am_ctx* ctx, am_grid* g, uint32_t nranks, uint32_t ran
   close(fd);
   if (m == MAP_FAILED) return fail(ctx, AM_EINTERNAL, "am_peer_connect: mmap failed");
   p->shm = static_cast<std::atomic<uint64_t>*>(m);
+  // the directory of every rank's published rows, for traces that read across slab edges
+  {
+    SlabDir d{};
+    d.n = nranks;
+    for (uint32_t r = 0; r < nranks; ++r) {
+      d.row0[r] = p->row0[r];
+      d.base[r] = p->p_publish[r];
+    }
+    d.row0[nranks] = g->total_h;
+    cudaError_t e = cudaMalloc(&p->zero_row, (size_t)g->g.pitch * 4);
+    if (!e) e = cudaMemset(p->zero_row, 0, (size_t)g->g.pitch * 4);
+    d.zero = p->zero_row;
+    if (!e) e = cudaMalloc(&p->dir, sizeof(SlabDir));
+    if (!e) e = cudaMemcpy(p->dir, &d, sizeof(SlabDir), cudaMemcpyHostToDevice);
+    if (e) {
+      (void)cudaGetLastError();
+      return fail(ctx, AM_ECUDA, "am_peer_connect: slab directory: %s", cudaGetErrorString(e));
+    }
+  }
   p->connected = true;
   return AM_OK;
 }
+
+namespace {
+// Every rank publishes its rows (after the peers finished reading its previous publish) and waits for
+// all the others' publishes: afterwards every rank's publish buffer holds its slab at the final layer.
+am_status peer_publish(am_ctx* ctx, am_grid* slab, PeerLink* p) {
+  const size_t rb = (size_t)slab->g.pitch * (slab->cell_bits / 8);
+  const uint64_t ia = p->n[kChA], id = p->n[kChD];
+  am_status st;
+  if (id > 0)
+    for (uint32_t r = 0; r < p->nranks; ++r)
+      if (r != p->rank && (st = peer_wait(ctx, p, r, kChD, kEvD0, id - 1))) return st;
+  CK(cudaMemcpyAsync(p->publish, static_cast<uint8_t*>(slab->val[slab->cur]) + (size_t)kK * rb,
+                     (size_t)slab->g.H * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((st = peer_signal(ctx, p, kChA, kEvA0, ia))) return st;
+  for (uint32_t r = 0; r < p->nranks; ++r)
+    if (r != p->rank && (st = peer_wait(ctx, p, r, kChA, kEvA0, ia))) return st;
+  ++p->n[kChA];
+  return AM_OK;
+}
+// this rank is done reading the peers' publish buffers
+am_status peer_release(am_ctx* ctx, PeerLink* p) {
+  am_status st = peer_signal(ctx, p, kChD, kEvD0, p->n[kChD]);
+  if (!st) ++p->n[kChD];
+  return st;
+}
+}  // namespace
 
 am_status am_peer_gather(am_ctx* ctx, am_grid* slab, am_grid* full) {
   if (!ctx || !slab || !full) return AM_EINVAL;
@@ -619,23 +668,46 @@ am_status am_peer_gather(am_ctx* ctx, am_grid* slab, am_grid* full) {
   CK(cudaSetDevice(ctx->device));
   am_status st = adopt_full(ctx, full, slab);
   if (st) return st;
+  if ((st = peer_publish(ctx, slab, p))) return st;
   const size_t rb = row_bytes(slab);
-  const uint64_t ia = p->n[kChA], id = p->n[kChD];
-  if (id > 0)  // every peer finished reading this rank's previous publish
-    for (uint32_t r = 0; r < p->nranks; ++r)
-      if (r != p->rank && (st = peer_wait(ctx, p, r, kChD, kEvD0, id - 1))) return st;
-  CK(cudaMemcpyAsync(p->publish, alloc_rows(slab, kK), (size_t)slab->g.H * rb, cudaMemcpyDeviceToDevice, ctx->stream));
-  if ((st = peer_signal(ctx, p, kChA, kEvA0, ia))) return st;
-  for (uint32_t r = 0; r < p->nranks; ++r)
-    if (r != p->rank && (st = peer_wait(ctx, p, r, kChA, kEvA0, ia))) return st;
   for (uint32_t r = 0; r < p->nranks; ++r)  // peer-to-peer copies of every slab into the full field
     CK(cudaMemcpyAsync(static_cast<uint8_t*>(full->val[0]) + (size_t)(kK + p->row0[r]) * rb, p->p_publish[r],
                        (size_t)p->rows[r] * rb, cudaMemcpyDeviceToDevice, ctx->stream));
-  if ((st = peer_signal(ctx, p, kChD, kEvD0, id))) return st;
-  ++p->n[kChA];
-  ++p->n[kChD];
+  if ((st = peer_release(ctx, p))) return st;
   CK(cudaStreamSynchronize(ctx->stream));
   return AM_OK;
+}
+
+am_status am_peer_trace_paths_device(am_ctx* ctx, am_grid* slab, const uint32_t* d_tgt, uint64_t n, uint32_t method,
+                                     uint64_t seed, uint64_t* d_offsets, uint32_t* d_pts, uint64_t cap,
+                                     int32_t* d_status) {
+  if (!ctx || !slab || !d_offsets || (n && (!d_tgt || !d_status))) return AM_EINVAL;
+  PeerLink* p = slab->peer;
+  if (!p || !p->connected) return fail(ctx, AM_EINVAL, "am_peer_trace_paths_device: slab not connected");
+  if (!slab->have_map || slab->plain_active) return fail(ctx, AM_EINVAL, "no propagated map");
+  if (method > 1) return fail(ctx, AM_EINVAL, "bad method");
+  if (!d_pts && cap) return fail(ctx, AM_EINVAL, "null point buffer");
+  CK(cudaSetDevice(ctx->device));
+  am_status st = peer_publish(ctx, slab, p);
+  if (st) return st;
+  MapView m{};
+  m.g = slab->g;
+  m.g.H = slab->total_h;                // grid coordinates of the whole map
+  m.g.rows = slab->total_h + 2 * m.g.pad;
+  m.val = nullptr;
+  m.dir = p->dir;
+  m.cell_bits = slab->cell_bits;
+  m.layers = slab->computed;  // point counts are rollback invariant (the same on every rank)
+  if (n) {
+    if ((st = trace_scratch(ctx, slab, n))) return st;
+    launch_path_counts(m, d_tgt, n, (int)method, seed, slab->d_counts, d_status, ctx->stream);
+    CKL();
+    launch_scan(slab->d_counts, n, d_offsets, ctx->stream);
+    CKL();
+    launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, ctx->stream, cap);
+    CKL();
+  }
+  return peer_release(ctx, p);
 }
 
 am_status am_comm_unique_id(uint8_t* id_out) {

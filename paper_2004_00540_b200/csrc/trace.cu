@@ -17,34 +17,39 @@ enum : int32_t { ST_OK = 0, ST_EINVAL = 1, ST_EUNCOVERED = 2, ST_EINTERNAL = 6 }
 
 struct Reader {
   MapView m;
+  // raw encoded cell at grid (r, c); (r, c) may lie up to the padding width outside the grid
+  __device__ __forceinline__ uint32_t raw(int r, int c) const {
+    const int ac = c + (int)m.g.pad;
+    if (m.cell_bits == 16) return m.row<uint16_t>(r + (int)m.g.pad)[ac];
+    return m.row<uint32_t>(r + (int)m.g.pad)[ac];
+  }
   __device__ __forceinline__ uint32_t value(uint32_t r, uint32_t c) const {
     if (m.cell_bits == 16) {
-      const uint32_t v = static_cast<const uint16_t*>(m.val)[m.g.idx(r, c)];
+      const uint32_t v = raw((int)r, (int)c);
       return (v & kFlag16) ? (v & 0x7FFFu) : 0u;
     }
     if (m.cell_bits == 32) {
-      const uint32_t v = static_cast<const uint32_t*>(m.val)[m.g.idx(r, c)];
+      const uint32_t v = raw((int)r, (int)c);
       return (v & kFlag32) ? (v & kLow32) : 0u;
     }
     return static_cast<const uint32_t*>(m.val)[(size_t)r * m.g.W + c];
   }
   // encoded fields only: (r, c) may lie up to the padding width outside the grid
   __device__ __forceinline__ uint32_t value_pad(int r, int c) const {
-    const size_t i = (size_t)(r + (int)m.g.pad) * m.g.pitch + (size_t)(c + (int)m.g.pad);
-    if (m.cell_bits == 16) {
-      const uint32_t v = static_cast<const uint16_t*>(m.val)[i];
-      return (v & kFlag16) ? (v & 0x7FFFu) : 0u;
-    }
-    const uint32_t v = static_cast<const uint32_t*>(m.val)[i];
+    const uint32_t v = raw(r, c);
+    if (m.cell_bits == 16) return (v & kFlag16) ? (v & 0x7FFFu) : 0u;
     return (v & kFlag32) ? (v & kLow32) : 0u;
   }
   __device__ __forceinline__ bool source(uint32_t r, uint32_t c) const {
+    // a distributed map has no source mask here: on a propagated (law-abiding) map the sources are
+    // exactly the cells at L+1
+    if (m.dir) return value(r, c) == m.layers + 1;
     if (m.cell_bits) return m.srcmask[m.g.idx(r, c)] != 0;
     return m.srcmask[(size_t)r * m.g.W + c] != 0;
   }
   __device__ __forceinline__ bool obstacle(uint32_t r, uint32_t c) const {
-    if (m.cell_bits == 16) return !(static_cast<const uint16_t*>(m.val)[m.g.idx(r, c)] & kFlag16);
-    if (m.cell_bits == 32) return !(static_cast<const uint32_t*>(m.val)[m.g.idx(r, c)] & kFlag32);
+    if (m.cell_bits == 16) return !(raw((int)r, (int)c) & kFlag16);
+    if (m.cell_bits == 32) return !(raw((int)r, (int)c) & kFlag32);
     return m.occ[(size_t)r * m.g.W + c] != 0;
   }
 };
@@ -177,7 +182,6 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
   const MapView& m = rd.m;
   const int pad = (int)m.g.pad, pitch = (int)m.g.pitch;
   const int rmax = (int)m.g.rows - pad - WR;  // window origin limits (grid coordinates)
-  const T* field = static_cast<const T*>(m.val);
   const uint32_t flag = sizeof(T) == 2 ? kFlag16 : kFlag32;
   const uint32_t top = flag | (m.layers + 1);  // raw value of a source
   uint64_t rng = seed;
@@ -196,7 +200,7 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
 #pragma unroll
     for (int h = 0; h < WR / 32; ++h) {
       const int row = lane + 32 * h;
-      const uint4* p = reinterpret_cast<const uint4*>(field + (size_t)(wr + row + pad) * pitch + ac);
+      const uint4* p = reinterpret_cast<const uint4*>(m.row<T>(wr + row + pad) + ac);
       uint4* o = reinterpret_cast<uint4*>(win + row * WC);
 #pragma unroll
       for (int q = 0; q < WC / kVec; ++q) o[q] = p[q];
@@ -204,7 +208,7 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
     __syncwarp();
     loaded = true;
   };
-  uint32_t cur = field[rd.m.g.idx(r, c)];
+  uint32_t cur = m.row<T>((int)r + pad)[(int)c + pad];
   uint64_t n = 0;
   uint32_t keep_r = 0, keep_c = 0;  // point n of this lane's slot (n % 32 == lane)
   auto record = [&]() {
@@ -308,7 +312,6 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
   const MapView& m = rd.m;
   const int pad = (int)m.g.pad, pitch = (int)m.g.pitch;
   const int rmax = (int)m.g.rows - pad - WR;
-  const T* field = static_cast<const T*>(m.val);
   const uint32_t flag = sizeof(T) == 2 ? kFlag16 : kFlag32;
   const uint32_t top = flag | (m.layers + 1);  // raw value of a source
   const int dr = lane / 5 - 2, dc = lane % 5 - 2;  // this lane's cell of the 5x5 (lanes < 25)
@@ -322,7 +325,7 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
 #pragma unroll
     for (int h = 0; h < WR / 32; ++h) {
       const int row = lane + 32 * h;
-      const uint4* p = reinterpret_cast<const uint4*>(field + (size_t)(wr + row + pad) * pitch + ac);
+      const uint4* p = reinterpret_cast<const uint4*>(m.row<T>(wr + row + pad) + ac);
       uint4* o = reinterpret_cast<uint4*>(win + row * WC);
 #pragma unroll
       for (int q = 0; q < WC / kVec; ++q) o[q] = p[q];
@@ -330,7 +333,7 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
     __syncwarp();
     loaded = true;
   };
-  uint32_t cur = field[m.g.idx(r, c)];
+  uint32_t cur = m.row<T>((int)r + pad)[(int)c + pad];
   uint64_t n = 0;
   uint32_t keep_r = 0, keep_c = 0;
   auto record = [&]() {

@@ -71,5 +71,17 @@ def test_peer_slabs_match_oracle(tmp_path, n, gen, w, h, dens, ns, layers, cap):
             got = r["results"][rep]
             assert (got["layers_used"], got["cause"]) == want, (r["rank"], rep, got, want)
         assert np.array_equal(np.load(os.path.join(tmp_path, f"map_{rep}.npy")), ref), rep
+        # paths traced on the distributed map (peer reads across slab edges) against the oracle's
+        L = ranks[0]["results"][rep]["layers_used"]
+        checked = 0
+        for r in range(n):
+            z = np.load(os.path.join(tmp_path, f"paths_{r}_{rep}.npz"))
+            for k, t in enumerate(z["tgt"]):
+                ost, opts = O.reconstruct_euclidean(occ, sm, ref, t, cap=L + 2)
+                assert int(z["st"][k]) == ost, (r, rep, tuple(t))
+                if ost == 0:
+                    assert np.array_equal(z["pts"][z["off"][k]:z["off"][k + 1]], opts), (r, rep, tuple(t))
+                    checked += 1
+        assert checked > 0
     if gen == "comb":
         assert ranks[0]["results"][0]["cell_bits"] == 32

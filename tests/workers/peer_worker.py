@@ -50,6 +50,17 @@ def main():
     dist.all_gather_object(blobs, am.peer_export(slab))
     am.peer_connect(slab, world, rank, blobs)
     full = am.Grid(occ, src, ctx)
+    # targets: every free cell on a sparse lattice (grid coordinates); this rank traces targets[rank::world]
+    # on the distributed map (peer reads across slab edges), without gathering it
+    import torch
+
+    lat = np.argwhere(occ[::7, ::5] == 0) * np.array([7, 5])
+    tgt = lat.astype(np.uint32)[rank::world]
+    nt = len(tgt)
+    dev = torch.device("cuda:0")
+    d_tgt = torch.from_numpy(tgt.astype(np.int32).reshape(-1)).to(dev) if nt else torch.zeros(2, dtype=torch.int32, device=dev)
+    d_off = torch.zeros(nt + 1, dtype=torch.int64, device=dev)
+    d_st = torch.zeros(max(nt, 1), dtype=torch.int32, device=dev)
     res = []
     for rep in range(a.reps):
         r = slab.propagate(a.layers) if a.layers else slab.propagate_auto(a.cap)
@@ -58,6 +69,15 @@ def main():
                     "blocks": r.block_launches, "tiles": r.tiles_processed})
         if rank == 0:
             np.save(os.path.join(a.out, f"map_{rep}.npy"), full.activity())
+        cap = max(nt, 1) * (r.layers_computed + 2)
+        d_pts = torch.zeros(2 * cap, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        am.peer_trace_device(slab, d_tgt.data_ptr(), nt, am.EUCLIDEAN, 0, d_off.data_ptr(), d_pts.data_ptr(), cap,
+                             d_st.data_ptr())
+        ctx.synchronize()
+        off = d_off.cpu().numpy().astype(np.int64)
+        np.savez(os.path.join(a.out, f"paths_{rank}_{rep}.npz"), tgt=tgt, off=off, st=d_st.cpu().numpy()[:nt],
+                 pts=d_pts.cpu().numpy().view(np.uint32)[: 2 * int(off[-1])].reshape(-1, 2))
     with open(os.path.join(a.out, f"rank{rank}.json"), "w") as f:
         json.dump({"rank": rank, "rows": [r0, r1], "results": res}, f)
     dist.barrier()
