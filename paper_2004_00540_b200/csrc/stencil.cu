@@ -412,6 +412,9 @@ __device__ __forceinline__ uint32_t tma_stage(const TmaStage& ts, uint32_t homes
 #ifndef AM_STAGES
 #define AM_STAGES 4
 #endif
+#ifndef AM_ST128
+#define AM_ST128 0  // 1: tile outputs as 16 B stores (lane pairs swap halves)
+#endif
 #ifndef AM_TILE_STAGES
 #define AM_TILE_STAGES 4
 #endif
@@ -692,10 +695,26 @@ __device__ __forceinline__ void tile_phase(const uint8_t* buf, int s0, int s1, u
     x[3] = __byte_perm(a.y, b.y, 0x7632);
   };
   auto emit = [&](const uint32_t (&x)[4]) {
+#if AM_ST128
+    // 16 B stores: lane pairs swap halves, the even lane writes both lanes' 8 cells of row A, the odd lane
+    // both lanes' cells of row B (halo pairs 0-1 / 30-31 store nothing: `st` is uniform per pair)
+    {
+      const uint32_t a0 = __byte_perm(x[0], x[1], 0x5410), a1 = __byte_perm(x[2], x[3], 0x5410);
+      const uint32_t b0 = __byte_perm(x[0], x[1], 0x7632), b1 = __byte_perm(x[2], x[3], 0x7632);
+      const bool odd = threadIdx.x & 1;
+      const uint32_t r0 = __shfl_xor_sync(0xffffffffu, odd ? a0 : b0, 1);
+      const uint32_t r1 = __shfl_xor_sync(0xffffffffu, odd ? a1 : b1, 1);
+      if (st) {
+        if (!odd) *reinterpret_cast<uint4*>(oA) = make_uint4(a0, a1, r0, r1);
+        else *reinterpret_cast<uint4*>(oB - 4) = make_uint4(r0, r1, b0, b1);
+      }
+    }
+#else
     if (st) {
       *reinterpret_cast<uint2*>(oA) = make_uint2(__byte_perm(x[0], x[1], 0x5410), __byte_perm(x[2], x[3], 0x5410));
       *reinterpret_cast<uint2*>(oB) = make_uint2(__byte_perm(x[0], x[1], 0x7632), __byte_perm(x[2], x[3], 0x7632));
     }
+#endif
     oA += pitch;
     oB += pitch;
     uint32_t rm = 0xFFFFFFFFu;
