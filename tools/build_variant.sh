@@ -18,6 +18,6 @@ for f in actmap_api report; do
   g++ -std=c++20 -O2 -fPIC -I$ROOT/include -c $SRC/$f.cpp -o $OUT/$f.o & pids+=($!)
 done
 for p in "${pids[@]}"; do wait $p; done
-$NVCC $ARCH -shared -cudart static -o $ROOT/build_ab/$NAME.so $OUT/*.o -ldl
+$NVCC $ARCH -shared -cudart static -o $ROOT/build_ab/$NAME.so $OUT/*.o -ldl -lpthread
 rm -rf "$OUT"
 echo "built build_ab/$NAME.so"
