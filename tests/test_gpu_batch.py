@@ -110,3 +110,34 @@ def test_batch_rejects_bad_input():
     occ[1, 0, 0] = 1
     with pytest.raises(am.InvalidInputError):
         am.Batch(occ, [[[1, 1]], [[0, 0]]])
+
+
+@pytest.mark.parametrize("n,w,h,dens", [
+    (7, 1000, 30, 0.3),   # 32 words per row: one warp per row group, 4 rows per thread
+    (5, 20, 1000, 0.3),   # one word per row: 256 row groups, 4 rows per thread
+    (3, 33, 257, 0.25),   # ragged words (33 columns) and rows
+    (9, 256, 256, 0.0),   # empty mazes: filled at floor-ish eccentricity
+    (4, 4, 4, 0.0),       # tiny mazes: 4 x 4
+])
+def test_batch_wave_shapes(n, w, h, dens):
+    """K5 (k_batch_wave) across maze shapes: word columns 1..32, rows per thread 1..32, ragged edges."""
+    occ = np.stack([O.random_maze(w, h, dens, 300 + i) for i in range(n)])
+    src = [O.sample_free_cells(occ[i], 1 + i % 2, 300 + i) for i in range(n)]
+    b = am.Batch(occ, src)
+    cap = 4 * max(w, h) + 8
+    check(b, occ, src, cap, range(n))
+    lu, cause, _ = b.propagate(layers=max(1, min(w, h) // 2))
+    maps = b.activity()
+    for i in range(n):
+        sm = O.source_mask(occ[i], src[i])
+        assert np.array_equal(maps[i], O.propagate(occ[i], sm, int(lu[i]))), i
+    b.close()
+
+
+def test_batch_large_cap_takes_the_tile_path():
+    """A cap past the 16-bit range falls back to the packed tile path (same results)."""
+    occ = np.stack([O.random_maze(40, 30, 0.3, 900 + i) for i in range(6)])
+    src = [O.sample_free_cells(occ[i], 1, 900 + i) for i in range(6)]
+    b = am.Batch(occ, src)
+    check(b, occ, src, 40000, range(6), method_seed=((am.EUCLIDEAN, 0),))
+    b.close()
