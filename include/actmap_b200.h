@@ -103,7 +103,10 @@ am_status am_grid_create_device(am_ctx *ctx, uint32_t width, uint32_t height, co
                                 const uint32_t *d_src_rc, uint64_t n_src, am_grid **out);
 am_status am_grid_destroy(am_ctx *ctx, am_grid *grid);
 /* A new grid with the same occupancy and SourceSet, built on the device from
- * `grid`'s resident copies (no host data; `grid` may be destroyed after). */
+ * `grid`'s resident copies (no host data; `grid` may be destroyed after).
+ * New surface: it keeps the value semantics of maps a planner returned
+ * (ActivityMap is returned by value, activity.hpp:17-18) without holding
+ * on to the caller's GridMap. */
 am_status am_grid_clone(am_ctx *ctx, const am_grid *grid, am_grid **out);
 am_status am_grid_get_info(const am_grid *grid, am_grid_info *out);
 
@@ -181,7 +184,9 @@ am_status am_comm_init(am_ctx *ctx, uint32_t nranks, uint32_t rank, const uint8_
 am_status am_comm_slab_rows(const am_ctx *ctx, uint32_t height, uint32_t *row0, uint32_t *row1);
 am_status am_comm_gather(am_ctx *ctx, am_grid *slab, am_grid *full);
 /* rows [row0, row1) of slab `rank` of `nranks` over `height` rows (the cut
- * am_comm_slab_rows uses; no communicator needed). */
+ * am_comm_slab_rows uses; no communicator needed).  New surface (SURVEY.md
+ * §8e): the reference's only parallelism is the `threads` knob of
+ * propagate (propagate.hpp:30-31), with results invariant in it. */
 am_status am_slab_rows(uint32_t height, uint32_t nranks, uint32_t rank, uint32_t *row0, uint32_t *row1);
 
 /* ---- peer-memory slab transport (no NCCL call on the per-block path) -----
