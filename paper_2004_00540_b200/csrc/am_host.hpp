@@ -18,6 +18,12 @@ constexpr int kLag = 2;        // blocks in flight before the host reads a fixed
 constexpr int kLagTiles = AM_LAG_TILES;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
 struct PeerLink;         // peer-memory slab transport state (multigpu.cu)
+// bit-plane propagation state of a single grid (bits.cu), allocated on first use
+struct BitState {
+  BitGeo bg{};
+  BitBook bk{};
+  int ctas = 0;
+};
 void peer_destroy(PeerLink* p);
 // Host side of a grid's fixed-point slots: pinned device-mapped mirror + one
 // event per slot.  Pinning and event creation are slow, so contexts recycle
@@ -81,6 +87,7 @@ struct am_grid {
   void* t_bnd = nullptr;                     // slabs: first / last kK rows gathered for the neighbours (2 x kK x pitch)
   uint8_t* t_src = nullptr;                  // per tile: a source in its staged rows (TileBook::tsrc)
   am::PeerLink* peer = nullptr;              // slabs: peer-memory transport (am_peer_connect)
+  am::BitState* bits = nullptr;              // bit-plane propagation (single grids, 16-bit runs)
   am::TileBook book() const {
     return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed, t_src};
   }

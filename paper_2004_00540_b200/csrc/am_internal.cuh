@@ -182,6 +182,47 @@ void launch_sentinel_layer(uint32_t W, uint32_t H, const uint8_t* occ, const uin
 void launch_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* d_src_rc, uint64_t n, uint8_t* d_srcmask,
                           const uint8_t* d_occ, int* d_err, cudaStream_t s);
 
+// ---- bit-plane propagation (bits.cu) ----
+// Tiles of kBTR rows x kBTW words (32 cells each); a warp holds a tile plus a
+// kBK-deep halo (32*kBRPL rows, kBTW+2 words) and runs kBK layers per launch.
+#ifndef AM_BK
+#define AM_BK 16
+#endif
+#ifndef AM_BRPL
+#define AM_BRPL 2
+#endif
+constexpr int kBK = AM_BK;
+constexpr int kBRPL = AM_BRPL;
+constexpr int kBTW = 4;
+constexpr int kBTR = 32 * kBRPL - 2 * kBK;
+struct BitGeo {
+  uint32_t W, H;
+  uint32_t nchunks, tbands;  // tile rows / tile columns
+  uint32_t wpr;              // plane words per row (tbands * kBTW)
+  uint32_t rows;             // plane rows (nchunks * kBTR)
+  __host__ __device__ uint32_t ntiles() const { return nchunks * tbands; }
+  __host__ __device__ size_t plane_words() const { return (size_t)rows * wpr; }
+};
+BitGeo make_bit_geo(uint32_t W, uint32_t H);
+// Device state of a bit-plane run.  State words and lists work as in TileBook
+// (state = old << 32 | cur, cur = (index + 1 of the block that last processed the
+// tile) << 1 | home plane; lists / counts by block parity / block mod 3).
+struct BitBook {
+  uint32_t* F;                 // free cells
+  uint32_t* C;                 // two coverage planes (C, C + plane_words)
+  unsigned long long* state;
+  uint32_t* sched;
+  uint32_t* list[2];
+  uint32_t* count;             // [6]
+  unsigned long long* stat;    // [0] tiles processed, [1] cells covered, [2] free cells
+};
+int bits_ctas_per_sm();
+void launch_bits_init(const BitGeo& bg, const Geo& g, const uint8_t* occ, BitBook bk, uint16_t* field, cudaStream_t s);
+void launch_bits_sources(const BitGeo& bg, const Geo& g, const uint32_t* rc, uint64_t n, BitBook bk, uint16_t* field,
+                         uint32_t lref, cudaStream_t s);
+void launch_bits_tiles(const BitGeo& bg, const Geo& g, int ctas, uint16_t* field, BitBook bk, uint32_t blk,
+                       uint32_t l0, uint32_t nl, uint32_t lref, FlagSink flag, FlagSink prev, cudaStream_t s);
+
 // ---- path extraction (trace.cu) ----
 // A map distributed over row slabs (peer transport): grid row r lives in slab s with row0[s] <= r <
 // row0[s+1], at base[s] + (r - row0[s]) * pitch cells (base: the slabs' published rows, peer-mapped);

@@ -168,6 +168,17 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->t_bnd);
   am::dfree(ctx, g->t_processed);
   am::dfree(ctx, g->t_src);
+  if (g->bits) {
+    am::dfree(ctx, g->bits->bk.F);
+    am::dfree(ctx, g->bits->bk.C);
+    am::dfree(ctx, g->bits->bk.state);
+    am::dfree(ctx, g->bits->bk.sched);
+    am::dfree(ctx, g->bits->bk.list[0]);
+    am::dfree(ctx, g->bits->bk.list[1]);
+    am::dfree(ctx, g->bits->bk.count);
+    am::dfree(ctx, g->bits->bk.stat);
+    delete g->bits;
+  }
   am::peer_destroy(g->peer);
   delete g;
 }
@@ -405,6 +416,161 @@ static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
   return AM_OK;
 }
 
+// Bit-plane propagation of a single grid (bits.cu).  The field is
+// written once per cell, relative to lref = min(target, 32766) layers, so the map
+// needs no decode: computed = lref, layers_used = the outcome, rollback = lref - used.
+// Auto runs that have not reached their fixed point by lref (beyond the 16-bit
+// range) return handoff = true with the field exactly at layer lref; the caller
+// continues there with the 16/32-bit tile kernels.
+constexpr uint32_t kBitsMaxRef = 32766u;
+
+static am_status bits_alloc(am_ctx* ctx, am_grid* g) {
+  if (g->bits) return AM_OK;
+  auto* b = new (std::nothrow) BitState();
+  if (!b) return fail(ctx, AM_EOOM, "bit state");
+  g->bits = b;
+  b->bg = make_bit_geo(g->g.W, g->g.H);
+  const size_t pw = b->bg.plane_words(), nt = b->bg.ntiles();
+  BitBook& k = b->bk;
+  CK(am::dmalloc(ctx, &k.F, pw * 4));
+  CK(am::dmalloc(ctx, &k.C, 2 * pw * 4));
+  CK(am::dmalloc(ctx, &k.state, nt * 8));
+  CK(am::dmalloc(ctx, &k.sched, nt * 4));
+  CK(am::dmalloc(ctx, &k.list[0], nt * 4));
+  CK(am::dmalloc(ctx, &k.list[1], nt * 4));
+  CK(am::dmalloc(ctx, &k.count, 6 * 4));
+  CK(am::dmalloc(ctx, &k.stat, 3 * 8));
+  b->ctas = ctx->sms * bits_ctas_per_sm();
+  return AM_OK;
+}
+
+static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom, am_prop_result* res,
+                            bool* handoff) {
+  *handoff = false;
+  am_status st = bits_alloc(ctx, g);
+  if (st) return st;
+  if ((st = set_cell_bits(ctx, g, 16))) return st;
+  BitState& B = *g->bits;
+  const BitGeo& bg = B.bg;
+  const size_t pw = bg.plane_words(), nt = bg.ntiles();
+  cudaStream_t s = ctx->stream;
+  const uint32_t lref = std::min(target, kBitsMaxRef);
+  uint16_t* field = static_cast<uint16_t*>(g->val[0]);
+  CK(cudaMemsetAsync(B.bk.C, 0, pw * 4, s));  // plane 0: every tile's home at layer 0
+  CK(cudaMemsetAsync(B.bk.state, 0, nt * 8, s));
+  CK(cudaMemsetAsync(B.bk.sched, 0, nt * 4, s));
+  CK(cudaMemsetAsync(B.bk.count, 0, 6 * 4, s));
+  CK(cudaMemsetAsync(B.bk.stat, 0, 3 * 8, s));
+  launch_bits_init(bg, g->g, g->occ, B.bk, field, s);
+  CKL();
+  launch_bits_sources(bg, g->g, g->src_rc, g->n_src, B.bk, field, lref, s);
+  CKL();
+  ctx->launches += 2;
+  g->cur = 0;
+  g->plain_active = 0;
+  g->have_map = 1;
+
+  am_prop_result r{};
+  const bool timing = (ctx->flags & AM_CTX_TIMING) != 0;
+  if (timing) {
+    while (ctx->timers.size() < 1) {
+      am_ctx::Timer t;
+      CK(cudaEventCreate(&t.a));
+      CK(cudaEventCreate(&t.b));
+      ctx->timers.push_back(t);
+    }
+    CK(cudaEventRecord(ctx->timers[0].a, s));
+  }
+  if (autom) CK(cudaMemsetAsync(g->d_flags, 0xFF, kFlagSlots * sizeof(uint32_t), s));
+  std::deque<PendingBlock> pend;
+  FlagSink unpublished{nullptr, nullptr, nullptr};
+  uint32_t l = 0, lprime = 0, blk = 0;
+  auto drain_one = [&]() -> am_status {
+    const PendingBlock b = pend.front();
+    pend.pop_front();
+    volatile uint32_t* h = g->fs->h + b.slot;
+    for (uint64_t spin = 1; *h == kSlotPending; ++spin) {
+      if ((spin & 4095) == 0) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess && *h == kSlotPending) return fail(ctx, AM_ECUDA, "flag slot never written");
+        if (q != cudaSuccess && q != cudaErrorNotReady) return fail(ctx, AM_ECUDA, "bits: %s", cudaGetErrorString(q));
+      }
+    }
+    if (!lprime) {
+      const uint32_t t = block_termination(b, *h);
+      if (t) lprime = t;
+    }
+    return AM_OK;
+  };
+  while (l < lref && !lprime) {
+    const uint32_t nl = std::min<uint32_t>(kBK, lref - l);
+    const int slot = (int)(blk % kFlagSlots);
+    FlagSink sink{g->d_flags + slot, g->d_flags + kFlagSlots, nullptr};
+    const FlagSink prev = unpublished;
+    if (autom) {
+      g->fs->h[slot] = kSlotPending;  // consumed kFlagSlots blocks ago (lag < kFlagSlots)
+      unpublished = FlagSink{sink.word, sink.done, g->fs->hdev + slot};  // published by the next launch
+    }
+    launch_bits_tiles(bg, g->g, B.ctas, field, B.bk, blk, l, nl, lref, sink, prev, s);
+    ++ctx->launches;
+    if (cudaError_t e = cudaPeekAtLastError()) return fail(ctx, AM_ECUDA, "k_bits_tiles: %s", cudaGetErrorString(e));
+    ++r.block_launches;
+    if (autom) pend.push_back(PendingBlock{slot, l, nl, 16, true});
+    l += nl;
+    ++blk;
+    while ((int)pend.size() > kLagTiles)
+      if ((st = drain_one())) return st;
+  }
+  if (unpublished.host) {
+    launch_publish_flag(unpublished, s);
+    CKL();
+  }
+  if (timing) CK(cudaEventRecord(ctx->timers[0].b, s));
+  while (!pend.empty())
+    if ((st = drain_one())) return st;
+  unsigned long long stat[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(stat, B.bk.stat, sizeof stat, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const bool any_zero = stat[1] < stat[2];
+  uint32_t used = l, cause = AM_STOP_FIXED;
+  if (autom) {
+    if (lprime) {
+      used = any_zero ? lprime : (lprime > 1 ? lprime - 1 : 1);
+      cause = any_zero ? AM_STOP_STALLED : AM_STOP_FILLED;
+    } else if (l == target) {
+      used = target;
+      cause = any_zero ? AM_STOP_CAP : AM_STOP_FILLED;
+    } else {
+      *handoff = true;  // field at layer lref, beyond the 16-bit range: continue with the tile kernels
+    }
+  }
+  g->computed = lref;
+  g->layers_used = *handoff ? lref : used;
+  if (timing) {
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, ctx->timers[0].a, ctx->timers[0].b));
+    r.stencil_ms = f;
+  }
+  r.layers_used = used;
+  r.cause = cause;
+  r.layers_computed = l;
+  r.cell_bits = 16;
+  r.tiles_processed = stat[0];
+  r.tiles_total = (uint64_t)nt * r.block_launches;
+  if (res) *res = r;
+  return AM_OK;
+}
+
+// bit-plane runs: a single grid, batched mode, 16-bit cells, not forced dense (AM_BITS=0 disables)
+static bool bits_eligible(std::vector<SlabRef>& slabs, Transport* tr, uint32_t mode, int start_bits) {
+  static const bool off = [] {
+    const char* e = getenv("AM_BITS");
+    return e && e[0] == '0';
+  }();
+  return !off && slabs.size() == 1 && !tr && !slabs[0].g->slab && mode == AM_MODE_BATCHED && start_bits == 16 &&
+         !(slabs[0].ctx->flags & AM_CTX_DENSE);
+}
+
 am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t layers, uint32_t auto_cap,
                             uint32_t mode, am_prop_result* res) {
   am_ctx* ctx = slabs[0].ctx;
@@ -417,8 +583,20 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   // 16-bit cells unless the run can never fit (fixed L beyond the 16-bit range)
   const int start_bits = (!autom && (uint64_t)target + 1 > kMax16Activity) ? 32 : 16;
   am_status st;
-  for (auto& s : slabs)
-    if ((st = reset_map(s.ctx, s.g, start_bits))) return st;
+  uint32_t l_init = 0;  // layer the field holds when the loop below starts
+  am_prop_result pre{};
+  if (bits_eligible(slabs, tr, mode, start_bits)) {
+    bool handoff = false;
+    if ((st = drive_bits(ctx, slabs[0].g, target, autom, &pre, &handoff))) return st;
+    if (!handoff) {
+      if (res) *res = pre;
+      return AM_OK;
+    }
+    l_init = slabs[0].g->computed;
+  } else {
+    for (auto& s : slabs)
+      if ((st = reset_map(s.ctx, s.g, start_bits))) return st;
+  }
 
   // exact active-tile skipping in batched mode.  Row slabs
   // must meet at tile-chunk boundaries, so their halo rows lie outside every
@@ -468,7 +646,10 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
       CK(cudaMemsetAsync(g->t_sched, 0, n * 4, c->stream));
       CK(cudaMemsetAsync(g->t_processed, 0, 8, c->stream));
       CK(cudaMemsetAsync(g->t_count, 0, 6 * 4, c->stream));
-      launch_tiles_init(g->g, g->srcmask, g->book(), c->stream);
+      if (l_init)  // handed over by the bit-plane run: every tile at l_init in val[0], all listed
+        launch_tiles_all(g->g, g->book(), 0, l_init, 0, c->stream);
+      else
+        launch_tiles_init(g->g, g->srcmask, g->book(), c->stream);
       CKL();
     }
   }
@@ -504,7 +685,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
     }
     return AM_OK;
   };
-  uint32_t l = 0;       // layers applied so far
+  uint32_t l = l_init;  // layers applied so far
   uint32_t lprime = 0;  // first layer without new cells (0 = not found)
   uint64_t nblock = 0;
   const int K = kK;
@@ -761,6 +942,8 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   r.cause = cause;
   r.layers_computed = l;
   r.cell_bits = slabs[0].g->cell_bits;
+  r.block_launches += pre.block_launches;
+  r.tiles_processed += pre.tiles_processed;
   if (res) *res = r;
   return AM_OK;
 }
