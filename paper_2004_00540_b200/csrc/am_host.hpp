@@ -23,6 +23,7 @@ struct BitState {
   BitGeo bg{};
   BitBook bk{};
   int ctas = 0;
+  uint32_t* own_t = nullptr;  // time planes when the second field is too small for them
 };
 void peer_destroy(PeerLink* p);
 // Host side of a grid's fixed-point slots: pinned device-mapped mirror + one

@@ -208,8 +208,8 @@ BitGeo make_bit_geo(uint32_t W, uint32_t H);
 // (state = old << 32 | cur, cur = (index + 1 of the block that last processed the
 // tile) << 1 | home plane; lists / counts by block parity / block mod 3).
 struct BitBook {
-  uint32_t* F;                 // free cells
-  uint32_t* C;                 // two coverage planes (C, C + plane_words)
+  uint4* P;                    // plane words {covered (home 0), covered (home 1), free, -}
+  uint32_t* T;                 // time planes: 16 words per plane word (bit k of t - 1 of its 32 cells)
   unsigned long long* state;
   uint32_t* sched;
   uint32_t* list[2];
@@ -217,11 +217,13 @@ struct BitBook {
   unsigned long long* stat;    // [0] tiles processed, [1] cells covered, [2] free cells
 };
 int bits_ctas_per_sm();
-void launch_bits_init(const BitGeo& bg, const Geo& g, const uint8_t* occ, BitBook bk, uint16_t* field, cudaStream_t s);
-void launch_bits_sources(const BitGeo& bg, const Geo& g, const uint32_t* rc, uint64_t n, BitBook bk, uint16_t* field,
-                         uint32_t lref, cudaStream_t s);
-void launch_bits_tiles(const BitGeo& bg, const Geo& g, int ctas, uint16_t* field, BitBook bk, uint32_t blk,
-                       uint32_t l0, uint32_t nl, uint32_t lref, FlagSink flag, FlagSink prev, cudaStream_t s);
+void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStream_t s);
+void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBook bk, cudaStream_t s);
+void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uint32_t nl, FlagSink flag,
+                       FlagSink prev, cudaStream_t s);
+// the encoded 16-bit field (values relative to lref layers) from the planes
+void launch_bits_finalize(const BitGeo& bg, const Geo& g, BitBook bk, uint32_t lref, uint16_t* field, int sms,
+                          cudaStream_t s);
 
 // ---- path extraction (trace.cu) ----
 // A map distributed over row slabs (peer transport): grid row r lives in slab s with row0[s] <= r <

@@ -44,38 +44,58 @@ constexpr int kBNW = kBTW + 2;   // words per region row (one halo word each sid
 constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-block layer index
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
-static_assert(kBK % kBRPL == 0 || kBRPL == 1, "halo rows fill whole lanes");
 constexpr int kBThreads = 128;
 
 __constant__ uint8_t kBFacing[3][3] = {{8, 2, 7}, {4, 0, 3}, {6, 1, 5}};
 
-__device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
 
-// Lists tile (c, b) for block blk + 1 unless already listed (warp-aggregated).
-__device__ __forceinline__ void bit_push(const BitGeo& bg, const BitBook& bk, uint32_t blk, bool want, int c, int b) {
-  const bool in = want && c >= 0 && b >= 0 && c < (int)bg.nchunks && b < (int)bg.tbands;
-  bool add = false;
-  if (in) add = atomicMax(&bk.sched[(uint32_t)c * bg.tbands + (uint32_t)b], blk + 2) < blk + 2;
+// Lists tile (c, b) for block blk + 1 unless already listed (warp-aggregated), in two halves so the
+// dedup atomic's round trip overlaps other work: bit_push_begin issues it, bit_push_end appends.
+struct PushTicket {
+  uint32_t old;  // previous sched value (lanes with a candidate)
+  int c, b;
+  bool in;
+};
+__device__ __forceinline__ PushTicket bit_push_begin(const BitGeo& bg, const BitBook& bk, uint32_t blk, bool want,
+                                                     int c, int b) {
+  PushTicket t{0xFFFFFFFFu, c, b, want && c >= 0 && b >= 0 && c < (int)bg.nchunks && b < (int)bg.tbands};
+  if (t.in) t.old = atomicMax(&bk.sched[(uint32_t)c * bg.tbands + (uint32_t)b], blk + 2);
+  return t;
+}
+__device__ __forceinline__ void bit_push_end(const BitBook& bk, uint32_t blk, const PushTicket& t) {
+  const bool add = t.in && t.old < blk + 2;
   const uint32_t m = __ballot_sync(0xffffffffu, add);
   if (!m) return;
   const int lane = threadIdx.x & 31;
   uint32_t base = 0;
   if (lane == __ffs(m) - 1) base = atomicAdd(&bk.count[(blk + 1) % 3], (uint32_t)__popc(m));
   base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-  if (add) ((blk + 1) & 1 ? bk.list[1] : bk.list[0])[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)b << 16 | (uint32_t)c;
+  if (add)
+    ((blk + 1) & 1 ? bk.list[1] : bk.list[0])[base + __popc(m & ((1u << lane) - 1u))] =
+        (uint32_t)t.b << 16 | (uint32_t)t.c;
+}
+__device__ __forceinline__ void bit_push(const BitGeo& bg, const BitBook& bk, uint32_t blk, bool want, int c, int b) {
+  bit_push_end(bk, blk, bit_push_begin(bg, bk, blk, want, c, b));
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 // One kBK-layer block over the listed tiles.  nl (<= kBK) layers are applied
 // (the last block of a fixed-L or capped run may be partial).
-__global__ void __launch_bounds__(kBThreads) k_bits_tiles(BitGeo bg, Geo g, uint16_t* __restrict__ field, BitBook bk,
-                                                          uint32_t blk, uint32_t l0, uint32_t nl, uint32_t lref,
+template <bool PART>
+__global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook bk, uint32_t blk, uint32_t nl,
                                                           FlagSink flag, FlagSink prev) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   if (prev.host && blockIdx.x == 0 && threadIdx.x == 0)
     *reinterpret_cast<volatile uint32_t*>(prev.host) = atomicExch(prev.word, 0xFFFFFFFFu);
-  const uint32_t n = bk.count[blk % 3];
   const uint32_t* __restrict__ list = (blk & 1) ? bk.list[1] : bk.list[0];
+  // static first item (spread over the SMs): its list entry is loaded alongside the list length
+  uint32_t w = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const uint32_t n = __ldcg(bk.count + blk % 3);
+  uint32_t it = w < bg.ntiles() ? __ldcg(list + w) : 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     bk.count[(blk + 2) % 3] = 0;
     bk.count[3 + (blk + 2) % 3] = 0;
@@ -83,58 +103,68 @@ __global__ void __launch_bounds__(kBThreads) k_bits_tiles(BitGeo bg, Geo g, uint
   }
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (kBThreads / 32);
+  const bool light = n <= nwarps;  // one item per warp at most: no fetch atomics
   const uint32_t mark = blk + 1;
-  const size_t plane = bg.plane_words();
   uint32_t wmin = 0xFFFFFFFFu;    // fixed-point word: min over new cells of (nl - 1 - in-block index)
   uint32_t covered = 0;           // cells this warp covered
-  // static first item (spread over the SMs), then dynamic
-  uint32_t w = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  // per warp: the time-plane words of the item's own rows (32 rows x kBTW row words x 16 words), staged
+  // with cp.async at item start so the read-modify-write after the layers finds them on chip
+  __shared__ uint4 tsm_all[kBThreads / 32][kBTR * kBTW * 4];
+  uint4* tsm = tsm_all[threadIdx.x >> 5];
   while (w < n) {
-    const uint32_t it = list[w];
     const uint32_t tb = it >> 16, tc = it & 0xFFFFu;
+    uint32_t fa = 0;  // the next item's index (heavy blocks), in flight during this item
+    if (!light && lane == 0) fa = atomicAdd(&bk.count[3 + blk % 3], 1u);
+    __syncwarp();  // the previous item's reads of tsm are done
+    {
+      const uint4* tg = reinterpret_cast<const uint4*>(bk.T) + ((size_t)tc * kBTR * bg.wpr + (size_t)tb * kBTW) * 4;
+#pragma unroll
+      for (int q = 0; q < kBTR * kBTW * 4 / 32; ++q) {
+        const int ch = lane + 32 * q, r = ch / (kBTW * 4), o = ch % (kBTW * 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(tsm + ch)),
+                     "l"(tg + (size_t)r * bg.wpr * 4 + o)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // states of the 3x3 tile neighbourhood: lane k < 9 reads (tc + k/3 - 1, tb + k%3 - 1)
     uint32_t s9 = 0;
-    bool ex = false;
     if (lane < 9) {
       const int c = (int)tc + lane / 3 - 1, b = (int)tb + lane % 3 - 1;
-      ex = c >= 0 && b >= 0 && c < (int)bg.nchunks && b < (int)bg.tbands;
-      if (ex) {
+      if (c >= 0 && b >= 0 && c < (int)bg.nchunks && b < (int)bg.tbands) {
         const unsigned long long sw = __ldcg(bk.state + (uint32_t)c * bg.tbands + (uint32_t)b);
         const uint32_t cur = (uint32_t)sw;
         s9 = (cur >> 1) == mark ? (uint32_t)(sw >> 32) : cur;
       }
     }
-    const uint32_t exm = __ballot_sync(0xffffffffu, ex);
-    const uint32_t hom = __ballot_sync(0xffffffffu, ex && (s9 & 1u));
-    const uint32_t sown = __shfl_sync(0xffffffffu, s9, 4);
-    // ---- load the region: rows tc*TR - K .. tc*TR + TR + K, words tb*TW - 1 .. tb*TW + TW
-    uint32_t C[kBRPL][kBNW], F[kBRPL][kBNW];
+    // ---- load the region (rows tc*TR - K .. tc*TR + TR + K, words tb*TW - 1 .. tb*TW + TW) while the
+    // states are in flight: each plane word is {coverage plane 0, coverage plane 1, free, -}, so both
+    // coverage planes come with the same 16 B load and the homes pick one afterwards
+    const bool exl = tb > 0, exr = tb + 1 < bg.tbands;
+    uint32_t C[kBRPL][kBNW], C1[kBRPL][kBNW], F[kBRPL][kBNW];
 #pragma unroll
     for (int i = 0; i < kBRPL; ++i) {
       const int tr = lane * kBRPL + i - kBK;  // tile-relative row
-      const int d = tr < 0 ? 0 : (tr >= kBTR ? 2 : 1);
       const int prow = (int)tc * kBTR + tr;
-      const size_t rb = (size_t)(prow < 0 ? 0 : prow) * bg.wpr + (size_t)tb * kBTW;
+      const bool er = prow >= 0 && prow < (int)bg.rows;
+      const size_t rb = (size_t)(er ? prow : 0) * bg.wpr + (size_t)tb * kBTW;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int k = d * 3 + q;
-        const bool e = (exm >> k) & 1u;
-        const uint32_t* cp = bk.C + (((hom >> k) & 1u) ? plane : 0);
-        if (q == 1) {
-          if (e) {
-            const uint4 cv = __ldcg(reinterpret_cast<const uint4*>(cp + rb));
-            const uint4 fv = __ldg(reinterpret_cast<const uint4*>(bk.F + rb));
-            C[i][1] = cv.x, C[i][2] = cv.y, C[i][3] = cv.z, C[i][4] = cv.w;
-            F[i][1] = fv.x, F[i][2] = fv.y, F[i][3] = fv.z, F[i][4] = fv.w;
-          } else {
+      for (int x = 0; x < kBNW; ++x) {
+        const bool e = er && (x == 0 ? exl : (x == kBNW - 1 ? exr : true));
+        const uint4 v = e ? __ldcg(bk.P + rb + x - 1) : make_uint4(0u, 0u, 0u, 0u);
+        C[i][x] = v.x, C1[i][x] = v.y, F[i][x] = v.z;
+      }
+    }
+    const uint32_t hom = __ballot_sync(0xffffffffu, s9 & 1u);
+    const uint32_t sown = __shfl_sync(0xffffffffu, s9, 4);
 #pragma unroll
-            for (int x = 1; x <= kBTW; ++x) C[i][x] = F[i][x] = 0u;
-          }
-        } else {
-          const size_t a = q == 0 ? rb - 1 : rb + kBTW;
-          C[i][q == 0 ? 0 : kBNW - 1] = e ? ldcg(cp + a) : 0u;
-          F[i][q == 0 ? 0 : kBNW - 1] = e ? __ldg(bk.F + a) : 0u;
-        }
+    for (int i = 0; i < kBRPL; ++i) {
+      const int tr = lane * kBRPL + i - kBK;
+      const int d = tr < 0 ? 0 : (tr >= kBTR ? 2 : 1);
+#pragma unroll
+      for (int x = 0; x < kBNW; ++x) {
+        const int q = x == 0 ? 0 : (x == kBNW - 1 ? 2 : 1);
+        if ((hom >> (d * 3 + q)) & 1u) C[i][x] = C1[i][x];
       }
     }
     // ---- kBK layers.  J[k]: bit k of the in-block index (layer - 1) of the cells covered in this block,
@@ -151,7 +181,7 @@ __global__ void __launch_bounds__(kBThreads) k_bits_tiles(BitGeo bg, Geo g, uint
 #pragma unroll
     for (int j = 1; j <= kBK; ++j) {
       uint32_t N[kBRPL][kBNW];
-      if ((uint32_t)j <= nl) {
+      if (!PART || (uint32_t)j <= nl) {
         uint32_t up[kBNW], dn[kBNW];
 #pragma unroll
         for (int x = 0; x < kBNW; ++x) {
@@ -199,34 +229,32 @@ __global__ void __launch_bounds__(kBThreads) k_bits_tiles(BitGeo bg, Geo g, uint
 #pragma unroll
         for (int x = 0; x < kBNW; ++x) C[i][x] = N[i][x];
     }
-    // ---- own rows: new cells into the field, coverage into the other plane
+    // ---- own rows: coverage into the other plane; the new cells' layer t into the time planes
+    // (T: 16 words per row word, word k = bit k of t-1 for the row word's 32 cells; t - 1 = l0 + in-block
+    // index, l0 = kBK * blk, so bits < kBNJ are J and the others the bits of blk; only the new cells' bits
+    // change, so T needs no initialisation)
     const uint32_t out_home = (sown & 1u) ^ 1u;
-    uint32_t jmax = 0, any_new = 0, m9 = 0;
+    uint32_t any_new = 0, m9 = 0, fr_all = 0;
+    uint32_t NW[kBRPL][kBTW];
 #pragma unroll
     for (int i = 0; i < kBRPL; ++i) {
       const int tr = lane * kBRPL + i - kBK;
-      if (tr < 0 || tr >= kBTR) continue;
-      const uint32_t row = tc * kBTR + (uint32_t)tr;
-      uint32_t* dst = bk.C + (out_home ? plane : 0) + (size_t)row * bg.wpr + (size_t)tb * kBTW;
-      __stcg(reinterpret_cast<uint4*>(dst), make_uint4(C[i][1], C[i][2], C[i][3], C[i][4]));
-      uint16_t* frow = field + (size_t)(row + g.pad) * g.pitch + g.pad + (size_t)tb * (32 * kBTW);
+      const bool own = tr >= 0 && tr < kBTR;
+#pragma unroll
+      for (int x = 0; x < kBTW; ++x) NW[i][x] = own ? C[i][x + 1] & ~C0[i][x] : 0u;
+      if (!own) continue;
+      const size_t rw = (size_t)(tc * kBTR + (uint32_t)tr) * bg.wpr + (size_t)tb * kBTW;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(bk.P + rw) + out_home;
+#pragma unroll
+      for (int x = 0; x < kBTW; ++x) __stcg(dst + 4 * x, C[i][x + 1]);
       uint32_t fr_any = 0;
 #pragma unroll
       for (int x = 0; x < kBTW; ++x) {
-        uint32_t m = C[i][x + 1] & ~C0[i][x];
-        covered += __popc(m);
-        any_new |= m;
+        covered += __popc(NW[i][x]);
+        any_new |= NW[i][x];
         fr_any |= FR[i][x];
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          uint32_t jj = 0;
-#pragma unroll
-          for (int k = 0; k < kBNJ; ++k) jj |= ((J[k][i][x] >> b) & 1u) << k;
-          jmax = jj > jmax ? jj : jmax;
-          frow[x * 32 + b] = (uint16_t)(kFlag16 | (lref - l0 - jj));
-        }
       }
+      fr_all |= fr_any;
       // frontier regions (bits: any, top, bottom, left, right, tl, tr, bl, br)
       constexpr uint32_t lowK = kBK >= 32 ? 0xFFFFFFFFu : (1u << kBK) - 1u;
       constexpr uint32_t highK = kBK >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> kBK);
@@ -240,22 +268,77 @@ __global__ void __launch_bounds__(kBThreads) k_bits_tiles(BitGeo bg, Geo g, uint
       }
     }
     m9 = __reduce_or_sync(0xffffffffu, m9);
-    const bool anyw = __any_sync(0xffffffffu, any_new != 0);
-    if (anyw) {
-      const uint32_t jm = __reduce_max_sync(0xffffffffu, any_new ? jmax : 0u);
-      const uint32_t v = nl - 1 - jm;
-      wmin = v < wmin ? v : wmin;
-    }
-    uint32_t next = 0;
-    if (lane == 0) next = atomicAdd(&bk.count[3 + blk % 3], 1u) + nwarps;
-    next = __shfl_sync(0xffffffffu, next, 0);
-    if (lane == 0)
-      bk.state[tc * bg.tbands + tb] = (unsigned long long)sown << 32 | (mark << 1 | out_home);
+    // list the next block's candidates (lane k < 9: the neighbour at (k/3 - 1, k%3 - 1) facing a frontier
+    // region); the dedup atomics travel while the time planes are updated
+    PushTicket pt;
     {
       const int dr = lane / 3 - 1, dc = lane % 3 - 1;
       const bool want = lane < 9 && ((m9 >> kBFacing[(lane / 3) % 3][lane % 3]) & 1u);
-      bit_push(bg, bk, blk, want, (int)tc - dr, (int)tb - dc);
+      pt = bit_push_begin(bg, bk, blk, want, (int)tc - dr, (int)tb - dc);
     }
+    uint32_t next = nwarps;
+    if (!light) {  // dynamic items past the static first one: the list entry loads during the update
+      next = __shfl_sync(0xffffffffu, fa, 0) + nwarps;
+      if (next < n) it = __ldcg(list + next);
+    }
+    // ---- time planes (T: 16 words per row word, word k = bit k of t-1 for the row word's 32 cells;
+    // t - 1 = l0 + in-block index, l0 = kBK * blk, so bits < kBNJ are J and the others the bits of blk;
+    // only the new cells' bits change, so T needs no initialisation)
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kBRPL; ++i) {
+      const int tr = lane * kBRPL + i - kBK;
+      if (tr < 0 || tr >= kBTR) continue;
+      const size_t rw = (size_t)(tc * kBTR + (uint32_t)tr) * bg.wpr + (size_t)tb * kBTW;
+#pragma unroll
+      for (int x = 0; x < kBTW; ++x) {
+        const uint32_t nw = NW[i][x];
+        if (!nw) continue;
+        const uint4* ts = tsm + (tr * kBTW + x) * 4;
+        uint32_t v[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 a4 = ts[q];
+          v[4 * q] = a4.x, v[4 * q + 1] = a4.y, v[4 * q + 2] = a4.z, v[4 * q + 3] = a4.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+          const uint32_t bitv = k < kBNJ ? J[k < kBNJ ? k : 0][i][x] : (((blk >> (k - kBNJ)) & 1u) ? nw : 0u);
+          v[k] = (v[k] & ~nw) | bitv;
+        }
+        uint4* tp = reinterpret_cast<uint4*>(bk.T + (rw + x) * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) __stcg(tp + q, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+      }
+    }
+    if (__any_sync(0xffffffffu, any_new != 0)) {
+      // in-block index of the warp's last new cell: kBK - 1 if a cell is new in the last layer, else the
+      // bit-sliced maximum over the new cells' J
+      uint32_t jm = kBK - 1;
+      if (!__any_sync(0xffffffffu, fr_all != 0)) {
+        jm = 0;
+#pragma unroll
+        for (int k = kBNJ - 1; k >= 0; --k) {
+          uint32_t a = 0;
+#pragma unroll
+          for (int i = 0; i < kBRPL; ++i)
+#pragma unroll
+            for (int x = 0; x < kBTW; ++x) a |= NW[i][x] & J[k][i][x];
+          const bool set = __any_sync(0xffffffffu, a != 0);
+          if (set) jm |= 1u << k;
+#pragma unroll
+          for (int i = 0; i < kBRPL; ++i)
+#pragma unroll
+            for (int x = 0; x < kBTW; ++x) NW[i][x] &= set ? J[k][i][x] : ~J[k][i][x];
+        }
+      }
+      const uint32_t v = nl - 1 - jm;
+      wmin = v < wmin ? v : wmin;
+    }
+    if (lane == 0)
+      bk.state[tc * bg.tbands + tb] = (unsigned long long)sown << 32 | (mark << 1 | out_home);
+    bit_push_end(bk, blk, pt);
     w = next;
   }
   covered = __reduce_add_sync(0xffffffffu, covered);
@@ -265,70 +348,137 @@ __global__ void __launch_bounds__(kBThreads) k_bits_tiles(BitGeo bg, Geo g, uint
   }
 }
 
-// F plane + layer-0 field from the dense occupancy (occ != 0: obstacle).  A warp
-// builds 32 words of one plane row: 32 ballots over coalesced byte loads, the
-// field cells (free: flag | 0, obstacle 0) written as it goes.
-__global__ void k_bits_init(BitGeo bg, Geo g, const uint8_t* __restrict__ occ, uint32_t* __restrict__ F,
-                            uint16_t* __restrict__ field, unsigned long long* __restrict__ free_cells) {
+// Plane words {0, 0, free, 0} from the dense occupancy (occ != 0: obstacle).  A warp builds 32 words of
+// one plane row: 32 ballots over coalesced byte loads.
+__global__ void k_bits_init(BitGeo bg, const uint8_t* __restrict__ occ, uint4* __restrict__ P,
+                            unsigned long long* __restrict__ free_cells) {
   const int lane = threadIdx.x & 31;
   const uint32_t row = blockIdx.y * (blockDim.x / 32) + (threadIdx.x >> 5);
   const uint32_t w0 = blockIdx.x * 32;
   if (row >= bg.rows) return;  // warp-uniform
-  uint32_t mine = 0, cnt = 0;
+  uint32_t mine = 0;
   const bool in_row = row < bg.H;
-  for (int k = 0; k < 32 && w0 + k < bg.wpr; ++k) {
+  const uint8_t* orow = occ + (size_t)row * bg.W;
+  uint8_t o[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {  // all 32 loads in flight
     const uint32_t col = (w0 + k) * 32 + lane;
-    const bool in = in_row && col < bg.W;
-    const bool fr = in && occ[(size_t)row * bg.W + col] == 0;
-    const uint32_t bits = __ballot_sync(0xffffffffu, fr);
-    if (lane == k) mine = bits;
-    if (in) field[(size_t)(row + g.pad) * g.pitch + g.pad + col] = fr ? (uint16_t)kFlag16 : (uint16_t)0;
+    o[k] = in_row && col < bg.W ? orow[col] : (uint8_t)1;
   }
-  if (w0 + lane < bg.wpr) F[(size_t)row * bg.wpr + w0 + lane] = mine;
-  cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mine));
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t bits = __ballot_sync(0xffffffffu, o[k] == 0);
+    if (lane == k) mine = bits;
+  }
+  if (w0 + lane < bg.wpr) P[(size_t)row * bg.wpr + w0 + lane] = make_uint4(0u, 0u, mine, 0u);  // not covered
+  const uint32_t cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mine));
   if (lane == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
 }
 
-// Sources (validated free cells): covered at layer 0 (activity lref + 1), and block 0's work list
-// (the 3x3 tile neighbourhood of each source's tile, pushed as block "-1").  One warp per source.
-__global__ void k_bits_sources(BitGeo bg, Geo g, const uint32_t* __restrict__ rc, uint64_t n, uint32_t* __restrict__ C,
-                               uint16_t* __restrict__ field, BitBook bk, uint32_t lref) {
+// Sources (validated free cells): covered at layer 0, time-plane value 0x7FFF (no covered cell has
+// t - 1 = 0x7FFF: t <= lref <= 32766), and block 0's work list (the 3x3 tile neighbourhood of each
+// source's tile, pushed as block "-1").  One warp per source.
+__global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint64_t n, BitBook bk) {
   const uint64_t s = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   if (s >= n) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const uint32_t r = rc[2 * s], c = rc[2 * s + 1];
+  const size_t rw = (size_t)r * bg.wpr + (c >> 5);
+  const uint32_t bit = 1u << (c & 31);
   if (lane == 0) {
-    const uint32_t bit = 1u << (c & 31);
-    const uint32_t old = atomicOr(C + (size_t)r * bg.wpr + (c >> 5), bit);
+    const uint32_t old = atomicOr(&bk.P[rw].x, bit);
     if (!(old & bit)) atomicAdd(&bk.stat[1], 1ull);
-    field[(size_t)(r + g.pad) * g.pitch + g.pad + c] = (uint16_t)(kFlag16 | (lref + 1));
   }
+  if (lane < 15) atomicOr(bk.T + rw * 16 + lane, bit);
   const int tc = (int)(r / kBTR), tb = (int)(c / (32 * kBTW));
   bit_push(bg, bk, 0xFFFFFFFFu, lane < 9, tc + lane / 3 - 1, tb + lane % 3 - 1);
+}
+
+// The encoded field (am_internal.cuh) from the planes, once per run: free covered cell flag | (lref - u)
+// with u = t - 1 from the time planes (lref + 1 at sources, u = 0x7FFF), free uncovered flag | 0,
+// obstacle 0.  A warp converts two row words per step: lane k < 16 loads time-plane word k of the first,
+// lanes 16-31 those of the second (128 B, coalesced), a 32 x 32 bit transpose over the lanes (five
+// butterfly shuffles) leaves lane c with both cells' u as a u16x2 pair, and two coalesced 64 B stores
+// follow.
+__global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uint16_t* __restrict__ field) {
+  constexpr int P = 4;  // row-word pairs per warp step (loads of all of them in flight together)
+  const int lane = threadIdx.x & 31;
+  const uint32_t groups = (bg.wpr / 2 + P - 1) / P;
+  const uint32_t total = bg.H * groups;  // < 2^32: H, W <= 65535
+  const uint32_t L2 = lref | lref << 16, S2 = (lref + 1) | (lref + 1) << 16;
+  const uint32_t nw = gridDim.x * (blockDim.x / 32);
+  for (uint32_t p = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < total; p += nw) {
+    const uint32_t row = p / groups, wb = 2 * P * (p - row * groups);
+    const size_t rb = (size_t)row * bg.wpr;
+    // lanes 0 .. 2P-1: the free / covered words of the group (covered from the tile's home plane)
+    uint32_t fv = 0, cv = 0;
+    const uint32_t wl = wb + lane;
+    if (lane < 2 * P && wl < bg.wpr) {
+      const uint4 pv = __ldcg(bk.P + rb + wl);
+      const uint32_t home = (uint32_t)__ldcg(bk.state + (row / kBTR) * bg.tbands + wl / kBTW) & 1u;
+      fv = pv.z;
+      cv = home ? pv.y : pv.x;
+    }
+    uint32_t x[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) x[q] = wb + 2 * q < bg.wpr ? __ldcs(bk.T + (rb + wb + 2 * q) * 16 + lane) : 0u;
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) {
+      const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
+                                                                                                    : 0x55555555u;
+      // lanes with bit j set keep the bits of columns with bit j set and take the partner's, moved down by
+      // j; the others keep / take the complementary columns, moved up (a rotation: the moved-out bits are 0)
+      const uint32_t keep = (lane & j) ? ~m : m;
+      const uint32_t rot = (lane & j) ? j : 32 - j;
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x[q], j) & keep;
+        x[q] = (x[q] & keep) | __funnelshift_r(y, y, rot);
+      }
+    }
+    uint16_t* dst = field + (size_t)(row + g.pad) * g.pitch + g.pad + (size_t)wb * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const uint32_t f0 = __shfl_sync(0xffffffffu, fv, 2 * q), f1 = __shfl_sync(0xffffffffu, fv, 2 * q + 1);
+      const uint32_t c0 = __shfl_sync(0xffffffffu, cv, 2 * q), c1 = __shfl_sync(0xffffffffu, cv, 2 * q + 1);
+      const uint32_t u = x[q] & 0x7FFF7FFFu;
+      const uint32_t src = __vcmpeq2(u, 0x7FFF7FFFu);
+      const uint32_t fm = (((f0 >> lane) & 1u) ? 0x0000FFFFu : 0u) | (((f1 >> lane) & 1u) ? 0xFFFF0000u : 0u);
+      const uint32_t cm = (((c0 >> lane) & 1u) ? 0x0000FFFFu : 0u) | (((c1 >> lane) & 1u) ? 0xFFFF0000u : 0u);
+      const uint32_t a = (__vsub2(L2, u) & ~src) | (S2 & src);
+      const uint32_t v = ((a & cm) | 0x80008000u) & fm;
+      const uint32_t col = (wb + 2 * q) * 32 + lane;
+      if (col < bg.W) dst[64 * q] = (uint16_t)(v & 0xFFFFu);
+      if (col + 32 < bg.W) dst[64 * q + 32] = (uint16_t)(v >> 16);
+    }
+  }
 }
 
 }  // namespace
 
 int bits_ctas_per_sm() {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bits_tiles, kBThreads, 0) != cudaSuccess) n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bits_tiles<false>, kBThreads, 0) != cudaSuccess) n = 1;
   return n < 1 ? 1 : n;
 }
 
-void launch_bits_init(const BitGeo& bg, const Geo& g, const uint8_t* occ, BitBook bk, uint16_t* field,
-                      cudaStream_t s) {
+void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStream_t s) {
   const dim3 grid((bg.wpr + 31) / 32, (bg.rows + 7) / 8);
-  k_bits_init<<<grid, 256, 0, s>>>(bg, g, occ, bk.F, field, bk.stat + 2);
+  k_bits_init<<<grid, 256, 0, s>>>(bg, occ, bk.P, bk.stat + 2);
 }
 
-void launch_bits_sources(const BitGeo& bg, const Geo& g, const uint32_t* rc, uint64_t n, BitBook bk, uint16_t* field,
-                         uint32_t lref, cudaStream_t s) {
+void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBook bk, cudaStream_t s) {
   if (!n) return;
-  k_bits_sources<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(bg, g, rc, n, bk.C, field, bk, lref);
+  k_bits_sources<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(bg, rc, n, bk);
 }
 
-void launch_bits_tiles(const BitGeo& bg, const Geo& g, int ctas, uint16_t* field, BitBook bk, uint32_t blk,
-                       uint32_t l0, uint32_t nl, uint32_t lref, FlagSink flag, FlagSink prev, cudaStream_t s) {
+void launch_bits_finalize(const BitGeo& bg, const Geo& g, BitBook bk, uint32_t lref, uint16_t* field, int sms,
+                          cudaStream_t s) {
+  k_bits_finalize<<<sms * 8, 256, 0, s>>>(bg, g, bk, lref, field);
+}
+
+void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uint32_t nl, FlagSink flag,
+                       FlagSink prev, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(kBThreads);
@@ -339,7 +489,11 @@ void launch_bits_tiles(const BitGeo& bg, const Geo& g, int ctas, uint16_t* field
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_bits_tiles, bg, g, field, bk, blk, l0, nl, lref, flag, prev);
+  // a partial block (the last of a fixed-L or capped run) skips its layers past nl
+  if (nl == (uint32_t)kBK)
+    cudaLaunchKernelEx(&cfg, k_bits_tiles<false>, bg, bk, blk, nl, flag, prev);
+  else
+    cudaLaunchKernelEx(&cfg, k_bits_tiles<true>, bg, bk, blk, nl, flag, prev);
 }
 
 }  // namespace am

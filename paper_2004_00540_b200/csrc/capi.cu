@@ -169,14 +169,14 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->t_processed);
   am::dfree(ctx, g->t_src);
   if (g->bits) {
-    am::dfree(ctx, g->bits->bk.F);
-    am::dfree(ctx, g->bits->bk.C);
+    am::dfree(ctx, g->bits->bk.P);
     am::dfree(ctx, g->bits->bk.state);
     am::dfree(ctx, g->bits->bk.sched);
     am::dfree(ctx, g->bits->bk.list[0]);
     am::dfree(ctx, g->bits->bk.list[1]);
     am::dfree(ctx, g->bits->bk.count);
     am::dfree(ctx, g->bits->bk.stat);
+    am::dfree(ctx, g->bits->own_t);
     delete g->bits;
   }
   am::peer_destroy(g->peer);
@@ -432,8 +432,7 @@ static am_status bits_alloc(am_ctx* ctx, am_grid* g) {
   b->bg = make_bit_geo(g->g.W, g->g.H);
   const size_t pw = b->bg.plane_words(), nt = b->bg.ntiles();
   BitBook& k = b->bk;
-  CK(am::dmalloc(ctx, &k.F, pw * 4));
-  CK(am::dmalloc(ctx, &k.C, 2 * pw * 4));
+  CK(am::dmalloc(ctx, &k.P, pw * 16));
   CK(am::dmalloc(ctx, &k.state, nt * 8));
   CK(am::dmalloc(ctx, &k.sched, nt * 4));
   CK(am::dmalloc(ctx, &k.list[0], nt * 4));
@@ -456,14 +455,22 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   cudaStream_t s = ctx->stream;
   const uint32_t lref = std::min(target, kBitsMaxRef);
   uint16_t* field = static_cast<uint16_t*>(g->val[0]);
-  CK(cudaMemsetAsync(B.bk.C, 0, pw * 4, s));  // plane 0: every tile's home at layer 0
+  // time planes (64 B per plane word): the second 16-bit field when it is large enough
+  const size_t tbytes = pw * 64, vbytes = (size_t)g->g.rows * g->g.pitch * 2;
+  if (tbytes <= vbytes) {
+    B.bk.T = static_cast<uint32_t*>(g->val[1]);
+    g->dirty[1] = 1;  // holds time planes now, not a clean field
+  } else {
+    if (!B.own_t) CK(am::dmalloc(ctx, &B.own_t, tbytes));
+    B.bk.T = B.own_t;
+  }
   CK(cudaMemsetAsync(B.bk.state, 0, nt * 8, s));
   CK(cudaMemsetAsync(B.bk.sched, 0, nt * 4, s));
   CK(cudaMemsetAsync(B.bk.count, 0, 6 * 4, s));
   CK(cudaMemsetAsync(B.bk.stat, 0, 3 * 8, s));
-  launch_bits_init(bg, g->g, g->occ, B.bk, field, s);
+  launch_bits_init(bg, g->occ, B.bk, s);
   CKL();
-  launch_bits_sources(bg, g->g, g->src_rc, g->n_src, B.bk, field, lref, s);
+  launch_bits_sources(bg, g->src_rc, g->n_src, B.bk, s);
   CKL();
   ctx->launches += 2;
   g->cur = 0;
@@ -511,7 +518,7 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
       g->fs->h[slot] = kSlotPending;  // consumed kFlagSlots blocks ago (lag < kFlagSlots)
       unpublished = FlagSink{sink.word, sink.done, g->fs->hdev + slot};  // published by the next launch
     }
-    launch_bits_tiles(bg, g->g, B.ctas, field, B.bk, blk, l, nl, lref, sink, prev, s);
+    launch_bits_tiles(bg, B.ctas, B.bk, blk, nl, sink, prev, s);
     ++ctx->launches;
     if (cudaError_t e = cudaPeekAtLastError()) return fail(ctx, AM_ECUDA, "k_bits_tiles: %s", cudaGetErrorString(e));
     ++r.block_launches;
@@ -525,6 +532,9 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
     launch_publish_flag(unpublished, s);
     CKL();
   }
+  launch_bits_finalize(bg, g->g, B.bk, lref, field, ctx->sms, s);  // the encoded field, once
+  CKL();
+  ctx->launches += 1;
   if (timing) CK(cudaEventRecord(ctx->timers[0].b, s));
   while (!pend.empty())
     if ((st = drain_one())) return st;
@@ -542,6 +552,8 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
       cause = any_zero ? AM_STOP_CAP : AM_STOP_FILLED;
     } else {
       *handoff = true;  // field at layer lref, beyond the 16-bit range: continue with the tile kernels
+      CK(cudaMemsetAsync(g->val[1], 0, vbytes, s));
+      g->dirty[1] = 0;
     }
   }
   g->computed = lref;

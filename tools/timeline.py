@@ -56,14 +56,14 @@ def main():
     print("idle gaps by transition:")
     for k, us in gaps.most_common(4):
         print(f"  {k:55s} {us / 1e3:8.3f} ms")
-    ends = [e["ts"] + e["dur"] for e in dev if e["cat"] == "kernel" and "block_tiles" in e["name"]]
+    ends = [e["ts"] + e["dur"] for e in dev if e["cat"] == "kernel" and ("block_tiles" in e["name"] or "bits_tiles" in e["name"])]
     if len(ends) > 10:
         step = [b - a for a, b in zip(ends, ends[1:])]  # per-block span: end-to-end spacing of consecutive blocks
         print("last 32 end spacings (us): " + " ".join(f"{x:.1f}" for x in step[-32:]))
         print("k_block_tiles end spacing by launch decile (mean us): " +
               " ".join(f"{sum(x) / len(x):.1f}" for x in (step[i * len(step) // 10:(i + 1) * len(step) // 10]
                                                           for i in range(10))))
-    tk = [e["dur"] for e in dev if e["cat"] == "kernel" and "block_tiles" in e["name"]]
+    tk = [e["dur"] for e in dev if e["cat"] == "kernel" and ("block_tiles" in e["name"] or "bits_tiles" in e["name"])]
     if tk:
         q = sorted(tk)
         pct = lambda p: q[min(len(q) - 1, int(p * len(q)))]
