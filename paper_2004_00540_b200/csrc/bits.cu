@@ -103,7 +103,10 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
   }
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (kBThreads / 32);
-  const bool light = n <= nwarps;  // one item per warp at most: no fetch atomics
+#ifndef AM_BITS_STATIC
+#define AM_BITS_STATIC 1  // items dealt round-robin (measured: the fetch atomic costs more than the imbalance)
+#endif
+  const bool light = AM_BITS_STATIC || n <= nwarps;  // one item per warp at most: no fetch atomics
   const uint32_t mark = blk + 1;
   uint32_t wmin = 0xFFFFFFFFu;    // fixed-point word: min over new cells of (nl - 1 - in-block index)
   uint32_t covered = 0;           // cells this warp covered
@@ -114,7 +117,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
   while (w < n) {
     const uint32_t tb = it >> 16, tc = it & 0xFFFFu;
     uint32_t fa = 0;  // the next item's index (heavy blocks), in flight during this item
-    if (!light && lane == 0) fa = atomicAdd(&bk.count[3 + blk % 3], 1u);
+    if (!light && lane == 0)  // inline PTX: the compiler's warp aggregation would consume the result here
+      asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(fa) : "l"(bk.count + 3 + blk % 3) : "memory");
     __syncwarp();  // the previous item's reads of tsm are done
     {
       const uint4* tg = reinterpret_cast<const uint4*>(bk.T) + ((size_t)tc * kBTR * bg.wpr + (size_t)tb * kBTW) * 4;
@@ -276,7 +280,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
       const bool want = lane < 9 && ((m9 >> kBFacing[(lane / 3) % 3][lane % 3]) & 1u);
       pt = bit_push_begin(bg, bk, blk, want, (int)tc - dr, (int)tb - dc);
     }
-    uint32_t next = nwarps;
+    uint32_t next = AM_BITS_STATIC ? w + nwarps : nwarps;
+    if (AM_BITS_STATIC && next < n) it = __ldcg(list + next);
     if (!light) {  // dynamic items past the static first one: the list entry loads during the update
       next = __shfl_sync(0xffffffffu, fa, 0) + nwarps;
       if (next < n) it = __ldcg(list + next);
