@@ -89,6 +89,7 @@ struct am_grid {
   uint8_t* t_src = nullptr;                  // per tile: a source in its staged rows (TileBook::tsrc)
   am::PeerLink* peer = nullptr;              // slabs: peer-memory transport (am_peer_connect)
   am::BitState* bits = nullptr;              // bit-plane propagation (single grids, 16-bit runs)
+  int bits_map = 0;                          // val[0] came from a bit-plane run whose planes are intact
   am::TileBook book() const {
     return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed, t_src};
   }

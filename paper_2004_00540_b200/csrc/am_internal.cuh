@@ -244,6 +244,11 @@ struct MapView {
   const uint8_t* occ;     // plain mode only: dense occupancy
   uint32_t layers;        // layers represented by the values (for point counts)
   const SlabDir* dir = nullptr;  // encoded maps only: the field is distributed over row slabs (val unused)
+  // maps of a bit-plane run (bits.cu) whose planes are intact: the walkers read coverage + time planes
+  const uint4* bp = nullptr;                 // {covered, u bit 0, u bit 1, free} per plane word (after k_bits_finalize)
+  const uint32_t* bt = nullptr;              // time planes, 16 words per plane word
+  const unsigned long long* bstate = nullptr;  // tile states (home plane)
+  BitGeo bg{};
   // allocated row arow of an encoded field (cell 0 = allocated column 0)
   template <typename T>
   __device__ __forceinline__ const T* row(int arow) const {

@@ -521,6 +521,7 @@ am_status wave_propagate(am_ctx* ctx, am_batch* b, uint32_t layers, uint32_t aut
   g->computed = g->layers_used = lref;  // values are lref + 1 - t; maze i's rollback is lref - used[i]
   g->plain_active = 0;
   g->have_map = 1;
+  g->bits_map = 0;
   uint32_t maxl = 0;
   for (uint32_t u : b->layers_used) maxl = std::max(maxl, u);
   *r = am_prop_result{};

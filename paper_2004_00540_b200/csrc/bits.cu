@@ -400,6 +400,7 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
 }
 
 // The encoded field (am_internal.cuh) from the planes, once per run: free covered cell flag | (lref - u)
+// (and the plane words rewritten for the path walkers as {covered, u bit 0, u bit 1, free})
 // with u = t - 1 from the time planes (lref + 1 at sources, u = 0x7FFF), free uncovered flag | 0,
 // obstacle 0.  A warp converts two row words per step: lane k < 16 loads time-plane word k of the first,
 // lanes 16-31 those of the second (128 B, coalesced), a 32 x 32 bit transpose over the lanes (five
@@ -421,8 +422,11 @@ __global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uin
     if (lane < 2 * P && wl < bg.wpr) {
       const uint4 pv = __ldcg(bk.P + rb + wl);
       const uint32_t home = (uint32_t)__ldcg(bk.state + (row / kBTR) * bg.tbands + wl / kBTW) & 1u;
+      const uint2 t01 = __ldcg(reinterpret_cast<const uint2*>(bk.T + (rb + wl) * 16));
       fv = pv.z;
       cv = home ? pv.y : pv.x;
+      // the walkers' plane word from now on: {covered, u bit 0, u bit 1, free} (the next run re-initialises P)
+      __stcg(bk.P + rb + wl, make_uint4(cv, t01.x, t01.y, fv));
     }
     uint32_t x[P];
 #pragma unroll

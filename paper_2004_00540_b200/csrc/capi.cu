@@ -558,6 +558,7 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   }
   g->computed = lref;
   g->layers_used = *handoff ? lref : used;
+  g->bits_map = *handoff ? 0 : 1;  // the walkers may read the planes (until val[1] is reused)
   if (timing) {
     float f = 0;
     CK(cudaEventElapsedTime(&f, ctx->timers[0].a, ctx->timers[0].b));
@@ -592,6 +593,7 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   if (target > kMaxLayers) return fail(ctx, AM_EINVAL, "layer count %u exceeds kMaxLayers", target);
   if (mode != AM_MODE_BATCHED && mode != AM_MODE_ITERATIVE) return fail(ctx, AM_EINVAL, "bad mode");
   CK(cudaSetDevice(ctx->device));
+  for (auto& sr : slabs) sr.g->bits_map = 0;
   // 16-bit cells unless the run can never fit (fixed L beyond the 16-bit range)
   const int start_bits = (!autom && (uint64_t)target + 1 > kMax16Activity) ? 32 : 16;
   am_status st;
@@ -1009,6 +1011,7 @@ static am_status download_impl(am_ctx* ctx, am_grid* g, uint32_t* dst, bool dst_
   // copied out on the copy stream: the PCIe copy is the floor, the decode hides behind it
   uint32_t* stage = (uint32_t*)g->val[g->cur ^ 1];
   g->dirty[g->cur ^ 1] = 1;
+  if (g->cur == 0) g->bits_map = 0;  // val[1] (the time planes) is the staging buffer now
   const size_t stage_bytes = (size_t)g->g.rows * g->g.pitch * (g->cell_bits / 8);
   constexpr int kChunks = 4;  // stage buffers in flight
   size_t rows_per = std::min(stage_bytes / (W * 4 * kChunks), std::max<size_t>(1, (256u << 20) / (W * 4)));
@@ -1074,6 +1077,12 @@ static am::MapView view_of(am_grid* g) {
     m.cell_bits = g->cell_bits;
     m.occ = g->occ;
     m.layers = g->computed;  // point counts are invariant under the rollback
+    if (g->bits_map && g->bits && g->cur == 0 && g->cell_bits == 16) {
+      m.bp = g->bits->bk.P;
+      m.bt = g->bits->bk.T;
+      m.bstate = g->bits->bk.state;
+      m.bg = g->bits->bg;
+    }
   }
   return m;
 }

@@ -455,6 +455,7 @@ static am_status adopt_full(am_ctx* ctx, am_grid* full, const am_grid* like) {
   full->cur = 0;
   full->plain_active = 0;
   full->have_map = 1;
+  full->bits_map = 0;
   full->computed = like->computed;
   full->layers_used = like->layers_used;
   return AM_OK;

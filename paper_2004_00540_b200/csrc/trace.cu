@@ -171,7 +171,10 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
 #ifndef AM_TWC
 #define AM_TWC 32  // 16-bit window columns (smaller windows stage faster; tools/ab_trace.sh)
 #endif
-constexpr int kWinBytes = AM_TWR * AM_TWC * 2 > 4096 ? AM_TWR * AM_TWC * 2 : 4096;  // shared memory per warp
+constexpr int kWinBytes = 4096 + 256;  // shared memory per warp: a window (<= 4 KB) + the plane walk's point ring
+#ifndef AM_TRACE_PLANES
+#define AM_TRACE_PLANES 1  // bit-plane runs: walk on the coverage / time planes (walk_planes)
+#endif
 
 template <typename T, int WR, int WC>
 __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int method, uint64_t seed, uint64_t limit,
@@ -378,6 +381,191 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
   return n;
 }
 
+// Walk on the planes of a bit-plane run (bits.cu): coverage C and the two low bits of u = t - 1 (the
+// layer a cell was covered at, minus one; sources 0x7FFF == -1 mod 4).  On a propagated map an
+// 8-neighbour n is an ascent candidate of c (activity + 1) exactly when both are covered and
+// u_c - u_n == 1 (activities of covered 8-neighbours differ by <= 1, activity = lref - u), and mod 4 that
+// is two LOP3s per 32 cells: (a0 ^ b0) & ~(a1 ^ b1 ^ b0) with a = u_c, b = u_n.  A warp stages a 64 x 64
+// window (two rows of two words per lane, one 16 B plane word {covered, u bit 0, u bit 1, free} each, as
+// k_bits_finalize leaves them),
+// builds every cell's candidates for all 8 directions with shifts and shuffles of whole words and stores
+// one 16 B record per word in shared memory.  Euclidean rule (pin P1): the first candidate of L, R, U, D,
+// UL, UR, DL, DR, kept as four move planes (row +1, row -1, column +1, column -1), so a step is one
+// broadcast 16 B shared-memory read, four shifts and two subtractions; the window's border cells get no
+// move, so "no move" means re-stage (8 cells behind the cell in its direction of travel) or, right after a
+// re-stage, a map without an ascending neighbour.  Simple rule (pin P2): the 8 candidate words (two
+// records), the seeded tie-break per step.  Points go to a 32-entry shared-memory ring, flushed by the
+// whole warp every 32 points.
+constexpr int kPR = 64, kPW = 2;  // plane window: rows, 32-cell words per row (two rows per lane)
+constexpr int kPTab = kPR * kPW * 2 * 16;  // window records (simple rule: two per word)
+
+// Stages the plane window around (r, c), 8 cells behind it in its direction of travel (ldr, ldc), and
+// builds the window records (out of line: the step loop stays short).
+template <int METHOD>
+__device__ __noinline__ void stage_planes(const MapView& m, uint32_t r, uint32_t c, int ldr, int ldc, uint4* tab,
+                                          int* wr_out, int* wc_out) {
+  const int lane = threadIdx.x & 31;
+  const BitGeo& bg = m.bg;
+  const int orr = ldr < 0 ? kPR - 8 : (ldr > 0 ? 8 : kPR / 2);
+  // columns: the origin is floored to a word, so the cell lands in [orc, orc + 31]
+  const int orc = ldc < 0 ? 32 * kPW - 33 : (ldc > 0 ? 1 : 16 * kPW - 16);
+  const int wr = (int)r - orr;
+  const int wc = (((int)c - orc) >> 5) * 32;  // arithmetic shift: floor
+  uint32_t X[2][kPW], A0[2][kPW], A1[2][kPW];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int x = 0; x < kPW; ++x) {
+      const int gr = wr + 2 * lane + i, gw = (wc >> 5) + x;
+      X[i][x] = A0[i][x] = A1[i][x] = 0u;
+      if (gr >= 0 && gr < (int)bg.H && gw >= 0 && gw < (int)bg.wpr) {  // planes are read-only here: L1
+        const uint4 p = __ldg(m.bp + (size_t)gr * bg.wpr + gw);  // {covered, u bit 0, u bit 1, free}
+        X[i][x] = p.x;
+        A0[i][x] = p.y;
+        A1[i][x] = p.z;
+      }
+    }
+  // rows above / below each of the lane's two rows
+  uint32_t UX[2][kPW], U0[2][kPW], U1[2][kPW], DX[2][kPW], D0[2][kPW], D1[2][kPW];
+#pragma unroll
+  for (int x = 0; x < kPW; ++x) {
+    UX[0][x] = __shfl_up_sync(0xffffffffu, X[1][x], 1);
+    U0[0][x] = __shfl_up_sync(0xffffffffu, A0[1][x], 1);
+    U1[0][x] = __shfl_up_sync(0xffffffffu, A1[1][x], 1);
+    DX[1][x] = __shfl_down_sync(0xffffffffu, X[0][x], 1);
+    D0[1][x] = __shfl_down_sync(0xffffffffu, A0[0][x], 1);
+    D1[1][x] = __shfl_down_sync(0xffffffffu, A1[0][x], 1);
+    UX[1][x] = X[0][x], U0[1][x] = A0[0][x], U1[1][x] = A1[0][x];
+    DX[0][x] = X[1][x], D0[0][x] = A0[1][x], D1[0][x] = A1[1][x];
+  }
+  __syncwarp();  // the previous window's records are no longer read
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int x = 0; x < kPW; ++x) {
+      // neighbour planes of word x of a row (dc = -1: bit j from column j - 1; +1: from j + 1)
+      auto shl = [&](const uint32_t(&w)[kPW]) { return x > 0 ? __funnelshift_l(w[x - 1], w[x], 1) : w[x] << 1; };
+      auto shr = [&](const uint32_t(&w)[kPW]) {
+        return x < kPW - 1 ? __funnelshift_r(w[x], w[x + 1], 1) : w[x] >> 1;
+      };
+      const uint32_t a0 = A0[i][x], a1 = A1[i][x];
+      auto cand = [&](uint32_t nc, uint32_t n0, uint32_t n1) { return nc & (a0 ^ n0) & ~(a1 ^ n1 ^ n0); };
+      const uint32_t cL = cand(shl(X[i]), shl(A0[i]), shl(A1[i]));
+      const uint32_t cR = cand(shr(X[i]), shr(A0[i]), shr(A1[i]));
+      const uint32_t cU = cand(UX[i][x], U0[i][x], U1[i][x]);
+      const uint32_t cD = cand(DX[i][x], D0[i][x], D1[i][x]);
+      const uint32_t cUL = cand(shl(UX[i]), shl(U0[i]), shl(U1[i]));
+      const uint32_t cUR = cand(shr(UX[i]), shr(U0[i]), shr(U1[i]));
+      const uint32_t cDL = cand(shl(DX[i]), shl(D0[i]), shl(D1[i]));
+      const uint32_t cDR = cand(shr(DX[i]), shr(D0[i]), shr(D1[i]));
+      // the window's border cells get no move (their neighbourhoods are not all staged)
+      const int wrow = 2 * lane + i;
+      const uint32_t inner = (wrow == 0 || wrow == kPR - 1) ? 0u
+                             : (x == 0 ? 0xFFFFFFFEu : 0xFFFFFFFFu) & (x == kPW - 1 ? 0x7FFFFFFFu : 0xFFFFFFFFu);
+      const int e = wrow * kPW + x;
+      if (METHOD == 1) {  // first of L, R, U, D, UL, UR, DL, DR
+        uint32_t taken = cL;
+        const uint32_t sR = cR & ~taken;
+        taken |= cR;
+        const uint32_t sU = cU & ~taken;
+        taken |= cU;
+        const uint32_t sD = cD & ~taken;
+        taken |= cD;
+        const uint32_t sUL = cUL & ~taken;
+        taken |= cUL;
+        const uint32_t sUR = cUR & ~taken;
+        taken |= cUR;
+        const uint32_t sDL = cDL & ~taken;
+        taken |= cDL;
+        const uint32_t sDR = cDR & ~taken;
+        tab[e] = make_uint4((sD | sDL | sDR) & inner, (sU | sUL | sUR) & inner, (sR | sUR | sDR) & inner,
+                            (cL | sUL | sDL) & inner);  // row +1, row -1, column +1, column -1
+      } else {  // simple: row-major candidate words (-1,-1) (-1,0) (-1,1) (0,-1) | (0,1) (1,-1) (1,0) (1,1)
+        tab[2 * e] = make_uint4(cUL & inner, cU & inner, cUR & inner, cL & inner);
+        tab[2 * e + 1] = make_uint4(cR & inner, cDL & inner, cD & inner, cDR & inner);
+      }
+    }
+  __syncwarp();
+  *wr_out = wr;
+  *wc_out = wc;
+}
+
+template <int METHOD>
+__device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64_t seed, uint32_t limit,
+                                uint32_t* out, int32_t* st, uint4* tab, uint2* ring) {
+  const int lane = threadIdx.x & 31;
+  const MapView& m = rd.m;
+  // simple rule: direction k (row-major) -> (dr, dc), 2-bit packed (d + 1)
+  constexpr uint32_t PR = 0xA940u, PC = 0x9224u;
+  uint64_t rng = seed;
+  int wr = 0, wc = 0, ldr = 0, ldc = 0;
+  auto stage = [&]() { stage_planes<METHOD>(m, r, c, ldr, ldc, tab, &wr, &wc); };
+  // point ring: lane 0 appends, the warp writes 32 points at a time
+  auto flush = [&](uint32_t upto) {  // points [upto & ~31, upto) are in the ring
+    __syncwarp();
+    const uint32_t base = (upto - 1) & ~31u;
+    if (base + lane < upto) reinterpret_cast<uint2*>(out)[base + lane] = ring[lane];
+    __syncwarp();
+  };
+  if (lane == 0) ring[0] = make_uint2(r, c);
+  int lr = 0, lc = 0;
+  bool fresh = false;  // the window was staged for the current cell
+  stage();
+  lr = (int)r - wr;
+  lc = (int)c - wc;
+  fresh = true;
+  uint32_t n = 1;
+  while (n < limit) {
+    int dr, dc;
+    for (;;) {
+      const int e = lr * kPW + (lc >> 5), b = lc & 31;
+      if (METHOD == 1) {
+        const uint4 q = tab[e];
+        const uint32_t dp = q.x >> b, dm = q.y >> b, cp = q.z >> b, cm = q.w >> b;
+        dr = (int)(dp & 1u) - (int)(dm & 1u);
+        dc = (int)(cp & 1u) - (int)(cm & 1u);
+        if ((dp | dm | cp | cm) & 1u) break;
+      } else {
+        const uint4 q0 = tab[2 * e], q1 = tab[2 * e + 1];
+        uint32_t mask = ((q0.x >> b) & 1u) | ((q0.y >> b) & 1u) << 1 | ((q0.z >> b) & 1u) << 2 |
+                        ((q0.w >> b) & 1u) << 3 | ((q1.x >> b) & 1u) << 4 | ((q1.y >> b) & 1u) << 5 |
+                        ((q1.z >> b) & 1u) << 6 | ((q1.w >> b) & 1u) << 7;
+        if (mask) {
+          const int cnt = __popc(mask);
+          int pick = 0;
+          if (cnt >= 2) pick = (int)__umul64hi(splitmix64(rng), (uint64_t)cnt);
+          for (int j = 0; j < pick; ++j) mask &= mask - 1;
+          const int k = __ffs(mask) - 1;
+          dr = (int)((PR >> (2 * k)) & 3u) - 1;
+          dc = (int)((PC >> (2 * k)) & 3u) - 1;
+          break;
+        }
+      }
+      if (fresh) {  // staged around this cell and still no move: no ascending neighbour
+        *st = ST_EINTERNAL;
+        return 0;
+      }
+      stage();
+      lr = (int)r - wr;
+      lc = (int)c - wc;
+      fresh = true;
+    }
+    fresh = false;
+    ldr = dr;
+    ldc = dc;
+    r = (uint32_t)((int)r + dr);
+    c = (uint32_t)((int)c + dc);
+    lr += dr;
+    lc += dc;
+    if (lane == 0) ring[n & 31] = make_uint2(r, c);
+    ++n;
+    if ((n & 31) == 0) flush(n);
+  }
+  if (n & 31) flush(n);
+  if (!rd.source(r, c)) *st = ST_EINTERNAL;  // the point count is exact on a law-abiding map
+  return n;
+}
+
 // Encoded maps: closed-form count L+2-A(t).  Plain maps: a counting walk.
 __global__ void k_path_counts(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method,
                               uint64_t seed, uint64_t* __restrict__ counts, int32_t* __restrict__ status) {
@@ -416,7 +604,13 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
   int32_t st = ST_OK;
   __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
   uint8_t* win = wins[(threadIdx.x >> 5) & 3];
-  const uint64_t got = AM_TRACE_2STEP && method == 1 && m.cell_bits == 16
+  const bool planes = AM_TRACE_PLANES && m.bt && m.cell_bits == 16 && !m.dir;
+  uint2* ring = reinterpret_cast<uint2*>(win + kPTab);
+  const uint64_t got = planes ? (method == 1 ? walk_planes<1>(rd, tgt[2 * w], tgt[2 * w + 1], seed, (uint32_t)limit,
+                                                              pts + 2 * off, &st, reinterpret_cast<uint4*>(win), ring)
+                                             : walk_planes<0>(rd, tgt[2 * w], tgt[2 * w + 1], seed, (uint32_t)limit,
+                                                              pts + 2 * off, &st, reinterpret_cast<uint4*>(win), ring))
+                       : AM_TRACE_2STEP && method == 1 && m.cell_bits == 16
                            ? walk_eucl2<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], limit, pts + 2 * off,
                                                                   &st, (uint16_t*)win)
                        : m.cell_bits == 16 ? walk_smem<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], method, seed,
