@@ -543,7 +543,6 @@ def run_configs(am, torch, ctx, info_c4, occ4, src4, hops4, parity):
     out = []
     O = load_oracle()[0] if parity else None
     h_pts = torch.empty((8 << 20, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    tile_cells = info_c4["tile_rows"] * info_c4["tile_cols"] * LAYERS_PER_BLOCK
 
     def grid_cfg(name, occ, src, tgt, cap, fixed=None, hops=None):
         hh, ww = occ.shape
@@ -561,7 +560,8 @@ def run_configs(am, torch, ctx, info_c4, occ4, src4, hops4, parity):
              "time_to_solve_s": round(t, 5), "layers_used": r.layers_used,
              "termination": ["filled", "stalled", "cap", "fixed"][r.cause if not fixed else 3],
              "dense_equivalent_gcell_per_s": round(ww * hh * L / t / 1e9, 1),
-             "executed_gcell_per_s": round(r.tiles_processed * tile_cells / t / 1e9, 1) if r.tiles_total else None,
+             "executed_gcell_per_s": round(r.cells_executed / t / 1e9, 1) if r.tiles_total else None,
+             "engine": r.engine,
              "paths_covered": int((st == 0).sum())}
         if parity:
             p, _ = check_grid(O, occ, src, g.activity(), L, None if fixed else cap, tgt, off, pts, st, PARITY_PATHS,
@@ -665,13 +665,14 @@ def run_b200(args, rank, world, local_rank):
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall0 = time.time()
     t_start.record(stream)
-    stencil_ms, blocks, res, tiles_done, tiles_all = 0.0, 0, None, 0, 0
+    stencil_ms, blocks, res, tiles_done, tiles_all, executed = 0.0, 0, None, 0, 0, 0
     for _ in range(args.steps):
         res = sol.step()
         stencil_ms += res.stencil_ms
         blocks += res.block_launches
         tiles_done += res.tiles_processed
         tiles_all += res.tiles_total
+        executed += res.cells_executed
     t_end.record(stream)
     ctx.synchronize()
     torch.cuda.synchronize()
@@ -699,12 +700,13 @@ def run_b200(args, rank, world, local_rank):
     per_launch_ms = stencil_ms / max(blocks, 1)
     tile_mode = tiles_all > 0
     info = sol.grid().info()
-    if tile_mode:
-        cells_per_launch = tiles_done * info["tile_rows"] * info["tile_cols"] * LAYERS_PER_BLOCK / max(blocks, 1)
-        kernel = "am::k_block_tiles<16>"
-    else:
-        cells_per_launch = W * rows_here * LAYERS_PER_BLOCK
-        kernel = "am::k_block<16>"
+    # executed cell-updates of the blocked launches (processed tiles x tile cells x layers per launch), counted
+    # by the library; the engine names the kernel that ran them
+    cells_per_launch = executed / max(blocks, 1)
+    kernel = {"bits": "am::k_bits_tiles<false>", "tiles": "am::k_block_tiles<16>",
+              "dense": "am::k_block<16>"}.get(res.engine, res.engine)
+    tile_geom = {"bits": "32 rows x 128 cols (1-bit planes)"}.get(res.engine,
+                                                                  f"{info['tile_rows']} rows x {info['tile_cols']} cols")
     alg_bytes = BYTES_PER_CELL_UPDATE * cells_per_launch
     achieved = alg_bytes / (per_launch_ms / 1000) / 1e9
     stencil_gcells = cells_per_launch / (per_launch_ms / 1000) / 1e9
@@ -798,17 +800,19 @@ def run_b200(args, rank, world, local_rank):
             "stencil_gcell_per_s": round(stencil_gcells, 2),
             "propagate_gcell_per_s": round(cell_updates / (prop_ms / 1000) / 1e9, 1),
             "cell_updates": {"dense_equivalent_per_step": int(cell_updates),
-                             "executed_per_step": int(tiles_done // args.steps * info["tile_rows"] * info["tile_cols"]
-                                                      * LAYERS_PER_BLOCK) if tiles_all else int(cell_updates)},
+                             "executed_per_step": int(executed // args.steps)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 3), "traffic": ncu_traffic("tiles" if tile_mode else "dense"),
+                         "frac": round(achieved / peak, 3), "traffic": ncu_traffic(res.engine),
                          "kernel": kernel, "algorithmic_bytes_per_launch": int(alg_bytes),
                          "mean_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src,
-                         "note": "9 B per cell-update (reference uint32 layout) x executed cell-updates per launch "
-                                 "(8 layers); traffic = ncu dram read+write per launch (profiles/)"},
+                         "layers_per_launch": res.block_layers,
+                         "note": "9 B per cell-update (reference uint32 layout, SURVEY 8d) x executed cell-updates "
+                                 "per launch (processed tiles x tile cells x layers per launch); traffic = ncu dram "
+                                 "read+write per launch (profiles/)"},
             "active_tiles": ({"processed": tiles_done // args.steps, "dense_equivalent": tiles_all // args.steps,
                               "fraction": round(tiles_done / max(tiles_all, 1), 4),
-                              "tile": f"{info['tile_rows']} rows x {info['tile_cols']} cols"} if tile_mode else None),
+                              "tile": tile_geom} if tile_mode else None),
+            "engine": res.engine,
             "dense_stencil": dense,
             "gpu_launches": int(launches),
             "clocks": clk,

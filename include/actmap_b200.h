@@ -64,7 +64,13 @@ typedef struct am_prop_result {
   double stencil_ms;        /* summed CUDA-event time of the block launches (AM_CTX_TIMING) */
   uint64_t tiles_processed; /* tile-blocks computed with active-tile skipping (0 in dense mode) */
   uint64_t tiles_total;     /* tiles per grid x blocks: the dense-equivalent tile-blocks */
+  uint64_t cells_executed;  /* cell-updates the blocked launches computed (processed tiles x tile cells x layers) */
+  uint32_t engine;          /* AM_ENGINE_*: which blocked kernel ran the bulk of the layers */
+  uint32_t block_layers;    /* layers per blocked launch of that kernel */
 } am_prop_result;
+
+/* am_prop_result.engine */
+enum { AM_ENGINE_DENSE = 0, AM_ENGINE_TILES = 1, AM_ENGINE_BITS = 2, AM_ENGINE_BATCH = 3 };
 
 typedef struct am_grid_info {
   uint32_t width, height, pitch, rows, bands, segments, seg_len, halo;

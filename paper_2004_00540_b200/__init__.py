@@ -57,7 +57,8 @@ class ParseError(InvalidInputError):
 class _PropResult(C.Structure):
     _fields_ = [("layers_used", C.c_uint32), ("cause", C.c_uint32), ("layers_computed", C.c_uint32),
                 ("cell_bits", C.c_uint32), ("block_launches", C.c_uint64), ("layer_launches", C.c_uint64),
-                ("stencil_ms", C.c_double), ("tiles_processed", C.c_uint64), ("tiles_total", C.c_uint64)]
+                ("stencil_ms", C.c_double), ("tiles_processed", C.c_uint64), ("tiles_total", C.c_uint64),
+                ("cells_executed", C.c_uint64), ("engine", C.c_uint32), ("block_layers", C.c_uint32)]
 
 
 class _GridInfo(C.Structure):
@@ -302,6 +303,9 @@ class PropResult:
         self.stencil_ms = r.stencil_ms
         self.tiles_processed = r.tiles_processed
         self.tiles_total = r.tiles_total
+        self.cells_executed = r.cells_executed
+        self.engine = ("dense", "tiles", "bits", "batch")[r.engine] if r.engine < 4 else str(r.engine)
+        self.block_layers = r.block_layers
 
 
 class Grid:

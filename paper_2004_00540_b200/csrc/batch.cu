@@ -523,8 +523,12 @@ am_status wave_propagate(am_ctx* ctx, am_batch* b, uint32_t layers, uint32_t aut
   g->have_map = 1;
   g->bits_map = 0;
   uint32_t maxl = 0;
-  for (uint32_t u : b->layers_used) maxl = std::max(maxl, u);
+  uint64_t sum_used = 0;
+  for (uint32_t u : b->layers_used) maxl = std::max(maxl, u), sum_used += u;
   *r = am_prop_result{};
+  r->cells_executed = sum_used * (uint64_t)b->mw * b->mh;  // every maze's cells x its own layers (on chip)
+  r->engine = AM_ENGINE_BATCH;
+  r->block_layers = 0;  // one launch runs every maze to its fixed point
   r->layers_used = maxl;
   r->cause = layers ? AM_STOP_FIXED : AM_STOP_CAP;
   r->layers_computed = maxl;

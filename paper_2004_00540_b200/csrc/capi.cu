@@ -570,6 +570,9 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   r.cell_bits = 16;
   r.tiles_processed = stat[0];
   r.tiles_total = (uint64_t)nt * r.block_launches;
+  r.cells_executed = stat[0] * (uint64_t)(kBTR * kBTW * 32) * kBK;
+  r.engine = AM_ENGINE_BITS;
+  r.block_layers = kBK;
   if (res) *res = r;
   return AM_OK;
 }
@@ -956,8 +959,23 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   r.cause = cause;
   r.layers_computed = l;
   r.cell_bits = slabs[0].g->cell_bits;
+  if (tiles) {
+    r.cells_executed = r.tiles_processed * (uint64_t)(kTileRows * kTileCols) * kK;
+    r.engine = AM_ENGINE_TILES;
+  } else {
+    uint64_t cells = 0;
+    for (auto& sr : slabs) cells += (uint64_t)sr.g->g.W * sr.g->g.H;  // owned rows of each slab
+    r.cells_executed = cells * kK * (r.block_launches / slabs.size());
+    r.engine = AM_ENGINE_DENSE;
+  }
+  r.block_layers = kK;
+  if (pre.block_launches) {  // a bit-plane run did the layers up to the handoff
+    r.engine = pre.engine;
+    r.block_layers = pre.block_layers;
+  }
   r.block_launches += pre.block_launches;
   r.tiles_processed += pre.tiles_processed;
+  r.cells_executed += pre.cells_executed;
   if (res) *res = r;
   return AM_OK;
 }
