@@ -24,6 +24,8 @@ struct BitState {
   BitBook bk{};
   int ctas = 0;
   uint32_t* own_t = nullptr;  // time planes when the second field is too small for them
+  uint64_t free_cells = 0;    // free cells of the grid (counted when the free plane is built)
+  bool planes_ready = false;  // the free plane of the grid's occupancy is built (once per grid)
 };
 void peer_destroy(PeerLink* p);
 // Host side of a grid's fixed-point slots: pinned device-mapped mirror + one
@@ -194,6 +196,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
                            const uint8_t* occ_full, const uint32_t* src, uint64_t n_src, bool device_ptrs,
                            bool slab, am_grid** out);
 am_status set_cell_bits(am_ctx* ctx, am_grid* g, int cell_bits);
+am_status bits_alloc(am_ctx* ctx, am_grid* g);  // bit-plane state + the grid's free plane (capi.cu)
 
 }  // namespace am
 

@@ -195,6 +195,11 @@ constexpr int kBK = AM_BK;
 constexpr int kBRPL = AM_BRPL;
 constexpr int kBTW = 4;
 constexpr int kBTR = 32 * kBRPL - 2 * kBK;
+// time planes: bit k < kBTPlanes of t - 1 per cell (t = the layer a cell was covered at); word slots
+// kBTPlanes .. 15 of a row word's 16 are unused during the run (k_bits_finalize puts covered / free there)
+constexpr int kBTPlanes = 14;
+constexpr uint32_t kBTSrcU = (1u << kBTPlanes) - 1u;     // sources' t - 1 (== -1 mod 2^kBTPlanes)
+constexpr uint32_t kBitsMaxRef = (1u << kBTPlanes) - 2u;  // layers a bit-plane run represents (16382)
 struct BitGeo {
   uint32_t W, H;
   uint32_t nchunks, tbands;  // tile rows / tile columns
@@ -206,9 +211,11 @@ struct BitGeo {
 BitGeo make_bit_geo(uint32_t W, uint32_t H);
 // Device state of a bit-plane run.  State words and lists work as in TileBook
 // (state = old << 32 | cur, cur = (index + 1 of the block that last processed the
-// tile) << 1 | home plane; lists / counts by block parity / block mod 3).
+// tile) << 1 | home plane; lists / counts by block parity / block mod 3).  cur = 0: no block of this run
+// has processed the tile and it holds no source, so its coverage words are stale and read as empty (runs
+// reset only the states, never the planes).
 struct BitBook {
-  uint4* P;                    // plane words {covered (home 0), covered (home 1), free, -}
+  uint4* P;                    // plane words {covered (home 0), covered (home 1), free, -}; free is built once per grid
   uint32_t* T;                 // time planes: 16 words per plane word (bit k of t - 1 of its 32 cells)
   unsigned long long* state;
   uint32_t* sched;
@@ -245,7 +252,7 @@ struct MapView {
   uint32_t layers;        // layers represented by the values (for point counts)
   const SlabDir* dir = nullptr;  // encoded maps only: the field is distributed over row slabs (val unused)
   // maps of a bit-plane run (bits.cu) whose planes are intact: the walkers read coverage + time planes
-  const uint4* bp = nullptr;                 // {covered, u bit 0, u bit 1, free} per plane word (after k_bits_finalize)
+  const uint4* bp = nullptr;                 // {covered, u bit 0, free, u bit 1} per plane word (after k_bits_finalize)
   const uint32_t* bt = nullptr;              // time planes, 16 words per plane word
   const unsigned long long* bstate = nullptr;  // tile states (home plane)
   BitGeo bg{};

@@ -45,6 +45,9 @@ constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
 constexpr int kBThreads = 128;
+#ifndef AM_BITS_NOT
+#define AM_BITS_NOT 0  // experiment only (wrong maps): no time-plane staging / updates
+#endif
 
 __constant__ uint8_t kBFacing[3][3] = {{8, 2, 7}, {4, 0, 3}, {6, 1, 5}};
 
@@ -84,8 +87,11 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 // One kBK-layer block over the listed tiles.  nl (<= kBK) layers are applied
 // (the last block of a fixed-L or capped run may be partial).
+#ifndef AM_BITS_MINB
+#define AM_BITS_MINB 4
+#endif
 template <bool PART>
-__global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook bk, uint32_t blk, uint32_t nl,
+__global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo bg, BitBook bk, uint32_t blk, uint32_t nl,
                                                           FlagSink flag, FlagSink prev) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
     if (!light && lane == 0)  // inline PTX: the compiler's warp aggregation would consume the result here
       asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(fa) : "l"(bk.count + 3 + blk % 3) : "memory");
     __syncwarp();  // the previous item's reads of tsm are done
-    {
+    if (!AM_BITS_NOT) {
       const uint4* tg = reinterpret_cast<const uint4*>(bk.T) + ((size_t)tc * kBTR * bg.wpr + (size_t)tb * kBTW) * 4;
 #pragma unroll
       for (int q = 0; q < kBTR * kBTW * 4 / 32; ++q) {
@@ -159,7 +165,10 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
         C[i][x] = v.x, C1[i][x] = v.y, F[i][x] = v.z;
       }
     }
+    // a state of 0 is a tile no block of this run has processed (and no source tile): its coverage words
+    // are stale (a previous run's, or the walkers' layout) and read as empty
     const uint32_t hom = __ballot_sync(0xffffffffu, s9 & 1u);
+    const uint32_t vld = __ballot_sync(0xffffffffu, s9 != 0u);
     const uint32_t sown = __shfl_sync(0xffffffffu, s9, 4);
 #pragma unroll
     for (int i = 0; i < kBRPL; ++i) {
@@ -168,7 +177,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
 #pragma unroll
       for (int x = 0; x < kBNW; ++x) {
         const int q = x == 0 ? 0 : (x == kBNW - 1 ? 2 : 1);
-        if ((hom >> (d * 3 + q)) & 1u) C[i][x] = C1[i][x];
+        const uint32_t b = d * 3 + q;
+        C[i][x] = !((vld >> b) & 1u) ? 0u : ((hom >> b) & 1u) ? C1[i][x] : C[i][x];
       }
     }
     // ---- kBK layers.  J[k]: bit k of the in-block index (layer - 1) of the cells covered in this block,
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
 #pragma unroll
     for (int i = 0; i < kBRPL; ++i) {
       const int tr = lane * kBRPL + i - kBK;
-      if (tr < 0 || tr >= kBTR) continue;
+      if (AM_BITS_NOT || tr < 0 || tr >= kBTR) continue;
       const size_t rw = (size_t)(tc * kBTR + (uint32_t)tr) * bg.wpr + (size_t)tb * kBTW;
 #pragma unroll
       for (int x = 0; x < kBTW; ++x) {
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(kBThreads, 4) k_bits_tiles(BitGeo bg, BitBook 
           v[4 * q] = a4.x, v[4 * q + 1] = a4.y, v[4 * q + 2] = a4.z, v[4 * q + 3] = a4.w;
         }
 #pragma unroll
-        for (int k = 0; k < 15; ++k) {
+        for (int k = 0; k < kBTPlanes; ++k) {
           const uint32_t bitv = k < kBNJ ? J[k < kBNJ ? k : 0][i][x] : (((blk >> (k - kBNJ)) & 1u) ? nw : 0u);
           v[k] = (v[k] & ~nw) | bitv;
         }
@@ -380,8 +390,24 @@ __global__ void k_bits_init(BitGeo bg, const uint8_t* __restrict__ occ, uint4* _
   if (lane == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
 }
 
-// Sources (validated free cells): covered at layer 0, time-plane value 0x7FFF (no covered cell has
-// t - 1 = 0x7FFF: t <= lref <= 32766), and block 0's work list (the 3x3 tile neighbourhood of each
+// The tiles holding a source start the run with valid coverage in home plane 0: their plane-0 words are
+// cleared here (before k_bits_sources sets the source bits) and their state set to kBitsSrcState.  One
+// warp per source; lane k clears rows k, k + 32, ... of the tile's kBTW words.
+constexpr uint32_t kBitsSrcState = 0xFFFFFFFEu;  // home 0, mark 0x7FFFFFFF (no block's mark), nonzero
+__global__ void k_bits_src_clear(BitGeo bg, const uint32_t* __restrict__ rc, uint64_t n, BitBook bk) {
+  const uint64_t s = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (s >= n) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const uint32_t tc = rc[2 * s] / kBTR, tb = rc[2 * s + 1] / (32 * kBTW);
+  for (int i = lane; i < kBTR * kBTW; i += 32) {
+    const uint32_t row = tc * kBTR + (uint32_t)i / kBTW, wd = tb * kBTW + (uint32_t)i % kBTW;
+    if (row < bg.rows) bk.P[(size_t)row * bg.wpr + wd].x = 0u;
+  }
+  if (lane == 0) bk.state[tc * bg.tbands + tb] = kBitsSrcState;
+}
+
+// Sources (validated free cells): covered at layer 0, time-plane value kBTSrcU (no covered cell has
+// t - 1 = kBTSrcU: t <= lref <= kBitsMaxRef), and block 0's work list (the 3x3 tile neighbourhood of each
 // source's tile, pushed as block "-1").  One warp per source.
 __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint64_t n, BitBook bk) {
   const uint64_t s = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
@@ -394,68 +420,79 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
     const uint32_t old = atomicOr(&bk.P[rw].x, bit);
     if (!(old & bit)) atomicAdd(&bk.stat[1], 1ull);
   }
-  if (lane < 15) atomicOr(bk.T + rw * 16 + lane, bit);
+  if (lane < kBTPlanes) atomicOr(bk.T + rw * 16 + lane, bit);
   const int tc = (int)(r / kBTR), tb = (int)(c / (32 * kBTW));
   bit_push(bg, bk, 0xFFFFFFFFu, lane < 9, tc + lane / 3 - 1, tb + lane % 3 - 1);
 }
 
 // The encoded field (am_internal.cuh) from the planes, once per run: free covered cell flag | (lref - u)
-// (and the plane words rewritten for the path walkers as {covered, u bit 0, u bit 1, free})
-// with u = t - 1 from the time planes (lref + 1 at sources, u = 0x7FFF), free uncovered flag | 0,
-// obstacle 0.  A warp converts two row words per step: lane k < 16 loads time-plane word k of the first,
-// lanes 16-31 those of the second (128 B, coalesced), a 32 x 32 bit transpose over the lanes (five
-// butterfly shuffles) leaves lane c with both cells' u as a u16x2 pair, and two coalesced 64 B stores
-// follow.
+// with u = t - 1 from the time planes (lref + 1 at sources: u = kBTSrcU == -1 mod 2^kBTPlanes), free
+// uncovered flag | 0, obstacle 0; and the plane words rewritten for the path walkers as {covered, u bit 0,
+// free, u bit 1} (the free plane stays where the next run reads it).  A warp converts two row words per
+// step: lane k of half h (lanes 16h .. 16h+15) holds plane word k of row word wb + 2q + h -- time planes
+// 0 .. kBTPlanes-1, then the covered word (the tile's home plane, or 0 in a tile no block processed) and
+// the free word -- and a 32 x 32 bit transpose over the lanes (five butterfly shuffles) leaves lane c
+// with cell c of both row words as a u16x2 {free, covered, u} pair: the encoding is then a handful of
+// word-wide ops, and two coalesced 64 B stores follow.
 __global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uint16_t* __restrict__ field) {
   constexpr int P = 4;  // row-word pairs per warp step (loads of all of them in flight together)
+  constexpr uint32_t kUMask = (1u << kBTPlanes) - 1u, kU2 = kUMask | kUMask << 16;
+  static_assert(kBTPlanes == 14, "planes 14 / 15 of a row word carry covered / free");
   const int lane = threadIdx.x & 31;
+  const int k = lane & 15;
   const uint32_t groups = (bg.wpr / 2 + P - 1) / P;
   const uint32_t total = bg.H * groups;  // < 2^32: H, W <= 65535
-  const uint32_t L2 = lref | lref << 16, S2 = (lref + 1) | (lref + 1) << 16;
+  // per half: (lref + 2^kBTPlanes) - u >= 0, no borrow across the halves; the low kBTPlanes bits are
+  // (lref - u) mod 2^kBTPlanes, which is lref + 1 at sources
+  const uint32_t K2 = (lref + (1u << kBTPlanes)) * 0x00010001u;
   const uint32_t nw = gridDim.x * (blockDim.x / 32);
   for (uint32_t p = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < total; p += nw) {
     const uint32_t row = p / groups, wb = 2 * P * (p - row * groups);
     const size_t rb = (size_t)row * bg.wpr;
-    // lanes 0 .. 2P-1: the free / covered words of the group (covered from the tile's home plane)
+    // lanes 0 .. 2P-1: the covered (the tile's home plane; nothing in a tile no block processed) and free
+    // words of the group's row words, and the walkers' plane word
     uint32_t fv = 0, cv = 0;
     const uint32_t wl = wb + lane;
     if (lane < 2 * P && wl < bg.wpr) {
       const uint4 pv = __ldcg(bk.P + rb + wl);
-      const uint32_t home = (uint32_t)__ldcg(bk.state + (row / kBTR) * bg.tbands + wl / kBTW) & 1u;
+      const uint32_t st = (uint32_t)__ldcg(bk.state + (row / kBTR) * bg.tbands + wl / kBTW);
       const uint2 t01 = __ldcg(reinterpret_cast<const uint2*>(bk.T + (rb + wl) * 16));
       fv = pv.z;
-      cv = home ? pv.y : pv.x;
-      // the walkers' plane word from now on: {covered, u bit 0, u bit 1, free} (the next run re-initialises P)
-      __stcg(bk.P + rb + wl, make_uint4(cv, t01.x, t01.y, fv));
+      cv = st == 0u ? 0u : (st & 1u) ? pv.y : pv.x;
+      __stcg(bk.P + rb + wl, make_uint4(cv, t01.x, fv, t01.y));  // {covered, u bit 0, free, u bit 1}
     }
-    uint32_t x[P];
+    uint32_t x[P];  // lanes 16 .. 31 read the next row word's planes (wpr is even)
 #pragma unroll
     for (int q = 0; q < P; ++q) x[q] = wb + 2 * q < bg.wpr ? __ldcs(bk.T + (rb + wb + 2 * q) * 16 + lane) : 0u;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const int from = 2 * q + (lane >> 4);
+      const uint32_t c = __shfl_sync(0xffffffffu, cv, from), f = __shfl_sync(0xffffffffu, fv, from);
+      x[q] = k == kBTPlanes ? c : k == kBTPlanes + 1 ? f : x[q];
+    }
 #pragma unroll
     for (int j = 16; j >= 1; j >>= 1) {
       const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
                                                                                                     : 0x55555555u;
       // lanes with bit j set keep the bits of columns with bit j set and take the partner's, moved down by
-      // j; the others keep / take the complementary columns, moved up (a rotation: the moved-out bits are 0)
+      // j; the others keep / take the complementary columns, moved up: the rotated partner word supplies
+      // exactly the ~keep columns, so one bit-select merges them
       const uint32_t keep = (lane & j) ? ~m : m;
       const uint32_t rot = (lane & j) ? j : 32 - j;
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x[q], j) & keep;
-        x[q] = (x[q] & keep) | __funnelshift_r(y, y, rot);
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x[q], j);
+        const uint32_t r = __funnelshift_r(y, y, rot);
+        x[q] = (x[q] & keep) | (r & ~keep);
       }
     }
     uint16_t* dst = field + (size_t)(row + g.pad) * g.pitch + g.pad + (size_t)wb * 32 + lane;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      const uint32_t f0 = __shfl_sync(0xffffffffu, fv, 2 * q), f1 = __shfl_sync(0xffffffffu, fv, 2 * q + 1);
-      const uint32_t c0 = __shfl_sync(0xffffffffu, cv, 2 * q), c1 = __shfl_sync(0xffffffffu, cv, 2 * q + 1);
-      const uint32_t u = x[q] & 0x7FFF7FFFu;
-      const uint32_t src = __vcmpeq2(u, 0x7FFF7FFFu);
-      const uint32_t fm = (((f0 >> lane) & 1u) ? 0x0000FFFFu : 0u) | (((f1 >> lane) & 1u) ? 0xFFFF0000u : 0u);
-      const uint32_t cm = (((c0 >> lane) & 1u) ? 0x0000FFFFu : 0u) | (((c1 >> lane) & 1u) ? 0xFFFF0000u : 0u);
-      const uint32_t a = (__vsub2(L2, u) & ~src) | (S2 & src);
-      const uint32_t v = ((a & cm) | 0x80008000u) & fm;
+      const uint32_t v0 = x[q];                                      // per half: free | covered | u
+      const uint32_t a = K2 - (v0 & kU2);                            // per half: low bits (lref - u) mod 2^14
+      const uint32_t cm = ((v0 >> kBTPlanes) & 0x00010001u) * kUMask;  // per half: kUMask if covered
+      const uint32_t v = (a & cm) | (v0 & 0x80008000u);              // covered implies free
       const uint32_t col = (wb + 2 * q) * 32 + lane;
       if (col < bg.W) dst[64 * q] = (uint16_t)(v & 0xFFFFu);
       if (col + 32 < bg.W) dst[64 * q + 32] = (uint16_t)(v >> 16);
@@ -478,6 +515,7 @@ void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStre
 
 void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBook bk, cudaStream_t s) {
   if (!n) return;
+  k_bits_src_clear<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(bg, rc, n, bk);
   k_bits_sources<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(bg, rc, n, bk);
 }
 

@@ -269,6 +269,8 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   } else if (h_err) {
     st = fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle (grid.hpp:78)");
   }
+  // single grids: the free plane of the bit-plane engine is part of the grid's device form (built once)
+  if (!st && !slab && !(ctx->flags & AM_CTX_DENSE)) st = bits_alloc(ctx, g);
   if (st) {
     grid_free(ctx, g);
     return st;
@@ -417,15 +419,32 @@ static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
 }
 
 // Bit-plane propagation of a single grid (bits.cu).  The field is
-// written once per cell, relative to lref = min(target, 32766) layers, so the map
+// written once per cell, relative to lref = min(target, kBitsMaxRef = 16382) layers, so the map
 // needs no decode: computed = lref, layers_used = the outcome, rollback = lref - used.
 // Auto runs that have not reached their fixed point by lref (beyond the 16-bit
 // range) return handoff = true with the field exactly at layer lref; the caller
 // continues there with the 16/32-bit tile kernels.
-constexpr uint32_t kBitsMaxRef = 32766u;
 
-static am_status bits_alloc(am_ctx* ctx, am_grid* g) {
-  if (g->bits) return AM_OK;
+static am_status bits_build_planes(am_ctx* ctx, am_grid* g) {
+  BitState& B = *g->bits;
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemsetAsync(B.bk.stat, 0, 3 * 8, s));
+  launch_bits_init(B.bg, g->occ, B.bk, s);
+  CKL();
+  ++ctx->launches;
+  unsigned long long fc = 0;
+  CK(cudaMemcpyAsync(&fc, B.bk.stat + 2, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  B.free_cells = fc;
+  B.planes_ready = true;
+  return AM_OK;
+}
+
+// Allocates the bit-plane state and builds the free plane from the grid's occupancy (occupancy is
+// immutable, so this runs once per grid: at creation for single grids, else on first use).
+am_status bits_alloc(am_ctx* ctx, am_grid* g) {
+  if (g->bits && g->bits->planes_ready) return AM_OK;
+  if (g->bits) return bits_build_planes(ctx, g);
   auto* b = new (std::nothrow) BitState();
   if (!b) return fail(ctx, AM_EOOM, "bit state");
   g->bits = b;
@@ -440,7 +459,7 @@ static am_status bits_alloc(am_ctx* ctx, am_grid* g) {
   CK(am::dmalloc(ctx, &k.count, 6 * 4));
   CK(am::dmalloc(ctx, &k.stat, 3 * 8));
   b->ctas = ctx->sms * bits_ctas_per_sm();
-  return AM_OK;
+  return bits_build_planes(ctx, g);
 }
 
 static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom, am_prop_result* res,
@@ -467,9 +486,8 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   CK(cudaMemsetAsync(B.bk.state, 0, nt * 8, s));
   CK(cudaMemsetAsync(B.bk.sched, 0, nt * 4, s));
   CK(cudaMemsetAsync(B.bk.count, 0, 6 * 4, s));
-  CK(cudaMemsetAsync(B.bk.stat, 0, 3 * 8, s));
-  launch_bits_init(bg, g->occ, B.bk, s);
-  CKL();
+  CK(cudaMemsetAsync(B.bk.stat, 0, 2 * 8, s));
+  // the planes are not reset: the cleared states mark every tile's coverage stale (bits.cu)
   launch_bits_sources(bg, g->src_rc, g->n_src, B.bk, s);
   CKL();
   ctx->launches += 2;
@@ -541,7 +559,7 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   unsigned long long stat[3] = {0, 0, 0};
   CK(cudaMemcpyAsync(stat, B.bk.stat, sizeof stat, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  const bool any_zero = stat[1] < stat[2];
+  const bool any_zero = stat[1] < B.free_cells;
   uint32_t used = l, cause = AM_STOP_FIXED;
   if (autom) {
     if (lprime) {

@@ -382,11 +382,11 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
 }
 
 // Walk on the planes of a bit-plane run (bits.cu): coverage C and the two low bits of u = t - 1 (the
-// layer a cell was covered at, minus one; sources 0x7FFF == -1 mod 4).  On a propagated map an
+// layer a cell was covered at, minus one; sources kBTSrcU == -1 mod 4).  On a propagated map an
 // 8-neighbour n is an ascent candidate of c (activity + 1) exactly when both are covered and
 // u_c - u_n == 1 (activities of covered 8-neighbours differ by <= 1, activity = lref - u), and mod 4 that
 // is two LOP3s per 32 cells: (a0 ^ b0) & ~(a1 ^ b1 ^ b0) with a = u_c, b = u_n.  A warp stages a 64 x 64
-// window (two rows of two words per lane, one 16 B plane word {covered, u bit 0, u bit 1, free} each, as
+// window (two rows of two words per lane, one 16 B plane word {covered, u bit 0, free, u bit 1} each, as
 // k_bits_finalize leaves them),
 // builds every cell's candidates for all 8 directions with shifts and shuffles of whole words and stores
 // one 16 B record per word in shared memory.  Euclidean rule (pin P1): the first candidate of L, R, U, D,
@@ -419,10 +419,10 @@ __device__ __noinline__ void stage_planes(const MapView& m, uint32_t r, uint32_t
       const int gr = wr + 2 * lane + i, gw = (wc >> 5) + x;
       X[i][x] = A0[i][x] = A1[i][x] = 0u;
       if (gr >= 0 && gr < (int)bg.H && gw >= 0 && gw < (int)bg.wpr) {  // planes are read-only here: L1
-        const uint4 p = __ldg(m.bp + (size_t)gr * bg.wpr + gw);  // {covered, u bit 0, u bit 1, free}
+        const uint4 p = __ldg(m.bp + (size_t)gr * bg.wpr + gw);  // {covered, u bit 0, free, u bit 1}
         X[i][x] = p.x;
         A0[i][x] = p.y;
-        A1[i][x] = p.z;
+        A1[i][x] = p.w;
       }
     }
   // rows above / below each of the lane's two rows
