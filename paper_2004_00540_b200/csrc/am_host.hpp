@@ -98,6 +98,7 @@ struct am_grid {
   // scratch for path extraction
   uint32_t* d_tgt = nullptr;
   uint64_t* d_counts = nullptr;
+  uint32_t* d_sched = nullptr;  // launch_trace's longest-first scheduling (kTraceSchedWords)
   uint64_t* d_offsets = nullptr;
   int32_t* d_status = nullptr;
   uint64_t tgt_cap = 0;

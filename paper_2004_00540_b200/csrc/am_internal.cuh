@@ -272,7 +272,9 @@ void launch_path_counts(const MapView& m, const uint32_t* tgt_rc, uint64_t n, in
 void launch_scan(const uint64_t* counts, uint64_t n, uint64_t* offsets, cudaStream_t s);
 void launch_trace(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int method, uint64_t seed,
                   const uint64_t* offsets, uint32_t* pts_rc, int32_t* status, cudaStream_t s,
-                  uint64_t pts_capacity = ~0ull);
+                  uint64_t pts_capacity = ~0ull, uint32_t* order = nullptr, uint32_t* sched = nullptr, int sms = 0);
+// scratch of launch_trace's longest-first scheduling: order (n words) and sched (this many words)
+constexpr int kTraceSchedWords = 1024 + 1;
 // paths in a grid of mazes packed on a cell_h x cell_w lattice -> each path's maze-local coordinates
 // (the maze is the one of the path's first point, its target)
 void launch_paths_local(uint32_t* pts_rc, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,

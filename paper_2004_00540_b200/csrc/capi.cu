@@ -157,6 +157,7 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->plain);
   am::dfree(ctx, g->d_tgt);
   am::dfree(ctx, g->d_counts);
+  am::dfree(ctx, g->d_sched);
   am::dfree(ctx, g->d_offsets);
   am::dfree(ctx, g->d_status);
   am::dfree(ctx, g->d_pts);
@@ -1124,6 +1125,7 @@ static am::MapView view_of(am_grid* g) {
 }
 
 static am_status ensure_targets(am_ctx* ctx, am_grid* g, uint64_t n) {
+  if (!g->d_sched) CK(am::dmalloc(ctx, &g->d_sched, am::kTraceSchedWords * sizeof(uint32_t)));
   if (n <= g->tgt_cap) return AM_OK;
   am::dfree(ctx, g->d_tgt);
   am::dfree(ctx, g->d_counts);
@@ -1237,8 +1239,9 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->d_offsets, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->d_status, status, n * 4, cudaMemcpyHostToDevice, s));
+  // the counts are consumed (offsets came from the caller): their buffer holds the trace order
   am::launch_trace(view_of(g), g->d_tgt, n, (int)method, seed, g->d_offsets, direct ? direct : g->d_pts,
-                   g->d_status, s);
+                   g->d_status, s, ~0ull, reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);
   CKL();
   if (cell_h) {
     am::launch_paths_local(g->d_pts, g->d_offsets, g->d_status, n, cell_h, cell_w, s);
@@ -1284,7 +1287,9 @@ am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, 
   CKL();
   am::launch_scan(g->d_counts, n, d_offsets, s);
   CKL();
-  am::launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, s, cap);  // paths past cap: AM_EINVAL
+  // paths past cap: AM_EINVAL; the counts are scanned into d_offsets, so their buffer holds the trace order
+  am::launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, s, cap,
+                   reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);
   CKL();
   return AM_OK;
 }

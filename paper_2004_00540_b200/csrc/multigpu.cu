@@ -705,7 +705,8 @@ am_status am_peer_trace_paths_device(am_ctx* ctx, am_grid* slab, const uint32_t*
     CKL();
     launch_scan(slab->d_counts, n, d_offsets, ctx->stream);
     CKL();
-    launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, ctx->stream, cap);
+    launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, ctx->stream, cap,
+                 reinterpret_cast<uint32_t*>(slab->d_counts), slab->d_sched, ctx->sms);
     CKL();
   }
   return peer_release(ctx, p);

@@ -171,7 +171,7 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
 #ifndef AM_TWC
 #define AM_TWC 32  // 16-bit window columns (smaller windows stage faster; tools/ab_trace.sh)
 #endif
-constexpr int kWinBytes = 4096 + 256;  // shared memory per warp: a window (<= 4 KB) + the plane walk's point ring
+constexpr int kWinBytes = 4096;  // shared memory per warp: a window (<= 4 KB)
 #ifndef AM_TRACE_PLANES
 #define AM_TRACE_PLANES 1  // bit-plane runs: walk on the coverage / time planes (walk_planes)
 #endif
@@ -394,18 +394,20 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
 // broadcast 16 B shared-memory read, four shifts and two subtractions; the window's border cells get no
 // move, so "no move" means re-stage (8 cells behind the cell in its direction of travel) or, right after a
 // re-stage, a map without an ascending neighbour.  Simple rule (pin P2): the 8 candidate words (two
-// records), the seeded tie-break per step.  Points go to a 32-entry shared-memory ring, flushed by the
+// records), the seeded tie-break per step.  Points are held in registers (lane k: point k mod 32), written by the
 // whole warp every 32 points.
 constexpr int kPR = 64, kPW = 2;  // plane window: rows, 32-cell words per row (two rows per lane)
 constexpr int kPTab = kPR * kPW * 2 * 16;  // window records (simple rule: two per word)
+static_assert(kPTab <= kWinBytes, "plane window records");
 
 // Stages the plane window around (r, c), 8 cells behind it in its direction of travel (ldr, ldc), and
 // builds the window records (out of line: the step loop stays short).
 template <int METHOD>
-__device__ __noinline__ void stage_planes(const MapView& m, uint32_t r, uint32_t c, int ldr, int ldc, uint4* tab,
-                                          int* wr_out, int* wc_out) {
+__device__ __noinline__ int2 stage_planes(const uint4* __restrict__ bp, uint32_t H, uint32_t wpr, uint32_t r,
+                                          uint32_t c, int ldr, int ldc, uint4* tab) {
+  // scalars by value and the origin returned in registers: a reference to the MapView would put the
+  // whole view in local memory for this out-of-line call
   const int lane = threadIdx.x & 31;
-  const BitGeo& bg = m.bg;
   const int orr = ldr < 0 ? kPR - 8 : (ldr > 0 ? 8 : kPR / 2);
   // columns: the origin is floored to a word, so the cell lands in [orc, orc + 31]
   const int orc = ldc < 0 ? 32 * kPW - 33 : (ldc > 0 ? 1 : 16 * kPW - 16);
@@ -418,8 +420,8 @@ __device__ __noinline__ void stage_planes(const MapView& m, uint32_t r, uint32_t
     for (int x = 0; x < kPW; ++x) {
       const int gr = wr + 2 * lane + i, gw = (wc >> 5) + x;
       X[i][x] = A0[i][x] = A1[i][x] = 0u;
-      if (gr >= 0 && gr < (int)bg.H && gw >= 0 && gw < (int)bg.wpr) {  // planes are read-only here: L1
-        const uint4 p = __ldg(m.bp + (size_t)gr * bg.wpr + gw);  // {covered, u bit 0, free, u bit 1}
+      if (gr >= 0 && gr < (int)H && gw >= 0 && gw < (int)wpr) {  // planes are read-only here: L1
+        const uint4 p = __ldg(bp + (size_t)gr * wpr + gw);  // {covered, u bit 0, free, u bit 1}
         X[i][x] = p.x;
         A0[i][x] = p.y;
         A1[i][x] = p.w;
@@ -486,28 +488,32 @@ __device__ __noinline__ void stage_planes(const MapView& m, uint32_t r, uint32_t
       }
     }
   __syncwarp();
-  *wr_out = wr;
-  *wc_out = wc;
+  return make_int2(wr, wc);
 }
 
 template <int METHOD>
 __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64_t seed, uint32_t limit,
-                                uint32_t* out, int32_t* st, uint4* tab, uint2* ring) {
+                                uint32_t* out, int32_t* st, uint4* tab) {
   const int lane = threadIdx.x & 31;
   const MapView& m = rd.m;
   // simple rule: direction k (row-major) -> (dr, dc), 2-bit packed (d + 1)
   constexpr uint32_t PR = 0xA940u, PC = 0x9224u;
   uint64_t rng = seed;
   int wr = 0, wc = 0, ldr = 0, ldc = 0;
-  auto stage = [&]() { stage_planes<METHOD>(m, r, c, ldr, ldc, tab, &wr, &wc); };
-  // point ring: lane 0 appends, the warp writes 32 points at a time
-  auto flush = [&](uint32_t upto) {  // points [upto & ~31, upto) are in the ring
-    __syncwarp();
-    const uint32_t base = (upto - 1) & ~31u;
-    if (base + lane < upto) reinterpret_cast<uint2*>(out)[base + lane] = ring[lane];
-    __syncwarp();
+  const uint4* const bp = m.bp;
+  const uint32_t bh = m.bg.H, bw = m.bg.wpr;
+  auto stage = [&]() {
+    const int2 o = stage_planes<METHOD>(bp, bh, bw, r, c, ldr, ldc, tab);
+    wr = o.x;
+    wc = o.y;
   };
-  if (lane == 0) ring[0] = make_uint2(r, c);
+  // points in registers: lane k holds point k mod 32 of the current group of 32 (a predicated move per
+  // step, no branch), and the warp writes a group at once
+  uint2 pt = make_uint2(r, c);
+  auto flush = [&](uint32_t upto) {  // points [(upto - 1) & ~31, upto) are held by the lanes
+    const uint32_t base = (upto - 1) & ~31u;
+    if (base + lane < upto) reinterpret_cast<uint2*>(out)[base + lane] = pt;
+  };
   int lr = 0, lc = 0;
   bool fresh = false;  // the window was staged for the current cell
   stage();
@@ -557,7 +563,7 @@ __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64
     c = (uint32_t)((int)c + dc);
     lr += dr;
     lc += dc;
-    if (lane == 0) ring[n & 31] = make_uint2(r, c);
+    pt = lane == (int)(n & 31) ? make_uint2(r, c) : pt;
     ++n;
     if ((n & 31) == 0) flush(n);
   }
@@ -589,11 +595,10 @@ __global__ void k_path_counts(MapView m, const uint32_t* __restrict__ tgt, uint6
   }
 }
 
-__global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method, uint64_t seed,
-                        const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pts,
-                        int32_t* __restrict__ status, uint64_t cap) {
-  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= n) return;
+// One target's path, by one warp.
+__device__ __forceinline__ void trace_one(const MapView& m, const uint32_t* __restrict__ tgt, uint64_t w, int method,
+                                          uint64_t seed, const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pts,
+                                          int32_t* __restrict__ status, uint64_t cap, uint8_t* win) {
   if (status[w] != ST_OK) return;
   Reader rd{m};
   const uint64_t off = offsets[w], limit = offsets[w + 1] - off;
@@ -602,14 +607,11 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
     return;
   }
   int32_t st = ST_OK;
-  __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
-  uint8_t* win = wins[(threadIdx.x >> 5) & 3];
   const bool planes = AM_TRACE_PLANES && m.bt && m.cell_bits == 16 && !m.dir;
-  uint2* ring = reinterpret_cast<uint2*>(win + kPTab);
   const uint64_t got = planes ? (method == 1 ? walk_planes<1>(rd, tgt[2 * w], tgt[2 * w + 1], seed, (uint32_t)limit,
-                                                              pts + 2 * off, &st, reinterpret_cast<uint4*>(win), ring)
+                                                              pts + 2 * off, &st, reinterpret_cast<uint4*>(win))
                                              : walk_planes<0>(rd, tgt[2 * w], tgt[2 * w + 1], seed, (uint32_t)limit,
-                                                              pts + 2 * off, &st, reinterpret_cast<uint4*>(win), ring))
+                                                              pts + 2 * off, &st, reinterpret_cast<uint4*>(win)))
                        : AM_TRACE_2STEP && method == 1 && m.cell_bits == 16
                            ? walk_eucl2<uint16_t, AM_TWR, AM_TWC>(rd, tgt[2 * w], tgt[2 * w + 1], limit, pts + 2 * off,
                                                                   &st, (uint16_t*)win)
@@ -623,6 +625,68 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
     if (st != ST_OK) status[w] = st;
     else if (got != limit) status[w] = ST_EINTERNAL;
   }
+}
+
+// order == nullptr: warp w traces target w.  Otherwise the warps take targets from order[] (longest paths
+// first, k_trace_order) through the counter *next: the walk time is set by the longest path, and every
+// warp sharing its SM sub-partition slows it down, so few warps per sub-partition with the longest paths
+// started first finish soonest (greedy longest-processing-time scheduling).
+__global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method, uint64_t seed,
+                        const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pts,
+                        int32_t* __restrict__ status, uint64_t cap, const uint32_t* __restrict__ order,
+                        uint32_t* next) {
+  __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
+  uint8_t* win = wins[(threadIdx.x >> 5) & 3];
+  if (!order) {
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    if (w < n) trace_one(m, tgt, w, method, seed, offsets, pts, status, cap, win);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(next, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= n) return;
+    trace_one(m, tgt, order[i], method, seed, offsets, pts, status, cap, win);
+    __syncwarp();
+  }
+}
+
+// Targets in order of decreasing path length (offsets[i + 1] - offsets[i], exact from the closed-form
+// counts), bucketed into kOrderBuckets length classes: a histogram, an exclusive scan and a scatter in one
+// CTA.  sched: kOrderBuckets + 1 words (the bucket cursors, then the trace counter, reset here).
+constexpr int kOrderBuckets = 1024;
+__global__ void __launch_bounds__(1024) k_trace_order(const uint64_t* __restrict__ offsets, uint64_t n,
+                                                      uint32_t* __restrict__ order, uint32_t* __restrict__ sched) {
+  __shared__ uint32_t hist[kOrderBuckets];
+  __shared__ uint64_t maxlen_s;
+  const int t = threadIdx.x;
+  for (int b = t; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
+  if (t == 0) maxlen_s = 0;
+  __syncthreads();
+  unsigned long long mx = 0;
+  for (uint64_t i = t; i < n; i += blockDim.x) mx = max(mx, (unsigned long long)(offsets[i + 1] - offsets[i]));
+  atomicMax(reinterpret_cast<unsigned long long*>(&maxlen_s), mx);
+  __syncthreads();
+  const uint64_t span = maxlen_s + 1;
+  auto bucket = [&](uint64_t i) {  // longest first
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    return kOrderBuckets - 1 - (int)(len * kOrderBuckets / span);
+  };
+  for (uint64_t i = t; i < n; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
+  __syncthreads();
+  if (t == 0) {  // 1024 buckets: a serial scan is a few microseconds
+    uint32_t acc = 0;
+    for (int b = 0; b < kOrderBuckets; ++b) {
+      const uint32_t v = hist[b];
+      hist[b] = acc;
+      acc += v;
+    }
+    sched[kOrderBuckets] = 0;
+  }
+  __syncthreads();
+  for (uint64_t i = t; i < n; i += blockDim.x) order[atomicAdd(&hist[bucket(i)], 1u)] = (uint32_t)i;
 }
 
 void launch_path_counts(const MapView& m, const uint32_t* tgt, uint64_t n, int method, uint64_t seed,
@@ -651,11 +715,22 @@ void launch_paths_local(uint32_t* pts, const uint64_t* offsets, const int32_t* s
   k_paths_local<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(pts, offsets, status, n, cell_h, cell_w);
 }
 
+#ifndef AM_TRACE_WPS
+#define AM_TRACE_WPS 2  // warps per SM sub-partition when the targets are scheduled longest-first
+#endif
 void launch_trace(const MapView& m, const uint32_t* tgt, uint64_t n, int method, uint64_t seed,
-                  const uint64_t* offsets, uint32_t* pts, int32_t* status, cudaStream_t s, uint64_t cap) {
+                  const uint64_t* offsets, uint32_t* pts, int32_t* status, cudaStream_t s, uint64_t cap,
+                  uint32_t* order, uint32_t* sched, int sms) {
   if (!n) return;
-  const unsigned blocks = (unsigned)((n * 32 + 127) / 128);
-  k_trace<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap);
+  const uint64_t blocks = (n * 32 + 127) / 128;
+  const uint64_t sched_blocks = (uint64_t)sms * AM_TRACE_WPS;  // 4 warps per CTA, one CTA per sub-partition
+  if (order && sched && sms > 0 && blocks > sched_blocks && n < (1ull << 32)) {
+    k_trace_order<<<1, 1024, 0, s>>>(offsets, n, order, sched);
+    k_trace<<<(unsigned)sched_blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap, order,
+                                                   sched + kOrderBuckets);
+    return;
+  }
+  k_trace<<<(unsigned)blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap, nullptr, nullptr);
 }
 
 }  // namespace am
