@@ -45,6 +45,12 @@ constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
 constexpr int kBThreads = 128;
+#ifndef AM_BITS_FRJ
+#define AM_BITS_FRJ 1  // the last layer's new cells from the in-block index bits (no register set in the loop)
+#endif
+#ifndef AM_BITS_TPRED
+#define AM_BITS_TPRED 1  // stage only the time-plane words a merge needs (see the staging after the region load)
+#endif
 #ifndef AM_BITS_NOT
 #define AM_BITS_NOT 0  // experiment only (wrong maps): no time-plane staging / updates
 #endif
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
     if (!light && lane == 0)  // inline PTX: the compiler's warp aggregation would consume the result here
       asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(fa) : "l"(bk.count + 3 + blk % 3) : "memory");
     __syncwarp();  // the previous item's reads of tsm are done
-    if (!AM_BITS_NOT) {
+    if (!AM_BITS_NOT && !AM_BITS_TPRED) {
       const uint4* tg = reinterpret_cast<const uint4*>(bk.T) + ((size_t)tc * kBTR * bg.wpr + (size_t)tb * kBTW) * 4;
 #pragma unroll
       for (int q = 0; q < kBTR * kBTW * 4 / 32; ++q) {
@@ -181,6 +187,32 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
         C[i][x] = !((vld >> b) & 1u) ? 0u : ((hom >> b) & 1u) ? C1[i][x] : C[i][x];
       }
     }
+    // time-plane words of the own rows that a merge after the layers will need: only words already holding
+    // covered cells (their bits must survive) and free uncovered ones (which may become new).  A word with
+    // no covered cell has no time bits to keep, so new cells are written over it without a read.  Each lane
+    // stages its own rows' words into its own slots, so no other lane waits on them.
+    uint32_t tneed = 0;  // bit i * kBTW + x
+    if (AM_BITS_TPRED && !AM_BITS_NOT) {
+#pragma unroll
+      for (int i = 0; i < kBRPL; ++i) {
+        const int tr = lane * kBRPL + i - kBK;
+        if (tr < 0 || tr >= kBTR) continue;
+        const uint4* tg = reinterpret_cast<const uint4*>(bk.T) +
+                          ((size_t)(tc * kBTR + (uint32_t)tr) * bg.wpr + (size_t)tb * kBTW) * 4;
+#pragma unroll
+        for (int x = 0; x < kBTW; ++x) {
+          const uint32_t cw = C[i][x + 1];
+          if (cw == 0u || (F[i][x + 1] & ~cw) == 0u) continue;
+          tneed |= 1u << (i * kBTW + x);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(tsm + (tr * kBTW + x) * 4 + qq)),
+                         "l"(tg + x * 4 + qq)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // ---- kBK layers.  J[k]: bit k of the in-block index (layer - 1) of the cells covered in this block,
     // built from snapshots (monotone coverage: the cells new in layers (a, b] are C_b & ~C_a)
     uint32_t C0[kBRPL][kBTW], J[kBNJ][kBRPL][kBTW], S[kBNJ][kBRPL][kBTW], FR[kBRPL][kBTW];
@@ -230,7 +262,7 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
 #pragma unroll
         for (int x = 0; x < kBTW; ++x) {
           const uint32_t nw = N[i][x + 1];
-          if (j == kBK) FR[i][x] = nw & ~C[i][x + 1];
+          if (!AM_BITS_FRJ && j == kBK) FR[i][x] = nw & ~C[i][x + 1];
 #pragma unroll
           for (int k = 0; k < kBNJ; ++k) {
             const int p = 1 << k;
@@ -242,6 +274,18 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
       for (int i = 0; i < kBRPL; ++i)
 #pragma unroll
         for (int x = 0; x < kBNW; ++x) C[i][x] = N[i][x];
+    }
+    // cells new in the last layer: in-block index kBK - 1, all J bits set (none in a partial block)
+    if (AM_BITS_FRJ) {
+#pragma unroll
+      for (int i = 0; i < kBRPL; ++i)
+#pragma unroll
+        for (int x = 0; x < kBTW; ++x) {
+          uint32_t f = C[i][x + 1] & ~C0[i][x];
+#pragma unroll
+          for (int k = 0; k < kBNJ; ++k) f &= J[k][i][x];
+          FR[i][x] = f;
+        }
     }
     // ---- own rows: coverage into the other plane; the new cells' layer t into the time planes
     // (T: 16 words per row word, word k = bit k of t-1 for the row word's 32 cells; t - 1 = l0 + in-block
@@ -312,10 +356,15 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
         if (!nw) continue;
         const uint4* ts = tsm + (tr * kBTW + x) * 4;
         uint32_t v[16];
+        if (!AM_BITS_TPRED || ((tneed >> (i * kBTW + x)) & 1u)) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 a4 = ts[q];
-          v[4 * q] = a4.x, v[4 * q + 1] = a4.y, v[4 * q + 2] = a4.z, v[4 * q + 3] = a4.w;
+          for (int q = 0; q < 4; ++q) {
+            const uint4 a4 = ts[q];
+            v[4 * q] = a4.x, v[4 * q + 1] = a4.y, v[4 * q + 2] = a4.z, v[4 * q + 3] = a4.w;
+          }
+        } else {  // no covered cell in the word before this block: nothing to keep
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = 0u;
         }
 #pragma unroll
         for (int k = 0; k < kBTPlanes; ++k) {
