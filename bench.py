@@ -740,11 +740,13 @@ def run_b200(args, rank, world, local_rank):
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
+            hb0 = ctx.h2d_bytes()
             t0 = time.perf_counter()
             off2, pts2, st2, dt = e2e_solve(am, ctx, h_occ, src, tgt, rank, world, h_map, h_pts, split if i else None,
                                             args.transport)
             ctx.synchronize()
             dfull = time.perf_counter() - t0  # including the full map download
+            h2d_step = ctx.h2d_bytes() - hb0  # what the library copied host -> device (packed occupancy)
             if dist:
                 t = torch.tensor([dt, dfull], dtype=torch.float64, device=reduce_device(dist, local_rank))
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -753,7 +755,7 @@ def run_b200(args, rank, world, local_rank):
                 e2e_times.append(dt)
                 full_times.append(dfull)
         e2e_s, full_s = statistics.median(e2e_times), statistics.median(full_times)
-        h2d = occ.nbytes + src.nbytes + tgt.nbytes * 2 // world + off2.nbytes + st2.nbytes
+        h2d = h2d_step
         d2h = pts2.nbytes + off2.nbytes + st2.nbytes * 2
         e2e = {"value": round(cell_updates / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "time_to_solve_s": round(e2e_s, 4), "runs": len(e2e_times),
@@ -761,6 +763,8 @@ def run_b200(args, rank, world, local_rank):
                "with_full_map_download": {"value": round(cell_updates / full_s / 1e9, 3),
                                           "time_to_solve_s": round(full_s, 4),
                                           "d2h_bytes_per_step": int(d2h + W * rows_here * 4)},
+               "h2d_note": "counted by the library (am_stats.h2d_bytes): the occupancy crosses PCIe packed to 1 bit "
+                           "per cell by host worker threads (upload.cu), plus sources, targets, offsets, status",
                "api": "am_grid_create(host occupancy + sources, pinned) + am_propagate(auto) + am_path_counts + "
                       "am_trace_paths (every path to pinned host memory); the uint32 activity map stays on the "
                       "device (the C++ ActivityMap fetches it lazily) and its download is reported separately" +

@@ -82,6 +82,7 @@ typedef struct am_stats {
   uint64_t kernel_launches; /* every kernel this context has launched */
   uint64_t pool_reserved;   /* device bytes held by the context's memory pool */
   uint64_t pool_used;       /* of which in use by live grids / scratch */
+  uint64_t h2d_bytes;       /* host-to-device bytes this context has copied (occupancy, sources, targets) */
 } am_stats;
 
 /* ---- context ---------------------------------------------------------- */

@@ -78,7 +78,8 @@ class _ParseInfo(C.Structure):
 
 
 class _Stats(C.Structure):
-    _fields_ = [("kernel_launches", C.c_uint64), ("pool_reserved", C.c_uint64), ("pool_used", C.c_uint64)]
+    _fields_ = [("kernel_launches", C.c_uint64), ("pool_reserved", C.c_uint64), ("pool_used", C.c_uint64),
+                ("h2d_bytes", C.c_uint64)]
 
 
 _lib = None
@@ -210,6 +211,12 @@ class Context:
         s = _Stats()
         _check(lib().am_ctx_stats(self.handle, C.byref(s)), self, "stats")
         return s.pool_reserved, s.pool_used
+
+    def h2d_bytes(self) -> int:
+        """Host-to-device bytes this context has copied so far (am_stats.h2d_bytes)."""
+        s = _Stats()
+        _check(lib().am_ctx_stats(self.handle, C.byref(s)), self, "stats")
+        return s.h2d_bytes
 
     def trim(self):
         """Return the pool's cached (unused) device memory to the driver (am_ctx_trim)."""

@@ -17,6 +17,8 @@ constexpr int kLag = 2;        // blocks in flight before the host reads a fixed
 #endif
 constexpr int kLagTiles = AM_LAG_TILES;  // same, active-tile mode (< kFlagSlots)
 struct Comm;             // NCCL communicator wrapper (multigpu.cu)
+struct HostPool;         // host worker threads (upload.cu)
+void host_pool_destroy(HostPool* p);
 struct PeerLink;         // peer-memory slab transport state (multigpu.cu)
 // bit-plane propagation state of a single grid (bits.cu), allocated on first use
 struct BitState {
@@ -55,6 +57,14 @@ struct am_ctx {
   std::vector<am::FlagSet*> flag_sets;  // recycled FlagSets of destroyed grids
   cudaStream_t copy_stream = nullptr;   // map downloads: D2H copies overlapping the chunk decode
   cudaEvent_t copy_ev[8] = {};
+  // packed occupancy upload (upload.cu): host workers, pinned staging, device copy of the packed rows
+  am::HostPool* hpool = nullptr;
+  uint32_t* h_pack = nullptr;
+  size_t h_pack_cap = 0;
+  uint32_t* d_pack = nullptr;
+  size_t d_pack_cap = 0;
+  uint32_t pack_rows = 0, pack_w = 0;  // the rows d_pack holds (valid until the next upload)
+  uint64_t h2d_bytes = 0;              // host-to-device bytes copied by this context
 };
 
 struct am_grid {
@@ -197,7 +207,10 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
                            const uint8_t* occ_full, const uint32_t* src, uint64_t n_src, bool device_ptrs,
                            bool slab, am_grid** out);
 am_status set_cell_bits(am_ctx* ctx, am_grid* g, int cell_bits);
-am_status bits_alloc(am_ctx* ctx, am_grid* g);  // bit-plane state + the grid's free plane (capi.cu)
+// bit-plane state + the grid's free plane (capi.cu); packed: the grid's occupancy as packed rows
+// (upload.cu) to build it from, else the dense bytes are read
+am_status bits_alloc(am_ctx* ctx, am_grid* g, const uint32_t* packed = nullptr);
+am_status upload_occupancy_packed(am_ctx* ctx, const uint8_t* occ, uint32_t W, uint32_t H, uint8_t* d_occ);
 
 }  // namespace am
 

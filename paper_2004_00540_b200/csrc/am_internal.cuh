@@ -225,6 +225,8 @@ struct BitBook {
 };
 int bits_ctas_per_sm();
 void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStream_t s);
+// the same from packed rows (bit = obstacle, (W + 31) / 32 words per row; upload.cu)
+void launch_bits_init_packed(const BitGeo& bg, const uint32_t* packed, BitBook bk, cudaStream_t s);
 void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBook bk, cudaStream_t s);
 void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uint32_t nl, FlagSink flag,
                        FlagSink prev, cudaStream_t s);
@@ -274,7 +276,7 @@ void launch_trace(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int meth
                   const uint64_t* offsets, uint32_t* pts_rc, int32_t* status, cudaStream_t s,
                   uint64_t pts_capacity = ~0ull, uint32_t* order = nullptr, uint32_t* sched = nullptr, int sms = 0);
 // scratch of launch_trace's longest-first scheduling: order (n words) and sched (this many words)
-constexpr int kTraceSchedWords = 1024 + 1;
+constexpr int kTraceSchedWords = 1024 + 2;
 // paths in a grid of mazes packed on a cell_h x cell_w lattice -> each path's maze-local coordinates
 // (the maze is the one of the path's first point, its target)
 void launch_paths_local(uint32_t* pts_rc, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,

@@ -439,6 +439,23 @@ __global__ void k_bits_init(BitGeo bg, const uint8_t* __restrict__ occ, uint4* _
   if (lane == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
 }
 
+// Plane words {0, 0, free, 0} from packed occupancy rows (bit = obstacle, pw = (W + 31) / 32 words per row).
+__global__ void k_bits_init_packed(BitGeo bg, const uint32_t* __restrict__ packed, uint4* __restrict__ P,
+                                   unsigned long long* __restrict__ free_cells) {
+  const uint32_t pw = (bg.W + 31) / 32;
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x, row = blockIdx.y;
+  uint32_t f = 0;
+  if (w < bg.wpr) {
+    if (row < bg.H && w < pw) {
+      const uint32_t valid = bg.W - 32 * w >= 32 ? 0xFFFFFFFFu : (1u << (bg.W - 32 * w)) - 1u;
+      f = ~__ldg(packed + (size_t)row * pw + w) & valid;
+    }
+    P[(size_t)row * bg.wpr + w] = make_uint4(0u, 0u, f, 0u);
+  }
+  const uint32_t cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(f));
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
+}
+
 // The tiles holding a source start the run with valid coverage in home plane 0: their plane-0 words are
 // cleared here (before k_bits_sources sets the source bits) and their state set to kBitsSrcState.  One
 // warp per source; lane k clears rows k, k + 32, ... of the tile's kBTW words.
@@ -560,6 +577,11 @@ int bits_ctas_per_sm() {
 void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStream_t s) {
   const dim3 grid((bg.wpr + 31) / 32, (bg.rows + 7) / 8);
   k_bits_init<<<grid, 256, 0, s>>>(bg, occ, bk.P, bk.stat + 2);
+}
+
+void launch_bits_init_packed(const BitGeo& bg, const uint32_t* packed, BitBook bk, cudaStream_t s) {
+  const dim3 grid((bg.wpr + 255) / 256, bg.rows);
+  k_bits_init_packed<<<grid, 256, 0, s>>>(bg, packed, bk.P, bk.stat + 2);
 }
 
 void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBook bk, cudaStream_t s) {

@@ -74,6 +74,9 @@ void am_ctx_destroy(am_ctx* ctx) {
     cudaEventDestroy(t.b);
   }
   for (auto* f : ctx->flag_sets) flag_set_free(f);
+  am::host_pool_destroy(ctx->hpool);
+  if (ctx->h_pack) cudaFreeHost(ctx->h_pack);
+  am::dfree(ctx, ctx->d_pack);
   for (auto& e : ctx->copy_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -91,6 +94,7 @@ am_status am_ctx_stats(const am_ctx* ctx, am_stats* out) {
   out->pool_reserved = cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &v) ? 0 : v;
   v = 0;
   out->pool_used = cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &v) ? 0 : v;
+  out->h2d_bytes = ctx->h2d_bytes;
   return AM_OK;
 }
 
@@ -243,15 +247,30 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
   if (!e) e = cudaMemsetAsync(g->d_flags + kFlagSlots, 0, sizeof(uint32_t), s);     // arrival counter
   if (!e) e = cudaMemsetAsync(g->d_flags + kFlagRecvUp, 0xFF, 2 * kFlagSlots * sizeof(uint32_t), s);  // no neighbour
   if (!e) e = cudaMemsetAsync(g->srcmask_dense, 0, dense, s);
-  if (!e)
+  // host occupancy of a large grid: packed to bits by host workers on the way (upload.cu, 8x fewer PCIe
+  // bytes); small grids and device pointers: a plain copy
+  static const bool pack_off = [] {
+    const char* v = getenv("AM_PACKED_UPLOAD");
+    return v && v[0] == '0';
+  }();
+  const bool packed = !e && !device_ptrs && !pack_off && dense >= ((size_t)1 << 20);
+  if (packed) {
+    if ((st = upload_occupancy_packed(ctx, occ_full + (size_t)row0 * W, W, H, g->occ))) {
+      grid_free(ctx, g);
+      return st;
+    }
+  } else if (!e) {
     e = cudaMemcpyAsync(g->occ, occ_full + (size_t)row0 * W, dense,
                         device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+    if (!device_ptrs) ctx->h2d_bytes += dense;
+  }
   if (!e) e = am::dmalloc(ctx, &d_src, n_src * 2 * sizeof(uint32_t));
   if (!e) e = am::dmalloc(ctx, &d_err, sizeof(int));
   if (!e) e = cudaMemsetAsync(d_err, 0, sizeof(int), s);
   if (!e)
     e = cudaMemcpyAsync(d_src, src, n_src * 2 * sizeof(uint32_t),
                         device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+  if (!e && !device_ptrs) ctx->h2d_bytes += n_src * 2 * sizeof(uint32_t);
   if (!e) {
     launch_srcmask_rows(g->g, H_total, row0, d_src, n_src, g->srcmask_dense, g->occ, g->srcmask, g->rowsrc, d_err,
                         s);
@@ -271,7 +290,7 @@ am_status grid_create_rows(am_ctx* ctx, uint32_t W, uint32_t H_total, uint32_t r
     st = fail(ctx, AM_EINVAL, "SourceSet: a source is out of bounds or on an obstacle (grid.hpp:78)");
   }
   // single grids: the free plane of the bit-plane engine is part of the grid's device form (built once)
-  if (!st && !slab && !(ctx->flags & AM_CTX_DENSE)) st = bits_alloc(ctx, g);
+  if (!st && !slab && !(ctx->flags & AM_CTX_DENSE)) st = bits_alloc(ctx, g, packed ? ctx->d_pack : nullptr);
   if (st) {
     grid_free(ctx, g);
     return st;
@@ -426,11 +445,14 @@ static am_status reset_map(am_ctx* ctx, am_grid* g, int cell_bits) {
 // range) return handoff = true with the field exactly at layer lref; the caller
 // continues there with the 16/32-bit tile kernels.
 
-static am_status bits_build_planes(am_ctx* ctx, am_grid* g) {
+static am_status bits_build_planes(am_ctx* ctx, am_grid* g, const uint32_t* packed) {
   BitState& B = *g->bits;
   cudaStream_t s = ctx->stream;
   CK(cudaMemsetAsync(B.bk.stat, 0, 3 * 8, s));
-  launch_bits_init(B.bg, g->occ, B.bk, s);
+  if (packed)
+    launch_bits_init_packed(B.bg, packed, B.bk, s);
+  else
+    launch_bits_init(B.bg, g->occ, B.bk, s);
   CKL();
   ++ctx->launches;
   unsigned long long fc = 0;
@@ -443,9 +465,9 @@ static am_status bits_build_planes(am_ctx* ctx, am_grid* g) {
 
 // Allocates the bit-plane state and builds the free plane from the grid's occupancy (occupancy is
 // immutable, so this runs once per grid: at creation for single grids, else on first use).
-am_status bits_alloc(am_ctx* ctx, am_grid* g) {
+am_status bits_alloc(am_ctx* ctx, am_grid* g, const uint32_t* packed) {
   if (g->bits && g->bits->planes_ready) return AM_OK;
-  if (g->bits) return bits_build_planes(ctx, g);
+  if (g->bits) return bits_build_planes(ctx, g, packed);
   auto* b = new (std::nothrow) BitState();
   if (!b) return fail(ctx, AM_EOOM, "bit state");
   g->bits = b;
@@ -460,7 +482,7 @@ am_status bits_alloc(am_ctx* ctx, am_grid* g) {
   CK(am::dmalloc(ctx, &k.count, 6 * 4));
   CK(am::dmalloc(ctx, &k.stat, 3 * 8));
   b->ctas = ctx->sms * bits_ctas_per_sm();
-  return bits_build_planes(ctx, g);
+  return bits_build_planes(ctx, g, packed);
 }
 
 static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom, am_prop_result* res,
@@ -1088,6 +1110,7 @@ am_status am_activity_upload(am_ctx* ctx, am_grid* g, const uint32_t* dense, uin
   const size_t n = (size_t)g->g.W * g->g.H;
   if (!g->plain) CK(am::dmalloc(ctx, &g->plain, n * 4));
   CK(cudaMemcpyAsync(g->plain, dense, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += n * 4;
   CK(cudaStreamSynchronize(ctx->stream));
   g->plain_active = 1;
   g->plain_layers = layers_applied;
@@ -1184,6 +1207,7 @@ am_status am_path_counts(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_t 
   if (st) return st;
   cudaStream_t s = ctx->stream;
   CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
+  ctx->h2d_bytes += n * 8;
   am::launch_path_counts(view_of(g), g->d_tgt, n, (int)method, seed, g->d_counts, g->d_status, s);
   CKL();
   am::launch_scan(g->d_counts, n, g->d_offsets, s);
@@ -1239,6 +1263,7 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   CK(cudaMemcpyAsync(g->d_tgt, tgt, n * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->d_offsets, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(g->d_status, status, n * 4, cudaMemcpyHostToDevice, s));
+  ctx->h2d_bytes += n * 8 + (n + 1) * 8 + n * 4;
   // the counts are consumed (offsets came from the caller): their buffer holds the trace order
   am::launch_trace(view_of(g), g->d_tgt, n, (int)method, seed, g->d_offsets, direct ? direct : g->d_pts,
                    g->d_status, s, ~0ull, reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);

@@ -631,17 +631,21 @@ __device__ __forceinline__ void trace_one(const MapView& m, const uint32_t* __re
 // first, k_trace_order) through the counter *next: the walk time is set by the longest path, and every
 // warp sharing its SM sub-partition slows it down, so few warps per sub-partition with the longest paths
 // started first finish soonest (greedy longest-processing-time scheduling).
+// sched (when order is set): [0] the counter, [1] whether k_trace_order chose the ordered mode; in that mode
+// only the first `workers` warps run.
 __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n, int method, uint64_t seed,
                         const uint64_t* __restrict__ offsets, uint32_t* __restrict__ pts,
                         int32_t* __restrict__ status, uint64_t cap, const uint32_t* __restrict__ order,
-                        uint32_t* next) {
+                        uint32_t* sched, uint32_t workers) {
   __shared__ __align__(16) uint8_t wins[4][kWinBytes];  // one window per warp (128-thread CTAs)
   uint8_t* win = wins[(threadIdx.x >> 5) & 3];
-  if (!order) {
-    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    if (w < n) trace_one(m, tgt, w, method, seed, offsets, pts, status, cap, win);
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (!order || !__ldcg(sched + 1)) {
+    if (gw < n) trace_one(m, tgt, gw, method, seed, offsets, pts, status, cap, win);
     return;
   }
+  if (gw >= workers) return;
+  uint32_t* next = sched;
   const int lane = threadIdx.x & 31;
   for (;;) {
     uint32_t i = 0;
@@ -657,8 +661,11 @@ __global__ void k_trace(MapView m, const uint32_t* __restrict__ tgt, uint64_t n,
 // counts), bucketed into kOrderBuckets length classes: a histogram, an exclusive scan and a scatter in one
 // CTA.  sched: kOrderBuckets + 1 words (the bucket cursors, then the trace counter, reset here).
 constexpr int kOrderBuckets = 1024;
+// The ordered mode pays only when the longest path is long against the mean work of a worker warp
+// (total points / workers): many short paths (C5) run faster one warp per target.
 __global__ void __launch_bounds__(1024) k_trace_order(const uint64_t* __restrict__ offsets, uint64_t n,
-                                                      uint32_t* __restrict__ order, uint32_t* __restrict__ sched) {
+                                                      uint32_t* __restrict__ order, uint32_t* __restrict__ sched,
+                                                      uint32_t workers) {
   __shared__ uint32_t hist[kOrderBuckets];
   __shared__ uint64_t maxlen_s;
   const int t = threadIdx.x;
@@ -669,6 +676,12 @@ __global__ void __launch_bounds__(1024) k_trace_order(const uint64_t* __restrict
   for (uint64_t i = t; i < n; i += blockDim.x) mx = max(mx, (unsigned long long)(offsets[i + 1] - offsets[i]));
   atomicMax(reinterpret_cast<unsigned long long*>(&maxlen_s), mx);
   __syncthreads();
+  const bool ordered = 2 * maxlen_s * workers >= offsets[n];
+  if (t == 0) {
+    sched[kOrderBuckets] = 0;
+    sched[kOrderBuckets + 1] = ordered ? 1u : 0u;
+  }
+  if (!ordered) return;
   const uint64_t span = maxlen_s + 1;
   auto bucket = [&](uint64_t i) {  // longest first
     const uint64_t len = offsets[i + 1] - offsets[i];
@@ -683,7 +696,6 @@ __global__ void __launch_bounds__(1024) k_trace_order(const uint64_t* __restrict
       hist[b] = acc;
       acc += v;
     }
-    sched[kOrderBuckets] = 0;
   }
   __syncthreads();
   for (uint64_t i = t; i < n; i += blockDim.x) order[atomicAdd(&hist[bucket(i)], 1u)] = (uint32_t)i;
@@ -715,6 +727,9 @@ void launch_paths_local(uint32_t* pts, const uint64_t* offsets, const int32_t* s
   k_paths_local<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(pts, offsets, status, n, cell_h, cell_w);
 }
 
+#ifndef AM_TRACE_SCHED
+#define AM_TRACE_SCHED 1  // longest-first scheduling of the targets (k_trace_order)
+#endif
 #ifndef AM_TRACE_WPS
 #define AM_TRACE_WPS 2  // warps per SM sub-partition when the targets are scheduled longest-first
 #endif
@@ -724,13 +739,14 @@ void launch_trace(const MapView& m, const uint32_t* tgt, uint64_t n, int method,
   if (!n) return;
   const uint64_t blocks = (n * 32 + 127) / 128;
   const uint64_t sched_blocks = (uint64_t)sms * AM_TRACE_WPS;  // 4 warps per CTA, one CTA per sub-partition
-  if (order && sched && sms > 0 && blocks > sched_blocks && n < (1ull << 32)) {
-    k_trace_order<<<1, 1024, 0, s>>>(offsets, n, order, sched);
-    k_trace<<<(unsigned)sched_blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap, order,
-                                                   sched + kOrderBuckets);
+  if (AM_TRACE_SCHED && order && sched && sms > 0 && blocks > sched_blocks && n < (1ull << 32)) {
+    const uint32_t workers = (uint32_t)sched_blocks * 4;
+    k_trace_order<<<1, 1024, 0, s>>>(offsets, n, order, sched, workers);
+    k_trace<<<(unsigned)blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap, order,
+                                             sched + kOrderBuckets, workers);
     return;
   }
-  k_trace<<<(unsigned)blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap, nullptr, nullptr);
+  k_trace<<<(unsigned)blocks, 128, 0, s>>>(m, tgt, n, method, seed, offsets, pts, status, cap, nullptr, nullptr, 0);
 }
 
 }  // namespace am

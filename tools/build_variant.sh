@@ -11,7 +11,7 @@ NVCC=/usr/local/cuda/bin/nvcc
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -ccbin g++ -I$ROOT/include $EXTRA"
 pids=()
-for f in stencil bits trace capi multigpu batch mapio; do
+for f in stencil bits trace capi multigpu batch mapio upload; do
   $NVCC $FLAGS -c $SRC/$f.cu -o $OUT/$f.o & pids+=($!)
 done
 for f in actmap_api report; do
