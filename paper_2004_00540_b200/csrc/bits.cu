@@ -40,7 +40,18 @@ BitGeo make_bit_geo(uint32_t W, uint32_t H) {
 
 namespace {
 
-constexpr int kBNW = kBTW + 2;   // words per region row (one halo word each side)
+#ifndef AM_BITS_PACKH
+#define AM_BITS_PACKH 1
+#endif
+// words per region row: the tile's kBTW words and the horizontal halo.  Packed (default): one word, bits
+// 16-31 = the kBK cells left of the tile, bits 0-15 = the kBK cells right of it, index 0, and the row is a
+// ring (word 0's left neighbour is word kBTW, word kBTW's right neighbour is word 0).  The two halves meet
+// at the outermost halo cells, whose errors travel one cell per layer and reach the tile after kBK + 1
+// layers, never within a block.  Unpacked: one full word each side (index 0 and kBTW + 1).
+static_assert(!AM_BITS_PACKH || kBK == 16, "packed halo: 16 cells each side");
+constexpr int kBNW = AM_BITS_PACKH ? kBTW + 1 : kBTW + 2;
+__device__ __forceinline__ constexpr int bleft(int x) { return AM_BITS_PACKH && x == 0 ? kBNW - 1 : x - 1; }
+__device__ __forceinline__ constexpr int bright(int x) { return AM_BITS_PACKH && x == kBNW - 1 ? 0 : x + 1; }
 constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-block layer index
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
@@ -158,6 +169,7 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
     // coverage planes come with the same 16 B load and the homes pick one afterwards
     const bool exl = tb > 0, exr = tb + 1 < bg.tbands;
     uint32_t C[kBRPL][kBNW], C1[kBRPL][kBNW], F[kBRPL][kBNW];
+    uint32_t HR0[kBRPL], HR1[kBRPL], HRF[kBRPL];  // packed halo: the right neighbour's word until the select
 #pragma unroll
     for (int i = 0; i < kBRPL; ++i) {
       const int tr = lane * kBRPL + i - kBK;  // tile-relative row
@@ -165,10 +177,14 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
       const bool er = prow >= 0 && prow < (int)bg.rows;
       const size_t rb = (size_t)(er ? prow : 0) * bg.wpr + (size_t)tb * kBTW;
 #pragma unroll
-      for (int x = 0; x < kBNW; ++x) {
-        const bool e = er && (x == 0 ? exl : (x == kBNW - 1 ? exr : true));
+      for (int x = 0; x < kBTW + 2; ++x) {  // memory words tb*TW - 1 .. tb*TW + TW
+        const bool e = er && (x == 0 ? exl : (x == kBTW + 1 ? exr : true));
         const uint4 v = e ? __ldcg(bk.P + rb + x - 1) : make_uint4(0u, 0u, 0u, 0u);
-        C[i][x] = v.x, C1[i][x] = v.y, F[i][x] = v.z;
+        if (AM_BITS_PACKH && x == kBTW + 1) {
+          HR0[i] = v.x, HR1[i] = v.y, HRF[i] = v.z;
+        } else {
+          C[i][x] = v.x, C1[i][x] = v.y, F[i][x] = v.z;
+        }
       }
     }
     // a state of 0 is a tile no block of this run has processed (and no source tile): its coverage words
@@ -182,9 +198,15 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
       const int d = tr < 0 ? 0 : (tr >= kBTR ? 2 : 1);
 #pragma unroll
       for (int x = 0; x < kBNW; ++x) {
-        const int q = x == 0 ? 0 : (x == kBNW - 1 ? 2 : 1);
+        const int q = x == 0 ? 0 : (x == kBTW + 1 ? 2 : 1);
         const uint32_t b = d * 3 + q;
         C[i][x] = !((vld >> b) & 1u) ? 0u : ((hom >> b) & 1u) ? C1[i][x] : C[i][x];
+      }
+      if (AM_BITS_PACKH) {  // halo word: left neighbour's high half | right neighbour's low half
+        const uint32_t b = d * 3 + 2;
+        const uint32_t cr = !((vld >> b) & 1u) ? 0u : ((hom >> b) & 1u) ? HR1[i] : HR0[i];
+        C[i][0] = __byte_perm(C[i][0], cr, 0x3254);  // bytes: cr.0 cr.1 C.2 C.3
+        F[i][0] = __byte_perm(F[i][0], HRF[i], 0x3254);
       }
     }
     // time-plane words of the own rows that a merge after the layers will need: only words already holding
@@ -245,8 +267,8 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
           }
 #pragma unroll
           for (int x = 0; x < kBNW; ++x) {
-            const uint32_t l = x > 0 ? __funnelshift_l(v[x - 1], v[x], 1) : v[x] << 1;
-            const uint32_t r = x < kBNW - 1 ? __funnelshift_r(v[x], v[x + 1], 1) : v[x] >> 1;
+            const uint32_t l = AM_BITS_PACKH || x > 0 ? __funnelshift_l(v[bleft(x)], v[x], 1) : v[x] << 1;
+            const uint32_t r = AM_BITS_PACKH || x < kBNW - 1 ? __funnelshift_r(v[x], v[bright(x)], 1) : v[x] >> 1;
             N[i][x] = (v[x] | l | r) & F[i][x];
           }
         }
