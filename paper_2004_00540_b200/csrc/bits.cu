@@ -56,6 +56,16 @@ constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
 constexpr int kBThreads = 128;
+#ifndef AM_BITS_PREF
+#define AM_BITS_PREF 0  // the next item's states and region load during the current item's bookkeeping
+                        // (measured: C4 +3.5%, the longer live ranges spill)
+#endif
+#ifndef AM_BITS_DONE
+#define AM_BITS_DONE 1  // tiles whose free cells are all covered are never listed again
+#endif
+#ifndef AM_BITS_STATS
+#define AM_BITS_STATS 0  // experiment: item counters in stat[3..5]
+#endif
 #ifndef AM_BITS_FRJ
 #define AM_BITS_FRJ 1  // the last layer's new cells from the in-block index bits (no register set in the loop)
 #endif
@@ -129,6 +139,7 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
 #ifndef AM_BITS_STATIC
 #define AM_BITS_STATIC 1  // items dealt round-robin (measured: the fetch atomic costs more than the imbalance)
 #endif
+  static_assert(!AM_BITS_PREF || AM_BITS_STATIC, "prefetching needs the static item order");
   const bool light = AM_BITS_STATIC || n <= nwarps;  // one item per warp at most: no fetch atomics
   const uint32_t mark = blk + 1;
   uint32_t wmin = 0xFFFFFFFFu;    // fixed-point word: min over new cells of (nl - 1 - in-block index)
@@ -137,6 +148,40 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
   // with cp.async at item start so the read-modify-write after the layers finds them on chip
   __shared__ uint4 tsm_all[kBThreads / 32][kBTR * kBTW * 4];
   uint4* tsm = tsm_all[threadIdx.x >> 5];
+  // An item's inputs: the states of its 3x3 tile neighbourhood (lane k < 9: (tc + k/3 - 1, tb + k%3 - 1),
+  // the pre-block state whether or not that tile was processed in this block yet) and its region (rows
+  // tc*TR - K .. tc*TR + TR + K, memory words tb*TW - 1 .. tb*TW + TW; each plane word is {coverage plane
+  // 0, coverage plane 1, free, -}, so both coverage planes come with one 16 B load and the homes pick one
+  // afterwards).  Neither changes during the block (a tile processed in it writes its other plane), so
+  // with AM_BITS_PREF the next item's inputs load while the current item finishes.
+  uint32_t R0[kBRPL][kBTW + 2], R1[kBRPL][kBTW + 2], RF[kBRPL][kBTW + 2], rs9 = 0;
+  auto load_item = [&](uint32_t item) {
+    const uint32_t ib = item >> 16, ic = item & 0xFFFFu;
+    rs9 = 0;
+    if (lane < 9) {
+      const int c = (int)ic + lane / 3 - 1, b = (int)ib + lane % 3 - 1;
+      if (c >= 0 && b >= 0 && c < (int)bg.nchunks && b < (int)bg.tbands) {
+        const unsigned long long sw = __ldcg(bk.state + (uint32_t)c * bg.tbands + (uint32_t)b);
+        const uint32_t cur = (uint32_t)sw;
+        rs9 = (cur >> 1) == mark ? (uint32_t)(sw >> 32) : cur;
+      }
+    }
+    const bool exl = ib > 0, exr = ib + 1 < bg.tbands;
+#pragma unroll
+    for (int i = 0; i < kBRPL; ++i) {
+      const int tr = lane * kBRPL + i - kBK;  // tile-relative row
+      const int prow = (int)ic * kBTR + tr;
+      const bool er = prow >= 0 && prow < (int)bg.rows;
+      const size_t rb = (size_t)(er ? prow : 0) * bg.wpr + (size_t)ib * kBTW;
+#pragma unroll
+      for (int x = 0; x < kBTW + 2; ++x) {
+        const bool e = er && (x == 0 ? exl : (x == kBTW + 1 ? exr : true));
+        const uint4 v = e ? __ldcg(bk.P + rb + x - 1) : make_uint4(0u, 0u, 0u, 0u);
+        R0[i][x] = v.x, R1[i][x] = v.y, RF[i][x] = v.z;
+      }
+    }
+  };
+  if (AM_BITS_PREF && w < n) load_item(it);
   while (w < n) {
     const uint32_t tb = it >> 16, tc = it & 0xFFFFu;
     uint32_t fa = 0;  // the next item's index (heavy blocks), in flight during this item
@@ -154,39 +199,21 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    // states of the 3x3 tile neighbourhood: lane k < 9 reads (tc + k/3 - 1, tb + k%3 - 1)
-    uint32_t s9 = 0;
-    if (lane < 9) {
-      const int c = (int)tc + lane / 3 - 1, b = (int)tb + lane % 3 - 1;
-      if (c >= 0 && b >= 0 && c < (int)bg.nchunks && b < (int)bg.tbands) {
-        const unsigned long long sw = __ldcg(bk.state + (uint32_t)c * bg.tbands + (uint32_t)b);
-        const uint32_t cur = (uint32_t)sw;
-        s9 = (cur >> 1) == mark ? (uint32_t)(sw >> 32) : cur;
-      }
-    }
-    // ---- load the region (rows tc*TR - K .. tc*TR + TR + K, words tb*TW - 1 .. tb*TW + TW) while the
-    // states are in flight: each plane word is {coverage plane 0, coverage plane 1, free, -}, so both
-    // coverage planes come with the same 16 B load and the homes pick one afterwards
-    const bool exl = tb > 0, exr = tb + 1 < bg.tbands;
+    if (!AM_BITS_PREF) load_item(it);
+    const uint32_t it_next = AM_BITS_PREF && w + nwarps < n ? __ldcg(list + w + nwarps) : 0u;
+    const uint32_t s9 = rs9;
     uint32_t C[kBRPL][kBNW], C1[kBRPL][kBNW], F[kBRPL][kBNW];
     uint32_t HR0[kBRPL], HR1[kBRPL], HRF[kBRPL];  // packed halo: the right neighbour's word until the select
 #pragma unroll
-    for (int i = 0; i < kBRPL; ++i) {
-      const int tr = lane * kBRPL + i - kBK;  // tile-relative row
-      const int prow = (int)tc * kBTR + tr;
-      const bool er = prow >= 0 && prow < (int)bg.rows;
-      const size_t rb = (size_t)(er ? prow : 0) * bg.wpr + (size_t)tb * kBTW;
+    for (int i = 0; i < kBRPL; ++i)
 #pragma unroll
-      for (int x = 0; x < kBTW + 2; ++x) {  // memory words tb*TW - 1 .. tb*TW + TW
-        const bool e = er && (x == 0 ? exl : (x == kBTW + 1 ? exr : true));
-        const uint4 v = e ? __ldcg(bk.P + rb + x - 1) : make_uint4(0u, 0u, 0u, 0u);
+      for (int x = 0; x < kBTW + 2; ++x) {
         if (AM_BITS_PACKH && x == kBTW + 1) {
-          HR0[i] = v.x, HR1[i] = v.y, HRF[i] = v.z;
+          HR0[i] = R0[i][x], HR1[i] = R1[i][x], HRF[i] = RF[i][x];
         } else {
-          C[i][x] = v.x, C1[i][x] = v.y, F[i][x] = v.z;
+          C[i][x] = R0[i][x], C1[i][x] = R1[i][x], F[i][x] = RF[i][x];
         }
       }
-    }
     // a state of 0 is a tile no block of this run has processed (and no source tile): its coverage words
     // are stale (a previous run's, or the walkers' layout) and read as empty
     const uint32_t hom = __ballot_sync(0xffffffffu, s9 & 1u);
@@ -297,6 +324,7 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
 #pragma unroll
         for (int x = 0; x < kBNW; ++x) C[i][x] = N[i][x];
     }
+    if (AM_BITS_PREF && w + nwarps < n) load_item(it_next);  // lands while this item finishes
     // cells new in the last layer: in-block index kBK - 1, all J bits set (none in a partial block)
     if (AM_BITS_FRJ) {
 #pragma unroll
@@ -357,7 +385,8 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
       pt = bit_push_begin(bg, bk, blk, want, (int)tc - dr, (int)tb - dc);
     }
     uint32_t next = AM_BITS_STATIC ? w + nwarps : nwarps;
-    if (AM_BITS_STATIC && next < n) it = __ldcg(list + next);
+    if (AM_BITS_PREF) it = it_next;
+    else if (AM_BITS_STATIC && next < n) it = __ldcg(list + next);
     if (!light) {  // dynamic items past the static first one: the list entry loads during the update
       next = __shfl_sync(0xffffffffu, fa, 0) + nwarps;
       if (next < n) it = __ldcg(list + next);
@@ -398,6 +427,25 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
         for (int q = 0; q < 4; ++q) __stcg(tp + q, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
       }
     }
+#if AM_BITS_STATS
+    {  // experiment counters: items without new cells, items whose own rows have no free uncovered cell
+      uint32_t fu = 0;
+#pragma unroll
+      for (int i = 0; i < kBRPL; ++i) {
+        const int tr = lane * kBRPL + i - kBK;
+        if (tr < 0 || tr >= kBTR) continue;
+#pragma unroll
+        for (int x = 0; x < kBTW; ++x) fu |= F[i][x + 1] & ~C[i][x + 1];
+      }
+      const bool none_new = !__any_sync(0xffffffffu, any_new != 0);
+      const bool full = !__any_sync(0xffffffffu, fu != 0);
+      if (lane == 0) {
+        if (none_new) atomicAdd(&bk.stat[3], 1ull);
+        if (full) atomicAdd(&bk.stat[4], 1ull);
+        if (none_new && !full) atomicAdd(&bk.stat[5], 1ull);
+      }
+    }
+#endif
     if (__any_sync(0xffffffffu, any_new != 0)) {
       // in-block index of the warp's last new cell: kBK - 1 if a cell is new in the last layer, else the
       // bit-sliced maximum over the new cells' J
@@ -424,6 +472,22 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
     }
     if (lane == 0)
       bk.state[tc * bg.tbands + tb] = (unsigned long long)sown << 32 | (mark << 1 | out_home);
+    if (AM_BITS_DONE) {
+      // every free cell of the tile is covered: its planes are final, so no later block needs it.  A
+      // schedule word of ~0 makes every later push of the tile a no-op (the dedup atomicMax sees it as
+      // listed); a push racing with this store lists it once more, which is harmless.  (Also counting
+      // tiles whose uncovered free cells are closed pockets -- none in the last layer's frontier, none on
+      // the border ring -- skipped 2.3% of the C4 items but cost as much per item as it saved.)
+      uint32_t fu = 0;
+#pragma unroll
+      for (int i = 0; i < kBRPL; ++i) {
+        const int tr = lane * kBRPL + i - kBK;
+        if (tr < 0 || tr >= kBTR) continue;
+#pragma unroll
+        for (int x = 0; x < kBTW; ++x) fu |= F[i][x + 1] & ~C[i][x + 1];
+      }
+      if (!__any_sync(0xffffffffu, fu != 0u) && lane == 0) bk.sched[tc * bg.tbands + tb] = 0xFFFFFFFFu;
+    }
     bit_push_end(bk, blk, pt);
     w = next;
   }

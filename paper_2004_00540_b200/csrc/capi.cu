@@ -480,7 +480,7 @@ am_status bits_alloc(am_ctx* ctx, am_grid* g, const uint32_t* packed) {
   CK(am::dmalloc(ctx, &k.list[0], nt * 4));
   CK(am::dmalloc(ctx, &k.list[1], nt * 4));
   CK(am::dmalloc(ctx, &k.count, 6 * 4));
-  CK(am::dmalloc(ctx, &k.stat, 3 * 8));
+  CK(am::dmalloc(ctx, &k.stat, 8 * 8));
   b->ctas = ctx->sms * bits_ctas_per_sm();
   return bits_build_planes(ctx, g, packed);
 }
@@ -510,6 +510,7 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   CK(cudaMemsetAsync(B.bk.sched, 0, nt * 4, s));
   CK(cudaMemsetAsync(B.bk.count, 0, 6 * 4, s));
   CK(cudaMemsetAsync(B.bk.stat, 0, 2 * 8, s));
+  CK(cudaMemsetAsync(B.bk.stat + 3, 0, 5 * 8, s));  // experiment counters (AM_BITS_STATS)
   // the planes are not reset: the cleared states mark every tile's coverage stale (bits.cu)
   launch_bits_sources(bg, g->src_rc, g->n_src, B.bk, s);
   CKL();
@@ -579,9 +580,12 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   if (timing) CK(cudaEventRecord(ctx->timers[0].b, s));
   while (!pend.empty())
     if ((st = drain_one())) return st;
-  unsigned long long stat[3] = {0, 0, 0};
+  unsigned long long stat[8] = {};
   CK(cudaMemcpyAsync(stat, B.bk.stat, sizeof stat, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (getenv("AM_BITS_STATS_PRINT"))
+    fprintf(stderr, "bits: items %llu, without new cells %llu, own rows fully covered %llu, no new but not full %llu\n",
+            stat[0], stat[3], stat[4], stat[5]);
   const bool any_zero = stat[1] < B.free_cells;
   uint32_t used = l, cause = AM_STOP_FIXED;
   if (autom) {
