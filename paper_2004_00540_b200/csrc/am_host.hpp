@@ -65,6 +65,7 @@ struct am_ctx {
   size_t d_pack_cap = 0;
   uint32_t pack_rows = 0, pack_w = 0;  // the rows d_pack holds (valid until the next upload)
   uint64_t h2d_bytes = 0;              // host-to-device bytes copied by this context
+  cudaStream_t map_stream = nullptr;   // k_bits_finalize (field encoding) beside the path walkers
 };
 
 struct am_grid {
@@ -102,6 +103,8 @@ struct am_grid {
   am::PeerLink* peer = nullptr;              // slabs: peer-memory transport (am_peer_connect)
   am::BitState* bits = nullptr;              // bit-plane propagation (single grids, 16-bit runs)
   int bits_map = 0;                          // val[0] came from a bit-plane run whose planes are intact
+  cudaEvent_t map_ev = nullptr;              // recorded on ctx->map_stream after the field encoding
+  int map_pending = 0;                       // ctx->stream has not waited on map_ev yet
   am::TileBook book() const {
     return am::TileBook{t_state, t_sched, {t_list[0], t_list[1]}, t_count, t_processed, t_src};
   }
@@ -210,6 +213,10 @@ am_status set_cell_bits(am_ctx* ctx, am_grid* g, int cell_bits);
 // bit-plane state + the grid's free plane (capi.cu); packed: the grid's occupancy as packed rows
 // (upload.cu) to build it from, else the dense bytes are read
 am_status bits_alloc(am_ctx* ctx, am_grid* g, const uint32_t* packed = nullptr);
+// Orders the context stream after the grid's field encoding (k_bits_finalize on the map stream): every
+// entry point that reads or rewrites the field calls this first; path counts and walks read the planes
+// and join after their launches.
+am_status join_map(am_ctx* ctx, am_grid* g);
 am_status upload_occupancy_packed(am_ctx* ctx, const uint8_t* occ, uint32_t W, uint32_t H, uint8_t* d_occ);
 
 }  // namespace am

@@ -253,11 +253,27 @@ struct MapView {
   const uint8_t* occ;     // plain mode only: dense occupancy
   uint32_t layers;        // layers represented by the values (for point counts)
   const SlabDir* dir = nullptr;  // encoded maps only: the field is distributed over row slabs (val unused)
-  // maps of a bit-plane run (bits.cu) whose planes are intact: the walkers read coverage + time planes
-  const uint4* bp = nullptr;                 // {covered, u bit 0, free, u bit 1} per plane word (after k_bits_finalize)
+  // maps of a bit-plane run (bits.cu) whose planes are intact: path counts and walkers read the planes
+  // (the encoded field may still be in flight on the map stream)
+  const uint4* bp = nullptr;                 // {covered (home 0), covered (home 1), free, -} per plane word
   const uint32_t* bt = nullptr;              // time planes, 16 words per plane word
-  const unsigned long long* bstate = nullptr;  // tile states (home plane)
+  const unsigned long long* bstate = nullptr;  // tile states (home plane; 0: nothing covered)
   BitGeo bg{};
+  // covered / free bits and t - 1 of cell (r, c) of a bit-plane map (r < H, c < W)
+  __device__ __forceinline__ uint32_t bword(uint32_t r, uint32_t c, uint32_t* free_bit) const {
+    const size_t w = (size_t)r * bg.wpr + (c >> 5);
+    const uint4 p = bp[w];
+    const uint32_t st = (uint32_t)bstate[(r / kBTR) * bg.tbands + (c >> 5) / kBTW];
+    *free_bit = (p.z >> (c & 31)) & 1u;
+    const uint32_t cov = st == 0u ? 0u : (st & 1u) ? p.y : p.x;
+    return (cov >> (c & 31)) & 1u;
+  }
+  __device__ __forceinline__ uint32_t bu(uint32_t r, uint32_t c) const {
+    const uint32_t* t = bt + ((size_t)r * bg.wpr + (c >> 5)) * 16;
+    uint32_t u = 0;
+    for (int k = 0; k < kBTPlanes; ++k) u |= ((t[k] >> (c & 31)) & 1u) << k;
+    return u;
+  }
   // allocated row arow of an encoded field (cell 0 = allocated column 0)
   template <typename T>
   __device__ __forceinline__ const T* row(int arow) const {

@@ -579,13 +579,14 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
 
 // The encoded field (am_internal.cuh) from the planes, once per run: free covered cell flag | (lref - u)
 // with u = t - 1 from the time planes (lref + 1 at sources: u = kBTSrcU == -1 mod 2^kBTPlanes), free
-// uncovered flag | 0, obstacle 0; and the plane words rewritten for the path walkers as {covered, u bit 0,
-// free, u bit 1} (the free plane stays where the next run reads it).  A warp converts two row words per
+// uncovered flag | 0, obstacle 0.  It only reads the planes, so it runs on the context's map stream beside
+// the path walkers (which read the planes too, never the field).  A warp converts two row words per
 // step: lane k of half h (lanes 16h .. 16h+15) holds plane word k of row word wb + 2q + h -- time planes
 // 0 .. kBTPlanes-1, then the covered word (the tile's home plane, or 0 in a tile no block processed) and
 // the free word -- and a 32 x 32 bit transpose over the lanes (five butterfly shuffles) leaves lane c
 // with cell c of both row words as a u16x2 {free, covered, u} pair: the encoding is then a handful of
 // word-wide ops, and two coalesced 64 B stores follow.
+constexpr uint32_t kFinalizeSteps = 4;
 __global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uint16_t* __restrict__ field) {
   constexpr int P = 4;  // row-word pairs per warp step (loads of all of them in flight together)
   constexpr uint32_t kUMask = (1u << kBTPlanes) - 1u, kU2 = kUMask | kUMask << 16;
@@ -597,21 +598,21 @@ __global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uin
   // per half: (lref + 2^kBTPlanes) - u >= 0, no borrow across the halves; the low kBTPlanes bits are
   // (lref - u) mod 2^kBTPlanes, which is lref + 1 at sources
   const uint32_t K2 = (lref + (1u << kBTPlanes)) * 0x00010001u;
-  const uint32_t nw = gridDim.x * (blockDim.x / 32);
-  for (uint32_t p = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < total; p += nw) {
+  // short-lived CTAs (kFinalizeSteps warp steps each, not grid-stride): beside the path walkers, the
+  // scheduler hands their SM slots to the higher-priority stream as they retire
+  const uint32_t w0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kFinalizeSteps;
+  for (uint32_t p = w0; p < total && p < w0 + kFinalizeSteps; ++p) {
     const uint32_t row = p / groups, wb = 2 * P * (p - row * groups);
     const size_t rb = (size_t)row * bg.wpr;
     // lanes 0 .. 2P-1: the covered (the tile's home plane; nothing in a tile no block processed) and free
-    // words of the group's row words, and the walkers' plane word
+    // words of the group's row words
     uint32_t fv = 0, cv = 0;
     const uint32_t wl = wb + lane;
     if (lane < 2 * P && wl < bg.wpr) {
       const uint4 pv = __ldcg(bk.P + rb + wl);
       const uint32_t st = (uint32_t)__ldcg(bk.state + (row / kBTR) * bg.tbands + wl / kBTW);
-      const uint2 t01 = __ldcg(reinterpret_cast<const uint2*>(bk.T + (rb + wl) * 16));
       fv = pv.z;
       cv = st == 0u ? 0u : (st & 1u) ? pv.y : pv.x;
-      __stcg(bk.P + rb + wl, make_uint4(cv, t01.x, fv, t01.y));  // {covered, u bit 0, free, u bit 1}
     }
     uint32_t x[P];  // lanes 16 .. 31 read the next row word's planes (wpr is even)
 #pragma unroll
@@ -678,7 +679,10 @@ void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBo
 
 void launch_bits_finalize(const BitGeo& bg, const Geo& g, BitBook bk, uint32_t lref, uint16_t* field, int sms,
                           cudaStream_t s) {
-  k_bits_finalize<<<sms * 8, 256, 0, s>>>(bg, g, bk, lref, field);
+  (void)sms;
+  const uint64_t total = (uint64_t)bg.H * ((bg.wpr / 2 + 3) / 4);  // warp steps (P = 4 row-word pairs each)
+  const uint64_t ctas = (total + 8 * kFinalizeSteps - 1) / (8 * kFinalizeSteps);
+  k_bits_finalize<<<(unsigned)ctas, 256, 0, s>>>(bg, g, bk, lref, field);
 }
 
 void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uint32_t nl, FlagSink flag,

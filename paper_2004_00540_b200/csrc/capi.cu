@@ -39,7 +39,11 @@ am_status am_ctx_create(const am_ctx_opts* opts, am_ctx** out) {
   ctx->device = opts ? opts->device : 0;
   ctx->flags = opts ? opts->flags : 0;
   cudaError_t e = cudaSetDevice(ctx->device);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  // the context stream at the highest priority: work beside it (the field encoding on the map stream)
+  // gives up SM slots to the path walkers as its short CTAs retire
+  int prio_least = 0, prio_greatest = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_greatest);
   if (e == cudaSuccess) {
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
@@ -80,6 +84,10 @@ void am_ctx_destroy(am_ctx* ctx) {
   for (auto& e : ctx->copy_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->map_stream) {
+    cudaStreamSynchronize(ctx->map_stream);
+    cudaStreamDestroy(ctx->map_stream);
+  }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);  // deferred by the driver while grids still hold memory
   delete ctx;
@@ -114,6 +122,7 @@ am_status am_ctx_get_stream(const am_ctx* ctx, void** stream) {
 
 am_status am_ctx_synchronize(am_ctx* ctx) {
   if (!ctx) return AM_EINVAL;
+  if (ctx->map_stream) CK(cudaStreamSynchronize(ctx->map_stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return AM_OK;
 }
@@ -162,6 +171,7 @@ static void grid_free(am_ctx* ctx, am_grid* g) {
   am::dfree(ctx, g->d_tgt);
   am::dfree(ctx, g->d_counts);
   am::dfree(ctx, g->d_sched);
+  if (g->map_ev) cudaEventDestroy(g->map_ev);
   am::dfree(ctx, g->d_offsets);
   am::dfree(ctx, g->d_status);
   am::dfree(ctx, g->d_pts);
@@ -323,6 +333,7 @@ am_status am_grid_destroy(am_ctx* ctx, am_grid* g) {
   if (!g) return AM_OK;
   if (!ctx) return AM_EINVAL;  // the grid's buffers belong to the context's pool
   cudaSetDevice(ctx->device);
+  am::join_map(ctx, g);
   cudaStreamSynchronize(ctx->stream);
   grid_free(ctx, g);
   return AM_OK;
@@ -463,6 +474,13 @@ static am_status bits_build_planes(am_ctx* ctx, am_grid* g, const uint32_t* pack
   return AM_OK;
 }
 
+am_status join_map(am_ctx* ctx, am_grid* g) {
+  if (!g || !g->map_pending) return AM_OK;
+  g->map_pending = 0;
+  CK(cudaStreamWaitEvent(ctx->stream, g->map_ev, 0));
+  return AM_OK;
+}
+
 // Allocates the bit-plane state and builds the free plane from the grid's occupancy (occupancy is
 // immutable, so this runs once per grid: at creation for single grids, else on first use).
 am_status bits_alloc(am_ctx* ctx, am_grid* g, const uint32_t* packed) {
@@ -574,10 +592,21 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
     launch_publish_flag(unpublished, s);
     CKL();
   }
-  launch_bits_finalize(bg, g->g, B.bk, lref, field, ctx->sms, s);  // the encoded field, once
-  CKL();
-  ctx->launches += 1;
   if (timing) CK(cudaEventRecord(ctx->timers[0].b, s));
+  // the encoded field, once, on the map stream: path counts and walkers read the planes meanwhile
+  if (!ctx->map_stream) {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CK(cudaStreamCreateWithPriority(&ctx->map_stream, cudaStreamNonBlocking, least));
+  }
+  if (!g->map_ev) CK(cudaEventCreateWithFlags(&g->map_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(g->map_ev, s));
+  CK(cudaStreamWaitEvent(ctx->map_stream, g->map_ev, 0));
+  launch_bits_finalize(bg, g->g, B.bk, lref, field, ctx->sms, ctx->map_stream);
+  CKL();
+  CK(cudaEventRecord(g->map_ev, ctx->map_stream));
+  g->map_pending = 1;
+  ctx->launches += 1;
   while (!pend.empty())
     if ((st = drain_one())) return st;
   unsigned long long stat[8] = {};
@@ -596,6 +625,7 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
       used = target;
       cause = any_zero ? AM_STOP_CAP : AM_STOP_FILLED;
     } else {
+      if ((st = join_map(ctx, g))) return st;
       *handoff = true;  // field at layer lref, beyond the 16-bit range: continue with the tile kernels
       CK(cudaMemsetAsync(g->val[1], 0, vbytes, s));
       g->dirty[1] = 0;
@@ -645,6 +675,8 @@ am_status drive_propagation(std::vector<SlabRef>& slabs, Transport* tr, uint32_t
   // 16-bit cells unless the run can never fit (fixed L beyond the 16-bit range)
   const int start_bits = (!autom && (uint64_t)target + 1 > kMax16Activity) ? 32 : 16;
   am_status st;
+  for (auto& sr : slabs)  // a previous run's field encoding still reads the planes this run rewrites
+    if ((st = join_map(sr.ctx, sr.g))) return st;
   uint32_t l_init = 0;  // layer the field holds when the loop below starts
   am_prop_result pre{};
   if (bits_eligible(slabs, tr, mode, start_bits)) {
@@ -1055,6 +1087,8 @@ static am_status download_impl(am_ctx* ctx, am_grid* g, uint32_t* dst, bool dst_
   if (!ctx || !g || !dst) return AM_EINVAL;
   if (!g->have_map) return am::fail(ctx, AM_EINVAL, "no activity map: call am_propagate first");
   CK(cudaSetDevice(ctx->device));
+  am_status jst = am::join_map(ctx, g);
+  if (jst) return jst;
   cudaStream_t s = ctx->stream;
   const size_t W = g->g.W, H = g->g.H;
   if (g->plain_active) {
@@ -1111,6 +1145,7 @@ am_status am_activity_upload(am_ctx* ctx, am_grid* g, const uint32_t* dense, uin
   if (!ctx || !g || !dense) return AM_EINVAL;
   if (g->slab) return am::fail(ctx, AM_EINVAL, "activity upload on a slab grid");
   CK(cudaSetDevice(ctx->device));
+  if (am_status jst = am::join_map(ctx, g)) return jst;
   const size_t n = (size_t)g->g.W * g->g.H;
   if (!g->plain) CK(am::dmalloc(ctx, &g->plain, n * 4));
   CK(cudaMemcpyAsync(g->plain, dense, n * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -1269,9 +1304,14 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   CK(cudaMemcpyAsync(g->d_status, status, n * 4, cudaMemcpyHostToDevice, s));
   ctx->h2d_bytes += n * 8 + (n + 1) * 8 + n * 4;
   // the counts are consumed (offsets came from the caller): their buffer holds the trace order
-  am::launch_trace(view_of(g), g->d_tgt, n, (int)method, seed, g->d_offsets, direct ? direct : g->d_pts,
-                   g->d_status, s, ~0ull, reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);
-  CKL();
+  {
+    const am::MapView m = view_of(g);
+    if (!m.bt && (st = am::join_map(ctx, g))) return st;  // the walkers read the field
+    am::launch_trace(m, g->d_tgt, n, (int)method, seed, g->d_offsets, direct ? direct : g->d_pts, g->d_status, s,
+                     ~0ull, reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);
+    CKL();
+    if ((st = am::join_map(ctx, g))) return st;  // the map is complete when the paths are
+  }
   if (cell_h) {
     am::launch_paths_local(g->d_pts, g->d_offsets, g->d_status, n, cell_h, cell_w, s);
     CKL();
@@ -1317,10 +1357,11 @@ am_status am_trace_paths_device(am_ctx* ctx, am_grid* g, const uint32_t* d_tgt, 
   am::launch_scan(g->d_counts, n, d_offsets, s);
   CKL();
   // paths past cap: AM_EINVAL; the counts are scanned into d_offsets, so their buffer holds the trace order
+  if (!m.bt && (st = am::join_map(ctx, g))) return st;  // the walkers read the field
   am::launch_trace(m, d_tgt, n, (int)method, seed, d_offsets, d_pts, d_status, s, cap,
                    reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);
   CKL();
-  return AM_OK;
+  return am::join_map(ctx, g);  // the map is complete when the paths are
 }
 
 // -------------------------------------------------------- single-shot ops
@@ -1430,6 +1471,7 @@ am_status am_bench_tile_kernel(am_ctx* ctx, am_grid* g, uint32_t items, uint32_t
                                float* ms_per_launch) {
   if (!ctx || !g || !ms_per_launch || !g->t_state || reps == 0 || stride == 0) return AM_EINVAL;
   CK(cudaSetDevice(ctx->device));
+  if (am_status jst = am::join_map(ctx, g)) return jst;
   am_status st = am::reset_map(ctx, g, 16);
   if (st) return st;
   g->have_map = 0;

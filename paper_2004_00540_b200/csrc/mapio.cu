@@ -853,6 +853,7 @@ am_status am_activity_export_pgm(am_ctx* ctx, am_grid* g, uint8_t* out, uint64_t
   if (!g->have_map) return fail(ctx, AM_EINVAL, "no activity map: call am_propagate first");
   if (g->slab) return fail(ctx, AM_EINVAL, "PGM export of a slab grid: gather it first");
   CK(cudaSetDevice(ctx->device));
+  if (am_status jst = am::join_map(ctx, g)) return jst;
   if (g->plain_active) return pgm_impl(ctx, g->g, 0, g->plain, 0, out, capacity, length);
   return pgm_impl(ctx, g->g, g->cell_bits, g->val[g->cur], g->computed - g->layers_used, out, capacity, length);
 }

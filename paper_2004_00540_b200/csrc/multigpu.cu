@@ -450,6 +450,7 @@ Transport* make_peer_transport(am_ctx* ctx, am_grid* g) { return new PeerTranspo
 
 // Places a propagated slab's own rows into the full grid's field.
 static am_status adopt_full(am_ctx* ctx, am_grid* full, const am_grid* like) {
+  if (am_status jst = join_map(ctx, full)) return jst;  // the full grid's own field encoding
   am_status st = set_cell_bits(ctx, full, like->cell_bits);
   if (st) return st;
   full->cur = 0;

@@ -24,6 +24,11 @@ struct Reader {
     return m.row<uint32_t>(r + (int)m.g.pad)[ac];
   }
   __device__ __forceinline__ uint32_t value(uint32_t r, uint32_t c) const {
+    if (m.bt) {  // bit-plane map: covered cells hold (lref - u) mod 2^14 (lref + 1 at sources)
+      uint32_t f;
+      if (!m.bword(r, c, &f)) return 0u;
+      return (m.layers - m.bu(r, c)) & kBTSrcU;
+    }
     if (m.cell_bits == 16) {
       const uint32_t v = raw((int)r, (int)c);
       return (v & kFlag16) ? (v & 0x7FFFu) : 0u;
@@ -48,6 +53,11 @@ struct Reader {
     return m.srcmask[(size_t)r * m.g.W + c] != 0;
   }
   __device__ __forceinline__ bool obstacle(uint32_t r, uint32_t c) const {
+    if (m.bt) {
+      uint32_t f;
+      (void)m.bword(r, c, &f);
+      return !f;
+    }
     if (m.cell_bits == 16) return !(raw((int)r, (int)c) & kFlag16);
     if (m.cell_bits == 32) return !(raw((int)r, (int)c) & kFlag32);
     return m.occ[(size_t)r * m.g.W + c] != 0;
@@ -386,8 +396,8 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
 // 8-neighbour n is an ascent candidate of c (activity + 1) exactly when both are covered and
 // u_c - u_n == 1 (activities of covered 8-neighbours differ by <= 1, activity = lref - u), and mod 4 that
 // is two LOP3s per 32 cells: (a0 ^ b0) & ~(a1 ^ b1 ^ b0) with a = u_c, b = u_n.  A warp stages a 64 x 64
-// window (two rows of two words per lane, one 16 B plane word {covered, u bit 0, free, u bit 1} each, as
-// k_bits_finalize leaves them),
+// window (two rows of two words per lane: per word the covered word of the tile's home plane, by its state,
+// and time planes 0 and 1 -- the propagation's own planes, read while k_bits_finalize encodes the field),
 // builds every cell's candidates for all 8 directions with shifts and shuffles of whole words and stores
 // one 16 B record per word in shared memory.  Euclidean rule (pin P1): the first candidate of L, R, U, D,
 // UL, UR, DL, DR, kept as four move planes (row +1, row -1, column +1, column -1), so a step is one
@@ -403,8 +413,9 @@ static_assert(kPTab <= kWinBytes, "plane window records");
 // Stages the plane window around (r, c), 8 cells behind it in its direction of travel (ldr, ldc), and
 // builds the window records (out of line: the step loop stays short).
 template <int METHOD>
-__device__ __noinline__ int2 stage_planes(const uint4* __restrict__ bp, uint32_t H, uint32_t wpr, uint32_t r,
-                                          uint32_t c, int ldr, int ldc, uint4* tab) {
+__device__ __noinline__ int2 stage_planes(const uint4* __restrict__ bp, const uint32_t* __restrict__ bt,
+                                          const unsigned long long* __restrict__ bstate, uint32_t H, uint32_t wpr,
+                                          uint32_t tbands, uint32_t r, uint32_t c, int ldr, int ldc, uint4* tab) {
   // scalars by value and the origin returned in registers: a reference to the MapView would put the
   // whole view in local memory for this out-of-line call
   const int lane = threadIdx.x & 31;
@@ -421,10 +432,13 @@ __device__ __noinline__ int2 stage_planes(const uint4* __restrict__ bp, uint32_t
       const int gr = wr + 2 * lane + i, gw = (wc >> 5) + x;
       X[i][x] = A0[i][x] = A1[i][x] = 0u;
       if (gr >= 0 && gr < (int)H && gw >= 0 && gw < (int)wpr) {  // planes are read-only here: L1
-        const uint4 p = __ldg(bp + (size_t)gr * wpr + gw);  // {covered, u bit 0, free, u bit 1}
-        X[i][x] = p.x;
-        A0[i][x] = p.y;
-        A1[i][x] = p.w;
+        const size_t pw = (size_t)gr * wpr + gw;
+        const uint4 p = __ldg(bp + pw);                                      // {cov 0, cov 1, free, -}
+        const uint2 u01 = __ldg(reinterpret_cast<const uint2*>(bt + pw * 16));  // t - 1, bits 0 and 1
+        const uint32_t st = (uint32_t)__ldg(bstate + ((uint32_t)gr / kBTR) * tbands + (uint32_t)gw / kBTW);
+        X[i][x] = st == 0u ? 0u : (st & 1u) ? p.y : p.x;
+        A0[i][x] = u01.x;
+        A1[i][x] = u01.y;
       }
     }
   // rows above / below each of the lane's two rows
@@ -501,9 +515,11 @@ __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64
   uint64_t rng = seed;
   int wr = 0, wc = 0, ldr = 0, ldc = 0;
   const uint4* const bp = m.bp;
-  const uint32_t bh = m.bg.H, bw = m.bg.wpr;
+  const uint32_t* const bt = m.bt;
+  const unsigned long long* const bs = m.bstate;
+  const uint32_t bh = m.bg.H, bw = m.bg.wpr, btb = m.bg.tbands;
   auto stage = [&]() {
-    const int2 o = stage_planes<METHOD>(bp, bh, bw, r, c, ldr, ldc, tab);
+    const int2 o = stage_planes<METHOD>(bp, bt, bs, bh, bw, btb, r, c, ldr, ldc, tab);
     wr = o.x;
     wc = o.y;
   };
