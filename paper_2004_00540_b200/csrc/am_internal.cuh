@@ -253,6 +253,7 @@ struct MapView {
   const uint8_t* occ;     // plain mode only: dense occupancy
   uint32_t layers;        // layers represented by the values (for point counts)
   const SlabDir* dir = nullptr;  // encoded maps only: the field is distributed over row slabs (val unused)
+  uint32_t cell_h = 0, cell_w = 0;  // > 0: mazes packed on this lattice, paths written maze-local
   // maps of a bit-plane run (bits.cu) whose planes are intact: path counts and walkers read the planes
   // (the encoded field may still be in flight on the map stream)
   const uint4* bp = nullptr;                 // {covered (home 0), covered (home 1), free, -} per plane word
@@ -293,9 +294,5 @@ void launch_trace(const MapView& m, const uint32_t* tgt_rc, uint64_t n, int meth
                   uint64_t pts_capacity = ~0ull, uint32_t* order = nullptr, uint32_t* sched = nullptr, int sms = 0);
 // scratch of launch_trace's longest-first scheduling: order (n words) and sched (this many words)
 constexpr int kTraceSchedWords = 1024 + 2;
-// paths in a grid of mazes packed on a cell_h x cell_w lattice -> each path's maze-local coordinates
-// (the maze is the one of the path's first point, its target)
-void launch_paths_local(uint32_t* pts_rc, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,
-                        uint32_t cell_w, cudaStream_t s);
 
 }  // namespace am

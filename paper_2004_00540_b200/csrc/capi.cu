@@ -1286,7 +1286,7 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   // A pinned (device-mapped) destination takes the points straight from the walkers: the 32-point
   // warp stores cross PCIe while the walk runs instead of a separate copy afterwards.
   uint32_t* direct = nullptr;
-  if (!cell_h && total) {
+  if (total) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, pts) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
       direct = static_cast<uint32_t*>(at.devicePointer);
@@ -1305,16 +1305,14 @@ am_status trace_paths_host(am_ctx* ctx, am_grid* g, const uint32_t* tgt, uint64_
   ctx->h2d_bytes += n * 8 + (n + 1) * 8 + n * 4;
   // the counts are consumed (offsets came from the caller): their buffer holds the trace order
   {
-    const am::MapView m = view_of(g);
+    am::MapView m = view_of(g);
+    m.cell_h = cell_h;  // batch lattices: the walkers write maze-local points
+    m.cell_w = cell_w;
     if (!m.bt && (st = am::join_map(ctx, g))) return st;  // the walkers read the field
     am::launch_trace(m, g->d_tgt, n, (int)method, seed, g->d_offsets, direct ? direct : g->d_pts, g->d_status, s,
                      ~0ull, reinterpret_cast<uint32_t*>(g->d_counts), g->d_sched, ctx->sms);
     CKL();
     if ((st = am::join_map(ctx, g))) return st;  // the map is complete when the paths are
-  }
-  if (cell_h) {
-    am::launch_paths_local(g->d_pts, g->d_offsets, g->d_status, n, cell_h, cell_w, s);
-    CKL();
   }
   if (total && !direct) CK(cudaMemcpyAsync(pts, g->d_pts, total * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(status, g->d_status, n * 4, cudaMemcpyDeviceToHost, s));

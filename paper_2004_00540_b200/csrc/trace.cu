@@ -17,6 +17,7 @@ enum : int32_t { ST_OK = 0, ST_EINVAL = 1, ST_EUNCOVERED = 2, ST_EINTERNAL = 6 }
 
 struct Reader {
   MapView m;
+  uint32_t or0 = 0, oc0 = 0;  // subtracted from every written point (a batch maze's origin: maze-local paths)
   // raw encoded cell at grid (r, c); (r, c) may lie up to the padding width outside the grid
   __device__ __forceinline__ uint32_t raw(int r, int c) const {
     const int ac = c + (int)m.g.pad;
@@ -89,8 +90,8 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
   uint32_t cur = rd.value(r, c);
   uint64_t n = 1;
   if (WRITE && lane == 0) {
-    out[0] = r;
-    out[1] = c;
+    out[0] = r - rd.or0;
+    out[1] = c - rd.oc0;
   }
   while (!rd.source(r, c)) {
     if (n >= limit) {
@@ -151,8 +152,8 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
     c = (uint32_t)((long)c + kDC[sel]);
     cur = best;
     if (WRITE && lane == 0) {
-      out[2 * n] = r;
-      out[2 * n + 1] = c;
+      out[2 * n] = r - rd.or0;
+      out[2 * n + 1] = c - rd.oc0;
     }
     ++n;
   }
@@ -226,7 +227,7 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
   uint32_t keep_r = 0, keep_c = 0;  // point n of this lane's slot (n % 32 == lane)
   auto record = [&]() {
     if ((int)(n & 31) == lane) keep_r = r, keep_c = c;
-    if ((n & 31) == 31) reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r, keep_c);
+    if ((n & 31) == 31) reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r - rd.or0, keep_c - rd.oc0);
     ++n;
   };
   record();
@@ -290,7 +291,7 @@ __device__ uint64_t walk_smem(const Reader& rd, uint32_t r, uint32_t c, int meth
   }
   // flush the partial group of points
   const uint64_t base = n & ~(uint64_t)31;
-  if (base + lane < n) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(keep_r, keep_c);
+  if (base + lane < n) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(keep_r - rd.or0, keep_c - rd.oc0);
   if (!rd.source(r, c)) *st = ST_EINTERNAL;  // a non-source at the top value would violate the law
   return n;
 }
@@ -351,7 +352,7 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
   uint32_t keep_r = 0, keep_c = 0;
   auto record = [&]() {
     if ((int)(n & 31) == lane) keep_r = r, keep_c = c;
-    if ((n & 31) == 31) reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r, keep_c);
+    if ((n & 31) == 31) reinterpret_cast<uint2*>(out)[n - 31 + lane] = make_uint2(keep_r - rd.or0, keep_c - rd.oc0);
     ++n;
   };
   record();
@@ -386,7 +387,7 @@ __device__ uint64_t walk_eucl2(const Reader& rd, uint32_t r, uint32_t c, uint64_
     record();
   }
   const uint64_t base = n & ~(uint64_t)31;
-  if (base + lane < n) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(keep_r, keep_c);
+  if (base + lane < n) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(keep_r - rd.or0, keep_c - rd.oc0);
   if (!rd.source(r, c)) *st = ST_EINTERNAL;
   return n;
 }
@@ -528,7 +529,7 @@ __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64
   uint2 pt = make_uint2(r, c);
   auto flush = [&](uint32_t upto) {  // points [(upto - 1) & ~31, upto) are held by the lanes
     const uint32_t base = (upto - 1) & ~31u;
-    if (base + lane < upto) reinterpret_cast<uint2*>(out)[base + lane] = pt;
+    if (base + lane < upto) reinterpret_cast<uint2*>(out)[base + lane] = make_uint2(pt.x - rd.or0, pt.y - rd.oc0);
   };
   int lr = 0, lc = 0;
   bool fresh = false;  // the window was staged for the current cell
@@ -623,6 +624,10 @@ __device__ __forceinline__ void trace_one(const MapView& m, const uint32_t* __re
     return;
   }
   int32_t st = ST_OK;
+  if (m.cell_h) {  // mazes packed on a lattice: points in the coordinates of the target's maze
+    rd.or0 = tgt[2 * w] / m.cell_h * m.cell_h;
+    rd.oc0 = tgt[2 * w + 1] / m.cell_w * m.cell_w;
+  }
   const bool planes = AM_TRACE_PLANES && m.bt && m.cell_bits == 16 && !m.dir;
   const uint64_t got = planes ? (method == 1 ? walk_planes<1>(rd, tgt[2 * w], tgt[2 * w + 1], seed, (uint32_t)limit,
                                                               pts + 2 * off, &st, reinterpret_cast<uint4*>(win))
@@ -724,24 +729,7 @@ void launch_path_counts(const MapView& m, const uint32_t* tgt, uint64_t n, int m
   k_path_counts<<<blocks, 128, 0, s>>>(m, tgt, n, method, seed, counts, status);
 }
 
-__global__ void k_paths_local(uint32_t* __restrict__ pts, const uint64_t* __restrict__ offsets,
-                              const int32_t* __restrict__ status, uint64_t n, uint32_t cell_h, uint32_t cell_w) {
-  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= n || status[w] != ST_OK) return;
-  const uint64_t b = offsets[w], e = offsets[w + 1];
-  if (b == e) return;
-  const uint32_t r0 = pts[2 * b] / cell_h * cell_h, c0 = pts[2 * b + 1] / cell_w * cell_w;
-  for (uint64_t p = b + (threadIdx.x & 31); p < e; p += 32) {
-    uint2 v = reinterpret_cast<const uint2*>(pts)[p];
-    reinterpret_cast<uint2*>(pts)[p] = make_uint2(v.x - r0, v.y - c0);
-  }
-}
 
-void launch_paths_local(uint32_t* pts, const uint64_t* offsets, const int32_t* status, uint64_t n, uint32_t cell_h,
-                        uint32_t cell_w, cudaStream_t s) {
-  if (!n) return;
-  k_paths_local<<<(unsigned)((n * 32 + 127) / 128), 128, 0, s>>>(pts, offsets, status, n, cell_h, cell_w);
-}
 
 #ifndef AM_TRACE_SCHED
 #define AM_TRACE_SCHED 1  // longest-first scheduling of the targets (k_trace_order)
