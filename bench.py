@@ -656,6 +656,13 @@ def run_b200(args, rank, world, local_rank):
     ev[2].record(stream)
     ctx.synchronize()
     prop_ms, path_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    # the same trace again, alone: after a bit-plane run the field encoding runs on the map stream beside
+    # the first trace (and is joined by it), so "paths" above is max(walk, encoding); this is the walk
+    ev[1].record(stream)
+    sol.trace()
+    ev[2].record(stream)
+    ctx.synchronize()
+    walk_ms = ev[1].elapsed_time(ev[2])
 
     launches0 = ctx.kernel_launches()
     if dist:
@@ -793,13 +800,18 @@ def run_b200(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u16x2" if res.cell_bits == 16 else "u32",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": ("u32 bit planes (1 bit per cell), u16 field" if res.engine == "bits" else
+                      "u16x2" if res.cell_bits == 16 else "u32"),
             "data": "synthetic",
             "config": bench_config(world),
             "time_to_solve_s": round(ms_step / 1000, 4),
             "layers_used": L, "layers_computed": res.layers_computed,
             "termination": ["filled", "stalled", "cap"][res.cause],
-            "phase_ms": {"propagate": round(prop_ms, 3), "paths": round(path_ms, 3),
+            "phase_ms": {"propagate": round(prop_ms, 3), "paths": round(path_ms, 3), "walk_alone": round(walk_ms, 3),
+                         "note": "paths = path counts + walks, overlapped with the field encoding of the "
+                                 "bit-plane run (map stream); walk_alone = the same calls without it",
+                         "walk_share": round(walk_ms / max(prop_ms + path_ms, 1e-9), 4),
                          "path_share": round(path_ms / max(prop_ms + path_ms, 1e-9), 4)},
             "stencil_gcell_per_s": round(stencil_gcells, 2),
             "propagate_gcell_per_s": round(cell_updates / (prop_ms / 1000) / 1e9, 1),
