@@ -811,7 +811,7 @@ def run_b200(args, rank, world, local_rank):
             "phase_ms": {"propagate": round(prop_ms, 3), "paths": round(path_ms, 3), "walk_alone": round(walk_ms, 3),
                          "note": "paths = path counts + walks, overlapped with the field encoding of the "
                                  "bit-plane run (map stream); walk_alone = the same calls without it",
-                         "walk_share": round(walk_ms / max(prop_ms + path_ms, 1e-9), 4),
+                         "walk_share_of_time_to_solve": round(walk_ms / ms_step, 4),
                          "path_share": round(path_ms / max(prop_ms + path_ms, 1e-9), 4)},
             "stencil_gcell_per_s": round(stencil_gcells, 2),
             "propagate_gcell_per_s": round(cell_updates / (prop_ms / 1000) / 1e9, 1),

@@ -586,37 +586,54 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
 // the free word -- and a 32 x 32 bit transpose over the lanes (five butterfly shuffles) leaves lane c
 // with cell c of both row words as a u16x2 {free, covered, u} pair: the encoding is then a handful of
 // word-wide ops, and two coalesced 64 B stores follow.
-constexpr uint32_t kFinalizeSteps = 4;
-__global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uint16_t* __restrict__ field) {
-  constexpr int P = 4;  // row-word pairs per warp step (loads of all of them in flight together)
+constexpr uint32_t kFinalizeSteps = 2;  // warp steps per warp (short-lived CTAs, see the launch)
+constexpr int kFinP = 4;                 // row-word pairs per warp step (their loads in flight together)
+__global__ void __launch_bounds__(256) k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref,
+                                                       uint16_t* __restrict__ field) {
+  constexpr int P = kFinP;
   constexpr uint32_t kUMask = (1u << kBTPlanes) - 1u, kU2 = kUMask | kUMask << 16;
   static_assert(kBTPlanes == 14, "planes 14 / 15 of a row word carry covered / free");
   const int lane = threadIdx.x & 31;
   const int k = lane & 15;
-  const uint32_t groups = (bg.wpr / 2 + P - 1) / P;
-  const uint32_t total = bg.H * groups;  // < 2^32: H, W <= 65535
+  const uint32_t row = blockIdx.y;  // one grid row per plane row: no index division
+  const size_t rb = (size_t)row * bg.wpr;
+  const uint32_t st_row = (row / kBTR) * bg.tbands;
   // per half: (lref + 2^kBTPlanes) - u >= 0, no borrow across the halves; the low kBTPlanes bits are
   // (lref - u) mod 2^kBTPlanes, which is lref + 1 at sources
   const uint32_t K2 = (lref + (1u << kBTPlanes)) * 0x00010001u;
-  // short-lived CTAs (kFinalizeSteps warp steps each, not grid-stride): beside the path walkers, the
-  // scheduler hands their SM slots to the higher-priority stream as they retire
-  const uint32_t w0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kFinalizeSteps;
-  for (uint32_t p = w0; p < total && p < w0 + kFinalizeSteps; ++p) {
-    const uint32_t row = p / groups, wb = 2 * P * (p - row * groups);
-    const size_t rb = (size_t)row * bg.wpr;
+  uint16_t* const frow = field + (size_t)(row + g.pad) * g.pitch + g.pad + lane;
+  uint32_t kp[5];  // the transpose's keep masks, materialised once per thread
+#pragma unroll
+  for (int jj = 0; jj < 5; ++jj) {
+    const int j = 16 >> jj;
+    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
+                                                                                                  : 0x55555555u;
+    kp[jj] = (lane & j) ? ~m : m;
+  }
+  const uint32_t wb0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kFinalizeSteps * 2 * P;
+#pragma unroll 1
+  for (uint32_t s = 0; s < kFinalizeSteps; ++s) {
+    const uint32_t wb = wb0 + s * 2 * P;  // first row word of the step (warp-uniform)
+    if (wb >= bg.wpr) break;
     // lanes 0 .. 2P-1: the covered (the tile's home plane; nothing in a tile no block processed) and free
-    // words of the group's row words
+    // words of the step's row words
     uint32_t fv = 0, cv = 0;
     const uint32_t wl = wb + lane;
     if (lane < 2 * P && wl < bg.wpr) {
       const uint4 pv = __ldcg(bk.P + rb + wl);
-      const uint32_t st = (uint32_t)__ldcg(bk.state + (row / kBTR) * bg.tbands + wl / kBTW);
+      const uint32_t st = (uint32_t)__ldcg(bk.state + st_row + wl / kBTW);
       fv = pv.z;
       cv = st == 0u ? 0u : (st & 1u) ? pv.y : pv.x;
     }
-    uint32_t x[P];  // lanes 16 .. 31 read the next row word's planes (wpr is even)
+    uint32_t x[P];  // lanes 16 .. 31 read the next row word's planes (wpr is even); every lane loads (an
+                    // unconditional load: no branch around it for the lanes that take covered / free)
+    const uint32_t* tb = bk.T + (rb + wb) * 16 + lane;
 #pragma unroll
-    for (int q = 0; q < P; ++q) x[q] = wb + 2 * q < bg.wpr ? __ldcs(bk.T + (rb + wb + 2 * q) * 16 + lane) : 0u;
+    for (int q = 0; q < P; ++q) {
+      x[q] = 0u;
+      if (wb + 2 * q < bg.wpr)  // warp-uniform
+        asm volatile("ld.global.cs.u32 %0, [%1];" : "=r"(x[q]) : "l"(tb + 32 * q));
+    }
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       const int from = 2 * q + (lane >> 4);
@@ -624,31 +641,37 @@ __global__ void k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref, uin
       x[q] = k == kBTPlanes ? c : k == kBTPlanes + 1 ? f : x[q];
     }
 #pragma unroll
-    for (int j = 16; j >= 1; j >>= 1) {
-      const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
-                                                                                                    : 0x55555555u;
+    for (int jj = 0; jj < 5; ++jj) {
+      const int j = 16 >> jj;
       // lanes with bit j set keep the bits of columns with bit j set and take the partner's, moved down by
       // j; the others keep / take the complementary columns, moved up: the rotated partner word supplies
-      // exactly the ~keep columns, so one bit-select merges them
-      const uint32_t keep = (lane & j) ? ~m : m;
+      // exactly the ~keep columns, so one bit-select (LOP3 0xE4) merges them
+      const uint32_t keep = kp[jj];
       const uint32_t rot = (lane & j) ? j : 32 - j;
 #pragma unroll
       for (int q = 0; q < P; ++q) {
         const uint32_t y = __shfl_xor_sync(0xffffffffu, x[q], j);
         const uint32_t r = __funnelshift_r(y, y, rot);
-        x[q] = (x[q] & keep) | (r & ~keep);
+        uint32_t o;
+        asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(o) : "r"(x[q]), "r"(r), "r"(keep));  // (x & keep) | (r & ~keep)
+        x[q] = o;
       }
     }
-    uint16_t* dst = field + (size_t)(row + g.pad) * g.pitch + g.pad + (size_t)wb * 32 + lane;
+    uint16_t* dst = frow + (size_t)wb * 32;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       const uint32_t v0 = x[q];                                      // per half: free | covered | u
       const uint32_t a = K2 - (v0 & kU2);                            // per half: low bits (lref - u) mod 2^14
       const uint32_t cm = ((v0 >> kBTPlanes) & 0x00010001u) * kUMask;  // per half: kUMask if covered
       const uint32_t v = (a & cm) | (v0 & 0x80008000u);              // covered implies free
-      const uint32_t col = (wb + 2 * q) * 32 + lane;
-      if (col < bg.W) dst[64 * q] = (uint16_t)(v & 0xFFFFu);
-      if (col + 32 < bg.W) dst[64 * q + 32] = (uint16_t)(v >> 16);
+      const uint32_t c0 = (wb + 2 * q) * 32;                         // warp-uniform
+      if (c0 + 64 <= bg.W) {  // both row words inside the grid
+        dst[64 * q] = (uint16_t)v;
+        dst[64 * q + 32] = (uint16_t)(v >> 16);
+      } else {
+        if (c0 + lane < bg.W) dst[64 * q] = (uint16_t)v;
+        if (c0 + 32 + lane < bg.W) dst[64 * q + 32] = (uint16_t)(v >> 16);
+      }
     }
   }
 }
@@ -680,9 +703,9 @@ void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBo
 void launch_bits_finalize(const BitGeo& bg, const Geo& g, BitBook bk, uint32_t lref, uint16_t* field, int sms,
                           cudaStream_t s) {
   (void)sms;
-  const uint64_t total = (uint64_t)bg.H * ((bg.wpr / 2 + 3) / 4);  // warp steps (P = 4 row-word pairs each)
-  const uint64_t ctas = (total + 8 * kFinalizeSteps - 1) / (8 * kFinalizeSteps);
-  k_bits_finalize<<<(unsigned)ctas, 256, 0, s>>>(bg, g, bk, lref, field);
+  const uint32_t words_per_cta = 8 * kFinalizeSteps * 2 * kFinP;  // 8 warps
+  const dim3 grid((bg.wpr + words_per_cta - 1) / words_per_cta, bg.H);
+  k_bits_finalize<<<grid, 256, 0, s>>>(bg, g, bk, lref, field);
 }
 
 void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uint32_t nl, FlagSink flag,

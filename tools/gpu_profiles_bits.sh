@@ -27,7 +27,7 @@ if [[ "$ARGS" == *" full "* ]]; then
   done
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_bits_finalize -c 1 \
     -o gpurun_out/prof_finalize -f $CMD > gpurun_out/ncu_finalize.log 2>&1; echo "ncu_finalize_rc=$?"
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_trace -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_trace$' -c 1 \
     -o gpurun_out/prof_trace -f $CMD > gpurun_out/ncu_trace.log 2>&1; echo "ncu_trace_rc=$?"
 fi
 if [[ "$ARGS" == *" dram "* ]]; then
