@@ -191,6 +191,9 @@ void launch_srcmask_dense(uint32_t W, uint32_t H, const uint32_t* d_src_rc, uint
 #ifndef AM_BRPL
 #define AM_BRPL 2
 #endif
+#ifndef AM_BITS_PCM
+#define AM_BITS_PCM 1
+#endif
 constexpr int kBK = AM_BK;
 constexpr int kBRPL = AM_BRPL;
 constexpr int kBTW = 4;
@@ -207,6 +210,17 @@ struct BitGeo {
   uint32_t rows;             // plane rows (nchunks * kBTR)
   __host__ __device__ uint32_t ntiles() const { return nchunks * tbands; }
   __host__ __device__ size_t plane_words() const { return (size_t)rows * wpr; }
+  // plane word (row, word) of P: column-major (a word column's rows contiguous), so the lane-per-row
+  // accesses of the tile kernel and the walkers touch 8 lines per warp instead of 32 (AM_BITS_PCM)
+  __host__ __device__ size_t pidx(uint32_t row, uint32_t word) const {
+#if AM_BITS_PCM
+    return (size_t)word * rows + row;
+#else
+    return (size_t)row * wpr + word;
+#endif
+  }
+  // row word (row, word) of the time planes T (16 words each): row-major
+  __host__ __device__ size_t tidx(uint32_t row, uint32_t word) const { return (size_t)row * wpr + word; }
 };
 BitGeo make_bit_geo(uint32_t W, uint32_t H);
 // Device state of a bit-plane run.  State words and lists work as in TileBook
@@ -262,15 +276,14 @@ struct MapView {
   BitGeo bg{};
   // covered / free bits and t - 1 of cell (r, c) of a bit-plane map (r < H, c < W)
   __device__ __forceinline__ uint32_t bword(uint32_t r, uint32_t c, uint32_t* free_bit) const {
-    const size_t w = (size_t)r * bg.wpr + (c >> 5);
-    const uint4 p = bp[w];
+    const uint4 p = bp[bg.pidx(r, c >> 5)];
     const uint32_t st = (uint32_t)bstate[(r / kBTR) * bg.tbands + (c >> 5) / kBTW];
     *free_bit = (p.z >> (c & 31)) & 1u;
     const uint32_t cov = st == 0u ? 0u : (st & 1u) ? p.y : p.x;
     return (cov >> (c & 31)) & 1u;
   }
   __device__ __forceinline__ uint32_t bu(uint32_t r, uint32_t c) const {
-    const uint32_t* t = bt + ((size_t)r * bg.wpr + (c >> 5)) * 16;
+    const uint32_t* t = bt + bg.tidx(r, c >> 5) * 16;
     uint32_t u = 0;
     for (int k = 0; k < kBTPlanes; ++k) u |= ((t[k] >> (c & 31)) & 1u) << k;
     return u;

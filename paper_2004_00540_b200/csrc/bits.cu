@@ -172,11 +172,11 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
       const int tr = lane * kBRPL + i - kBK;  // tile-relative row
       const int prow = (int)ic * kBTR + tr;
       const bool er = prow >= 0 && prow < (int)bg.rows;
-      const size_t rb = (size_t)(er ? prow : 0) * bg.wpr + (size_t)ib * kBTW;
+      const uint32_t prw = er ? (uint32_t)prow : 0u;
 #pragma unroll
       for (int x = 0; x < kBTW + 2; ++x) {
         const bool e = er && (x == 0 ? exl : (x == kBTW + 1 ? exr : true));
-        const uint4 v = e ? __ldcg(bk.P + rb + x - 1) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 v = e ? __ldcg(bk.P + bg.pidx(prw, ib * kBTW + x - 1)) : make_uint4(0u, 0u, 0u, 0u);
         R0[i][x] = v.x, R1[i][x] = v.y, RF[i][x] = v.z;
       }
     }
@@ -351,10 +351,10 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
 #pragma unroll
       for (int x = 0; x < kBTW; ++x) NW[i][x] = own ? C[i][x + 1] & ~C0[i][x] : 0u;
       if (!own) continue;
-      const size_t rw = (size_t)(tc * kBTR + (uint32_t)tr) * bg.wpr + (size_t)tb * kBTW;
-      uint32_t* dst = reinterpret_cast<uint32_t*>(bk.P + rw) + out_home;
+      const uint32_t orow = tc * kBTR + (uint32_t)tr;
 #pragma unroll
-      for (int x = 0; x < kBTW; ++x) __stcg(dst + 4 * x, C[i][x + 1]);
+      for (int x = 0; x < kBTW; ++x)
+        __stcg(reinterpret_cast<uint32_t*>(bk.P + bg.pidx(orow, tb * kBTW + x)) + out_home, C[i][x + 1]);
       uint32_t fr_any = 0;
 #pragma unroll
       for (int x = 0; x < kBTW; ++x) {
@@ -520,26 +520,39 @@ __global__ void k_bits_init(BitGeo bg, const uint8_t* __restrict__ occ, uint4* _
     const uint32_t bits = __ballot_sync(0xffffffffu, o[k] == 0);
     if (lane == k) mine = bits;
   }
-  if (w0 + lane < bg.wpr) P[(size_t)row * bg.wpr + w0 + lane] = make_uint4(0u, 0u, mine, 0u);  // not covered
+  if (w0 + lane < bg.wpr) P[bg.pidx(row, w0 + lane)] = make_uint4(0u, 0u, mine, 0u);  // not covered
   const uint32_t cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mine));
   if (lane == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
 }
 
 // Plane words {0, 0, free, 0} from packed occupancy rows (bit = obstacle, pw = (W + 31) / 32 words per row).
+// A CTA converts 32 rows x 32 words: read along the packed rows, written along P's layout (a shared-memory
+// transpose when P is column-major).
 __global__ void k_bits_init_packed(BitGeo bg, const uint32_t* __restrict__ packed, uint4* __restrict__ P,
                                    unsigned long long* __restrict__ free_cells) {
+  __shared__ uint32_t t[32][33];
   const uint32_t pw = (bg.W + 31) / 32;
-  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x, row = blockIdx.y;
-  uint32_t f = 0;
-  if (w < bg.wpr) {
+  const uint32_t w0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 warps
+  uint32_t cnt = 0;
+  for (uint32_t k = ty; k < 32; k += 8) {  // warp ty: rows r0 + k, lane: word w0 + tx
+    const uint32_t row = r0 + k, w = w0 + tx;
+    uint32_t f = 0;
     if (row < bg.H && w < pw) {
       const uint32_t valid = bg.W - 32 * w >= 32 ? 0xFFFFFFFFu : (1u << (bg.W - 32 * w)) - 1u;
       f = ~__ldg(packed + (size_t)row * pw + w) & valid;
     }
-    P[(size_t)row * bg.wpr + w] = make_uint4(0u, 0u, f, 0u);
+    t[k][tx] = f;
+    cnt += __popc(f);
   }
-  const uint32_t cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(f));
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
+  __syncthreads();
+  for (uint32_t k = ty; k < 32; k += 8) {
+    // AM_BITS_PCM: warp ty writes word w0 + k for rows r0 + tx (contiguous); else row r0 + k, words w0 + tx
+    const uint32_t row = AM_BITS_PCM ? r0 + tx : r0 + k, w = AM_BITS_PCM ? w0 + k : w0 + tx;
+    if (row < bg.rows && w < bg.wpr) P[bg.pidx(row, w)] = make_uint4(0u, 0u, AM_BITS_PCM ? t[tx][k] : t[k][tx], 0u);
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (tx == 0 && cnt) atomicAdd(free_cells, (unsigned long long)cnt);
 }
 
 // The tiles holding a source start the run with valid coverage in home plane 0: their plane-0 words are
@@ -553,7 +566,7 @@ __global__ void k_bits_src_clear(BitGeo bg, const uint32_t* __restrict__ rc, uin
   const uint32_t tc = rc[2 * s] / kBTR, tb = rc[2 * s + 1] / (32 * kBTW);
   for (int i = lane; i < kBTR * kBTW; i += 32) {
     const uint32_t row = tc * kBTR + (uint32_t)i / kBTW, wd = tb * kBTW + (uint32_t)i % kBTW;
-    if (row < bg.rows) bk.P[(size_t)row * bg.wpr + wd].x = 0u;
+    if (row < bg.rows) bk.P[bg.pidx(row, wd)].x = 0u;
   }
   if (lane == 0) bk.state[tc * bg.tbands + tb] = kBitsSrcState;
 }
@@ -566,10 +579,10 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
   if (s >= n) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const uint32_t r = rc[2 * s], c = rc[2 * s + 1];
-  const size_t rw = (size_t)r * bg.wpr + (c >> 5);
+  const size_t rw = bg.tidx(r, c >> 5);
   const uint32_t bit = 1u << (c & 31);
   if (lane == 0) {
-    const uint32_t old = atomicOr(&bk.P[rw].x, bit);
+    const uint32_t old = atomicOr(&bk.P[bg.pidx(r, c >> 5)].x, bit);
     if (!(old & bit)) atomicAdd(&bk.stat[1], 1ull);
   }
   if (lane < kBTPlanes) atomicOr(bk.T + rw * 16 + lane, bit);
@@ -620,7 +633,7 @@ __global__ void __launch_bounds__(256) k_bits_finalize(BitGeo bg, Geo g, BitBook
     uint32_t fv = 0, cv = 0;
     const uint32_t wl = wb + lane;
     if (lane < 2 * P && wl < bg.wpr) {
-      const uint4 pv = __ldcg(bk.P + rb + wl);
+      const uint4 pv = __ldcg(bk.P + bg.pidx(row, wl));
       const uint32_t st = (uint32_t)__ldcg(bk.state + st_row + wl / kBTW);
       fv = pv.z;
       cv = st == 0u ? 0u : (st & 1u) ? pv.y : pv.x;
@@ -690,7 +703,7 @@ void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStre
 }
 
 void launch_bits_init_packed(const BitGeo& bg, const uint32_t* packed, BitBook bk, cudaStream_t s) {
-  const dim3 grid((bg.wpr + 255) / 256, bg.rows);
+  const dim3 grid((bg.wpr + 31) / 32, (bg.rows + 31) / 32);
   k_bits_init_packed<<<grid, 256, 0, s>>>(bg, packed, bk.P, bk.stat + 2);
 }
 

@@ -416,7 +416,8 @@ static_assert(kPTab <= kWinBytes, "plane window records");
 template <int METHOD>
 __device__ __noinline__ int2 stage_planes(const uint4* __restrict__ bp, const uint32_t* __restrict__ bt,
                                           const unsigned long long* __restrict__ bstate, uint32_t H, uint32_t wpr,
-                                          uint32_t tbands, uint32_t r, uint32_t c, int ldr, int ldc, uint4* tab) {
+                                          uint32_t tbands, uint32_t prows, uint32_t r, uint32_t c, int ldr, int ldc,
+                                          uint4* tab) {
   // scalars by value and the origin returned in registers: a reference to the MapView would put the
   // whole view in local memory for this out-of-line call
   const int lane = threadIdx.x & 31;
@@ -433,8 +434,8 @@ __device__ __noinline__ int2 stage_planes(const uint4* __restrict__ bp, const ui
       const int gr = wr + 2 * lane + i, gw = (wc >> 5) + x;
       X[i][x] = A0[i][x] = A1[i][x] = 0u;
       if (gr >= 0 && gr < (int)H && gw >= 0 && gw < (int)wpr) {  // planes are read-only here: L1
-        const size_t pw = (size_t)gr * wpr + gw;
-        const uint4 p = __ldg(bp + pw);                                      // {cov 0, cov 1, free, -}
+        const size_t pw = (size_t)gr * wpr + gw;  // time planes: row-major
+        const uint4 p = __ldg(bp + (AM_BITS_PCM ? (size_t)gw * prows + gr : pw));  // {cov 0, cov 1, free, -}
         const uint2 u01 = __ldg(reinterpret_cast<const uint2*>(bt + pw * 16));  // t - 1, bits 0 and 1
         const uint32_t st = (uint32_t)__ldg(bstate + ((uint32_t)gr / kBTR) * tbands + (uint32_t)gw / kBTW);
         X[i][x] = st == 0u ? 0u : (st & 1u) ? p.y : p.x;
@@ -518,9 +519,9 @@ __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64
   const uint4* const bp = m.bp;
   const uint32_t* const bt = m.bt;
   const unsigned long long* const bs = m.bstate;
-  const uint32_t bh = m.bg.H, bw = m.bg.wpr, btb = m.bg.tbands;
+  const uint32_t bh = m.bg.H, bw = m.bg.wpr, btb = m.bg.tbands, brows = m.bg.rows;
   auto stage = [&]() {
-    const int2 o = stage_planes<METHOD>(bp, bt, bs, bh, bw, btb, r, c, ldr, ldc, tab);
+    const int2 o = stage_planes<METHOD>(bp, bt, bs, bh, bw, btb, brows, r, c, ldr, ldc, tab);
     wr = o.x;
     wc = o.y;
   };
