@@ -265,3 +265,34 @@ def test_packed_occupancy_upload(w, h):
         g.close()
     finally:
         ctx.close()
+
+
+def test_map_stream_ordering():
+    """The field of a bit-plane run is encoded on the context's map stream beside the path walkers; every
+    reader joins it.  Interleave runs, walks and downloads on two grids of one context and check each map
+    against the oracle (a missing join shows up as a stale or half-encoded field)."""
+    ctx = am.Context(0)
+    try:
+        grids = []
+        for seed, (w, h) in enumerate([(1500, 900), (700, 1300)]):
+            occ = O.random_maze(w, h, 0.35, 40 + seed)
+            src = O.sample_free_cells(occ, 4, 41 + seed)
+            tgt = O.sample_free_cells(occ, 30, 42 + seed, exclude=src)
+            grids.append((occ, src, O.source_mask(occ, src), tgt, am.Grid(occ, src, ctx)))
+        for L in (9, 300, 64):
+            for occ, src, sm, tgt, g in grids:
+                g.propagate(L)
+            for occ, src, sm, tgt, g in reversed(grids):
+                g.trace(tgt, am.EUCLIDEAN)  # joins after its launch
+            for occ, src, sm, tgt, g in grids:
+                assert np.array_equal(g.activity(), O.propagate(occ, sm, L, threads=8)), L
+        occ, src, sm, tgt, g = grids[0]
+        r = g.propagate_auto(4000)
+        r2 = g.propagate_auto(4000)  # the second run starts while the first run's encoding may be in flight
+        assert (r.layers_used, r.cause) == (r2.layers_used, r2.cause)
+        hops = O.bfs_multi_source(occ, sm)
+        assert O.check_activity(occ, g.activity(), hops, r2.layers_used)[0] == 0
+        for *_, g in grids:
+            g.close()
+    finally:
+        ctx.close()
