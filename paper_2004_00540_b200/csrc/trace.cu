@@ -183,6 +183,9 @@ __device__ uint64_t walk(const Reader& rd, uint32_t r, uint32_t c, int method, u
 #define AM_TWC 32  // 16-bit window columns (smaller windows stage faster; tools/ab_trace.sh)
 #endif
 constexpr int kWinBytes = 4096;  // shared memory per warp: a window (<= 4 KB)
+#ifndef AM_TRACE_FAST
+#define AM_TRACE_FAST 1  // Euclidean plane walk: linear window index, flush outside the step loop
+#endif
 #ifndef AM_TRACE_PLANES
 #define AM_TRACE_PLANES 1  // bit-plane runs: walk on the coverage / time planes (walk_planes)
 #endif
@@ -539,6 +542,46 @@ __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64
   lc = (int)c - wc;
   fresh = true;
   uint32_t n = 1;
+  if (METHOD == 1 && AM_TRACE_FAST) {
+    // Euclidean rule, tight loop: the cell as one window index pos = row * 64 + column (its record is word
+    // pos >> 5, bit pos & 31), one index update per step, and the 32-point flush out of the step loop (the
+    // inner loop runs to the next multiple of 32 or the end of the path)
+    static_assert(kPW == 2, "window rows of 64 cells");
+    int pos = lr * 64 + lc;
+    while (n < limit) {
+      const uint32_t stop = min(limit, (n | 31u) + 1u);
+      bool leave = false;
+      while (n < stop) {
+        const uint4 q = tab[pos >> 5];
+        const uint32_t b = (uint32_t)pos & 31u;
+        const uint32_t dp = (q.x >> b) & 1u, dm = (q.y >> b) & 1u, cp = (q.z >> b) & 1u, cm = (q.w >> b) & 1u;
+        if (!(dp | dm | cp | cm)) {
+          leave = true;
+          break;
+        }
+        const int dr = (int)dp - (int)dm, dc = (int)cp - (int)cm;
+        pos += dr * 64 + dc;
+        r = (uint32_t)((int)r + dr);
+        c = (uint32_t)((int)c + dc);
+        ldr = dr;
+        ldc = dc;
+        pt = lane == (int)(n & 31) ? make_uint2(r, c) : pt;
+        ++n;
+        fresh = false;
+      }
+      if (leave) {  // no move inside this window: re-stage (SPEC.md:205 if it was just staged)
+        if (fresh) {
+          *st = ST_EINTERNAL;
+          return 0;
+        }
+        stage();
+        pos = ((int)r - wr) * 64 + ((int)c - wc);
+        fresh = true;
+        continue;
+      }
+      if ((n & 31) == 0) flush(n);
+    }
+  }
   while (n < limit) {
     int dr, dc;
     for (;;) {
