@@ -582,6 +582,53 @@ __device__ uint64_t walk_planes(const Reader& rd, uint32_t r, uint32_t c, uint64
       if ((n & 31) == 0) flush(n);
     }
   }
+  if (METHOD == 0 && AM_TRACE_FAST) {
+    // simple rule (pin P2), the same tight loop: the 8 candidate bits of the cell from its two records,
+    // the seeded draw only when >= 2 candidates tie
+    static_assert(kPW == 2, "window rows of 64 cells");
+    int pos = lr * 64 + lc;
+    while (n < limit) {
+      const uint32_t stop = min(limit, (n | 31u) + 1u);
+      bool leave = false;
+      while (n < stop) {
+        const uint4 q0 = tab[2 * (pos >> 5)], q1 = tab[2 * (pos >> 5) + 1];
+        const uint32_t b = (uint32_t)pos & 31u;
+        uint32_t mask = ((q0.x >> b) & 1u) | ((q0.y >> b) & 1u) << 1 | ((q0.z >> b) & 1u) << 2 |
+                        ((q0.w >> b) & 1u) << 3 | ((q1.x >> b) & 1u) << 4 | ((q1.y >> b) & 1u) << 5 |
+                        ((q1.z >> b) & 1u) << 6 | ((q1.w >> b) & 1u) << 7;
+        if (!mask) {
+          leave = true;
+          break;
+        }
+        const int cnt = __popc(mask);
+        if (cnt >= 2) {
+          const int pick = (int)__umul64hi(splitmix64(rng), (uint64_t)cnt);
+          for (int j = 0; j < pick; ++j) mask &= mask - 1;
+        }
+        const int k = __ffs(mask) - 1;
+        const int dr = (int)((PR >> (2 * k)) & 3u) - 1, dc = (int)((PC >> (2 * k)) & 3u) - 1;
+        pos += dr * 64 + dc;
+        r = (uint32_t)((int)r + dr);
+        c = (uint32_t)((int)c + dc);
+        ldr = dr;
+        ldc = dc;
+        pt = lane == (int)(n & 31) ? make_uint2(r, c) : pt;
+        ++n;
+        fresh = false;
+      }
+      if (leave) {
+        if (fresh) {
+          *st = ST_EINTERNAL;
+          return 0;
+        }
+        stage();
+        pos = ((int)r - wr) * 64 + ((int)c - wc);
+        fresh = true;
+        continue;
+      }
+      if ((n & 31) == 0) flush(n);
+    }
+  }
   while (n < limit) {
     int dr, dc;
     for (;;) {
