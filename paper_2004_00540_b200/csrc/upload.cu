@@ -5,7 +5,8 @@
 // host worker threads pack the caller's rows to 32-cell words (SSE2 compare + movemask, 16 bytes per
 // instruction) into a pinned staging buffer, chunk by chunk, and each chunk is copied (1/8 of the bytes)
 // and expanded back to the dense byte form on the device while the workers pack the next ones.  The packed
-// words stay on the device for the grid's free plane (bits.cu), so the bytes are read once.
+// words stay on the device for the grid's free plane (bits.cu), so the bytes are read once.  From a pinned
+// source a share of the rows crosses as raw bytes beside the workers and is packed on the device.
 #include <emmintrin.h>
 
 #include <algorithm>
@@ -127,6 +128,24 @@ __global__ void k_unpack_occ(const uint32_t* __restrict__ packed, uint32_t W, ui
     if (c < W) row[c] = (uint8_t)((v >> lane) & 1u);
   }
 }
+// Packed rows [r0, r1) from dense bytes already on the device (the raw-copied share of an upload): a warp
+// per 32 words of a row, 32 ballots over coalesced byte loads.
+__global__ void k_pack_occ(const uint8_t* __restrict__ occ, uint32_t W, uint32_t pw, uint32_t r0, uint32_t r1,
+                           uint32_t* __restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t r = r0 + blockIdx.y;
+  const uint32_t w0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32;
+  if (r >= r1 || w0 >= pw) return;  // warp-uniform
+  const uint8_t* row = occ + (size_t)r * W;
+  uint32_t mine = 0;
+#pragma unroll 8
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t c = (w0 + k) * 32 + lane;
+    const uint32_t obst = __ballot_sync(0xffffffffu, c < W && row[c] != 0);
+    if (lane == k) mine = obst;
+  }
+  if (w0 + lane < pw) packed[(size_t)r * pw + w0 + lane] = mine;
+}
 }  // namespace
 
 // Host occupancy rows [0, H) (W bytes each) -> d_occ (dense bytes) and ctx->d_pack (packed words, pw per
@@ -152,25 +171,56 @@ am_status upload_occupancy_packed(am_ctx* ctx, const uint8_t* occ, uint32_t W, u
   if (!ctx->hpool) ctx->hpool = new HostPool(pool_workers());
   HostPool& pool = *ctx->hpool;
   const int threads = (int)pool.th.size() + 1;
-  const uint32_t chunks = std::max(1u, std::min<uint32_t>(H, (uint32_t)threads * 4));
-  const uint32_t rows_per = (H + chunks - 1) / chunks;
-  const uint32_t nch = (H + rows_per - 1) / rows_per;
+  // A pinned source lets the copy engine take a share of the rows as raw bytes (packed on the device
+  // afterwards) while the host workers pack the rest: the workers are bound by host memory bandwidth, the
+  // copy engine by PCIe, so the two run side by side (AM_RAW_SHARE: the share in percent, default 20).
+  uint32_t raw_rows = 0;
+  {
+    cudaPointerAttributes at{};
+    static const int share = [] {
+      const char* v = getenv("AM_RAW_SHARE");
+      return v ? std::max(0, std::min(100, atoi(v))) : 20;
+    }();
+    if (share && cudaPointerGetAttributes(&at, occ) == cudaSuccess && at.type == cudaMemoryTypeHost)
+      raw_rows = (uint32_t)((uint64_t)H * share / 100);
+    (void)cudaGetLastError();
+  }
+  cudaStream_t s = ctx->stream;
+  if (raw_rows) {
+    if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    if (!ctx->copy_ev[0]) CK(cudaEventCreateWithFlags(&ctx->copy_ev[0], cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->copy_ev[0], s));  // d_occ / d_pack are free to overwrite (stream order)
+    CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[0], 0));
+    CK(cudaMemcpyAsync(d_occ, occ, (size_t)raw_rows * W, cudaMemcpyHostToDevice, ctx->copy_stream));
+    for (uint32_t r0 = 0; r0 < raw_rows; r0 += 65535) {  // grid.y limit
+      const uint32_t r1 = std::min(raw_rows, r0 + 65535);
+      const dim3 grid((pw + 32 * 8 - 1) / (32 * 8), r1 - r0);
+      k_pack_occ<<<grid, 256, 0, ctx->copy_stream>>>(d_occ, W, pw, r0, r1, ctx->d_pack);
+      ++ctx->launches;
+      CK(cudaPeekAtLastError());
+    }
+    CK(cudaEventRecord(ctx->copy_ev[0], ctx->copy_stream));
+    ctx->h2d_bytes += (size_t)raw_rows * W;
+  }
+  const uint32_t HP = H - raw_rows;  // rows the host workers pack: [raw_rows, H)
+  const uint32_t chunks = std::max(1u, std::min<uint32_t>(std::max(HP, 1u), (uint32_t)threads * 4));
+  const uint32_t rows_per = (std::max(HP, 1u) + chunks - 1) / chunks;
+  const uint32_t nch = HP ? (HP + rows_per - 1) / rows_per : 0;
   std::vector<std::atomic<int>> ready(nch);
   for (auto& a : ready) a.store(0);
   uint32_t* hp = ctx->h_pack;
   pool.start((int)nch, [&](int k) {
-    const uint32_t r0 = (uint32_t)k * rows_per, r1 = std::min(H, r0 + rows_per);
+    const uint32_t r0 = raw_rows + (uint32_t)k * rows_per, r1 = std::min(H, r0 + rows_per);
     pack_rows(occ, W, r0, r1, pw, hp + (size_t)r0 * pw);
     ready[k].store(1, std::memory_order_release);
   });
-  cudaStream_t s = ctx->stream;
   am_status st = AM_OK;
   for (uint32_t k = 0; k < nch; ++k) {
     // the calling thread packs too, then enqueues the chunks in order as they complete
     while (!ready[k].load(std::memory_order_acquire)) {
       const int j = pool.next.fetch_add(1);
       if (j < (int)nch) {
-        const uint32_t r0 = (uint32_t)j * rows_per, r1 = std::min(H, r0 + rows_per);
+        const uint32_t r0 = raw_rows + (uint32_t)j * rows_per, r1 = std::min(H, r0 + rows_per);
         pack_rows(occ, W, r0, r1, pw, hp + (size_t)r0 * pw);
         ready[j].store(1, std::memory_order_release);
       } else {
@@ -178,7 +228,7 @@ am_status upload_occupancy_packed(am_ctx* ctx, const uint8_t* occ, uint32_t W, u
       }
     }
     if (st) continue;
-    const uint32_t r0 = k * rows_per, r1 = std::min(H, r0 + rows_per);
+    const uint32_t r0 = raw_rows + k * rows_per, r1 = std::min(H, r0 + rows_per);
     cudaError_t e = cudaMemcpyAsync(ctx->d_pack + (size_t)r0 * pw, hp + (size_t)r0 * pw, (size_t)(r1 - r0) * pw * 4,
                                     cudaMemcpyHostToDevice, s);
     if (!e) {
@@ -190,7 +240,11 @@ am_status upload_occupancy_packed(am_ctx* ctx, const uint8_t* occ, uint32_t W, u
     if (e) st = fail(ctx, AM_ECUDA, "occupancy upload: %s", cudaGetErrorString(e));
   }
   pool.wait();  // `ready` and the job live on this frame
-  ctx->h2d_bytes += bytes;
+  if (raw_rows && !st) {
+    const cudaError_t e = cudaStreamWaitEvent(s, ctx->copy_ev[0], 0);  // the raw share is copied and packed
+    if (e) st = fail(ctx, AM_ECUDA, "occupancy upload: %s", cudaGetErrorString(e));
+  }
+  ctx->h2d_bytes += (size_t)(H - raw_rows) * pw * 4;
   ctx->pack_rows = H;
   ctx->pack_w = W;
   return st;

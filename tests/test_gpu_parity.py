@@ -239,23 +239,30 @@ def test_repeated_runs_slabs_batch_dense_are_identical():
     dctx.close()
 
 
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("w,h", [(1031, 1033), (2081, 515), (32, 40000), (1024, 1024)])
-def test_packed_occupancy_upload(w, h):
+def test_packed_occupancy_upload(w, h, pinned):
     """Grids of >= 2^20 cells cross PCIe packed to 1 bit per cell (upload.cu): any nonzero byte is an
     obstacle (grid.hpp:20), ragged row ends, chunk edges; maps equal the oracle's, and the library's H2D
-    byte counter shows the packed size."""
+    byte counter shows the packed size.  From pinned memory the first rows cross as raw bytes and are
+    packed on the device beside the host workers (the split must not show in the maps)."""
     rng = np.random.default_rng(w + h)
     occ = O.random_maze(w, h, 0.35, w)
     vals = rng.integers(1, 256, size=occ.shape, dtype=np.uint8)
     occ_multi = np.where(occ != 0, vals, 0).astype(np.uint8)  # obstacles as arbitrary nonzero bytes
+    if pinned:
+        import torch
+
+        occ_multi = torch.from_numpy(occ_multi).pin_memory().numpy()
     src = O.sample_free_cells(occ, 5, 3)
     sm = O.source_mask(occ, src)
     ctx = am.Context(0)
     try:
         b0 = ctx.h2d_bytes()
         g = am.Grid(occ_multi, src, ctx)
-        packed = h * ((w + 31) // 32) * 4
-        assert ctx.h2d_bytes() - b0 == packed + src.nbytes
+        pw = (w + 31) // 32
+        raw = h * 20 // 100 if pinned else 0  # AM_RAW_SHARE default
+        assert ctx.h2d_bytes() - b0 == raw * w + (h - raw) * pw * 4 + src.nbytes
         for L in (5, 64):
             g.propagate(L)
             assert np.array_equal(g.activity(), O.propagate(occ, sm, L, threads=8)), (w, h, L)
