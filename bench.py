@@ -126,6 +126,17 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _dram_line(traffic, per_launch_ms, peak):
+    """The physical side of the roofline: the ncu DRAM bytes of one launch over the live mean launch time.
+    The modelled frac above counts the reference's per-layer uint32 traffic; the bit-plane kernel keeps its
+    16 layers on chip, so this fraction says how close it runs to HBM itself."""
+    if not traffic or not per_launch_ms:
+        return None
+    gbs = traffic / (per_launch_ms / 1000) / 1e9
+    return {"achieved": round(gbs, 1), "frac": round(gbs / peak, 3), "unit": "GB/s",
+            "basis": "ncu dram bytes per launch (profiles/ncu_traffic.json) / live mean launch time"}
+
+
 def ncu_traffic(kind):
     """dram bytes (read + write) per launch of the dominant kernel from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -841,6 +852,7 @@ def run_b200(args, rank, world, local_rank):
                          "kernel": kernel, "algorithmic_bytes_per_launch": int(alg_bytes),
                          "mean_launch_ms": round(per_launch_ms, 4), "peak_source": peak_src,
                          "layers_per_launch": res.block_layers,
+                         "dram": _dram_line(ncu_traffic(res.engine), per_launch_ms, peak),
                          "note": "9 B per cell-update (reference uint32 layout, SURVEY 8d) x executed cell-updates "
                                  "per launch (processed tiles x tile cells x layers per launch); traffic = ncu dram "
                                  "read+write per launch (profiles/)"},

@@ -2,13 +2,11 @@
 //
 // GridMap holds one byte per cell (grid.hpp:56), and a C4 grid is 537 MB: copied as bytes it is ~10 ms of
 // PCIe, half of an end-to-end solve.  Only "obstacle or not" matters (grid.hpp:20, nonzero = obstacle), so
-// host worker threads pack the caller's rows to 32-cell words (SSE2 compare + movemask, 16 bytes per
-// instruction) into a pinned staging buffer, chunk by chunk, and each chunk is copied (1/8 of the bytes)
+// host worker threads pack the caller's rows to 32-cell words (pack.cpp: AVX-512BW / AVX2 / SSE2
+// compares) into a pinned staging buffer, chunk by chunk, and each chunk is copied (1/8 of the bytes)
 // and expanded back to the dense byte form on the device while the workers pack the next ones.  The packed
 // words stay on the device for the grid's free plane (bits.cu), so the bytes are read once.  From a pinned
 // source a share of the rows crosses as raw bytes beside the workers and is packed on the device.
-#include <emmintrin.h>
-
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -87,28 +85,9 @@ static int pool_workers() {
   return (int)std::min(31u, hw > 1 ? hw - 1 : 0u);
 }
 
-// Packs rows [r0, r1) of a W-wide byte grid: bit c of word w of a row is 1 if cell 32w + c is an obstacle
-// (nonzero byte); bits past W are 0.  pw words per packed row.
-static void pack_rows(const uint8_t* occ, uint32_t W, uint32_t r0, uint32_t r1, uint32_t pw, uint32_t* out) {
-  const __m128i z = _mm_setzero_si128();
-  const uint32_t full = W / 32;
-  for (uint32_t r = r0; r < r1; ++r) {
-    const uint8_t* row = occ + (size_t)r * W;
-    uint32_t* o = out + (size_t)(r - r0) * pw;
-    for (uint32_t w = 0; w < full; ++w) {
-      const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(row + 32 * w));
-      const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(row + 32 * w + 16));
-      const uint32_t fa = (uint32_t)_mm_movemask_epi8(_mm_cmpeq_epi8(a, z));  // 1: free
-      const uint32_t fb = (uint32_t)_mm_movemask_epi8(_mm_cmpeq_epi8(b, z));
-      o[w] = ~(fa | fb << 16);
-    }
-    if (full < pw) {
-      uint32_t v = 0;
-      for (uint32_t c = 32 * full; c < W; ++c) v |= (row[c] != 0 ? 1u : 0u) << (c & 31);
-      o[full] = v;
-    }
-  }
-}
+// pack.cpp
+void pack_rows(const uint8_t* occ, uint32_t W, uint32_t r0, uint32_t r1, uint32_t pw, uint32_t* out);
+int pack_isa();  // 0 SSE2, 1 AVX2, 2 AVX-512BW
 
 namespace {
 // Dense bytes (0 free / 1 obstacle) of packed rows [r0, r1): one warp per 32 packed words (1024 cells),
@@ -172,15 +151,14 @@ am_status upload_occupancy_packed(am_ctx* ctx, const uint8_t* occ, uint32_t W, u
   HostPool& pool = *ctx->hpool;
   const int threads = (int)pool.th.size() + 1;
   // A pinned source lets the copy engine take a share of the rows as raw bytes (packed on the device
-  // afterwards) while the host workers pack the rest: the workers are bound by host memory bandwidth, the
-  // copy engine by PCIe, so the two run side by side (AM_RAW_SHARE: the share in percent, default 20).
+  // afterwards) while the host workers pack the rest (AM_RAW_SHARE: the share in percent).  It pays while
+  // the packing is instruction-bound (SSE2 / AVX2: 20%); with AVX-512 the workers alone reach the host's
+  // memory bandwidth and a raw share only competes for it (default 0).
   uint32_t raw_rows = 0;
   {
     cudaPointerAttributes at{};
-    static const int share = [] {
-      const char* v = getenv("AM_RAW_SHARE");
-      return v ? std::max(0, std::min(100, atoi(v))) : 20;
-    }();
+    const char* v = getenv("AM_RAW_SHARE");
+    const int share = v ? std::max(0, std::min(100, atoi(v))) : pack_isa() == 2 ? 0 : 20;
     if (share && cudaPointerGetAttributes(&at, occ) == cudaSuccess && at.type == cudaMemoryTypeHost)
       raw_rows = (uint32_t)((uint64_t)H * share / 100);
     (void)cudaGetLastError();

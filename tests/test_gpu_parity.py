@@ -241,11 +241,13 @@ def test_repeated_runs_slabs_batch_dense_are_identical():
 
 @pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("w,h", [(1031, 1033), (2081, 515), (32, 40000), (1024, 1024)])
-def test_packed_occupancy_upload(w, h, pinned):
+def test_packed_occupancy_upload(w, h, pinned, monkeypatch):
     """Grids of >= 2^20 cells cross PCIe packed to 1 bit per cell (upload.cu): any nonzero byte is an
     obstacle (grid.hpp:20), ragged row ends, chunk edges; maps equal the oracle's, and the library's H2D
     byte counter shows the packed size.  From pinned memory the first rows cross as raw bytes and are
-    packed on the device beside the host workers (the split must not show in the maps)."""
+    packed on the device beside the host workers (the split must not show in the maps; AM_RAW_SHARE is
+    read per upload)."""
+    monkeypatch.setenv("AM_RAW_SHARE", "20")
     rng = np.random.default_rng(w + h)
     occ = O.random_maze(w, h, 0.35, w)
     vals = rng.integers(1, 256, size=occ.shape, dtype=np.uint8)
@@ -261,7 +263,7 @@ def test_packed_occupancy_upload(w, h, pinned):
         b0 = ctx.h2d_bytes()
         g = am.Grid(occ_multi, src, ctx)
         pw = (w + 31) // 32
-        raw = h * 20 // 100 if pinned else 0  # AM_RAW_SHARE default
+        raw = h * 20 // 100 if pinned else 0
         assert ctx.h2d_bytes() - b0 == raw * w + (h - raw) * pw * 4 + src.nbytes
         for L in (5, 64):
             g.propagate(L)

@@ -14,7 +14,7 @@ pids=()
 for f in stencil bits trace capi multigpu batch mapio upload; do
   $NVCC $FLAGS -c $SRC/$f.cu -o $OUT/$f.o & pids+=($!)
 done
-for f in actmap_api report; do
+for f in actmap_api report pack; do
   g++ -std=c++20 -O2 -fPIC -I$ROOT/include -c $SRC/$f.cpp -o $OUT/$f.o & pids+=($!)
 done
 for p in "${pids[@]}"; do wait $p; done
