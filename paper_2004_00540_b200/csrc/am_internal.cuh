@@ -234,8 +234,9 @@ struct BitBook {
   unsigned long long* state;
   uint32_t* sched;
   uint32_t* list[2];
-  uint32_t* count;             // [6]
+  uint32_t* count;             // [12]: [0..2] items per block, [3..5] fetch counters, [6..8] k_bits_run flags
   unsigned long long* stat;    // [0] tiles processed, [1] cells covered, [2] free cells
+  uint32_t* hcount;            // mapped host mirror (device address) of each block's items by slot, or null
 };
 int bits_ctas_per_sm();
 void launch_bits_init(const BitGeo& bg, const uint8_t* occ, BitBook bk, cudaStream_t s);
@@ -244,6 +245,11 @@ void launch_bits_init_packed(const BitGeo& bg, const uint32_t* packed, BitBook b
 void launch_bits_sources(const BitGeo& bg, const uint32_t* rc, uint64_t n, BitBook bk, cudaStream_t s);
 void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uint32_t nl, FlagSink flag,
                        FlagSink prev, cudaStream_t s);
+// k_bits_run: CTAs per cluster it can run with (0: no cluster fits), the tiles one pass of its warps covers
+int bits_run_cluster();
+uint32_t bits_run_warps(int cluster);
+void launch_bits_run(const BitGeo& bg, int cluster, BitBook bk, uint32_t blk, uint32_t blk_end, uint32_t nmax,
+                     bool autom, uint32_t seq, uint32_t* rec, cudaStream_t s);
 // the encoded 16-bit field (values relative to lref layers) from the planes
 void launch_bits_finalize(const BitGeo& bg, const Geo& g, BitBook bk, uint32_t lref, uint16_t* field, int sms,
                           cudaStream_t s);

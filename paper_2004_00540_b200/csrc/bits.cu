@@ -23,6 +23,8 @@
 // 32*kBRPL-row x (kBTW+2)-word region: lane i owns rows i*kBRPL .. +kBRPL-1,
 // vertical neighbours come from the adjacent lanes (two shuffles per word
 // column and layer), horizontal ones from the lane's own words.
+#include <cstdlib>
+
 #include "am_internal.cuh"
 
 namespace am {
@@ -56,6 +58,12 @@ constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
 constexpr int kBThreads = 128;
+constexpr int kBTsmBytes = kBThreads / 32 * kBTR * kBTW * 4 * 16;  // time-plane staging (dynamic smem)
+#ifndef AM_BITS_RUN_THREADS
+#define AM_BITS_RUN_THREADS 256
+#endif
+constexpr int kBRunThreads = AM_BITS_RUN_THREADS;                    // k_bits_run: one CTA per SM
+constexpr int kBRunSmem = kBRunThreads / 32 * kBTR * kBTW * 4 * 16;
 #ifndef AM_BITS_PREF
 #define AM_BITS_PREF 0  // the next item's states and region load during the current item's bookkeeping
                         // (measured: C4 +3.5%, the longer live ranges spill)
@@ -117,37 +125,33 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 #ifndef AM_BITS_MINB
 #define AM_BITS_MINB 4
 #endif
+// The items of block blk for the warp whose first item is list entry w (nwarps warps share the list,
+// round-robin); leader: the one thread that resets the counters two blocks ahead and counts the items.
+// wmin / covered accumulate the warp's fixed-point word and covered cells (k_bits_tiles, k_bits_run).
 template <bool PART>
-__global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo bg, BitBook bk, uint32_t blk, uint32_t nl,
-                                                          FlagSink flag, FlagSink prev) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" :::);
-  if (prev.host && blockIdx.x == 0 && threadIdx.x == 0)
-    *reinterpret_cast<volatile uint32_t*>(prev.host) = atomicExch(prev.word, 0xFFFFFFFFu);
+__device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, uint32_t blk, uint32_t nl, uint32_t w,
+                                           uint32_t nwarps, bool leader, uint4* tsm, uint32_t& wmin,
+                                           uint32_t& covered) {
   const uint32_t* __restrict__ list = (blk & 1) ? bk.list[1] : bk.list[0];
   // static first item (spread over the SMs): its list entry is loaded alongside the list length
-  uint32_t w = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const uint32_t n = __ldcg(bk.count + blk % 3);
   uint32_t it = w < bg.ntiles() ? __ldcg(list + w) : 0u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (leader) {
     bk.count[(blk + 2) % 3] = 0;
     bk.count[3 + (blk + 2) % 3] = 0;
     atomicAdd(&bk.stat[0], (unsigned long long)n);
+    if (bk.hcount) reinterpret_cast<volatile uint32_t*>(bk.hcount)[blk % kFlagSlots] = n;  // host policy (drive_bits)
   }
   const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = gridDim.x * (kBThreads / 32);
 #ifndef AM_BITS_STATIC
 #define AM_BITS_STATIC 1  // items dealt round-robin (measured: the fetch atomic costs more than the imbalance)
 #endif
   static_assert(!AM_BITS_PREF || AM_BITS_STATIC, "prefetching needs the static item order");
   const bool light = AM_BITS_STATIC || n <= nwarps;  // one item per warp at most: no fetch atomics
   const uint32_t mark = blk + 1;
-  uint32_t wmin = 0xFFFFFFFFu;    // fixed-point word: min over new cells of (nl - 1 - in-block index)
-  uint32_t covered = 0;           // cells this warp covered
-  // per warp: the time-plane words of the item's own rows (32 rows x kBTW row words x 16 words), staged
-  // with cp.async at item start so the read-modify-write after the layers finds them on chip
-  __shared__ uint4 tsm_all[kBThreads / 32][kBTR * kBTW * 4];
-  uint4* tsm = tsm_all[threadIdx.x >> 5];
+  // wmin: fixed-point word, min over new cells of (nl - 1 - in-block index); covered: cells the warp covered.
+  // tsm, per warp: the time-plane words of the item's own rows (32 rows x kBTW row words x 16 words),
+  // staged with cp.async at item start so the read-modify-write after the layers finds them on chip
   // An item's inputs: the states of its 3x3 tile neighbourhood (lane k < 9: (tc + k/3 - 1, tb + k%3 - 1),
   // the pre-block state whether or not that tile was processed in this block yet) and its region (rows
   // tc*TR - K .. tc*TR + TR + K, memory words tb*TW - 1 .. tb*TW + TW; each plane word is {coverage plane
@@ -491,10 +495,76 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
     bit_push_end(bk, blk, pt);
     w = next;
   }
+}
+
+template <bool PART>
+__global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo bg, BitBook bk, uint32_t blk, uint32_t nl,
+                                                          FlagSink flag, FlagSink prev) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  if (prev.host && blockIdx.x == 0 && threadIdx.x == 0)
+    *reinterpret_cast<volatile uint32_t*>(prev.host) = atomicExch(prev.word, 0xFFFFFFFFu);
+  extern __shared__ uint4 tsm_all[];  // kBTsmBytes: kBThreads / 32 warps x kBTR * kBTW * 4 slots
+  uint32_t wmin = 0xFFFFFFFFu, covered = 0;
+  bits_block<PART>(bg, bk, blk, nl, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, gridDim.x * (kBThreads / 32),
+                   blockIdx.x == 0 && threadIdx.x == 0, tsm_all + (threadIdx.x >> 5) * (kBTR * kBTW * 4), wmin,
+                   covered);
   covered = __reduce_add_sync(0xffffffffu, covered);
-  if (lane == 0) {
+  if ((threadIdx.x & 31) == 0) {
     if (covered) atomicAdd(&bk.stat[1], (unsigned long long)covered);
     if (wmin != 0xFFFFFFFFu) atomicMin(flag.word, wmin);
+  }
+}
+
+// Light stretches in one thread-block cluster: while a block lists at most nmax tiles, the
+// cluster's warps run block after block with a hardware cluster barrier between them instead of a kernel
+// boundary (the boundary is ~2.9 us; a light block's own chain ~4 us).  Same items, same bookkeeping as
+// k_bits_tiles; the fixed-point word of block b is count[6 + b % 3] (reset one block ahead by the leader)
+// and the auto-run termination of drive_bits is evaluated here after each block.  Stops before block
+// blk_end, when a block lists more than nmax tiles, or at the fixed point (autom); the outcome goes to
+// the mapped record rec: {seq, next block, termination layer or 0, next block's items, blocks run}.
+__global__ void __launch_bounds__(kBRunThreads, 1) k_bits_run(BitGeo bg, BitBook bk, uint32_t blk, uint32_t blk_end,
+                                                               uint32_t nmax, uint32_t autom, uint32_t seq,
+                                                               uint32_t* rec) {
+  extern __shared__ uint4 tsm_all[];
+  uint4* tsm = tsm_all + (threadIdx.x >> 5) * (kBTR * kBTW * 4);
+  uint32_t crank, csize;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  const uint32_t nwarps = csize * (kBRunThreads / 32), w0 = (threadIdx.x >> 5) * csize + crank;
+  const bool leader = crank == 0 && threadIdx.x == 0;
+  uint32_t lprime = 0, n_next = 0, blocks = 0;
+  for (;;) {
+    const uint32_t n = __ldcg(bk.count + blk % 3);
+    if (blk >= blk_end || n > nmax) {
+      n_next = n;
+      break;
+    }
+    if (leader) bk.count[6 + (blk + 1) % 3] = 0xFFFFFFFFu;
+    uint32_t wmin = 0xFFFFFFFFu, covered = 0;
+    bits_block<false>(bg, bk, blk, kBK, w0, nwarps, leader, tsm, wmin, covered);
+    covered = __reduce_add_sync(0xffffffffu, covered);
+    if ((threadIdx.x & 31) == 0) {
+      if (covered) atomicAdd(&bk.stat[1], (unsigned long long)covered);
+      if (wmin != 0xFFFFFFFFu) atomicMin(bk.count + 6 + blk % 3, wmin);
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const uint32_t m = __ldcg(bk.count + 6 + blk % 3);
+    const uint32_t start = kBK * blk;
+    ++blk, ++blocks;
+    if (autom) {  // drive_bits' block_termination for a full 16-bit block
+      const uint32_t t = m >= 0x7FFFu ? start + 1 : m >= 1 ? start + kBK + 1 - m : 0u;
+      if (t) {
+        lprime = t;
+        break;
+      }
+    }
+  }
+  if (leader) {
+    volatile uint32_t* r = rec;
+    r[1] = blk, r[2] = lprime, r[3] = n_next, r[4] = blocks;
+    __threadfence_system();
+    r[0] = seq;
   }
 }
 
@@ -691,9 +761,20 @@ __global__ void __launch_bounds__(256) k_bits_finalize(BitGeo bg, Geo g, BitBook
 
 }  // namespace
 
+static void bits_smem_attr() {
+  static const bool done = [] {
+    cudaFuncSetAttribute(k_bits_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBTsmBytes);
+    cudaFuncSetAttribute(k_bits_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBTsmBytes);
+    return true;
+  }();
+  (void)done;
+}
+
 int bits_ctas_per_sm() {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bits_tiles<false>, kBThreads, 0) != cudaSuccess) n = 1;
+  bits_smem_attr();
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bits_tiles<false>, kBThreads, kBTsmBytes) != cudaSuccess)
+    n = 1;
   return n < 1 ? 1 : n;
 }
 
@@ -726,8 +807,9 @@ void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uin
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(kBThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = kBTsmBytes;
   cfg.stream = s;
+  bits_smem_attr();
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -738,6 +820,46 @@ void launch_bits_tiles(const BitGeo& bg, int ctas, BitBook bk, uint32_t blk, uin
     cudaLaunchKernelEx(&cfg, k_bits_tiles<false>, bg, bk, blk, nl, flag, prev);
   else
     cudaLaunchKernelEx(&cfg, k_bits_tiles<true>, bg, bk, blk, nl, flag, prev);
+}
+
+int bits_run_cluster() {
+  static const int size = [] {
+    cudaFuncSetAttribute(k_bits_run, cudaFuncAttributeMaxDynamicSharedMemorySize, kBRunSmem);
+    cudaFuncSetAttribute(k_bits_run, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c : {16, 8, 4}) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(kBRunThreads);
+      cfg.dynamicSmemBytes = kBRunSmem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k_bits_run, &cfg) == cudaSuccess && n >= 1) return c;
+      (void)cudaGetLastError();
+    }
+    return 0;
+  }();
+  return size;
+}
+
+uint32_t bits_run_warps(int cluster) { return (uint32_t)cluster * (kBRunThreads / 32); }
+
+void launch_bits_run(const BitGeo& bg, int cluster, BitBook bk, uint32_t blk, uint32_t blk_end, uint32_t nmax,
+                     bool autom, uint32_t seq, uint32_t* rec, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(kBRunThreads);
+  cfg.dynamicSmemBytes = kBRunSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_bits_run, bg, bk, blk, blk_end, nmax, (uint32_t)autom, seq, rec);
 }
 
 }  // namespace am

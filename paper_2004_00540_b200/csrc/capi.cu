@@ -146,7 +146,8 @@ static cudaError_t take_flag_set(am_ctx* ctx, am::FlagSet** out) {
   }
   auto* f = new (std::nothrow) am::FlagSet();
   if (!f) return cudaErrorMemoryAllocation;
-  cudaError_t e = cudaHostAlloc(&f->h, am::kFlagSlots * sizeof(uint32_t), cudaHostAllocMapped);
+  // slots, then each bit-plane block's items by slot and the k_bits_run record (drive_bits)
+  cudaError_t e = cudaHostAlloc(&f->h, (2 * am::kFlagSlots + 8) * sizeof(uint32_t), cudaHostAllocMapped);
   if (!e) e = cudaHostGetDevicePointer((void**)&f->hdev, f->h, 0);
   for (int i = 0; !e && i < am::kFlagSlots; ++i) e = cudaEventCreateWithFlags(&f->ev[i], cudaEventDisableTiming);
   if (e) {
@@ -497,7 +498,7 @@ am_status bits_alloc(am_ctx* ctx, am_grid* g, const uint32_t* packed) {
   CK(am::dmalloc(ctx, &k.sched, nt * 4));
   CK(am::dmalloc(ctx, &k.list[0], nt * 4));
   CK(am::dmalloc(ctx, &k.list[1], nt * 4));
-  CK(am::dmalloc(ctx, &k.count, 6 * 4));
+  CK(am::dmalloc(ctx, &k.count, 12 * 4));
   CK(am::dmalloc(ctx, &k.stat, 8 * 8));
   b->ctas = ctx->sms * bits_ctas_per_sm();
   return bits_build_planes(ctx, g, packed);
@@ -527,6 +528,7 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   CK(cudaMemsetAsync(B.bk.state, 0, nt * 8, s));
   CK(cudaMemsetAsync(B.bk.sched, 0, nt * 4, s));
   CK(cudaMemsetAsync(B.bk.count, 0, 6 * 4, s));
+  CK(cudaMemsetAsync(B.bk.count + 6, 0xFF, 3 * 4, s));  // k_bits_run's fixed-point words
   CK(cudaMemsetAsync(B.bk.stat, 0, 2 * 8, s));
   CK(cudaMemsetAsync(B.bk.stat + 3, 0, 5 * 8, s));  // experiment counters (AM_BITS_STATS)
   // the planes are not reset: the cleared states mark every tile's coverage stale (bits.cu)
@@ -552,6 +554,18 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
   std::deque<PendingBlock> pend;
   FlagSink unpublished{nullptr, nullptr, nullptr};
   uint32_t l = 0, lprime = 0, blk = 0;
+  // Light stretches run in one cluster (k_bits_run) while a block lists at most run_max tiles: entered
+  // from the start when the sources fit, later when a drained block (kLagTiles behind) listed few tiles;
+  // after a stretch ends on a heavy block, normal launches for at least run_gap blocks (hysteresis).
+  // (AM_BITS_RUN=0 disables the stretches, AM_BITS_RUN_MAX overrides run_max; both read per run)
+  const char* run_env = getenv("AM_BITS_RUN");
+  const char* max_env = getenv("AM_BITS_RUN_MAX");
+  const int run_cluster = run_env && run_env[0] == '0' ? 0 : bits_run_cluster();
+  const uint32_t run_max = !run_cluster ? 0 : max_env ? (uint32_t)atoi(max_env) : bits_run_warps(run_cluster);
+  const uint32_t run_gap = kLagTiles + 8;
+  B.bk.hcount = g->fs->hdev + kFlagSlots;
+  bool want_run = run_cluster && g->n_src <= run_max;
+  uint32_t since_run = run_gap;
   auto drain_one = [&]() -> am_status {
     const PendingBlock b = pend.front();
     pend.pop_front();
@@ -567,9 +581,43 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
       const uint32_t t = block_termination(b, *h);
       if (t) lprime = t;
     }
+    if (run_cluster && since_run >= run_gap && g->fs->h[kFlagSlots + b.slot] <= run_max) want_run = true;
     return AM_OK;
   };
   while (l < lref && !lprime) {
+    if (want_run && lref - l >= (uint32_t)kBK) {
+      want_run = false;
+      if (unpublished.host) {
+        launch_publish_flag(unpublished, s);
+        CKL();
+        unpublished = FlagSink{nullptr, nullptr, nullptr};
+      }
+      volatile uint32_t* rec = g->fs->h + 2 * kFlagSlots;
+      const uint32_t seq = rec[0] + 1;
+      launch_bits_run(bg, run_cluster, B.bk, blk, blk + (lref - l) / kBK, run_max, autom, seq,
+                      g->fs->hdev + 2 * kFlagSlots, s);
+      ++ctx->launches;
+      if (cudaError_t e = cudaPeekAtLastError()) return fail(ctx, AM_ECUDA, "k_bits_run: %s", cudaGetErrorString(e));
+      while (!pend.empty())  // the blocks before the stretch (an earlier fixed point wins)
+        if ((st = drain_one())) return st;
+      for (uint64_t spin = 1; rec[0] != seq; ++spin) {
+        if ((spin & 4095) == 0) {
+          const cudaError_t q = cudaStreamQuery(s);
+          if (q == cudaSuccess && rec[0] != seq) return fail(ctx, AM_ECUDA, "run record never written");
+          if (q != cudaSuccess && q != cudaErrorNotReady) return fail(ctx, AM_ECUDA, "bits: %s", cudaGetErrorString(q));
+        }
+      }
+      const uint32_t nb = rec[4];
+      static const bool run_print = getenv("AM_BITS_RUN_PRINT") != nullptr;
+      if (run_print) fprintf(stderr, "bits run: blocks %u..%u, next items %u, end %u\n", blk, rec[1], rec[3], rec[2]);
+      blk = rec[1];
+      l += nb * kBK;
+      r.block_launches += nb;
+      if (autom && !lprime && rec[2]) lprime = rec[2];
+      since_run = 0;
+      continue;
+    }
+    ++since_run;
     const uint32_t nl = std::min<uint32_t>(kBK, lref - l);
     const int slot = (int)(blk % kFlagSlots);
     FlagSink sink{g->d_flags + slot, g->d_flags + kFlagSlots, nullptr};

@@ -305,3 +305,35 @@ def test_map_stream_ordering():
             g.close()
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("run_max", ["off", "1", "12", "60", "400"])
+def test_cluster_stretches_match_oracle(run_max, monkeypatch):
+    """Light stretches (k_bits_run: one thread-block cluster runs block after block while few tiles are
+    listed) entered from the start, left when the front grows, re-entered in the tail: forced thresholds
+    (AM_BITS_RUN_MAX, read per run) give every transition pattern.  Fixed-L maps equal the oracle; auto
+    runs match the BFS law and the BFS-predicted outcome (tests/test_gpu_scale.py)."""
+    from tests.test_gpu_scale import predicted_auto
+
+    if run_max == "off":
+        monkeypatch.setenv("AM_BITS_RUN", "0")
+    else:
+        monkeypatch.setenv("AM_BITS_RUN_MAX", run_max)
+    ctx = am.Context(0)
+    try:
+        for w, h, dens, ns, seed in [(2000, 1500, 0.3, 3, 61), (1500, 2100, 0.45, 40, 62), (4096, 300, 0.2, 1, 63)]:
+            occ = O.random_maze(w, h, dens, seed)
+            src = O.sample_free_cells(occ, ns, seed)
+            sm = O.source_mask(occ, src)
+            g = am.Grid(occ, src, ctx)
+            for L in (16, 100, 333):
+                g.propagate(L)
+                assert np.array_equal(g.activity(), O.propagate(occ, sm, L, threads=8)), (w, h, L, run_max)
+            hops = O.bfs_multi_source(occ, sm)
+            for cap in (48, 4 * max(w, h)):
+                r = g.propagate_auto(cap)
+                assert (r.layers_used, r.cause) == predicted_auto(occ, hops, cap), (w, h, cap, run_max)
+                assert O.check_activity(occ, g.activity(), hops, r.layers_used)[0] == 0, (w, h, cap, run_max)
+            g.close()
+    finally:
+        ctx.close()
