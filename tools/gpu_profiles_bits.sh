@@ -29,6 +29,8 @@ if [[ "$ARGS" == *" full "* ]]; then
     -o gpurun_out/prof_finalize -f $CMD > gpurun_out/ncu_finalize.log 2>&1; echo "ncu_finalize_rc=$?"
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_trace$' -c 1 \
     -o gpurun_out/prof_trace -f $CMD > gpurun_out/ncu_trace.log 2>&1; echo "ncu_trace_rc=$?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_bits_run -s 1 -c 1 \
+    -o gpurun_out/prof_run -f $CMD > gpurun_out/ncu_run.log 2>&1; echo "ncu_run_rc=$?"
 fi
 if [[ "$ARGS" == *" dram "* ]]; then
   S="python tools/solve_time.py 1 tiles"
