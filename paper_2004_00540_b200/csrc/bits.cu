@@ -132,14 +132,17 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // The items of block blk for the warp whose first item is list entry w (nwarps warps share the list,
 // round-robin); leader: the one thread that resets the counters two blocks ahead and counts the items.
 // wmin / covered accumulate the warp's fixed-point word and covered cells (k_bits_tiles, k_bits_run).
+__device__ __forceinline__ uint32_t bits_first_item(const BitGeo& bg, const BitBook& bk, uint32_t blk, uint32_t w) {
+  const uint32_t* __restrict__ list = (blk & 1) ? bk.list[1] : bk.list[0];
+  return w < bg.ntiles() ? __ldcg(list + w) : 0u;
+}
+// n: the block's list length, it: the warp's first list entry (bits_first_item), loaded by the caller
+// so they travel together with its other loads
 template <bool PART>
 __device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, uint32_t blk, uint32_t nl, uint32_t w,
-                                           uint32_t nwarps, bool leader, uint4* tsm, uint32_t& wmin,
-                                           uint32_t& covered) {
+                                           uint32_t nwarps, bool leader, uint4* tsm, uint32_t n, uint32_t it,
+                                           uint32_t& wmin, uint32_t& covered) {
   const uint32_t* __restrict__ list = (blk & 1) ? bk.list[1] : bk.list[0];
-  // static first item (spread over the SMs): its list entry is loaded alongside the list length
-  const uint32_t n = __ldcg(bk.count + blk % 3);
-  uint32_t it = w < bg.ntiles() ? __ldcg(list + w) : 0u;
   if (leader) {
     bk.count[(blk + 2) % 3] = 0;
     bk.count[3 + (blk + 2) % 3] = 0;
@@ -543,8 +546,11 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
     *reinterpret_cast<volatile uint32_t*>(prev.host) = atomicExch(prev.word, 0xFFFFFFFFu);
   extern __shared__ uint4 tsm_all[];  // kBTsmBytes: kBThreads / 32 warps x kBTR * kBTW * 4 slots
   uint32_t wmin = 0xFFFFFFFFu, covered = 0;
-  bits_block<PART>(bg, bk, blk, nl, (threadIdx.x >> 5) * gridDim.x + blockIdx.x, gridDim.x * (kBThreads / 32),
-                   blockIdx.x == 0 && threadIdx.x == 0, tsm_all + (threadIdx.x >> 5) * (kBTR * kBTW * 4), wmin,
+  // static first item (spread over the SMs): its list entry is loaded alongside the list length
+  const uint32_t w = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const uint32_t n = __ldcg(bk.count + blk % 3);
+  bits_block<PART>(bg, bk, blk, nl, w, gridDim.x * (kBThreads / 32), blockIdx.x == 0 && threadIdx.x == 0,
+                   tsm_all + (threadIdx.x >> 5) * (kBTR * kBTW * 4), n, bits_first_item(bg, bk, blk, w), wmin,
                    covered);
   covered = __reduce_add_sync(0xffffffffu, covered);
   if ((threadIdx.x & 31) == 0) {
@@ -571,22 +577,25 @@ __global__ void __launch_bounds__(kBRunThreads, 1) k_bits_run(BitGeo bg, BitBook
   const uint32_t nwarps = csize * (kBRunThreads / 32), w0 = (threadIdx.x >> 5) * csize + crank;
   const bool leader = crank == 0 && threadIdx.x == 0;
   uint32_t lprime = 0, n_next = 0, blocks = 0;
+  uint32_t n = __ldcg(bk.count + blk % 3), it = bits_first_item(bg, bk, blk, w0);
   for (;;) {
-    const uint32_t n = __ldcg(bk.count + blk % 3);
     if (blk >= blk_end || n > nmax) {
       n_next = n;
       break;
     }
     if (leader) bk.count[6 + (blk + 1) % 3] = 0xFFFFFFFFu;
     uint32_t wmin = 0xFFFFFFFFu, covered = 0;
-    bits_block<false>(bg, bk, blk, kBK, w0, nwarps, leader, tsm, wmin, covered);
+    bits_block<false>(bg, bk, blk, kBK, w0, nwarps, leader, tsm, n, it, wmin, covered);
     covered = __reduce_add_sync(0xffffffffu, covered);
     if ((threadIdx.x & 31) == 0) {
       if (covered) atomicAdd(&bk.stat[1], (unsigned long long)covered);
       if (wmin != 0xFFFFFFFFu) atomicMin(bk.count + 6 + blk % 3, wmin);
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    // the fixed-point word, the next block's list length and first entries: one round trip
     const uint32_t m = __ldcg(bk.count + 6 + blk % 3);
+    n = __ldcg(bk.count + (blk + 1) % 3);
+    it = bits_first_item(bg, bk, blk + 1, w0);
     const uint32_t start = kBK * blk;
     ++blk, ++blocks;
     if (autom) {  // drive_bits' block_termination for a full 16-bit block
