@@ -715,7 +715,10 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
 // the free word -- and a 32 x 32 bit transpose over the lanes (five butterfly shuffles) leaves lane c
 // with cell c of both row words as a u16x2 {free, covered, u} pair: the encoding is then a handful of
 // word-wide ops, and two coalesced 64 B stores follow.
-constexpr uint32_t kFinalizeSteps = 2;  // warp steps per warp (short-lived CTAs, see the launch)
+#ifndef AM_FIN_STEPS
+#define AM_FIN_STEPS 2
+#endif
+constexpr uint32_t kFinalizeSteps = AM_FIN_STEPS;  // warp steps per warp (short-lived CTAs, see the launch)
 constexpr int kFinP = 4;                 // row-word pairs per warp step (their loads in flight together)
 __global__ void __launch_bounds__(256) k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref,
                                                        uint16_t* __restrict__ field) {
