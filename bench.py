@@ -28,6 +28,7 @@ import argparse
 import gc
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -147,15 +148,55 @@ def ncu_traffic(kind):
         return None
 
 
+class NvmlSampler:
+    """The same clocks and throttle reasons read through NVML (the library nvidia-smi queries) from a
+    thread every 5 ms: the fallback when nvidia-smi's buffered output holds no sample of a short region."""
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+    def __init__(self, index):
+        import threading
+        self.rows, self.stop_ev, self.t = [], threading.Event(), None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self.stop_ev.is_set():
+                    try:
+                        self.rows.append((time.time(), float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                          float(mx), int(reasons(h))))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.005)
+
+            self.t = threading.Thread(target=run, daemon=True)
+            self.t.start()
+        except Exception:
+            self.t = None
+
+    def stop(self):
+        if self.t:
+            self.stop_ev.set()
+            self.t.join(timeout=2)
+        return [(ts, sm, mx, [("Active" if r & b else "Not Active") for b in self.BITS.values()])
+                for ts, sm, mx, r in self.rows]
+
+
 class ClockSampler:
     def __init__(self, index):
         self.p = None
+        self.nvml = NvmlSampler(index)
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.f = open(self.path, "w")
+            # line-buffered (stdbuf): nvidia-smi's block-buffered output is lost when it is terminated
             self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index),
+                (["stdbuf", "-oL"] if shutil.which("stdbuf") else []) + ["nvidia-smi", "-i", str(index),
                  "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
@@ -166,28 +207,32 @@ class ClockSampler:
     def stop(self, window=None):
         """Median SM clock and throttle reasons of the samples taken inside `window` (wall-clock (t0, t1) of
         the timed region; the sampler starts before the warm-up so nvidia-smi is polling by then)."""
-        if not self.p:
-            return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.close()
+        nv_rows = self.nvml.stop()
         import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 8:
-                    continue
-                try:
-                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                    rows.append((ts, float(parts[1]), float(parts[2]), parts[4:8]))
-                except ValueError:
-                    continue
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) < 8:
+                        continue
+                    try:
+                        ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                        rows.append((ts, float(parts[1]), float(parts[2]), parts[4:8]))
+                    except ValueError:
+                        continue
+        source = "nvidia-smi"
         inside = [r for r in rows if window is None or window[0] <= r[0] <= window[1]]
+        nv_inside = [r for r in nv_rows if window is None or window[0] <= r[0] <= window[1]]
+        if len(nv_inside) > len(inside):  # nvidia-smi polls every ~100 ms in practice; NVML every 5 ms
+            rows, inside, source = nv_rows, nv_inside, "nvml (the library nvidia-smi reads), 5 ms"
         scope = "timed region"
         if not inside and rows and window is not None:  # region shorter than the polling interval
             mid = 0.5 * (window[0] + window[1])
@@ -197,7 +242,7 @@ class ClockSampler:
             return None
         reasons = sorted({n for r in inside for n, v in zip(names, r[3]) if v.lower().startswith("active")})
         return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
-                "reasons": reasons, "samples": len(inside), "scope": scope}
+                "reasons": reasons, "samples": len(inside), "scope": scope, "source": source}
 
 
 def cpu_model():
