@@ -156,6 +156,9 @@ __device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, 
   static_assert(!AM_BITS_PREF || AM_BITS_STATIC, "prefetching needs the static item order");
   const bool light = AM_BITS_STATIC || n <= nwarps;  // one item per warp at most: no fetch atomics
   const uint32_t mark = blk + 1;
+  uint32_t hmask[kBTPlanes - kBNJ];  // all-ones where bit k of blk is set: the time planes above the J bits
+#pragma unroll
+  for (int k = 0; k < kBTPlanes - kBNJ; ++k) hmask[k] = 0u - ((blk >> k) & 1u);
   // wmin: fixed-point word, min over new cells of (nl - 1 - in-block index); covered: cells the warp covered.
   // tsm, per warp: the time-plane words of the item's own rows (32 rows x kBTW row words x 16 words),
   // staged with cp.async at item start so the read-modify-write after the layers finds them on chip
@@ -463,8 +466,13 @@ __device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, 
         }
 #pragma unroll
         for (int k = 0; k < kBTPlanes; ++k) {
-          const uint32_t bitv = k < kBNJ ? J[k < kBNJ ? k : 0][i][x] : (((blk >> (k - kBNJ)) & 1u) ? nw : 0u);
-          v[k] = (v[k] & ~nw) | bitv;
+          // planes >= kBNJ: bit k - kBNJ of blk for every new cell: one LOP3 (v & ~nw) | (nw & mask) with
+          // the block's masks made once per block (the compiler otherwise re-tests each bit per word)
+          if (k < kBNJ) {
+            v[k] = (v[k] & ~nw) | J[k < kBNJ ? k : 0][i][x];
+          } else {
+            asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(v[k]) : "r"(v[k]), "r"(nw), "r"(hmask[k < kBNJ ? 0 : k - kBNJ]));
+          }
         }
         uint4* tp = reinterpret_cast<uint4*>(bk.T + (rw + x) * 16);
 #pragma unroll
