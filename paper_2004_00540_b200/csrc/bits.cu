@@ -84,6 +84,9 @@ constexpr int kBRunSmem = kBRunThreads / 32 * kBTR * kBTW * 4 * 16;
 #define AM_BITS_HFIRST 0  // experiment: horizontal dilation per row first, then the vertical OR (one op fewer
                           // per column; measured C4 +2.4%: the extra live registers spill at 128)
 #endif
+#ifndef AM_BITS_HMASK_ASM
+#define AM_BITS_HMASK_ASM 1
+#endif
 #ifndef AM_BITS_NOT
 #define AM_BITS_NOT 0  // experiment only (wrong maps): no time-plane staging / updates
 #endif
@@ -471,7 +474,11 @@ __device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, 
           if (k < kBNJ) {
             v[k] = (v[k] & ~nw) | J[k < kBNJ ? k : 0][i][x];
           } else {
+#if AM_BITS_HMASK_ASM
             asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(v[k]) : "r"(v[k]), "r"(nw), "r"(hmask[k < kBNJ ? 0 : k - kBNJ]));
+#else
+            v[k] = (v[k] & ~nw) | (nw & hmask[k < kBNJ ? 0 : k - kBNJ]);
+#endif
           }
         }
         uint4* tp = reinterpret_cast<uint4*>(bk.T + (rw + x) * 16);
