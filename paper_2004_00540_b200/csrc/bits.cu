@@ -562,6 +562,8 @@ __global__ void __launch_bounds__(kBThreads, AM_BITS_MINB) k_bits_tiles(BitGeo b
   extern __shared__ uint4 tsm_all[];  // kBTsmBytes: kBThreads / 32 warps x kBTR * kBTW * 4 slots
   uint32_t wmin = 0xFFFFFFFFu, covered = 0;
   // static first item (spread over the SMs): its list entry is loaded alongside the list length
+  // item k of the block goes to warp k / gridDim of CTA k % gridDim: the first items spread over every CTA
+  // (CTA-major orders measured C4 +7%)
   const uint32_t w = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const uint32_t n = __ldcg(bk.count + blk % 3);
   bits_block<PART>(bg, bk, blk, nl, w, gridDim.x * (kBThreads / 32), blockIdx.x == 0 && threadIdx.x == 0,
