@@ -592,6 +592,9 @@ static am_status drive_bits(am_ctx* ctx, am_grid* g, uint32_t target, bool autom
         CKL();
         unpublished = FlagSink{nullptr, nullptr, nullptr};
       }
+      // the cluster's fixed-point words start clean: a stretch that ended on a heavy block left the words
+      // of its last two blocks set, and the next stretch may start on either
+      CK(cudaMemsetAsync(B.bk.count + 6, 0xFF, 3 * 4, s));
       volatile uint32_t* rec = g->fs->h + 2 * kFlagSlots;
       const uint32_t seq = rec[0] + 1;
       launch_bits_run(bg, run_cluster, B.bk, blk, blk + (lref - l) / kBK, run_max, autom, seq,

@@ -337,3 +337,28 @@ def test_cluster_stretches_match_oracle(run_max, monkeypatch):
             g.close()
     finally:
         ctx.close()
+
+
+def test_cluster_stretch_thresholds_sweep(monkeypatch):
+    """Many stretch thresholds on small grids whose propagation ends in light blocks: every entry / exit /
+    re-entry point of the cluster stretches must give the BFS-predicted outcome and a law-abiding map
+    (a stretch re-entered right at the fixed point must not see the previous stretch's fixed-point words)."""
+    from tests.test_gpu_scale import predicted_auto
+
+    ctx = am.Context(0)
+    try:
+        for seed in range(4):
+            occ = O.random_maze(700, 500, 0.3 + 0.05 * seed, 70 + seed)
+            src = O.sample_free_cells(occ, 1 + 3 * seed, 71 + seed)
+            sm = O.source_mask(occ, src)
+            hops = O.bfs_multi_source(occ, sm)
+            want = predicted_auto(occ, hops, 4000)
+            g = am.Grid(occ, src, ctx)
+            for run_max in ("0", "1", "2", "3", "5", "8", "13", "21", "34", "55", "89"):
+                monkeypatch.setenv("AM_BITS_RUN_MAX", run_max)
+                r = g.propagate_auto(4000)
+                assert (r.layers_used, r.cause) == want, (seed, run_max, r.layers_used, r.cause, want)
+                assert O.check_activity(occ, g.activity(), hops, r.layers_used)[0] == 0, (seed, run_max)
+            g.close()
+    finally:
+        ctx.close()
