@@ -98,6 +98,13 @@ am_status am_ctx_trim(am_ctx *ctx);
 /* The cudaStream_t every kernel of this context is launched on (so callers
  * can bracket work with CUDA events on the launching stream). */
 am_status am_ctx_get_stream(const am_ctx *ctx, void **stream);
+/* Pinned, device-mapped host memory on the context's device.  Host buffers of
+ * this kind are written by the kernels directly (am_trace_paths streams the
+ * points into them while the paths are walked; am_grid_create reads them with
+ * the copy engine); any other host pointer is staged.  No reference
+ * counterpart: the C++ API (actmap_api.cpp) keeps its trace buffers here. */
+am_status am_host_alloc(am_ctx *ctx, size_t bytes, void **out);
+am_status am_host_free(am_ctx *ctx, void *p);
 
 /* ---- grid + sources (GridMap grid.hpp:18-57, SourceSet grid.hpp:80-90) --
  * occupancy: width*height bytes, row-major, nonzero = obstacle.

@@ -4,9 +4,11 @@
 // reference exception types (errors.hpp) and does O(path) host
 // post-processing (straighten, metrics).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -96,6 +98,26 @@ uint64_t occupancy_hash(std::span<const uint8_t> occ) {
   return h;
 }
 
+// f(i) for i in [0, n) on up to 16 host threads (grain: 16 consecutive indices per fetch); small n inline
+template <class F>
+void parallel_for(size_t n, F&& f) {
+  const unsigned hw = std::thread::hardware_concurrency();
+  const unsigned nt = std::min<unsigned>(hw ? hw : 1, 16);
+  if (n < 256 || nt <= 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t i; (i = next.fetch_add(16)) < n;)
+      for (size_t j = i; j < std::min(n, i + 16); ++j) f(j);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
+
 std::vector<uint32_t> flatten(const std::vector<Coord>& cs) {
   std::vector<uint32_t> rc(cs.size() * 2);
   for (size_t i = 0; i < cs.size(); ++i) {
@@ -140,6 +162,23 @@ struct DeviceMap {
   DeviceMap& operator=(const DeviceMap&) = delete;
   ~DeviceMap() {
     if (grid) am_grid_destroy(ctx, grid);
+    if (pts) am_host_free(ctx, pts);
+  }
+  // pinned trace buffer (am_host_alloc): the walkers write the points into it directly
+  uint32_t* pts = nullptr;
+  size_t pts_words = 0;
+  uint32_t* trace_buffer(size_t words) {
+    if (words > pts_words) {
+      if (pts) am_host_free(ctx, pts);
+      pts = nullptr;
+      pts_words = 0;
+      void* p = nullptr;
+      const size_t want = words + words / 4;
+      check(am_host_alloc(ctx, want * 4, &p), ctx, "trace buffer");
+      pts = static_cast<uint32_t*>(p);
+      pts_words = want;
+    }
+    return pts;
   }
   bool matches(const GridMap& g, const SourceSet& s) const {
     if (g.width() != width || g.height() != height || g.obstacle_count() != obstacles) return false;
@@ -427,19 +466,18 @@ std::vector<Path> trace_batch(detail::DeviceMap& dev, std::span<const Coord> tar
   status.assign(n, 0);
   check(am_path_counts(dev.ctx, dev.grid, rc.data(), n, method, seed, off.data(), status.data()), dev.ctx,
         "path counts");
-  std::vector<uint32_t> pts(2 * off[n] + 2);
-  check(am_trace_paths(dev.ctx, dev.grid, rc.data(), n, method, seed, off.data(), pts.data(), off[n], status.data()),
+  const uint32_t* pts = dev.trace_buffer(2 * off[n] + 2);  // pinned: the walkers stream the points into it
+  check(am_trace_paths(dev.ctx, dev.grid, rc.data(), n, method, seed, off.data(), dev.pts, off[n], status.data()),
         dev.ctx, "trace paths");
   std::vector<Path> paths(n);
-  for (size_t i = 0; i < n; ++i) {
-    if (status[i] != AM_OK) continue;
-    auto& p = paths[i].points;
-    p.reserve(off[i + 1] - off[i]);
-    for (uint64_t k = off[i]; k < off[i + 1]; ++k) {
-      if (pts[2 * k] == 0xFFFFFFFFu) break;  // removed by device-side straightening of uploaded maps
-      p.push_back(Coord{pts[2 * k], pts[2 * k + 1]});
-    }
-  }
+  parallel_for(n, [&](size_t i) {
+    if (status[i] != AM_OK) return;
+    uint64_t end = off[i];  // points removed by device-side straightening of uploaded maps end a path
+    while (end < off[i + 1] && pts[2 * end] != 0xFFFFFFFFu) ++end;
+    static_assert(sizeof(Coord) == 8, "Coord is {row, col}: the (row, col) pairs are Coord arrays");
+    const Coord* first = reinterpret_cast<const Coord*>(pts + 2 * off[i]);
+    paths[i].points.assign(first, first + (end - off[i]));
+  });
   return paths;
 }
 
@@ -603,21 +641,23 @@ std::vector<TargetReport> Planner::target_reports(std::span<const Coord> targets
                                                   bool emit_points, CornerRule rule) {
   auto planned = reconstruct_all(targets, method, seed, rule);
   std::vector<TargetReport> out(planned.size());
-  for (size_t i = 0; i < planned.size(); ++i) {
+  for (size_t i = 0; i < planned.size(); ++i) {  // errors in target order, as a sequential loop reports them
+    if (planned[i].status == TargetStatus::kInvalid)
+      throw InvalidInputError("target out of bounds or on an obstacle " + to_string(planned[i].target));
+    if (planned[i].status == TargetStatus::kInternal)
+      throw Error("activity map has no ascending neighbour on the path from " + to_string(planned[i].target));
+  }
+  parallel_for(planned.size(), [&](size_t i) {
     TargetReport& t = out[i];
     t.target = planned[i].target;
-    if (planned[i].status == TargetStatus::kInvalid)
-      throw InvalidInputError("target out of bounds or on an obstacle " + to_string(t.target));
-    if (planned[i].status == TargetStatus::kInternal)
-      throw Error("activity map has no ascending neighbour on the path from " + to_string(t.target));
-    if (planned[i].status != TargetStatus::kOk) continue;  // uncovered: recorded, not thrown (validate.hpp:76-77)
+    if (planned[i].status != TargetStatus::kOk) return;  // uncovered: recorded, not thrown (validate.hpp:76-77)
     const Path& path = planned[i].path;
     t.covered = true;
     t.reached_source = path.source();
     t.steps = path.steps();
     t.euclidean_length = path_metrics(path).euclidean_length;
     if (emit_points) t.points = std::move(planned[i].path.points);
-  }
+  });
   return out;
 }
 

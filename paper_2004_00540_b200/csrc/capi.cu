@@ -114,6 +114,20 @@ am_status am_ctx_trim(am_ctx* ctx) {
   return AM_OK;
 }
 
+am_status am_host_alloc(am_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return AM_EINVAL;
+  *out = nullptr;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocMapped));
+  return AM_OK;
+}
+
+am_status am_host_free(am_ctx* ctx, void* p) {
+  if (!ctx) return AM_EINVAL;
+  if (p) CK(cudaFreeHost(p));
+  return AM_OK;
+}
+
 am_status am_ctx_get_stream(const am_ctx* ctx, void** stream) {
   if (!ctx || !stream) return AM_EINVAL;
   *stream = (void*)ctx->stream;
