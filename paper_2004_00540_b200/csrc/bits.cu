@@ -736,7 +736,10 @@ __global__ void k_bits_sources(BitGeo bg, const uint32_t* __restrict__ rc, uint6
 #define AM_FIN_STEPS 2
 #endif
 constexpr uint32_t kFinalizeSteps = AM_FIN_STEPS;  // warp steps per warp (short-lived CTAs, see the launch)
-constexpr int kFinP = 4;                 // row-word pairs per warp step (their loads in flight together)
+#ifndef AM_FIN_P
+#define AM_FIN_P 8
+#endif
+constexpr int kFinP = AM_FIN_P;          // row-word pairs per warp step (their loads in flight together)
 __global__ void __launch_bounds__(256) k_bits_finalize(BitGeo bg, Geo g, BitBook bk, uint32_t lref,
                                                        uint16_t* __restrict__ field) {
   constexpr int P = kFinP;
