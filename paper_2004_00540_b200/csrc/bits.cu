@@ -57,7 +57,10 @@ __device__ __forceinline__ constexpr int bright(int x) { return AM_BITS_PACKH &&
 constexpr int kBNJ = kBK == 8 ? 3 : kBK == 16 ? 4 : 5;  // bit planes of the in-block layer index
 static_assert(kBK == 8 || kBK == 16 || kBK == 32, "layers per bit block");
 static_assert(kBTR >= kBK && kBTR > 0, "tiles at least kBK rows");
-constexpr int kBThreads = 128;
+#ifndef AM_BITS_THREADS
+#define AM_BITS_THREADS 128
+#endif
+constexpr int kBThreads = AM_BITS_THREADS;
 constexpr int kBTsmBytes = kBThreads / 32 * kBTR * kBTW * 4 * 16;  // time-plane staging (dynamic smem)
 #ifndef AM_BITS_RUN_THREADS
 #define AM_BITS_RUN_THREADS 256
