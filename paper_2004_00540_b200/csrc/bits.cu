@@ -90,6 +90,9 @@ constexpr int kBRunSmem = kBRunThreads / 32 * kBTR * kBTW * 4 * 16;
 #ifndef AM_BITS_HMASK_ASM
 #define AM_BITS_HMASK_ASM 1
 #endif
+#ifndef AM_BITS_PF2
+#define AM_BITS_PF2 0  // experiment: L2 prefetch of the next item's region after the layers
+#endif
 #ifndef AM_BITS_NOT
 #define AM_BITS_NOT 0  // experiment only (wrong maps): no time-plane staging / updates
 #endif
@@ -220,7 +223,8 @@ __device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, 
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     if (!AM_BITS_PREF) load_item(it);
-    const uint32_t it_next = AM_BITS_PREF && w + nwarps < n ? __ldcg(list + w + nwarps) : 0u;
+    const uint32_t it_next =
+        (AM_BITS_PREF || AM_BITS_PF2) && w + nwarps < n ? __ldcg(list + w + nwarps) : 0xFFFFFFFFu;
     const uint32_t s9 = rs9;
     uint32_t C[kBRPL][kBNW], C1[kBRPL][kBNW], F[kBRPL][kBNW];
     uint32_t HR0[kBRPL], HR1[kBRPL], HRF[kBRPL];  // packed halo: the right neighbour's word until the select
@@ -378,6 +382,20 @@ __device__ __forceinline__ void bits_block(const BitGeo& bg, const BitBook& bk, 
         for (int x = 0; x < kBNW; ++x) C[i][x] = N[i][x];
     }
     if (AM_BITS_PREF && w + nwarps < n) load_item(it_next);  // lands while this item finishes
+    if (AM_BITS_PF2 && it_next != 0xFFFFFFFFu) {  // the next item's region lines into L2 (no registers held)
+      const uint32_t nb = it_next >> 16, nc = it_next & 0xFFFFu;
+#pragma unroll
+      for (int i = 0; i < kBRPL; ++i) {
+        const int prow = (int)nc * kBTR + lane * kBRPL + i - kBK;
+        if (prow < 0 || prow >= (int)bg.rows) continue;
+#pragma unroll
+        for (int x = 0; x < kBTW + 2; ++x) {
+          const int wd = (int)(nb * kBTW) + x - 1;
+          if (wd < 0 || wd >= (int)bg.wpr) continue;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(bk.P + bg.pidx((uint32_t)prow, (uint32_t)wd)));
+        }
+      }
+    }
     // cells new in the last layer: in-block index kBK - 1, all J bits set (none in a partial block)
     if (AM_BITS_FRJ) {
 #pragma unroll
